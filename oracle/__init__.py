@@ -1,0 +1,266 @@
+"""CPU ORACLE for the CL-Splats local-optimisation step (TEST INFRASTRUCTURE).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` legs may import this package.  The product package
+``paper_2506_21117_b200`` never imports it and shares no code with it.
+
+The arithmetic lives in ``cls_oracle.c`` (plain C, fp64, OpenMP); this module
+only compiles/loads it and marshals numpy arrays.  See the C file's header for
+the paper passages each function follows and DESIGN.md for the readings.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+from typing import Dict, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "cls_oracle.c")
+_LIB = os.path.join(_HERE, "libclsoracle.so")
+_lock = threading.Lock()
+_lib = None
+
+TILE = 16
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle (gcc, fp64, OpenMP, no FP contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fopenmp", "-ffp-contract=off", "-fPIC",
+                               "-shared", _SRC, "-o", tmp, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            L = ctypes.CDLL(_LIB)
+            P = ctypes.c_void_p
+            i64, i32, d = ctypes.c_int64, ctypes.c_int, ctypes.c_double
+            L.orc_membership.argtypes = [i64, P, i32, P, P, P, P, P]
+            L.orc_project.argtypes = [i64, i32, P, P, P, P, P, P, P, d, d, d, d, i32, i32] + [P] * 11
+            L.orc_render_view.restype = ctypes.c_int
+            L.orc_render_view.argtypes = [i64, P, P, P, P, P, P, P, P, P, i32, i32, P, i32, i32, P, d, P, d,
+                                          P, P, P, P, P, P, P, P, P]
+            L.orc_backward_project.argtypes = [i64, i32, P, P, P, P, P, P, P, d, d, d, d, i32, i32, P, P, P, P]
+            L.orc_adam.argtypes = [i64, P, P, P, P, P, P, d, d, d, i32]
+            L.orc_sh_basis.argtypes = [i32, d, d, d, P]
+            L.orc_num_threads.restype = ctypes.c_int
+            _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def num_threads() -> int:
+    return int(lib().orc_num_threads())
+
+
+def sh_basis(degree: int, d) -> np.ndarray:
+    out = np.zeros(16, np.float64)
+    lib().orc_sh_basis(degree, float(d[0]), float(d[1]), float(d[2]), _p(out))
+    return out[: (degree + 1) ** 2]
+
+
+# ---------------------------------------------------------------------------
+# stage wrappers
+# ---------------------------------------------------------------------------
+
+def membership(scene) -> np.ndarray:
+    """bool[N]: centre inside the union of the change regions (R21)."""
+    n = scene.n
+    kinds = np.array([r.kind for r in scene.regions], np.int32)
+    ra = _f64([r.a for r in scene.regions]).reshape(-1, 3) if scene.regions else np.zeros((0, 3))
+    rb = _f64([r.b for r in scene.regions]).reshape(-1, 3) if scene.regions else np.zeros((0, 3))
+    rr = _f64([r.r for r in scene.regions])
+    out = np.zeros(n, np.uint8)
+    means = _f64(scene.means)
+    lib().orc_membership(n, _p(means), len(scene.regions), _p(kinds), _p(_f64(ra)), _p(_f64(rb)),
+                         _p(rr), _p(out))
+    return out.astype(bool)
+
+
+def _cam_args(cam):
+    R = _f64(cam.R).reshape(9)
+    t = _f64(cam.t).reshape(3)
+    return R, t
+
+
+def project(scene, view: int) -> Dict[str, np.ndarray]:
+    cam = scene.cameras[view]
+    n = scene.n
+    R, t = _cam_args(cam)
+    out = dict(culled=np.zeros(n, np.int32), tcam=np.zeros((n, 3)), uv=np.zeros((n, 2)),
+               cov2d=np.zeros((n, 3)), conic=np.zeros((n, 3)), opac=np.zeros(n),
+               radius=np.zeros(n, np.int32), rect=np.zeros((n, 4), np.int32),
+               depth_key=np.zeros(n, np.float32), rgb=np.zeros((n, 3)), clamped=np.zeros((n, 3), np.int32))
+    arrs = [_f64(scene.means), _f64(scene.log_scales), _f64(scene.quats), _f64(scene.opacity_logits),
+            _f64(scene.sh)]
+    lib().orc_project(n, scene.sh_degree, *[_p(a) for a in arrs], _p(R), _p(t), cam.fx, cam.fy, cam.cx,
+                      cam.cy, cam.width, cam.height,
+                      *[_p(out[k]) for k in ("culled", "tcam", "uv", "cov2d", "conic", "opac", "radius",
+                                              "rect", "depth_key", "rgb", "clamped")])
+    out["_keep"] = (R, t, arrs)
+    return out
+
+
+def render(scene, view: int, active: np.ndarray, proj=None, literal: bool = False, all_tiles: bool = False,
+           dL_dC: Optional[np.ndarray] = None, with_grad: bool = True, loss_scale: Optional[float] = None,
+           delta: float = 1e-5, use_target: bool = True) -> Dict[str, np.ndarray]:
+    """Forward (+ per-pixel backward into 2D gradients) of one view."""
+    cam = scene.cameras[view]
+    W, H = cam.width, cam.height
+    TX, TY = -(-W // TILE), -(-H // TILE)
+    if proj is None:
+        proj = project(scene, view)
+    n = scene.n
+    act = np.ascontiguousarray(active, np.uint8)
+    if loss_scale is None:
+        loss_scale = 1.0 / (3.0 * H * W * len(scene.cameras))
+    target = None
+    if use_target and scene.targets is not None:
+        target = np.ascontiguousarray(scene.targets[view], np.float32)
+    dl_in = None if dL_dC is None else _f64(dL_dC).reshape(3, H, W)
+    out = dict(image=np.zeros((3, H, W)), T_final=np.zeros((H, W)), n_contrib=np.zeros((H, W), np.int32),
+               tile_mask=np.zeros((TY, TX), np.uint8), ambiguous=np.zeros((H, W), np.uint8),
+               dL_dC=np.zeros((3, H, W)), grad2d=np.zeros((n, 9)) if with_grad else None,
+               sig=np.zeros((H, W), np.uint64))
+    loss_sum = ctypes.c_double(0.0)
+    bg = _f64(scene.bg)
+    ntiles = lib().orc_render_view(
+        n, _p(proj["culled"]), _p(proj["uv"]), _p(proj["conic"]), _p(proj["opac"]), _p(proj["rect"]),
+        _p(proj["depth_key"]), _p(proj["rgb"]), _p(proj["clamped"]), _p(act), W, H, _p(bg),
+        int(literal), int(all_tiles), None if target is None else _p(target), float(loss_scale),
+        None if dl_in is None else _p(dl_in), float(delta),
+        _p(out["image"]), _p(out["T_final"]), _p(out["n_contrib"]), _p(out["tile_mask"]),
+        _p(out["ambiguous"]), ctypes.byref(loss_sum), _p(out["dL_dC"]),
+        None if out["grad2d"] is None else _p(out["grad2d"]), _p(out["sig"]))
+    out["loss_sum"] = loss_sum.value
+    out["n_active_tiles"] = int(ntiles)
+    out["tile_mask"] = out["tile_mask"].astype(bool)
+    out["ambiguous"] = out["ambiguous"].astype(bool)
+    return out
+
+
+def grad_stride(sh_degree: int) -> int:
+    return 11 + 3 * (sh_degree + 1) ** 2
+
+
+def backward_project(scene, view: int, active: np.ndarray, proj, grad2d: np.ndarray,
+                     grad: Optional[np.ndarray] = None) -> np.ndarray:
+    """Accumulate the 3D gradients of one view into ``grad`` [N, 11+3K]."""
+    cam = scene.cameras[view]
+    n = scene.n
+    if grad is None:
+        grad = np.zeros((n, grad_stride(scene.sh_degree)))
+    R, t = _cam_args(cam)
+    arrs = [_f64(scene.means), _f64(scene.log_scales), _f64(scene.quats), _f64(scene.opacity_logits),
+            _f64(scene.sh)]
+    act = np.ascontiguousarray(active, np.uint8)
+    g2 = _f64(grad2d)
+    lib().orc_backward_project(n, scene.sh_degree, *[_p(a) for a in arrs], _p(R), _p(t), cam.fx, cam.fy,
+                               cam.cx, cam.cy, cam.width, cam.height, _p(act), _p(proj["culled"]), _p(g2),
+                               _p(grad))
+    return grad
+
+
+def forward_backward(scene, views: Optional[Sequence[int]] = None, active: Optional[np.ndarray] = None,
+                     literal: bool = False, all_tiles: bool = False, dL_dC=None, n_views_total=None,
+                     delta: float = 1e-5, with_grad: bool = True):
+    """One full forward + backward over ``views`` (default all).  Returns
+    dict(active, idx, loss, renders[list], grad [N, stride])."""
+    if views is None:
+        views = range(len(scene.cameras))
+    views = list(views)
+    if active is None:
+        active = membership(scene)
+    if n_views_total is None:
+        n_views_total = len(scene.cameras)
+    H, W = scene.height, scene.width
+    scale = 1.0 / (3.0 * H * W * n_views_total)
+    grad = np.zeros((scene.n, grad_stride(scene.sh_degree)))
+    renders = []
+    loss = 0.0
+    for j, v in enumerate(views):
+        proj = project(scene, v)
+        up = None if dL_dC is None else dL_dC[j]
+        r = render(scene, v, active, proj, literal=literal, all_tiles=all_tiles, dL_dC=up,
+                   with_grad=with_grad, loss_scale=scale, delta=delta)
+        if with_grad:
+            backward_project(scene, v, active, proj, r["grad2d"], grad)
+        loss += r["loss_sum"] * scale
+        r["proj"] = proj
+        renders.append(r)
+    return dict(active=active, idx=np.nonzero(active)[0], loss=loss, renders=renders, grad=grad)
+
+
+# ---------------------------------------------------------------------------
+# layout helpers (marshalling to the C-ABI row layout, no method arithmetic)
+# ---------------------------------------------------------------------------
+
+def k4(sh_degree: int) -> int:
+    return -(-3 * (sh_degree + 1) ** 2 // 4)
+
+
+def row_floats(sh_degree: int) -> int:
+    return 4 * (3 + k4(sh_degree))
+
+
+def pack_rows(grad: np.ndarray, sh_degree: int) -> np.ndarray:
+    """[M, 11+3K] oracle gradient rows -> [M, 4*(3+K4)] ABI rows
+    (chunk0 = mean xyz + opacity logit, chunk1 = quat wxyz, chunk2 = log-scale xyz + pad,
+    chunks 3.. = SH coefficients flattened (coefficient-major, channel-minor) + pad)."""
+    K = (sh_degree + 1) ** 2
+    out = np.zeros((grad.shape[0], row_floats(sh_degree)))
+    out[:, 0:3] = grad[:, 0:3]
+    out[:, 3] = grad[:, 10]
+    out[:, 4:8] = grad[:, 3:7]
+    out[:, 8:11] = grad[:, 7:10]
+    out[:, 12:12 + 3 * K] = grad[:, 11:11 + 3 * K]
+    return out
+
+
+def lr_row(sh_degree: int, lr6) -> np.ndarray:
+    """Per-float learning rate of one ABI row (lr6 = mean, quat, scale, opacity, sh_dc, sh_rest);
+    pad lanes get NaN (never written)."""
+    K = (sh_degree + 1) ** 2
+    row = np.full(row_floats(sh_degree), np.nan)
+    row[0:3] = lr6[0]
+    row[3] = lr6[3]
+    row[4:8] = lr6[1]
+    row[8:11] = lr6[2]
+    row[12:15] = lr6[4]
+    row[15:12 + 3 * K] = lr6[5]
+    return row
+
+
+def adam_rows(theta: np.ndarray, m: np.ndarray, v: np.ndarray, g: np.ndarray, lr_per_float: np.ndarray,
+              beta1=0.9, beta2=0.999, eps=1e-15, step=1):
+    """Masked Adam on ABI rows: theta/m/v [A, F] (the active rows, gathered), g [A, F].
+    Pad lanes (lr NaN) are untouched.  Operates in place on float64 copies and returns them."""
+    theta = _f64(theta).copy()
+    m = _f64(m).copy()
+    v = _f64(v).copy()
+    A, F = theta.shape
+    valid = ~np.isnan(lr_per_float)
+    cols = np.nonzero(valid)[0]
+    elem = (np.arange(A)[:, None] * F + cols[None, :]).reshape(-1).astype(np.int64)
+    gg = _f64(g).reshape(-1)[elem].copy()
+    lr = np.broadcast_to(lr_per_float[cols][None, :], (A, len(cols))).reshape(-1).copy()
+    th, mm, vv = theta.reshape(-1), m.reshape(-1), v.reshape(-1)
+    lib().orc_adam(len(elem), _p(elem), _p(th), _p(mm), _p(vv), _p(gg), _p(lr), beta1, beta2, eps, int(step))
+    return theta, m, v
