@@ -1,0 +1,195 @@
+/*
+ * cls.h -- C ABI of the B200-native CL-Splats local-optimisation step.
+ *
+ * One step of the method of PAPER.md §3.3 "Local Optimization Kernel"
+ * (L190-201) and Supp. L508-541: dynamic tile mask from the changed set O^t
+ * (modification 1, L538-539), forward/backward rendering restricted to the
+ * active tiles (modification 2, L540), backward preprocessing restricted to
+ * O^t (modification 3, L541), and an optimizer step on O^t only with masked
+ * Adam moments (L508-509).  The result equals a full-frame 3DGS step restricted
+ * to O^t (L194, L201).  Base conventions are those of 3DGS (L449); every
+ * reading is listed in DESIGN.md ("Readings R1-R27").
+ *
+ * Conventions for every entry point:
+ *   - Pointers marked (device) are CUDA device pointers on the ctx's device;
+ *     pointers marked (host) are host memory read synchronously during the call.
+ *   - Every call is asynchronous on `stream` (a cudaStream_t passed as void*)
+ *     unless stated otherwise, returns a cls_status, and never aborts or prints.
+ *     On failure cls_last_error(ctx) holds a one-line detail.
+ *   - float4-typed arrays are passed as `float *` and must be 16-byte aligned.
+ *   - A ctx is bound to one device, is not thread-safe, and owns all scratch.
+ *
+ * Data layout of a scene with n Gaussians and SH degree D (0..3), K=(D+1)^2,
+ * K4 = ceil(3K/4) ("chunk-major SoA", one float4 per Gaussian per chunk):
+ *   mean_op   float4[n]      (x, y, z, opacity logit)              -- P:102 mean, opacity
+ *   quat      float4[n]      (w, x, y, z), not necessarily unit    -- rotation (R17)
+ *   log_scale float4[n]      (log sx, log sy, log sz, pad)         -- scale = exp (R18)
+ *   sh        float4[K4][n]  coefficient k, channel c at float 3k+c of the Gaussian's
+ *                            K4 chunks (chunk j of Gaussian i at sh[j*n + i])
+ * A parameter "row" is the 3 + K4 float4 chunks of one Gaussian in the order
+ * (mean_op, quat, log_scale, sh chunks) -- ROW4 = 3 + K4 float4 = 16 (D=0) or 60 (D=3) floats.
+ */
+#ifndef CLS_H
+#define CLS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    CLS_OK = 0,
+    CLS_ERR_INVALID_ARGUMENT = 1,   /* null pointer, n<=0, bad degree, fx<=0, radius<=0, lo>hi ... */
+    CLS_ERR_DIMENSION_MISMATCH = 2, /* views of one call with different W x H, or over the ctx limits */
+    CLS_ERR_CAPACITY = 3,           /* a device-side capacity (records, pairs) overflowed; nothing truncated silently */
+    CLS_ERR_STATE = 4,              /* call order violated (bwd without fwd, Adam without bwd ...) */
+    CLS_ERR_CUDA = 5,               /* a CUDA runtime error; detail in cls_last_error */
+    CLS_ERR_OUT_OF_MEMORY = 6       /* scratch allocation failed at cls_create */
+} cls_status;
+
+typedef struct cls_ctx cls_ctx;
+
+/* Pinhole camera, world->camera: p_cam = R p + t, R row-major orthonormal.
+ * Pixel (x, y) samples the intrinsics point (x + 1/2, y + 1/2) (reading R11),
+ * i.e. a Gaussian projects to pixel-index coordinates u = fx tx/tz + cx - 1/2. */
+typedef struct {
+    float fx, fy, cx, cy;
+    float R[9];
+    float t[3];
+    int32_t width, height;   /* >= 16 each */
+} cls_camera;
+
+/* A change region (P:175-182 bounding spheres s_i = (m_i, 1.1 d_i)).
+ * kind 0: sphere, centre a, radius r > 0 (|mu - a|^2 <= r^2, inclusive).
+ * kind 1: axis-aligned box lo = a, hi = b, a <= b (inclusive); BASELINE config c3. */
+typedef struct {
+    int32_t kind;
+    float a[3];
+    float b[3];
+    float r;
+} cls_region;
+
+typedef struct {
+    int64_t n;                 /* number of Gaussians, >= 1 */
+    int32_t sh_degree;         /* 0..3 */
+    const float *mean_op;      /* (device) float4[n] */
+    const float *quat;         /* (device) float4[n] */
+    const float *log_scale;    /* (device) float4[n] */
+    const float *sh;           /* (device) float4[K4][n] */
+} cls_gaussians;
+
+/* Capacities fixed at cls_create; scratch is sized from them once. */
+typedef struct {
+    int64_t max_gaussians;     /* n of every call <= this */
+    int64_t max_records;       /* sum over views of (Gaussian, view) records overlapping active tiles */
+    int64_t max_pairs;         /* sum over views of (Gaussian, active tile) pairs, < 2^31 */
+    int64_t max_active;        /* |O^t| (sizes the per-view 2D gradient buffer) */
+    int32_t max_views;         /* views per call, <= CLS_MAX_VIEWS */
+    int32_t max_width, max_height;
+} cls_limits;
+
+#define CLS_MAX_VIEWS 64
+#define CLS_MAX_REGIONS 64
+
+/* flags of cls_render_fwd */
+#define CLS_FLAG_ALL_TILES 1u   /* every tile active: the full-frame 3DGS step ("w/o Kernel") */
+
+typedef struct {
+    int64_t n_active;          /* A = |O^t| of the last fwd */
+    int64_t n_records;         /* (Gaussian, view) records kept */
+    int64_t n_pairs;           /* (Gaussian, active tile) pairs sorted */
+    int64_t n_items;           /* active (view, tile) work items rendered */
+    int64_t n_active_tiles[CLS_MAX_VIEWS];
+    int32_t overflow;          /* bit 0 records, bit 1 pairs, bit 2 active set */
+    int32_t n_views;
+    int64_t max_list;          /* longest per-tile list */
+    int64_t n_huge_tiles;      /* tiles sorted by the global-memory fallback */
+} cls_stats_t;
+
+/* Create a context on `device` with the given capacities (host struct).
+ * Allocates all scratch; returns CLS_ERR_OUT_OF_MEMORY if that fails. Synchronous. */
+cls_status cls_create(cls_ctx **ctx, int device, const cls_limits *lim);
+cls_status cls_destroy(cls_ctx *ctx);
+
+/*
+ * Forward pass of one local-optimisation step over n_views views (all W x H equal).
+ *   1. membership of every centre in the union of `regions` -> stable list O^t (idx[A])  (R21)
+ *   2. dynamic tile mask per view from the projections of O^t              (R9)
+ *   3. projection of every Gaussian vs the mask -> records; (view|tile|depth) binning and
+ *      per-tile depth sort
+ *   4. front-to-back compositing of the active tiles only                   (R1-R3)
+ *   5. if targets != NULL: fused L1 loss over active-tile pixels,
+ *      L = sum |C - T*| / (3 H W n_views_total), and dL/dC kept for cls_render_bwd (R19)
+ * Arguments:
+ *   g            (host struct, device arrays) scene; unchanged until the matching bwd
+ *   cams         (host) cls_camera[n_views]
+ *   n_views_total views of the whole step across ranks (>= n_views; loss normalisation)
+ *   regions      (host) cls_region[n_regions], n_regions <= CLS_MAX_REGIONS (0 -> A = 0)
+ *   bg           (host) float[3] background colour (R20: black in all configs)
+ *   targets      (device) float[n_views][3][H][W] or NULL
+ *   images       (device) float[n_views][3][H][W] out or NULL; pixels of inactive tiles = bg
+ *   tile_mask    (device) uint8[n_views][ceil(H/16)][ceil(W/16)] out or NULL
+ *   loss         (device) float scalar out or NULL (written only when targets != NULL)
+ *   flags        CLS_FLAG_ALL_TILES or 0
+ *   stream       cudaStream_t
+ */
+cls_status cls_render_fwd(cls_ctx *ctx, const cls_gaussians *g, const cls_camera *cams, int32_t n_views,
+                          int32_t n_views_total, const cls_region *regions, int32_t n_regions,
+                          const float *bg, const float *targets, float *images, uint8_t *tile_mask,
+                          float *loss, uint32_t flags, void *stream);
+
+/* Size and device list of O^t from the last fwd.  Blocks the host only until the
+ * membership kernel of that fwd has finished (an event recorded right after it).
+ *   A    (host) out: number of active Gaussians
+ *   idx  (host) out, optional: device pointer to int32[A] ascending Gaussian indices,
+ *        owned by ctx, valid until the next fwd. */
+cls_status cls_active(cls_ctx *ctx, int64_t *A, const int32_t **idx);
+
+/* Copy idx[A] of the last fwd into `dst` (device int32[>= A]), asynchronously on `stream`. */
+cls_status cls_copy_active(cls_ctx *ctx, int32_t *dst, void *stream);
+
+/*
+ * Backward pass of the last fwd: reverse walk of every active tile,
+ * gradients accumulated ONLY into active Gaussians (frozen ones are composited
+ * but never differentiated), then the 2D -> 3D chain rule per active Gaussian.
+ *   dL_dimages   (device) float[n_views][3][H][W] upstream gradient, or NULL to use the
+ *                fused-L1 gradient of the fwd (CLS_ERR_STATE if the fwd had no targets)
+ *   grad_active  (device) float4[A][ROW4] out (fully overwritten; row k belongs to idx[k])
+ */
+cls_status cls_render_bwd(cls_ctx *ctx, const cls_gaussians *g, const float *dL_dimages,
+                          float *grad_active, void *stream);
+
+/*
+ * Masked Adam (R22): for the A rows of the last fwd's O^t only,
+ *   m <- b1 m + (1-b1) g;  v <- b2 v + (1-b2) g^2;
+ *   theta <- theta - lr (m / (1 - b1^step)) / (sqrt(v / (1 - b2^step)) + eps).
+ * Rows not in O^t, and pad lanes, are never read-modified-written.
+ *   mean_op, quat, log_scale, sh  (device) parameters, layout as cls_gaussians, updated in place
+ *   m, v         (device) float4[3 + K4][n] moments, chunk c of Gaussian i at [c*n + i]
+ *   grad_active  (device) float4[A][ROW4] (e.g. from cls_render_bwd, all-reduced across ranks)
+ *   lr           (host) float[6]: mean, quat, scale, opacity, sh DC, sh rest
+ *   step         Adam step t >= 1
+ */
+cls_status cls_adam_masked(cls_ctx *ctx, float *mean_op, float *quat, float *log_scale, float *sh,
+                           float *m, float *v, const float *grad_active, const float *lr,
+                           float beta1, float beta2, float eps, int32_t step, void *stream);
+
+/* Counters of the last fwd (host struct out).  Synchronises the ctx's last stream.
+ * Returns CLS_ERR_CAPACITY if a capacity overflowed during that fwd. */
+cls_status cls_stats(cls_ctx *ctx, cls_stats_t *out);
+
+/* Optional: after cls_render_fwd, copy the per-(view, active Gaussian) 2D gradients
+ * of the last bwd -- float[n_views][A][12] (u, v, conic a, b, c, opacity, r, g, b, 0, 0, 0) --
+ * into `out` (device).  For stage-wise parity tests. */
+cls_status cls_debug_grad2d(cls_ctx *ctx, float *out, void *stream);
+
+const char *cls_status_string(cls_status s);
+const char *cls_last_error(const cls_ctx *ctx);
+/* Number of kernels launched by the library since cls_create (host counter). */
+int64_t cls_launch_count(const cls_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CLS_H */

@@ -1,0 +1,299 @@
+// cls_internal.cuh -- device-side types and helpers of the B200 CL-Splats step.
+// Used only by the CUDA translation units of libcls.so (never by oracle/).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/cls.h"
+
+#define CLS_TILE 16
+#define CLS_BLOCK_PIX 256
+
+namespace cls {
+
+// ---------------------------------------------------------------------------
+// kernel-parameter structs (passed by value as __grid_constant__; no H2D copies)
+// ---------------------------------------------------------------------------
+struct GCam {
+    float R[9];
+    float t[3];
+    float fx, fy, cx, cy;
+    float oc[3];   // camera centre -R^T t (for SH view directions)
+    float pad;
+};
+
+struct CamSet {
+    int n;              // views in this call
+    int W, H, TX, TY, T;
+    GCam c[CLS_MAX_VIEWS];
+};
+
+struct RegSet {
+    int n;
+    int kind[CLS_MAX_REGIONS];
+    float a[CLS_MAX_REGIONS][3];
+    float b[CLS_MAX_REGIONS][3];
+    float r[CLS_MAX_REGIONS];
+};
+
+// device counters, zeroed by one memset per fwd
+struct Counters {
+    int member_tiles;       // decoupled look-back tile ticket (membership)
+    int A;                  // |O^t|
+    int n_records;
+    int tiles_scan_tiles;   // look-back ticket (tile scan)
+    unsigned long long n_pairs;
+    int n_items;
+    int n_small, n_large, n_huge;
+    int fwd_work, bwd_work;
+    int overflow;           // bit0 records, bit1 pairs
+    int max_list;
+    int active_tiles[CLS_MAX_VIEWS];
+};
+
+// all scratch of a ctx (device pointers), passed by value to kernels
+struct Scratch {
+    // membership
+    int *idx;               // [maxN]   O^t, ascending
+    int *ord;               // [maxN]   active ordinal or -1
+    unsigned long long *st_member;  // look-back status
+    // masks
+    uint8_t *mask;          // [V][T]
+    int *sat;               // [V][(TY+1)(TX+1)]
+    int *diff;              // [V][(TY+1)(TX+1)]  corner differences of record rects
+    // records
+    float4 *rec_xy;         // (u_hi, u_lo, v_hi, v_lo)
+    float4 *rec_co;         // (conic a, b, c, opacity)
+    float4 *rec_rgb;        // (r, g, b, active ordinal as int bits)
+    int2 *rec_rect;         // (x0 | y0 << 16, x1 | y1 << 16)
+    int2 *rec_meta;         // (gid, view | active << 31)
+    unsigned *rec_depth;    // fp32 bits of the depth key
+    long long max_records;
+    // tiles
+    int *tile_cnt;          // [V*T]
+    int *tile_off;          // [V*T]
+    int *tile_cursor;       // [V*T]
+    unsigned long long *st_tiles;
+    int *items;             // [V*T] (v*T + t) of active tiles, in (v, t) order
+    int *item_of_tile;      // [V*T] item index or -1
+    int *cls_small, *cls_large, *cls_huge;  // item lists per sort class
+    int *first_active;      // [items] first list position holding an active Gaussian (n if none)
+    // pairs
+    unsigned long long *pair_key;   // (depth bits << 32) | gid
+    unsigned *pair_val;             // record id | active << 31; sorted in place per tile
+    unsigned long long *sort_tmp_key;  // huge-tile fallback scratch
+    unsigned *sort_tmp_val;
+    long long max_pairs;
+    // per-pixel forward state, per item [items][256]
+    float *px_T;
+    int *px_last;
+    float *px_dl;           // [items][3][256] fused-L1 dL/dC
+    float *item_loss;       // [items]
+    // gradients
+    float4 *grad2d;         // [V][A][3]
+    Counters *cnt;
+    int max_items;
+};
+
+// ---------------------------------------------------------------------------
+// helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int iceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// Packed decoupled look-back status: bits 63..62 flag (0 none, 1 aggregate, 2 prefix), 62-bit payload.
+#define LB_FLAG_AGG (1ull << 62)
+#define LB_FLAG_PRE (2ull << 62)
+#define LB_PAYLOAD (~(3ull << 62))
+
+// Returns the exclusive prefix of `agg` for block ticket `tile` (call from ONE thread).
+__device__ __forceinline__ unsigned long long lookback(unsigned long long *status, int tile,
+                                                       unsigned long long agg)
+{
+    volatile unsigned long long *vs = status;
+    if (tile == 0) {
+        vs[0] = LB_FLAG_PRE | agg;
+        return 0ull;
+    }
+    vs[tile] = LB_FLAG_AGG | agg;
+    __threadfence();
+    unsigned long long prefix = 0;
+    int j = tile - 1;
+    while (true) {
+        unsigned long long s;
+        do {
+            s = vs[j];
+        } while ((s >> 62) == 0ull);
+        prefix += s & LB_PAYLOAD;
+        if ((s >> 62) == 2ull) break;
+        --j;
+    }
+    __threadfence();
+    vs[tile] = LB_FLAG_PRE | (prefix + agg);
+    return prefix;
+}
+
+// ---------------------------------------------------------------------------
+// Projection of one Gaussian into one camera, fp64 geometry (3DGS base).
+// Same definitions as DESIGN.md R5-R13; written independently of the oracle.
+// ---------------------------------------------------------------------------
+struct Proj {
+    double tx, ty, tz;
+    double u, v;
+    double A, B, C;       // Sigma' (with low-pass)
+    double ca, cb, cc;    // conic
+    int radius;
+    int x0, y0, x1, y1;
+};
+
+__device__ __forceinline__ void quat_rot(double w, double x, double y, double z, double Rq[9])
+{
+    Rq[0] = 1.0 - 2.0 * (y * y + z * z); Rq[1] = 2.0 * (x * y - w * z);       Rq[2] = 2.0 * (x * z + w * y);
+    Rq[3] = 2.0 * (x * y + w * z);       Rq[4] = 1.0 - 2.0 * (x * x + z * z); Rq[5] = 2.0 * (y * z - w * x);
+    Rq[6] = 2.0 * (x * z - w * y);       Rq[7] = 2.0 * (y * z + w * x);       Rq[8] = 1.0 - 2.0 * (x * x + y * y);
+}
+
+// returns false if culled (near plane, det <= 0, empty rect)
+__device__ __forceinline__ bool project_gaussian(const float4 mo, const float4 q, const float4 ls, const GCam &c,
+                                                 int W, int H, int TX, int TY, Proj &p)
+{
+    const double mx = mo.x, my = mo.y, mz = mo.z;
+    p.tx = (double)c.R[0] * mx + (double)c.R[1] * my + (double)c.R[2] * mz + (double)c.t[0];
+    p.ty = (double)c.R[3] * mx + (double)c.R[4] * my + (double)c.R[5] * mz + (double)c.t[1];
+    p.tz = (double)c.R[6] * mx + (double)c.R[7] * my + (double)c.R[8] * mz + (double)c.t[2];
+    if (!(p.tz > 0.2)) return false;
+    // Sigma = M M^T, M = R(q^) diag(exp(l))
+    double qw = q.x, qx = q.y, qy = q.z, qz = q.w;
+    double qn = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+    qw /= qn; qx /= qn; qy /= qn; qz /= qn;
+    double Rq[9];
+    quat_rot(qw, qx, qy, qz, Rq);
+    double s0 = exp((double)ls.x), s1 = exp((double)ls.y), s2 = exp((double)ls.z);
+    double M[9] = {Rq[0] * s0, Rq[1] * s1, Rq[2] * s2, Rq[3] * s0, Rq[4] * s1, Rq[5] * s2,
+                   Rq[6] * s0, Rq[7] * s1, Rq[8] * s2};
+    // J with the frustum clamp (R10)
+    const double fx = c.fx, fy = c.fy;
+    const double limx = 1.3 * ((double)W / (2.0 * fx)), limy = 1.3 * ((double)H / (2.0 * fy));
+    double xz = p.tx / p.tz, yz = p.ty / p.tz;
+    xz = fmin(fmax(xz, -limx), limx);
+    yz = fmin(fmax(yz, -limy), limy);
+    const double xt = xz * p.tz, yt = yz * p.tz;
+    const double j00 = fx / p.tz, j02 = -(fx * xt) / (p.tz * p.tz);
+    const double j11 = fy / p.tz, j12 = -(fy * yt) / (p.tz * p.tz);
+    // T = J W (2x3); then V = T M (2x3); Sigma' = V V^T + 0.3 I
+    double T0[3], T1[3];
+    for (int b = 0; b < 3; b++) {
+        T0[b] = j00 * (double)c.R[b] + j02 * (double)c.R[6 + b];
+        T1[b] = j11 * (double)c.R[3 + b] + j12 * (double)c.R[6 + b];
+    }
+    double V0[3], V1[3];
+    for (int b = 0; b < 3; b++) {
+        V0[b] = T0[0] * M[b] + T0[1] * M[3 + b] + T0[2] * M[6 + b];
+        V1[b] = T1[0] * M[b] + T1[1] * M[3 + b] + T1[2] * M[6 + b];
+    }
+    p.A = V0[0] * V0[0] + V0[1] * V0[1] + V0[2] * V0[2] + 0.3;
+    p.B = V0[0] * V1[0] + V0[1] * V1[1] + V0[2] * V1[2];
+    p.C = V1[0] * V1[0] + V1[1] * V1[1] + V1[2] * V1[2] + 0.3;
+    const double det = p.A * p.C - p.B * p.B;
+    if (!(det > 0.0)) return false;
+    p.ca = p.C / det;
+    p.cb = -p.B / det;
+    p.cc = p.A / det;
+    const double mid = 0.5 * (p.A + p.C);
+    const double disc = mid * mid - det;
+    const double lam = mid + sqrt(disc > 0.1 ? disc : 0.1);
+    p.radius = (int)ceil(3.0 * sqrt(lam));
+    p.u = fx * p.tx / p.tz + (double)c.cx - 0.5;
+    p.v = fy * p.ty / p.tz + (double)c.cy - 0.5;
+    const double r = (double)p.radius;
+    int x0 = (int)((p.u - r) / CLS_TILE), y0 = (int)((p.v - r) / CLS_TILE);
+    int x1 = (int)((p.u + r + CLS_TILE - 1) / CLS_TILE), y1 = (int)((p.v + r + CLS_TILE - 1) / CLS_TILE);
+    p.x0 = min(max(x0, 0), TX); p.x1 = min(max(x1, 0), TX);
+    p.y0 = min(max(y0, 0), TY); p.y1 = min(max(y1, 0), TY);
+    return (p.x1 - p.x0) * (p.y1 - p.y0) != 0;
+}
+
+// number of active tiles in [x0,x1) x [y0,y1) from a summed-area table with row pitch TX+1
+__device__ __forceinline__ int sat_count(const int *S, int TXp1, int x0, int y0, int x1, int y1)
+{
+    return S[y1 * TXp1 + x1] - S[y0 * TXp1 + x1] - S[y1 * TXp1 + x0] + S[y0 * TXp1 + x0];
+}
+
+// ---------------------------------------------------------------------------
+// per-pixel alpha of one staged Gaussian.  Forward and backward MUST take the same
+// discrete decisions, so the op sequence is pinned with _rn intrinsics (no contraction).
+// dx, dy = (u - x, v - y) in tile-local fp32 coordinates.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float power_of(float ca, float cb, float cc, float dx, float dy)
+{
+    const float qa = __fmul_rn(ca, __fmul_rn(dx, dx));
+    const float qc = __fmul_rn(cc, __fmul_rn(dy, dy));
+    const float qb = __fmul_rn(cb, __fmul_rn(dx, dy));
+    return __fsub_rn(__fmul_rn(-0.5f, __fadd_rn(qa, qc)), qb);
+}
+
+// SH basis (3DGS order and signs, R15), fp32
+__device__ __forceinline__ void sh_eval_basis(int D, float x, float y, float z, float *Y)
+{
+    Y[0] = 0.28209479177387814f;
+    if (D < 1) return;
+    Y[1] = -0.4886025119029199f * y;
+    Y[2] = 0.4886025119029199f * z;
+    Y[3] = -0.4886025119029199f * x;
+    if (D < 2) return;
+    const float xx = x * x, yy = y * y, zz = z * z;
+    Y[4] = 1.0925484305920792f * x * y;
+    Y[5] = -1.0925484305920792f * y * z;
+    Y[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
+    Y[7] = -1.0925484305920792f * x * z;
+    Y[8] = 0.5462742152960396f * (xx - yy);
+    if (D < 3) return;
+    Y[9] = -0.5900435899266435f * y * (3.0f * xx - yy);
+    Y[10] = 2.890611442640554f * x * y * z;
+    Y[11] = -0.4570457994644658f * y * (4.0f * zz - xx - yy);
+    Y[12] = 0.3731763325901154f * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+    Y[13] = -0.4570457994644658f * x * (4.0f * zz - xx - yy);
+    Y[14] = 1.445305721320277f * z * (xx - yy);
+    Y[15] = -0.5900435899266435f * x * (xx - 3.0f * yy);
+}
+
+__device__ __forceinline__ float sh_lane(const float4 &v, int lane)
+{
+    return lane == 0 ? v.x : (lane == 1 ? v.y : (lane == 2 ? v.z : v.w));
+}
+
+// unit viewing direction d = (mu - o_cam)/|mu - o_cam|; returns 1/|mu - o_cam|
+__device__ __forceinline__ float view_dir(const float4 &mo, const GCam &c, float d[3])
+{
+    float x = mo.x - c.oc[0], y = mo.y - c.oc[1], z = mo.z - c.oc[2];
+    const float inv = rsqrtf(x * x + y * y + z * z);
+    d[0] = x * inv; d[1] = y * inv; d[2] = z * inv;
+    return inv;
+}
+
+// raw SH colour (before the +1/2 offset's clamp): col = SH(d) + 1/2, fp32.  Forward and
+// backward call this same function so the clamp decision (col < 0) is identical.
+template <int D>
+__device__ __forceinline__ void sh_color_raw(const float4 *__restrict__ sh, int n, int i, const float d[3],
+                                             float Y[16], float col[3])
+{
+    constexpr int K = (D + 1) * (D + 1);
+    constexpr int K4 = (3 * K + 3) / 4;
+    sh_eval_basis(D, d[0], d[1], d[2], Y);
+    col[0] = col[1] = col[2] = 0.5f;
+#pragma unroll
+    for (int ch4 = 0; ch4 < K4; ch4++) {
+        const float4 f = __ldg(sh + (size_t)ch4 * n + i);
+#pragma unroll
+        for (int l = 0; l < 4; l++) {
+            const int e = 4 * ch4 + l;
+            if (e < 3 * K) col[e % 3] += Y[e / 3] * sh_lane(f, l);
+        }
+    }
+}
+
+}  // namespace cls
+
+// host-side launch helpers (ctx.cu)
+namespace cls {
+struct LaunchInfo;
+}

@@ -1,0 +1,382 @@
+// ctx.cu -- the C ABI of libcls (include/cls.h): context, capacities, validation and
+// the launch orchestration of one local-optimisation step.  Every arithmetic step of the
+// path runs in the kernels of k_*.cu; this file only validates, marshals the host
+// structs into kernel parameters and enqueues work.
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <new>
+#include <string>
+
+#include "kernels.h"
+
+using namespace cls;
+
+struct cls_ctx {
+    int device = 0;
+    cls_limits lim{};
+    int maxTX = 0, maxTY = 0, maxT = 0;
+    Scratch s{};
+    Counters *h_cnt = nullptr;   // pinned copy of the counters of the last fwd
+    int *h_A = nullptr;          // pinned
+    cudaEvent_t ev_member = nullptr, ev_fwd = nullptr;
+    bool fwd_valid = false, has_targets = false, bwd_valid = false;
+    StepDims dims{};
+    CamSet cams{};
+    float3 bg{};
+    cudaStream_t last_stream = nullptr;
+    int64_t launches0 = 0;
+    std::string err;
+};
+
+namespace {
+
+cls_status fail(cls_ctx *c, cls_status st, const char *fmt, ...)
+{
+    if (c) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        c->err = buf;
+    }
+    return st;
+}
+
+cls_status check_cuda(cls_ctx *c, const char *where)
+{
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(c, CLS_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+    return CLS_OK;
+}
+
+template <typename T>
+bool dalloc(T **p, size_t count)
+{
+    if (count == 0) count = 1;
+    return cudaMalloc((void **)p, sizeof(T) * count) == cudaSuccess;
+}
+
+bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+const char *cls_status_string(cls_status s)
+{
+    switch (s) {
+    case CLS_OK: return "CLS_OK";
+    case CLS_ERR_INVALID_ARGUMENT: return "CLS_ERR_INVALID_ARGUMENT";
+    case CLS_ERR_DIMENSION_MISMATCH: return "CLS_ERR_DIMENSION_MISMATCH";
+    case CLS_ERR_CAPACITY: return "CLS_ERR_CAPACITY";
+    case CLS_ERR_STATE: return "CLS_ERR_STATE";
+    case CLS_ERR_CUDA: return "CLS_ERR_CUDA";
+    case CLS_ERR_OUT_OF_MEMORY: return "CLS_ERR_OUT_OF_MEMORY";
+    }
+    return "CLS_ERR_UNKNOWN";
+}
+
+const char *cls_last_error(const cls_ctx *ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
+
+int64_t cls_launch_count(const cls_ctx *ctx) { return ctx ? (int64_t)(g_launches - ctx->launches0) : 0; }
+
+cls_status cls_destroy(cls_ctx *c)
+{
+    if (!c) return CLS_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(c->device);
+    void *ptrs[] = {c->s.idx, c->s.ord, c->s.st_member, c->s.mask, c->s.sat, c->s.diff, c->s.rec_xy, c->s.rec_co,
+                    c->s.rec_rgb, c->s.rec_rect, c->s.rec_meta, c->s.rec_depth, c->s.tile_cnt, c->s.tile_off,
+                    c->s.tile_cursor, c->s.st_tiles, c->s.items, c->s.item_of_tile, c->s.cls_small, c->s.cls_large,
+                    c->s.cls_huge, c->s.first_active, c->s.pair_key, c->s.pair_val, c->s.sort_tmp_key,
+                    c->s.sort_tmp_val, c->s.px_T, c->s.px_last, c->s.px_dl, c->s.item_loss, c->s.grad2d, c->s.cnt};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    if (c->h_cnt) cudaFreeHost(c->h_cnt);
+    if (c->h_A) cudaFreeHost(c->h_A);
+    if (c->ev_member) cudaEventDestroy(c->ev_member);
+    if (c->ev_fwd) cudaEventDestroy(c->ev_fwd);
+    delete c;
+    return CLS_OK;
+}
+
+cls_status cls_create(cls_ctx **out, int device, const cls_limits *lim)
+{
+    if (!out || !lim) return CLS_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    if (lim->max_gaussians <= 0 || lim->max_views <= 0 || lim->max_views > CLS_MAX_VIEWS || lim->max_width < 16 ||
+        lim->max_height < 16 || lim->max_records <= 0 || lim->max_pairs <= 0 || lim->max_pairs >= (1ll << 31) ||
+        lim->max_active <= 0 || lim->max_gaussians >= (1ll << 31) || lim->max_records >= (1ll << 31))
+        return CLS_ERR_INVALID_ARGUMENT;
+    if (cudaSetDevice(device) != cudaSuccess) return CLS_ERR_CUDA;
+    cls_ctx *c = new (std::nothrow) cls_ctx();
+    if (!c) return CLS_ERR_OUT_OF_MEMORY;
+    c->device = device;
+    c->lim = *lim;
+    c->launches0 = g_launches;
+    c->maxTX = (lim->max_width + CLS_TILE - 1) / CLS_TILE;
+    c->maxTY = (lim->max_height + CLS_TILE - 1) / CLS_TILE;
+    c->maxT = c->maxTX * c->maxTY;
+    const size_t N = (size_t)lim->max_gaussians, V = (size_t)lim->max_views, VT = V * c->maxT;
+    const size_t R = (size_t)lim->max_records, P = (size_t)lim->max_pairs;
+    const size_t SAT = V * (c->maxTY + 1) * (c->maxTX + 1);
+    Scratch &s = c->s;
+    bool ok = dalloc(&s.idx, N) && dalloc(&s.ord, N) && dalloc(&s.st_member, N / 2048 + 2) && dalloc(&s.mask, VT) &&
+              dalloc(&s.sat, SAT) && dalloc(&s.diff, SAT) && dalloc(&s.rec_xy, R) && dalloc(&s.rec_co, R) &&
+              dalloc(&s.rec_rgb, R) && dalloc(&s.rec_rect, R) && dalloc(&s.rec_meta, R) && dalloc(&s.rec_depth, R) &&
+              dalloc(&s.tile_cnt, VT) && dalloc(&s.tile_off, VT) && dalloc(&s.tile_cursor, VT) &&
+              dalloc(&s.st_tiles, VT / 2048 + 2) && dalloc(&s.items, VT) && dalloc(&s.item_of_tile, VT) &&
+              dalloc(&s.cls_small, VT) && dalloc(&s.cls_large, VT) && dalloc(&s.cls_huge, VT) &&
+              dalloc(&s.first_active, VT) && dalloc(&s.pair_key, P) && dalloc(&s.pair_val, P) &&
+              dalloc(&s.sort_tmp_key, (size_t)1 << 22) && dalloc(&s.sort_tmp_val, (size_t)1 << 22) &&
+              dalloc(&s.px_T, VT * 256) && dalloc(&s.px_last, VT * 256) && dalloc(&s.px_dl, VT * 768) &&
+              dalloc(&s.item_loss, VT) && dalloc(&s.grad2d, V * (size_t)lim->max_active * 3) && dalloc(&s.cnt, 1);
+    if (ok) ok = cudaMallocHost((void **)&c->h_cnt, sizeof(Counters)) == cudaSuccess &&
+                 cudaMallocHost((void **)&c->h_A, sizeof(int)) == cudaSuccess;
+    if (ok) ok = cudaEventCreateWithFlags(&c->ev_member, cudaEventDisableTiming) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&c->ev_fwd, cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) {
+        cudaGetLastError();
+        cls_destroy(c);
+        return CLS_ERR_OUT_OF_MEMORY;
+    }
+    s.max_records = (long long)R;
+    s.max_pairs = (long long)P;
+    s.max_items = (int)VT;
+    memset(c->h_cnt, 0, sizeof(Counters));
+    *out = c;
+    return CLS_OK;
+}
+
+cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *cams, int32_t n_views,
+                          int32_t n_views_total, const cls_region *regions, int32_t n_regions, const float *bg,
+                          const float *targets, float *images, uint8_t *tile_mask, float *loss, uint32_t flags,
+                          void *stream)
+{
+    if (!c) return CLS_ERR_INVALID_ARGUMENT;
+    c->fwd_valid = false;
+    c->bwd_valid = false;
+    if (!g || !cams || !bg || (n_regions > 0 && !regions))
+        return fail(c, CLS_ERR_INVALID_ARGUMENT, "null pointer argument");
+    if (g->n <= 0 || g->sh_degree < 0 || g->sh_degree > 3 || !g->mean_op || !g->quat || !g->log_scale || !g->sh)
+        return fail(c, CLS_ERR_INVALID_ARGUMENT, "bad Gaussian set (n=%lld, degree=%d)", (long long)g->n,
+                    g->sh_degree);
+    if (!aligned16(g->mean_op) || !aligned16(g->quat) || !aligned16(g->log_scale) || !aligned16(g->sh) ||
+        (targets && !aligned16(targets)))
+        return fail(c, CLS_ERR_INVALID_ARGUMENT, "float4 arrays must be 16-byte aligned");
+    if (g->n > c->lim.max_gaussians)
+        return fail(c, CLS_ERR_DIMENSION_MISMATCH, "n=%lld exceeds max_gaussians", (long long)g->n);
+    if (n_views <= 0 || n_views > c->lim.max_views || n_views_total < n_views)
+        return fail(c, CLS_ERR_DIMENSION_MISMATCH, "bad view count %d (total %d)", n_views, n_views_total);
+    if (n_regions < 0 || n_regions > CLS_MAX_REGIONS)
+        return fail(c, CLS_ERR_INVALID_ARGUMENT, "bad region count %d", n_regions);
+    const int W = cams[0].width, H = cams[0].height;
+    for (int v = 0; v < n_views; v++) {
+        const cls_camera &cm = cams[v];
+        if (cm.width < 16 || cm.height < 16 || !(cm.fx > 0.f) || !(cm.fy > 0.f))
+            return fail(c, CLS_ERR_INVALID_ARGUMENT, "view %d: bad intrinsics or size", v);
+        if (cm.width != W || cm.height != H)
+            return fail(c, CLS_ERR_DIMENSION_MISMATCH, "view %d: %dx%d differs from %dx%d", v, cm.width, cm.height, W,
+                        H);
+    }
+    if (W > c->lim.max_width || H > c->lim.max_height)
+        return fail(c, CLS_ERR_DIMENSION_MISMATCH, "image %dx%d exceeds the ctx limits", W, H);
+    RegSet regs{};
+    regs.n = n_regions;
+    for (int j = 0; j < n_regions; j++) {
+        const cls_region &r = regions[j];
+        if (r.kind == 0) {
+            if (!(r.r > 0.f)) return fail(c, CLS_ERR_INVALID_ARGUMENT, "region %d: radius must be > 0", j);
+        } else if (r.kind == 1) {
+            if (!(r.a[0] <= r.b[0] && r.a[1] <= r.b[1] && r.a[2] <= r.b[2]))
+                return fail(c, CLS_ERR_INVALID_ARGUMENT, "region %d: box lo > hi", j);
+        } else {
+            return fail(c, CLS_ERR_INVALID_ARGUMENT, "region %d: unknown kind %d", j, r.kind);
+        }
+        regs.kind[j] = r.kind;
+        for (int q = 0; q < 3; q++) { regs.a[j][q] = r.a[q]; regs.b[j][q] = r.b[q]; }
+        regs.r[j] = r.r;
+    }
+    if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, CLS_ERR_CUDA, "cudaSetDevice failed");
+    cudaStream_t st = (cudaStream_t)stream;
+    StepDims d{};
+    d.n = (int)g->n;
+    d.D = g->sh_degree;
+    d.K4 = (3 * (d.D + 1) * (d.D + 1) + 3) / 4;
+    d.V = n_views;
+    d.W = W; d.H = H;
+    d.TX = (W + CLS_TILE - 1) / CLS_TILE;
+    d.TY = (H + CLS_TILE - 1) / CLS_TILE;
+    d.T = d.TX * d.TY;
+    d.all_tiles = (flags & CLS_FLAG_ALL_TILES) ? 1 : 0;
+    CamSet cs{};
+    cs.n = n_views; cs.W = W; cs.H = H; cs.TX = d.TX; cs.TY = d.TY; cs.T = d.T;
+    for (int v = 0; v < n_views; v++) {
+        const cls_camera &cm = cams[v];
+        GCam &gc = cs.c[v];
+        memcpy(gc.R, cm.R, sizeof gc.R);
+        memcpy(gc.t, cm.t, sizeof gc.t);
+        gc.fx = cm.fx; gc.fy = cm.fy; gc.cx = cm.cx; gc.cy = cm.cy;
+        for (int q = 0; q < 3; q++)   // o_cam = -R^T t
+            gc.oc[q] = (float)-((double)cm.R[q] * cm.t[0] + (double)cm.R[3 + q] * cm.t[1] + (double)cm.R[6 + q] * cm.t[2]);
+        gc.pad = 0.f;
+    }
+    Params p{reinterpret_cast<const float4 *>(g->mean_op), reinterpret_cast<const float4 *>(g->quat),
+             reinterpret_cast<const float4 *>(g->log_scale), reinterpret_cast<const float4 *>(g->sh)};
+    const float3 bgc = make_float3(bg[0], bg[1], bg[2]);
+    const float loss_scale = (float)(1.0 / (3.0 * (double)H * (double)W * (double)n_views_total));
+    Scratch s = c->s;
+    s.max_items = d.V * d.T;
+
+    cudaMemsetAsync(s.cnt, 0, sizeof(Counters), st);
+    launch_member(p, d, regs, s, st);
+    cudaMemcpyAsync(c->h_A, &s.cnt->A, sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaEventRecord(c->ev_member, st);
+    launch_active_mask(p, d, cs, s, st);
+    launch_project(p, d, cs, s, st);
+    launch_bin(d, cs, s, st);
+    launch_fwd(d, cs, s, targets, images, loss_scale, bgc, st);
+    if (images) launch_fill_bg(d, s, images, bgc, st);
+    if (targets && loss) launch_loss(s, loss_scale, loss, st);
+    if (tile_mask) cudaMemcpyAsync(tile_mask, s.mask, (size_t)d.V * d.T, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(c->h_cnt, s.cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st);
+    cudaEventRecord(c->ev_fwd, st);
+    cls_status e = check_cuda(c, "cls_render_fwd");
+    if (e != CLS_OK) return e;
+    c->dims = d;
+    c->cams = cs;
+    c->bg = bgc;
+    c->has_targets = targets != nullptr;
+    c->fwd_valid = true;
+    c->last_stream = st;
+    return CLS_OK;
+}
+
+cls_status cls_active(cls_ctx *c, int64_t *A, const int32_t **idx)
+{
+    if (!c || !A) return CLS_ERR_INVALID_ARGUMENT;
+    if (!c->fwd_valid) return fail(c, CLS_ERR_STATE, "cls_active before cls_render_fwd");
+    if (cudaEventSynchronize(c->ev_member) != cudaSuccess)
+        return fail(c, CLS_ERR_CUDA, "membership event: %s", cudaGetErrorString(cudaGetLastError()));
+    *A = *c->h_A;
+    if (idx) *idx = c->s.idx;
+    if (*c->h_A > c->lim.max_active)
+        return fail(c, CLS_ERR_CAPACITY, "active set %d exceeds max_active %lld", *c->h_A,
+                    (long long)c->lim.max_active);
+    return CLS_OK;
+}
+
+cls_status cls_copy_active(cls_ctx *c, int32_t *dst, void *stream)
+{
+    if (!c || !dst) return CLS_ERR_INVALID_ARGUMENT;
+    if (!c->fwd_valid) return fail(c, CLS_ERR_STATE, "cls_copy_active before cls_render_fwd");
+    if (cudaEventSynchronize(c->ev_member) != cudaSuccess) return fail(c, CLS_ERR_CUDA, "membership event");
+    const int A = *c->h_A;
+    if (A > 0) cudaMemcpyAsync(dst, c->s.idx, sizeof(int) * (size_t)A, cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
+    return check_cuda(c, "cls_copy_active");
+}
+
+__global__ void k_zero_grad2d(Scratch s, int V, long long cap)
+{
+    const long long A = s.cnt->A;
+    if (A > cap) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&s.cnt->overflow, 4);
+        return;
+    }
+    const long long total = (long long)V * A * 3;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x)
+        s.grad2d[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+cls_status cls_render_bwd(cls_ctx *c, const cls_gaussians *g, const float *dL_dimages, float *grad_active,
+                          void *stream)
+{
+    if (!c) return CLS_ERR_INVALID_ARGUMENT;
+    if (!c->fwd_valid) return fail(c, CLS_ERR_STATE, "cls_render_bwd without a preceding cls_render_fwd");
+    if (!g || !grad_active) return fail(c, CLS_ERR_INVALID_ARGUMENT, "null pointer argument");
+    if (g->n != c->dims.n || g->sh_degree != c->dims.D)
+        return fail(c, CLS_ERR_STATE, "Gaussian set differs from the one of the fwd");
+    if (!dL_dimages && !c->has_targets)
+        return fail(c, CLS_ERR_STATE, "no dL_dimages and the fwd had no targets (no fused L1 gradient)");
+    if (!aligned16(grad_active)) return fail(c, CLS_ERR_INVALID_ARGUMENT, "grad_active must be 16-byte aligned");
+    cudaSetDevice(c->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    Params p{reinterpret_cast<const float4 *>(g->mean_op), reinterpret_cast<const float4 *>(g->quat),
+             reinterpret_cast<const float4 *>(g->log_scale), reinterpret_cast<const float4 *>(g->sh)};
+    Scratch s = c->s;
+    k_zero_grad2d<<<148 * 4, 256, 0, st>>>(s, c->dims.V, (long long)c->lim.max_active);
+    g_launches++;
+    launch_bwd_raster(c->dims, s, dL_dimages, c->bg, st);
+    launch_bwd_project(p, c->dims, c->cams, s, grad_active, st);
+    cls_status e = check_cuda(c, "cls_render_bwd");
+    if (e != CLS_OK) return e;
+    c->bwd_valid = true;
+    c->last_stream = st;
+    return CLS_OK;
+}
+
+cls_status cls_adam_masked(cls_ctx *c, float *mean_op, float *quat, float *log_scale, float *sh, float *m, float *v,
+                           const float *grad_active, const float *lr, float beta1, float beta2, float eps,
+                           int32_t step, void *stream)
+{
+    if (!c) return CLS_ERR_INVALID_ARGUMENT;
+    if (!c->fwd_valid) return fail(c, CLS_ERR_STATE, "cls_adam_masked without a preceding cls_render_fwd");
+    if (!mean_op || !quat || !log_scale || !sh || !m || !v || !grad_active || !lr)
+        return fail(c, CLS_ERR_INVALID_ARGUMENT, "null pointer argument");
+    if (step < 1 || !(beta1 >= 0.f && beta1 < 1.f) || !(beta2 >= 0.f && beta2 < 1.f) || !(eps >= 0.f))
+        return fail(c, CLS_ERR_INVALID_ARGUMENT, "bad Adam hyper-parameters (step=%d)", step);
+    if (!aligned16(mean_op) || !aligned16(quat) || !aligned16(log_scale) || !aligned16(sh) || !aligned16(m) ||
+        !aligned16(v) || !aligned16(grad_active))
+        return fail(c, CLS_ERR_INVALID_ARGUMENT, "float4 arrays must be 16-byte aligned");
+    cudaSetDevice(c->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const float bc1 = (float)(1.0 - pow((double)beta1, (double)step));
+    const float bc2 = (float)(1.0 - pow((double)beta2, (double)step));
+    launch_adam(c->dims, c->s, (float4 *)mean_op, (float4 *)quat, (float4 *)log_scale, (float4 *)sh, (float4 *)m,
+                (float4 *)v, (const float4 *)grad_active, lr, beta1, beta2, eps, bc1, bc2, st);
+    c->last_stream = st;
+    return check_cuda(c, "cls_adam_masked");
+}
+
+cls_status cls_stats(cls_ctx *c, cls_stats_t *out)
+{
+    if (!c || !out) return CLS_ERR_INVALID_ARGUMENT;
+    if (!c->fwd_valid) return fail(c, CLS_ERR_STATE, "cls_stats before cls_render_fwd");
+    if (cudaEventSynchronize(c->ev_fwd) != cudaSuccess)
+        return fail(c, CLS_ERR_CUDA, "fwd event: %s", cudaGetErrorString(cudaGetLastError()));
+    if (c->last_stream) cudaStreamSynchronize(c->last_stream);
+    // refresh the overflow bit (bwd may have set bit 2)
+    int ovf = 0;
+    cudaMemcpy(&ovf, &c->s.cnt->overflow, sizeof(int), cudaMemcpyDeviceToHost);
+    const Counters &h = *c->h_cnt;
+    memset(out, 0, sizeof *out);
+    out->n_active = h.A;
+    out->n_records = h.n_records;
+    out->n_pairs = (int64_t)h.n_pairs;
+    out->n_items = h.n_items;
+    out->n_views = c->dims.V;
+    for (int v = 0; v < c->dims.V; v++) out->n_active_tiles[v] = h.active_tiles[v];
+    out->overflow = h.overflow | ovf;
+    out->max_list = h.max_list;
+    out->n_huge_tiles = h.n_huge;
+    if (out->overflow)
+        return fail(c, CLS_ERR_CAPACITY, "capacity overflow (bits %d): records %d/%lld pairs %llu/%lld A %d/%lld",
+                    out->overflow, h.n_records, (long long)c->lim.max_records, h.n_pairs,
+                    (long long)c->lim.max_pairs, h.A, (long long)c->lim.max_active);
+    return check_cuda(c, "cls_stats");
+}
+
+cls_status cls_debug_grad2d(cls_ctx *c, float *out, void *stream)
+{
+    if (!c || !out) return CLS_ERR_INVALID_ARGUMENT;
+    if (!c->bwd_valid) return fail(c, CLS_ERR_STATE, "cls_debug_grad2d before cls_render_bwd");
+    cudaEventSynchronize(c->ev_member);
+    const size_t bytes = sizeof(float4) * 3 * (size_t)c->dims.V * (size_t)(*c->h_A);
+    cudaMemcpyAsync(out, c->s.grad2d, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
+    return check_cuda(c, "cls_debug_grad2d");
+}
+
+}  // extern "C"

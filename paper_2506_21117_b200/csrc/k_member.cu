@@ -1,0 +1,176 @@
+// k_member.cu -- subsystem (1): active-region membership with stable warp-ballot
+// compaction, and the dynamic tile mask (PAPER.md Supp. L538-539, modification 1).
+//
+// Membership (reading R21): Gaussian i is in O^t iff its centre lies in
+// the union of the change regions (spheres, or axis-aligned boxes for config c3),
+// boundaries inclusive.  The test is done in fp64 with a fixed operation order so
+// that the integer decision is the one the fp64 definition takes.
+// Compaction is order preserving (idx ascending) -- identical on every DP rank (H5) --
+// via warp ballots + popc, a block scan and a single-pass decoupled look-back.
+#include "kernels.h"
+
+namespace cls {
+
+int64_t g_launches = 0;
+
+#define MEMBER_THREADS 256
+#define MEMBER_ITEMS 8
+#define MEMBER_TILE (MEMBER_THREADS * MEMBER_ITEMS)
+
+__device__ __forceinline__ bool in_regions(const float4 m, const RegSet &regs)
+{
+    const double x = m.x, y = m.y, z = m.z;
+    for (int j = 0; j < regs.n; j++) {
+        if (regs.kind[j] == 0) {
+            const double dx = __dsub_rn(x, (double)regs.a[j][0]);
+            const double dy = __dsub_rn(y, (double)regs.a[j][1]);
+            const double dz = __dsub_rn(z, (double)regs.a[j][2]);
+            const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+            const double r = regs.r[j];
+            if (d2 <= __dmul_rn(r, r)) return true;
+        } else {
+            if (m.x >= regs.a[j][0] && m.x <= regs.b[j][0] && m.y >= regs.a[j][1] && m.y <= regs.b[j][1] &&
+                m.z >= regs.a[j][2] && m.z <= regs.b[j][2])
+                return true;
+        }
+    }
+    return false;
+}
+
+__global__ void __launch_bounds__(MEMBER_THREADS)
+k_member(const float4 *__restrict__ mean_op, int n, const __grid_constant__ RegSet regs, Scratch s)
+{
+    __shared__ int s_tile;
+    __shared__ int s_wcnt[MEMBER_ITEMS][MEMBER_THREADS / 32];
+    __shared__ unsigned long long s_prefix;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(&s.cnt->member_tiles, 1);
+    __syncthreads();
+    const int tile = s_tile;
+    const int base = tile * MEMBER_TILE;
+    unsigned ballots[MEMBER_ITEMS];
+#pragma unroll
+    for (int k = 0; k < MEMBER_ITEMS; k++) {
+        const int i = base + k * MEMBER_THREADS + tid;
+        bool in = false;
+        if (i < n) in = in_regions(__ldg(mean_op + i), regs);
+        ballots[k] = __ballot_sync(0xffffffffu, in);
+        if (lane == 0) s_wcnt[k][warp] = __popc(ballots[k]);
+    }
+    __syncthreads();
+    // exclusive scan over (round, warp) in index order, by warp 0
+    if (warp == 0) {
+        const int nw = MEMBER_THREADS / 32;
+        const int total_cells = MEMBER_ITEMS * nw;   // 64
+        int v0 = lane < total_cells ? s_wcnt[lane / nw][lane % nw] : 0;
+        int v1 = lane + 32 < total_cells ? s_wcnt[(lane + 32) / nw][(lane + 32) % nw] : 0;
+        int inc0 = v0, inc1 = v1;
+        for (int o = 1; o < 32; o <<= 1) {
+            int t0 = __shfl_up_sync(0xffffffffu, inc0, o);
+            int t1 = __shfl_up_sync(0xffffffffu, inc1, o);
+            if (lane >= o) { inc0 += t0; inc1 += t1; }
+        }
+        const int tot0 = __shfl_sync(0xffffffffu, inc0, 31);
+        inc1 += tot0;
+        if (lane < total_cells) s_wcnt[lane / nw][lane % nw] = inc0 - v0;
+        if (lane + 32 < total_cells) s_wcnt[(lane + 32) / nw][(lane + 32) % nw] = inc1 - v1;
+        const int agg = __shfl_sync(0xffffffffu, inc1, 31);
+        if (lane == 0) {
+            unsigned long long pre = lookback(s.st_member, tile, (unsigned long long)agg);
+            s_prefix = pre;
+            if (tile == (int)gridDim.x - 1) s.cnt->A = (int)(pre + agg);
+        }
+    }
+    __syncthreads();
+    const int prefix = (int)s_prefix;
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int k = 0; k < MEMBER_ITEMS; k++) {
+        const int i = base + k * MEMBER_THREADS + tid;
+        if (i >= n) continue;
+        const bool in = (ballots[k] >> lane) & 1u;
+        const int pos = prefix + s_wcnt[k][warp] + __popc(ballots[k] & lt);
+        if (in) s.idx[pos] = i;
+        s.ord[i] = in ? pos : -1;
+    }
+}
+
+void launch_member(const Params &g, const StepDims &d, const RegSet &regs, const Scratch &s, cudaStream_t st)
+{
+    const int blocks = (d.n + MEMBER_TILE - 1) / MEMBER_TILE;
+    cudaMemsetAsync(s.st_member, 0, sizeof(unsigned long long) * blocks, st);
+    k_member<<<blocks, MEMBER_THREADS, 0, st>>>(g.mean_op, d.n, regs, s);
+    g_launches++;
+}
+
+// ---------------------------------------------------------------------------
+// Active tile mask (modification 1): project every active Gaussian into every view
+// and set the tiles of its rect (reading R9: rect overlap, the only reading under
+// which the exactness claim P:201 holds).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+k_active_rects(const float4 *__restrict__ mean_op, const float4 *__restrict__ quat,
+               const float4 *__restrict__ log_scale, const __grid_constant__ CamSet cams, Scratch s)
+{
+    const int A = s.cnt->A;
+    const long long total = (long long)A * cams.n;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int k = (int)(e / cams.n), v = (int)(e % cams.n);
+        const int i = s.idx[k];
+        Proj p;
+        if (!project_gaussian(__ldg(mean_op + i), __ldg(quat + i), __ldg(log_scale + i), cams.c[v], cams.W, cams.H,
+                              cams.TX, cams.TY, p))
+            continue;
+        uint8_t *mk = s.mask + (size_t)v * cams.T;
+        for (int ty = p.y0; ty < p.y1; ty++)
+            for (int tx = p.x0; tx < p.x1; tx++) mk[ty * cams.TX + tx] = 1;
+    }
+}
+
+// summed-area table of each view's mask, one block per view
+__global__ void __launch_bounds__(256) k_sat(const __grid_constant__ CamSet cams, Scratch s)
+{
+    const int v = blockIdx.x;
+    const int TX = cams.TX, TY = cams.TY, P = TX + 1;
+    const uint8_t *mk = s.mask + (size_t)v * cams.T;
+    int *S = s.sat + (size_t)v * (TY + 1) * P;
+    for (int x = threadIdx.x; x < P; x += blockDim.x) S[x] = 0;
+    // row prefix sums
+    for (int y = threadIdx.x; y < TY; y += blockDim.x) {
+        int acc = 0;
+        S[(y + 1) * P] = 0;
+        for (int x = 0; x < TX; x++) {
+            acc += mk[y * TX + x];
+            S[(y + 1) * P + x + 1] = acc;
+        }
+    }
+    __syncthreads();
+    // column prefix sums
+    for (int x = threadIdx.x; x < P; x += blockDim.x) {
+        int acc = 0;
+        for (int y = 1; y <= TY; y++) {
+            acc += S[y * P + x];
+            S[y * P + x] = acc;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s.cnt->active_tiles[v] = S[TY * P + TX];
+}
+
+void launch_active_mask(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st)
+{
+    if (d.all_tiles) {
+        cudaMemsetAsync(s.mask, 1, (size_t)d.V * d.T, st);
+    } else {
+        cudaMemsetAsync(s.mask, 0, (size_t)d.V * d.T, st);
+        int blocks = (int)std::min<long long>(((long long)d.n * d.V + 255) / 256, 148LL * 8);
+        if (blocks < 1) blocks = 1;
+        k_active_rects<<<blocks, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, cams, s);
+        g_launches++;
+    }
+    k_sat<<<d.V, 256, 0, st>>>(cams, s);
+    g_launches++;
+}
+
+}  // namespace cls

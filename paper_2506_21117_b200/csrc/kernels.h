@@ -1,0 +1,45 @@
+// kernels.h -- host launchers of the step's kernels (one per subsystem of BASELINE north_star).
+#pragma once
+#include <algorithm>
+
+#include "cls_internal.cuh"
+
+namespace cls {
+
+struct StepDims {
+    int n;          // Gaussians
+    int D;          // SH degree
+    int K4;         // float4 SH chunks
+    int V, W, H, TX, TY, T;
+    int all_tiles;
+};
+
+struct Params {
+    const float4 *mean_op, *quat, *log_scale, *sh;
+};
+
+// (1) membership + stable compaction -> idx, ord, A        (k_member.cu)
+void launch_member(const Params &g, const StepDims &d, const RegSet &regs, const Scratch &s, cudaStream_t st);
+// (1b) active tile mask per view + summed-area tables       (k_member.cu)
+void launch_active_mask(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st);
+// (2) projection / cull of every Gaussian vs the mask -> records (k_project.cu)
+void launch_project(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st);
+// (3) binning: tile counts, scan, key emission, per-tile sort  (k_bin.cu)
+void launch_bin(const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st);
+// (4) forward compositing + fused L1                           (k_raster.cu)
+void launch_fwd(const StepDims &d, const CamSet &cams, const Scratch &s, const float *targets, float *images,
+                float loss_scale, float3 bg, cudaStream_t st);
+void launch_fill_bg(const StepDims &d, const Scratch &s, float *images, float3 bg, cudaStream_t st);
+void launch_loss(const Scratch &s, float loss_scale, float *loss, cudaStream_t st);
+// (5) backward raster + backward projection                    (k_raster.cu, k_bwd_project.cu)
+void launch_bwd_raster(const StepDims &d, const Scratch &s, const float *dL_dimages, float3 bg, cudaStream_t st);
+void launch_bwd_project(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s,
+                        float *grad_active, cudaStream_t st);
+// (6) masked Adam                                              (k_adam.cu)
+void launch_adam(const StepDims &d, const Scratch &s, float4 *mean_op, float4 *quat, float4 *log_scale, float4 *sh,
+                 float4 *m, float4 *v, const float4 *grad_active, const float lr[6], float b1, float b2, float eps,
+                 float bc1, float bc2, cudaStream_t st);
+
+extern int64_t g_launches;   // kernels launched by this process through libcls (host counter)
+
+}  // namespace cls

@@ -1,0 +1,259 @@
+"""Python front end of the local-optimisation step (§3.3, Supp. L508-541).
+
+PyTorch is used only for device memory, streams and process groups; every step of the
+path (membership, mask, projection, binning, compositing, backward, Adam) runs in
+libcls.so's CUDA kernels through the C ABI (``_native``).  This module only lays the
+parameters out in the ABI's chunk-major float4 SoA format and marshals host structs.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _native as N
+from ._native import check, lib
+
+
+def k4(sh_degree: int) -> int:
+    return -(-3 * (sh_degree + 1) ** 2 // 4)
+
+
+def row4(sh_degree: int) -> int:
+    return 3 + k4(sh_degree)
+
+
+def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+class GaussianParams:
+    """Device-resident scene in the C-ABI layout plus its Adam moments.
+
+    mean_op [n,4] (x,y,z,opacity logit), quat [n,4] (w,x,y,z), log_scale [n,4] (pad lane 0),
+    sh [K4,n,4] (coefficient k, channel c at float 3k+c of the row), m/v [3+K4,n,4].
+    """
+
+    def __init__(self, mean_op, quat, log_scale, sh, sh_degree: int):
+        self.mean_op, self.quat, self.log_scale, self.sh = mean_op, quat, log_scale, sh
+        self.sh_degree = int(sh_degree)
+        self.n = int(mean_op.shape[0])
+        self.device = mean_op.device
+        r = row4(self.sh_degree)
+        self.m = torch.zeros((r, self.n, 4), dtype=torch.float32, device=self.device)
+        self.v = torch.zeros((r, self.n, 4), dtype=torch.float32, device=self.device)
+        self.step = 0
+
+    @classmethod
+    def from_arrays(cls, means, log_scales, quats, opacity_logits, sh, sh_degree, device="cuda"):
+        n = len(means)
+        K = (sh_degree + 1) ** 2
+        kk = k4(sh_degree)
+        mo = np.zeros((n, 4), np.float32)
+        mo[:, :3] = means
+        mo[:, 3] = opacity_logits
+        ls = np.zeros((n, 4), np.float32)
+        ls[:, :3] = log_scales
+        shf = np.zeros((n, 4 * kk), np.float32)
+        shf[:, : 3 * K] = np.asarray(sh, np.float32).reshape(n, 3 * K)
+        shc = np.ascontiguousarray(shf.reshape(n, kk, 4).transpose(1, 0, 2))
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(device)
+        return cls(t(mo), t(np.asarray(quats, np.float32)), t(ls), t(shc), sh_degree)
+
+    @classmethod
+    def from_scene(cls, scene, device="cuda"):
+        return cls.from_arrays(scene.means, scene.log_scales, scene.quats, scene.opacity_logits, scene.sh,
+                               scene.sh_degree, device)
+
+    def struct(self) -> N.cls_gaussians:
+        return N.cls_gaussians(self.n, self.sh_degree, self.mean_op.data_ptr(), self.quat.data_ptr(),
+                               self.log_scale.data_ptr(), self.sh.data_ptr())
+
+    def rows(self, idx: torch.Tensor) -> torch.Tensor:
+        """Gather ABI rows [len(idx), ROW4, 4] of the parameters (layout helper for tests)."""
+        idx = idx.long()
+        parts = [self.mean_op[idx][:, None], self.quat[idx][:, None], self.log_scale[idx][:, None],
+                 self.sh[:, idx].permute(1, 0, 2)]
+        return torch.cat(parts, dim=1)
+
+    def moment_rows(self, which: str, idx: torch.Tensor) -> torch.Tensor:
+        t = self.m if which == "m" else self.v
+        return t[:, idx.long()].permute(1, 0, 2)
+
+    def to_numpy(self):
+        """(means, log_scales, quats, opacity_logits, sh[n,K,3]) as float32 numpy (layout helper)."""
+        K = (self.sh_degree + 1) ** 2
+        mo = self.mean_op.cpu().numpy()
+        shf = self.sh.permute(1, 0, 2).reshape(self.n, -1).cpu().numpy()[:, : 3 * K].reshape(self.n, K, 3)
+        return (mo[:, :3].copy(), self.log_scale.cpu().numpy()[:, :3].copy(), self.quat.cpu().numpy().copy(),
+                mo[:, 3].copy(), shf.copy())
+
+
+def camera_structs(cameras) -> ctypes.Array:
+    arr = (N.cls_camera * len(cameras))()
+    for j, c in enumerate(cameras):
+        arr[j].fx, arr[j].fy, arr[j].cx, arr[j].cy = float(c.fx), float(c.fy), float(c.cx), float(c.cy)
+        arr[j].R[:] = [float(x) for x in np.asarray(c.R, np.float32).reshape(9)]
+        arr[j].t[:] = [float(x) for x in np.asarray(c.t, np.float32).reshape(3)]
+        arr[j].width, arr[j].height = int(c.width), int(c.height)
+    return arr
+
+
+def region_structs(regions) -> ctypes.Array:
+    arr = (N.cls_region * max(len(regions), 1))()
+    for j, r in enumerate(regions):
+        arr[j].kind = int(r.kind)
+        arr[j].a[:] = [float(x) for x in np.asarray(r.a, np.float32).reshape(3)]
+        arr[j].b[:] = [float(x) for x in np.asarray(r.b, np.float32).reshape(3)]
+        arr[j].r = float(r.r)
+    return arr
+
+
+def default_limits(n, n_views, width, height, records_per_view=None, pairs_per_view=None, max_active=None):
+    TX, TY = -(-width // 16), -(-height // 16)
+    if records_per_view is None:
+        records_per_view = min(n, max(4096, n // 2))
+    if pairs_per_view is None:
+        pairs_per_view = min(TX * TY * 4096, 24 * records_per_view + 65536)
+    lim = N.cls_limits()
+    lim.max_gaussians = n
+    lim.max_records = min(int(records_per_view) * n_views, 2**31 - 1)
+    lim.max_pairs = min(int(pairs_per_view) * n_views, 2**31 - 2)
+    lim.max_active = max_active if max_active is not None else n
+    lim.max_views = n_views
+    lim.max_width, lim.max_height = width, height
+    return lim
+
+
+@dataclass
+class ForwardResult:
+    loss: Optional[torch.Tensor]
+    images: Optional[torch.Tensor]
+    tile_mask: Optional[torch.Tensor]
+
+
+class LocalOptimizer:
+    """One ctx of libcls bound to a device; runs fwd / bwd / masked Adam of the step."""
+
+    def __init__(self, params: GaussianParams, regions, limits: Optional[N.cls_limits] = None,
+                 lr=(1e-3,) * 6, betas=(0.9, 0.999), eps=1e-15, bg=(0.0, 0.0, 0.0), max_views=None,
+                 width=None, height=None):
+        self.params = params
+        self.regions = list(regions)
+        self.lr = (ctypes.c_float * 6)(*[float(x) for x in lr])
+        self.betas = betas
+        self.eps = float(eps)
+        self.bg = (ctypes.c_float * 3)(*[float(x) for x in bg])
+        if limits is None:
+            limits = default_limits(params.n, max_views or 8, width or 1920, height or 1080)
+        self.limits = limits
+        dev = params.device.index if params.device.index is not None else torch.cuda.current_device()
+        h = ctypes.c_void_p()
+        check(lib.cls_create(ctypes.byref(h), dev, ctypes.byref(limits)))
+        self.ctx = h
+        self._reg = region_structs(self.regions)
+        self._A = None
+        self._fwd_views = 0
+
+    def close(self):
+        if self.ctx:
+            lib.cls_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- the three C-ABI calls -------------------------------------------------------------------
+    def forward(self, cameras, targets: Optional[torch.Tensor] = None, n_views_total: Optional[int] = None,
+                images: bool = False, tile_mask: bool = False, all_tiles: bool = False,
+                stream=None) -> ForwardResult:
+        cams = camera_structs(cameras)
+        V = len(cameras)
+        W, H = cameras[0].width, cameras[0].height
+        dev = self.params.device
+        loss = torch.zeros(1, dtype=torch.float32, device=dev) if targets is not None else None
+        img = torch.empty((V, 3, H, W), dtype=torch.float32, device=dev) if images else None
+        tm = torch.empty((V, -(-H // 16), -(-W // 16)), dtype=torch.uint8, device=dev) if tile_mask else None
+        if targets is not None:
+            assert targets.is_contiguous() and targets.dtype == torch.float32 and tuple(targets.shape) == (V, 3, H, W)
+        g = self.params.struct()
+        st = check(lib.cls_render_fwd(
+            self.ctx, ctypes.byref(g), cams, V, int(n_views_total or V), self._reg, len(self.regions), self.bg,
+            ctypes.c_void_p(targets.data_ptr() if targets is not None else None),
+            ctypes.c_void_p(img.data_ptr() if img is not None else None),
+            ctypes.c_void_p(tm.data_ptr() if tm is not None else None),
+            ctypes.c_void_p(loss.data_ptr() if loss is not None else None),
+            N.CLS_FLAG_ALL_TILES if all_tiles else 0, ctypes.c_void_p(_stream_ptr(stream))), self.ctx)
+        self._A = None
+        self._fwd_views = V
+        return ForwardResult(loss, img, tm)
+
+    def active_count(self) -> int:
+        A = ctypes.c_int64()
+        check(lib.cls_active(self.ctx, ctypes.byref(A), None), self.ctx)
+        self._A = int(A.value)
+        return self._A
+
+    def active_indices(self, stream=None) -> torch.Tensor:
+        A = self.active_count()
+        out = torch.empty(max(A, 1), dtype=torch.int32, device=self.params.device)
+        check(lib.cls_copy_active(self.ctx, ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(_stream_ptr(stream))),
+              self.ctx)
+        return out[:A]
+
+    def backward(self, dL_dimages: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        A = self.active_count() if self._A is None else self._A
+        grad = torch.empty((max(A, 1), row4(self.params.sh_degree), 4), dtype=torch.float32,
+                           device=self.params.device)
+        g = self.params.struct()
+        check(lib.cls_render_bwd(self.ctx, ctypes.byref(g),
+                                 ctypes.c_void_p(dL_dimages.data_ptr() if dL_dimages is not None else None),
+                                 ctypes.c_void_p(grad.data_ptr()), ctypes.c_void_p(_stream_ptr(stream))), self.ctx)
+        return grad[:A]
+
+    def adam(self, grad: torch.Tensor, step: Optional[int] = None, stream=None):
+        p = self.params
+        if step is None:
+            p.step += 1
+            step = p.step
+        gptr = grad.data_ptr() if grad.numel() else p.m.data_ptr()   # A = 0: nothing is read
+        check(lib.cls_adam_masked(self.ctx, ctypes.c_void_p(p.mean_op.data_ptr()), ctypes.c_void_p(p.quat.data_ptr()),
+                                  ctypes.c_void_p(p.log_scale.data_ptr()), ctypes.c_void_p(p.sh.data_ptr()),
+                                  ctypes.c_void_p(p.m.data_ptr()), ctypes.c_void_p(p.v.data_ptr()),
+                                  ctypes.c_void_p(gptr), self.lr, float(self.betas[0]), float(self.betas[1]),
+                                  self.eps, int(step), ctypes.c_void_p(_stream_ptr(stream))), self.ctx)
+
+    def debug_grad2d(self) -> torch.Tensor:
+        A = self.active_count() if self._A is None else self._A
+        out = torch.empty((self._fwd_views, max(A, 1), 12), dtype=torch.float32, device=self.params.device)
+        check(lib.cls_debug_grad2d(self.ctx, ctypes.c_void_p(out.data_ptr()),
+                                   ctypes.c_void_p(_stream_ptr(None))), self.ctx)
+        return out[:, :A]
+
+    def stats(self) -> dict:
+        st = N.cls_stats_t()
+        check(lib.cls_stats(self.ctx, ctypes.byref(st)), self.ctx)
+        return st.as_dict()
+
+    def launch_count(self) -> int:
+        return int(lib.cls_launch_count(self.ctx))
+
+    # -- one full local-optimisation step ----------------------------------------------------------
+    def step(self, cameras, targets: torch.Tensor, n_views_total: Optional[int] = None,
+             allreduce: Optional[Callable[[torch.Tensor, torch.Tensor], None]] = None, stream=None):
+        """fwd -> |O^t| -> bwd -> (optional all-reduce of grad rows + loss) -> masked Adam.
+        Returns the device loss tensor (this rank's share unless all-reduced)."""
+        res = self.forward(cameras, targets, n_views_total=n_views_total, stream=stream)
+        grad = self.backward(stream=stream)
+        if allreduce is not None:
+            allreduce(grad, res.loss)
+        self.adam(grad, stream=stream)
+        return res.loss

@@ -1,0 +1,92 @@
+"""Shared helpers of the GPU parity tests: run the CUDA path through the C ABI and the
+oracle on the same seeded inputs, and compare them with the protocol of DESIGN.md
+("Parity protocol")."""
+from __future__ import annotations
+
+import numpy as np
+
+import oracle
+
+IMG_TOL = 1e-4          # north_star: images within 1e-4 absolute per channel
+AMB_TOL = 5e-3          # ambiguous pixels: at most one threshold flip
+AMB_FRAC = 1e-3         # at most this fraction of compared pixels may be ambiguous
+GRAD_REL = 1e-3         # north_star: gradients within 1e-3 relative ...
+GRAD_ABS_FRAC = 1e-5    # ... or 1e-5 x max|g| of the column (absolute floor)
+
+
+def gpu_run(scene, views=None, dL=None, all_tiles=False, images=True, limits=None, step_adam=False, lr=None):
+    """Run fwd (+bwd) of the CUDA path. Returns numpy results."""
+    import torch
+    from paper_2506_21117_b200 import GaussianParams, LocalOptimizer, default_limits
+
+    views = list(range(len(scene.cameras))) if views is None else list(views)
+    cams = [scene.cameras[v] for v in views]
+    W, H = scene.width, scene.height
+    params = GaussianParams.from_scene(scene)
+    if limits is None:
+        limits = default_limits(scene.n, max(len(cams), 1), W, H)
+    opt = LocalOptimizer(params, scene.regions, limits=limits, lr=lr or (1e-3,) * 6)
+    tg = None
+    if scene.targets is not None:
+        tg = torch.from_numpy(np.ascontiguousarray(scene.targets[views])).cuda()
+    res = opt.forward(cams, tg, n_views_total=len(scene.cameras), images=images, tile_mask=True,
+                      all_tiles=all_tiles)
+    idx = opt.active_indices()
+    up = None
+    if dL is not None:
+        up = torch.from_numpy(np.ascontiguousarray(np.asarray(dL, np.float32))).cuda()
+    grad = opt.backward(up)
+    g2d = opt.debug_grad2d()
+    out = dict(idx=idx.cpu().numpy(), tile_mask=res.tile_mask.cpu().numpy().astype(bool),
+               loss=None if res.loss is None else float(res.loss.item()), grad=grad.cpu().numpy(),
+               grad2d=g2d.cpu().numpy(), stats=opt.stats(), launches=opt.launch_count())
+    if images:
+        out["images"] = res.images.cpu().numpy()
+    if step_adam:
+        rows_before = params.rows(idx).cpu().numpy()
+        opt.adam(grad)
+        torch.cuda.synchronize()
+        out["rows_before"] = rows_before
+        out["rows_after"] = params.rows(idx).cpu().numpy()
+        out["m_after"] = params.moment_rows("m", idx).cpu().numpy()
+        out["v_after"] = params.moment_rows("v", idx).cpu().numpy()
+        out["params"] = params
+    out["opt"] = opt
+    return out
+
+
+def compare_images(gpu_img, orc_render, mask_tiles=True):
+    """Image parity: |d| <= 1e-4 outside the ambiguity set; ambiguous pixels <= 5e-3 and rare."""
+    o = orc_render["image"]
+    amb = orc_render["ambiguous"]
+    d = np.abs(gpu_img.astype(np.float64) - o).max(axis=0)
+    n_amb = int(amb.sum())
+    ok = d[~amb]
+    worst = float(ok.max()) if ok.size else 0.0
+    worst_amb = float(d[amb].max()) if n_amb else 0.0
+    return dict(worst=worst, worst_amb=worst_amb, n_amb=n_amb, n_pix=int(d.size),
+                n_bad=int((ok > IMG_TOL).sum()))
+
+
+def assert_images(gpu_img, orc_render):
+    r = compare_images(gpu_img, orc_render)
+    assert r["n_bad"] == 0, r
+    assert r["worst_amb"] <= AMB_TOL, r
+    assert r["n_amb"] <= max(AMB_FRAC * r["n_pix"], 2), r
+    return r
+
+
+def compare_grads(g_gpu, g_orc, rel=GRAD_REL, abs_frac=GRAD_ABS_FRAC):
+    """|dg| <= max(rel |g_oracle|, abs_frac max_column |g_oracle|) element-wise."""
+    g_gpu = np.asarray(g_gpu, np.float64).reshape(g_orc.shape)
+    colmax = np.abs(g_orc).max(axis=0, keepdims=True)
+    tol = np.maximum(rel * np.abs(g_orc), abs_frac * colmax)
+    err = np.abs(g_gpu - g_orc)
+    bad = err > tol + 1e-30
+    return dict(n_bad=int(bad.sum()), n=int(bad.size), worst_rel=float((err / (tol + 1e-30)).max()) if err.size else 0.0,
+                where=np.argwhere(bad)[:5].tolist())
+
+
+def oracle_rows(fb, sh_degree):
+    """Oracle gradient rows of the active set in the ABI layout [A, 4*ROW4]."""
+    return oracle.pack_rows(fb["grad"][fb["idx"]], sh_degree)

@@ -1,0 +1,230 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle on the same seeded
+inputs.  Bars (BASELINE north_star): membership, tile masks
+exact; images within 1e-4 outside the ambiguity set; gradients within 1e-3 relative
+(or 1e-5 x column max); Adam within 1e-6 relative; frozen rows bit-identical."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests import gpu_helpers as H
+
+pytestmark = pytest.mark.gpu
+
+SCENES = {
+    "c1": lambda: synth.make_scene("c1"),
+    "c2r": lambda: synth.make_scene("c2", n=20000, width=296, height=232, n_views=2),
+    "c3s": lambda: synth.make_scene("c3", n=150000, n_views=2),
+    "c5s": lambda: synth.make_scene("c5", n=150000, n_views=5),
+}
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def _rand_upstream(scene, seed):
+    rng = np.random.default_rng(seed)
+    return rng.standard_normal((len(scene.cameras), 3, scene.height, scene.width)).astype(np.float32)
+
+
+@pytest.mark.parametrize("name", list(SCENES))
+def test_forward_and_membership(torch_cuda, name):
+    sc = SCENES[name]()
+    g = H.gpu_run(sc)
+    fb = oracle.forward_backward(sc, with_grad=False)
+    assert np.array_equal(g["idx"], fb["idx"]), "active list must be exact"
+    assert g["stats"]["n_active"] == len(fb["idx"])
+    for v, r in enumerate(fb["renders"]):
+        assert np.array_equal(g["tile_mask"][v], r["tile_mask"]), f"tile mask view {v}"
+        H.assert_images(g["images"][v], r)
+    assert g["loss"] == pytest.approx(fb["loss"], rel=2e-5)
+    assert g["launches"] > 0
+
+
+@pytest.mark.parametrize("name", list(SCENES))
+def test_gradients_random_upstream(torch_cuda, name):
+    sc = SCENES[name]()
+    up = _rand_upstream(sc, 99)
+    g = H.gpu_run(sc, dL=up)
+    fb = oracle.forward_backward(sc, dL_dC=up.astype(np.float64))
+    assert np.array_equal(g["idx"], fb["idx"])
+    go = H.oracle_rows(fb, sc.sh_degree)
+    r = H.compare_grads(g["grad"], go)
+    assert r["n_bad"] == 0, r
+
+
+@pytest.mark.parametrize("name", ["c1", "c2r"])
+def test_grad2d_stage_parity(torch_cuda, name):
+    sc = SCENES[name]()
+    up = _rand_upstream(sc, 5)
+    g = H.gpu_run(sc, dL=up)
+    fb = oracle.forward_backward(sc, dL_dC=up.astype(np.float64))
+    idx = fb["idx"]
+    for v, rd in enumerate(fb["renders"]):
+        go = rd["grad2d"][idx]                      # (u, v, a, b, c, o, r, g, b)
+        gg = g["grad2d"][v][:, :9]
+        r = H.compare_grads(gg, go)
+        assert r["n_bad"] == 0, (v, r)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2r"])
+def test_gradients_fused_l1(torch_cuda, name):
+    sc = SCENES[name]()
+    g = H.gpu_run(sc)
+    fb = oracle.forward_backward(sc)
+    go = H.oracle_rows(fb, sc.sh_degree)
+    r = H.compare_grads(g["grad"], go)
+    assert r["n_bad"] == 0, r
+
+
+def test_adam_parity_and_frozen_rows(torch_cuda):
+    torch = torch_cuda
+    sc = SCENES["c2r"]()
+    g = H.gpu_run(sc, step_adam=True)
+    params = g["params"]
+    idx = g["idx"]
+    lr = oracle.lr_row(sc.sh_degree, [1e-3] * 6)
+    F = len(lr)
+    th, m, v = oracle.adam_rows(g["rows_before"].reshape(-1, F), np.zeros((len(idx), F)), np.zeros((len(idx), F)),
+                                g["grad"].reshape(-1, F).astype(np.float64), lr, step=1)
+    valid = ~np.isnan(lr)
+    ga = g["rows_after"].reshape(-1, F)
+    assert np.allclose(ga[:, valid], th[:, valid], rtol=1e-6, atol=1e-9)
+    assert np.allclose(g["m_after"].reshape(-1, F)[:, valid], m[:, valid], rtol=1e-6, atol=1e-30)
+    assert np.allclose(g["v_after"].reshape(-1, F)[:, valid], v[:, valid], rtol=1e-5, atol=1e-38)
+    # pad lanes untouched
+    assert np.array_equal(ga[:, ~valid], g["rows_before"].reshape(-1, F)[:, ~valid])
+    # frozen rows bit-identical, moments stay exactly 0
+    frozen = np.setdiff1d(np.arange(sc.n), idx)
+    base = synth.make_scene("c2", n=20000, width=296, height=232, n_views=2)
+    means, ls, q, op, sh = params.to_numpy()
+    assert np.array_equal(means[frozen], base.means[frozen])
+    assert np.array_equal(ls[frozen], base.log_scales[frozen])
+    assert np.array_equal(q[frozen], base.quats[frozen])
+    assert np.array_equal(op[frozen], base.opacity_logits[frozen])
+    assert np.array_equal(sh[frozen], base.sh[frozen])
+    fr = torch.from_numpy(frozen).cuda()
+    assert torch.count_nonzero(params.m[:, fr]).item() == 0
+    assert torch.count_nonzero(params.v[:, fr]).item() == 0
+
+
+def test_full_step_parity(torch_cuda):
+    """(vii) one full step from the seeded state: images, gradients and parameters."""
+    sc = SCENES["c3s"]()
+    g = H.gpu_run(sc, step_adam=True)
+    fb = oracle.forward_backward(sc)
+    for v, r in enumerate(fb["renders"]):
+        H.assert_images(g["images"][v], r)
+    go = H.oracle_rows(fb, sc.sh_degree)
+    assert H.compare_grads(g["grad"], go)["n_bad"] == 0
+    lr = oracle.lr_row(sc.sh_degree, [1e-3] * 6)
+    F = len(lr)
+    A = len(fb["idx"])
+    th, _, _ = oracle.adam_rows(g["rows_before"].reshape(-1, F), np.zeros((A, F)), np.zeros((A, F)), go, lr, step=1)
+    valid = ~np.isnan(lr)
+    big = np.abs(go) >= 1e-5 * np.abs(go).max(axis=0, keepdims=True)
+    ga = g["rows_after"].reshape(-1, F)
+    sel = big & valid[None, :]
+    assert np.all(np.abs(ga[sel] - th[sel]) <= 1e-6 * np.abs(th[sel]) + 1e-3 * 1e-3)
+    # entries with near-zero gradients may flip sign at step 1: still bounded by 2 lr
+    assert np.all(np.abs(ga[valid[None, :] & ~big] - th[valid[None, :] & ~big]) <= 2e-3 + 1e-6)
+
+
+def test_exactness_masked_equals_full_frame(torch_cuda):
+    """P:201 on the GPU: masked-tile gradients == all-tiles gradients on O^t (fp32 rounding)."""
+    sc = SCENES["c2r"]()
+    up = _rand_upstream(sc, 3)
+    a = H.gpu_run(sc, dL=up)
+    b = H.gpu_run(sc, dL=up, all_tiles=True)
+    assert np.array_equal(a["idx"], b["idx"])
+    ga = a["grad"].reshape(len(a["idx"]), -1).astype(np.float64)
+    gb = b["grad"].reshape(len(b["idx"]), -1).astype(np.float64)
+    r = H.compare_grads(ga, gb, rel=1e-5, abs_frac=1e-6)
+    assert r["n_bad"] == 0, r
+    assert b["stats"]["n_items"] > a["stats"]["n_items"]
+
+
+def test_empty_active_set(torch_cuda):
+    sc = synth.make_scene("c1")
+    sc.regions = [synth.Region(synth.REGION_SPHERE, np.array([50.0, 50, 50], np.float32), np.zeros(3, np.float32), 0.1)]
+    g = H.gpu_run(sc, step_adam=True)
+    assert g["idx"].size == 0 and g["stats"]["n_items"] == 0
+    assert not g["tile_mask"].any()
+    assert np.all(g["images"] == 0.0)
+    assert g["loss"] == 0.0
+
+
+@pytest.mark.parametrize("wh", [(17, 16), (33, 47), (250, 130)])
+def test_ragged_sizes(torch_cuda, wh):
+    W, Hh = wh
+    sc = synth.make_scene("c1", n=1500, width=W, height=Hh)
+    sc.regions[0].r = 0.8
+    up = _rand_upstream(sc, 7)
+    g = H.gpu_run(sc, dL=up)
+    fb = oracle.forward_backward(sc, dL_dC=up.astype(np.float64))
+    assert np.array_equal(g["idx"], fb["idx"])
+    H.assert_images(g["images"][0], fb["renders"][0])
+    assert H.compare_grads(g["grad"], H.oracle_rows(fb, sc.sh_degree))["n_bad"] == 0
+
+
+def test_capacity_overflow_is_reported(torch_cuda):
+    from paper_2506_21117_b200 import default_limits
+    from paper_2506_21117_b200._native import ClsError
+    sc = synth.make_scene("c1")
+    lim = default_limits(sc.n, 1, sc.width, sc.height)
+    lim.max_pairs = 16
+    with pytest.raises(ClsError, match="CAPACITY"):
+        H.gpu_run(sc, limits=lim)
+
+
+def test_invalid_arguments(torch_cuda):
+    import ctypes
+    from paper_2506_21117_b200 import GaussianParams, LocalOptimizer
+    from paper_2506_21117_b200._native import ClsError
+    sc = synth.make_scene("c1")
+    opt = LocalOptimizer(GaussianParams.from_scene(sc), sc.regions, max_views=2, width=128, height=128)
+    with pytest.raises(ClsError, match="STATE"):
+        opt.backward()
+    bad = synth.Camera(sc.cameras[0].R, sc.cameras[0].t, -1.0, 1.0, 64, 64, 128, 128)
+    with pytest.raises(ClsError, match="INVALID_ARGUMENT"):
+        opt.forward([bad])
+    other = synth.Camera(sc.cameras[0].R, sc.cameras[0].t, 100.0, 100.0, 64, 64, 128, 112)
+    with pytest.raises(ClsError, match="DIMENSION_MISMATCH"):
+        opt.forward([sc.cameras[0], other])
+    opt.regions = [synth.Region(synth.REGION_SPHERE, np.zeros(3, np.float32), np.zeros(3, np.float32), -1.0)]
+    from paper_2506_21117_b200.step import region_structs
+    opt._reg = region_structs(opt.regions)
+    with pytest.raises(ClsError, match="INVALID_ARGUMENT"):
+        opt.forward([sc.cameras[0]])
+
+
+def test_deterministic_forward(torch_cuda):
+    sc = SCENES["c2r"]()
+    a = H.gpu_run(sc)
+    b = H.gpu_run(sc)
+    assert np.array_equal(a["images"], b["images"])
+    assert a["loss"] == b["loss"]
+
+
+@pytest.mark.slow
+def test_full_size_c4_sampled_views(torch_cuda):
+    """BASELINE config c4 at full size (3M Gaussians, 1920x1080), in the bench's launch
+    configuration, on 2 of its 32 views: membership of all 3M exact, images and gradients."""
+    sc = synth.make_scene("c4")
+    views = [0, 1]
+    sub = synth.Scene(sc.name, sc.means, sc.log_scales, sc.quats, sc.opacity_logits, sc.sh, sc.sh_degree,
+                      [sc.cameras[v] for v in views], sc.regions, sc.targets[views])
+    up = _rand_upstream(sub, 11)
+    g = H.gpu_run(sub, dL=up)
+    fb = oracle.forward_backward(sub, dL_dC=up.astype(np.float64))
+    assert np.array_equal(g["idx"], fb["idx"])
+    for v, r in enumerate(fb["renders"]):
+        assert np.array_equal(g["tile_mask"][v], r["tile_mask"])
+        H.assert_images(g["images"][v], r)
+    r = H.compare_grads(g["grad"], H.oracle_rows(fb, sub.sh_degree))
+    assert r["n_bad"] == 0, r
