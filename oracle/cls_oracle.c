@@ -334,7 +334,11 @@ static inline int in_rect(const int32_t *rc, int tx, int ty)
  * non-culled Gaussians (support rule applied per pixel); literal = 0 builds per-tile
  * candidate lists by brute force.  Both evaluate the same operations in the same order.
  * all_tiles = 1 makes every tile active (full-frame 3DGS step, "w/o Kernel").
- * ambiguous[p] = 1 if along p's path some |255 alpha - 1| < delta or |1e4 T' - 1| < delta.
+ * ambiguous[p] = 1 if a discrete decision along p's path lies within the fp32 error bound of
+ * its threshold: with eps = delta the relative error bound of an
+ * fp32 alpha, a skip is ambiguous if |255 alpha - 1| < eps + 1e-7, and a termination test is
+ * ambiguous if |1e4 T' - 1| < E + eps alpha/(1 - alpha) + 1e-7, where E = sum over the already
+ * composited Gaussians of (eps alpha/(1 - alpha) + 1.2e-7) bounds the relative error of fp32 T.
  * sig[p] (optional) = FNV hash of p's composited index sequence (discrete state of the pixel).
  * Returns the number of active tiles.
  */
@@ -435,6 +439,7 @@ int orc_render_view(int64_t n, const int32_t *culled, const double *uv, const do
                     double T = 1.0, C[3] = {0.0, 0.0, 0.0};
                     int64_t K = 0;
                     int amb = 0;
+                    double Erel = 0.0;   /* relative error bound of an fp32 T (ambiguity only) */
                     int64_t len = literal ? nv : tile_start[tile + 1] - tile_start[tile];
                     for (int64_t s = 0; s < len; s++) {
                         int64_t i = literal ? order[s].idx : tile_list[tile_start[tile] + s];
@@ -446,11 +451,13 @@ int orc_render_view(int64_t n, const int32_t *culled, const double *uv, const do
                         double G = exp(p);
                         double a = opac[i] * G;
                         if (a > 0.99) a = 0.99;
-                        if (fabs(255.0 * a - 1.0) < delta) amb = 1;
+                        if (fabs(255.0 * a - 1.0) < delta + 1e-7) amb = 1;
                         if (a < 1.0 / 255.0) continue;
                         double Tn = T * (1.0 - a);
-                        if (fabs(1e4 * Tn - 1.0) < delta) amb = 1;
+                        double ea = delta * a / (1.0 - a);
+                        if (fabs(1e4 * Tn - 1.0) < Erel + ea + 1e-7) amb = 1;
                         if (Tn < 1e-4) break;
+                        Erel += ea + 1.2e-7;
                         for (int ch = 0; ch < 3; ch++) C[ch] += a * T * rgb[3 * i + ch];
                         if (K == cap) {
                             cap *= 2;

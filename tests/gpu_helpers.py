@@ -8,7 +8,7 @@ import numpy as np
 import oracle
 
 IMG_TOL = 1e-4          # north_star: images within 1e-4 absolute per channel
-AMB_TOL = 5e-3          # ambiguous pixels: at most one threshold flip
+AMB_TOL = 1.1e-2        # ambiguous pixels: one threshold flip, <= max(1/255, 1e-4/(1-0.99))
 AMB_FRAC = 1e-3         # at most this fraction of compared pixels may be ambiguous
 GRAD_REL = 1e-3         # north_star: gradients within 1e-3 relative ...
 GRAD_ABS_FRAC = 1e-5    # ... or 1e-5 x max|g| of the column (absolute floor)
