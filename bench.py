@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""Benchmark of the CL-Splats local-optimisation step (fwd + bwd + masked Adam) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+
+One step = one pass of the whole hot path (membership, tile mask, projection, binning,
+masked compositing + fused L1, masked backward, [NCCL all-reduce of the active gradient
+rows when N > 1], masked Adam) over all views of the config.  N > 1: run under
+torch.distributed.run, one rank per GPU; the views are sharded over the ranks (weak in the
+Gaussians, strong in the views: the total work per step is fixed).
+
+Prints ONE JSON line (rank 0).  `value` = steps/s of the whole job, timed with CUDA events
+on the launching stream over exactly K steps bracketed by barrier + synchronize, max over
+ranks.  The roofline of the dominant kernel uses the library's own CUDA-event timing of
+each kernel group over the same timed region.  `--impl reference` times the CPU oracle
+(oracle/, fp64) on a bounded sample of the same workload on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+# algorithmic FP32 FLOPs per (pixel, list entry) evaluation:
+#   forward: LDL^T exponent 10, alpha 2, tests 2, transmittance 2, (composite 7 when composited)
+#   backward walk: exponent 10, alpha 2, tests 2, T division 2, colour-behind 7
+FWD_FLOPS_PER_EVAL = 16.0
+BWD_FLOPS_PER_EVAL = 23.0
+SM_COUNT, FP32_LANES = 148, 128
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[0]) for r in self.rows if num(r[0])]
+        mx = [num(r[1]) for r in self.rows if num(r[1])]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if "Active" in r[4 + k]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def limits_for(cfg: str, n: int, n_views: int, W: int, H: int, all_tiles: bool):
+    from paper_2506_21117_b200 import default_limits
+    TX, TY = -(-W // 16), -(-H // 16)
+    rec = n // 2 if not all_tiles else n
+    pairs = min(TX * TY * 2048, 8_000_000 if not all_tiles else 24_000_000)
+    pairs = min(pairs, (2**31 - 2) // max(n_views, 1))
+    return default_limits(n, n_views, W, H, records_per_view=min(rec, (2**31 - 1) // max(n_views, 1)),
+                          pairs_per_view=pairs, max_active=min(n, 400_000))
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_21117_b200 import GaussianParams, LocalOptimizer
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    sc = synth.make_scene(args.config)
+    V = len(sc.cameras)
+    shards = np.array_split(np.arange(V), world)
+    my_views = [int(v) for v in shards[rank]]
+    cams = [sc.cameras[v] for v in my_views]
+    W, H = sc.width, sc.height
+    params = GaussianParams.from_scene(sc, device=f"cuda:{local}")
+    lim = limits_for(args.config, sc.n, len(cams), W, H, args.all_tiles)
+    opt = LocalOptimizer(params, sc.regions, limits=lim)
+    tg_host = torch.from_numpy(np.ascontiguousarray(sc.targets[my_views])).pin_memory()
+    tg = tg_host.to(f"cuda:{local}")
+    stream = torch.cuda.current_stream()
+
+    def allreduce(grad, loss):
+        if world > 1:
+            flat = torch.cat([grad.reshape(-1), loss])
+            dist.all_reduce(flat)
+            grad.copy_(flat[:-1].view_as(grad))
+            loss.copy_(flat[-1:])
+
+    def step():
+        res = opt.forward(cams, tg, n_views_total=V, all_tiles=args.all_tiles)
+        grad = opt.backward()
+        allreduce(grad, res.loss)
+        opt.adam(grad)
+        return res.loss
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    st0 = opt.stats()
+    # ---------------- timed region (device) ----------------
+    opt.profile(True)
+    opt.profile_read()
+    launches0 = opt.launch_count()
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            loss = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms_total = e0.elapsed_time(e1)
+    launches = opt.launch_count() - launches0
+    prof = opt.profile_read()
+    opt.profile(False)
+    stats = opt.stats()
+    t = torch.tensor([ms_total], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    value = 1000.0 / ms_step
+
+    # ---------------- end to end through the public API, host buffers ----------------
+    e2e = None
+    if not args.no_e2e:
+        loss_host = torch.empty(1, dtype=torch.float32).pin_memory()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        w0 = time.perf_counter()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            tg.copy_(tg_host, non_blocking=True)             # this step's inputs: the views' target images
+            loss = step()
+            loss_host.copy_(loss, non_blocking=True)         # the step's result
+        f1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+        te = torch.tensor([f0.elapsed_time(f1), wall * 1e3], dtype=torch.float64, device=f"cuda:{local}")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": 1000.0 * args.steps / float(te[1].item()), "unit": "steps/s",
+               "h2d_bytes_per_step": int(tg_host.numel() * 4) * world, "d2h_bytes_per_step": 4 * world,
+               "device_ms_per_step": float(te[0].item()) / args.steps}
+
+    out = None
+    if rank == 0:
+        peaks = _peaks()
+        hbm = peaks.get("hbm_gbs", 6650.0)
+        clocks = clk.summary()
+        per = {k: v for k, v in prof.items() if v["calls"]}
+        dom = max(per, key=lambda k: per[k]["ms"]) if per else None
+        step_ms_sum = sum(v["ms"] for v in per.values())
+        # algorithmic work of the dominant kernel per launch
+        roof = None
+        if dom in ("bwd_raster", "fwd_raster"):
+            evals = stats["n_bwd_evals"] if dom == "bwd_raster" else stats["n_fwd_evals"]
+            flops = evals * (BWD_FLOPS_PER_EVAL if dom == "bwd_raster" else FWD_FLOPS_PER_EVAL)
+            avg_ms = per[dom]["ms"] / per[dom]["calls"]
+            ach = flops / (avg_ms * 1e-3) / 1e12
+            sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+            peak = SM_COUNT * FP32_LANES * 2 * sm_mhz * 1e6 / 1e12
+            roof = {"kernel": dom, "bound": "alu", "achieved": round(ach, 3), "peak": round(peak, 2),
+                    "unit": "TFLOP/s", "frac": round(ach / peak, 4), "traffic": None,
+                    "peak_source": f"FP32 FMA lanes 148x128x2 at sm_max {sm_mhz:.0f} MHz (MEASURED_PEAKS.json)",
+                    "units_per_launch": int(evals), "unit_name": "(pixel, entry) evaluations",
+                    "share_of_step": round(per[dom]["ms"] / max(step_ms_sum, 1e-9), 3)}
+        elif dom is not None:
+            roof = {"kernel": dom, "bound": "hbm", "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None,
+                    "traffic": None}
+        out = {
+            "metric": "local-opt steps/s (fwd+bwd+masked Adam)",
+            "value": round(value, 4), "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "impl": "ours",
+            "config": {"workload": args.config, "gaussians": sc.n, "views": V, "width": W, "height": H,
+                       "sh_degree": sc.sh_degree, "active": int(stats["n_active"]),
+                       "mode": "all-tiles (w/o kernel)" if args.all_tiles else "masked (local kernel)",
+                       "parallelism": f"views/dp{world}", "l2": "inputs larger than L2 (params+moments "
+                       f"{sc.n * (12 + 3 * 4 * 4) * 4 * 3 / 1e9:.2f} GB)"},
+            "mpix_per_s": {"rendered": round(sum(stats["n_active_tiles"]) * 256 * world * value / 1e6, 2),
+                           "frame_equivalent": round(V * W * H * value / 1e6, 2)},
+            "e2e": e2e, "gpu_launches": int(launches), "roofline": roof, "clocks": clocks,
+            "kernels_ms_per_step": {k: round(v["ms"] / args.steps, 4) for k, v in per.items()},
+            "counts": {k: stats[k] for k in ("n_records", "n_pairs", "n_items", "max_list", "n_huge_tiles",
+                                             "n_fwd_evals", "n_bwd_evals")},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(sc, args.cpu_views)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    opt.close()
+    return out
+
+
+def cpu_baseline(sc, n_views):
+    """The oracle (as it stands) on a bounded sample: the first `n_views` views of the workload
+    (all Gaussians projected, fwd + bwd over their active tiles) plus the masked Adam of the
+    active rows, timed on the host cores and scaled to the whole step (x V / n_views)."""
+    import oracle
+    sub = synth.Scene(sc.name, sc.means, sc.log_scales, sc.quats, sc.opacity_logits, sc.sh, sc.sh_degree,
+                      sc.cameras[:n_views], sc.regions, sc.targets[:n_views])
+    t0 = time.perf_counter()
+    fb = oracle.forward_backward(sub, n_views_total=len(sc.cameras))
+    rows = oracle.pack_rows(fb["grad"][fb["idx"]], sc.sh_degree)
+    lr = oracle.lr_row(sc.sh_degree, [1e-3] * 6)
+    oracle.adam_rows(np.zeros_like(rows), np.zeros_like(rows), np.zeros_like(rows), rows, lr, step=1)
+    dt = time.perf_counter() - t0
+    V = len(sc.cameras)
+    step_s = dt * V / n_views
+    return {"value": round(1.0 / step_s, 6), "unit": "steps/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{n_views} of {V} views ({sc.n} Gaussians projected, fwd+bwd over active tiles) + masked "
+                      f"Adam; {dt:.2f} s measured, scaled x{V / n_views:g} to one step"}
+
+
+def run_reference(args):
+    """Reference arm = the CPU oracle as it stands, on this arm's config and metric."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return None
+    import oracle
+    sc = synth.make_scene(args.config)
+    V = len(sc.cameras)
+    sub = synth.Scene(sc.name, sc.means, sc.log_scales, sc.quats, sc.opacity_logits, sc.sh, sc.sh_degree,
+                      sc.cameras[:1], sc.regions, sc.targets[:1])
+    times = []
+    for k in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        fb = oracle.forward_backward(sub, n_views_total=V)
+        rows = oracle.pack_rows(fb["grad"][fb["idx"]], sc.sh_degree)
+        lr = oracle.lr_row(sc.sh_degree, [1e-3] * 6)
+        oracle.adam_rows(np.zeros_like(rows), np.zeros_like(rows), np.zeros_like(rows), rows, lr, step=1)
+        if k >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    step_s = statistics.mean(times) * V          # one sampled view per step, scaled to all V views
+    value = 1.0 / step_s
+    sample = f"1 of {V} views per step (fwd+bwd+Adam, fp64 oracle), scaled x{V}"
+    return {"metric": "local-opt steps/s (fwd+bwd+masked Adam)", "value": round(value, 6), "unit": "steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 2),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": args.config, "gaussians": sc.n, "views": V, "width": sc.width,
+                       "height": sc.height},
+            "cpu_baseline": {"value": round(value, 6), "unit": "steps/s", "cores": oracle.num_threads(),
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": round(value, 6), "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c4", choices=synth.CONFIG_NAMES)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--all-tiles", action="store_true", help="full-frame step (P:347 'w/o Kernel')")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-views", type=int, default=1)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    out = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -105,7 +105,19 @@ typedef struct {
     int32_t n_views;
     int64_t max_list;          /* longest per-tile list */
     int64_t n_huge_tiles;      /* tiles sorted by the global-memory fallback */
+    int64_t n_fwd_evals;       /* (pixel, list entry) evaluations of the forward compositing */
+    int64_t n_bwd_evals;       /* (pixel, list entry) evaluations of the backward walk (after its bwd) */
 } cls_stats_t;
+
+#define CLS_PROF_GROUPS 16
+/* Per-kernel-group device time accumulated while profiling is enabled (CUDA events recorded
+ * on the launching stream around each group of launches). */
+typedef struct {
+    int32_t n;                         /* groups used */
+    char name[CLS_PROF_GROUPS][24];
+    double ms[CLS_PROF_GROUPS];        /* total milliseconds since the last read */
+    int64_t calls[CLS_PROF_GROUPS];    /* number of timed calls of the group */
+} cls_profile_t;
 
 /* Create a context on `device` with the given capacities (host struct).
  * Allocates all scratch; returns CLS_ERR_OUT_OF_MEMORY if that fails. Synchronous. */
@@ -178,6 +190,11 @@ cls_status cls_adam_masked(cls_ctx *ctx, float *mean_op, float *quat, float *log
 /* Counters of the last fwd (host struct out).  Synchronises the ctx's last stream.
  * Returns CLS_ERR_CAPACITY if a capacity overflowed during that fwd. */
 cls_status cls_stats(cls_ctx *ctx, cls_stats_t *out);
+
+/* Enable/disable per-kernel-group event timing (adds two event records per group). */
+cls_status cls_profile_enable(cls_ctx *ctx, int32_t on);
+/* Synchronise the pending timing events, return the accumulated times and reset them. */
+cls_status cls_profile_read(cls_ctx *ctx, cls_profile_t *out);
 
 /* Optional: after cls_render_fwd, copy the per-(view, active Gaussian) 2D gradients
  * of the last bwd -- float[n_views][A][12] (u, v, conic a, b, c, opacity, r, g, b, 0, 0, 0) --

@@ -20,7 +20,9 @@ STATUS = {0: "CLS_OK", 1: "CLS_ERR_INVALID_ARGUMENT", 2: "CLS_ERR_DIMENSION_MISM
 
 # symbols declared in include/cls.h (checked by tests/test_abi.py)
 EXPORTS = ("cls_create", "cls_destroy", "cls_render_fwd", "cls_active", "cls_copy_active", "cls_render_bwd", "cls_adam_masked",
-           "cls_stats", "cls_debug_grad2d", "cls_status_string", "cls_last_error", "cls_launch_count")
+           "cls_stats", "cls_profile_enable", "cls_profile_read", "cls_debug_grad2d", "cls_status_string",
+           "cls_last_error", "cls_launch_count")
+CLS_PROF_GROUPS = 16
 
 
 class ClsError(RuntimeError):
@@ -54,12 +56,21 @@ class cls_stats_t(ctypes.Structure):
     _fields_ = [("n_active", ctypes.c_int64), ("n_records", ctypes.c_int64), ("n_pairs", ctypes.c_int64),
                 ("n_items", ctypes.c_int64), ("n_active_tiles", ctypes.c_int64 * CLS_MAX_VIEWS),
                 ("overflow", ctypes.c_int32), ("n_views", ctypes.c_int32), ("max_list", ctypes.c_int64),
-                ("n_huge_tiles", ctypes.c_int64)]
+                ("n_huge_tiles", ctypes.c_int64), ("n_fwd_evals", ctypes.c_int64), ("n_bwd_evals", ctypes.c_int64)]
 
     def as_dict(self):
         return dict(n_active=self.n_active, n_records=self.n_records, n_pairs=self.n_pairs, n_items=self.n_items,
                     n_active_tiles=list(self.n_active_tiles[: self.n_views]), overflow=self.overflow,
-                    max_list=self.max_list, n_huge_tiles=self.n_huge_tiles)
+                    max_list=self.max_list, n_huge_tiles=self.n_huge_tiles, n_fwd_evals=self.n_fwd_evals,
+                    n_bwd_evals=self.n_bwd_evals)
+
+
+class cls_profile_t(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("name", (ctypes.c_char * 24) * 16), ("ms", ctypes.c_double * 16),
+                ("calls", ctypes.c_int64 * 16)]
+
+    def as_dict(self):
+        return {self.name[i].value.decode(): dict(ms=self.ms[i], calls=self.calls[i]) for i in range(self.n)}
 
 
 def _load():
@@ -79,6 +90,8 @@ def _load():
                                   ctypes.c_float, ctypes.c_int32, V]
     L.cls_stats.argtypes = [V, P(cls_stats_t)]
     L.cls_debug_grad2d.argtypes = [V, V, V]
+    L.cls_profile_enable.argtypes = [V, ctypes.c_int32]
+    L.cls_profile_read.argtypes = [V, P(cls_profile_t)]
     L.cls_status_string.argtypes = [ctypes.c_int]
     L.cls_status_string.restype = ctypes.c_char_p
     L.cls_last_error.argtypes = [V]
@@ -86,7 +99,7 @@ def _load():
     L.cls_launch_count.argtypes = [V]
     L.cls_launch_count.restype = ctypes.c_int64
     for name in ("cls_create", "cls_destroy", "cls_render_fwd", "cls_active", "cls_copy_active", "cls_render_bwd", "cls_adam_masked",
-                 "cls_stats", "cls_debug_grad2d"):
+                 "cls_stats", "cls_debug_grad2d", "cls_profile_enable", "cls_profile_read"):
         getattr(L, name).restype = ctypes.c_int
     return L
 

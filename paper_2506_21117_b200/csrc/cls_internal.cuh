@@ -49,6 +49,8 @@ struct Counters {
     int overflow;           // bit0 records, bit1 pairs
     int max_list;
     int active_tiles[CLS_MAX_VIEWS];
+    unsigned long long fwd_evals;   // (pixel, list entry) evaluations of the forward
+    unsigned long long bwd_evals;   // (pixel, list entry) evaluations of the backward walk
 };
 
 // all scratch of a ctx (device pointers), passed by value to kernels
@@ -63,8 +65,9 @@ struct Scratch {
     int *diff;              // [V][(TY+1)(TX+1)]  corner differences of record rects
     // records
     float4 *rec_xy;         // (u_hi, u_lo, v_hi, v_lo)
-    float4 *rec_co;         // (conic a, b, c, opacity)
-    float4 *rec_rgb;        // (r, g, b, active ordinal as int bits)
+    float4 *rec_co;         // (+-a_p [sign: pivot y], beta_hi, gamma, opacity)  LDL^T conic, see power_ldl
+    float4 *rec_rgb;        // (r, g, b, beta_lo)
+    int *rec_ord;           // active ordinal or -1
     int2 *rec_rect;         // (x0 | y0 << 16, x1 | y1 << 16)
     int2 *rec_meta;         // (gid, view | active << 31)
     unsigned *rec_depth;    // fp32 bits of the depth key
@@ -219,16 +222,24 @@ __device__ __forceinline__ int sat_count(const int *S, int TXp1, int x0, int y0,
 }
 
 // ---------------------------------------------------------------------------
-// per-pixel alpha of one staged Gaussian.  Forward and backward MUST take the same
-// discrete decisions, so the op sequence is pinned with _rn intrinsics (no contraction).
-// dx, dy = (u - x, v - y) in tile-local fp32 coordinates.
+// Per-pixel exponent of one staged Gaussian, in a cancellation-free form.
+// The conic form a dx^2 + 2 b dx dy + c dy^2 (3DGS: p = -(a dx^2 + c dy^2)/2 - b dx dy) loses
+// all precision in fp32 for large, elongated splats (terms ~1e4 px^2, result ~5).  With the
+// pivot on the larger diagonal entry (a >= c: pivot x) it is written as an LDL^T sum of two
+// non-negative terms:  a dx^2 + 2 b dx dy + c dy^2 = a_p s^2 + gamma t^2,
+//   pivot x: s = dx + beta dy, t = dy, a_p = a, beta = b/a (|beta| <= 1), gamma = 1/Sigma'_yy
+//   pivot y: s = dy + beta dx, t = dx, a_p = c, beta = b/c,            gamma = 1/Sigma'_xx
+// s0, t0 (the tile-origin values) are formed in fp64 at staging; per pixel only the small
+// offsets (|px + beta py| <= 30) are subtracted in fp32.  Forward and backward call this
+// same function, with _rn intrinsics, so they take identical discrete decisions.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ float power_of(float ca, float cb, float cc, float dx, float dy)
+__device__ __forceinline__ float power_ldl(float s0, float t0, float beta, float ap, float gam, float px, float py,
+                                           float &s, float &t)
 {
-    const float qa = __fmul_rn(ca, __fmul_rn(dx, dx));
-    const float qc = __fmul_rn(cc, __fmul_rn(dy, dy));
-    const float qb = __fmul_rn(cb, __fmul_rn(dx, dy));
-    return __fsub_rn(__fmul_rn(-0.5f, __fadd_rn(qa, qc)), qb);
+    s = __fsub_rn(s0, __fmaf_rn(beta, py, px));
+    t = __fsub_rn(t0, py);
+    const float q = __fmaf_rn(ap, __fmul_rn(s, s), __fmul_rn(gam, __fmul_rn(t, t)));
+    return __fmul_rn(-0.5f, q);
 }
 
 // SH basis (3DGS order and signs, R15), fp32

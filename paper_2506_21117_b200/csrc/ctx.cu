@@ -9,6 +9,7 @@
 
 #include <new>
 #include <string>
+#include <vector>
 
 #include "kernels.h"
 
@@ -29,7 +30,47 @@ struct cls_ctx {
     cudaStream_t last_stream = nullptr;
     int64_t launches0 = 0;
     std::string err;
+    // profiling: CUDA events around each kernel group, on the launching stream
+    bool prof_on = false;
+    struct ProfRec { int id; cudaEvent_t a, b; };
+    std::vector<ProfRec> prof_pending;
+    std::vector<cudaEvent_t> ev_pool;
+    double prof_ms[CLS_PROF_GROUPS] = {};
+    int64_t prof_n[CLS_PROF_GROUPS] = {};
 };
+
+static const char *PROF_NAMES[] = {"member", "active_mask", "project", "bin_count", "emit", "sort",
+                                   "fwd_raster", "fill_bg", "loss", "zero_grad2d", "bwd_raster", "bwd_project",
+                                   "adam"};
+enum { P_MEMBER, P_MASK, P_PROJECT, P_BINCOUNT, P_EMIT, P_SORT, P_FWD, P_FILL, P_LOSS, P_ZERO, P_BWD_RASTER,
+       P_BWD_PROJECT, P_ADAM, P_COUNT };
+static_assert(P_COUNT <= CLS_PROF_GROUPS, "profile groups");
+
+static cudaEvent_t prof_event(cls_ctx *c)
+{
+    if (!c->ev_pool.empty()) {
+        cudaEvent_t e = c->ev_pool.back();
+        c->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+template <typename F>
+static void run(cls_ctx *c, int id, cudaStream_t st, F &&f)
+{
+    if (!c->prof_on) {
+        f();
+        return;
+    }
+    cudaEvent_t a = prof_event(c), b = prof_event(c);
+    cudaEventRecord(a, st);
+    f();
+    cudaEventRecord(b, st);
+    c->prof_pending.push_back({id, a, b});
+}
 
 namespace {
 
@@ -89,7 +130,7 @@ cls_status cls_destroy(cls_ctx *c)
     if (!c) return CLS_ERR_INVALID_ARGUMENT;
     cudaSetDevice(c->device);
     void *ptrs[] = {c->s.idx, c->s.ord, c->s.st_member, c->s.mask, c->s.sat, c->s.diff, c->s.rec_xy, c->s.rec_co,
-                    c->s.rec_rgb, c->s.rec_rect, c->s.rec_meta, c->s.rec_depth, c->s.tile_cnt, c->s.tile_off,
+                    c->s.rec_rgb, c->s.rec_ord, c->s.rec_rect, c->s.rec_meta, c->s.rec_depth, c->s.tile_cnt, c->s.tile_off,
                     c->s.tile_cursor, c->s.st_tiles, c->s.items, c->s.item_of_tile, c->s.cls_small, c->s.cls_large,
                     c->s.cls_huge, c->s.first_active, c->s.pair_key, c->s.pair_val, c->s.sort_tmp_key,
                     c->s.sort_tmp_val, c->s.px_T, c->s.px_last, c->s.px_dl, c->s.item_loss, c->s.grad2d, c->s.cnt};
@@ -99,6 +140,8 @@ cls_status cls_destroy(cls_ctx *c)
     if (c->h_A) cudaFreeHost(c->h_A);
     if (c->ev_member) cudaEventDestroy(c->ev_member);
     if (c->ev_fwd) cudaEventDestroy(c->ev_fwd);
+    for (auto &r : c->prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
     delete c;
     return CLS_OK;
 }
@@ -126,7 +169,7 @@ cls_status cls_create(cls_ctx **out, int device, const cls_limits *lim)
     Scratch &s = c->s;
     bool ok = dalloc(&s.idx, N) && dalloc(&s.ord, N) && dalloc(&s.st_member, N / 2048 + 2) && dalloc(&s.mask, VT) &&
               dalloc(&s.sat, SAT) && dalloc(&s.diff, SAT) && dalloc(&s.rec_xy, R) && dalloc(&s.rec_co, R) &&
-              dalloc(&s.rec_rgb, R) && dalloc(&s.rec_rect, R) && dalloc(&s.rec_meta, R) && dalloc(&s.rec_depth, R) &&
+              dalloc(&s.rec_rgb, R) && dalloc(&s.rec_ord, R) && dalloc(&s.rec_rect, R) && dalloc(&s.rec_meta, R) && dalloc(&s.rec_depth, R) &&
               dalloc(&s.tile_cnt, VT) && dalloc(&s.tile_off, VT) && dalloc(&s.tile_cursor, VT) &&
               dalloc(&s.st_tiles, VT / 2048 + 2) && dalloc(&s.items, VT) && dalloc(&s.item_of_tile, VT) &&
               dalloc(&s.cls_small, VT) && dalloc(&s.cls_large, VT) && dalloc(&s.cls_huge, VT) &&
@@ -232,15 +275,17 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     s.max_items = d.V * d.T;
 
     cudaMemsetAsync(s.cnt, 0, sizeof(Counters), st);
-    launch_member(p, d, regs, s, st);
+    run(c, P_MEMBER, st, [&] { launch_member(p, d, regs, s, st); });
     cudaMemcpyAsync(c->h_A, &s.cnt->A, sizeof(int), cudaMemcpyDeviceToHost, st);
     cudaEventRecord(c->ev_member, st);
-    launch_active_mask(p, d, cs, s, st);
-    launch_project(p, d, cs, s, st);
-    launch_bin(d, cs, s, st);
-    launch_fwd(d, cs, s, targets, images, loss_scale, bgc, st);
-    if (images) launch_fill_bg(d, s, images, bgc, st);
-    if (targets && loss) launch_loss(s, loss_scale, loss, st);
+    run(c, P_MASK, st, [&] { launch_active_mask(p, d, cs, s, st); });
+    run(c, P_PROJECT, st, [&] { launch_project(p, d, cs, s, st); });
+    run(c, P_BINCOUNT, st, [&] { launch_bin_count(d, cs, s, st); });
+    run(c, P_EMIT, st, [&] { launch_emit(d, cs, s, st); });
+    run(c, P_SORT, st, [&] { launch_sort(d, s, st); });
+    run(c, P_FWD, st, [&] { launch_fwd(d, cs, s, targets, images, loss_scale, bgc, st); });
+    if (images) run(c, P_FILL, st, [&] { launch_fill_bg(d, s, images, bgc, st); });
+    if (targets && loss) run(c, P_LOSS, st, [&] { launch_loss(s, loss_scale, loss, st); });
     if (tile_mask) cudaMemcpyAsync(tile_mask, s.mask, (size_t)d.V * d.T, cudaMemcpyDeviceToDevice, st);
     cudaMemcpyAsync(c->h_cnt, s.cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st);
     cudaEventRecord(c->ev_fwd, st);
@@ -279,18 +324,6 @@ cls_status cls_copy_active(cls_ctx *c, int32_t *dst, void *stream)
     return check_cuda(c, "cls_copy_active");
 }
 
-__global__ void k_zero_grad2d(Scratch s, int V, long long cap)
-{
-    const long long A = s.cnt->A;
-    if (A > cap) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&s.cnt->overflow, 4);
-        return;
-    }
-    const long long total = (long long)V * A * 3;
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x)
-        s.grad2d[e] = make_float4(0.f, 0.f, 0.f, 0.f);
-}
-
 cls_status cls_render_bwd(cls_ctx *c, const cls_gaussians *g, const float *dL_dimages, float *grad_active,
                           void *stream)
 {
@@ -307,10 +340,9 @@ cls_status cls_render_bwd(cls_ctx *c, const cls_gaussians *g, const float *dL_di
     Params p{reinterpret_cast<const float4 *>(g->mean_op), reinterpret_cast<const float4 *>(g->quat),
              reinterpret_cast<const float4 *>(g->log_scale), reinterpret_cast<const float4 *>(g->sh)};
     Scratch s = c->s;
-    k_zero_grad2d<<<148 * 4, 256, 0, st>>>(s, c->dims.V, (long long)c->lim.max_active);
-    g_launches++;
-    launch_bwd_raster(c->dims, s, dL_dimages, c->bg, st);
-    launch_bwd_project(p, c->dims, c->cams, s, grad_active, st);
+    run(c, P_ZERO, st, [&] { launch_zero_grad2d(c->dims, s, (long long)c->lim.max_active, st); });
+    run(c, P_BWD_RASTER, st, [&] { launch_bwd_raster(c->dims, s, dL_dimages, c->bg, st); });
+    run(c, P_BWD_PROJECT, st, [&] { launch_bwd_project(p, c->dims, c->cams, s, grad_active, st); });
     cls_status e = check_cuda(c, "cls_render_bwd");
     if (e != CLS_OK) return e;
     c->bwd_valid = true;
@@ -335,8 +367,10 @@ cls_status cls_adam_masked(cls_ctx *c, float *mean_op, float *quat, float *log_s
     cudaStream_t st = (cudaStream_t)stream;
     const float bc1 = (float)(1.0 - pow((double)beta1, (double)step));
     const float bc2 = (float)(1.0 - pow((double)beta2, (double)step));
-    launch_adam(c->dims, c->s, (float4 *)mean_op, (float4 *)quat, (float4 *)log_scale, (float4 *)sh, (float4 *)m,
-                (float4 *)v, (const float4 *)grad_active, lr, beta1, beta2, eps, bc1, bc2, st);
+    run(c, P_ADAM, st, [&] {
+        launch_adam(c->dims, c->s, (float4 *)mean_op, (float4 *)quat, (float4 *)log_scale, (float4 *)sh, (float4 *)m,
+                    (float4 *)v, (const float4 *)grad_active, lr, beta1, beta2, eps, bc1, bc2, st);
+    });
     c->last_stream = st;
     return check_cuda(c, "cls_adam_masked");
 }
@@ -362,11 +396,47 @@ cls_status cls_stats(cls_ctx *c, cls_stats_t *out)
     out->overflow = h.overflow | ovf;
     out->max_list = h.max_list;
     out->n_huge_tiles = h.n_huge;
+    out->n_fwd_evals = (int64_t)h.fwd_evals;
+    unsigned long long bev = 0;
+    cudaMemcpy(&bev, &c->s.cnt->bwd_evals, sizeof bev, cudaMemcpyDeviceToHost);
+    out->n_bwd_evals = (int64_t)bev;
     if (out->overflow)
         return fail(c, CLS_ERR_CAPACITY, "capacity overflow (bits %d): records %d/%lld pairs %llu/%lld A %d/%lld",
                     out->overflow, h.n_records, (long long)c->lim.max_records, h.n_pairs,
                     (long long)c->lim.max_pairs, h.A, (long long)c->lim.max_active);
     return check_cuda(c, "cls_stats");
+}
+
+cls_status cls_profile_enable(cls_ctx *c, int32_t on)
+{
+    if (!c) return CLS_ERR_INVALID_ARGUMENT;
+    c->prof_on = on != 0;
+    return CLS_OK;
+}
+
+cls_status cls_profile_read(cls_ctx *c, cls_profile_t *out)
+{
+    if (!c || !out) return CLS_ERR_INVALID_ARGUMENT;
+    for (auto &r : c->prof_pending) {
+        if (cudaEventSynchronize(r.b) != cudaSuccess) return fail(c, CLS_ERR_CUDA, "profile event");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        c->prof_ms[r.id] += ms;
+        c->prof_n[r.id] += 1;
+        c->ev_pool.push_back(r.a);
+        c->ev_pool.push_back(r.b);
+    }
+    c->prof_pending.clear();
+    memset(out, 0, sizeof *out);
+    out->n = P_COUNT;
+    for (int i = 0; i < P_COUNT; i++) {
+        snprintf(out->name[i], sizeof out->name[i], "%s", PROF_NAMES[i]);
+        out->ms[i] = c->prof_ms[i];
+        out->calls[i] = c->prof_n[i];
+        c->prof_ms[i] = 0.0;
+        c->prof_n[i] = 0;
+    }
+    return check_cuda(c, "cls_profile_read");
 }
 
 cls_status cls_debug_grad2d(cls_ctx *c, float *out, void *stream)

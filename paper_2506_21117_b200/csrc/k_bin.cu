@@ -279,7 +279,24 @@ __global__ void __launch_bounds__(1024) k_sort_huge(Scratch s)
     }
 }
 
-void launch_bin(const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st)
+void launch_bin_count(const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st)
+{
+    const int total = d.V * d.T;
+    k_tile_counts<<<d.V, 256, 0, st>>>(cams, s);
+    const int blocks = (total + TSCAN_TILE - 1) / TSCAN_TILE;
+    cudaMemsetAsync(s.st_tiles, 0, sizeof(unsigned long long) * blocks, st);
+    k_tiles_scan<<<blocks, TSCAN_THREADS, 0, st>>>(total, s);
+    g_launches += 2;
+}
+
+void launch_emit(const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st)
+{
+    cudaMemsetAsync(s.tile_cursor, 0, sizeof(int) * (size_t)d.V * d.T, st);
+    k_emit<<<148 * 8, 256, 0, st>>>(cams, s);
+    g_launches++;
+}
+
+void launch_sort(const StepDims &d, const Scratch &s, cudaStream_t st)
 {
     static bool attr_set = false;
     if (!attr_set) {
@@ -289,17 +306,10 @@ void launch_bin(const StepDims &d, const CamSet &cams, const Scratch &s, cudaStr
                              LARGE_CAP * 12);
         attr_set = true;
     }
-    const int total = d.V * d.T;
-    k_tile_counts<<<d.V, 256, 0, st>>>(cams, s);
-    const int blocks = (total + TSCAN_TILE - 1) / TSCAN_TILE;
-    cudaMemsetAsync(s.st_tiles, 0, sizeof(unsigned long long) * blocks, st);
-    k_tiles_scan<<<blocks, TSCAN_THREADS, 0, st>>>(total, s);
-    cudaMemsetAsync(s.tile_cursor, 0, sizeof(int) * (size_t)total, st);
-    k_emit<<<148 * 8, 256, 0, st>>>(cams, s);
     k_sort_tiles<SMALL_CAP, 512><<<148 * 4, 512, SMALL_CAP * 12, st>>>(s.cls_small, 0, s);
     k_sort_tiles<LARGE_CAP, 1024><<<148, 1024, LARGE_CAP * 12, st>>>(s.cls_large, 1, s);
     k_sort_huge<<<1, 1024, 0, st>>>(s);
-    g_launches += 6;
+    g_launches += 3;
 }
 
 }  // namespace cls

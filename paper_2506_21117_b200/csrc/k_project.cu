@@ -88,9 +88,18 @@ k_project(const float4 *__restrict__ mean_op, const float4 *__restrict__ quat, c
         const float uh = __double2float_rn(p.u), vh = __double2float_rn(p.v);
         s.rec_xy[slot] = make_float4(uh, __double2float_rn(p.u - (double)uh), vh, __double2float_rn(p.v - (double)vh));
         const float o = (float)(1.0 / (1.0 + exp(-(double)mo.w)));
-        s.rec_co[slot] = make_float4(__double2float_rn(p.ca), __double2float_rn(p.cb), __double2float_rn(p.cc), o);
+        // LDL^T form of the conic (see power_ldl): pivot on the larger diagonal entry.
+        // conic a = C/det, b = -B/det, c = A/det  =>  a >= c  <=>  C >= A
+        const bool piv_y = p.A > p.C;
+        const double ap = piv_y ? p.cc : p.ca;
+        const double beta = piv_y ? (-p.B / p.A) : (-p.B / p.C);
+        const double gam = piv_y ? (1.0 / p.A) : (1.0 / p.C);
+        const float bh = __double2float_rn(beta);
+        const float apf = __double2float_rn(ap);
+        s.rec_co[slot] = make_float4(piv_y ? -apf : apf, bh, __double2float_rn(gam), o);
         s.rec_rgb[slot] = make_float4(fmaxf(col[0], 0.0f), fmaxf(col[1], 0.0f), fmaxf(col[2], 0.0f),
-                                      __int_as_float(ordi));
+                                      __double2float_rn(beta - (double)bh));
+        s.rec_ord[slot] = ordi;
         s.rec_rect[slot] = make_int2(p.x0 | (p.y0 << 16), p.x1 | (p.y1 << 16));
         s.rec_meta[slot] = make_int2(i, v | (ordi >= 0 ? (int)0x80000000u : 0));
         s.rec_depth[slot] = __float_as_uint(__double2float_rn(p.tz));

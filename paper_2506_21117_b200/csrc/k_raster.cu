@@ -17,12 +17,12 @@ namespace cls {
 
 #define RT_THREADS 256
 
-struct Staged {
-    float4 a;   // (du, dv, conic a, conic b)   tile-local 2D mean, conic
-    float4 b;   // (conic c, opacity, r, g)
-    float2 c;   // (b, active ordinal bits)
-};
-
+// One staged Gaussian of a tile (40 B of shared memory):
+//   sa = (s0, t0, beta, +-a_p)  LDL^T exponent terms at the tile origin (power_ldl); sign of a_p = pivot y
+//   sb = (gamma, opacity, r, g)
+//   sc = (b, active ordinal bits)
+// s0, t0 are formed in fp64 from the record's hi/lo 2D mean and beta (H1), once
+// per (tile, Gaussian) and amortised over the tile's 256 pixels.
 __device__ __forceinline__ void stage(const Scratch &s, unsigned val, int tx, int ty, float4 &sa, float4 &sb,
                                       float2 &sc)
 {
@@ -30,12 +30,16 @@ __device__ __forceinline__ void stage(const Scratch &s, unsigned val, int tx, in
     const float4 xy = s.rec_xy[rid];
     const float4 co = s.rec_co[rid];
     const float4 rgb = s.rec_rgb[rid];
-    // (u_hi - 16 tx) is exact in fp32; adding u_lo rounds once at tile scale (~1e-6 px)
-    const float du = __fadd_rn(__fsub_rn(xy.x, (float)(CLS_TILE * tx)), xy.y);
-    const float dv = __fadd_rn(__fsub_rn(xy.z, (float)(CLS_TILE * ty)), xy.w);
-    sa = make_float4(du, dv, co.x, co.y);
+    const int ord = s.rec_ord[rid];
+    const double dx0 = ((double)xy.x - (double)(CLS_TILE * tx)) + (double)xy.y;
+    const double dy0 = ((double)xy.z - (double)(CLS_TILE * ty)) + (double)xy.w;
+    const double beta = (double)co.y + (double)rgb.w;
+    const bool piv_y = co.x < 0.f;
+    const double s0 = piv_y ? fma(beta, dx0, dy0) : fma(beta, dy0, dx0);
+    const double t0 = piv_y ? dx0 : dy0;
+    sa = make_float4(__double2float_rn(s0), __double2float_rn(t0), co.y, co.x);
     sb = make_float4(co.z, co.w, rgb.x, rgb.y);
-    sc = make_float2(rgb.z, rgb.w);
+    sc = make_float2(rgb.z, __int_as_float(ord));
 }
 
 __device__ __forceinline__ float block_sum(float v, float *red)
@@ -87,6 +91,7 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         const bool inside = x < W && y < H;
         float Tr = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f;
         int last = -1;
+        int nev = 0;
         bool done = !inside;
         for (int b0 = 0; b0 < n; b0 += RT_THREADS) {
             if (__syncthreads_count(done) == RT_THREADS) break;
@@ -95,10 +100,12 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
             __syncthreads();
             const int cnt = min(RT_THREADS, n - b0);
             for (int k = 0; k < cnt && !done; k++) {
+                ++nev;
                 const float4 A = sa[k];
                 const float4 B = sb[k];
-                const float dx = __fsub_rn(A.x, flx), dy = __fsub_rn(A.y, fly);
-                const float pw = power_of(A.z, A.w, B.x, dx, dy);
+                const bool py = A.w < 0.f;
+                float ss, tt;
+                const float pw = power_ldl(A.x, A.y, A.z, fabsf(A.w), B.x, py ? fly : flx, py ? flx : fly, ss, tt);
                 if (pw > 0.0f) continue;
                 const float alpha = fminf(0.99f, __fmul_rn(B.y, __expf(pw)));
                 if (alpha < (1.0f / 255.0f)) continue;
@@ -144,6 +151,8 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
             const float tot = block_sum(l1, red);
             if (tid == 0) s.item_loss[item] = tot;
         }
+        const float evs = block_sum((float)nev, red);   // exact: < 2^24 per tile
+        if (tid == 0) atomicAdd(&s.cnt->fwd_evals, (unsigned long long)evs);
     }
 }
 
@@ -265,6 +274,7 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         float S0 = 0.f, S1 = 0.f, S2 = 0.f;
         const float bgT0 = Tf * bg.x, bgT1 = Tf * bg.y, bgT2 = Tf * bg.z;
         float4 *gbase = s.grad2d + (size_t)v * A * 3;
+        int nev = 0;
         for (int bend = end; bend > first; bend -= RT_THREADS) {
             const int bstart = max(bend - RT_THREADS, first);
             __syncthreads();
@@ -278,11 +288,12 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
                 const float2 Cc = sc[k];
                 const int ordk = __float_as_int(Cc.y);
                 bool on = inside && jj <= last;
-                float dx = 0.f, dy = 0.f, G = 0.f, alpha = 0.f;
+                nev += on;
+                const bool pvy = Aa.w < 0.f;
+                const float ap = fabsf(Aa.w);
+                float ss = 0.f, tt = 0.f, G = 0.f, alpha = 0.f;
                 if (on) {
-                    dx = __fsub_rn(Aa.x, flx);
-                    dy = __fsub_rn(Aa.y, fly);
-                    const float pw = power_of(Aa.z, Aa.w, Bb.x, dx, dy);
+                    const float pw = power_ldl(Aa.x, Aa.y, Aa.z, ap, Bb.x, pvy ? fly : flx, pvy ? flx : fly, ss, tt);
                     if (pw > 0.0f) on = false;
                     else {
                         G = __expf(pw);
@@ -308,8 +319,13 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
                         if (Bb.y * G < 0.99f) {
                             const float dLdp = alpha * dLda;
                             r[5] = G * dLda;
-                            r[0] = -dLdp * (Aa.z * dx + Aa.w * dy);
-                            r[1] = -dLdp * (Aa.w * dx + Bb.x * dy);
+                            // conic b = beta a_p; dp/d(pivot coord) = -a_p s, dp/d(other) = -(b s + gamma t)
+                            const float bq = Aa.z * ap;
+                            const float gp = -ap * ss, go = -(bq * ss + Bb.x * tt);
+                            const float dpiv = ss - Aa.z * tt;   // pivot-axis offset (dx for pivot x)
+                            const float dx = pvy ? tt : dpiv, dy = pvy ? dpiv : tt;
+                            r[0] = dLdp * (pvy ? go : gp);
+                            r[1] = dLdp * (pvy ? gp : go);
                             r[2] = -0.5f * dLdp * dx * dx;
                             r[3] = -dLdp * dx * dy;
                             r[4] = -0.5f * dLdp * dy * dy;
@@ -338,8 +354,28 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
                 }
             }
         }
+        for (int o = 16; o > 0; o >>= 1) nev += __shfl_xor_sync(0xffffffffu, nev, o);
+        if (lane == 0 && nev) atomicAdd(&s.cnt->bwd_evals, (unsigned long long)nev);
         __syncthreads();
     }
+}
+
+__global__ void k_zero_grad2d(Scratch s, int V, long long cap)
+{
+    const long long A = s.cnt->A;
+    if (A > cap) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&s.cnt->overflow, 4);
+        return;
+    }
+    const long long total = (long long)V * A * 3;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x)
+        s.grad2d[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+void launch_zero_grad2d(const StepDims &d, const Scratch &s, long long cap, cudaStream_t st)
+{
+    k_zero_grad2d<<<148 * 4, 256, 0, st>>>(s, d.V, cap);
+    g_launches++;
 }
 
 void launch_bwd_raster(const StepDims &d, const Scratch &s, const float *dL_dimages, float3 bg, cudaStream_t st)

@@ -25,13 +25,16 @@ void launch_active_mask(const Params &g, const StepDims &d, const CamSet &cams, 
 // (2) projection / cull of every Gaussian vs the mask -> records (k_project.cu)
 void launch_project(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st);
 // (3) binning: tile counts, scan, key emission, per-tile sort  (k_bin.cu)
-void launch_bin(const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st);
+void launch_bin_count(const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st);
+void launch_emit(const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st);
+void launch_sort(const StepDims &d, const Scratch &s, cudaStream_t st);
 // (4) forward compositing + fused L1                           (k_raster.cu)
 void launch_fwd(const StepDims &d, const CamSet &cams, const Scratch &s, const float *targets, float *images,
                 float loss_scale, float3 bg, cudaStream_t st);
 void launch_fill_bg(const StepDims &d, const Scratch &s, float *images, float3 bg, cudaStream_t st);
 void launch_loss(const Scratch &s, float loss_scale, float *loss, cudaStream_t st);
 // (5) backward raster + backward projection                    (k_raster.cu, k_bwd_project.cu)
+void launch_zero_grad2d(const StepDims &d, const Scratch &s, long long cap, cudaStream_t st);
 void launch_bwd_raster(const StepDims &d, const Scratch &s, const float *dL_dimages, float3 bg, cudaStream_t st);
 void launch_bwd_project(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s,
                         float *grad_active, cudaStream_t st);

@@ -117,7 +117,7 @@ def region_structs(regions) -> ctypes.Array:
 def default_limits(n, n_views, width, height, records_per_view=None, pairs_per_view=None, max_active=None):
     TX, TY = -(-width // 16), -(-height // 16)
     if records_per_view is None:
-        records_per_view = min(n, max(4096, n // 2))
+        records_per_view = n          # all-tiles mode keeps every visible Gaussian
     if pairs_per_view is None:
         pairs_per_view = min(TX * TY * 4096, 24 * records_per_view + 65536)
     lim = N.cls_limits()
@@ -242,6 +242,14 @@ class LocalOptimizer:
         st = N.cls_stats_t()
         check(lib.cls_stats(self.ctx, ctypes.byref(st)), self.ctx)
         return st.as_dict()
+
+    def profile(self, on: bool = True):
+        check(lib.cls_profile_enable(self.ctx, 1 if on else 0), self.ctx)
+
+    def profile_read(self) -> dict:
+        pr = N.cls_profile_t()
+        check(lib.cls_profile_read(self.ctx, ctypes.byref(pr)), self.ctx)
+        return pr.as_dict()
 
     def launch_count(self) -> int:
         return int(lib.cls_launch_count(self.ctx))
