@@ -96,7 +96,7 @@ class ClockSampler:
         sm = [num(r[0]) for r in self.rows if num(r[0])]
         mx = [num(r[1]) for r in self.rows if num(r[1])]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4) if "Active" in r[4 + k]})
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[4 + k].strip() == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.rows)}
 

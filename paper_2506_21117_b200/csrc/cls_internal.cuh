@@ -41,6 +41,7 @@ struct Counters {
     int member_tiles;       // decoupled look-back tile ticket (membership)
     int A;                  // |O^t|
     int n_records;
+    int n_cand;
     int tiles_scan_tiles;   // look-back ticket (tile scan)
     unsigned long long n_pairs;
     int n_items;
@@ -72,6 +73,8 @@ struct Scratch {
     int2 *rec_meta;         // (gid, view | active << 31)
     unsigned *rec_depth;    // fp32 bits of the depth key
     long long max_records;
+    int2 *cand;             // (Gaussian, view) candidates of the fp32 pre-test
+    long long max_cand;
     // tiles
     int *tile_cnt;          // [V*T]
     int *tile_off;          // [V*T]
@@ -82,8 +85,8 @@ struct Scratch {
     int *cls_small, *cls_large, *cls_huge;  // item lists per sort class
     int *first_active;      // [items] first list position holding an active Gaussian (n if none)
     // pairs
-    unsigned long long *pair_key;   // (depth bits << 32) | gid
-    unsigned *pair_val;             // record id | active << 31; sorted in place per tile
+    unsigned long long *pairs;      // bucketed (depth bits << 32) | record | active << 31
+    unsigned *tile_list;            // per-tile depth-ordered record | active << 31
     unsigned long long *sort_tmp_key;  // huge-tile fallback scratch
     unsigned *sort_tmp_val;
     long long max_pairs;

@@ -130,9 +130,9 @@ cls_status cls_destroy(cls_ctx *c)
     if (!c) return CLS_ERR_INVALID_ARGUMENT;
     cudaSetDevice(c->device);
     void *ptrs[] = {c->s.idx, c->s.ord, c->s.st_member, c->s.mask, c->s.sat, c->s.diff, c->s.rec_xy, c->s.rec_co,
-                    c->s.rec_rgb, c->s.rec_ord, c->s.rec_rect, c->s.rec_meta, c->s.rec_depth, c->s.tile_cnt, c->s.tile_off,
+                    c->s.rec_rgb, c->s.rec_ord, c->s.cand, c->s.rec_rect, c->s.rec_meta, c->s.rec_depth, c->s.tile_cnt, c->s.tile_off,
                     c->s.tile_cursor, c->s.st_tiles, c->s.items, c->s.item_of_tile, c->s.cls_small, c->s.cls_large,
-                    c->s.cls_huge, c->s.first_active, c->s.pair_key, c->s.pair_val, c->s.sort_tmp_key,
+                    c->s.cls_huge, c->s.first_active, c->s.pairs, c->s.tile_list, c->s.sort_tmp_key,
                     c->s.sort_tmp_val, c->s.px_T, c->s.px_last, c->s.px_dl, c->s.item_loss, c->s.grad2d, c->s.cnt};
     for (void *p : ptrs)
         if (p) cudaFree(p);
@@ -169,11 +169,11 @@ cls_status cls_create(cls_ctx **out, int device, const cls_limits *lim)
     Scratch &s = c->s;
     bool ok = dalloc(&s.idx, N) && dalloc(&s.ord, N) && dalloc(&s.st_member, N / 2048 + 2) && dalloc(&s.mask, VT) &&
               dalloc(&s.sat, SAT) && dalloc(&s.diff, SAT) && dalloc(&s.rec_xy, R) && dalloc(&s.rec_co, R) &&
-              dalloc(&s.rec_rgb, R) && dalloc(&s.rec_ord, R) && dalloc(&s.rec_rect, R) && dalloc(&s.rec_meta, R) && dalloc(&s.rec_depth, R) &&
+              dalloc(&s.rec_rgb, R) && dalloc(&s.rec_ord, R) && dalloc(&s.cand, R + R / 2 + 1024) && dalloc(&s.rec_rect, R) && dalloc(&s.rec_meta, R) && dalloc(&s.rec_depth, R) &&
               dalloc(&s.tile_cnt, VT) && dalloc(&s.tile_off, VT) && dalloc(&s.tile_cursor, VT) &&
               dalloc(&s.st_tiles, VT / 2048 + 2) && dalloc(&s.items, VT) && dalloc(&s.item_of_tile, VT) &&
               dalloc(&s.cls_small, VT) && dalloc(&s.cls_large, VT) && dalloc(&s.cls_huge, VT) &&
-              dalloc(&s.first_active, VT) && dalloc(&s.pair_key, P) && dalloc(&s.pair_val, P) &&
+              dalloc(&s.first_active, VT) && dalloc(&s.pairs, P) && dalloc(&s.tile_list, P) &&
               dalloc(&s.sort_tmp_key, (size_t)1 << 22) && dalloc(&s.sort_tmp_val, (size_t)1 << 22) &&
               dalloc(&s.px_T, VT * 256) && dalloc(&s.px_last, VT * 256) && dalloc(&s.px_dl, VT * 768) &&
               dalloc(&s.item_loss, VT) && dalloc(&s.grad2d, V * (size_t)lim->max_active * 3) && dalloc(&s.cnt, 1);
@@ -187,6 +187,7 @@ cls_status cls_create(cls_ctx **out, int device, const cls_limits *lim)
         return CLS_ERR_OUT_OF_MEMORY;
     }
     s.max_records = (long long)R;
+    s.max_cand = (long long)(R + R / 2 + 1024);
     s.max_pairs = (long long)P;
     s.max_items = (int)VT;
     memset(c->h_cnt, 0, sizeof(Counters));

@@ -2,71 +2,137 @@
 // the call, culled against the dynamic tile mask, with SH->RGB for the survivors.
 //
 // PAPER.md Supp. L523 (Forward::Preprocess) and L538-539 ("we reuse the computed
-// projection to create the per-tile depth ordering").  One thread per Gaussian loops
-// over the views, so the 48 B of geometry (float4 SoA: mean_op, quat, log_scale) is
-// read from HBM once per step, not once per view.  A conservative fp32 bound on the
-// tile rect rejects most (Gaussian, view) pairs with ~40 FLOPs; survivors take the
-// exact fp64 geometry (so rects, culling and depth keys are the fp64 definition's),
-// are tested against the view's summed-area table of active tiles (O(1)), and are
-// written as compact records with one warp-aggregated atomic per warp.
+// projection to create the per-tile depth ordering").  Pass A: one thread per Gaussian
+// loops over the views, so the 48 B of geometry (float4 SoA: mean_op, quat, log_scale)
+// is read from HBM once per step, not once per view; a conservative fp32 bound on the
+// tile rect (fp32 EWA covariance + margin) tested against the view's summed-area table
+// of active tiles (O(1)) rejects most (Gaussian, view) pairs.  Pass B: the survivors,
+// compacted so that warps stay converged, take the exact fp64 geometry (rects, culling
+// and depth keys are the fp64 definition's) and are written as compact records with one
+// warp-aggregated atomic per warp.
 #include <algorithm>
 
 #include "kernels.h"
 
 namespace cls {
 
-template <int D>
+// ---- pass A: conservative fp32 test of every (Gaussian, view); survivors -> candidate list ----
+// The fp32 2D covariance bounds the exact radius within a relative 1e-3 + 1 px margin and the
+// fp32 centre within 2 px, so no pair the exact fp64 test keeps is ever rejected here.
 __global__ void __launch_bounds__(256)
-k_project(const float4 *__restrict__ mean_op, const float4 *__restrict__ quat, const float4 *__restrict__ log_scale,
-          const float4 *__restrict__ sh, int n, const __grid_constant__ CamSet cams, Scratch s)
+k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ quat,
+               const float4 *__restrict__ log_scale, int n, const __grid_constant__ CamSet cams, Scratch s)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const bool valid = i < n;
     float4 mo = make_float4(0, 0, 0, 0), q = make_float4(1, 0, 0, 0), ls = make_float4(0, 0, 0, 0);
-    int ordi = -1;
     if (valid) {
         mo = __ldg(mean_op + i);
         q = __ldg(quat + i);
         ls = __ldg(log_scale + i);
-        ordi = s.ord[i];
     }
-    const float smax = __expf(fmaxf(ls.x, fmaxf(ls.y, ls.z))) * 1.0001f;
+    // M = R(q^) diag(exp(l)) in fp32, view independent
+    const float qn = rsqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
+    const float w = q.x * qn, x = q.y * qn, y = q.z * qn, z = q.w * qn;
+    const float s0 = __expf(ls.x), s1 = __expf(ls.y), s2 = __expf(ls.z);
+    const float M[9] = {(1.f - 2.f * (y * y + z * z)) * s0, 2.f * (x * y - w * z) * s1, 2.f * (x * z + w * y) * s2,
+                        2.f * (x * y + w * z) * s0, (1.f - 2.f * (x * x + z * z)) * s1, 2.f * (y * z - w * x) * s2,
+                        2.f * (x * z - w * y) * s0, 2.f * (y * z + w * x) * s1, (1.f - 2.f * (x * x + y * y)) * s2};
     const int W = cams.W, H = cams.H, TX = cams.TX, TY = cams.TY, P = TX + 1;
     for (int v = 0; v < cams.n; v++) {
         const GCam &c = cams.c[v];
-        const int *S = s.sat + (size_t)v * (TY + 1) * P;
+        bool cand = false;
+        if (valid) {
+            const float tz = c.R[6] * mo.x + c.R[7] * mo.y + c.R[8] * mo.z + c.t[2];
+            if (tz >= 0.199f) {
+                if (tz <= 1.0f) {
+                    cand = true;   // close to the near plane: leave it to the exact test
+                } else {
+                    const float tx = c.R[0] * mo.x + c.R[1] * mo.y + c.R[2] * mo.z + c.t[0];
+                    const float ty = c.R[3] * mo.x + c.R[4] * mo.y + c.R[5] * mo.z + c.t[1];
+                    const float limx = 1.3f * (W / (2.0f * c.fx)), limy = 1.3f * (H / (2.0f * c.fy));
+                    const float iz = 1.0f / tz;
+                    const float xz = fminf(fmaxf(tx * iz, -limx), limx), yz = fminf(fmaxf(ty * iz, -limy), limy);
+                    const float j00 = c.fx * iz, j02 = -c.fx * xz * iz, j11 = c.fy * iz, j12 = -c.fy * yz * iz;
+                    float V0[3], V1[3];
+#pragma unroll
+                    for (int b = 0; b < 3; b++) {
+                        const float t0 = j00 * c.R[b] + j02 * c.R[6 + b];
+                        const float t1 = j11 * c.R[3 + b] + j12 * c.R[6 + b];
+                        V0[b] = t0;
+                        V1[b] = t1;
+                    }
+                    float A0 = 0.f, A1 = 0.f, B0 = 0.f;
+#pragma unroll
+                    for (int b = 0; b < 3; b++) {
+                        const float u0 = V0[0] * M[b] + V0[1] * M[3 + b] + V0[2] * M[6 + b];
+                        const float u1 = V1[0] * M[b] + V1[1] * M[3 + b] + V1[2] * M[6 + b];
+                        A0 += u0 * u0;
+                        A1 += u1 * u1;
+                        B0 += u0 * u1;
+                    }
+                    const float A = A0 + 0.3f, C = A1 + 0.3f;
+                    const float mid = 0.5f * (A + C);
+                    const float det = A * C - B0 * B0;
+                    const float lam = mid + sqrtf(fmaxf(0.1f, mid * mid - det));
+                    const float rb = 3.0f * sqrtf(lam) * 1.001f + 1.0f;
+                    const float u = c.fx * tx * iz + c.cx - 0.5f;
+                    const float vv = c.fy * ty * iz + c.cy - 0.5f;
+                    const float fx0 = fminf(fmaxf(floorf((u - rb - 2.0f) * (1.0f / CLS_TILE)), -1.0f), TX + 1.0f);
+                    const float fx1 = fminf(fmaxf(floorf((u + rb + 2.0f + CLS_TILE - 1) * (1.0f / CLS_TILE)) + 1.0f,
+                                                  -1.0f), TX + 1.0f);
+                    const float fy0 = fminf(fmaxf(floorf((vv - rb - 2.0f) * (1.0f / CLS_TILE)), -1.0f), TY + 1.0f);
+                    const float fy1 = fminf(fmaxf(floorf((vv + rb + 2.0f + CLS_TILE - 1) * (1.0f / CLS_TILE)) + 1.0f,
+                                                  -1.0f), TY + 1.0f);
+                    const int bx0 = min(max((int)fx0, 0), TX), bx1 = min(max((int)fx1, 0), TX);
+                    const int by0 = min(max((int)fy0, 0), TY), by1 = min(max((int)fy1, 0), TY);
+                    const int *S = s.sat + (size_t)v * (TY + 1) * P;
+                    cand = bx1 > bx0 && by1 > by0 && sat_count(S, P, bx0, by0, bx1, by1) > 0;
+                }
+            }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, cand);
+        if (bal == 0u) continue;
+        int base = 0;
+        const int leader = __ffs(bal) - 1;
+        if (lane == leader) base = atomicAdd(&s.cnt->n_cand, __popc(bal));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (!cand) continue;
+        const long long slot = (long long)base + __popc(bal & ((1u << lane) - 1u));
+        if (slot >= s.max_cand) {
+            atomicOr(&s.cnt->overflow, 1);
+            continue;
+        }
+        s.cand[slot] = make_int2(i, v);
+    }
+}
+
+// ---- pass B: exact fp64 projection of the candidates, records for those touching active tiles ----
+template <int D>
+__global__ void __launch_bounds__(256)
+k_project_exact(const float4 *__restrict__ mean_op, const float4 *__restrict__ quat,
+                const float4 *__restrict__ log_scale, const float4 *__restrict__ sh, int n,
+                const __grid_constant__ CamSet cams, Scratch s)
+{
+    const int ncand = min(s.cnt->n_cand, (int)s.max_cand);
+    const int lane = threadIdx.x & 31;
+    const int W = cams.W, H = cams.H, TX = cams.TX, TY = cams.TY, P = TX + 1;
+    for (int base_e = blockIdx.x * blockDim.x; base_e < ncand; base_e += gridDim.x * blockDim.x) {
+        const int e = base_e + threadIdx.x;
         bool keep = false;
         Proj p;
-        if (valid) {
-            // ---- conservative fp32 pre-test (never rejects a pair the exact test keeps) ----
-            const float tz = c.R[6] * mo.x + c.R[7] * mo.y + c.R[8] * mo.z + c.t[2];
-            bool maybe = tz >= 0.199f;
-            if (maybe && tz > 1.0f) {
-                const float tx = c.R[0] * mo.x + c.R[1] * mo.y + c.R[2] * mo.z + c.t[0];
-                const float ty = c.R[3] * mo.x + c.R[4] * mo.y + c.R[5] * mo.z + c.t[1];
-                const float tzl = tz * 0.999f;
-                const float limx = 1.3f * (W / (2.0f * c.fx)), limy = 1.3f * (H / (2.0f * c.fy));
-                const float ax = fminf(fabsf(tx) / tzl + 1e-3f, limx), ay = fminf(fabsf(ty) / tzl + 1e-3f, limy);
-                const float jf2 = (c.fx * c.fx * (1.0f + ax * ax) + c.fy * c.fy * (1.0f + ay * ay)) / (tzl * tzl);
-                const float tr = jf2 * smax * smax;                 // >= trace(T Sigma T^T)
-                const float lam = tr + 0.6f + 0.3163f;               // >= lambda_max(Sigma')
-                const float rb = 3.0f * sqrtf(lam) * 1.001f + 2.0f;
-                const float u = c.fx * tx / tz + c.cx - 0.5f;
-                const float vv = c.fy * ty / tz + c.cy - 0.5f;
-                const float fx0 = fminf(fmaxf(floorf((u - rb) * (1.0f / CLS_TILE)), -1.0f), (float)TX + 1.0f);
-                const float fx1 = fminf(fmaxf(floorf((u + rb + CLS_TILE - 1) * (1.0f / CLS_TILE)) + 1.0f, -1.0f),
-                                        (float)TX + 1.0f);
-                const float fy0 = fminf(fmaxf(floorf((vv - rb) * (1.0f / CLS_TILE)), -1.0f), (float)TY + 1.0f);
-                const float fy1 = fminf(fmaxf(floorf((vv + rb + CLS_TILE - 1) * (1.0f / CLS_TILE)) + 1.0f, -1.0f),
-                                        (float)TY + 1.0f);
-                const int bx0 = min(max((int)fx0, 0), TX), bx1 = min(max((int)fx1, 0), TX);
-                const int by0 = min(max((int)fy0, 0), TY), by1 = min(max((int)fy1, 0), TY);
-                maybe = bx1 > bx0 && by1 > by0 && sat_count(S, P, bx0, by0, bx1, by1) > 0;
-            }
-            // ---- exact fp64 projection ----
-            if (maybe && project_gaussian(mo, q, ls, c, W, H, TX, TY, p))
+        int i = 0, v = 0;
+        float4 mo = make_float4(0, 0, 0, 0);
+        if (e < ncand) {
+            const int2 cv = s.cand[e];
+            i = cv.x;
+            v = cv.y;
+            mo = __ldg(mean_op + i);
+            if (project_gaussian(mo, __ldg(quat + i), __ldg(log_scale + i), cams.c[v], W, H, TX, TY, p)) {
+                const int *S = s.sat + (size_t)v * (TY + 1) * P;
                 keep = sat_count(S, P, p.x0, p.y0, p.x1, p.y1) > 0;
+            }
         }
         const unsigned bal = __ballot_sync(0xffffffffu, keep);
         if (bal == 0u) continue;
@@ -80,6 +146,8 @@ k_project(const float4 *__restrict__ mean_op, const float4 *__restrict__ quat, c
             atomicOr(&s.cnt->overflow, 1);
             continue;
         }
+        const GCam &c = cams.c[v];
+        const int ordi = s.ord[i];
         // ---- colour from SH at the viewing direction (R15), fp32 ----
         float dir[3], Y[16], col[3];
         view_dir(mo, c, dir);
@@ -116,13 +184,15 @@ void launch_project(const Params &g, const StepDims &d, const CamSet &cams, cons
 {
     cudaMemsetAsync(s.diff, 0, sizeof(int) * (size_t)d.V * (d.TY + 1) * (d.TX + 1), st);
     const int blocks = (d.n + 255) / 256;
+    k_project_cand<<<blocks, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, d.n, cams, s);
+    const int grid = 148 * 8;
     switch (d.D) {
-    case 0: k_project<0><<<blocks, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s); break;
-    case 1: k_project<1><<<blocks, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s); break;
-    case 2: k_project<2><<<blocks, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s); break;
-    default: k_project<3><<<blocks, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s); break;
+    case 0: k_project_exact<0><<<grid, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s); break;
+    case 1: k_project_exact<1><<<grid, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s); break;
+    case 2: k_project_exact<2><<<grid, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s); break;
+    default: k_project_exact<3><<<grid, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s); break;
     }
-    g_launches++;
+    g_launches += 2;
 }
 
 }  // namespace cls

@@ -96,7 +96,7 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         for (int b0 = 0; b0 < n; b0 += RT_THREADS) {
             if (__syncthreads_count(done) == RT_THREADS) break;
             const int j = b0 + tid;
-            if (j < n) stage(s, s.pair_val[off + j], tx, ty, sa[tid], sb[tid], sc[tid]);
+            if (j < n) stage(s, s.tile_list[off + j], tx, ty, sa[tid], sb[tid], sc[tid]);
             __syncthreads();
             const int cnt = min(RT_THREADS, n - b0);
             for (int k = 0; k < cnt && !done; k++) {
@@ -279,7 +279,7 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
             const int bstart = max(bend - RT_THREADS, first);
             __syncthreads();
             const int j = bstart + tid;
-            if (j < bend) stage(s, s.pair_val[off + j], tx, ty, sa[tid], sb[tid], sc[tid]);
+            if (j < bend) stage(s, s.tile_list[off + j], tx, ty, sa[tid], sb[tid], sc[tid]);
             __syncthreads();
             for (int k = bend - 1 - bstart; k >= 0; k--) {
                 const int jj = bstart + k;
