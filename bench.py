@@ -247,7 +247,7 @@ def run_ours(args):
             "e2e": e2e, "gpu_launches": int(launches), "roofline": roof, "clocks": clocks,
             "kernels_ms_per_step": {k: round(v["ms"] / args.steps, 4) for k, v in per.items()},
             "counts": {k: stats[k] for k in ("n_records", "n_pairs", "n_items", "max_list", "n_huge_tiles",
-                                             "n_fwd_evals", "n_bwd_evals")},
+                                             "n_fwd_evals", "n_bwd_evals", "n_candidates", "n_kept_pairs")},
         }
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(sc, args.cpu_views)

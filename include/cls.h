@@ -107,6 +107,8 @@ typedef struct {
     int64_t n_huge_tiles;      /* tiles sorted by the global-memory fallback */
     int64_t n_fwd_evals;       /* (pixel, list entry) evaluations of the forward compositing */
     int64_t n_bwd_evals;       /* (pixel, list entry) evaluations of the backward walk (after its bwd) */
+    int64_t n_candidates;      /* (Gaussian, view) pairs passing the fp32 projection pre-test */
+    int64_t n_kept_pairs;      /* pairs kept after the exact alpha-footprint culling (<= n_pairs) */
 } cls_stats_t;
 
 #define CLS_PROF_GROUPS 16

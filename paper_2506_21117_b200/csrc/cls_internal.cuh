@@ -43,7 +43,8 @@ struct Counters {
     int n_records;
     int n_cand;
     int tiles_scan_tiles;   // look-back ticket (tile scan)
-    unsigned long long n_pairs;
+    unsigned long long n_pairs;     // (record, active tile of its rect) pairs: bucket capacity
+    unsigned long long n_kept;      // pairs kept after the exact footprint culling
     int n_items;
     int n_small, n_large, n_huge;
     int fwd_work, bwd_work;
@@ -63,6 +64,7 @@ struct Scratch {
     // masks
     uint8_t *mask;          // [V][T]
     int *sat;               // [V][(TY+1)(TX+1)]
+    unsigned *rowmask;      // [V][TY][ceil(TX/32)] active-tile row bitmasks
     int *diff;              // [V][(TY+1)(TX+1)]  corner differences of record rects
     // records
     float4 *rec_xy;         // (u_hi, u_lo, v_hi, v_lo)

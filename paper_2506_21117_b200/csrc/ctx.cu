@@ -39,10 +39,10 @@ struct cls_ctx {
     int64_t prof_n[CLS_PROF_GROUPS] = {};
 };
 
-static const char *PROF_NAMES[] = {"member", "active_mask", "project", "bin_count", "emit", "sort",
+static const char *PROF_NAMES[] = {"member", "active_mask", "project_cand", "project_exact", "bin_count", "emit", "sort",
                                    "fwd_raster", "fill_bg", "loss", "zero_grad2d", "bwd_raster", "bwd_project",
                                    "adam"};
-enum { P_MEMBER, P_MASK, P_PROJECT, P_BINCOUNT, P_EMIT, P_SORT, P_FWD, P_FILL, P_LOSS, P_ZERO, P_BWD_RASTER,
+enum { P_MEMBER, P_MASK, P_PROJECT, P_PROJECT_EXACT, P_BINCOUNT, P_EMIT, P_SORT, P_FWD, P_FILL, P_LOSS, P_ZERO, P_BWD_RASTER,
        P_BWD_PROJECT, P_ADAM, P_COUNT };
 static_assert(P_COUNT <= CLS_PROF_GROUPS, "profile groups");
 
@@ -129,7 +129,7 @@ cls_status cls_destroy(cls_ctx *c)
 {
     if (!c) return CLS_ERR_INVALID_ARGUMENT;
     cudaSetDevice(c->device);
-    void *ptrs[] = {c->s.idx, c->s.ord, c->s.st_member, c->s.mask, c->s.sat, c->s.diff, c->s.rec_xy, c->s.rec_co,
+    void *ptrs[] = {c->s.idx, c->s.ord, c->s.st_member, c->s.mask, c->s.sat, c->s.rowmask, c->s.diff, c->s.rec_xy, c->s.rec_co,
                     c->s.rec_rgb, c->s.rec_ord, c->s.cand, c->s.rec_rect, c->s.rec_meta, c->s.rec_depth, c->s.tile_cnt, c->s.tile_off,
                     c->s.tile_cursor, c->s.st_tiles, c->s.items, c->s.item_of_tile, c->s.cls_small, c->s.cls_large,
                     c->s.cls_huge, c->s.first_active, c->s.pairs, c->s.tile_list, c->s.sort_tmp_key,
@@ -168,7 +168,7 @@ cls_status cls_create(cls_ctx **out, int device, const cls_limits *lim)
     const size_t SAT = V * (c->maxTY + 1) * (c->maxTX + 1);
     Scratch &s = c->s;
     bool ok = dalloc(&s.idx, N) && dalloc(&s.ord, N) && dalloc(&s.st_member, N / 2048 + 2) && dalloc(&s.mask, VT) &&
-              dalloc(&s.sat, SAT) && dalloc(&s.diff, SAT) && dalloc(&s.rec_xy, R) && dalloc(&s.rec_co, R) &&
+              dalloc(&s.sat, SAT) && dalloc(&s.rowmask, V * c->maxTY * ((c->maxTX + 31) / 32)) && dalloc(&s.diff, SAT) && dalloc(&s.rec_xy, R) && dalloc(&s.rec_co, R) &&
               dalloc(&s.rec_rgb, R) && dalloc(&s.rec_ord, R) && dalloc(&s.cand, R + R / 2 + 1024) && dalloc(&s.rec_rect, R) && dalloc(&s.rec_meta, R) && dalloc(&s.rec_depth, R) &&
               dalloc(&s.tile_cnt, VT) && dalloc(&s.tile_off, VT) && dalloc(&s.tile_cursor, VT) &&
               dalloc(&s.st_tiles, VT / 2048 + 2) && dalloc(&s.items, VT) && dalloc(&s.item_of_tile, VT) &&
@@ -280,7 +280,8 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     cudaMemcpyAsync(c->h_A, &s.cnt->A, sizeof(int), cudaMemcpyDeviceToHost, st);
     cudaEventRecord(c->ev_member, st);
     run(c, P_MASK, st, [&] { launch_active_mask(p, d, cs, s, st); });
-    run(c, P_PROJECT, st, [&] { launch_project(p, d, cs, s, st); });
+    run(c, P_PROJECT, st, [&] { launch_project_cand(p, d, cs, s, st); });
+    run(c, P_PROJECT_EXACT, st, [&] { launch_project_exact(p, d, cs, s, st); });
     run(c, P_BINCOUNT, st, [&] { launch_bin_count(d, cs, s, st); });
     run(c, P_EMIT, st, [&] { launch_emit(d, cs, s, st); });
     run(c, P_SORT, st, [&] { launch_sort(d, s, st); });
@@ -397,6 +398,10 @@ cls_status cls_stats(cls_ctx *c, cls_stats_t *out)
     out->overflow = h.overflow | ovf;
     out->max_list = h.max_list;
     out->n_huge_tiles = h.n_huge;
+    out->n_candidates = h.n_cand;
+    unsigned long long kept = 0;
+    cudaMemcpy(&kept, &c->s.cnt->n_kept, sizeof kept, cudaMemcpyDeviceToHost);
+    out->n_kept_pairs = (int64_t)kept;
     out->n_fwd_evals = (int64_t)h.fwd_evals;
     unsigned long long bev = 0;
     cudaMemcpy(&bev, &c->s.cnt->bwd_evals, sizeof bev, cudaMemcpyDeviceToHost);

@@ -135,15 +135,76 @@ __global__ void __launch_bounds__(TSCAN_THREADS) k_tiles_scan(int total, Scratch
 }
 
 // Emission: every (record, active tile of its rect) pair is written into the bucket of its
-// (view, tile) as one 64-bit word (depth bits << 32 | record | active << 31).  Small rects are
-// walked by their own lane; rects of more than 32 tiles by the whole warp (no long serial tails).
-__device__ __forceinline__ void emit_tile(const Scratch &s, int v, int T, int TX, int tx, int ty, unsigned long long w)
+// (view, tile) as one 64-bit word (depth bits << 32 | record | active << 31) -- unless the
+// record's alpha >= 1/255 ellipse misses every pixel centre of the tile.  That culling is
+// exact: the minimum over the tile's pixel-centre rectangle of q = a dx^2 + 2b dx dy + c dy^2
+// (fp64, closed form on the rectangle's edges) exceeds 2 ln(255 o) + margin, so every pixel of
+// the tile would skip the entry (its alpha < 1/255); results are unchanged, work is not.
+// Buckets are sized by the rect counts (upper bounds); the cursors give the kept counts.
+// Small rects are walked by their own lane; rects of more than 32 tiles by the whole warp.
+struct EmitRec {
+    double u, v, a, b, c, qcut;   // centre, conic (from the LDL^T record), culling threshold
+    double ba, bc;                // b/a, b/c (edge minimisers)
+    int x0, y0, x1, y1, view;
+    unsigned long long w;
+};
+
+__device__ __forceinline__ double edge_min(double a, double b, double c, double b_over_c, double dx0, double dy_lo,
+                                           double dy_hi)
+{
+    // min over dy in [dy_lo, dy_hi] of a dx0^2 + 2 b dx0 dy + c dy^2 (c > 0): at dy = -(b/c) dx0
+    double dy = -b_over_c * dx0;
+    dy = fmin(fmax(dy, dy_lo), dy_hi);
+    return a * dx0 * dx0 + 2.0 * b * dx0 * dy + c * dy * dy;
+}
+
+// true if some pixel centre of tile (tx, ty) can have q <= qcut
+__device__ __forceinline__ bool tile_touched(const EmitRec &r, int tx, int ty)
+{
+    const double xl = CLS_TILE * tx, xh = xl + (CLS_TILE - 1), yl = CLS_TILE * ty, yh = yl + (CLS_TILE - 1);
+    if (r.u >= xl && r.u <= xh && r.v >= yl && r.v <= yh) return true;
+    // dx = u - x, dy = v - y over the rectangle; the minimum lies on an edge
+    const double dxl = r.u - xh, dxh = r.u - xl, dyl = r.v - yh, dyh = r.v - yl;
+    double m = edge_min(r.a, r.b, r.c, r.bc, dxl, dyl, dyh);
+    m = fmin(m, edge_min(r.a, r.b, r.c, r.bc, dxh, dyl, dyh));
+    m = fmin(m, edge_min(r.c, r.b, r.a, r.ba, dyl, dxl, dxh));   // symmetric: roles of x and y swapped
+    m = fmin(m, edge_min(r.c, r.b, r.a, r.ba, dyh, dxl, dxh));
+    return m <= r.qcut;
+}
+
+__device__ __forceinline__ void emit_tile(const Scratch &s, const EmitRec &r, int T, int TX, int tx, int ty)
 {
     const int t = ty * TX + tx;
-    if (!s.mask[(size_t)v * T + t]) return;
-    const size_t e = (size_t)v * T + t;
+    if (!s.mask[(size_t)r.view * T + t]) return;
+    if (!tile_touched(r, tx, ty)) return;
+    const size_t e = (size_t)r.view * T + t;
     const int pos = s.tile_off[e] + atomicAdd(&s.tile_cursor[e], 1);
-    s.pairs[pos] = w;
+    s.pairs[pos] = r.w;
+}
+
+__device__ __forceinline__ EmitRec load_rec(const Scratch &s, int r)
+{
+    EmitRec q;
+    const int2 rc = s.rec_rect[r];
+    const int2 meta = s.rec_meta[r];
+    const float4 xy = s.rec_xy[r];
+    const float4 co = s.rec_co[r];
+    const float4 rgb = s.rec_rgb[r];
+    q.view = meta.y & 0x7fffffff;
+    q.w = ((unsigned long long)s.rec_depth[r] << 32) | ((unsigned)r | ((unsigned)meta.y & 0x80000000u));
+    q.x0 = rc.x & 0xffff; q.y0 = rc.x >> 16; q.x1 = rc.y & 0xffff; q.y1 = rc.y >> 16;
+    q.u = (double)xy.x + (double)xy.y;
+    q.v = (double)xy.z + (double)xy.w;
+    const double ap = fabs((double)co.x), beta = (double)co.y + (double)rgb.w, gam = co.z;
+    // LDL^T -> conic: pivot x: a = ap, b = ap beta, c = ap beta^2 + gamma (pivot y: a <-> c)
+    const double pa = ap, pb = ap * beta, pc = ap * beta * beta + gam;
+    if (co.x < 0.f) { q.a = pc; q.b = pb; q.c = pa; }
+    else { q.a = pa; q.b = pb; q.c = pc; }
+    q.ba = q.b / q.a;
+    q.bc = q.b / q.c;
+    // alpha >= 1/255  <=>  q <= 2 ln(255 o); margin covers the fp32 per-pixel evaluation
+    q.qcut = co.w > 0.f ? 2.0 * log(255.0 * (double)co.w) * (1.0 + 1e-6) + 2e-3 : -1.0;
+    return q;
 }
 
 __global__ void __launch_bounds__(256) k_emit(const __grid_constant__ CamSet cams, Scratch s)
@@ -154,50 +215,66 @@ __global__ void __launch_bounds__(256) k_emit(const __grid_constant__ CamSet cam
     const int lane = threadIdx.x & 31;
     for (int base = blockIdx.x * blockDim.x; base < nrec; base += gridDim.x * blockDim.x) {
         const int r = base + threadIdx.x;
-        int x0 = 0, y0 = 0, x1 = 0, y1 = 0, v = 0;
-        unsigned long long w = 0;
-        if (r < nrec) {
-            const int2 rc = s.rec_rect[r];
-            const int2 meta = s.rec_meta[r];
-            v = meta.y & 0x7fffffff;
-            w = ((unsigned long long)s.rec_depth[r] << 32) | ((unsigned)r | ((unsigned)meta.y & 0x80000000u));
-            x0 = rc.x & 0xffff; y0 = rc.x >> 16; x1 = rc.y & 0xffff; y1 = rc.y >> 16;
-        }
-        const int area = (x1 - x0) * (y1 - y0);
+        EmitRec q;
+        q.x0 = q.y0 = q.x1 = q.y1 = 0;
+        if (r < nrec) q = load_rec(s, r);
+        const int area = (q.x1 - q.x0) * (q.y1 - q.y0);
         const bool big = area > 32;
-        if (!big)
-            for (int ty = y0; ty < y1; ty++)
-                for (int tx = x0; tx < x1; tx++) emit_tile(s, v, T, TX, tx, ty, w);
+        if (!big && q.qcut >= 0.0)
+            for (int ty = q.y0; ty < q.y1; ty++)
+                for (int tx = q.x0; tx < q.x1; tx++) emit_tile(s, q, T, TX, tx, ty);
         unsigned bigs = __ballot_sync(0xffffffffu, big);
         while (bigs) {
             const int src = __ffs(bigs) - 1;
             bigs &= bigs - 1;
-            const int bx0 = __shfl_sync(0xffffffffu, x0, src), by0 = __shfl_sync(0xffffffffu, y0, src);
-            const int bw = __shfl_sync(0xffffffffu, x1 - x0, src), ba = __shfl_sync(0xffffffffu, area, src);
-            const int bv = __shfl_sync(0xffffffffu, v, src);
-            const unsigned long long bwd = __shfl_sync(0xffffffffu, w, src);
-            for (int k = lane; k < ba; k += 32) emit_tile(s, bv, T, TX, bx0 + k % bw, by0 + k / bw, bwd);
+            EmitRec b;
+            b.u = __shfl_sync(0xffffffffu, q.u, src); b.v = __shfl_sync(0xffffffffu, q.v, src);
+            b.a = __shfl_sync(0xffffffffu, q.a, src); b.b = __shfl_sync(0xffffffffu, q.b, src);
+            b.c = __shfl_sync(0xffffffffu, q.c, src); b.qcut = __shfl_sync(0xffffffffu, q.qcut, src);
+            b.ba = __shfl_sync(0xffffffffu, q.ba, src); b.bc = __shfl_sync(0xffffffffu, q.bc, src);
+            b.x0 = __shfl_sync(0xffffffffu, q.x0, src); b.y0 = __shfl_sync(0xffffffffu, q.y0, src);
+            b.x1 = __shfl_sync(0xffffffffu, q.x1, src); b.y1 = __shfl_sync(0xffffffffu, q.y1, src);
+            b.view = __shfl_sync(0xffffffffu, q.view, src);
+            b.w = __shfl_sync(0xffffffffu, q.w, src);
+            const int bw = b.x1 - b.x0, ba = bw * (b.y1 - b.y0);
+            if (b.qcut < 0.0) continue;
+            for (int k = lane; k < ba; k += 32) emit_tile(s, b, T, TX, b.x0 + k % bw, b.y0 + k / bw);
         }
     }
 }
 
+// kept counts: the cursors of the emission (<= the rect counts the buckets were sized by)
+__global__ void k_kept_counts(Scratch s)
+{
+    const int n_items = s.cnt->n_items;
+    unsigned long long kept = 0;
+    for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < n_items; it += gridDim.x * blockDim.x) {
+        const int e = s.items[it];
+        const int c = s.tile_cursor[e];
+        s.tile_cnt[e] = c;
+        kept += (unsigned long long)c;
+    }
+    for (int o = 16; o > 0; o >>= 1) kept += __shfl_xor_sync(0xffffffffu, kept, o);
+    if ((threadIdx.x & 31) == 0 && kept) atomicAdd(&s.cnt->n_kept, kept);
+}
+
 // ---- on-chip stable LSD radix sort of one bucket by the 32-bit depth key ----
-// Warp-striped arrangement (warp w owns entries [w*PER_WARP, (w+1)*PER_WARP)); per pass a
-// warp ranks its 32 entries of a round with __match_any_sync, keeps running per-(warp, digit)
-// counts in shared memory, and a block scan in (digit, warp) order gives stable positions.
+// Warp-striped arrangement: with R = ceil(n / THREADS) rounds, warp w owns the contiguous
+// entries [w*32R, (w+1)*32R).  Per 8-bit pass a warp ranks the 32 entries of a round with
+// __match_any_sync and keeps running per-(digit, warp) counts in shared memory (digit-major,
+// so the block scan reads them contiguously); the exclusive scan gives stable positions.
 // Equal depth keys are then ordered by Gaussian index (reading R13) -- rare, short runs.
 template <int CAP, int THREADS>
 __global__ void __launch_bounds__(THREADS) k_sort_tiles(const int *__restrict__ list, int which, Scratch s)
 {
     constexpr int WARPS = THREADS / 32;
-    constexpr int ITEMS = CAP / THREADS;
-    constexpr int PER_WARP = ITEMS * 32;
+    constexpr int MAXR = CAP / THREADS;
     constexpr int CELLS = 256 * WARPS;
     constexpr int CPT = CELLS / THREADS;   // scan cells per thread (8)
     extern __shared__ unsigned smem_u32[];
     unsigned *keyA = smem_u32;
     unsigned *keyB = keyA + CAP;
-    int *run = reinterpret_cast<int *>(keyB + CAP);                 // [WARPS][256]
+    int *run = reinterpret_cast<int *>(keyB + CAP);                 // [256][WARPS]
     unsigned short *idxA = reinterpret_cast<unsigned short *>(run + CELLS);
     unsigned short *idxB = idxA + CAP;
     __shared__ int s_first;
@@ -211,40 +288,41 @@ __global__ void __launch_bounds__(THREADS) k_sort_tiles(const int *__restrict__ 
         const int e = s.items[item];
         const int n = s.tile_cnt[e];
         const int off = s.tile_off[e];
+        const int R = (n + THREADS - 1) / THREADS;
+        const int wbase = warp * 32 * R;
         const unsigned long long *pr = s.pairs + off;
         for (int j = tid; j < n; j += THREADS) {
             keyA[j] = (unsigned)(pr[j] >> 32);
             idxA[j] = (unsigned short)j;
         }
-        __syncthreads();
         for (int shift = 0; shift < 32; shift += 8) {
             for (int c = tid; c < CELLS; c += THREADS) run[c] = 0;
             __syncthreads();
-            int myrank[ITEMS], mydig[ITEMS];
+            int mine[MAXR];   // (rank << 8) | digit
 #pragma unroll
-            for (int r = 0; r < ITEMS; r++) {
-                const int j = warp * PER_WARP + r * 32 + lane;
-                const bool act = j < n;
-                const int d = act ? (int)((keyA[j] >> shift) & 255u) : 256 + lane;
-                const unsigned peers = __match_any_sync(0xffffffffu, d);
-                const int leader = __ffs(peers) - 1;
-                int base = 0;
-                if (act && lane == leader) {
-                    base = run[warp * 256 + d];
-                    run[warp * 256 + d] = base + __popc(peers);
+            for (int r = 0; r < MAXR; r++) {
+                if (r < R) {
+                    const int j = wbase + r * 32 + lane;
+                    const bool act = j < n;
+                    const int d = act ? (int)((keyA[j] >> shift) & 255u) : 256 + lane;
+                    const unsigned peers = __match_any_sync(0xffffffffu, d);
+                    const int leader = __ffs(peers) - 1;
+                    int base = 0;
+                    if (act && lane == leader) {
+                        base = run[d * WARPS + warp];
+                        run[d * WARPS + warp] = base + __popc(peers);
+                    }
+                    base = __shfl_sync(0xffffffffu, base, leader);
+                    mine[r] = ((base + __popc(peers & lt)) << 8) | (d & 255);
                 }
-                base = __shfl_sync(0xffffffffu, base, leader);
-                myrank[r] = base + __popc(peers & lt);
-                mydig[r] = d;
             }
             __syncthreads();
-            // exclusive scan over cells in (digit, warp) order: cell c = d * WARPS + w
+            // exclusive scan of run[] in (digit, warp) order
             int loc[CPT];
             int sum = 0;
 #pragma unroll
             for (int q = 0; q < CPT; q++) {
-                const int c = tid * CPT + q;
-                loc[q] = run[(c % WARPS) * 256 + c / WARPS];
+                loc[q] = run[tid * CPT + q];
                 sum += loc[q];
             }
             int inc = sum;
@@ -269,16 +347,15 @@ __global__ void __launch_bounds__(THREADS) k_sort_tiles(const int *__restrict__ 
             int pre = s_wsum[warp] + inc - sum;
 #pragma unroll
             for (int q = 0; q < CPT; q++) {
-                const int c = tid * CPT + q;
-                run[(c % WARPS) * 256 + c / WARPS] = pre;
+                run[tid * CPT + q] = pre;
                 pre += loc[q];
             }
             __syncthreads();
 #pragma unroll
-            for (int r = 0; r < ITEMS; r++) {
-                const int j = warp * PER_WARP + r * 32 + lane;
-                if (j < n) {
-                    const int pos = run[warp * 256 + mydig[r]] + myrank[r];
+            for (int r = 0; r < MAXR; r++) {
+                const int j = wbase + r * 32 + lane;
+                if (r < R && j < n) {
+                    const int pos = run[(mine[r] & 255) * WARPS + warp] + (mine[r] >> 8);
                     keyB[pos] = keyA[j];
                     idxB[pos] = idxA[j];
                 }
@@ -287,6 +364,7 @@ __global__ void __launch_bounds__(THREADS) k_sort_tiles(const int *__restrict__ 
             unsigned *tk = keyA; keyA = keyB; keyB = tk;
             unsigned short *ti = idxA; idxA = idxB; idxB = ti;
         }
+        __syncthreads();
         // ties: runs of equal depth ordered by Gaussian index
         for (int j = tid; j < n; j += THREADS) {
             const bool start = (j == 0 || keyA[j] != keyA[j - 1]) && j + 1 < n && keyA[j + 1] == keyA[j];
@@ -315,7 +393,6 @@ __global__ void __launch_bounds__(THREADS) k_sort_tiles(const int *__restrict__ 
         if (first < n) atomicMin(&s_first, first);
         __syncthreads();
         if (tid == 0) s.first_active[item] = s_first;
-        __syncthreads();
     }
 }
 
@@ -401,20 +478,21 @@ void launch_emit(const StepDims &d, const CamSet &cams, const Scratch &s, cudaSt
 {
     cudaMemsetAsync(s.tile_cursor, 0, sizeof(int) * (size_t)d.V * d.T, st);
     k_emit<<<148 * 8, 256, 0, st>>>(cams, s);
-    g_launches++;
+    k_kept_counts<<<148 * 2, 256, 0, st>>>(s);
+    g_launches += 2;
 }
 
 void launch_sort(const StepDims &d, const Scratch &s, cudaStream_t st)
 {
-    constexpr size_t SM_SMALL = sort_smem<SMALL_CAP, 512>();
+    constexpr size_t SM_SMALL = sort_smem<SMALL_CAP, 256>();
     constexpr size_t SM_LARGE = sort_smem<LARGE_CAP, 1024>();
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_sort_tiles<SMALL_CAP, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_SMALL);
+        cudaFuncSetAttribute(k_sort_tiles<SMALL_CAP, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_SMALL);
         cudaFuncSetAttribute(k_sort_tiles<LARGE_CAP, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_LARGE);
         attr_set = true;
     }
-    k_sort_tiles<SMALL_CAP, 512><<<148 * 2, 512, SM_SMALL, st>>>(s.cls_small, 0, s);
+    k_sort_tiles<SMALL_CAP, 256><<<148 * 4, 256, SM_SMALL, st>>>(s.cls_small, 0, s);
     k_sort_tiles<LARGE_CAP, 1024><<<148, 1024, SM_LARGE, st>>>(s.cls_large, 1, s);
     k_sort_huge<<<1, 1024, 0, st>>>(s);
     g_launches += 3;

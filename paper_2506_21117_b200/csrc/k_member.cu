@@ -156,6 +156,18 @@ __global__ void __launch_bounds__(256) k_sat(const __grid_constant__ CamSet cams
     }
     __syncthreads();
     if (threadIdx.x == 0) s.cnt->active_tiles[v] = S[TY * P + TX];
+    // row bitmasks of the active tiles (projection pass A)
+    const int W32 = (TX + 31) >> 5;
+    unsigned *rm = s.rowmask + (size_t)v * TY * W32;
+    for (int k = threadIdx.x; k < TY * W32; k += blockDim.x) {
+        const int y = k / W32, w = k % W32;
+        unsigned bits = 0u;
+        for (int b = 0; b < 32; b++) {
+            const int x = w * 32 + b;
+            if (x < TX && mk[y * TX + x]) bits |= 1u << b;
+        }
+        rm[k] = bits;
+    }
 }
 
 void launch_active_mask(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st)

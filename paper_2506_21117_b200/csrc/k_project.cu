@@ -18,93 +18,134 @@ namespace cls {
 
 // ---- pass A: conservative fp32 test of every (Gaussian, view); survivors -> candidate list ----
 // The fp32 2D covariance bounds the exact radius within a relative 1e-3 + 1 px margin and the
-// fp32 centre within 2 px, so no pair the exact fp64 test keeps is ever rejected here.
+// fp32 centre within 2 px, so no pair the exact fp64 test keeps is ever rejected here.  The
+// active tiles of every view are held in shared memory as row bitmasks (persistent CTAs load
+// them once).  Candidates are appended Gaussian-major (one atomic per warp), so consecutive
+// candidates share a Gaussian and pass B re-reads its parameters from L1.
+__device__ __forceinline__ bool rect_hits(const unsigned *rm, int W32, int x0, int y0, int x1, int y1)
+{
+    const int w0 = x0 >> 5, w1 = (x1 - 1) >> 5;
+    const unsigned m0 = 0xffffffffu << (x0 & 31);
+    const unsigned m1 = 0xffffffffu >> (31 - ((x1 - 1) & 31));
+    for (int y = y0; y < y1; y++) {
+        const unsigned *row = rm + y * W32;
+        if (w0 == w1) {
+            if (row[w0] & m0 & m1) return true;
+        } else {
+            if (row[w0] & m0) return true;
+            for (int w = w0 + 1; w < w1; w++)
+                if (row[w]) return true;
+            if (row[w1] & m1) return true;
+        }
+    }
+    return false;
+}
+
 __global__ void __launch_bounds__(256)
 k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ quat,
-               const float4 *__restrict__ log_scale, int n, const __grid_constant__ CamSet cams, Scratch s)
+               const float4 *__restrict__ log_scale, int n, const __grid_constant__ CamSet cams, Scratch s,
+               bool use_smem)
 {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    extern __shared__ unsigned s_rows[];   // [V][TY][W32] active-tile row bitmasks (if they fit)
     const int lane = threadIdx.x & 31;
-    const bool valid = i < n;
-    float4 mo = make_float4(0, 0, 0, 0), q = make_float4(1, 0, 0, 0), ls = make_float4(0, 0, 0, 0);
-    if (valid) {
-        mo = __ldg(mean_op + i);
-        q = __ldg(quat + i);
-        ls = __ldg(log_scale + i);
+    const int W = cams.W, H = cams.H, TX = cams.TX, TY = cams.TY;
+    const int W32 = (TX + 31) >> 5;
+    const int per_view = TY * W32;
+    const unsigned *rows = s.rowmask;
+    if (use_smem) {
+        for (int k = threadIdx.x; k < cams.n * per_view; k += blockDim.x) s_rows[k] = s.rowmask[k];
+        __syncthreads();
+        rows = s_rows;
     }
-    // M = R(q^) diag(exp(l)) in fp32, view independent
-    const float qn = rsqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
-    const float w = q.x * qn, x = q.y * qn, y = q.z * qn, z = q.w * qn;
-    const float s0 = __expf(ls.x), s1 = __expf(ls.y), s2 = __expf(ls.z);
-    const float M[9] = {(1.f - 2.f * (y * y + z * z)) * s0, 2.f * (x * y - w * z) * s1, 2.f * (x * z + w * y) * s2,
-                        2.f * (x * y + w * z) * s0, (1.f - 2.f * (x * x + z * z)) * s1, 2.f * (y * z - w * x) * s2,
-                        2.f * (x * z - w * y) * s0, 2.f * (y * z + w * x) * s1, (1.f - 2.f * (x * x + y * y)) * s2};
-    const int W = cams.W, H = cams.H, TX = cams.TX, TY = cams.TY, P = TX + 1;
-    for (int v = 0; v < cams.n; v++) {
-        const GCam &c = cams.c[v];
-        bool cand = false;
+    for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+        const int i = base + threadIdx.x;
+        const bool valid = i < n;
+        float4 mo = make_float4(0, 0, 0, 0), q = make_float4(1, 0, 0, 0), ls = make_float4(0, 0, 0, 0);
         if (valid) {
-            const float tz = c.R[6] * mo.x + c.R[7] * mo.y + c.R[8] * mo.z + c.t[2];
-            if (tz >= 0.199f) {
-                if (tz <= 1.0f) {
-                    cand = true;   // close to the near plane: leave it to the exact test
-                } else {
-                    const float tx = c.R[0] * mo.x + c.R[1] * mo.y + c.R[2] * mo.z + c.t[0];
-                    const float ty = c.R[3] * mo.x + c.R[4] * mo.y + c.R[5] * mo.z + c.t[1];
-                    const float limx = 1.3f * (W / (2.0f * c.fx)), limy = 1.3f * (H / (2.0f * c.fy));
-                    const float iz = 1.0f / tz;
-                    const float xz = fminf(fmaxf(tx * iz, -limx), limx), yz = fminf(fmaxf(ty * iz, -limy), limy);
-                    const float j00 = c.fx * iz, j02 = -c.fx * xz * iz, j11 = c.fy * iz, j12 = -c.fy * yz * iz;
-                    float V0[3], V1[3];
-#pragma unroll
-                    for (int b = 0; b < 3; b++) {
-                        const float t0 = j00 * c.R[b] + j02 * c.R[6 + b];
-                        const float t1 = j11 * c.R[3 + b] + j12 * c.R[6 + b];
-                        V0[b] = t0;
-                        V1[b] = t1;
-                    }
-                    float A0 = 0.f, A1 = 0.f, B0 = 0.f;
-#pragma unroll
-                    for (int b = 0; b < 3; b++) {
-                        const float u0 = V0[0] * M[b] + V0[1] * M[3 + b] + V0[2] * M[6 + b];
-                        const float u1 = V1[0] * M[b] + V1[1] * M[3 + b] + V1[2] * M[6 + b];
-                        A0 += u0 * u0;
-                        A1 += u1 * u1;
-                        B0 += u0 * u1;
-                    }
-                    const float A = A0 + 0.3f, C = A1 + 0.3f;
-                    const float mid = 0.5f * (A + C);
-                    const float det = A * C - B0 * B0;
-                    const float lam = mid + sqrtf(fmaxf(0.1f, mid * mid - det));
-                    const float rb = 3.0f * sqrtf(lam) * 1.001f + 1.0f;
-                    const float u = c.fx * tx * iz + c.cx - 0.5f;
-                    const float vv = c.fy * ty * iz + c.cy - 0.5f;
-                    const float fx0 = fminf(fmaxf(floorf((u - rb - 2.0f) * (1.0f / CLS_TILE)), -1.0f), TX + 1.0f);
-                    const float fx1 = fminf(fmaxf(floorf((u + rb + 2.0f + CLS_TILE - 1) * (1.0f / CLS_TILE)) + 1.0f,
-                                                  -1.0f), TX + 1.0f);
-                    const float fy0 = fminf(fmaxf(floorf((vv - rb - 2.0f) * (1.0f / CLS_TILE)), -1.0f), TY + 1.0f);
-                    const float fy1 = fminf(fmaxf(floorf((vv + rb + 2.0f + CLS_TILE - 1) * (1.0f / CLS_TILE)) + 1.0f,
-                                                  -1.0f), TY + 1.0f);
-                    const int bx0 = min(max((int)fx0, 0), TX), bx1 = min(max((int)fx1, 0), TX);
-                    const int by0 = min(max((int)fy0, 0), TY), by1 = min(max((int)fy1, 0), TY);
-                    const int *S = s.sat + (size_t)v * (TY + 1) * P;
-                    cand = bx1 > bx0 && by1 > by0 && sat_count(S, P, bx0, by0, bx1, by1) > 0;
+            mo = __ldg(mean_op + i);
+            q = __ldg(quat + i);
+            ls = __ldg(log_scale + i);
+        }
+        // M = R(q^) diag(exp(l)) in fp32, view independent
+        const float qn = rsqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
+        const float w = q.x * qn, x = q.y * qn, y = q.z * qn, z = q.w * qn;
+        const float s0 = __expf(ls.x), s1 = __expf(ls.y), s2 = __expf(ls.z);
+        const float M[9] = {(1.f - 2.f * (y * y + z * z)) * s0, 2.f * (x * y - w * z) * s1, 2.f * (x * z + w * y) * s2,
+                            2.f * (x * y + w * z) * s0, (1.f - 2.f * (x * x + z * z)) * s1, 2.f * (y * z - w * x) * s2,
+                            2.f * (x * z - w * y) * s0, 2.f * (y * z + w * x) * s1, (1.f - 2.f * (x * x + y * y)) * s2};
+        unsigned long long vmask = 0ull;
+        if (valid) {
+            for (int v = 0; v < cams.n; v++) {
+                const GCam &c = cams.c[v];
+                const float tz = c.R[6] * mo.x + c.R[7] * mo.y + c.R[8] * mo.z + c.t[2];
+                if (tz < 0.199f) continue;
+                if (tz <= 1.0f) {           // close to the near plane: leave it to the exact test
+                    vmask |= 1ull << v;
+                    continue;
                 }
+                const float tx = c.R[0] * mo.x + c.R[1] * mo.y + c.R[2] * mo.z + c.t[0];
+                const float ty = c.R[3] * mo.x + c.R[4] * mo.y + c.R[5] * mo.z + c.t[1];
+                const float limx = 1.3f * (W / (2.0f * c.fx)), limy = 1.3f * (H / (2.0f * c.fy));
+                const float iz = __frcp_rn(tz);
+                const float xz = fminf(fmaxf(tx * iz, -limx), limx), yz = fminf(fmaxf(ty * iz, -limy), limy);
+                const float u = c.fx * tx * iz + c.cx - 0.5f;
+                const float vv = c.fy * ty * iz + c.cy - 0.5f;
+                const float j00 = c.fx * iz, j02 = -c.fx * xz * iz, j11 = c.fy * iz, j12 = -c.fy * yz * iz;
+                float A0 = 0.f, A1 = 0.f, B0 = 0.f;
+                float V0[3], V1[3];
+#pragma unroll
+                for (int b = 0; b < 3; b++) {
+                    V0[b] = j00 * c.R[b] + j02 * c.R[6 + b];
+                    V1[b] = j11 * c.R[3 + b] + j12 * c.R[6 + b];
+                }
+#pragma unroll
+                for (int b = 0; b < 3; b++) {
+                    const float u0 = V0[0] * M[b] + V0[1] * M[3 + b] + V0[2] * M[6 + b];
+                    const float u1 = V1[0] * M[b] + V1[1] * M[3 + b] + V1[2] * M[6 + b];
+                    A0 += u0 * u0;
+                    A1 += u1 * u1;
+                    B0 += u0 * u1;
+                }
+                const float A = A0 + 0.3f, C = A1 + 0.3f;
+                const float mid = 0.5f * (A + C);
+                const float det = A * C - B0 * B0;
+                const float lam = mid + __fsqrt_rn(fmaxf(0.1f, mid * mid - det));
+                const float rb = 3.0f * __fsqrt_rn(lam) * 1.001f + 1.0f;
+                const float fx0 = fminf(fmaxf(floorf((u - rb - 2.0f) * (1.0f / CLS_TILE)), -1.0f), TX + 1.0f);
+                const float fx1 =
+                    fminf(fmaxf(floorf((u + rb + 2.0f + CLS_TILE - 1) * (1.0f / CLS_TILE)) + 1.0f, -1.0f), TX + 1.0f);
+                const float fy0 = fminf(fmaxf(floorf((vv - rb - 2.0f) * (1.0f / CLS_TILE)), -1.0f), TY + 1.0f);
+                const float fy1 =
+                    fminf(fmaxf(floorf((vv + rb + 2.0f + CLS_TILE - 1) * (1.0f / CLS_TILE)) + 1.0f, -1.0f), TY + 1.0f);
+                const int bx0 = min(max((int)fx0, 0), TX), bx1 = min(max((int)fx1, 0), TX);
+                const int by0 = min(max((int)fy0, 0), TY), by1 = min(max((int)fy1, 0), TY);
+                if (bx1 > bx0 && by1 > by0 && rect_hits(rows + v * per_view, W32, bx0, by0, bx1, by1))
+                    vmask |= 1ull << v;
             }
         }
-        const unsigned bal = __ballot_sync(0xffffffffu, cand);
-        if (bal == 0u) continue;
-        int base = 0;
-        const int leader = __ffs(bal) - 1;
-        if (lane == leader) base = atomicAdd(&s.cnt->n_cand, __popc(bal));
-        base = __shfl_sync(0xffffffffu, base, leader);
-        if (!cand) continue;
-        const long long slot = (long long)base + __popc(bal & ((1u << lane) - 1u));
-        if (slot >= s.max_cand) {
-            atomicOr(&s.cnt->overflow, 1);
+        // Gaussian-major append: lane order, then view order
+        const int cnt = __popcll(vmask);
+        int inc = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        const int tot = __shfl_sync(0xffffffffu, inc, 31);
+        if (tot == 0) continue;
+        int wb = 0;
+        if (lane == 31) wb = atomicAdd(&s.cnt->n_cand, tot);
+        wb = __shfl_sync(0xffffffffu, wb, 31);
+        long long slot = (long long)wb + inc - cnt;
+        if (slot + cnt > s.max_cand) {
+            if (cnt) atomicOr(&s.cnt->overflow, 1);
             continue;
         }
-        s.cand[slot] = make_int2(i, v);
+        while (vmask) {
+            const int v = __ffsll(vmask) - 1;
+            vmask &= vmask - 1;
+            s.cand[slot++] = make_int2(i, v);
+        }
     }
 }
 
@@ -115,6 +156,10 @@ k_project_exact(const float4 *__restrict__ mean_op, const float4 *__restrict__ q
                 const float4 *__restrict__ log_scale, const float4 *__restrict__ sh, int n,
                 const __grid_constant__ CamSet cams, Scratch s)
 {
+    __shared__ GCam s_cams[CLS_MAX_VIEWS];   // lanes index different views: no constant-bank serialisation
+    for (int k = threadIdx.x; k < cams.n * (int)(sizeof(GCam) / 4); k += blockDim.x)
+        reinterpret_cast<float *>(s_cams)[k] = reinterpret_cast<const float *>(cams.c)[k];
+    __syncthreads();
     const int ncand = min(s.cnt->n_cand, (int)s.max_cand);
     const int lane = threadIdx.x & 31;
     const int W = cams.W, H = cams.H, TX = cams.TX, TY = cams.TY, P = TX + 1;
@@ -129,7 +174,7 @@ k_project_exact(const float4 *__restrict__ mean_op, const float4 *__restrict__ q
             i = cv.x;
             v = cv.y;
             mo = __ldg(mean_op + i);
-            if (project_gaussian(mo, __ldg(quat + i), __ldg(log_scale + i), cams.c[v], W, H, TX, TY, p)) {
+            if (project_gaussian(mo, __ldg(quat + i), __ldg(log_scale + i), s_cams[v], W, H, TX, TY, p)) {
                 const int *S = s.sat + (size_t)v * (TY + 1) * P;
                 keep = sat_count(S, P, p.x0, p.y0, p.x1, p.y1) > 0;
             }
@@ -146,7 +191,7 @@ k_project_exact(const float4 *__restrict__ mean_op, const float4 *__restrict__ q
             atomicOr(&s.cnt->overflow, 1);
             continue;
         }
-        const GCam &c = cams.c[v];
+        const GCam &c = s_cams[v];
         const int ordi = s.ord[i];
         // ---- colour from SH at the viewing direction (R15), fp32 ----
         float dir[3], Y[16], col[3];
@@ -180,11 +225,24 @@ k_project_exact(const float4 *__restrict__ mean_op, const float4 *__restrict__ q
     }
 }
 
-void launch_project(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st)
+void launch_project_cand(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st)
 {
     cudaMemsetAsync(s.diff, 0, sizeof(int) * (size_t)d.V * (d.TY + 1) * (d.TX + 1), st);
-    const int blocks = (d.n + 255) / 256;
-    k_project_cand<<<blocks, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, d.n, cams, s);
+    size_t smem = sizeof(unsigned) * (size_t)d.V * d.TY * ((d.TX + 31) / 32);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_project_cand, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        attr = true;
+    }
+    const bool use_smem = smem <= 96 * 1024;
+    if (!use_smem) smem = 0;
+    const int blocks = std::min((d.n + 255) / 256, 148 * 8);
+    k_project_cand<<<blocks, 256, smem, st>>>(g.mean_op, g.quat, g.log_scale, d.n, cams, s, use_smem);
+    g_launches++;
+}
+
+void launch_project_exact(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st)
+{
     const int grid = 148 * 8;
     switch (d.D) {
     case 0: k_project_exact<0><<<grid, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s); break;
@@ -192,7 +250,7 @@ void launch_project(const Params &g, const StepDims &d, const CamSet &cams, cons
     case 2: k_project_exact<2><<<grid, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s); break;
     default: k_project_exact<3><<<grid, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s); break;
     }
-    g_launches += 2;
+    g_launches++;
 }
 
 }  // namespace cls

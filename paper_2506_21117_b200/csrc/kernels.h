@@ -23,7 +23,8 @@ void launch_member(const Params &g, const StepDims &d, const RegSet &regs, const
 // (1b) active tile mask per view + summed-area tables       (k_member.cu)
 void launch_active_mask(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st);
 // (2) projection / cull of every Gaussian vs the mask -> records (k_project.cu)
-void launch_project(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st);
+void launch_project_cand(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st);
+void launch_project_exact(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st);
 // (3) binning: tile counts, scan, key emission, per-tile sort  (k_bin.cu)
 void launch_bin_count(const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st);
 void launch_emit(const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st);
