@@ -18,8 +18,8 @@
 
 namespace cls {
 
-#define SMALL_CAP 4096
-#define LARGE_CAP 16384
+#define SMALL_CAP 2048
+#define LARGE_CAP 12288
 #define HUGE_CAP (1 << 22)
 
 // 2D inclusive prefix of the rect-corner differences -> pairs per active tile
@@ -121,12 +121,8 @@ __global__ void __launch_bounds__(TSCAN_THREADS) k_tiles_scan(int total, Scratch
         s.tile_off[e] = (int)(run & ((1ull << PACK_SHIFT) - 1));
         if (pv) {
             const int item = (int)(run >> PACK_SHIFT);
-            const int c = s.tile_cnt[e];
             s.items[item] = e;
             s.item_of_tile[e] = item;
-            if (c <= SMALL_CAP) s.cls_small[atomicAdd(&s.cnt->n_small, 1)] = item;
-            else if (c <= LARGE_CAP) s.cls_large[atomicAdd(&s.cnt->n_large, 1)] = item;
-            else s.cls_huge[atomicAdd(&s.cnt->n_huge, 1)] = item;
         } else {
             s.item_of_tile[e] = -1;
         }
@@ -209,37 +205,46 @@ __device__ __forceinline__ EmitRec load_rec(const Scratch &s, int r)
 
 __global__ void __launch_bounds__(256) k_emit(const __grid_constant__ CamSet cams, Scratch s)
 {
+    // load-balanced: the warp stages its 32 records in shared memory and walks the
+    // concatenation of their rects, one (record, tile) pair per lane per iteration
+    __shared__ EmitRec s_rec[8][32];
+    __shared__ int s_pre[8][33];
     if (s.cnt->overflow) return;
     const int nrec = s.cnt->n_records;
     const int TX = cams.TX, T = cams.T;
-    const int lane = threadIdx.x & 31;
-    for (int base = blockIdx.x * blockDim.x; base < nrec; base += gridDim.x * blockDim.x) {
-        const int r = base + threadIdx.x;
-        EmitRec q;
-        q.x0 = q.y0 = q.x1 = q.y1 = 0;
-        if (r < nrec) q = load_rec(s, r);
-        const int area = (q.x1 - q.x0) * (q.y1 - q.y0);
-        const bool big = area > 32;
-        if (!big && q.qcut >= 0.0)
-            for (int ty = q.y0; ty < q.y1; ty++)
-                for (int tx = q.x0; tx < q.x1; tx++) emit_tile(s, q, T, TX, tx, ty);
-        unsigned bigs = __ballot_sync(0xffffffffu, big);
-        while (bigs) {
-            const int src = __ffs(bigs) - 1;
-            bigs &= bigs - 1;
-            EmitRec b;
-            b.u = __shfl_sync(0xffffffffu, q.u, src); b.v = __shfl_sync(0xffffffffu, q.v, src);
-            b.a = __shfl_sync(0xffffffffu, q.a, src); b.b = __shfl_sync(0xffffffffu, q.b, src);
-            b.c = __shfl_sync(0xffffffffu, q.c, src); b.qcut = __shfl_sync(0xffffffffu, q.qcut, src);
-            b.ba = __shfl_sync(0xffffffffu, q.ba, src); b.bc = __shfl_sync(0xffffffffu, q.bc, src);
-            b.x0 = __shfl_sync(0xffffffffu, q.x0, src); b.y0 = __shfl_sync(0xffffffffu, q.y0, src);
-            b.x1 = __shfl_sync(0xffffffffu, q.x1, src); b.y1 = __shfl_sync(0xffffffffu, q.y1, src);
-            b.view = __shfl_sync(0xffffffffu, q.view, src);
-            b.w = __shfl_sync(0xffffffffu, q.w, src);
-            const int bw = b.x1 - b.x0, ba = bw * (b.y1 - b.y0);
-            if (b.qcut < 0.0) continue;
-            for (int k = lane; k < ba; k += 32) emit_tile(s, b, T, TX, b.x0 + k % bw, b.y0 + k / bw);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int base = blockIdx.x * blockDim.x + wid * 32; base < nrec; base += gridDim.x * blockDim.x) {
+        const int r = base + lane;
+        int area = 0;
+        if (r < nrec) {
+            const EmitRec q = load_rec(s, r);
+            s_rec[wid][lane] = q;
+            if (q.qcut >= 0.0) area = (q.x1 - q.x0) * (q.y1 - q.y0);
         }
+        int inc = area;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        s_pre[wid][lane + 1] = inc;
+        if (lane == 0) s_pre[wid][0] = 0;
+        const int total = __shfl_sync(0xffffffffu, inc, 31);
+        __syncwarp();
+        for (int k = lane; k < total; k += 32) {
+            // owning record: largest j with s_pre[j] <= k
+            int lo = 0, hi = 31;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (s_pre[wid][mid] <= k) lo = mid;
+                else hi = mid - 1;
+            }
+            const EmitRec &q = s_rec[wid][lo];
+            const int loc = k - s_pre[wid][lo];
+            const int bw = q.x1 - q.x0;
+            emit_tile(s, q, T, TX, q.x0 + loc % bw, q.y0 + loc / bw);
+        }
+        __syncwarp();
     }
 }
 
@@ -253,32 +258,40 @@ __global__ void k_kept_counts(Scratch s)
         const int c = s.tile_cursor[e];
         s.tile_cnt[e] = c;
         kept += (unsigned long long)c;
+        if (c <= SMALL_CAP) s.cls_small[atomicAdd(&s.cnt->n_small, 1)] = it;
+        else if (c <= LARGE_CAP) s.cls_large[atomicAdd(&s.cnt->n_large, 1)] = it;
+        else s.cls_huge[atomicAdd(&s.cnt->n_huge, 1)] = it;
     }
     for (int o = 16; o > 0; o >>= 1) kept += __shfl_xor_sync(0xffffffffu, kept, o);
     if ((threadIdx.x & 31) == 0 && kept) atomicAdd(&s.cnt->n_kept, kept);
 }
 
 // ---- on-chip stable LSD radix sort of one bucket by the 32-bit depth key ----
-// Warp-striped arrangement: with R = ceil(n / THREADS) rounds, warp w owns the contiguous
-// entries [w*32R, (w+1)*32R).  Per 8-bit pass a warp ranks the 32 entries of a round with
-// __match_any_sync and keeps running per-(digit, warp) counts in shared memory (digit-major,
-// so the block scan reads them contiguously); the exclusive scan gives stable positions.
-// Equal depth keys are then ordered by Gaussian index (reading R13) -- rare, short runs.
+// Keys are offset by the tile's minimum (order preserved), so only ceil(bits / 9) passes of
+// 9-bit digits run (usually 3).  Warp-striped arrangement: with R = ceil(n / THREADS) rounds,
+// warp w owns the contiguous entries [w*32R, (w+1)*32R).  Per pass each warp ranks its rounds
+// with __match_any_sync + a shared-memory atomicAdd by each digit's leader (issued in program
+// order, so ranks are stable and the rounds pipeline); a block scan over (digit, warp) gives
+// stable positions.  Equal depth keys are ordered by Gaussian index afterwards (reading R13).
+#define SORT_BITS 9
+#define SORT_BINS (1 << SORT_BITS)
+
 template <int CAP, int THREADS>
 __global__ void __launch_bounds__(THREADS) k_sort_tiles(const int *__restrict__ list, int which, Scratch s)
 {
     constexpr int WARPS = THREADS / 32;
     constexpr int MAXR = CAP / THREADS;
-    constexpr int CELLS = 256 * WARPS;
-    constexpr int CPT = CELLS / THREADS;   // scan cells per thread (8)
+    constexpr int WP = WARPS + 1;                       // padded row of the run table
+    constexpr int DPT = SORT_BINS / THREADS;            // digits per thread in the scan
     extern __shared__ unsigned smem_u32[];
     unsigned *keyA = smem_u32;
     unsigned *keyB = keyA + CAP;
-    int *run = reinterpret_cast<int *>(keyB + CAP);                 // [256][WARPS]
-    unsigned short *idxA = reinterpret_cast<unsigned short *>(run + CELLS);
+    int *run = reinterpret_cast<int *>(keyB + CAP);     // [SORT_BINS][WP]
+    unsigned short *idxA = reinterpret_cast<unsigned short *>(run + SORT_BINS * WP);
     unsigned short *idxB = idxA + CAP;
     __shared__ int s_first;
     __shared__ int s_wsum[WARPS];
+    __shared__ unsigned s_kmin, s_kmax;
     if (s.cnt->overflow) return;
     const int count = which == 0 ? s.cnt->n_small : s.cnt->n_large;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -291,40 +304,55 @@ __global__ void __launch_bounds__(THREADS) k_sort_tiles(const int *__restrict__ 
         const int R = (n + THREADS - 1) / THREADS;
         const int wbase = warp * 32 * R;
         const unsigned long long *pr = s.pairs + off;
+        if (tid == 0) { s_kmin = 0xffffffffu; s_kmax = 0u; s_first = n; }
+        __syncthreads();
+        unsigned kmn = 0xffffffffu, kmx = 0u;
         for (int j = tid; j < n; j += THREADS) {
-            keyA[j] = (unsigned)(pr[j] >> 32);
+            const unsigned k = (unsigned)(pr[j] >> 32);
+            keyA[j] = k;
             idxA[j] = (unsigned short)j;
+            kmn = min(kmn, k);
+            kmx = max(kmx, k);
         }
-        for (int shift = 0; shift < 32; shift += 8) {
-            for (int c = tid; c < CELLS; c += THREADS) run[c] = 0;
-            __syncthreads();
-            int mine[MAXR];   // (rank << 8) | digit
+        for (int o = 16; o > 0; o >>= 1) {
+            kmn = min(kmn, __shfl_xor_sync(0xffffffffu, kmn, o));
+            kmx = max(kmx, __shfl_xor_sync(0xffffffffu, kmx, o));
+        }
+        if (lane == 0 && n > 0) { atomicMin(&s_kmin, kmn); atomicMax(&s_kmax, kmx); }
+        for (int c = tid; c < SORT_BINS * WP; c += THREADS) run[c] = 0;
+        __syncthreads();
+        const unsigned kmin = s_kmin;
+        const int bits = n > 0 ? 32 - __clz((int)(s_kmax - kmin)) : 0;
+        for (int j = tid; j < n; j += THREADS) keyA[j] -= kmin;
+        __syncthreads();
+        for (int shift = 0; shift < bits; shift += SORT_BITS) {
+            int mine[MAXR];   // (rank << 10) | digit
 #pragma unroll
             for (int r = 0; r < MAXR; r++) {
                 if (r < R) {
                     const int j = wbase + r * 32 + lane;
                     const bool act = j < n;
-                    const int d = act ? (int)((keyA[j] >> shift) & 255u) : 256 + lane;
+                    const int d = act ? (int)((keyA[j] >> shift) & (SORT_BINS - 1)) : SORT_BINS + lane;
                     const unsigned peers = __match_any_sync(0xffffffffu, d);
                     const int leader = __ffs(peers) - 1;
                     int base = 0;
-                    if (act && lane == leader) {
-                        base = run[d * WARPS + warp];
-                        run[d * WARPS + warp] = base + __popc(peers);
-                    }
+                    if (act && lane == leader) base = atomicAdd(&run[d * WP + warp], __popc(peers));
                     base = __shfl_sync(0xffffffffu, base, leader);
-                    mine[r] = ((base + __popc(peers & lt)) << 8) | (d & 255);
+                    mine[r] = ((base + __popc(peers & lt)) << 10) | (d & (SORT_BINS - 1));
                 }
             }
             __syncthreads();
             // exclusive scan of run[] in (digit, warp) order
-            int loc[CPT];
+            int loc[DPT * WARPS];
             int sum = 0;
 #pragma unroll
-            for (int q = 0; q < CPT; q++) {
-                loc[q] = run[tid * CPT + q];
-                sum += loc[q];
-            }
+            for (int q = 0; q < DPT; q++)
+#pragma unroll
+                for (int w = 0; w < WARPS; w++) {
+                    const int v = run[(tid * DPT + q) * WP + w];
+                    loc[q * WARPS + w] = v;
+                    sum += v;
+                }
             int inc = sum;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -333,38 +361,33 @@ __global__ void __launch_bounds__(THREADS) k_sort_tiles(const int *__restrict__ 
             }
             if (lane == 31) s_wsum[warp] = inc;
             __syncthreads();
-            if (warp == 0) {
-                int w = lane < WARPS ? s_wsum[lane] : 0;
-                int wi2 = w;
+            int wpre = 0;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int t = __shfl_up_sync(0xffffffffu, wi2, o);
-                    if (lane >= o) wi2 += t;
+            for (int w = 0; w < WARPS; w++) wpre += (w < warp) ? s_wsum[w] : 0;
+            int pre = wpre + inc - sum;
+#pragma unroll
+            for (int q = 0; q < DPT; q++)
+#pragma unroll
+                for (int w = 0; w < WARPS; w++) {
+                    run[(tid * DPT + q) * WP + w] = pre;
+                    pre += loc[q * WARPS + w];
                 }
-                if (lane < WARPS) s_wsum[lane] = wi2 - w;
-            }
-            __syncthreads();
-            int pre = s_wsum[warp] + inc - sum;
-#pragma unroll
-            for (int q = 0; q < CPT; q++) {
-                run[tid * CPT + q] = pre;
-                pre += loc[q];
-            }
             __syncthreads();
 #pragma unroll
             for (int r = 0; r < MAXR; r++) {
                 const int j = wbase + r * 32 + lane;
                 if (r < R && j < n) {
-                    const int pos = run[(mine[r] & 255) * WARPS + warp] + (mine[r] >> 8);
+                    const int pos = run[(mine[r] & (SORT_BINS - 1)) * WP + warp] + (mine[r] >> 10);
                     keyB[pos] = keyA[j];
                     idxB[pos] = idxA[j];
                 }
             }
             __syncthreads();
+            for (int c = tid; c < SORT_BINS * WP; c += THREADS) run[c] = 0;
             unsigned *tk = keyA; keyA = keyB; keyB = tk;
             unsigned short *ti = idxA; idxA = idxB; idxB = ti;
+            __syncthreads();
         }
-        __syncthreads();
         // ties: runs of equal depth ordered by Gaussian index
         for (int j = tid; j < n; j += THREADS) {
             const bool start = (j == 0 || keyA[j] != keyA[j - 1]) && j + 1 < n && keyA[j + 1] == keyA[j];
@@ -382,7 +405,6 @@ __global__ void __launch_bounds__(THREADS) k_sort_tiles(const int *__restrict__ 
                 idxA[b + 1] = ia;
             }
         }
-        if (tid == 0) s_first = n;
         __syncthreads();
         int first = n;
         for (int j = tid; j < n; j += THREADS) {
@@ -399,7 +421,7 @@ __global__ void __launch_bounds__(THREADS) k_sort_tiles(const int *__restrict__ 
 template <int CAP, int THREADS>
 constexpr size_t sort_smem()
 {
-    return (size_t)CAP * 4 * 2 + (size_t)256 * (THREADS / 32) * 4 + (size_t)CAP * 2 * 2;
+    return (size_t)CAP * 4 * 2 + (size_t)SORT_BINS * (THREADS / 32 + 1) * 4 + (size_t)CAP * 2 * 2;
 }
 
 // global-memory fallback for buckets longer than LARGE_CAP (one block, buckets in turn):
@@ -485,15 +507,15 @@ void launch_emit(const StepDims &d, const CamSet &cams, const Scratch &s, cudaSt
 void launch_sort(const StepDims &d, const Scratch &s, cudaStream_t st)
 {
     constexpr size_t SM_SMALL = sort_smem<SMALL_CAP, 256>();
-    constexpr size_t SM_LARGE = sort_smem<LARGE_CAP, 1024>();
+    constexpr size_t SM_LARGE = sort_smem<LARGE_CAP, 512>();
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(k_sort_tiles<SMALL_CAP, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_SMALL);
-        cudaFuncSetAttribute(k_sort_tiles<LARGE_CAP, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_LARGE);
+        cudaFuncSetAttribute(k_sort_tiles<LARGE_CAP, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_LARGE);
         attr_set = true;
     }
-    k_sort_tiles<SMALL_CAP, 256><<<148 * 4, 256, SM_SMALL, st>>>(s.cls_small, 0, s);
-    k_sort_tiles<LARGE_CAP, 1024><<<148, 1024, SM_LARGE, st>>>(s.cls_large, 1, s);
+    k_sort_tiles<SMALL_CAP, 256><<<148 * 5, 256, SM_SMALL, st>>>(s.cls_small, 0, s);
+    k_sort_tiles<LARGE_CAP, 512><<<148, 512, SM_LARGE, st>>>(s.cls_large, 1, s);
     k_sort_huge<<<1, 1024, 0, st>>>(s);
     g_launches += 3;
 }

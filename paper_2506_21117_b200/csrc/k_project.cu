@@ -75,10 +75,13 @@ k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
                             2.f * (x * z - w * y) * s0, 2.f * (y * z + w * x) * s1, (1.f - 2.f * (x * x + y * y)) * s2};
         unsigned long long vmask = 0ull;
         if (valid) {
+            // 2 ln(255 o) (+ margin): no pixel has alpha >= 1/255 beyond q > qcut
+            const float op = 1.0f / (1.0f + __expf(-mo.w));
+            const float qcut = 2.0f * __logf(255.0f * op) * 1.001f + 0.05f;
             for (int v = 0; v < cams.n; v++) {
                 const GCam &c = cams.c[v];
                 const float tz = c.R[6] * mo.x + c.R[7] * mo.y + c.R[8] * mo.z + c.t[2];
-                if (tz < 0.199f) continue;
+                if (tz < 0.199f || qcut < 0.0f) continue;
                 if (tz <= 1.0f) {           // close to the near plane: leave it to the exact test
                     vmask |= 1ull << v;
                     continue;
@@ -111,12 +114,15 @@ k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
                 const float det = A * C - B0 * B0;
                 const float lam = mid + __fsqrt_rn(fmaxf(0.1f, mid * mid - det));
                 const float rb = 3.0f * __fsqrt_rn(lam) * 1.001f + 1.0f;
-                const float fx0 = fminf(fmaxf(floorf((u - rb - 2.0f) * (1.0f / CLS_TILE)), -1.0f), TX + 1.0f);
+                // alpha >= 1/255 footprint: |u - x| <= sqrt(qcut Sigma'_xx), |v - y| <= sqrt(qcut Sigma'_yy)
+                const float hx = fminf(rb, __fsqrt_rn(fmaxf(qcut, 0.f) * A) * 1.001f + 1.0f);
+                const float hy = fminf(rb, __fsqrt_rn(fmaxf(qcut, 0.f) * C) * 1.001f + 1.0f);
+                const float fx0 = fminf(fmaxf(floorf((u - hx - 2.0f) * (1.0f / CLS_TILE)), -1.0f), TX + 1.0f);
                 const float fx1 =
-                    fminf(fmaxf(floorf((u + rb + 2.0f + CLS_TILE - 1) * (1.0f / CLS_TILE)) + 1.0f, -1.0f), TX + 1.0f);
-                const float fy0 = fminf(fmaxf(floorf((vv - rb - 2.0f) * (1.0f / CLS_TILE)), -1.0f), TY + 1.0f);
+                    fminf(fmaxf(floorf((u + hx + 2.0f + CLS_TILE - 1) * (1.0f / CLS_TILE)) + 1.0f, -1.0f), TX + 1.0f);
+                const float fy0 = fminf(fmaxf(floorf((vv - hy - 2.0f) * (1.0f / CLS_TILE)), -1.0f), TY + 1.0f);
                 const float fy1 =
-                    fminf(fmaxf(floorf((vv + rb + 2.0f + CLS_TILE - 1) * (1.0f / CLS_TILE)) + 1.0f, -1.0f), TY + 1.0f);
+                    fminf(fmaxf(floorf((vv + hy + 2.0f + CLS_TILE - 1) * (1.0f / CLS_TILE)) + 1.0f, -1.0f), TY + 1.0f);
                 const int bx0 = min(max((int)fx0, 0), TX), bx1 = min(max((int)fx1, 0), TX);
                 const int by0 = min(max((int)fy0, 0), TY), by1 = min(max((int)fy1, 0), TY);
                 if (bx1 > bx0 && by1 > by0 && rect_hits(rows + v * per_view, W32, bx0, by0, bx1, by1))
@@ -175,8 +181,24 @@ k_project_exact(const float4 *__restrict__ mean_op, const float4 *__restrict__ q
             v = cv.y;
             mo = __ldg(mean_op + i);
             if (project_gaussian(mo, __ldg(quat + i), __ldg(log_scale + i), s_cams[v], W, H, TX, TY, p)) {
-                const int *S = s.sat + (size_t)v * (TY + 1) * P;
-                keep = sat_count(S, P, p.x0, p.y0, p.x1, p.y1) > 0;
+                // emission rect = 3-sigma rect (support, R8) n bounding box of the alpha >= 1/255
+                // footprint (exact culling: outside it every pixel has alpha < 1/255)
+                const double o64 = 1.0 / (1.0 + exp(-(double)mo.w));
+                const double qcut = 2.0 * log(255.0 * o64) * (1.0 + 1e-6) + 2e-3;
+                if (qcut >= 0.0) {
+                    const double hx = sqrt(qcut * p.A) + 1e-3, hy = sqrt(qcut * p.C) + 1e-3;
+                    // pixel x is reached iff |u - x| <= hx; tile tx holds x in [16 tx, 16 tx + 15]
+                    const int fx0 = (int)fmin(fmax(floor((p.u - hx - (CLS_TILE - 1)) / CLS_TILE) + 1.0, -1.0), TX + 1.0);
+                    const int fx1 = (int)fmin(fmax(floor((p.u + hx) / CLS_TILE) + 1.0, -1.0), TX + 1.0);
+                    const int fy0 = (int)fmin(fmax(floor((p.v - hy - (CLS_TILE - 1)) / CLS_TILE) + 1.0, -1.0), TY + 1.0);
+                    const int fy1 = (int)fmin(fmax(floor((p.v + hy) / CLS_TILE) + 1.0, -1.0), TY + 1.0);
+                    p.x0 = max(p.x0, fx0); p.x1 = min(p.x1, fx1);
+                    p.y0 = max(p.y0, fy0); p.y1 = min(p.y1, fy1);
+                    if (p.x1 > p.x0 && p.y1 > p.y0) {
+                        const int *S = s.sat + (size_t)v * (TY + 1) * P;
+                        keep = sat_count(S, P, p.x0, p.y0, p.x1, p.y1) > 0;
+                    }
+                }
             }
         }
         const unsigned bal = __ballot_sync(0xffffffffu, keep);
