@@ -65,6 +65,7 @@ struct Scratch {
     uint8_t *mask;          // [V][T]
     int *sat;               // [V][(TY+1)(TX+1)]
     unsigned *rowmask;      // [V][TY][ceil(TX/32)] active-tile row bitmasks
+    int4 *view_bbox;        // [V] tile bbox of the active tiles
     int *diff;              // [V][(TY+1)(TX+1)]  corner differences of record rects
     // records
     float4 *rec_xy;         // (u_hi, u_lo, v_hi, v_lo)

@@ -156,6 +156,21 @@ __global__ void __launch_bounds__(256) k_sat(const __grid_constant__ CamSet cams
     }
     __syncthreads();
     if (threadIdx.x == 0) s.cnt->active_tiles[v] = S[TY * P + TX];
+    // tile bbox of the active tiles (x0, y0, x1, y1 exclusive; empty: x1 <= x0)
+    __shared__ int s_bb[4];
+    if (threadIdx.x == 0) { s_bb[0] = TX; s_bb[1] = TY; s_bb[2] = 0; s_bb[3] = 0; }
+    __syncthreads();
+    {
+        int x0 = TX, y0 = TY, x1 = 0, y1 = 0;
+        for (int t = threadIdx.x; t < TX * TY; t += blockDim.x)
+            if (mk[t]) {
+                const int x = t % TX, y = t / TX;
+                x0 = min(x0, x); y0 = min(y0, y); x1 = max(x1, x + 1); y1 = max(y1, y + 1);
+            }
+        atomicMin(&s_bb[0], x0); atomicMin(&s_bb[1], y0); atomicMax(&s_bb[2], x1); atomicMax(&s_bb[3], y1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s.view_bbox[v] = make_int4(s_bb[0], s_bb[1], s_bb[2], s_bb[3]);
     // row bitmasks of the active tiles (projection pass A)
     const int W32 = (TX + 31) >> 5;
     unsigned *rm = s.rowmask + (size_t)v * TY * W32;

@@ -51,6 +51,13 @@ k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
     const int W = cams.W, H = cams.H, TX = cams.TX, TY = cams.TY;
     const int W32 = (TX + 31) >> 5;
     const int per_view = TY * W32;
+    __shared__ float4 s_bbox[CLS_MAX_VIEWS];   // pixel bbox (x0, y0, x1, y1) of each view's active tiles
+    for (int k = threadIdx.x; k < cams.n; k += blockDim.x) {
+        const int4 b = s.view_bbox[k];
+        s_bbox[k] = b.z > b.x ? make_float4(CLS_TILE * b.x, CLS_TILE * b.y, CLS_TILE * b.z - 1, CLS_TILE * b.w - 1)
+                              : make_float4(1e30f, 1e30f, -1e30f, -1e30f);
+    }
+    __syncthreads();
     const unsigned *rows = s.rowmask;
     if (use_smem) {
         for (int k = threadIdx.x; k < cams.n * per_view; k += blockDim.x) s_rows[k] = s.rowmask[k];
@@ -70,6 +77,8 @@ k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
         const float qn = rsqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
         const float w = q.x * qn, x = q.y * qn, y = q.z * qn, z = q.w * qn;
         const float s0 = __expf(ls.x), s1 = __expf(ls.y), s2 = __expf(ls.z);
+        const float smx = fmaxf(s0, fmaxf(s1, s2)) * 1.001f;
+        const float smax2 = smx * smx;
         const float M[9] = {(1.f - 2.f * (y * y + z * z)) * s0, 2.f * (x * y - w * z) * s1, 2.f * (x * z + w * y) * s2,
                             2.f * (x * y + w * z) * s0, (1.f - 2.f * (x * x + z * z)) * s1, 2.f * (y * z - w * x) * s2,
                             2.f * (x * z - w * y) * s0, 2.f * (y * z + w * x) * s1, (1.f - 2.f * (x * x + y * y)) * s2};
@@ -81,11 +90,7 @@ k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
             for (int v = 0; v < cams.n; v++) {
                 const GCam &c = cams.c[v];
                 const float tz = c.R[6] * mo.x + c.R[7] * mo.y + c.R[8] * mo.z + c.t[2];
-                if (tz < 0.199f || qcut < 0.0f) continue;
-                if (tz <= 1.0f) {           // close to the near plane: leave it to the exact test
-                    vmask |= 1ull << v;
-                    continue;
-                }
+                if (tz < 0.199f || qcut < 0.0f) continue;   // exact culls t_z <= 0.2 (R5)
                 const float tx = c.R[0] * mo.x + c.R[1] * mo.y + c.R[2] * mo.z + c.t[0];
                 const float ty = c.R[3] * mo.x + c.R[4] * mo.y + c.R[5] * mo.z + c.t[1];
                 const float limx = 1.3f * (W / (2.0f * c.fx)), limy = 1.3f * (H / (2.0f * c.fy));
@@ -93,6 +98,12 @@ k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
                 const float xz = fminf(fmaxf(tx * iz, -limx), limx), yz = fminf(fmaxf(ty * iz, -limy), limy);
                 const float u = c.fx * tx * iz + c.cx - 0.5f;
                 const float vv = c.fy * ty * iz + c.cy - 0.5f;
+                {   // cheap screen vs the pixel bbox of the view's active tiles: radius <= 3 |J|_F s_max + margin
+                    const float jf2 = (c.fx * c.fx * (1.0f + xz * xz) + c.fy * c.fy * (1.0f + yz * yz)) * iz * iz;
+                    const float rc = 3.0f * __fsqrt_rn(jf2 * smax2 + 0.92f) * 1.001f + 34.0f;   // + tile rounding of the rect
+                    const float4 bb = s_bbox[v];
+                    if (u + rc < bb.x || u - rc > bb.z || vv + rc < bb.y || vv - rc > bb.w) continue;
+                }
                 const float j00 = c.fx * iz, j02 = -c.fx * xz * iz, j11 = c.fy * iz, j12 = -c.fy * yz * iz;
                 float A0 = 0.f, A1 = 0.f, B0 = 0.f;
                 float V0[3], V1[3];
@@ -111,18 +122,30 @@ k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
                 }
                 const float A = A0 + 0.3f, C = A1 + 0.3f;
                 const float mid = 0.5f * (A + C);
-                const float det = A * C - B0 * B0;
-                const float lam = mid + __fsqrt_rn(fmaxf(0.1f, mid * mid - det));
-                const float rb = 3.0f * __fsqrt_rn(lam) * 1.001f + 1.0f;
-                // alpha >= 1/255 footprint: |u - x| <= sqrt(qcut Sigma'_xx), |v - y| <= sqrt(qcut Sigma'_yy)
-                const float hx = fminf(rb, __fsqrt_rn(fmaxf(qcut, 0.f) * A) * 1.001f + 1.0f);
-                const float hy = fminf(rb, __fsqrt_rn(fmaxf(qcut, 0.f) * C) * 1.001f + 1.0f);
-                const float fx0 = fminf(fmaxf(floorf((u - hx - 2.0f) * (1.0f / CLS_TILE)), -1.0f), TX + 1.0f);
-                const float fx1 =
-                    fminf(fmaxf(floorf((u + hx + 2.0f + CLS_TILE - 1) * (1.0f / CLS_TILE)) + 1.0f, -1.0f), TX + 1.0f);
-                const float fy0 = fminf(fmaxf(floorf((vv - hy - 2.0f) * (1.0f / CLS_TILE)), -1.0f), TY + 1.0f);
-                const float fy1 =
-                    fminf(fmaxf(floorf((vv + hy + 2.0f + CLS_TILE - 1) * (1.0f / CLS_TILE)) + 1.0f, -1.0f), TY + 1.0f);
+                // lambda_max via the cancellation-free form: mid^2 - det = ((A - C)/2)^2 + B^2
+                const float hd = 0.5f * (A - C);
+                const float lam = mid + __fsqrt_rn(fmaxf(0.1f, hd * hd + B0 * B0));
+                // conservative mirrors (fp32 error margins) of the exact 3-sigma rect (R7/R8:
+                // x0 = trunc((u - r)/16), x1 = trunc((u + r + 15)/16), r = ceil(3 sqrt(lambda))) and of
+                // the exact alpha-footprint tile range; the candidate rect is their intersection
+                // margins: relative fp32 error of u, Sigma' grows like 1/t_z near the near plane
+                // (cancellation in t = R mu + t0 ~ 3e-6 absolute): 1e-3 relative + 0.5 px covers t_z >= 0.199
+                const float r32 = ceilf(3.0f * __fsqrt_rn(lam) * 1.001f + 0.01f);
+                const float em = 0.5f + 1e-3f * fabsf(u - c.cx) + 1e-3f * fabsf(vv - c.cy);
+                const float rx0 = floorf((u - r32 - em) * (1.0f / CLS_TILE));
+                const float rx1 = floorf((u + r32 + em + CLS_TILE - 1) * (1.0f / CLS_TILE));
+                const float ry0 = floorf((vv - r32 - em) * (1.0f / CLS_TILE));
+                const float ry1 = floorf((vv + r32 + em + CLS_TILE - 1) * (1.0f / CLS_TILE));
+                const float hx = __fsqrt_rn(fmaxf(qcut, 0.f) * A) * 1.001f + em;
+                const float hy = __fsqrt_rn(fmaxf(qcut, 0.f) * C) * 1.001f + em;
+                const float gx0 = floorf((u - hx - (CLS_TILE - 1)) * (1.0f / CLS_TILE)) + 1.0f;
+                const float gx1 = floorf((u + hx) * (1.0f / CLS_TILE)) + 1.0f;
+                const float gy0 = floorf((vv - hy - (CLS_TILE - 1)) * (1.0f / CLS_TILE)) + 1.0f;
+                const float gy1 = floorf((vv + hy) * (1.0f / CLS_TILE)) + 1.0f;
+                const float fx0 = fminf(fmaxf(fmaxf(rx0, gx0), -1.0f), TX + 1.0f);
+                const float fx1 = fminf(fmaxf(fminf(rx1, gx1), -1.0f), TX + 1.0f);
+                const float fy0 = fminf(fmaxf(fmaxf(ry0, gy0), -1.0f), TY + 1.0f);
+                const float fy1 = fminf(fmaxf(fminf(ry1, gy1), -1.0f), TY + 1.0f);
                 const int bx0 = min(max((int)fx0, 0), TX), bx1 = min(max((int)fx1, 0), TX);
                 const int by0 = min(max((int)fy0, 0), TY), by1 = min(max((int)fy1, 0), TY);
                 if (bx1 > bx0 && by1 > by0 && rect_hits(rows + v * per_view, W32, bx0, by0, bx1, by1))
