@@ -123,10 +123,10 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2506_21117_b200.dist import allreduce_rows, shard_views
     sc = synth.make_scene(args.config)
     V = len(sc.cameras)
-    shards = np.array_split(np.arange(V), world)
-    my_views = [int(v) for v in shards[rank]]
+    my_views = shard_views(V, world, rank)
     cams = [sc.cameras[v] for v in my_views]
     W, H = sc.width, sc.height
     params = GaussianParams.from_scene(sc, device=f"cuda:{local}")
@@ -136,17 +136,10 @@ def run_ours(args):
     tg = tg_host.to(f"cuda:{local}")
     stream = torch.cuda.current_stream()
 
-    def allreduce(grad, loss):
-        if world > 1:
-            flat = torch.cat([grad.reshape(-1), loss])
-            dist.all_reduce(flat)
-            grad.copy_(flat[:-1].view_as(grad))
-            loss.copy_(flat[-1:])
-
     def step():
         res = opt.forward(cams, tg, n_views_total=V, all_tiles=args.all_tiles)
         grad = opt.backward()
-        allreduce(grad, res.loss)
+        allreduce_rows(grad, res.loss)          # the step's only exchange (N > 1): one NCCL all-reduce
         opt.adam(grad)
         return res.loss
 
