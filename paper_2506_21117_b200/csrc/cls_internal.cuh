@@ -68,10 +68,10 @@ struct Scratch {
     int4 *view_bbox;        // [V] tile bbox of the active tiles
     int *diff;              // [V][(TY+1)(TX+1)]  corner differences of record rects
     // records
-    float4 *rec_xy;         // (u_hi, u_lo, v_hi, v_lo)
-    float4 *rec_co;         // (+-a_p [sign: pivot y], beta_hi, gamma, opacity)  LDL^T conic, see power_ldl
-    float4 *rec_rgb;        // (r, g, b, beta_lo)
-    int *rec_ord;           // active ordinal or -1
+    float4 *rec_xy;         // (u_hi, u_lo, v_hi, v_lo)  2D mean as fp32 hi/lo pairs (H1)
+    float4 *rec_co;         // (a1, a2, b1, b2)  scaled LDL^T exponent coefficients, see raster_q
+    float4 *rec_rgb;        // (r, g, b, opacity)
+    float2 *rec_aux;        // (qcut' = kappa (2 ln(255 o)(1 + 1e-6) + 2e-3) rounded up, active ordinal bits or -1)
     int2 *rec_rect;         // (x0 | y0 << 16, x1 | y1 << 16)
     int2 *rec_meta;         // (gid, view | active << 31)
     unsigned *rec_depth;    // fp32 bits of the depth key
@@ -228,24 +228,29 @@ __device__ __forceinline__ int sat_count(const int *S, int TXp1, int x0, int y0,
 }
 
 // ---------------------------------------------------------------------------
-// Per-pixel exponent of one staged Gaussian, in a cancellation-free form.
-// The conic form a dx^2 + 2 b dx dy + c dy^2 (3DGS: p = -(a dx^2 + c dy^2)/2 - b dx dy) loses
-// all precision in fp32 for large, elongated splats (terms ~1e4 px^2, result ~5).  With the
-// pivot on the larger diagonal entry (a >= c: pivot x) it is written as an LDL^T sum of two
-// non-negative terms:  a dx^2 + 2 b dx dy + c dy^2 = a_p s^2 + gamma t^2,
-//   pivot x: s = dx + beta dy, t = dy, a_p = a, beta = b/a (|beta| <= 1), gamma = 1/Sigma'_yy
-//   pivot y: s = dy + beta dx, t = dx, a_p = c, beta = b/c,            gamma = 1/Sigma'_xx
-// s0, t0 (the tile-origin values) are formed in fp64 at staging; per pixel only the small
-// offsets (|px + beta py| <= 30) are subtracted in fp32.  Forward and backward call this
-// same function, with _rn intrinsics, so they take identical discrete decisions.
+// Per-pixel exponent of one Gaussian, in a cancellation-free scaled LDL^T form (reading R29).
+// The conic form q = a dx^2 + 2 b dx dy + c dy^2 (3DGS: alpha = o exp(-q/2)) loses all
+// precision in fp32 for large, elongated splats (terms ~1e4 px^2, result ~5).  With the pivot
+// on the larger diagonal entry it is a sum of two squares,
+//   pivot x (a >= c): q = a (dx + beta dy)^2 + gamma dy^2,  beta = b/a, gamma = 1/Sigma'_yy
+//   pivot y (c >  a): q = c (dy + beta dx)^2 + gamma dx^2,  beta = b/c, gamma = 1/Sigma'_xx
+// and with kappa = log2(e)/2 folded in, kappa q = s'^2 + t'^2 with s', t' LINEAR in (dx, dy):
+//   s' = a1 dx + a2 dy,  t' = b1 dx + b2 dy        (pivot x: a1 = sqrt(kappa a), a2 = a1 beta,
+//   b1 = 0, b2 = sqrt(kappa gamma); pivot y: a1 = sqrt(kappa c) beta, a2 = sqrt(kappa c),
+//   b1 = sqrt(kappa gamma), b2 = 0), so exp(-q/2) = 2^-(s'^2 + t'^2).
+// The tile-origin values S0 = a1 dx0 + a2 dy0, T0 = b1 dx0 + b2 dy0 (dx0 = u - 16 tx) are formed
+// in fp64 once per (tile, Gaussian) at staging; per pixel (x, y) of the tile only
+// s' = S0 - a1 x - a2 y, t' = T0 - b1 x - b2 y run in fp32.  Forward and backward evaluate
+// exactly these operations (raster_q), so they take identical discrete decisions.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ float power_ldl(float s0, float t0, float beta, float ap, float gam, float px, float py,
-                                           float &s, float &t)
+#define CLS_KAPPA 0.72134752044448170368   // log2(e) / 2
+
+// kappa q for pixel row y given the per-(thread, Gaussian) column terms sx = S0 - a1 x, tx = T0 - b1 x
+__device__ __forceinline__ float raster_q(float sx, float tx, float a2, float b2, float fy, float &s, float &t)
 {
-    s = __fsub_rn(s0, __fmaf_rn(beta, py, px));
-    t = __fsub_rn(t0, py);
-    const float q = __fmaf_rn(ap, __fmul_rn(s, s), __fmul_rn(gam, __fmul_rn(t, t)));
-    return __fmul_rn(-0.5f, q);
+    s = __fmaf_rn(-a2, fy, sx);
+    t = __fmaf_rn(-b2, fy, tx);
+    return __fmaf_rn(s, s, __fmul_rn(t, t));
 }
 
 // SH basis (3DGS order and signs, R15), fp32

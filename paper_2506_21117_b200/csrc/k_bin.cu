@@ -185,21 +185,21 @@ __device__ __forceinline__ EmitRec load_rec(const Scratch &s, int r)
     const int2 meta = s.rec_meta[r];
     const float4 xy = s.rec_xy[r];
     const float4 co = s.rec_co[r];
-    const float4 rgb = s.rec_rgb[r];
     q.view = meta.y & 0x7fffffff;
     q.w = ((unsigned long long)s.rec_depth[r] << 32) | ((unsigned)r | ((unsigned)meta.y & 0x80000000u));
     q.x0 = rc.x & 0xffff; q.y0 = rc.x >> 16; q.x1 = rc.y & 0xffff; q.y1 = rc.y >> 16;
     q.u = (double)xy.x + (double)xy.y;
     q.v = (double)xy.z + (double)xy.w;
-    const double ap = fabs((double)co.x), beta = (double)co.y + (double)rgb.w, gam = co.z;
-    // LDL^T -> conic: pivot x: a = ap, b = ap beta, c = ap beta^2 + gamma (pivot y: a <-> c)
-    const double pa = ap, pb = ap * beta, pc = ap * beta * beta + gam;
-    if (co.x < 0.f) { q.a = pc; q.b = pb; q.c = pa; }
-    else { q.a = pa; q.b = pb; q.c = pc; }
+    // the raster's exponent kappa q = (a1 dx + a2 dy)^2 + (b1 dx + b2 dy)^2 (raster_q) as a conic
+    const double a1 = co.x, a2 = co.y, b1 = co.z, b2 = co.w;
+    q.a = a1 * a1 + b1 * b1;
+    q.b = a1 * a2 + b1 * b2;
+    q.c = a2 * a2 + b2 * b2;
     q.ba = q.b / q.a;
     q.bc = q.b / q.c;
-    // alpha >= 1/255  <=>  q <= 2 ln(255 o); margin covers the fp32 per-pixel evaluation
-    q.qcut = co.w > 0.f ? 2.0 * log(255.0 * (double)co.w) * (1.0 + 1e-6) + 2e-3 : -1.0;
+    // the raster composites only where kappa q <= qcut' (its pre-exponential test); + 1e-4 covers the
+    // fp32 evaluation of s', t' in the raster (<= 1e-5 absolute in kappa q)
+    q.qcut = (double)s.rec_aux[r].x + 1e-4;
     return q;
 }
 

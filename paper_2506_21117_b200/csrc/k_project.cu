@@ -245,19 +245,23 @@ k_project_exact(const float4 *__restrict__ mean_op, const float4 *__restrict__ q
         // ---- record ----
         const float uh = __double2float_rn(p.u), vh = __double2float_rn(p.v);
         s.rec_xy[slot] = make_float4(uh, __double2float_rn(p.u - (double)uh), vh, __double2float_rn(p.v - (double)vh));
-        const float o = (float)(1.0 / (1.0 + exp(-(double)mo.w)));
-        // LDL^T form of the conic (see power_ldl): pivot on the larger diagonal entry.
-        // conic a = C/det, b = -B/det, c = A/det  =>  a >= c  <=>  C >= A
-        const bool piv_y = p.A > p.C;
-        const double ap = piv_y ? p.cc : p.ca;
-        const double beta = piv_y ? (-p.B / p.A) : (-p.B / p.C);
-        const double gam = piv_y ? (1.0 / p.A) : (1.0 / p.C);
-        const float bh = __double2float_rn(beta);
-        const float apf = __double2float_rn(ap);
-        s.rec_co[slot] = make_float4(piv_y ? -apf : apf, bh, __double2float_rn(gam), o);
-        s.rec_rgb[slot] = make_float4(fmaxf(col[0], 0.0f), fmaxf(col[1], 0.0f), fmaxf(col[2], 0.0f),
-                                      __double2float_rn(beta - (double)bh));
-        s.rec_ord[slot] = ordi;
+        const double o64 = 1.0 / (1.0 + exp(-(double)mo.w));
+        // scaled LDL^T coefficients of the exponent (raster_q, reading R29): pivot on the larger
+        // diagonal conic entry; conic a = C/det >= c = A/det  <=>  C >= A
+        double a1, a2, b1, b2;
+        if (p.C >= p.A) {   // pivot x: beta = b/a = -B/C, gamma = 1/C
+            const double k = sqrt(CLS_KAPPA * p.ca);
+            a1 = k; a2 = k * (-p.B / p.C); b1 = 0.0; b2 = sqrt(CLS_KAPPA / p.C);
+        } else {            // pivot y: beta = b/c = -B/A, gamma = 1/A
+            const double k = sqrt(CLS_KAPPA * p.cc);
+            a1 = k * (-p.B / p.A); a2 = k; b1 = sqrt(CLS_KAPPA / p.A); b2 = 0.0;
+        }
+        s.rec_co[slot] = make_float4(__double2float_rn(a1), __double2float_rn(a2), __double2float_rn(b1),
+                                     __double2float_rn(b2));
+        s.rec_rgb[slot] = make_float4(fmaxf(col[0], 0.0f), fmaxf(col[1], 0.0f), fmaxf(col[2], 0.0f), (float)o64);
+        // pre-exponential test threshold: alpha >= 1/255 needs q <= 2 ln(255 o); margin covers fp32
+        const double qc = CLS_KAPPA * (2.0 * log(255.0 * o64) * (1.0 + 1e-6) + 2e-3);
+        s.rec_aux[slot] = make_float2(__double2float_ru(qc), __int_as_float(ordi));
         s.rec_rect[slot] = make_int2(p.x0 | (p.y0 << 16), p.x1 | (p.y1 << 16));
         s.rec_meta[slot] = make_int2(i, v | (ordi >= 0 ? (int)0x80000000u : 0));
         s.rec_depth[slot] = __float_as_uint(__double2float_rn(p.tz));

@@ -4,27 +4,29 @@
 // PAPER.md Supp. L540 (modification 2): "During forward and backward rendering, we
 // utilize the generated mask to terminate threads associated with tiles marked as
 // false".  On B200 the false tiles are never launched at all: persistent CTAs (one
-// 16x16-pixel tile per 256-thread CTA at a time) pull only the ACTIVE (view, tile) work
-// items from a device queue.  Each CTA stages its tile's depth-ordered Gaussians in
-// shared memory 256 at a time, converting the 2D mean to tile-local fp32 once per
-// (tile, Gaussian) from the record's hi/lo pair (H1), and composites front to
-// back (R1-R3).  Frozen Gaussians are composited but never differentiated: the
+// 16x16-pixel tile per 64-thread CTA at a time, four pixels per thread) pull only the
+// ACTIVE (view, tile) work items from a device queue.  Each CTA stages its tile's
+// depth-ordered Gaussians in shared memory 128 at a time, forming the exponent's
+// tile-origin terms in fp64 once per (tile, Gaussian) from the record's hi/lo 2D mean
+// (H1, reading R29), and composites front to back (R1-R3) with ~20 fp32
+// instructions per (pixel, Gaussian).  Frozen Gaussians are composited but never differentiated: the
 // backward walk updates T and the colour-behind sum for them, and only ACTIVE entries
 // run the gradient math and the warp-reduced atomics.
 #include "kernels.h"
 
 namespace cls {
 
-#define RT_THREADS 128   // one 16x16 tile per CTA, two pixels per thread: (lx, ly) and (lx, ly + 8)
-#define RT_BATCH 256     // Gaussians staged per batch (two per thread)
+#define RT_THREADS 64    // one 16x16 tile per CTA; thread (lx, ly) owns the 4 pixels (lx, ly + 4k), k = 0..3
+#define RT_PX 4
+#define RT_BATCH 128     // Gaussians staged per batch (two per thread)
 
-// One staged Gaussian of a tile (48 B of shared memory):
-//   sa = (s0, t0, beta, +-a_p)  LDL^T exponent terms at the tile origin (power_ldl); sign of a_p = pivot y
-//   sb = (gamma, opacity, r, g)
-//   sc = (b, qcut, active ordinal bits, 0)
-// s0, t0 are formed in fp64 from the record's hi/lo 2D mean and beta (H1), once
-// per (tile, Gaussian) and amortised over the tile's 256 pixels.  qcut = 2 ln(255 o) + 1e-3:
-// q > qcut implies alpha < 1/255, so such pixels skip the exponential; the alpha test itself
+// One staged Gaussian of a tile (48 B of shared memory), raster_q terms:
+//   sa = (S0, a1, a2, T0)   S0 = a1 dx0 + a2 dy0, T0 = b1 dx0 + b2 dy0 at the tile origin (fp64 -> fp32)
+//   sb = (b1, b2, o, qcut')
+//   sc = (r, g, b, active ordinal bits or -1)
+// S0, T0 are formed in fp64 from the record's hi/lo 2D mean (H1) once per
+// (tile, Gaussian) and amortised over the tile's 256 pixels.  qcut' bounds kappa q from above
+// wherever alpha >= 1/255, so pixels beyond it skip the exponential; the alpha test itself
 // still takes the decision (the pre-test only removes work, never changes a result).
 __device__ __forceinline__ void stage(const Scratch &s, unsigned val, int tx, int ty, float4 &sa, float4 &sb,
                                       float4 &sc)
@@ -33,34 +35,21 @@ __device__ __forceinline__ void stage(const Scratch &s, unsigned val, int tx, in
     const float4 xy = s.rec_xy[rid];
     const float4 co = s.rec_co[rid];
     const float4 rgb = s.rec_rgb[rid];
-    const int ord = s.rec_ord[rid];
+    const float2 ax = s.rec_aux[rid];
     const double dx0 = ((double)xy.x - (double)(CLS_TILE * tx)) + (double)xy.y;
     const double dy0 = ((double)xy.z - (double)(CLS_TILE * ty)) + (double)xy.w;
-    const double beta = (double)co.y + (double)rgb.w;
-    const bool piv_y = co.x < 0.f;
-    const double s0 = piv_y ? fma(beta, dx0, dy0) : fma(beta, dy0, dx0);
-    const double t0 = piv_y ? dx0 : dy0;
-    const float qcut = co.w > 0.f ? __double2float_ru(2.0 * log(255.0 * (double)co.w) + 1e-3) : -1.0f;
-    sa = make_float4(__double2float_rn(s0), __double2float_rn(t0), co.y, co.x);
-    sb = make_float4(co.z, co.w, rgb.x, rgb.y);
-    sc = make_float4(rgb.z, qcut, __int_as_float(ord), 0.f);
+    const double S0 = fma((double)co.y, dy0, (double)co.x * dx0);
+    const double T0 = fma((double)co.w, dy0, (double)co.z * dx0);
+    sa = make_float4(__double2float_rn(S0), co.x, co.y, __double2float_rn(T0));
+    sb = make_float4(co.z, co.w, rgb.w, ax.x);
+    sc = make_float4(rgb.x, rgb.y, rgb.z, ax.y);
 }
 
-// q = a_p s^2 + gamma t^2 for pixel (lx, ly) of the tile (pinned op order; see power_ldl)
-__device__ __forceinline__ float quad_at(const float4 &A, float gam, float flx, float fly, float &ss, float &tt)
-{
-    const bool py = A.w < 0.f;
-    const float px = py ? fly : flx, pyv = py ? flx : fly;
-    ss = __fsub_rn(A.x, __fmaf_rn(A.z, pyv, px));
-    tt = __fsub_rn(A.y, pyv);
-    return __fmaf_rn(fabsf(A.w), __fmul_rn(ss, ss), __fmul_rn(gam, __fmul_rn(tt, tt)));
-}
-
-// alpha of a (pixel, Gaussian) with q <= qcut: min(0.99, o exp(-q/2)) via ex2.approx
-__device__ __forceinline__ float alpha_of(float q, float o, float &G)
+// alpha = min(0.99, o 2^-q') of a (pixel, Gaussian) with q' <= qcut'; G = 2^-q' = exp(-q/2)
+__device__ __forceinline__ float alpha_of(float qk, float o, float &G)
 {
     float e;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(__fmul_rn(q, -0.72134752044448170368f)));   // -0.5 log2(e)
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-qk));
     G = e;
     return fminf(0.99f, __fmul_rn(o, e));
 }
@@ -80,37 +69,11 @@ __device__ __forceinline__ float block_sum(float v, float *red)
     return r;
 }
 
-struct PixF {   // forward state of one pixel
-    float T, C0, C1, C2;
-    int last, nev;
-    bool done;
-};
-
-__device__ __forceinline__ void composite(PixF &P, const float4 &A, const float4 &B, const float4 &Cc, float flx,
-                                          float fly, int pos)
-{
-    ++P.nev;
-    float ss, tt;
-    const float q = quad_at(A, B.x, flx, fly, ss, tt);
-    if (q > Cc.y) return;                          // alpha < 1/255 for sure
-    float G;
-    const float alpha = alpha_of(q, B.y, G);
-    if (alpha < (1.0f / 255.0f)) return;
-    const float Tn = __fmul_rn(P.T, __fsub_rn(1.0f, alpha));
-    if (Tn < 1e-4f) {
-        P.done = true;
-        return;
-    }
-    const float w = alpha * P.T;
-    P.C0 += w * B.z;
-    P.C1 += w * B.w;
-    P.C2 += w * Cc.x;
-    P.T = Tn;
-    P.last = pos;
-}
-
 // ---------------------------------------------------------------------------
-// forward
+// forward.  Per pixel (R1-R3): alpha = min(0.99, o e^p); skip alpha < 1/255; stop (that Gaussian
+// not composited) when T (1 - alpha) < 1e-4.  A terminated pixel keeps T < 0 (|T| = T_final):
+// every later T (1 - alpha) is negative, so it re-takes the termination branch and never
+// composites again -- no per-pixel "done" flags, the warp stays converged.
 // ---------------------------------------------------------------------------
 template <bool TARGET, bool IMAGE>
 __global__ void __launch_bounds__(RT_THREADS)
@@ -125,9 +88,10 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
     if (s.cnt->overflow) return;
     const int n_items = s.cnt->n_items;
     const int tid = threadIdx.x;
-    const int lx = tid & 15, ly = tid >> 4;   // second pixel at ly + 8
-    const float flx = (float)lx, fly0 = (float)ly, fly1 = (float)(ly + 8);
+    const int lx = tid & 15, ly = tid >> 4;   // pixels (lx, ly + 4k)
+    const float flx = (float)lx;
     const int W = cams.W, H = cams.H, TX = cams.TX, T = cams.T;
+    unsigned long long evals = 0;
     while (true) {
         if (tid == 0) s_item = atomicAdd(&s.cnt->fwd_work, 1);
         __syncthreads();
@@ -139,35 +103,70 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         const int tx = t % TX, ty = t / TX;
         const int n = s.tile_cnt[e];
         const int off = s.tile_off[e];
-        const int x = tx * CLS_TILE + lx, y0 = ty * CLS_TILE + ly, y1 = y0 + 8;
-        const bool in0 = x < W && y0 < H, in1 = x < W && y1 < H;
-        PixF P0{1.f, 0.f, 0.f, 0.f, -1, 0, !in0}, P1{1.f, 0.f, 0.f, 0.f, -1, 0, !in1};
+        const int x = tx * CLS_TILE + lx;
+        float Tr[RT_PX], C0[RT_PX], C1[RT_PX], C2[RT_PX];
+        int last[RT_PX], term[RT_PX];
+#pragma unroll
+        for (int k = 0; k < RT_PX; k++) {
+            const bool in = x < W && ty * CLS_TILE + ly + 4 * k < H;
+            Tr[k] = in ? 1.f : -1.f;   // out-of-image pixels start terminated
+            C0[k] = C1[k] = C2[k] = 0.f;
+            last[k] = -1;
+            term[k] = in ? n - 1 : -1;   // out-of-image pixels evaluate nothing
+        }
         for (int b0 = 0; b0 < n; b0 += RT_BATCH) {
-            if (__syncthreads_count(P0.done && P1.done) == RT_THREADS) break;
+            const bool live = Tr[0] > 0.f || Tr[1] > 0.f || Tr[2] > 0.f || Tr[3] > 0.f;
+            if (__syncthreads_count(live) == 0) break;
             for (int j = tid; j < RT_BATCH && b0 + j < n; j += RT_THREADS)
                 stage(s, s.tile_list[off + b0 + j], tx, ty, sa[j], sb[j], sc[j]);
             __syncthreads();
             const int cnt = min(RT_BATCH, n - b0);
             for (int k = 0; k < cnt; k++) {
-                if (P0.done && P1.done) break;
+                // warp-level exit once all its pixels terminated (checked every 4 entries)
+                if ((k & 3) == 0 &&
+                    !__any_sync(0xffffffffu, fmaxf(fmaxf(Tr[0], Tr[1]), fmaxf(Tr[2], Tr[3])) > 0.f))
+                    break;
                 const float4 A = sa[k], B = sb[k], Cc = sc[k];
-                if (!P0.done) composite(P0, A, B, Cc, flx, fly0, b0 + k);
-                if (!P1.done) composite(P1, A, B, Cc, flx, fly1, b0 + k);
+                const float sx = __fmaf_rn(-A.y, flx, A.x), txx = __fmaf_rn(-B.x, flx, A.w);
+                const int pos = b0 + k;
+#pragma unroll
+                for (int p = 0; p < RT_PX; p++) {
+                    // branch-free: the exponential is cheaper than a branch around it; beyond qcut'
+                    // the alpha test rejects anyway (ex2 -> 0), so results equal the pre-tested form.
+                    // A skipped entry (alpha < 1/255) gets alpha = 0, so Tn = T exactly; then
+                    // Tn < 1e-4 happens exactly at the terminating entry or on an already
+                    // terminated pixel (T < 0).
+                    float ss, tt, G;
+                    const float qk = raster_q(sx, txx, A.z, B.y, (float)(ly + 4 * p), ss, tt);
+                    float alpha = alpha_of(qk, B.z, G);
+                    const bool hit = alpha >= (1.0f / 255.0f);
+                    alpha = hit ? alpha : 0.f;
+                    const float Tn = __fmul_rn(Tr[p], __fsub_rn(1.0f, alpha));
+                    const bool ok = Tn >= 1e-4f;
+                    const float w = ok ? alpha * Tr[p] : 0.f;
+                    C0[p] = __fmaf_rn(w, Cc.x, C0[p]);
+                    C1[p] = __fmaf_rn(w, Cc.y, C1[p]);
+                    C2[p] = __fmaf_rn(w, Cc.z, C2[p]);
+                    if (ok && hit) last[p] = pos;
+                    if (!ok) term[p] = min(term[p], pos);   // first termination (evaluation count)
+                    Tr[p] = ok ? Tn : -fabsf(Tr[p]);
+                }
             }
         }
         float l1 = 0.f;
 #pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const PixF &P = h ? P1 : P0;
-            const int yy = h ? y1 : y0;
-            const bool in = h ? in1 : in0;
-            const int pl = tid + h * RT_THREADS;          // pixel slot (ly + 8h) * 16 + lx
+        for (int p = 0; p < RT_PX; p++) {
+            const int yy = ty * CLS_TILE + ly + 4 * p;
+            const bool in = x < W && yy < H;
+            const float Tf = fabsf(Tr[p]);
+            evals += (unsigned long long)(term[p] + 1);   // entries 0..term evaluated for this pixel
+            const int pl = tid + p * RT_THREADS;          // pixel slot (ly + 4p) * 16 + lx
             const size_t px = (size_t)item * CLS_BLOCK_PIX + pl;
-            s.px_T[px] = P.T;
-            s.px_last[px] = P.last;
+            s.px_T[px] = Tf;
+            s.px_last[px] = last[p];
             float *dl = s.px_dl + (size_t)item * 3 * CLS_BLOCK_PIX + pl;
             if (in) {
-                const float o0 = P.C0 + P.T * bg.x, o1 = P.C1 + P.T * bg.y, o2 = P.C2 + P.T * bg.z;
+                const float o0 = C0[p] + Tf * bg.x, o1 = C1[p] + Tf * bg.y, o2 = C2[p] + Tf * bg.z;
                 const size_t HW = (size_t)H * W;
                 const size_t pix = (size_t)v * 3 * HW + (size_t)yy * W + x;
                 if (IMAGE) {
@@ -190,15 +189,15 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
             const float tot = block_sum(l1, red);
             if (tid == 0) s.item_loss[item] = tot;
         }
-        const float evs = block_sum((float)(P0.nev + P1.nev), red);   // exact: < 2^24 per tile
-        if (tid == 0) atomicAdd(&s.cnt->fwd_evals, (unsigned long long)evs);
     }
+    for (int o = 16; o > 0; o >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, o);
+    if ((tid & 31) == 0 && evals) atomicAdd(&s.cnt->fwd_evals, evals);
 }
 
 void launch_fwd(const StepDims &d, const CamSet &cams, const Scratch &s, const float *targets, float *images,
                 float loss_scale, float3 bg, cudaStream_t st)
 {
-    const int grid = 148 * 12;
+    const int grid = 148 * 16;
     if (targets && images) k_fwd<true, true><<<grid, RT_THREADS, 0, st>>>(cams, s, targets, images, loss_scale, bg);
     else if (targets) k_fwd<true, false><<<grid, RT_THREADS, 0, st>>>(cams, s, targets, images, loss_scale, bg);
     else if (images) k_fwd<false, true><<<grid, RT_THREADS, 0, st>>>(cams, s, targets, images, loss_scale, bg);
@@ -261,57 +260,15 @@ void launch_loss(const Scratch &s, float loss_scale, float *loss, cudaStream_t s
 //   dL/dalpha = sum_ch g_ch (c_k,ch T_k - (S_ch + T_final bg_ch) / (1 - alpha_k))
 //   if o G < 0.99 (R4): dL/do = G dL/dalpha, dL/dp = alpha dL/dalpha, else 0
 //   dp/du = -(a dx + b dy), dp/dv = -(b dx + c dy), dp/da = -dx^2/2, dp/db = -dx dy, dp/dc = -dy^2/2
-//   (in LDL^T terms: dp/d(pivot coord) = -a_p s, dp/d(other) = -(b s + gamma t), b = beta a_p)
-// summed over the thread's two pixels and the warp (shuffles), then added into
-// grad2d[v][ordinal] with float4 atomics.
+// with dx = u - x, dy = v - y and the conic (a, b, c) = (a1^2 + b1^2, a1 a2 + b1 b2, a2^2 + b2^2) / kappa
+// of the raster's own exponent; summed over the thread's 4 pixels and the warp (shuffles), then
+// added into grad2d[v][ordinal] with float4 atomics.  Frozen entries only update T and S.
+// The alpha of every (pixel, entry) is recomputed with exactly the forward's operations.
 // ---------------------------------------------------------------------------
 struct PixB {   // backward state of one pixel
     float T, Tf, S0, S1, S2, g0, g1, g2;
     int last;
-    bool in;
 };
-
-__device__ __forceinline__ bool walk(PixB &P, const float4 &A, const float4 &B, const float4 &Cc, float flx, float fly,
-                                     int jj, bool active, float bgx, float bgy, float bgz, float r[9])
-{
-    if (!P.in || jj > P.last) return false;
-    float ss, tt;
-    const float q = quad_at(A, B.x, flx, fly, ss, tt);
-    if (q > Cc.y) return false;
-    float G;
-    const float alpha = alpha_of(q, B.y, G);
-    if (alpha < (1.0f / 255.0f)) return false;
-    const float omi = __fsub_rn(1.0f, alpha);
-    P.T = __fdiv_rn(P.T, omi);   // transmittance in front of entry jj
-    const float w = alpha * P.T;
-    if (active) {
-        const float inv = 1.0f / omi;
-        const float dLda = P.g0 * (B.z * P.T - (P.S0 + P.Tf * bgx) * inv) + P.g1 * (B.w * P.T - (P.S1 + P.Tf * bgy) * inv) +
-                           P.g2 * (Cc.x * P.T - (P.S2 + P.Tf * bgz) * inv);
-        r[6] += w * P.g0;
-        r[7] += w * P.g1;
-        r[8] += w * P.g2;
-        if (B.y * G < 0.99f) {
-            const float dLdp = alpha * dLda;
-            r[5] += G * dLda;
-            const bool pvy = A.w < 0.f;
-            const float ap = fabsf(A.w);
-            const float bq = A.z * ap;
-            const float gp = -ap * ss, go = -(bq * ss + B.x * tt);
-            const float dpiv = ss - A.z * tt;   // pivot-axis offset (dx for pivot x)
-            const float dx = pvy ? tt : dpiv, dy = pvy ? dpiv : tt;
-            r[0] += dLdp * (pvy ? go : gp);
-            r[1] += dLdp * (pvy ? gp : go);
-            r[2] += -0.5f * dLdp * dx * dx;
-            r[3] += -dLdp * dx * dy;
-            r[4] += -0.5f * dLdp * dy * dy;
-        }
-    }
-    P.S0 += B.z * w;
-    P.S1 += B.w * w;
-    P.S2 += Cc.x * w;
-    return true;
-}
 
 __global__ void __launch_bounds__(RT_THREADS)
 k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ dL_dimg, float3 bg)
@@ -319,14 +276,17 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
     __shared__ float4 sa[RT_BATCH];
     __shared__ float4 sb[RT_BATCH];
     __shared__ float4 sc[RT_BATCH];
+    __shared__ float2 sd[RT_BATCH];    // tile-local 2D mean (dx0, dy0) in fp32
     __shared__ int s_item, s_maxlast;
     if (s.cnt->overflow) return;
     const int n_items = s.cnt->n_items;
     const int A = s.cnt->A;
     const int tid = threadIdx.x, lane = tid & 31;
     const int lx = tid & 15, ly = tid >> 4;
-    const float flx = (float)lx, fly0 = (float)ly, fly1 = (float)(ly + 8);
+    const float flx = (float)lx;
     const int W = cams.W, H = cams.H, TX = cams.TX, T = cams.T;
+    const float ik = (float)(1.0 / CLS_KAPPA);
+    unsigned long long evals = 0;
     while (true) {
         if (tid == 0) {
             s_item = atomicAdd(&s.cnt->bwd_work, 1);
@@ -340,54 +300,97 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         const int tx = t % TX, ty = t / TX;
         const int off = s.tile_off[e];
         const int first = s.first_active[item];
-        const int x = tx * CLS_TILE + lx, y0 = ty * CLS_TILE + ly;
-        PixB P[2];
+        const int x = tx * CLS_TILE + lx;
+        PixB P[RT_PX];
+        int ml = -1;
 #pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const int yy = y0 + 8 * h;
-            const int pl = tid + h * RT_THREADS;
+        for (int p = 0; p < RT_PX; p++) {
+            const int yy = ty * CLS_TILE + ly + 4 * p;
+            const int pl = tid + p * RT_THREADS;
             const size_t px = (size_t)item * CLS_BLOCK_PIX + pl;
-            P[h].in = x < W && yy < H;
-            P[h].last = s.px_last[px];
-            P[h].Tf = s.px_T[px];
-            P[h].T = P[h].Tf;
-            P[h].S0 = P[h].S1 = P[h].S2 = 0.f;
-            P[h].g0 = P[h].g1 = P[h].g2 = 0.f;
-            if (P[h].in) {
+            const bool in = x < W && yy < H;
+            P[p].last = in ? s.px_last[px] : -1;
+            P[p].Tf = s.px_T[px];
+            P[p].T = P[p].Tf;
+            P[p].S0 = P[p].S1 = P[p].S2 = 0.f;
+            P[p].g0 = P[p].g1 = P[p].g2 = 0.f;
+            if (in) {
                 if (dL_dimg) {
                     const size_t HW = (size_t)H * W;
                     const size_t pix = (size_t)v * 3 * HW + (size_t)yy * W + x;
-                    P[h].g0 = dL_dimg[pix]; P[h].g1 = dL_dimg[pix + HW]; P[h].g2 = dL_dimg[pix + 2 * HW];
+                    P[p].g0 = dL_dimg[pix]; P[p].g1 = dL_dimg[pix + HW]; P[p].g2 = dL_dimg[pix + 2 * HW];
                 } else {
                     const float *dl = s.px_dl + (size_t)item * 3 * CLS_BLOCK_PIX + pl;
-                    P[h].g0 = dl[0]; P[h].g1 = dl[CLS_BLOCK_PIX]; P[h].g2 = dl[2 * CLS_BLOCK_PIX];
+                    P[p].g0 = dl[0]; P[p].g1 = dl[CLS_BLOCK_PIX]; P[p].g2 = dl[2 * CLS_BLOCK_PIX];
                 }
             }
+            ml = max(ml, P[p].last);
         }
-        const int ml = max(P[0].in ? P[0].last : -1, P[1].in ? P[1].last : -1);
         if (ml >= first) atomicMax(&s_maxlast, ml);
         __syncthreads();
         const int end = s_maxlast + 1;   // exclusive
         float4 *gbase = s.grad2d + (size_t)v * A * 3;
-        int nev = 0;
         for (int bend = end; bend > first; bend -= RT_BATCH) {
             const int bstart = max(bend - RT_BATCH, first);
             __syncthreads();
-            for (int j = tid; j < bend - bstart; j += RT_THREADS)
-                stage(s, s.tile_list[off + bstart + j], tx, ty, sa[j], sb[j], sc[j]);
+            for (int j = tid; j < bend - bstart; j += RT_THREADS) {
+                const unsigned val = s.tile_list[off + bstart + j];
+                stage(s, val, tx, ty, sa[j], sb[j], sc[j]);
+                const float4 xy = s.rec_xy[val & 0x7fffffffu];
+                sd[j] = make_float2(__double2float_rn(((double)xy.x - (double)(CLS_TILE * tx)) + (double)xy.y),
+                                    __double2float_rn(((double)xy.z - (double)(CLS_TILE * ty)) + (double)xy.w));
+            }
             __syncthreads();
             for (int k = bend - 1 - bstart; k >= 0; k--) {
                 const int jj = bstart + k;
                 const float4 Aa = sa[k], Bb = sb[k], Cc = sc[k];
-                const int ordk = __float_as_int(Cc.z);
+                const int ordk = __float_as_int(Cc.w);
                 const bool active = ordk >= 0;   // uniform over the CTA
+                const float sx = __fmaf_rn(-Aa.y, flx, Aa.x), txx = __fmaf_rn(-Bb.x, flx, Aa.w);
                 float r[9];
 #pragma unroll
                 for (int q = 0; q < 9; q++) r[q] = 0.f;
-                const bool on0 = walk(P[0], Aa, Bb, Cc, flx, fly0, jj, active, bg.x, bg.y, bg.z, r);
-                const bool on1 = walk(P[1], Aa, Bb, Cc, flx, fly1, jj, active, bg.x, bg.y, bg.z, r);
-                nev += (int)(P[0].in && jj <= P[0].last) + (int)(P[1].in && jj <= P[1].last);
-                if (active && __any_sync(0xffffffffu, on0 || on1)) {
+                bool any = false;
+#pragma unroll
+                for (int p = 0; p < RT_PX; p++) {
+                    if (jj > P[p].last) continue;
+                    ++evals;
+                    float ss, tt;
+                    const float qk = raster_q(sx, txx, Aa.z, Bb.y, (float)(ly + 4 * p), ss, tt);
+                    float G;   // same operations as the forward (no pre-test there either)
+                    const float alpha = alpha_of(qk, Bb.z, G);
+                    if (alpha < (1.0f / 255.0f)) continue;
+                    const float omi = __fsub_rn(1.0f, alpha);
+                    P[p].T = __fdiv_rn(P[p].T, omi);   // transmittance in front of entry jj
+                    const float w = alpha * P[p].T;
+                    if (active) {
+                        any = true;
+                        const float inv = 1.0f / omi;
+                        const float dLda = P[p].g0 * (Cc.x * P[p].T - (P[p].S0 + P[p].Tf * bg.x) * inv) +
+                                           P[p].g1 * (Cc.y * P[p].T - (P[p].S1 + P[p].Tf * bg.y) * inv) +
+                                           P[p].g2 * (Cc.z * P[p].T - (P[p].S2 + P[p].Tf * bg.z) * inv);
+                        r[6] += w * P[p].g0;
+                        r[7] += w * P[p].g1;
+                        r[8] += w * P[p].g2;
+                        if (Bb.z * G < 0.99f) {
+                            const float dLdp = alpha * dLda;
+                            r[5] += G * dLda;
+                            const float2 d0 = sd[k];
+                            const float dx = d0.x - flx, dy = d0.y - (float)(ly + 4 * p);
+                            const float ca = (Aa.y * Aa.y + Bb.x * Bb.x) * ik, cb = (Aa.y * Aa.z + Bb.x * Bb.y) * ik,
+                                        cc = (Aa.z * Aa.z + Bb.y * Bb.y) * ik;
+                            r[0] += -dLdp * (ca * dx + cb * dy);
+                            r[1] += -dLdp * (cb * dx + cc * dy);
+                            r[2] += -0.5f * dLdp * dx * dx;
+                            r[3] += -dLdp * dx * dy;
+                            r[4] += -0.5f * dLdp * dy * dy;
+                        }
+                    }
+                    P[p].S0 += Cc.x * w;
+                    P[p].S1 += Cc.y * w;
+                    P[p].S2 += Cc.z * w;
+                }
+                if (active && __any_sync(0xffffffffu, any)) {
 #pragma unroll
                     for (int q = 0; q < 9; q++) {
                         float a = r[q];
@@ -403,10 +406,10 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
                 }
             }
         }
-        for (int o = 16; o > 0; o >>= 1) nev += __shfl_xor_sync(0xffffffffu, nev, o);
-        if (lane == 0 && nev) atomicAdd(&s.cnt->bwd_evals, (unsigned long long)nev);
         __syncthreads();
     }
+    for (int o = 16; o > 0; o >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, o);
+    if (lane == 0 && evals) atomicAdd(&s.cnt->bwd_evals, evals);
 }
 
 __global__ void k_zero_grad2d(Scratch s, int V, long long cap)
@@ -431,7 +434,7 @@ void launch_bwd_raster(const StepDims &d, const Scratch &s, const float *dL_dima
 {
     CamSet cams;
     cams.n = d.V; cams.W = d.W; cams.H = d.H; cams.TX = d.TX; cams.TY = d.TY; cams.T = d.T;
-    k_bwd<<<148 * 12, RT_THREADS, 0, st>>>(cams, s, dL_dimages, bg);
+    k_bwd<<<148 * 16, RT_THREADS, 0, st>>>(cams, s, dL_dimages, bg);
     g_launches++;
 }
 
