@@ -17,11 +17,26 @@
 namespace cls {
 
 // ---- pass A: conservative fp32 test of every (Gaussian, view); survivors -> candidate list ----
-// The fp32 2D covariance bounds the exact radius within a relative 1e-3 + 1 px margin and the
-// fp32 centre within 2 px, so no pair the exact fp64 test keeps is ever rejected here.  The
-// active tiles of every view are held in shared memory as row bitmasks (persistent CTAs load
-// them once).  Candidates are appended Gaussian-major (one atomic per warp), so consecutive
-// candidates share a Gaussian and pass B re-reads its parameters from L1.
+// Two stages per warp (32 Gaussians, one per lane; their geometry is read from HBM once per
+// step, not once per view):
+//  stage 1, per (lane's Gaussian, view), lanes uniform in the view: near-plane cull and an
+//    ISOTROPIC bound of the kept footprint -- radius <= min(3 sqrt(lb) + 1, sqrt(qcut lb)) with
+//    lb = |J|_F^2 s_max^2 + 0.3 >= lambda_max(Sigma') -- tested against the view's active-tile row
+//    bitmasks (rects of at most 3 tile rows; taller ones pass on).  Survivors go to a per-warp queue in shared memory.
+//  stage 2, 32 queued (Gaussian, view) pairs at a time (full SIMT width): the fp32 EWA covariance,
+//    a conservative mirror of the exact rect n alpha-footprint, tested against the view's
+//    summed-area table of active tiles (O(1)).  Survivors are appended (one atomic per warp) to the candidates.
+// Every margin is conservative: no pair the exact fp64 test keeps is ever rejected here.
+#define PC_THREADS 256
+#define PC_WARPS (PC_THREADS / 32)
+#define PC_Q 64   // ring buffer of queued (Gaussian lane, view) pairs per warp
+
+struct CamSoA {   // camera fields in shared memory, [field][view]: lanes on different views hit different banks
+    float R[9][CLS_MAX_VIEWS], t[3][CLS_MAX_VIEWS];
+    float fx[CLS_MAX_VIEWS], fy[CLS_MAX_VIEWS], cx[CLS_MAX_VIEWS], cy[CLS_MAX_VIEWS];
+    float limx[CLS_MAX_VIEWS], limy[CLS_MAX_VIEWS];
+};
+
 __device__ __forceinline__ bool rect_hits(const unsigned *rm, int W32, int x0, int y0, int x1, int y1)
 {
     const int w0 = x0 >> 5, w1 = (x1 - 1) >> 5;
@@ -41,140 +56,213 @@ __device__ __forceinline__ bool rect_hits(const unsigned *rm, int W32, int x0, i
     return false;
 }
 
-__global__ void __launch_bounds__(256)
+// stage 2: fp32 EWA test of Gaussian gl of the warp's batch in view v
+__device__ __forceinline__ bool cand_exact32(const float (*gM)[32], const float (*gP)[32], int gl, int v,
+                                             const CamSoA &C, const int *__restrict__ sat, int TX, int TY)
+{
+    const float mx = gP[0][gl], my = gP[1][gl], mz = gP[2][gl], qcut = gP[3][gl];
+    const float tz = C.R[6][v] * mx + C.R[7][v] * my + C.R[8][v] * mz + C.t[2][v];
+    const float tx = C.R[0][v] * mx + C.R[1][v] * my + C.R[2][v] * mz + C.t[0][v];
+    const float ty = C.R[3][v] * mx + C.R[4][v] * my + C.R[5][v] * mz + C.t[1][v];
+    const float fx = C.fx[v], fy = C.fy[v], limx = C.limx[v], limy = C.limy[v];
+    const float iz = __frcp_rn(tz);
+    const float xz = fminf(fmaxf(tx * iz, -limx), limx), yz = fminf(fmaxf(ty * iz, -limy), limy);
+    const float u = fx * tx * iz + C.cx[v] - 0.5f;
+    const float vv = fy * ty * iz + C.cy[v] - 0.5f;
+    const float j00 = fx * iz, j02 = -fx * xz * iz, j11 = fy * iz, j12 = -fy * yz * iz;
+    float V0[3], V1[3];
+#pragma unroll
+    for (int b = 0; b < 3; b++) {
+        V0[b] = j00 * C.R[b][v] + j02 * C.R[6 + b][v];
+        V1[b] = j11 * C.R[3 + b][v] + j12 * C.R[6 + b][v];
+    }
+    float A0 = 0.f, A1 = 0.f, B0 = 0.f;
+#pragma unroll
+    for (int b = 0; b < 3; b++) {
+        const float u0 = V0[0] * gM[b][gl] + V0[1] * gM[3 + b][gl] + V0[2] * gM[6 + b][gl];
+        const float u1 = V1[0] * gM[b][gl] + V1[1] * gM[3 + b][gl] + V1[2] * gM[6 + b][gl];
+        A0 += u0 * u0;
+        A1 += u1 * u1;
+        B0 += u0 * u1;
+    }
+    const float A = A0 + 0.3f, Cc = A1 + 0.3f;
+    const float mid = 0.5f * (A + Cc);
+    // lambda_max via the cancellation-free form: mid^2 - det = ((A - C)/2)^2 + B^2
+    const float hd = 0.5f * (A - Cc);
+    const float lam = mid + __fsqrt_rn(fmaxf(0.1f, hd * hd + B0 * B0));
+    // conservative mirrors (fp32 error margins) of the exact 3-sigma rect (R7/R8:
+    // x0 = trunc((u - r)/16), x1 = trunc((u + r + 15)/16), r = ceil(3 sqrt(lambda))) and of
+    // the exact alpha-footprint tile range; the candidate rect is their intersection.
+    // margins: relative fp32 error of u, Sigma' grows like 1/t_z near the near plane
+    // (cancellation in t = R mu + t0 ~ 3e-6 absolute): 1e-3 relative + 0.5 px covers t_z >= 0.199
+    const float r32 = ceilf(3.0f * __fsqrt_rn(lam) * 1.001f + 0.01f);
+    const float em = 0.5f + 1e-3f * fabsf(u - C.cx[v]) + 1e-3f * fabsf(vv - C.cy[v]);
+    const float rx0 = floorf((u - r32 - em) * (1.0f / CLS_TILE));
+    const float rx1 = floorf((u + r32 + em + CLS_TILE - 1) * (1.0f / CLS_TILE));
+    const float ry0 = floorf((vv - r32 - em) * (1.0f / CLS_TILE));
+    const float ry1 = floorf((vv + r32 + em + CLS_TILE - 1) * (1.0f / CLS_TILE));
+    const float hx = __fsqrt_rn(fmaxf(qcut, 0.f) * A) * 1.001f + em;
+    const float hy = __fsqrt_rn(fmaxf(qcut, 0.f) * Cc) * 1.001f + em;
+    const float gx0 = floorf((u - hx - (CLS_TILE - 1)) * (1.0f / CLS_TILE)) + 1.0f;
+    const float gx1 = floorf((u + hx) * (1.0f / CLS_TILE)) + 1.0f;
+    const float gy0 = floorf((vv - hy - (CLS_TILE - 1)) * (1.0f / CLS_TILE)) + 1.0f;
+    const float gy1 = floorf((vv + hy) * (1.0f / CLS_TILE)) + 1.0f;
+    const float fx0 = fminf(fmaxf(fmaxf(rx0, gx0), -1.0f), TX + 1.0f);
+    const float fx1 = fminf(fmaxf(fminf(rx1, gx1), -1.0f), TX + 1.0f);
+    const float fy0 = fminf(fmaxf(fmaxf(ry0, gy0), -1.0f), TY + 1.0f);
+    const float fy1 = fminf(fmaxf(fminf(ry1, gy1), -1.0f), TY + 1.0f);
+    const int bx0 = min(max((int)fx0, 0), TX), bx1 = min(max((int)fx1, 0), TX);
+    const int by0 = min(max((int)fy0, 0), TY), by1 = min(max((int)fy1, 0), TY);
+    if (!(bx1 > bx0 && by1 > by0)) return false;
+    const int *S = sat + (size_t)v * (TY + 1) * (TX + 1);
+    return sat_count(S, TX + 1, bx0, by0, bx1, by1) > 0;
+}
+
+__device__ __forceinline__ float rcp_approx(float x)
+{
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+template <bool SMEM_ROWS>
+__global__ void __launch_bounds__(PC_THREADS)
 k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ quat,
-               const float4 *__restrict__ log_scale, int n, const __grid_constant__ CamSet cams, Scratch s,
-               bool use_smem)
+               const float4 *__restrict__ log_scale, int n, const __grid_constant__ CamSet cams, Scratch s)
 {
     extern __shared__ unsigned s_rows[];   // [V][TY][W32] active-tile row bitmasks (if they fit)
-    const int lane = threadIdx.x & 31;
-    const int W = cams.W, H = cams.H, TX = cams.TX, TY = cams.TY;
+    __shared__ CamSoA C;
+    __shared__ float gM[PC_WARPS][9][32];   // M = R(q^) diag(exp(l)) of the warp's 32 Gaussians
+    __shared__ float gP[PC_WARPS][4][32];   // (x, y, z, qcut)
+    __shared__ unsigned short q[PC_WARPS][PC_Q];   // queued (lane | view << 5)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int W = cams.W, H = cams.H, TX = cams.TX, TY = cams.TY, V = cams.n;
     const int W32 = (TX + 31) >> 5;
     const int per_view = TY * W32;
-    __shared__ float4 s_bbox[CLS_MAX_VIEWS];   // pixel bbox (x0, y0, x1, y1) of each view's active tiles
-    for (int k = threadIdx.x; k < cams.n; k += blockDim.x) {
-        const int4 b = s.view_bbox[k];
-        s_bbox[k] = b.z > b.x ? make_float4(CLS_TILE * b.x, CLS_TILE * b.y, CLS_TILE * b.z - 1, CLS_TILE * b.w - 1)
-                              : make_float4(1e30f, 1e30f, -1e30f, -1e30f);
+    for (int k = threadIdx.x; k < V; k += blockDim.x) {
+        const GCam &c = cams.c[k];
+        for (int f = 0; f < 9; f++) C.R[f][k] = c.R[f];
+        for (int f = 0; f < 3; f++) C.t[f][k] = c.t[f];
+        C.fx[k] = c.fx; C.fy[k] = c.fy; C.cx[k] = c.cx; C.cy[k] = c.cy;
+        C.limx[k] = 1.3f * (W / (2.0f * c.fx));
+        C.limy[k] = 1.3f * (H / (2.0f * c.fy));
     }
+    const unsigned *rows = SMEM_ROWS ? s_rows : s.rowmask;
+    if (SMEM_ROWS)
+        for (int k = threadIdx.x; k < V * per_view; k += blockDim.x) s_rows[k] = s.rowmask[k];
     __syncthreads();
-    const unsigned *rows = s.rowmask;
-    if (use_smem) {
-        for (int k = threadIdx.x; k < cams.n * per_view; k += blockDim.x) s_rows[k] = s.rowmask[k];
-        __syncthreads();
-        rows = s_rows;
-    }
-    for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
-        const int i = base + threadIdx.x;
+    unsigned short *qw = q[wid];
+    const int nwarps = gridDim.x * PC_WARPS;
+    for (int base = (blockIdx.x * PC_WARPS + wid) * 32; base < n; base += nwarps * 32) {
+        const int i = base + lane;
         const bool valid = i < n;
-        float4 mo = make_float4(0, 0, 0, 0), q = make_float4(1, 0, 0, 0), ls = make_float4(0, 0, 0, 0);
+        float4 mo = make_float4(0, 0, 0, 0), qq = make_float4(1, 0, 0, 0), ls = make_float4(0, 0, 0, 0);
         if (valid) {
             mo = __ldg(mean_op + i);
-            q = __ldg(quat + i);
+            qq = __ldg(quat + i);
             ls = __ldg(log_scale + i);
         }
         // M = R(q^) diag(exp(l)) in fp32, view independent
-        const float qn = rsqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
-        const float w = q.x * qn, x = q.y * qn, y = q.z * qn, z = q.w * qn;
+        const float qn = rsqrtf(qq.x * qq.x + qq.y * qq.y + qq.z * qq.z + qq.w * qq.w);
+        const float w = qq.x * qn, x = qq.y * qn, y = qq.z * qn, z = qq.w * qn;
         const float s0 = __expf(ls.x), s1 = __expf(ls.y), s2 = __expf(ls.z);
         const float smx = fmaxf(s0, fmaxf(s1, s2)) * 1.001f;
         const float smax2 = smx * smx;
-        const float M[9] = {(1.f - 2.f * (y * y + z * z)) * s0, 2.f * (x * y - w * z) * s1, 2.f * (x * z + w * y) * s2,
-                            2.f * (x * y + w * z) * s0, (1.f - 2.f * (x * x + z * z)) * s1, 2.f * (y * z - w * x) * s2,
-                            2.f * (x * z - w * y) * s0, 2.f * (y * z + w * x) * s1, (1.f - 2.f * (x * x + y * y)) * s2};
-        unsigned long long vmask = 0ull;
-        if (valid) {
-            // 2 ln(255 o) (+ margin): no pixel has alpha >= 1/255 beyond q > qcut
-            const float op = 1.0f / (1.0f + __expf(-mo.w));
-            const float qcut = 2.0f * __logf(255.0f * op) * 1.001f + 0.05f;
-            for (int v = 0; v < cams.n; v++) {
-                const GCam &c = cams.c[v];
-                const float tz = c.R[6] * mo.x + c.R[7] * mo.y + c.R[8] * mo.z + c.t[2];
-                if (tz < 0.199f || qcut < 0.0f) continue;   // exact culls t_z <= 0.2 (R5)
-                const float tx = c.R[0] * mo.x + c.R[1] * mo.y + c.R[2] * mo.z + c.t[0];
-                const float ty = c.R[3] * mo.x + c.R[4] * mo.y + c.R[5] * mo.z + c.t[1];
-                const float limx = 1.3f * (W / (2.0f * c.fx)), limy = 1.3f * (H / (2.0f * c.fy));
-                const float iz = __frcp_rn(tz);
-                const float xz = fminf(fmaxf(tx * iz, -limx), limx), yz = fminf(fmaxf(ty * iz, -limy), limy);
-                const float u = c.fx * tx * iz + c.cx - 0.5f;
-                const float vv = c.fy * ty * iz + c.cy - 0.5f;
-                {   // cheap screen vs the pixel bbox of the view's active tiles: radius <= 3 |J|_F s_max + margin
-                    const float jf2 = (c.fx * c.fx * (1.0f + xz * xz) + c.fy * c.fy * (1.0f + yz * yz)) * iz * iz;
-                    const float rc = 3.0f * __fsqrt_rn(jf2 * smax2 + 0.92f) * 1.001f + 34.0f;   // + tile rounding of the rect
-                    const float4 bb = s_bbox[v];
-                    if (u + rc < bb.x || u - rc > bb.z || vv + rc < bb.y || vv - rc > bb.w) continue;
-                }
-                const float j00 = c.fx * iz, j02 = -c.fx * xz * iz, j11 = c.fy * iz, j12 = -c.fy * yz * iz;
-                float A0 = 0.f, A1 = 0.f, B0 = 0.f;
-                float V0[3], V1[3];
+        gM[wid][0][lane] = (1.f - 2.f * (y * y + z * z)) * s0;
+        gM[wid][1][lane] = 2.f * (x * y - w * z) * s1;
+        gM[wid][2][lane] = 2.f * (x * z + w * y) * s2;
+        gM[wid][3][lane] = 2.f * (x * y + w * z) * s0;
+        gM[wid][4][lane] = (1.f - 2.f * (x * x + z * z)) * s1;
+        gM[wid][5][lane] = 2.f * (y * z - w * x) * s2;
+        gM[wid][6][lane] = 2.f * (x * z - w * y) * s0;
+        gM[wid][7][lane] = 2.f * (y * z + w * x) * s1;
+        gM[wid][8][lane] = (1.f - 2.f * (x * x + y * y)) * s2;
+        // 2 ln(255 o) (+ margin): no pixel has alpha >= 1/255 beyond q > qcut
+        const float op = 1.0f / (1.0f + __expf(-mo.w));
+        const float qcut = valid ? 2.0f * __logf(255.0f * op) * 1.001f + 0.05f : -1.0f;
+        gP[wid][0][lane] = mo.x; gP[wid][1][lane] = mo.y; gP[wid][2][lane] = mo.z; gP[wid][3][lane] = qcut;
+        // isotropic extent factor of the kept footprint: min(3 sqrt(lb) + 1, sqrt(qcut lb))
+        const float kq = sqrtf(fmaxf(qcut, 0.f)) * 1.002f;
+        __syncwarp();
+        int head = 0, tail = 0;   // ring buffer [head, tail) of queued pairs, warp-uniform
+        for (int v = 0; v <= V; v++) {
+            if (v < V) {
+                // ---- stage 1 (uniform view v; camera reads are smem broadcasts) ----
+                bool pass = false;
+                const float tz = C.R[6][v] * mo.x + C.R[7][v] * mo.y + C.R[8][v] * mo.z + C.t[2][v];
+                if (qcut >= 0.f && tz >= 0.199f) {   // exact culls t_z <= 0.2 (R5)
+                    const float tx = C.R[0][v] * mo.x + C.R[1][v] * mo.y + C.R[2][v] * mo.z + C.t[0][v];
+                    const float ty = C.R[3][v] * mo.x + C.R[4][v] * mo.y + C.R[5][v] * mo.z + C.t[1][v];
+                    const float iz = rcp_approx(tz);   // tz >= 0.199; the margins absorb the approximation
+                    const float xr = tx * iz, yr = ty * iz;
+                    const float u = C.fx[v] * xr + C.cx[v] - 0.5f, vv = C.fy[v] * yr + C.cy[v] - 0.5f;
+                    const float xz = fminf(fmaxf(xr, -C.limx[v]), C.limx[v]);
+                    const float yz = fminf(fmaxf(yr, -C.limy[v]), C.limy[v]);
+                    const float fx2 = C.fx[v] * C.fx[v], fy2 = C.fy[v] * C.fy[v];
+                    const float jf2 = (fx2 * (1.0f + xz * xz) + fy2 * (1.0f + yz * yz)) * iz * iz;
+                    const float lb = jf2 * smax2 * 1.002f + 0.301f;
+                    const float sl = lb * rsqrtf(lb) * 1.0001f;
+                    const float em = 0.5f + 1e-3f * fabsf(u - C.cx[v]) + 1e-3f * fabsf(vv - C.cy[v]);
+                    const float R = fminf(3.0f * sl * 1.001f + 1.01f, kq * sl) + em + 0.01f;
+                    // tiles holding a pixel within R of the centre (the exact rect n footprint lies inside)
+                    const float inv = 1.0f / CLS_TILE;
+                    const int tx0 = max((int)floorf((u - R) * inv), 0), tx1 = min((int)floorf((u + R) * inv) + 1, TX);
+                    const int ty0 = max((int)floorf((vv - R) * inv), 0), ty1 = min((int)floorf((vv + R) * inv) + 1, TY);
+                    // small rects (at most 3 rows, 2 bitmask words: the common case) test the row
+                    // bitmasks here, branch-free; larger ones pass on to stage 2's O(1) summed-area
+                    // table test, so no lane loops
+                    if (tx0 < tx1 && ty0 < ty1) {
+                        const int w0 = tx0 >> 5, w1 = (tx1 - 1) >> 5;
+                        if (ty1 - ty0 > 3 || w1 - w0 > 1) {
+                            pass = true;
+                        } else {
+                            const unsigned m0 = 0xffffffffu << (tx0 & 31);
+                            const unsigned m1 = 0xffffffffu >> (31 - ((tx1 - 1) & 31));
+                            const unsigned mA = w0 == w1 ? (m0 & m1) : m0, mB = w0 == w1 ? 0u : m1;
+                            const unsigned *rv = rows + v * per_view;
+                            unsigned acc = 0u;
 #pragma unroll
-                for (int b = 0; b < 3; b++) {
-                    V0[b] = j00 * c.R[b] + j02 * c.R[6 + b];
-                    V1[b] = j11 * c.R[3 + b] + j12 * c.R[6 + b];
+                            for (int r = 0; r < 3; r++) {
+                                const int y = min(ty0 + r, ty1 - 1);
+                                acc |= (rv[y * W32 + w0] & mA) | (rv[y * W32 + w1] & mB);
+                            }
+                            pass = acc != 0u;
+                        }
+                    }
                 }
-#pragma unroll
-                for (int b = 0; b < 3; b++) {
-                    const float u0 = V0[0] * M[b] + V0[1] * M[3 + b] + V0[2] * M[6 + b];
-                    const float u1 = V1[0] * M[b] + V1[1] * M[3 + b] + V1[2] * M[6 + b];
-                    A0 += u0 * u0;
-                    A1 += u1 * u1;
-                    B0 += u0 * u1;
+                const unsigned bal = __ballot_sync(0xffffffffu, pass);
+                if (pass) qw[(tail + __popc(bal & ((1u << lane) - 1u))) & (PC_Q - 1)] = (unsigned short)(lane | (v << 5));
+                tail += __popc(bal);
+                __syncwarp();
+            }
+            // ---- stage 2: full chunks of 32 (and the rest after the last view) ----
+            while (tail - head >= 32 || (v == V && tail > head)) {
+                const int cnt = min(32, tail - head);
+                bool keep = false;
+                int gi = 0, gv = 0;
+                if (lane < cnt) {
+                    const unsigned e = qw[(head + lane) & (PC_Q - 1)];
+                    const int gl = e & 31;
+                    gv = e >> 5;
+                    gi = base + gl;
+                    keep = cand_exact32(gM[wid], gP[wid], gl, gv, C, s.sat, TX, TY);
                 }
-                const float A = A0 + 0.3f, C = A1 + 0.3f;
-                const float mid = 0.5f * (A + C);
-                // lambda_max via the cancellation-free form: mid^2 - det = ((A - C)/2)^2 + B^2
-                const float hd = 0.5f * (A - C);
-                const float lam = mid + __fsqrt_rn(fmaxf(0.1f, hd * hd + B0 * B0));
-                // conservative mirrors (fp32 error margins) of the exact 3-sigma rect (R7/R8:
-                // x0 = trunc((u - r)/16), x1 = trunc((u + r + 15)/16), r = ceil(3 sqrt(lambda))) and of
-                // the exact alpha-footprint tile range; the candidate rect is their intersection
-                // margins: relative fp32 error of u, Sigma' grows like 1/t_z near the near plane
-                // (cancellation in t = R mu + t0 ~ 3e-6 absolute): 1e-3 relative + 0.5 px covers t_z >= 0.199
-                const float r32 = ceilf(3.0f * __fsqrt_rn(lam) * 1.001f + 0.01f);
-                const float em = 0.5f + 1e-3f * fabsf(u - c.cx) + 1e-3f * fabsf(vv - c.cy);
-                const float rx0 = floorf((u - r32 - em) * (1.0f / CLS_TILE));
-                const float rx1 = floorf((u + r32 + em + CLS_TILE - 1) * (1.0f / CLS_TILE));
-                const float ry0 = floorf((vv - r32 - em) * (1.0f / CLS_TILE));
-                const float ry1 = floorf((vv + r32 + em + CLS_TILE - 1) * (1.0f / CLS_TILE));
-                const float hx = __fsqrt_rn(fmaxf(qcut, 0.f) * A) * 1.001f + em;
-                const float hy = __fsqrt_rn(fmaxf(qcut, 0.f) * C) * 1.001f + em;
-                const float gx0 = floorf((u - hx - (CLS_TILE - 1)) * (1.0f / CLS_TILE)) + 1.0f;
-                const float gx1 = floorf((u + hx) * (1.0f / CLS_TILE)) + 1.0f;
-                const float gy0 = floorf((vv - hy - (CLS_TILE - 1)) * (1.0f / CLS_TILE)) + 1.0f;
-                const float gy1 = floorf((vv + hy) * (1.0f / CLS_TILE)) + 1.0f;
-                const float fx0 = fminf(fmaxf(fmaxf(rx0, gx0), -1.0f), TX + 1.0f);
-                const float fx1 = fminf(fmaxf(fminf(rx1, gx1), -1.0f), TX + 1.0f);
-                const float fy0 = fminf(fmaxf(fmaxf(ry0, gy0), -1.0f), TY + 1.0f);
-                const float fy1 = fminf(fmaxf(fminf(ry1, gy1), -1.0f), TY + 1.0f);
-                const int bx0 = min(max((int)fx0, 0), TX), bx1 = min(max((int)fx1, 0), TX);
-                const int by0 = min(max((int)fy0, 0), TY), by1 = min(max((int)fy1, 0), TY);
-                if (bx1 > bx0 && by1 > by0 && rect_hits(rows + v * per_view, W32, bx0, by0, bx1, by1))
-                    vmask |= 1ull << v;
+                head += cnt;
+                __syncwarp();
+                const unsigned bal = __ballot_sync(0xffffffffu, keep);
+                if (bal) {
+                    int wb = 0;
+                    if (lane == 0) wb = atomicAdd(&s.cnt->n_cand, __popc(bal));
+                    wb = __shfl_sync(0xffffffffu, wb, 0);
+                    if (keep) {
+                        const long long slot = (long long)wb + __popc(bal & ((1u << lane) - 1u));
+                        if (slot < s.max_cand) s.cand[slot] = make_int2(gi, gv);
+                        else atomicOr(&s.cnt->overflow, 1);
+                    }
+                }
             }
         }
-        // Gaussian-major append: lane order, then view order
-        const int cnt = __popcll(vmask);
-        int inc = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += t;
-        }
-        const int tot = __shfl_sync(0xffffffffu, inc, 31);
-        if (tot == 0) continue;
-        int wb = 0;
-        if (lane == 31) wb = atomicAdd(&s.cnt->n_cand, tot);
-        wb = __shfl_sync(0xffffffffu, wb, 31);
-        long long slot = (long long)wb + inc - cnt;
-        if (slot + cnt > s.max_cand) {
-            if (cnt) atomicOr(&s.cnt->overflow, 1);
-            continue;
-        }
-        while (vmask) {
-            const int v = __ffsll(vmask) - 1;
-            vmask &= vmask - 1;
-            s.cand[slot++] = make_int2(i, v);
-        }
+        __syncwarp();
     }
 }
 
@@ -280,13 +368,14 @@ void launch_project_cand(const Params &g, const StepDims &d, const CamSet &cams,
     size_t smem = sizeof(unsigned) * (size_t)d.V * d.TY * ((d.TX + 31) / 32);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_project_cand, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        cudaFuncSetAttribute(k_project_cand<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
         attr = true;
     }
-    const bool use_smem = smem <= 96 * 1024;
-    if (!use_smem) smem = 0;
-    const int blocks = std::min((d.n + 255) / 256, 148 * 8);
-    k_project_cand<<<blocks, 256, smem, st>>>(g.mean_op, g.quat, g.log_scale, d.n, cams, s, use_smem);
+    const int blocks = std::min((d.n + PC_THREADS - 1) / PC_THREADS, 148 * 3);
+    if (smem <= 96 * 1024)
+        k_project_cand<true><<<blocks, PC_THREADS, smem, st>>>(g.mean_op, g.quat, g.log_scale, d.n, cams, s);
+    else
+        k_project_cand<false><<<blocks, PC_THREADS, 0, st>>>(g.mean_op, g.quat, g.log_scale, d.n, cams, s);
     g_launches++;
 }
 
