@@ -7,6 +7,7 @@
 #include "../../include/cls.h"
 
 #define CLS_TILE 16
+#define FOOT_SMALL_ROWS 4   // footprints of at most this many tile rows are handled per thread
 #define CLS_BLOCK_PIX 256
 
 namespace cls {
@@ -43,12 +44,13 @@ struct Counters {
     int n_records;
     int n_cand;
     int tiles_scan_tiles;   // look-back ticket (tile scan)
-    unsigned long long n_pairs;     // (record, active tile of its rect) pairs: bucket capacity
-    unsigned long long n_kept;      // pairs kept after the exact footprint culling
+    unsigned long long n_pairs;     // (record, active tile) pairs kept by the exact footprint culling
+    int n_pairs32;          // min(n_pairs, max_pairs): element count of the pair sort
+    int n_big;              // records with tall footprints (warp-per-record counting / emission)
+    int scan_ticket;        // tile ticket of the order-preserving scan of the per-record pair counts
     int n_items;
-    int n_small, n_large, n_huge;
     int fwd_work, bwd_work;
-    int overflow;           // bit0 records, bit1 pairs
+    int overflow;           // bit0 records, bit1 pairs, bit2 active set
     int max_list;
     int active_tiles[CLS_MAX_VIEWS];
     unsigned long long fwd_evals;   // (pixel, list entry) evaluations of the forward
@@ -74,25 +76,30 @@ struct Scratch {
     float2 *rec_aux;        // (qcut' = kappa (2 ln(255 o)(1 + 1e-6) + 2e-3) rounded up, active ordinal bits or -1)
     int2 *rec_rect;         // (x0 | y0 << 16, x1 | y1 << 16)
     int2 *rec_meta;         // (gid, view | active << 31)
-    unsigned *rec_depth;    // fp32 bits of the depth key
     long long max_records;
     int2 *cand;             // (Gaussian, view) candidates of the fp32 pre-test
     long long max_cand;
+    // record depth sort: key (view << 32 | fp32 depth bits), value record id
+    unsigned long long *rkey, *rkey_alt;
+    unsigned *rval, *rval_alt;
+    const unsigned *rsorted;        // record ids in (view, depth, Gaussian index) order (rval or rval_alt)
+    unsigned *rcnt;                 // per record (storage order): active tiles its footprint reaches
+    unsigned *rcnt_s, *roff;        // the same per sorted position, and their exclusive offsets
+    unsigned *rpos;                 // sorted position of each record
+    unsigned *big;                  // records whose footprint spans > FOOT_SMALL_ROWS tile rows
+    unsigned long long *st_scan;    // look-back status of the offsets scan
     // tiles
-    int *tile_cnt;          // [V*T]
-    int *tile_off;          // [V*T]
-    int *tile_cursor;       // [V*T]
+    int *tile_end;          // [V*T] end of the tile's range in the sorted pairs (== tile_off if empty)
+    int *tile_off;          // [V*T] start of the tile's range
     unsigned long long *st_tiles;
     int *items;             // [V*T] (v*T + t) of active tiles, in (v, t) order
     int *item_of_tile;      // [V*T] item index or -1
-    int *cls_small, *cls_large, *cls_huge;  // item lists per sort class
-    int *first_active;      // [items] first list position holding an active Gaussian (n if none)
-    // pairs
-    unsigned long long *pairs;      // bucketed (depth bits << 32) | record | active << 31
-    unsigned *tile_list;            // per-tile depth-ordered record | active << 31
-    unsigned long long *sort_tmp_key;  // huge-tile fallback scratch
-    unsigned *sort_tmp_val;
+    int *first_active;      // [items] absolute position of the first pair holding an active Gaussian (INT_MAX if none)
+    // pairs: ((v*T + t) << 32) | record | active << 31, emitted in depth order, stably sorted by tile
+    unsigned long long *pairs, *pairs_alt;
+    const unsigned long long *spairs;   // the sorted buffer (pairs or pairs_alt)
     long long max_pairs;
+    unsigned *rs_counts, *rs_totals;    // radix sort scratch
     // per-pixel forward state, per item [items][256]
     float *px_T;
     int *px_last;
@@ -311,6 +318,91 @@ __device__ __forceinline__ void sh_color_raw(const float4 *__restrict__ sh, int 
             if (e < 3 * K) col[e % 3] += Y[e / 3] * sh_lane(f, l);
         }
     }
+}
+
+// -------- alpha-footprint of a record, per tile row --------
+// The raster composites (pixel, record) only where kappa q = a' dx^2 + 2 b' dx dy + c' dy^2 <= qcut'
+// (dx = u - x, dy = v - y, (a', b', c') from the record's coefficients, raster_q).  For the pixel
+// rows of tile row ty (dy in [v - 16ty - 15, v - 16ty]) the set of reached dx is an interval: its
+// right end max over dy of (-b' dy + sqrt(a' Q - det dy^2))/a' is concave in dy, maximised at the
+// ellipse's rightmost point dy_r = -b' sqrt(Q c'/det)/c' clamped to the row band (the left end
+// symmetrically at -dy_r).  A tile is kept iff its pixel-centre interval [16 tx, 16 tx + 15] meets
+// the reached x-interval -- the same set as minimising q over the tile's pixel-centre rectangle --
+// enlarged by conservative margins: Q = qcut' (1 + 1e-4) + 1e-3 covers the raster's fp32
+// evaluation (<= 1e-5 in kappa q), and the interval ends get 2e-3 of the ellipse's half-extent +
+// 0.05 px for this fp32 evaluation (sqrt near the ellipse's rim loses ~sqrt(1e-7) of the extent).
+// A conservative superset only adds list entries the raster skips; results are unchanged.
+struct FootRec {
+    float u, v, ia, b, det, aQ, ey, dyr, mx;
+    int x0, y0, x1, y1, view;
+    unsigned w;   // record | active << 31
+};
+
+// from the record's stored fields (the counting in k_project_exact and the emission call this
+// with bit-identical inputs, so both see the same tile sets)
+__device__ __forceinline__ FootRec foot_make(unsigned r, const int2 rc, const int2 meta, const float4 xy, const float4 co,
+                                             float qc)
+{
+    FootRec f;
+    f.view = meta.y & 0x7fffffff;
+    f.w = r | ((unsigned)meta.y & 0x80000000u);
+    f.x0 = rc.x & 0xffff; f.y0 = rc.x >> 16; f.x1 = rc.y & 0xffff; f.y1 = rc.y >> 16;
+    f.u = xy.x + xy.y;
+    f.v = xy.z + xy.w;
+    const float a1 = co.x, a2 = co.y, b1 = co.z, b2 = co.w;
+    const float a = a1 * a1 + b1 * b1, c = a2 * a2 + b2 * b2;
+    f.b = a1 * a2 + b1 * b2;
+    const float t = a1 * b2 - a2 * b1;   // a' c' - b'^2 = (a1 b2 - a2 b1)^2, cancellation free
+    f.det = t * t;
+    const float Q = qc * 1.0001f + 1e-3f;
+    f.ia = 1.0f / a;
+    f.aQ = a * Q;
+    const float ex = sqrtf(Q * c / f.det);     // half-extent in x (rightmost dx)
+    f.ey = sqrtf(Q * a / f.det) * 1.002f + 0.05f;
+    f.dyr = -f.b * ex / c;
+    f.mx = 2e-3f * ex + 0.05f;
+    return f;
+}
+
+// tile columns [lo, hi] (inclusive, within the rect) reached in tile row ty; false if none
+__device__ __forceinline__ bool foot_row(const FootRec &f, int ty, int &lo, int &hi)
+{
+    const float dyl = fmaxf(f.v - (float)(CLS_TILE * ty + CLS_TILE - 1), -f.ey);
+    const float dyh = fminf(f.v - (float)(CLS_TILE * ty), f.ey);
+    if (dyl > dyh) return false;
+    const float yr = fminf(fmaxf(f.dyr, dyl), dyh), yl = fminf(fmaxf(-f.dyr, dyl), dyh);
+    const float wr = sqrtf(fmaxf(f.aQ - f.det * yr * yr, 0.0f));
+    const float wl = sqrtf(fmaxf(f.aQ - f.det * yl * yl, 0.0f));
+    const float dx_hi = (wr - f.b * yr) * f.ia + f.mx, dx_lo = -(f.b * yl + wl) * f.ia - f.mx;
+    // pixel x = u - dx in [u - dx_hi, u - dx_lo]; tiles whose [16 tx, 16 tx + 15] meets it
+    lo = max((int)ceilf((f.u - dx_hi - (CLS_TILE - 1)) * (1.0f / CLS_TILE)), f.x0);
+    hi = min((int)floorf((f.u - dx_lo) * (1.0f / CLS_TILE)), f.x1 - 1);
+    return lo <= hi;
+}
+
+__device__ __forceinline__ FootRec foot_load(const Scratch &s, unsigned r)
+{
+    return foot_make(r, s.rec_rect[r], s.rec_meta[r], s.rec_xy[r], s.rec_co[r], s.rec_aux[r].x);
+}
+
+// active tiles of row bitmask `rm` (W32 words) in columns [lo, hi] of word w
+__device__ __forceinline__ unsigned row_bits(const unsigned *rm, int w, int lo, int hi)
+{
+    const int b0 = max(lo - 32 * w, 0), b1 = min(hi - 32 * w, 31);
+    if (b0 > b1) return 0u;
+    return rm[w] & (0xffffffffu >> (31 - b1)) & (0xffffffffu << b0);
+}
+
+// number of active tiles the footprint reaches (rmv: the view's row bitmasks)
+__device__ __forceinline__ unsigned foot_count(const FootRec &f, const unsigned *rmv, int W32)
+{
+    unsigned cnt = 0u;
+    for (int ty = f.y0; ty < f.y1; ty++) {
+        int lo, hi;
+        if (!foot_row(f, ty, lo, hi)) continue;
+        for (int w = lo >> 5; w <= (hi >> 5); w++) cnt += __popc(row_bits(rmv + ty * W32, w, lo, hi));
+    }
+    return cnt;
 }
 
 }  // namespace cls

@@ -101,8 +101,8 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         const int e = s.items[item];
         const int v = e / T, t = e - v * T;
         const int tx = t % TX, ty = t / TX;
-        const int n = s.tile_cnt[e];
         const int off = s.tile_off[e];
+        const int n = s.tile_end[e] - off;
         const int x = tx * CLS_TILE + lx;
         float Tr[RT_PX], C0[RT_PX], C1[RT_PX], C2[RT_PX];
         int last[RT_PX], term[RT_PX];
@@ -118,7 +118,7 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
             const bool live = Tr[0] > 0.f || Tr[1] > 0.f || Tr[2] > 0.f || Tr[3] > 0.f;
             if (__syncthreads_count(live) == 0) break;
             for (int j = tid; j < RT_BATCH && b0 + j < n; j += RT_THREADS)
-                stage(s, s.tile_list[off + b0 + j], tx, ty, sa[j], sb[j], sc[j]);
+                stage(s, (unsigned)s.spairs[off + b0 + j], tx, ty, sa[j], sb[j], sc[j]);
             __syncthreads();
             const int cnt = min(RT_BATCH, n - b0);
             for (int k = 0; k < cnt; k++) {
@@ -299,7 +299,7 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         const int v = e / T, t = e - v * T;
         const int tx = t % TX, ty = t / TX;
         const int off = s.tile_off[e];
-        const int first = s.first_active[item];
+        const int first = min(s.first_active[item] - off, s.tile_end[e] - off);   // absolute -> list position
         const int x = tx * CLS_TILE + lx;
         PixB P[RT_PX];
         int ml = -1;
@@ -334,7 +334,7 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
             const int bstart = max(bend - RT_BATCH, first);
             __syncthreads();
             for (int j = tid; j < bend - bstart; j += RT_THREADS) {
-                const unsigned val = s.tile_list[off + bstart + j];
+                const unsigned val = (unsigned)s.spairs[off + bstart + j];
                 stage(s, val, tx, ty, sa[j], sb[j], sc[j]);
                 const float4 xy = s.rec_xy[val & 0x7fffffffu];
                 sd[j] = make_float2(__double2float_rn(((double)xy.x - (double)(CLS_TILE * tx)) + (double)xy.y),

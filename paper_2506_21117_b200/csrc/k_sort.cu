@@ -1,0 +1,354 @@
+// k_sort.cu -- device-wide STABLE LSD radix sort of 64-bit keys (optionally with 32-bit
+// values) and an order-preserving exclusive scan, both with the element count read from
+// device memory (no host synchronisation inside a step, H8).
+//
+// Used by the binning of subsystem (3) (PAPER.md Supp. L539, "per-tile depth ordering";
+// reading R13: depth, ties by Gaussian index): the records are sorted by (view, depth)
+// and the (tile, record) pairs -- emitted in that order -- by their (view, tile) key, so
+// every tile's list comes out in depth order without a per-tile sort.
+//
+// Design (B200): persistent grid of RS_GRID blocks; block b owns a contiguous range of
+// 4096-element tiles, so stability across blocks is by construction.  Per pass:
+//   upsweep    per-block digit histograms (shared-memory atomics) -> counts[digit][block]
+//   scan       one warp per digit scans counts[digit][*] (exclusive), totals[digit]
+//   downsweep  per tile: stable in-warp ranking with __match_any_sync in element order,
+//              a (digit, warp) table scan, staging in shared memory in sorted order, and
+//              coalesced scatter to digit_base[digit] + rank (runs of equal digits are
+//              contiguous in the output).
+#include "kernels.h"
+
+namespace cls {
+
+#define RS_THREADS 256
+#define RS_WARPS (RS_THREADS / 32)
+#define RS_ITEMS 16
+#define RS_TILE (RS_THREADS * RS_ITEMS)   // 4096 elements per tile, 512 per warp
+
+__device__ __forceinline__ void rs_block_range(int n, int &t0, int &t1)
+{
+    const int ntiles = (n + RS_TILE - 1) / RS_TILE;
+    const int per = (ntiles + gridDim.x - 1) / gridDim.x;
+    t0 = min(ntiles, (int)blockIdx.x * per);
+    t1 = min(ntiles, t0 + per);
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(RS_THREADS)
+k_rs_upsweep(const unsigned long long *__restrict__ keys, const int *__restrict__ n_ptr, int max_n, int shift,
+             unsigned *__restrict__ counts, const int *__restrict__ skip)
+{
+    constexpr int BINS = 1 << BITS;
+    __shared__ unsigned hist[BINS];
+    for (int d = threadIdx.x; d < BINS; d += RS_THREADS) hist[d] = 0u;
+    __syncthreads();
+    const int n = (skip && *skip) ? 0 : min(*n_ptr, max_n);
+    int t0, t1;
+    rs_block_range(n, t0, t1);
+    const int e0 = t0 * RS_TILE, e1 = min(n, t1 * RS_TILE);
+    for (int i = e0 + threadIdx.x; i < e1; i += RS_THREADS)
+        atomicAdd(&hist[(unsigned)(keys[i] >> shift) & (BINS - 1)], 1u);
+    __syncthreads();
+    for (int d = threadIdx.x; d < BINS; d += RS_THREADS) counts[(size_t)d * gridDim.x + blockIdx.x] = hist[d];
+}
+
+// one warp per digit: exclusive scan of counts[d][0..G) in place; totals[d] = sum
+__global__ void __launch_bounds__(256) k_rs_scan(unsigned *__restrict__ counts, unsigned *__restrict__ totals,
+                                                 int bins, int G)
+{
+    const int d = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (d >= bins) return;
+    unsigned *row = counts + (size_t)d * G;
+    unsigned carry = 0u;
+    for (int b0 = 0; b0 < G; b0 += 32) {
+        const int b = b0 + lane;
+        const unsigned v = b < G ? row[b] : 0u;
+        unsigned inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        if (b < G) row[b] = carry + inc - v;
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (lane == 0) totals[d] = carry;
+}
+
+template <int BITS, bool VALS>
+__global__ void __launch_bounds__(RS_THREADS, 3)
+k_rs_downsweep(const unsigned long long *__restrict__ kin, unsigned long long *__restrict__ kout,
+               const unsigned *__restrict__ vin, unsigned *__restrict__ vout, const int *__restrict__ n_ptr, int max_n,
+               int shift, const unsigned *__restrict__ counts, const unsigned *__restrict__ totals,
+               const int *__restrict__ skip)
+{
+    constexpr int BINS = 1 << BITS;
+    constexpr int WP = RS_WARPS + 1;
+    constexpr int DPT = BINS / RS_THREADS;   // digits per thread in the table scan (1 or 2)
+    static_assert(DPT >= 1, "BINS >= threads");
+    extern __shared__ __align__(16) unsigned char rs_smem[];
+    unsigned long long *skey = reinterpret_cast<unsigned long long *>(rs_smem);      // [RS_TILE]
+    unsigned *sval = reinterpret_cast<unsigned *>(skey + RS_TILE);                   // [RS_TILE] (VALS)
+    unsigned *run = sval + (VALS ? RS_TILE : 0);                                     // [BINS][WP]
+    unsigned *dbase = run + BINS * WP;                                               // [BINS] global base
+    unsigned *dexcl = dbase + BINS;                                                  // [BINS] tile-local excl
+    unsigned *dcnt = dexcl + BINS;                                                   // [BINS] tile counts
+    __shared__ unsigned s_wsum[RS_WARPS];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const int n = (skip && *skip) ? 0 : min(*n_ptr, max_n);
+    int t0, t1;
+    rs_block_range(n, t0, t1);
+    if (t0 >= t1) return;
+    // global base of each digit for this block: exclusive scan of totals + counts[d][block]
+    {
+        unsigned loc[DPT];
+        unsigned sum = 0u;
+#pragma unroll
+        for (int q = 0; q < DPT; q++) {
+            loc[q] = totals[tid * DPT + q];
+            sum += loc[q];
+        }
+        unsigned inc = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        if (lane == 31) s_wsum[warp] = inc;
+        __syncthreads();
+        unsigned pre = inc - sum;
+        for (int w = 0; w < warp; w++) pre += s_wsum[w];
+#pragma unroll
+        for (int q = 0; q < DPT; q++) {
+            const int d = tid * DPT + q;
+            dbase[d] = pre + counts[(size_t)d * gridDim.x + blockIdx.x];
+            pre += loc[q];
+        }
+        __syncthreads();
+    }
+    for (int t = t0; t < t1; t++) {
+        const int base = t * RS_TILE;
+        const int tn = min(RS_TILE, n - base);
+        for (int c = tid; c < BINS * WP; c += RS_THREADS) run[c] = 0u;
+        __syncthreads();
+        // ---- stable ranking: warp w owns tile elements [w*512, (w+1)*512), rounds in order ----
+        // all 16 loads in flight at once; only the digits stay live (keys are re-read at staging,
+        // L1/L2 hits), so registers stay low enough for 3 blocks per SM
+        int mine[RS_ITEMS];   // digit, then (rank << 12) | digit
+        {
+            unsigned long long kk[RS_ITEMS];
+#pragma unroll
+            for (int r = 0; r < RS_ITEMS; r++) {
+                const int j = warp * (RS_TILE / RS_WARPS) + r * 32 + lane;
+                kk[r] = j < tn ? __ldcs(kin + base + j) : 0ull;
+            }
+#pragma unroll
+            for (int r = 0; r < RS_ITEMS; r++) {
+                const int j = warp * (RS_TILE / RS_WARPS) + r * 32 + lane;
+                mine[r] = j < tn ? (int)((unsigned)(kk[r] >> shift) & (BINS - 1)) : BINS + lane;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < RS_ITEMS; r++) {
+            const int j = warp * (RS_TILE / RS_WARPS) + r * 32 + lane;
+            const bool act = j < tn;
+            const int d = mine[r];
+            const unsigned peers = __match_any_sync(0xffffffffu, d);
+            const int leader = __ffs(peers) - 1;
+            unsigned b = 0u;
+            if (act && lane == leader) {   // the warp owns column `warp` of run[]: no atomics needed
+                b = run[d * WP + warp];
+                run[d * WP + warp] = b + (unsigned)__popc(peers);
+            }
+            b = __shfl_sync(0xffffffffu, b, leader);
+            mine[r] = (int)(((b + __popc(peers & lt)) << 12) | (unsigned)(d & (BINS - 1)));
+        }
+        __syncthreads();
+        // ---- exclusive scan of run[] in (digit, warp) order ----
+        {
+            unsigned loc[DPT * RS_WARPS];
+            unsigned sum = 0u;
+#pragma unroll
+            for (int q = 0; q < DPT; q++)
+#pragma unroll
+                for (int w = 0; w < RS_WARPS; w++) {
+                    const unsigned x = run[(tid * DPT + q) * WP + w];
+                    loc[q * RS_WARPS + w] = x;
+                    sum += x;
+                }
+            unsigned inc = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned tt = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += tt;
+            }
+            if (lane == 31) s_wsum[warp] = inc;
+            __syncthreads();
+            unsigned pre = inc - sum;
+            for (int w = 0; w < warp; w++) pre += s_wsum[w];
+#pragma unroll
+            for (int q = 0; q < DPT; q++) {
+                const int d = tid * DPT + q;
+                dexcl[d] = pre;
+                unsigned c = 0u;
+#pragma unroll
+                for (int w = 0; w < RS_WARPS; w++) {
+                    run[d * WP + w] = pre;
+                    pre += loc[q * RS_WARPS + w];
+                    c += loc[q * RS_WARPS + w];
+                }
+                dcnt[d] = c;
+            }
+        }
+        __syncthreads();
+        // ---- stage in tile-local sorted order ----
+#pragma unroll
+        for (int r = 0; r < RS_ITEMS; r++) {
+            const int j = warp * (RS_TILE / RS_WARPS) + r * 32 + lane;
+            if (j < tn) {
+                const int d = mine[r] & (BINS - 1);
+                const unsigned lp = run[d * WP + warp] + ((unsigned)mine[r] >> 12);
+                skey[lp] = __ldcs(kin + base + j);
+                if (VALS) sval[lp] = __ldcs(vin + base + j);
+            }
+        }
+        __syncthreads();
+        // ---- coalesced scatter ----
+        for (int j = tid; j < tn; j += RS_THREADS) {
+            const unsigned long long kk = skey[j];
+            const int d = (int)((unsigned)(kk >> shift) & (BINS - 1));
+            const unsigned g = dbase[d] + (unsigned)j - dexcl[d];
+            kout[g] = kk;
+            if (VALS) vout[g] = sval[j];
+        }
+        __syncthreads();
+        for (int d = tid; d < BINS; d += RS_THREADS) dbase[d] += dcnt[d];
+        __syncthreads();
+    }
+}
+
+template <int BITS, bool VALS>
+constexpr size_t rs_smem()
+{
+    return (size_t)RS_TILE * 8 + (VALS ? (size_t)RS_TILE * 4 : 0) + (size_t)(1 << BITS) * (RS_WARPS + 1) * 4 +
+           (size_t)(1 << BITS) * 4 * 3;
+}
+
+template <int BITS, bool VALS>
+static void rs_pass(unsigned long long *kin, unsigned long long *kout, unsigned *vin, unsigned *vout, const int *n_ptr,
+                    int max_n, int shift, unsigned *counts, unsigned *totals, const int *skip, cudaStream_t st)
+{
+    constexpr size_t SM = rs_smem<BITS, VALS>();
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_rs_downsweep<BITS, VALS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
+        attr = true;
+    }
+    k_rs_upsweep<BITS><<<RS_GRID, RS_THREADS, 0, st>>>(kin, n_ptr, max_n, shift, counts, skip);
+    k_rs_scan<<<((1 << BITS) + 7) / 8, 256, 0, st>>>(counts, totals, 1 << BITS, RS_GRID);
+    k_rs_downsweep<BITS, VALS><<<RS_GRID, RS_THREADS, SM, st>>>(kin, kout, vin, vout, n_ptr, max_n, shift, counts,
+                                                                totals, skip);
+    g_launches += 3;
+}
+
+int radix_sort_u64(unsigned long long *keys, unsigned long long *keys_alt, unsigned *vals, unsigned *vals_alt,
+                   const int *n_ptr, int max_n, int begin_bit, int end_bit, int digit_bits, unsigned *counts,
+                   unsigned *totals, const int *skip, cudaStream_t st)
+{
+    int which = 0;
+    for (int shift = begin_bit; shift < end_bit; shift += digit_bits) {
+        unsigned long long *ki = which ? keys_alt : keys, *ko = which ? keys : keys_alt;
+        unsigned *vi = which ? vals_alt : vals, *vo = which ? vals : vals_alt;
+        if (digit_bits == 8) {
+            if (vals) rs_pass<8, true>(ki, ko, vi, vo, n_ptr, max_n, shift, counts, totals, skip, st);
+            else rs_pass<8, false>(ki, ko, nullptr, nullptr, n_ptr, max_n, shift, counts, totals, skip, st);
+        } else {
+            if (vals) rs_pass<9, true>(ki, ko, vi, vo, n_ptr, max_n, shift, counts, totals, skip, st);
+            else rs_pass<9, false>(ki, ko, nullptr, nullptr, n_ptr, max_n, shift, counts, totals, skip, st);
+        }
+        which ^= 1;
+    }
+    return which;
+}
+
+// ---------------------------------------------------------------------------
+// exclusive scan of n (device count) unsigned values, single pass with decoupled look-back;
+// writes the total to *total.  The look-back status array must be zeroed before the launch.
+// ---------------------------------------------------------------------------
+#define SC_THREADS 256
+#define SC_ITEMS 8
+#define SC_TILE (SC_THREADS * SC_ITEMS)
+
+__global__ void __launch_bounds__(SC_THREADS)
+k_scan_excl(const unsigned *__restrict__ in, unsigned *__restrict__ out, const int *__restrict__ n_ptr, int max_n,
+            unsigned long long *status, int *ticket, unsigned long long *total, const int *__restrict__ skip)
+{
+    __shared__ int s_tile;
+    __shared__ unsigned long long s_warp[SC_THREADS / 32];
+    __shared__ unsigned long long s_prefix;
+    const int n = (skip && *skip) ? 0 : min(*n_ptr, max_n);
+    const int ntiles = (n + SC_TILE - 1) / SC_TILE;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    while (true) {
+        if (tid == 0) s_tile = atomicAdd(ticket, 1);
+        __syncthreads();
+        const int tile = s_tile;
+        __syncthreads();
+        if (tile >= ntiles) {
+            if (tile == 0 && tid == 0) *total = 0ull;   // empty input
+            return;
+        }
+        const int b = tile * SC_TILE + tid * SC_ITEMS;
+        unsigned v[SC_ITEMS];
+        unsigned long long sum = 0;
+#pragma unroll
+        for (int k = 0; k < SC_ITEMS; k++) {
+            v[k] = b + k < n ? in[b + k] : 0u;
+            sum += v[k];
+        }
+        unsigned long long inc = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        if (lane == 31) s_warp[warp] = inc;
+        __syncthreads();
+        if (warp == 0) {
+            const unsigned long long w = lane < SC_THREADS / 32 ? s_warp[lane] : 0ull;
+            unsigned long long wi = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long t = __shfl_up_sync(0xffffffffu, wi, o);
+                if (lane >= o) wi += t;
+            }
+            if (lane < SC_THREADS / 32) s_warp[lane] = wi - w;
+            const unsigned long long agg = __shfl_sync(0xffffffffu, wi, SC_THREADS / 32 - 1);
+            if (lane == 0) {
+                const unsigned long long pre = lookback(status, tile, agg);
+                s_prefix = pre;
+                if (tile == ntiles - 1) *total = pre + agg;
+            }
+        }
+        __syncthreads();
+        unsigned long long run = s_prefix + s_warp[warp] + (inc - sum);
+#pragma unroll
+        for (int k = 0; k < SC_ITEMS; k++) {
+            if (b + k < n) out[b + k] = (unsigned)run;
+            run += v[k];
+        }
+        __syncthreads();
+    }
+}
+
+void scan_excl_u32(const unsigned *in, unsigned *out, const int *n_ptr, int max_n, unsigned long long *status,
+                   int *ticket, unsigned long long *total, const int *skip, cudaStream_t st)
+{
+    const int tiles = (max_n + SC_TILE - 1) / SC_TILE;
+    cudaMemsetAsync(status, 0, sizeof(unsigned long long) * (size_t)(tiles + 1), st);
+    cudaMemsetAsync(ticket, 0, sizeof(int), st);
+    k_scan_excl<<<148 * 4, SC_THREADS, 0, st>>>(in, out, n_ptr, max_n, status, ticket, total, skip);
+    g_launches++;
+}
+
+}  // namespace cls
