@@ -104,7 +104,7 @@ typedef struct {
     int32_t overflow;          /* bit 0 records, bit 1 pairs, bit 2 active set */
     int32_t n_views;
     int64_t max_list;          /* longest per-tile list */
-    int64_t n_huge_tiles;      /* tiles sorted by the global-memory fallback */
+    int64_t n_tall_records;    /* records whose footprint spans > 4 tile rows (binned warp-per-record) */
     int64_t n_fwd_evals;       /* (pixel, list entry) evaluations of the forward compositing */
     int64_t n_bwd_evals;       /* (pixel, list entry) evaluations of the backward walk (after its bwd) */
     int64_t n_candidates;      /* (Gaussian, view) pairs passing the fp32 projection pre-test */

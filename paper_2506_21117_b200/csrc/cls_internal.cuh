@@ -57,6 +57,15 @@ struct Counters {
     unsigned long long bwd_evals;   // (pixel, list entry) evaluations of the backward walk
 };
 
+// One (Gaussian, view) record, 64 B = two full 32 B sectors per random access.
+struct __align__(16) Rec {
+    float4 xy;    // (u_hi, u_lo, v_hi, v_lo)  2D mean as fp32 hi/lo pairs (H1)
+    float4 co;    // (a1, a2, b1, b2)  scaled LDL^T exponent coefficients, see raster_q
+    float4 rgb;   // (r, g, b, opacity)
+    float4 aux;   // (qcut' = kappa (2 ln(255 o)(1 + 1e-6) + 2e-3) rounded up, active ordinal bits or -1,
+                  //  rect x0 | y0 << 16 bits, rect x1 | y1 << 16 bits)
+};
+
 // all scratch of a ctx (device pointers), passed by value to kernels
 struct Scratch {
     // membership
@@ -70,12 +79,9 @@ struct Scratch {
     int4 *view_bbox;        // [V] tile bbox of the active tiles
     int *diff;              // [V][(TY+1)(TX+1)]  corner differences of record rects
     // records
-    float4 *rec_xy;         // (u_hi, u_lo, v_hi, v_lo)  2D mean as fp32 hi/lo pairs (H1)
-    float4 *rec_co;         // (a1, a2, b1, b2)  scaled LDL^T exponent coefficients, see raster_q
-    float4 *rec_rgb;        // (r, g, b, opacity)
-    float2 *rec_aux;        // (qcut' = kappa (2 ln(255 o)(1 + 1e-6) + 2e-3) rounded up, active ordinal bits or -1)
-    int2 *rec_rect;         // (x0 | y0 << 16, x1 | y1 << 16)
-    int2 *rec_meta;         // (gid, view | active << 31)
+    Rec *rec;               // records in creation order (k_project_exact)
+    int *rec_gid;           // their Gaussian index (ties of the depth order, R13)
+    Rec *srec;              // records in (view, depth, index) order: the binning and the raster read these
     long long max_records;
     int2 *cand;             // (Gaussian, view) candidates of the fp32 pre-test
     long long max_cand;
@@ -83,10 +89,9 @@ struct Scratch {
     unsigned long long *rkey, *rkey_alt;
     unsigned *rval, *rval_alt;
     const unsigned *rsorted;        // record ids in (view, depth, Gaussian index) order (rval or rval_alt)
-    unsigned *rcnt;                 // per record (storage order): active tiles its footprint reaches
-    unsigned *rcnt_s, *roff;        // the same per sorted position, and their exclusive offsets
-    unsigned *rpos;                 // sorted position of each record
-    unsigned *big;                  // records whose footprint spans > FOOT_SMALL_ROWS tile rows
+    const unsigned long long *rskey;   // the sorted keys (view in the high word)
+    unsigned *rcnt, *roff;          // per sorted record: active tiles its footprint reaches, exclusive offsets
+    unsigned *big;                  // sorted records whose footprint spans > FOOT_SMALL_ROWS tile rows
     unsigned long long *st_scan;    // look-back status of the offsets scan
     // tiles
     int *tile_end;          // [V*T] end of the tile's range in the sorted pairs (== tile_off if empty)
@@ -338,23 +343,22 @@ struct FootRec {
     unsigned w;   // record | active << 31
 };
 
-// from the record's stored fields (the counting in k_project_exact and the emission call this
-// with bit-identical inputs, so both see the same tile sets)
-__device__ __forceinline__ FootRec foot_make(unsigned r, const int2 rc, const int2 meta, const float4 xy, const float4 co,
-                                             float qc)
+// from a record (the counting and the emission both read the sorted copy: same tile sets)
+__device__ __forceinline__ FootRec foot_make(const Rec &R, int view, unsigned w)
 {
     FootRec f;
-    f.view = meta.y & 0x7fffffff;
-    f.w = r | ((unsigned)meta.y & 0x80000000u);
-    f.x0 = rc.x & 0xffff; f.y0 = rc.x >> 16; f.x1 = rc.y & 0xffff; f.y1 = rc.y >> 16;
-    f.u = xy.x + xy.y;
-    f.v = xy.z + xy.w;
-    const float a1 = co.x, a2 = co.y, b1 = co.z, b2 = co.w;
+    f.view = view;
+    f.w = w;
+    const int ra = __float_as_int(R.aux.z), rb = __float_as_int(R.aux.w);
+    f.x0 = ra & 0xffff; f.y0 = ra >> 16; f.x1 = rb & 0xffff; f.y1 = rb >> 16;
+    f.u = R.xy.x + R.xy.y;
+    f.v = R.xy.z + R.xy.w;
+    const float a1 = R.co.x, a2 = R.co.y, b1 = R.co.z, b2 = R.co.w;
     const float a = a1 * a1 + b1 * b1, c = a2 * a2 + b2 * b2;
     f.b = a1 * a2 + b1 * b2;
     const float t = a1 * b2 - a2 * b1;   // a' c' - b'^2 = (a1 b2 - a2 b1)^2, cancellation free
     f.det = t * t;
-    const float Q = qc * 1.0001f + 1e-3f;
+    const float Q = R.aux.x * 1.0001f + 1e-3f;
     f.ia = 1.0f / a;
     f.aQ = a * Q;
     const float ex = sqrtf(Q * c / f.det);     // half-extent in x (rightmost dx)
@@ -380,9 +384,11 @@ __device__ __forceinline__ bool foot_row(const FootRec &f, int ty, int &lo, int 
     return lo <= hi;
 }
 
-__device__ __forceinline__ FootRec foot_load(const Scratch &s, unsigned r)
+// sorted record i (pair value: i | active << 31)
+__device__ __forceinline__ FootRec foot_load(const Scratch &s, unsigned i)
 {
-    return foot_make(r, s.rec_rect[r], s.rec_meta[r], s.rec_xy[r], s.rec_co[r], s.rec_aux[r].x);
+    const Rec R = s.srec[i];
+    return foot_make(R, (int)(s.rskey[i] >> 32), i | (__float_as_int(R.aux.y) < 0 ? 0u : 0x80000000u));
 }
 
 // active tiles of row bitmask `rm` (W32 words) in columns [lo, hi] of word w

@@ -39,11 +39,11 @@ struct cls_ctx {
     int64_t prof_n[CLS_PROF_GROUPS] = {};
 };
 
-static const char *PROF_NAMES[] = {"member", "active_mask", "project_cand", "project_exact", "bin_sort",
-                                   "fwd_raster", "fill_bg", "loss", "zero_grad2d", "bwd_raster", "bwd_project",
-                                   "adam"};
-enum { P_MEMBER, P_MASK, P_PROJECT, P_PROJECT_EXACT, P_BIN, P_FWD, P_FILL, P_LOSS, P_ZERO, P_BWD_RASTER,
-       P_BWD_PROJECT, P_ADAM, P_COUNT };
+static const char *PROF_NAMES[] = {"member", "active_mask", "project_cand", "project_exact", "rec_sort", "bin_count",
+                                   "emit", "pair_sort", "fwd_raster", "fill_bg", "loss", "zero_grad2d", "bwd_raster",
+                                   "bwd_project", "adam"};
+enum { P_MEMBER, P_MASK, P_PROJECT, P_PROJECT_EXACT, P_RECSORT, P_BINCOUNT, P_EMIT, P_PAIRSORT, P_FWD, P_FILL, P_LOSS,
+       P_ZERO, P_BWD_RASTER, P_BWD_PROJECT, P_ADAM, P_COUNT };
 static_assert(P_COUNT <= CLS_PROF_GROUPS, "profile groups");
 
 static cudaEvent_t prof_event(cls_ctx *c)
@@ -129,9 +129,9 @@ cls_status cls_destroy(cls_ctx *c)
 {
     if (!c) return CLS_ERR_INVALID_ARGUMENT;
     cudaSetDevice(c->device);
-    void *ptrs[] = {c->s.idx, c->s.ord, c->s.st_member, c->s.mask, c->s.sat, c->s.rowmask, c->s.view_bbox, c->s.rec_xy,
-                    c->s.rec_co, c->s.rec_rgb, c->s.rec_aux, c->s.cand, c->s.rec_rect, c->s.rec_meta, c->s.rkey,
-                    c->s.rkey_alt, c->s.rval, c->s.rval_alt, c->s.rcnt, c->s.rcnt_s, c->s.rpos, c->s.big, c->s.roff, c->s.st_scan, c->s.tile_end,
+    void *ptrs[] = {c->s.idx, c->s.ord, c->s.st_member, c->s.mask, c->s.sat, c->s.rowmask, c->s.view_bbox, c->s.rec,
+                    c->s.srec, c->s.rec_gid, c->s.cand, c->s.rkey,
+                    c->s.rkey_alt, c->s.rval, c->s.rval_alt, c->s.rcnt, c->s.big, c->s.roff, c->s.st_scan, c->s.tile_end,
                     c->s.tile_off, c->s.st_tiles, c->s.items, c->s.item_of_tile, c->s.first_active, c->s.pairs,
                     c->s.pairs_alt, c->s.rs_counts, c->s.rs_totals, c->s.px_T, c->s.px_last, c->s.px_dl,
                     c->s.item_loss, c->s.grad2d, c->s.cnt};
@@ -170,10 +170,9 @@ cls_status cls_create(cls_ctx **out, int device, const cls_limits *lim)
     Scratch &s = c->s;
     bool ok = dalloc(&s.idx, N) && dalloc(&s.ord, N) && dalloc(&s.st_member, N / 2048 + 2) && dalloc(&s.mask, VT) &&
               dalloc(&s.sat, SAT) && dalloc(&s.rowmask, V * c->maxTY * ((c->maxTX + 31) / 32)) &&
-              dalloc(&s.view_bbox, V) && dalloc(&s.rec_xy, R) && dalloc(&s.rec_co, R) && dalloc(&s.rec_rgb, R) &&
-              dalloc(&s.rec_aux, R) && dalloc(&s.cand, R + R / 2 + 1024) && dalloc(&s.rec_rect, R) &&
-              dalloc(&s.rec_meta, R) && dalloc(&s.rkey, R) && dalloc(&s.rkey_alt, R) && dalloc(&s.rval, R) &&
-              dalloc(&s.rval_alt, R) && dalloc(&s.rcnt, R) && dalloc(&s.rcnt_s, R) && dalloc(&s.rpos, R) && dalloc(&s.big, R) && dalloc(&s.roff, R) && dalloc(&s.st_scan, R / 2048 + 2) &&
+              dalloc(&s.view_bbox, V) && dalloc(&s.rec, R) && dalloc(&s.srec, R) && dalloc(&s.rec_gid, R) &&
+              dalloc(&s.cand, R + R / 2 + 1024) && dalloc(&s.rkey, R) && dalloc(&s.rkey_alt, R) && dalloc(&s.rval, R) &&
+              dalloc(&s.rval_alt, R) && dalloc(&s.rcnt, R) && dalloc(&s.big, R) && dalloc(&s.roff, R) && dalloc(&s.st_scan, R / 2048 + 2) &&
               dalloc(&s.tile_end, VT) && dalloc(&s.tile_off, VT) && dalloc(&s.st_tiles, VT / 2048 + 2) &&
               dalloc(&s.items, VT) && dalloc(&s.item_of_tile, VT) && dalloc(&s.first_active, VT) &&
               dalloc(&s.pairs, P) && dalloc(&s.pairs_alt, P) && dalloc(&s.rs_counts, (size_t)512 * RS_GRID) &&
@@ -285,7 +284,10 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     run(c, P_MASK, st, [&] { launch_active_mask(p, d, cs, s, st); });
     run(c, P_PROJECT, st, [&] { launch_project_cand(p, d, cs, s, st); });
     run(c, P_PROJECT_EXACT, st, [&] { launch_project_exact(p, d, cs, s, st); });
-    run(c, P_BIN, st, [&] { launch_bin(d, cs, s, st); });
+    run(c, P_RECSORT, st, [&] { launch_bin_recsort(d, cs, s, st); });
+    run(c, P_BINCOUNT, st, [&] { launch_bin_count(d, cs, s, st); });
+    run(c, P_EMIT, st, [&] { launch_bin_emit(d, cs, s, st); });
+    run(c, P_PAIRSORT, st, [&] { launch_bin_pairsort(d, cs, s, st); });
     run(c, P_FWD, st, [&] { launch_fwd(d, cs, s, targets, images, loss_scale, bgc, st); });
     if (images) run(c, P_FILL, st, [&] { launch_fill_bg(d, s, images, bgc, st); });
     if (targets && loss) run(c, P_LOSS, st, [&] { launch_loss(s, loss_scale, loss, st); });
@@ -295,6 +297,7 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     cls_status e = check_cuda(c, "cls_render_fwd");
     if (e != CLS_OK) return e;
     c->s.rsorted = s.rsorted;
+    c->s.rskey = s.rskey;
     c->s.spairs = s.spairs;
     c->dims = d;
     c->cams = cs;
@@ -400,7 +403,7 @@ cls_status cls_stats(cls_ctx *c, cls_stats_t *out)
     for (int v = 0; v < c->dims.V; v++) out->n_active_tiles[v] = h.active_tiles[v];
     out->overflow = h.overflow | ovf;
     out->max_list = h.max_list;
-    out->n_huge_tiles = 0;   // no per-tile sort any more (k_bin.cu): no oversize fallback
+    out->n_tall_records = h.n_big;
     out->n_candidates = h.n_cand;
     out->n_kept_pairs = (int64_t)h.n_pairs;
     out->n_fwd_evals = (int64_t)h.fwd_evals;

@@ -6,10 +6,10 @@
 // R13).  B200 design: no per-pair depth keys are sorted at all.
 //   1. the ~6M records are sorted ONCE by (view, fp32 depth) with a stable LSD radix sort
 //      (k_sort.cu); runs of equal keys are then ordered by Gaussian index (k_rec_ties);
-//   2. per record, the number of ACTIVE tiles its alpha >= 1/255 footprint reaches (closed-form
-//      x-interval of the ellipse per tile row, row bitmasks; counted in k_project_exact), put in
-//      sorted order -> order-preserving exclusive scan -> each record's contiguous output range;
-//   3. emission at those ranges (no atomics): pair = (view*T + tile) << 32 | record;
+//   2. the records are gathered into that order (64 B each); per sorted record, the number of
+//      ACTIVE tiles its alpha >= 1/255 footprint reaches (closed-form x-interval of the ellipse per
+//      tile row, row bitmasks) -> order-preserving exclusive scan -> contiguous output ranges;
+//   3. emission at those ranges (no atomics): pair = (view*T + tile) << 32 | sorted record;
 //   4. a stable 2-pass LSD radix sort of the pairs by their (view, tile) key keeps the
 //      depth order inside every tile;
 //   5. tile ranges and the first active entry from the sorted keys.
@@ -91,9 +91,9 @@ __global__ void k_rec_ties(Scratch s, const unsigned long long *__restrict__ key
         while (end < n && key[end] == k) end++;
         for (int a = i + 1; a < end; a++) {   // insertion sort of the run by Gaussian index
             const unsigned va = val[a];
-            const int ga = s.rec_meta[va].x;
+            const int ga = s.rec_gid[va];
             int b = a - 1;
-            while (b >= i && s.rec_meta[val[b]].x > ga) {
+            while (b >= i && s.rec_gid[val[b]] > ga) {
                 val[b + 1] = val[b];
                 b--;
             }
@@ -102,15 +102,26 @@ __global__ void k_rec_ties(Scratch s, const unsigned long long *__restrict__ key
     }
 }
 
-// 2. sorted order of the per-record pair counts (computed by k_project_exact) and the inverse
-// permutation pos[record] = sorted position
-__global__ void __launch_bounds__(256) k_rec_gather(Scratch s)
+// 2. records gathered into (view, depth, index) order (one 64 B record per access), and the
+// number of ACTIVE tiles each footprint reaches (row bitmasks, popc); tall footprints
+// (> FOOT_SMALL_ROWS tile rows) are listed for the warp-per-record kernels (no divergence)
+__global__ void __launch_bounds__(256) k_permute(const __grid_constant__ CamSet cams, Scratch s)
 {
     const int n = s.cnt->overflow ? 0 : min(s.cnt->n_records, (int)s.max_records);
+    const int TY = cams.TY, W32 = (cams.TX + 31) >> 5;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const unsigned r = s.rsorted[i];
-        s.rpos[r] = (unsigned)i;
-        s.rcnt_s[i] = s.rcnt[r];
+        const Rec R = s.rec[s.rsorted[i]];
+        s.srec[i] = R;
+        const int rb = __float_as_int(R.aux.w), ra = __float_as_int(R.aux.z);
+        unsigned cnt = 0u;
+        if ((rb >> 16) - (ra >> 16) <= FOOT_SMALL_ROWS) {
+            const int view = (int)(s.rskey[i] >> 32);
+            const FootRec f = foot_make(R, view, 0u);
+            cnt = foot_count(f, s.rowmask + (size_t)view * TY * W32, W32);
+        } else {
+            s.big[atomicAdd(&s.cnt->n_big, 1)] = (unsigned)i;
+        }
+        s.rcnt[i] = cnt;
     }
 }
 
@@ -121,8 +132,8 @@ __global__ void __launch_bounds__(256) k_big_count(const __grid_constant__ CamSe
     const int TY = cams.TY, W32 = (cams.TX + 31) >> 5;
     const int lane = threadIdx.x & 31;
     for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nb; k += (gridDim.x * blockDim.x) >> 5) {
-        const unsigned r = s.big[k];
-        const FootRec f = foot_load(s, r);
+        const unsigned i = s.big[k];
+        const FootRec f = foot_load(s, i);
         const unsigned *rmv = s.rowmask + (size_t)f.view * TY * W32;
         unsigned cnt = 0u;
         for (int ty = f.y0 + lane; ty < f.y1; ty += 32) {
@@ -131,32 +142,36 @@ __global__ void __launch_bounds__(256) k_big_count(const __grid_constant__ CamSe
             for (int w = lo >> 5; w <= (hi >> 5); w++) cnt += __popc(row_bits(rmv + ty * W32, w, lo, hi));
         }
         for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-        if (lane == 0) s.rcnt[r] = cnt;
+        if (lane == 0) s.rcnt[i] = cnt;
     }
 }
 
 // pairs of tile row ty of footprint f, written from `out`
-__device__ __forceinline__ unsigned long long *emit_row(const FootRec &f, const unsigned *rmv, int W32, int TX,
-                                                        unsigned long long vb, int ty, int lo, int hi,
-                                                        unsigned long long *out)
+template <typename OUT>
+__device__ __forceinline__ void emit_row(const FootRec &f, const unsigned *rmv, int W32, int TX, unsigned long long vb,
+                                         int ty, int lo, int hi, OUT &&out)
 {
     for (int w = lo >> 5; w <= (hi >> 5); w++) {
         unsigned bits = row_bits(rmv + ty * W32, w, lo, hi);
         while (bits) {
             const int tx = 32 * w + __ffs(bits) - 1;
             bits &= bits - 1;
-            *out++ = ((vb + (unsigned long long)(ty * TX + tx)) << 32) | f.w;
+            out(((vb + (unsigned long long)(ty * TX + tx)) << 32) | f.w);
         }
     }
-    return out;
 }
 
-// 3. emission: record r's pairs at roff[pos[r]] .. + rcnt[r] (its place in the depth order), tiles
-// in (row, column) order -- any fixed order works, the stable pair sort only needs record order.
-// Records are read in their (unsorted) storage order, so the loads are coalesced; tall footprints
-// are left to k_emit_big.
-__global__ void __launch_bounds__(256) k_emit(const __grid_constant__ CamSet cams, Scratch s)
+// 3. emission in sorted-record order: record i's pairs at roff[i] .. roff[i] + rcnt[i], tiles in
+// (row, column) order -- any fixed order works, the stable pair sort only needs record order.
+// A warp's 32 consecutive records own one contiguous output range: staged in shared memory and
+// stored with coalesced writes (ranges over EM_CAP write through).  Tall footprints are written
+// afterwards by k_emit_big (their part of a staged range is overwritten then).
+#define EM_WARPS 8
+#define EM_CAP 512
+
+__global__ void __launch_bounds__(EM_WARPS * 32) k_emit(const __grid_constant__ CamSet cams, Scratch s)
 {
+    __shared__ unsigned long long stage_buf[EM_WARPS][EM_CAP];
     if (s.cnt->overflow) return;
     const int n = min(s.cnt->n_records, (int)s.max_records);
     const unsigned long long total = s.cnt->n_pairs;
@@ -166,18 +181,35 @@ __global__ void __launch_bounds__(256) k_emit(const __grid_constant__ CamSet cam
     }
     if ((long long)total > s.max_pairs) return;
     const int TX = cams.TX, TY = cams.TY, T = cams.T, W32 = (TX + 31) >> 5;
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
-        if (s.rcnt[r] == 0u) continue;
-        const int2 rc = s.rec_rect[r];
-        if ((rc.y >> 16) - (rc.x >> 16) > FOOT_SMALL_ROWS) continue;
-        const FootRec f = foot_load(s, (unsigned)r);
-        const unsigned *rmv = s.rowmask + (size_t)f.view * TY * W32;
-        const unsigned long long vb = (unsigned long long)f.view * T;
-        unsigned long long *out = s.pairs + s.roff[s.rpos[r]];
-        for (int ty = f.y0; ty < f.y1; ty++) {
-            int lo, hi;
-            if (foot_row(f, ty, lo, hi)) out = emit_row(f, rmv, W32, TX, vb, ty, lo, hi, out);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned long long *buf = stage_buf[wid];
+    for (int i0 = (blockIdx.x * EM_WARPS + wid) * 32; i0 < n; i0 += gridDim.x * EM_WARPS * 32) {
+        const int i = i0 + lane;
+        const int il = min(i0 + 31, n - 1);
+        const unsigned base = s.roff[i0];
+        const unsigned end = s.roff[il] + s.rcnt[il];
+        const bool staged = end - base <= EM_CAP;
+        if (i < n && s.rcnt[i] != 0u) {
+            const FootRec f = foot_load(s, (unsigned)i);
+            if (f.y1 - f.y0 <= FOOT_SMALL_ROWS) {
+                const unsigned *rmv = s.rowmask + (size_t)f.view * TY * W32;
+                const unsigned long long vb = (unsigned long long)f.view * T;
+                unsigned o = s.roff[i];
+                for (int ty = f.y0; ty < f.y1; ty++) {
+                    int lo, hi;
+                    if (!foot_row(f, ty, lo, hi)) continue;
+                    emit_row(f, rmv, W32, TX, vb, ty, lo, hi, [&](unsigned long long pv) {
+                        if (staged) buf[o - base] = pv;
+                        else s.pairs[o] = pv;
+                        o++;
+                    });
+                }
+            }
         }
+        __syncwarp();
+        if (staged)
+            for (unsigned j = lane; j < end - base; j += 32) s.pairs[base + j] = buf[j];
+        __syncwarp();
     }
 }
 
@@ -189,12 +221,12 @@ __global__ void __launch_bounds__(256) k_emit_big(const __grid_constant__ CamSet
     const int TX = cams.TX, TY = cams.TY, T = cams.T, W32 = (TX + 31) >> 5;
     const int lane = threadIdx.x & 31;
     for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nb; k += (gridDim.x * blockDim.x) >> 5) {
-        const unsigned r = s.big[k];
-        if (s.rcnt[r] == 0u) continue;
-        const FootRec f = foot_load(s, r);
+        const unsigned i = s.big[k];
+        if (s.rcnt[i] == 0u) continue;
+        const FootRec f = foot_load(s, i);
         const unsigned *rmv = s.rowmask + (size_t)f.view * TY * W32;
         const unsigned long long vb = (unsigned long long)f.view * T;
-        unsigned base = s.roff[s.rpos[r]];
+        unsigned base = s.roff[i];
         for (int ty0 = f.y0; ty0 < f.y1; ty0 += 32) {   // rows in chunks of 32, in order
             const int ty = ty0 + lane;
             int lo = 0, hi = -1;
@@ -206,7 +238,10 @@ __global__ void __launch_bounds__(256) k_emit_big(const __grid_constant__ CamSet
                 const unsigned t = __shfl_up_sync(0xffffffffu, inc, o);
                 if (lane >= o) inc += t;
             }
-            if (c) emit_row(f, rmv, W32, TX, vb, ty, lo, hi, s.pairs + base + inc - c);
+            if (c) {
+                unsigned long long *out = s.pairs + base + inc - c;
+                emit_row(f, rmv, W32, TX, vb, ty, lo, hi, [&](unsigned long long pv) { *out++ = pv; });
+            }
             base += __shfl_sync(0xffffffffu, inc, 31);
         }
     }
@@ -246,14 +281,13 @@ static int bits_for(long long x)   // bits to represent 0..x
     return b;
 }
 
-void launch_bin(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st)
+// 1. items + record depth sort + ties
+void launch_bin_recsort(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st)
 {
     const int VT = d.V * d.T;
-    // items of the active tiles
     const int blocks = (VT + TSCAN_TILE - 1) / TSCAN_TILE;
     cudaMemsetAsync(s.st_tiles, 0, sizeof(unsigned long long) * blocks, st);
     k_tiles_scan<<<blocks, TSCAN_THREADS, 0, st>>>(VT, s);
-    // 1. records by (view, depth), ties by index
     const int rbits = 32 + bits_for(d.V - 1);
     const int R = (int)s.max_records;
     const int w = radix_sort_u64(s.rkey, s.rkey_alt, s.rval, s.rval_alt, &s.cnt->n_records, R, 0, rbits, 8,
@@ -261,27 +295,43 @@ void launch_bin(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t 
     unsigned long long *rk = w ? s.rkey_alt : s.rkey;
     unsigned *rv = w ? s.rval_alt : s.rval;
     s.rsorted = rv;
+    s.rskey = rk;
     k_rec_ties<<<148 * 4, 256, 0, st>>>(s, rk, rv);
-    // 2. exact per-record pair counts and their offsets
+    g_launches += 2;
+}
+
+// 2. sorted records, exact per-record pair counts and their offsets
+void launch_bin_count(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st)
+{
+    k_permute<<<148 * 8, 256, 0, st>>>(cams, s);
     k_big_count<<<148 * 8, 256, 0, st>>>(cams, s);
-    k_rec_gather<<<148 * 8, 256, 0, st>>>(s);
-    scan_excl_u32(s.rcnt_s, s.roff, &s.cnt->n_records, R, s.st_scan, &s.cnt->scan_ticket, &s.cnt->n_pairs,
-                  &s.cnt->overflow, st);
-    // 3. emission
-    k_emit<<<148 * 8, 256, 0, st>>>(cams, s);
+    scan_excl_u32(s.rcnt, s.roff, &s.cnt->n_records, (int)s.max_records, s.st_scan, &s.cnt->scan_ticket,
+                  &s.cnt->n_pairs, &s.cnt->overflow, st);
+    g_launches += 2;
+}
+
+// 3. emission
+void launch_bin_emit(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st)
+{
+    k_emit<<<148 * 4, EM_WARPS * 32, 0, st>>>(cams, s);
     k_emit_big<<<148 * 8, 256, 0, st>>>(cams, s);
-    // 4. stable sort of the pairs by (view, tile)
+    g_launches += 2;
+}
+
+// 4. stable sort of the pairs by (view, tile), 5. ranges
+void launch_bin_pairsort(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st)
+{
+    const int VT = d.V * d.T;
     const int tbits = std::max(bits_for(VT - 1), 1);
     const int w2 = radix_sort_u64(s.pairs, s.pairs_alt, nullptr, nullptr, &s.cnt->n_pairs32, (int)s.max_pairs, 32,
                                   32 + tbits, 9, s.rs_counts, s.rs_totals, &s.cnt->overflow, st);
     s.spairs = w2 ? s.pairs_alt : s.pairs;
-    // 5. ranges
     cudaMemsetAsync(s.tile_off, 0, sizeof(int) * (size_t)VT, st);
     cudaMemsetAsync(s.tile_end, 0, sizeof(int) * (size_t)VT, st);
     cudaMemsetAsync(s.first_active, 0x7f, sizeof(int) * (size_t)VT, st);
     k_ranges<<<148 * 8, 256, 0, st>>>(s);
     k_max_list<<<148, 256, 0, st>>>(s);
-    g_launches += 8;
+    g_launches += 2;
 }
 
 }  // namespace cls

@@ -332,7 +332,6 @@ k_project_exact(const float4 *__restrict__ mean_op, const float4 *__restrict__ q
         sh_color_raw<D>(sh, n, i, dir, Y, col);
         // ---- record ----
         const float uh = __double2float_rn(p.u), vh = __double2float_rn(p.v);
-        s.rec_xy[slot] = make_float4(uh, __double2float_rn(p.u - (double)uh), vh, __double2float_rn(p.v - (double)vh));
         const double o64 = 1.0 / (1.0 + exp(-(double)mo.w));
         // scaled LDL^T coefficients of the exponent (raster_q, reading R29): pivot on the larger
         // diagonal conic entry; conic a = C/det >= c = A/det  <=>  C >= A
@@ -344,29 +343,16 @@ k_project_exact(const float4 *__restrict__ mean_op, const float4 *__restrict__ q
             const double k = sqrt(CLS_KAPPA * p.cc);
             a1 = k * (-p.B / p.A); a2 = k; b1 = sqrt(CLS_KAPPA / p.A); b2 = 0.0;
         }
-        s.rec_co[slot] = make_float4(__double2float_rn(a1), __double2float_rn(a2), __double2float_rn(b1),
-                                     __double2float_rn(b2));   // == cof below
-        s.rec_rgb[slot] = make_float4(fmaxf(col[0], 0.0f), fmaxf(col[1], 0.0f), fmaxf(col[2], 0.0f), (float)o64);
         // pre-exponential test threshold: alpha >= 1/255 needs q <= 2 ln(255 o); margin covers fp32
         const double qc = CLS_KAPPA * (2.0 * log(255.0 * o64) * (1.0 + 1e-6) + 2e-3);
-        const float qcf = __double2float_ru(qc);
-        const float4 cof = make_float4(__double2float_rn(a1), __double2float_rn(a2), __double2float_rn(b1),
-                                       __double2float_rn(b2));
-        const int2 rect = make_int2(p.x0 | (p.y0 << 16), p.x1 | (p.y1 << 16));
-        const int2 meta = make_int2(i, v | (ordi >= 0 ? (int)0x80000000u : 0));
-        s.rec_aux[slot] = make_float2(qcf, __int_as_float(ordi));
-        s.rec_rect[slot] = rect;
-        s.rec_meta[slot] = meta;
-        // active tiles the alpha-footprint reaches (binning, k_bin.cu) from the stored fields; tall
-        // footprints (> FOOT_SMALL_ROWS tile rows) go to a list counted warp-per-record (no divergence)
-        if (p.y1 - p.y0 <= FOOT_SMALL_ROWS) {
-            const float4 xyf = make_float4(uh, __double2float_rn(p.u - (double)uh), vh, __double2float_rn(p.v - (double)vh));
-            const FootRec f = foot_make((unsigned)slot, rect, meta, xyf, cof, qcf);
-            const int W32 = (TX + 31) >> 5;
-            s.rcnt[slot] = foot_count(f, s.rowmask + (size_t)v * TY * W32, W32);
-        } else {
-            s.big[atomicAdd(&s.cnt->n_big, 1)] = (unsigned)slot;
-        }
+        Rec R;
+        R.xy = make_float4(uh, __double2float_rn(p.u - (double)uh), vh, __double2float_rn(p.v - (double)vh));
+        R.co = make_float4(__double2float_rn(a1), __double2float_rn(a2), __double2float_rn(b1), __double2float_rn(b2));
+        R.rgb = make_float4(fmaxf(col[0], 0.0f), fmaxf(col[1], 0.0f), fmaxf(col[2], 0.0f), (float)o64);
+        R.aux = make_float4(__double2float_ru(qc), __int_as_float(ordi), __int_as_float(p.x0 | (p.y0 << 16)),
+                            __int_as_float(p.x1 | (p.y1 << 16)));
+        s.rec[slot] = R;
+        s.rec_gid[slot] = i;
         // depth-sort key (reading R13): view, then fp32 round-to-nearest of the fp64 depth
         // (positive floats order as their bit patterns); value: the record id
         s.rkey[slot] = ((unsigned long long)v << 32) | __float_as_uint(__double2float_rn(p.tz));

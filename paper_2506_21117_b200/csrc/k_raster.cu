@@ -31,11 +31,9 @@ namespace cls {
 __device__ __forceinline__ void stage(const Scratch &s, unsigned val, int tx, int ty, float4 &sa, float4 &sb,
                                       float4 &sc)
 {
-    const unsigned rid = val & 0x7fffffffu;
-    const float4 xy = s.rec_xy[rid];
-    const float4 co = s.rec_co[rid];
-    const float4 rgb = s.rec_rgb[rid];
-    const float2 ax = s.rec_aux[rid];
+    const Rec &R = s.srec[val & 0x7fffffffu];
+    const float4 xy = R.xy, co = R.co, rgb = R.rgb;
+    const float2 ax = make_float2(R.aux.x, R.aux.y);
     const double dx0 = ((double)xy.x - (double)(CLS_TILE * tx)) + (double)xy.y;
     const double dy0 = ((double)xy.z - (double)(CLS_TILE * ty)) + (double)xy.w;
     const double S0 = fma((double)co.y, dy0, (double)co.x * dx0);
@@ -336,7 +334,7 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
             for (int j = tid; j < bend - bstart; j += RT_THREADS) {
                 const unsigned val = (unsigned)s.spairs[off + bstart + j];
                 stage(s, val, tx, ty, sa[j], sb[j], sc[j]);
-                const float4 xy = s.rec_xy[val & 0x7fffffffu];
+                const float4 xy = s.srec[val & 0x7fffffffu].xy;
                 sd[j] = make_float2(__double2float_rn(((double)xy.x - (double)(CLS_TILE * tx)) + (double)xy.y),
                                     __double2float_rn(((double)xy.z - (double)(CLS_TILE * ty)) + (double)xy.w));
             }

@@ -21,8 +21,8 @@ namespace cls {
 
 #define RS_THREADS 256
 #define RS_WARPS (RS_THREADS / 32)
-#define RS_ITEMS 16
-#define RS_TILE (RS_THREADS * RS_ITEMS)   // 4096 elements per tile, 512 per warp
+#define RS_ITEMS 8
+#define RS_TILE (RS_THREADS * RS_ITEMS)   // 2048 elements per tile, 256 per warp
 
 __device__ __forceinline__ void rs_block_range(int n, int &t0, int &t1)
 {
@@ -74,8 +74,22 @@ __global__ void __launch_bounds__(256) k_rs_scan(unsigned *__restrict__ counts, 
     if (lane == 0) totals[d] = carry;
 }
 
+// lanes of the warp whose digit equals mine: BITS ballots (cheap, pipelined) instead of match.any
+template <int BITS>
+__device__ __forceinline__ unsigned rs_peers(int d, bool act)
+{
+    unsigned m = __ballot_sync(0xffffffffu, act);
+#pragma unroll
+    for (int b = 0; b < BITS; b++) {
+        const bool bit = (d >> b) & 1;
+        const unsigned v = __ballot_sync(0xffffffffu, bit);
+        m &= bit ? v : ~v;
+    }
+    return act ? m : 0u;
+}
+
 template <int BITS, bool VALS>
-__global__ void __launch_bounds__(RS_THREADS, 3)
+__global__ void __launch_bounds__(RS_THREADS, 4)
 k_rs_downsweep(const unsigned long long *__restrict__ kin, unsigned long long *__restrict__ kout,
                const unsigned *__restrict__ vin, unsigned *__restrict__ vout, const int *__restrict__ n_ptr, int max_n,
                int shift, const unsigned *__restrict__ counts, const unsigned *__restrict__ totals,
@@ -132,36 +146,29 @@ k_rs_downsweep(const unsigned long long *__restrict__ kin, unsigned long long *_
         for (int c = tid; c < BINS * WP; c += RS_THREADS) run[c] = 0u;
         __syncthreads();
         // ---- stable ranking: warp w owns tile elements [w*512, (w+1)*512), rounds in order ----
-        // all 16 loads in flight at once; only the digits stay live (keys are re-read at staging,
-        // L1/L2 hits), so registers stay low enough for 3 blocks per SM
-        int mine[RS_ITEMS];   // digit, then (rank << 12) | digit
-        {
-            unsigned long long kk[RS_ITEMS];
+        unsigned long long kk[RS_ITEMS];
+        unsigned vv[VALS ? RS_ITEMS : 1];
+        int mine[RS_ITEMS];   // (rank << 12) | digit
 #pragma unroll
-            for (int r = 0; r < RS_ITEMS; r++) {
-                const int j = warp * (RS_TILE / RS_WARPS) + r * 32 + lane;
-                kk[r] = j < tn ? __ldcs(kin + base + j) : 0ull;
-            }
-#pragma unroll
-            for (int r = 0; r < RS_ITEMS; r++) {
-                const int j = warp * (RS_TILE / RS_WARPS) + r * 32 + lane;
-                mine[r] = j < tn ? (int)((unsigned)(kk[r] >> shift) & (BINS - 1)) : BINS + lane;
-            }
+        for (int r = 0; r < RS_ITEMS; r++) {
+            const int j = warp * (RS_TILE / RS_WARPS) + r * 32 + lane;
+            kk[r] = j < tn ? kin[base + j] : 0ull;
+            if (VALS) vv[r] = j < tn ? vin[base + j] : 0u;
         }
 #pragma unroll
         for (int r = 0; r < RS_ITEMS; r++) {
             const int j = warp * (RS_TILE / RS_WARPS) + r * 32 + lane;
             const bool act = j < tn;
-            const int d = mine[r];
-            const unsigned peers = __match_any_sync(0xffffffffu, d);
+            const int d = (int)((unsigned)(kk[r] >> shift) & (BINS - 1));
+            const unsigned peers = rs_peers<BITS>(d, act);
             const int leader = __ffs(peers) - 1;
             unsigned b = 0u;
             if (act && lane == leader) {   // the warp owns column `warp` of run[]: no atomics needed
                 b = run[d * WP + warp];
                 run[d * WP + warp] = b + (unsigned)__popc(peers);
             }
-            b = __shfl_sync(0xffffffffu, b, leader);
-            mine[r] = (int)(((b + __popc(peers & lt)) << 12) | (unsigned)(d & (BINS - 1)));
+            b = __shfl_sync(0xffffffffu, b, act ? leader : 0);
+            mine[r] = (int)(((b + __popc(peers & lt)) << 12) | (unsigned)d);
         }
         __syncthreads();
         // ---- exclusive scan of run[] in (digit, warp) order ----
@@ -208,8 +215,8 @@ k_rs_downsweep(const unsigned long long *__restrict__ kin, unsigned long long *_
             if (j < tn) {
                 const int d = mine[r] & (BINS - 1);
                 const unsigned lp = run[d * WP + warp] + ((unsigned)mine[r] >> 12);
-                skey[lp] = __ldcs(kin + base + j);
-                if (VALS) sval[lp] = __ldcs(vin + base + j);
+                skey[lp] = kk[r];
+                if (VALS) sval[lp] = vv[r];
             }
         }
         __syncthreads();

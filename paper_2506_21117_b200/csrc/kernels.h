@@ -26,14 +26,17 @@ void launch_active_mask(const Params &g, const StepDims &d, const CamSet &cams, 
 void launch_project_cand(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st);
 void launch_project_exact(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st);
 // (3) binning: record depth sort, exact pair counts, ordered emission, pair sort by tile (k_bin.cu)
-void launch_bin(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st);
+void launch_bin_recsort(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st);
+void launch_bin_count(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st);
+void launch_bin_emit(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st);
+void launch_bin_pairsort(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st);
 // device-wide stable LSD radix sort (k_sort.cu); returns 1 if the result is in the *_alt buffers
 int radix_sort_u64(unsigned long long *keys, unsigned long long *keys_alt, unsigned *vals, unsigned *vals_alt,
                    const int *n_ptr, int max_n, int begin_bit, int end_bit, int digit_bits, unsigned *counts,
                    unsigned *totals, const int *skip, cudaStream_t st);
 void scan_excl_u32(const unsigned *in, unsigned *out, const int *n_ptr, int max_n, unsigned long long *status,
                    int *ticket, unsigned long long *total, const int *skip, cudaStream_t st);
-#define RS_GRID (148 * 3)
+#define RS_GRID (148 * 4)
 
 // (4) forward compositing + fused L1                           (k_raster.cu)
 void launch_fwd(const StepDims &d, const CamSet &cams, const Scratch &s, const float *targets, float *images,
