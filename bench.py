@@ -253,7 +253,7 @@ def run_ours(args):
             "e2e": e2e, "gpu_launches": int(launches), "roofline": roof, "clocks": clocks,
             "kernels_ms_per_step": {k: round(v["ms"] / args.steps, 4) for k, v in per.items()},
             "kernel_rates": groups,
-            "counts": {k: stats[k] for k in ("n_records", "n_pairs", "n_items", "max_list", "n_tall_records",
+            "counts": {k: stats[k] for k in ("n_records", "n_pairs", "n_items", "max_list", "n_units",
                                              "n_fwd_evals", "n_bwd_evals", "n_candidates", "n_kept_pairs")},
         }
         if world == 1 and not args.no_cpu_baseline:

@@ -20,12 +20,13 @@
  *   - A ctx is bound to one device, is not thread-safe, and owns all scratch.
  *
  * Data layout of a scene with n Gaussians and SH degree D (0..3), K=(D+1)^2,
- * K4 = ceil(3K/4) ("chunk-major SoA", one float4 per Gaussian per chunk):
+ * K4 = ceil(3K/4): geometry as float4 SoA (streamed by every all-Gaussian kernel), SH and the
+ * Adam moments Gaussian-major (gathered per record / per active row: whole 32 B sectors):
  *   mean_op   float4[n]      (x, y, z, opacity logit)              -- P:102 mean, opacity
  *   quat      float4[n]      (w, x, y, z), not necessarily unit    -- rotation (R17)
  *   log_scale float4[n]      (log sx, log sy, log sz, pad)         -- scale = exp (R18)
- *   sh        float4[K4][n]  coefficient k, channel c at float 3k+c of the Gaussian's
- *                            K4 chunks (chunk j of Gaussian i at sh[j*n + i])
+ *   sh        float4[n][K4]  coefficient k, channel c at float 3k+c of the Gaussian's
+ *                            K4 chunks (chunk j of Gaussian i at sh[i*K4 + j])
  * A parameter "row" is the 3 + K4 float4 chunks of one Gaussian in the order
  * (mean_op, quat, log_scale, sh chunks) -- ROW4 = 3 + K4 float4 = 16 (D=0) or 60 (D=3) floats.
  */
@@ -76,7 +77,7 @@ typedef struct {
     const float *mean_op;      /* (device) float4[n] */
     const float *quat;         /* (device) float4[n] */
     const float *log_scale;    /* (device) float4[n] */
-    const float *sh;           /* (device) float4[K4][n] */
+    const float *sh;           /* (device) float4[n][K4] */
 } cls_gaussians;
 
 /* Capacities fixed at cls_create; scratch is sized from them once. */
@@ -86,7 +87,7 @@ typedef struct {
     int64_t max_pairs;         /* sum over views of (Gaussian, active tile) pairs, < 2^31 */
     int64_t max_active;        /* |O^t| (sizes the per-view 2D gradient buffer) */
     int32_t max_views;         /* views per call, <= CLS_MAX_VIEWS */
-    int32_t max_width, max_height;
+    int32_t max_width, max_height;   /* 16 .. 16384 */
 } cls_limits;
 
 #define CLS_MAX_VIEWS 64
@@ -104,7 +105,7 @@ typedef struct {
     int32_t overflow;          /* bit 0 records, bit 1 pairs, bit 2 active set */
     int32_t n_views;
     int64_t max_list;          /* longest per-tile list */
-    int64_t n_tall_records;    /* records whose footprint spans > 4 tile rows (binned warp-per-record) */
+    int64_t n_units;           /* (record, tile row) work units of the binning */
     int64_t n_fwd_evals;       /* (pixel, list entry) evaluations of the forward compositing */
     int64_t n_bwd_evals;       /* (pixel, list entry) evaluations of the backward walk (after its bwd) */
     int64_t n_candidates;      /* (Gaussian, view) pairs passing the fp32 projection pre-test */
@@ -180,7 +181,7 @@ cls_status cls_render_bwd(cls_ctx *ctx, const cls_gaussians *g, const float *dL_
  *   theta <- theta - lr (m / (1 - b1^step)) / (sqrt(v / (1 - b2^step)) + eps).
  * Rows not in O^t, and pad lanes, are never read-modified-written.
  *   mean_op, quat, log_scale, sh  (device) parameters, layout as cls_gaussians, updated in place
- *   m, v         (device) float4[3 + K4][n] moments, chunk c of Gaussian i at [c*n + i]
+ *   m, v         (device) float4[n][3 + K4] moments, chunk c of Gaussian i at [i*(3+K4) + c]
  *   grad_active  (device) float4[A][ROW4] (e.g. from cls_render_bwd, all-reduced across ranks)
  *   lr           (host) float[6]: mean, quat, scale, opacity, sh DC, sh rest
  *   step         Adam step t >= 1

@@ -7,7 +7,6 @@
 #include "../../include/cls.h"
 
 #define CLS_TILE 16
-#define FOOT_SMALL_ROWS 4   // footprints of at most this many tile rows are handled per thread
 #define CLS_BLOCK_PIX 256
 
 namespace cls {
@@ -46,8 +45,9 @@ struct Counters {
     int tiles_scan_tiles;   // look-back ticket (tile scan)
     unsigned long long n_pairs;     // (record, active tile) pairs kept by the exact footprint culling
     int n_pairs32;          // min(n_pairs, max_pairs): element count of the pair sort
-    int n_big;              // records with tall footprints (warp-per-record counting / emission)
-    int scan_ticket;        // tile ticket of the order-preserving scan of the per-record pair counts
+    unsigned long long n_units;     // (record, tile row) work units of the binning
+    int n_units32;
+    int scan_ticket, scan_ticket2;  // tile tickets of the two order-preserving scans of the binning
     int n_items;
     int fwd_work, bwd_work;
     int overflow;           // bit0 records, bit1 pairs, bit2 active set
@@ -90,8 +90,11 @@ struct Scratch {
     unsigned *rval, *rval_alt;
     const unsigned *rsorted;        // record ids in (view, depth, Gaussian index) order (rval or rval_alt)
     const unsigned long long *rskey;   // the sorted keys (view in the high word)
-    unsigned *rcnt, *roff;          // per sorted record: active tiles its footprint reaches, exclusive offsets
-    unsigned *big;                  // sorted records whose footprint spans > FOOT_SMALL_ROWS tile rows
+    unsigned *rcnt, *roff;          // per sorted record: tile rows of its footprint rect, their exclusive offsets
+    unsigned *urec;                 // per (record, tile row) unit: the sorted record
+    uint2 *uinfo;                   // per unit: (record | active << 31, ty | lo << 10 | hi << 20)
+    unsigned *ucnt, *uoff;          // per unit: active tiles reached, their exclusive offsets (pair positions)
+    long long max_units;
     unsigned long long *st_scan;    // look-back status of the offsets scan
     // tiles
     int *tile_end;          // [V*T] end of the tile's range in the sorted pairs (== tile_off if empty)
@@ -150,6 +153,49 @@ __device__ __forceinline__ unsigned long long lookback(unsigned long long *statu
     }
     __threadfence();
     vs[tile] = LB_FLAG_PRE | (prefix + agg);
+    return prefix;
+}
+
+// Warp-wide decoupled look-back (call from all 32 lanes of ONE warp): the 32 predecessors are
+// inspected at once, so a long chain of tiles that have published only their aggregate costs
+// one status load per 32 tiles instead of one per tile.  Returns the exclusive prefix.
+__device__ __forceinline__ unsigned long long lookback_warp(unsigned long long *status, int tile,
+                                                            unsigned long long agg)
+{
+    volatile unsigned long long *vs = status;
+    const int lane = threadIdx.x & 31;
+    if (tile == 0) {
+        if (lane == 0) vs[0] = LB_FLAG_PRE | agg;
+        __syncwarp();
+        return 0ull;
+    }
+    if (lane == 0) {
+        vs[tile] = LB_FLAG_AGG | agg;
+        __threadfence();
+    }
+    __syncwarp();
+    unsigned long long prefix = 0;
+    int base = tile - 1;
+    while (true) {
+        const int j = base - lane;
+        unsigned long long s = LB_FLAG_PRE;   // before tile 0: an empty inclusive prefix
+        if (j >= 0) {
+            do {
+                s = vs[j];
+            } while ((s >> 62) == 0ull);
+        }
+        const unsigned pre = __ballot_sync(0xffffffffu, (s >> 62) == 2ull);
+        const int stop = pre ? __ffs(pre) - 1 : 31;   // nearest predecessor with an inclusive prefix
+        unsigned long long v = lane <= stop ? (s & LB_PAYLOAD) : 0ull;
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        prefix += v;
+        if (pre) break;
+        base -= 32;
+    }
+    if (lane == 0) {
+        __threadfence();
+        vs[tile] = LB_FLAG_PRE | (prefix + agg);
+    }
     return prefix;
 }
 
@@ -316,7 +362,7 @@ __device__ __forceinline__ void sh_color_raw(const float4 *__restrict__ sh, int 
     col[0] = col[1] = col[2] = 0.5f;
 #pragma unroll
     for (int ch4 = 0; ch4 < K4; ch4++) {
-        const float4 f = __ldg(sh + (size_t)ch4 * n + i);
+        const float4 f = __ldg(sh + (size_t)i * K4 + ch4);
 #pragma unroll
         for (int l = 0; l < 4; l++) {
             const int e = 4 * ch4 + l;

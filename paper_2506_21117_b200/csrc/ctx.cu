@@ -131,7 +131,7 @@ cls_status cls_destroy(cls_ctx *c)
     cudaSetDevice(c->device);
     void *ptrs[] = {c->s.idx, c->s.ord, c->s.st_member, c->s.mask, c->s.sat, c->s.rowmask, c->s.view_bbox, c->s.rec,
                     c->s.srec, c->s.rec_gid, c->s.cand, c->s.rkey,
-                    c->s.rkey_alt, c->s.rval, c->s.rval_alt, c->s.rcnt, c->s.big, c->s.roff, c->s.st_scan, c->s.tile_end,
+                    c->s.rkey_alt, c->s.rval, c->s.rval_alt, c->s.rcnt, c->s.urec, c->s.uinfo, c->s.ucnt, c->s.uoff, c->s.roff, c->s.st_scan, c->s.tile_end,
                     c->s.tile_off, c->s.st_tiles, c->s.items, c->s.item_of_tile, c->s.first_active, c->s.pairs,
                     c->s.pairs_alt, c->s.rs_counts, c->s.rs_totals, c->s.px_T, c->s.px_last, c->s.px_dl,
                     c->s.item_loss, c->s.grad2d, c->s.cnt};
@@ -153,7 +153,8 @@ cls_status cls_create(cls_ctx **out, int device, const cls_limits *lim)
     *out = nullptr;
     if (lim->max_gaussians <= 0 || lim->max_views <= 0 || lim->max_views > CLS_MAX_VIEWS || lim->max_width < 16 ||
         lim->max_height < 16 || lim->max_records <= 0 || lim->max_pairs <= 0 || lim->max_pairs >= (1ll << 31) ||
-        lim->max_active <= 0 || lim->max_gaussians >= (1ll << 31) || lim->max_records >= (1ll << 31))
+        lim->max_active <= 0 || lim->max_gaussians >= (1ll << 31) || lim->max_records >= (1ll << 31) ||
+        lim->max_width > 16384 || lim->max_height > 16384)
         return CLS_ERR_INVALID_ARGUMENT;
     if (cudaSetDevice(device) != cudaSuccess) return CLS_ERR_CUDA;
     cls_ctx *c = new (std::nothrow) cls_ctx();
@@ -172,7 +173,8 @@ cls_status cls_create(cls_ctx **out, int device, const cls_limits *lim)
               dalloc(&s.sat, SAT) && dalloc(&s.rowmask, V * c->maxTY * ((c->maxTX + 31) / 32)) &&
               dalloc(&s.view_bbox, V) && dalloc(&s.rec, R) && dalloc(&s.srec, R) && dalloc(&s.rec_gid, R) &&
               dalloc(&s.cand, R + R / 2 + 1024) && dalloc(&s.rkey, R) && dalloc(&s.rkey_alt, R) && dalloc(&s.rval, R) &&
-              dalloc(&s.rval_alt, R) && dalloc(&s.rcnt, R) && dalloc(&s.big, R) && dalloc(&s.roff, R) && dalloc(&s.st_scan, R / 2048 + 2) &&
+              dalloc(&s.rval_alt, R) && dalloc(&s.rcnt, R) && dalloc(&s.urec, P) && dalloc(&s.uinfo, P) &&
+              dalloc(&s.ucnt, P) && dalloc(&s.uoff, P) && dalloc(&s.roff, R) && dalloc(&s.st_scan, std::max(R, P) / 2048 + 2) &&
               dalloc(&s.tile_end, VT) && dalloc(&s.tile_off, VT) && dalloc(&s.st_tiles, VT / 2048 + 2) &&
               dalloc(&s.items, VT) && dalloc(&s.item_of_tile, VT) && dalloc(&s.first_active, VT) &&
               dalloc(&s.pairs, P) && dalloc(&s.pairs_alt, P) && dalloc(&s.rs_counts, (size_t)512 * RS_GRID) &&
@@ -191,6 +193,7 @@ cls_status cls_create(cls_ctx **out, int device, const cls_limits *lim)
     s.max_records = (long long)R;
     s.max_cand = (long long)(R + R / 2 + 1024);
     s.max_pairs = (long long)P;
+    s.max_units = (long long)P;   // units (record, tile row) are bounded like the pairs
     s.max_items = (int)VT;
     memset(c->h_cnt, 0, sizeof(Counters));
     *out = c;
@@ -403,7 +406,7 @@ cls_status cls_stats(cls_ctx *c, cls_stats_t *out)
     for (int v = 0; v < c->dims.V; v++) out->n_active_tiles[v] = h.active_tiles[v];
     out->overflow = h.overflow | ovf;
     out->max_list = h.max_list;
-    out->n_tall_records = h.n_big;
+    out->n_units = (int64_t)h.n_units;
     out->n_candidates = h.n_cand;
     out->n_kept_pairs = (int64_t)h.n_pairs;
     out->n_fwd_evals = (int64_t)h.fwd_evals;

@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(256) k_adam(const __grid_constant__ AdamArgs a
             lr4[0] = lr4[1] = lr4[2] = a.lr[2];
             lr4[3] = -1.0f;   // pad lane
         } else {
-            pp = a.sh + (size_t)(c - 3) * a.n + i;
+            pp = a.sh + (size_t)i * a.K4 + (c - 3);
 #pragma unroll
             for (int l = 0; l < 4; l++) {
                 const int f = 4 * (c - 3) + l;
@@ -59,16 +59,16 @@ __global__ void __launch_bounds__(256) k_adam(const __grid_constant__ AdamArgs a
             }
         }
         float4 p = *pp;
-        float4 m = a.m[(size_t)c * a.n + i];
-        float4 v = a.v[(size_t)c * a.n + i];
+        float4 m = a.m[(size_t)i * a.ROW4 + c];
+        float4 v = a.v[(size_t)i * a.ROW4 + c];
         const float4 g = a.g[(size_t)k * a.ROW4 + c];
         if (lr4[0] >= 0.f) adam_lane(p.x, m.x, v.x, g.x, lr4[0], a);
         if (lr4[1] >= 0.f) adam_lane(p.y, m.y, v.y, g.y, lr4[1], a);
         if (lr4[2] >= 0.f) adam_lane(p.z, m.z, v.z, g.z, lr4[2], a);
         if (lr4[3] >= 0.f) adam_lane(p.w, m.w, v.w, g.w, lr4[3], a);
         *pp = p;
-        a.m[(size_t)c * a.n + i] = m;
-        a.v[(size_t)c * a.n + i] = v;
+        a.m[(size_t)i * a.ROW4 + c] = m;
+        a.v[(size_t)i * a.ROW4 + c] = v;
     }
 }
 

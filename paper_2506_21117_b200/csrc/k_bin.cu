@@ -6,9 +6,9 @@
 // R13).  B200 design: no per-pair depth keys are sorted at all.
 //   1. the ~6M records are sorted ONCE by (view, fp32 depth) with a stable LSD radix sort
 //      (k_sort.cu); runs of equal keys are then ordered by Gaussian index (k_rec_ties);
-//   2. the records are gathered into that order (64 B each); per sorted record, the number of
-//      ACTIVE tiles its alpha >= 1/255 footprint reaches (closed-form x-interval of the ellipse per
-//      tile row, row bitmasks) -> order-preserving exclusive scan -> contiguous output ranges;
+//   2. the records are gathered into that order (64 B each); the work units are (record, tile row)
+//      pairs: per unit the closed-form x-interval of the alpha >= 1/255 ellipse over the row band
+//      and the number of ACTIVE tiles in it (row bitmasks) -> order-preserving exclusive scan;
 //   3. emission at those ranges (no atomics): pair = (view*T + tile) << 32 | sorted record;
 //   4. a stable 2-pass LSD radix sort of the pairs by their (view, tile) key keeps the
 //      depth order inside every tile;
@@ -102,78 +102,64 @@ __global__ void k_rec_ties(Scratch s, const unsigned long long *__restrict__ key
     }
 }
 
-// 2. records gathered into (view, depth, index) order (one 64 B record per access), and the
-// number of ACTIVE tiles each footprint reaches (row bitmasks, popc); tall footprints
-// (> FOOT_SMALL_ROWS tile rows) are listed for the warp-per-record kernels (no divergence)
-__global__ void __launch_bounds__(256) k_permute(const __grid_constant__ CamSet cams, Scratch s)
+// 2. records gathered into (view, depth, index) order (one 64 B record per access) and the
+// number of tile rows of each footprint rect: the work units of the binning are (record, tile row)
+// pairs, so every thread does the same small amount of work however tall a footprint is.
+__global__ void __launch_bounds__(256) k_permute(Scratch s)
 {
     const int n = s.cnt->overflow ? 0 : min(s.cnt->n_records, (int)s.max_records);
-    const int TY = cams.TY, W32 = (cams.TX + 31) >> 5;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const Rec R = s.rec[s.rsorted[i]];
         s.srec[i] = R;
-        const int rb = __float_as_int(R.aux.w), ra = __float_as_int(R.aux.z);
-        unsigned cnt = 0u;
-        if ((rb >> 16) - (ra >> 16) <= FOOT_SMALL_ROWS) {
-            const int view = (int)(s.rskey[i] >> 32);
-            const FootRec f = foot_make(R, view, 0u);
-            cnt = foot_count(f, s.rowmask + (size_t)view * TY * W32, W32);
-        } else {
-            s.big[atomicAdd(&s.cnt->n_big, 1)] = (unsigned)i;
-        }
-        s.rcnt[i] = cnt;
+        s.rcnt[i] = (unsigned)((__float_as_int(R.aux.w) >> 16) - (__float_as_int(R.aux.z) >> 16));
     }
 }
 
-// 2b. tall footprints: one warp per record, lanes over its tile rows
-__global__ void __launch_bounds__(256) k_big_count(const __grid_constant__ CamSet cams, Scratch s)
+// unit -> record map: urec[roff[i] + k] = i for the record's k-th tile row
+__global__ void __launch_bounds__(256) k_fill_units(Scratch s)
 {
-    const int nb = s.cnt->overflow ? 0 : s.cnt->n_big;
+    const int n = s.cnt->overflow ? 0 : min(s.cnt->n_records, (int)s.max_records);
+    const unsigned long long U = s.cnt->n_units;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if ((long long)U > s.max_units) atomicOr(&s.cnt->overflow, 2);
+        s.cnt->n_units32 = (int)min((unsigned long long)s.max_units, U);
+    }
+    if ((long long)U > s.max_units) return;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const unsigned o = s.roff[i], c = s.rcnt[i];
+        for (unsigned k = 0; k < c; k++) s.urec[o + k] = (unsigned)i;
+    }
+}
+
+// per unit (record i, tile row ty): the footprint's tile columns [lo, hi] in that row and the
+// number of ACTIVE tiles among them; uinfo = (i | active << 31, ty | lo << 10 | hi << 20)
+__global__ void __launch_bounds__(256) k_unit_count(const __grid_constant__ CamSet cams, Scratch s)
+{
+    const int U = s.cnt->overflow ? 0 : s.cnt->n_units32;
     const int TY = cams.TY, W32 = (cams.TX + 31) >> 5;
-    const int lane = threadIdx.x & 31;
-    for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nb; k += (gridDim.x * blockDim.x) >> 5) {
-        const unsigned i = s.big[k];
+    for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < U; u += gridDim.x * blockDim.x) {
+        const unsigned i = s.urec[u];
         const FootRec f = foot_load(s, i);
-        const unsigned *rmv = s.rowmask + (size_t)f.view * TY * W32;
+        const int ty = f.y0 + (int)((unsigned)u - s.roff[i]);
+        int lo, hi;
         unsigned cnt = 0u;
-        for (int ty = f.y0 + lane; ty < f.y1; ty += 32) {
-            int lo, hi;
-            if (!foot_row(f, ty, lo, hi)) continue;
-            for (int w = lo >> 5; w <= (hi >> 5); w++) cnt += __popc(row_bits(rmv + ty * W32, w, lo, hi));
+        if (foot_row(f, ty, lo, hi)) {
+            const unsigned *rm = s.rowmask + ((size_t)f.view * TY + ty) * W32;
+            for (int w = lo >> 5; w <= (hi >> 5); w++) cnt += __popc(row_bits(rm, w, lo, hi));
+        } else {
+            lo = 1; hi = 0;
         }
-        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-        if (lane == 0) s.rcnt[i] = cnt;
+        s.ucnt[u] = cnt;
+        s.uinfo[u] = make_uint2(f.w, (unsigned)ty | ((unsigned)lo << 10) | ((unsigned)(hi & 1023) << 20));
     }
 }
 
-// pairs of tile row ty of footprint f, written from `out`
-template <typename OUT>
-__device__ __forceinline__ void emit_row(const FootRec &f, const unsigned *rmv, int W32, int TX, unsigned long long vb,
-                                         int ty, int lo, int hi, OUT &&out)
+// 3. emission: unit u's pairs at uoff[u] .. + ucnt[u]; units are in (sorted record, row) order, so
+// consecutive threads write consecutive ranges (coalesced) and the pairs come out in record order.
+__global__ void __launch_bounds__(256) k_emit(const __grid_constant__ CamSet cams, Scratch s)
 {
-    for (int w = lo >> 5; w <= (hi >> 5); w++) {
-        unsigned bits = row_bits(rmv + ty * W32, w, lo, hi);
-        while (bits) {
-            const int tx = 32 * w + __ffs(bits) - 1;
-            bits &= bits - 1;
-            out(((vb + (unsigned long long)(ty * TX + tx)) << 32) | f.w);
-        }
-    }
-}
-
-// 3. emission in sorted-record order: record i's pairs at roff[i] .. roff[i] + rcnt[i], tiles in
-// (row, column) order -- any fixed order works, the stable pair sort only needs record order.
-// A warp's 32 consecutive records own one contiguous output range: staged in shared memory and
-// stored with coalesced writes (ranges over EM_CAP write through).  Tall footprints are written
-// afterwards by k_emit_big (their part of a staged range is overwritten then).
-#define EM_WARPS 8
-#define EM_CAP 512
-
-__global__ void __launch_bounds__(EM_WARPS * 32) k_emit(const __grid_constant__ CamSet cams, Scratch s)
-{
-    __shared__ unsigned long long stage_buf[EM_WARPS][EM_CAP];
     if (s.cnt->overflow) return;
-    const int n = min(s.cnt->n_records, (int)s.max_records);
+    const int U = s.cnt->n_units32;
     const unsigned long long total = s.cnt->n_pairs;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if ((long long)total > s.max_pairs) atomicOr(&s.cnt->overflow, 2);
@@ -181,68 +167,22 @@ __global__ void __launch_bounds__(EM_WARPS * 32) k_emit(const __grid_constant__ 
     }
     if ((long long)total > s.max_pairs) return;
     const int TX = cams.TX, TY = cams.TY, T = cams.T, W32 = (TX + 31) >> 5;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    unsigned long long *buf = stage_buf[wid];
-    for (int i0 = (blockIdx.x * EM_WARPS + wid) * 32; i0 < n; i0 += gridDim.x * EM_WARPS * 32) {
-        const int i = i0 + lane;
-        const int il = min(i0 + 31, n - 1);
-        const unsigned base = s.roff[i0];
-        const unsigned end = s.roff[il] + s.rcnt[il];
-        const bool staged = end - base <= EM_CAP;
-        if (i < n && s.rcnt[i] != 0u) {
-            const FootRec f = foot_load(s, (unsigned)i);
-            if (f.y1 - f.y0 <= FOOT_SMALL_ROWS) {
-                const unsigned *rmv = s.rowmask + (size_t)f.view * TY * W32;
-                const unsigned long long vb = (unsigned long long)f.view * T;
-                unsigned o = s.roff[i];
-                for (int ty = f.y0; ty < f.y1; ty++) {
-                    int lo, hi;
-                    if (!foot_row(f, ty, lo, hi)) continue;
-                    emit_row(f, rmv, W32, TX, vb, ty, lo, hi, [&](unsigned long long pv) {
-                        if (staged) buf[o - base] = pv;
-                        else s.pairs[o] = pv;
-                        o++;
-                    });
-                }
+    for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < U; u += gridDim.x * blockDim.x) {
+        if (s.ucnt[u] == 0u) continue;
+        const uint2 inf = s.uinfo[u];
+        const unsigned i = inf.x & 0x7fffffffu;
+        const int ty = (int)(inf.y & 1023u), lo = (int)((inf.y >> 10) & 1023u), hi = (int)(inf.y >> 20);
+        const int view = (int)(s.rskey[i] >> 32);
+        const unsigned *rm = s.rowmask + ((size_t)view * TY + ty) * W32;
+        const unsigned long long kb = ((unsigned long long)view * T + (unsigned long long)ty * TX) << 32;
+        unsigned long long *out = s.pairs + s.uoff[u];
+        for (int w = lo >> 5; w <= (hi >> 5); w++) {
+            unsigned bits = row_bits(rm, w, lo, hi);
+            while (bits) {
+                const int tx = 32 * w + __ffs(bits) - 1;
+                bits &= bits - 1;
+                *out++ = (kb + ((unsigned long long)tx << 32)) | inf.x;
             }
-        }
-        __syncwarp();
-        if (staged)
-            for (unsigned j = lane; j < end - base; j += 32) s.pairs[base + j] = buf[j];
-        __syncwarp();
-    }
-}
-
-// 3b. tall footprints: one warp per record; lane offsets from a warp scan of the row counts
-__global__ void __launch_bounds__(256) k_emit_big(const __grid_constant__ CamSet cams, Scratch s)
-{
-    if (s.cnt->overflow) return;
-    const int nb = s.cnt->n_big;
-    const int TX = cams.TX, TY = cams.TY, T = cams.T, W32 = (TX + 31) >> 5;
-    const int lane = threadIdx.x & 31;
-    for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nb; k += (gridDim.x * blockDim.x) >> 5) {
-        const unsigned i = s.big[k];
-        if (s.rcnt[i] == 0u) continue;
-        const FootRec f = foot_load(s, i);
-        const unsigned *rmv = s.rowmask + (size_t)f.view * TY * W32;
-        const unsigned long long vb = (unsigned long long)f.view * T;
-        unsigned base = s.roff[i];
-        for (int ty0 = f.y0; ty0 < f.y1; ty0 += 32) {   // rows in chunks of 32, in order
-            const int ty = ty0 + lane;
-            int lo = 0, hi = -1;
-            unsigned c = 0u;
-            if (ty < f.y1 && foot_row(f, ty, lo, hi))
-                for (int w = lo >> 5; w <= (hi >> 5); w++) c += __popc(row_bits(rmv + ty * W32, w, lo, hi));
-            unsigned inc = c;
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned t = __shfl_up_sync(0xffffffffu, inc, o);
-                if (lane >= o) inc += t;
-            }
-            if (c) {
-                unsigned long long *out = s.pairs + base + inc - c;
-                emit_row(f, rmv, W32, TX, vb, ty, lo, hi, [&](unsigned long long pv) { *out++ = pv; });
-            }
-            base += __shfl_sync(0xffffffffu, inc, 31);
         }
     }
 }
@@ -300,22 +240,25 @@ void launch_bin_recsort(const StepDims &d, const CamSet &cams, Scratch &s, cudaS
     g_launches += 2;
 }
 
-// 2. sorted records, exact per-record pair counts and their offsets
+// 2. sorted records, their (record, tile row) units, exact per-unit pair counts and offsets
 void launch_bin_count(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st)
 {
-    k_permute<<<148 * 8, 256, 0, st>>>(cams, s);
-    k_big_count<<<148 * 8, 256, 0, st>>>(cams, s);
-    scan_excl_u32(s.rcnt, s.roff, &s.cnt->n_records, (int)s.max_records, s.st_scan, &s.cnt->scan_ticket,
+    const int R = (int)s.max_records;
+    k_permute<<<148 * 8, 256, 0, st>>>(s);
+    scan_excl_u32(s.rcnt, s.roff, &s.cnt->n_records, R, s.st_scan, &s.cnt->scan_ticket, &s.cnt->n_units,
+                  &s.cnt->overflow, st);
+    k_fill_units<<<148 * 8, 256, 0, st>>>(s);
+    k_unit_count<<<148 * 8, 256, 0, st>>>(cams, s);
+    scan_excl_u32(s.ucnt, s.uoff, &s.cnt->n_units32, (int)s.max_units, s.st_scan, &s.cnt->scan_ticket2,
                   &s.cnt->n_pairs, &s.cnt->overflow, st);
-    g_launches += 2;
+    g_launches += 3;
 }
 
 // 3. emission
 void launch_bin_emit(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st)
 {
-    k_emit<<<148 * 4, EM_WARPS * 32, 0, st>>>(cams, s);
-    k_emit_big<<<148 * 8, 256, 0, st>>>(cams, s);
-    g_launches += 2;
+    k_emit<<<148 * 8, 256, 0, st>>>(cams, s);
+    g_launches += 1;
 }
 
 // 4. stable sort of the pairs by (view, tile), 5. ranges

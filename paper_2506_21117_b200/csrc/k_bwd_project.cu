@@ -167,7 +167,7 @@ k_bwd_project(const float4 *__restrict__ mean_op, const float4 *__restrict__ qua
             float dd[3] = {0.f, 0.f, 0.f};
 #pragma unroll
             for (int ch4 = 0; ch4 < K4; ch4++) {
-                const float4 f = __ldg(sh + (size_t)ch4 * n + i);
+                const float4 f = __ldg(sh + (size_t)i * K4 + ch4);
 #pragma unroll
                 for (int l = 0; l < 4; l++) {
                     const int e = 4 * ch4 + l;

@@ -155,12 +155,21 @@ k_rs_downsweep(const unsigned long long *__restrict__ kin, unsigned long long *_
             kk[r] = j < tn ? kin[base + j] : 0ull;
             if (VALS) vv[r] = j < tn ? vin[base + j] : 0u;
         }
+        // all rounds' peer masks first (independent match.any, their latencies overlap), then the
+        // per-warp running counts in round order (stable)
+        unsigned pm[RS_ITEMS];
+#pragma unroll
+        for (int r = 0; r < RS_ITEMS; r++) {
+            const int j = warp * (RS_TILE / RS_WARPS) + r * 32 + lane;
+            const int d = (int)((unsigned)(kk[r] >> shift) & (BINS - 1));
+            pm[r] = __match_any_sync(0xffffffffu, j < tn ? d : BINS + lane);
+        }
 #pragma unroll
         for (int r = 0; r < RS_ITEMS; r++) {
             const int j = warp * (RS_TILE / RS_WARPS) + r * 32 + lane;
             const bool act = j < tn;
             const int d = (int)((unsigned)(kk[r] >> shift) & (BINS - 1));
-            const unsigned peers = rs_peers<BITS>(d, act);
+            const unsigned peers = pm[r];
             const int leader = __ffs(peers) - 1;
             unsigned b = 0u;
             if (act && lane == leader) {   // the warp owns column `warp` of run[]: no atomics needed
@@ -308,11 +317,16 @@ k_scan_excl(const unsigned *__restrict__ in, unsigned *__restrict__ out, const i
         const int b = tile * SC_TILE + tid * SC_ITEMS;
         unsigned v[SC_ITEMS];
         unsigned long long sum = 0;
+        if (b + SC_ITEMS <= n) {   // two 16 B vector loads (the arrays are 16 B aligned, b is a multiple of 8)
+            const uint4 p0 = *reinterpret_cast<const uint4 *>(in + b);
+            const uint4 p1 = *reinterpret_cast<const uint4 *>(in + b + 4);
+            v[0] = p0.x; v[1] = p0.y; v[2] = p0.z; v[3] = p0.w; v[4] = p1.x; v[5] = p1.y; v[6] = p1.z; v[7] = p1.w;
+        } else {
 #pragma unroll
-        for (int k = 0; k < SC_ITEMS; k++) {
-            v[k] = b + k < n ? in[b + k] : 0u;
-            sum += v[k];
+            for (int k = 0; k < SC_ITEMS; k++) v[k] = b + k < n ? in[b + k] : 0u;
         }
+#pragma unroll
+        for (int k = 0; k < SC_ITEMS; k++) sum += v[k];
         unsigned long long inc = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -331,18 +345,27 @@ k_scan_excl(const unsigned *__restrict__ in, unsigned *__restrict__ out, const i
             }
             if (lane < SC_THREADS / 32) s_warp[lane] = wi - w;
             const unsigned long long agg = __shfl_sync(0xffffffffu, wi, SC_THREADS / 32 - 1);
+            const unsigned long long pre = lookback_warp(status, tile, agg);
             if (lane == 0) {
-                const unsigned long long pre = lookback(status, tile, agg);
                 s_prefix = pre;
                 if (tile == ntiles - 1) *total = pre + agg;
             }
         }
         __syncthreads();
         unsigned long long run = s_prefix + s_warp[warp] + (inc - sum);
+        unsigned o[SC_ITEMS];
 #pragma unroll
         for (int k = 0; k < SC_ITEMS; k++) {
-            if (b + k < n) out[b + k] = (unsigned)run;
+            o[k] = (unsigned)run;
             run += v[k];
+        }
+        if (b + SC_ITEMS <= n) {
+            *reinterpret_cast<uint4 *>(out + b) = make_uint4(o[0], o[1], o[2], o[3]);
+            *reinterpret_cast<uint4 *>(out + b + 4) = make_uint4(o[4], o[5], o[6], o[7]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < SC_ITEMS; k++)
+                if (b + k < n) out[b + k] = o[k];
         }
         __syncthreads();
     }

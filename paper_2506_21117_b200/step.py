@@ -36,7 +36,7 @@ class GaussianParams:
     """Device-resident scene in the C-ABI layout plus its Adam moments.
 
     mean_op [n,4] (x,y,z,opacity logit), quat [n,4] (w,x,y,z), log_scale [n,4] (pad lane 0),
-    sh [K4,n,4] (coefficient k, channel c at float 3k+c of the row), m/v [3+K4,n,4].
+    sh [n,K4,4] (coefficient k, channel c at float 3k+c of the Gaussian's chunks), m/v [n,3+K4,4].
     """
 
     def __init__(self, mean_op, quat, log_scale, sh, sh_degree: int):
@@ -45,8 +45,8 @@ class GaussianParams:
         self.n = int(mean_op.shape[0])
         self.device = mean_op.device
         r = row4(self.sh_degree)
-        self.m = torch.zeros((r, self.n, 4), dtype=torch.float32, device=self.device)
-        self.v = torch.zeros((r, self.n, 4), dtype=torch.float32, device=self.device)
+        self.m = torch.zeros((self.n, r, 4), dtype=torch.float32, device=self.device)
+        self.v = torch.zeros((self.n, r, 4), dtype=torch.float32, device=self.device)
         self.step = 0
 
     @classmethod
@@ -61,7 +61,7 @@ class GaussianParams:
         ls[:, :3] = log_scales
         shf = np.zeros((n, 4 * kk), np.float32)
         shf[:, : 3 * K] = np.asarray(sh, np.float32).reshape(n, 3 * K)
-        shc = np.ascontiguousarray(shf.reshape(n, kk, 4).transpose(1, 0, 2))
+        shc = np.ascontiguousarray(shf.reshape(n, kk, 4))
         t = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(device)
         return cls(t(mo), t(np.asarray(quats, np.float32)), t(ls), t(shc), sh_degree)
 
@@ -78,18 +78,18 @@ class GaussianParams:
         """Gather ABI rows [len(idx), ROW4, 4] of the parameters (layout helper for tests)."""
         idx = idx.long()
         parts = [self.mean_op[idx][:, None], self.quat[idx][:, None], self.log_scale[idx][:, None],
-                 self.sh[:, idx].permute(1, 0, 2)]
+                 self.sh[idx]]
         return torch.cat(parts, dim=1)
 
     def moment_rows(self, which: str, idx: torch.Tensor) -> torch.Tensor:
         t = self.m if which == "m" else self.v
-        return t[:, idx.long()].permute(1, 0, 2)
+        return t[idx.long()]
 
     def to_numpy(self):
         """(means, log_scales, quats, opacity_logits, sh[n,K,3]) as float32 numpy (layout helper)."""
         K = (self.sh_degree + 1) ** 2
         mo = self.mean_op.cpu().numpy()
-        shf = self.sh.permute(1, 0, 2).reshape(self.n, -1).cpu().numpy()[:, : 3 * K].reshape(self.n, K, 3)
+        shf = self.sh.reshape(self.n, -1).cpu().numpy()[:, : 3 * K].reshape(self.n, K, 3)
         return (mo[:, :3].copy(), self.log_scale.cpu().numpy()[:, :3].copy(), self.quat.cpu().numpy().copy(),
                 mo[:, 3].copy(), shf.copy())
 
