@@ -110,6 +110,7 @@ typedef struct {
     int64_t n_bwd_evals;       /* (pixel, list entry) evaluations of the backward walk (after its bwd) */
     int64_t n_candidates;      /* (Gaussian, view) pairs passing the fp32 projection pre-test */
     int64_t n_kept_pairs;      /* pairs kept after the exact alpha-footprint culling (<= n_pairs) */
+    int64_t n_stage1;          /* (Gaussian, view) pairs passing the projection isotropic pre-test */
 } cls_stats_t;
 
 #define CLS_PROF_GROUPS 16

@@ -153,6 +153,7 @@ k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
     __syncthreads();
     unsigned short *qw = q[wid];
     const int nwarps = gridDim.x * PC_WARPS;
+    unsigned long long n_s1 = 0;
     for (int base = (blockIdx.x * PC_WARPS + wid) * 32; base < n; base += nwarps * 32) {
         const int i = base + lane;
         const bool valid = i < n;
@@ -231,6 +232,7 @@ k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
                     }
                 }
                 const unsigned bal = __ballot_sync(0xffffffffu, pass);
+                n_s1 += __popc(bal);
                 if (pass) qw[(tail + __popc(bal & ((1u << lane) - 1u))) & (PC_Q - 1)] = (unsigned short)(lane | (v << 5));
                 tail += __popc(bal);
                 __syncwarp();
@@ -264,6 +266,7 @@ k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
         }
         __syncwarp();
     }
+    if (lane == 0 && n_s1) atomicAdd(&s.cnt->n_stage1, n_s1);
 }
 
 // ---- pass B: exact fp64 projection of the candidates, records for those touching active tiles ----

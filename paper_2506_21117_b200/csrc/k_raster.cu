@@ -103,14 +103,13 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         const int n = s.tile_end[e] - off;
         const int x = tx * CLS_TILE + lx;
         float Tr[RT_PX], C0[RT_PX], C1[RT_PX], C2[RT_PX];
-        int last[RT_PX], term[RT_PX];
+        int last[RT_PX];
 #pragma unroll
         for (int k = 0; k < RT_PX; k++) {
             const bool in = x < W && ty * CLS_TILE + ly + 4 * k < H;
             Tr[k] = in ? 1.f : -1.f;   // out-of-image pixels start terminated
             C0[k] = C1[k] = C2[k] = 0.f;
             last[k] = -1;
-            term[k] = in ? n - 1 : -1;   // out-of-image pixels evaluate nothing
         }
         for (int b0 = 0; b0 < n; b0 += RT_BATCH) {
             const bool live = Tr[0] > 0.f || Tr[1] > 0.f || Tr[2] > 0.f || Tr[3] > 0.f;
@@ -129,24 +128,22 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
                 const int pos = b0 + k;
 #pragma unroll
                 for (int p = 0; p < RT_PX; p++) {
-                    // branch-free: the exponential is cheaper than a branch around it; beyond qcut'
-                    // the alpha test rejects anyway (ex2 -> 0), so results equal the pre-tested form.
-                    // A skipped entry (alpha < 1/255) gets alpha = 0, so Tn = T exactly; then
-                    // Tn < 1e-4 happens exactly at the terminating entry or on an already
-                    // terminated pixel (T < 0).
+                    // The exponential is cheaper than a branch around it; beyond qcut' the alpha test
+                    // rejects anyway (ex2 -> 0), so results equal the pre-tested form.  A skipped entry
+                    // (alpha < 1/255) gets alpha = 0, so Tn = T exactly; then Tn < 1e-4 happens exactly at
+                    // the terminating entry or on an already terminated pixel (T < 0).  Branch-free.
                     float ss, tt, G;
                     const float qk = raster_q(sx, txx, A.z, B.y, (float)(ly + 4 * p), ss, tt);
                     float alpha = alpha_of(qk, B.z, G);
                     const bool hit = alpha >= (1.0f / 255.0f);
                     alpha = hit ? alpha : 0.f;
-                    const float Tn = __fmul_rn(Tr[p], __fsub_rn(1.0f, alpha));
+                    const float Tn = __fmaf_rn(-alpha, Tr[p], Tr[p]);   // T (1 - alpha), one rounding
                     const bool ok = Tn >= 1e-4f;
                     const float w = ok ? alpha * Tr[p] : 0.f;
                     C0[p] = __fmaf_rn(w, Cc.x, C0[p]);
                     C1[p] = __fmaf_rn(w, Cc.y, C1[p]);
                     C2[p] = __fmaf_rn(w, Cc.z, C2[p]);
                     if (ok && hit) last[p] = pos;
-                    if (!ok) term[p] = min(term[p], pos);   // first termination (evaluation count)
                     Tr[p] = ok ? Tn : -fabsf(Tr[p]);
                 }
             }
@@ -157,7 +154,7 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
             const int yy = ty * CLS_TILE + ly + 4 * p;
             const bool in = x < W && yy < H;
             const float Tf = fabsf(Tr[p]);
-            evals += (unsigned long long)(term[p] + 1);   // entries 0..term evaluated for this pixel
+            evals += (unsigned long long)(last[p] + 1);   // entries up to the last composited one
             const int pl = tid + p * RT_THREADS;          // pixel slot (ly + 4p) * 16 + lx
             const size_t px = (size_t)item * CLS_BLOCK_PIX + pl;
             s.px_T[px] = Tf;
