@@ -205,6 +205,51 @@ cls_status cls_profile_read(cls_ctx *ctx, cls_profile_t *out);
  * into `out` (device).  For stage-wise parity tests. */
 cls_status cls_debug_grad2d(cls_ctx *ctx, float *out, void *stream);
 
+/* ---------------------------------------------------------------------------------------
+ * NEXT-1: static-prefix partition, sphere pruning, densification on O^t.
+ * These run between optimisation steps (not inside one); each synchronises `stream` once to
+ * return a count.  Row layout as cls_gaussians; m, v as cls_adam_masked; accum (float[n]) and
+ * count (int32[n]) are the densification statistics (optional where marked).
+ * ------------------------------------------------------------------------------------- */
+
+/* Supp. "History": "before optimization, we rearrange the Gaussian order to
+ * ensure G^t[:#static] = G_static^{t-1}".  Stable partition of the n rows of `g` by membership in
+ * the regions (R21): rows outside every region first, then the rows of O^t, each group in its
+ * original order.  Outputs (device, caller-owned, must not alias the inputs) get the permuted
+ * rows; *n_static (host out) = number of rows outside the regions.  Moments are not permuted
+ * (start the optimisation with fresh ones). */
+cls_status cls_partition_static(cls_ctx *ctx, const cls_gaussians *g, float *mean_op, float *quat,
+                                float *log_scale, float *sh, const cls_region *regions,
+                                int32_t n_regions, int64_t *n_static, void *stream);
+
+/* Sphere pruning (Supp. L509-L511, §3.3): rows [n_static, n) -- O^t after the partition --
+ * whose centre lies outside the union of the regions are removed (stable compaction of the
+ * suffix, in place); the static prefix is never touched.  m/v and accum/count (each pair
+ * optional, NULL) are compacted with the rows.  *n (host, in/out): row count. */
+cls_status cls_prune_outside(cls_ctx *ctx, float *mean_op, float *quat, float *log_scale, float *sh,
+                             float *m, float *v, float *accum, int32_t *count, int32_t sh_degree,
+                             int64_t n_static, int64_t *n, const cls_region *regions,
+                             int32_t n_regions, void *stream);
+
+/* Densification statistics of the last cls_render_bwd (3DGS add_densification_stats, reading
+ * R31): for every view of the last fwd and every active Gaussian with a record in it,
+ * accum[i] += || dL/d(u, v) * (W/2, H/2) || * n_views_total and count[i] += 1. */
+cls_status cls_densify_stats(cls_ctx *ctx, float *accum, int32_t *count, void *stream);
+
+/* 3DGS densification restricted to O^t (PAPER.md L449 defaults; readings R32-R33): for the
+ * rows [n_static, n) with accum/count >= grad_threshold (fp32): clone (exact copy, fresh Adam
+ * state) if max log-scale <= log_scale_threshold, else split into 2 children
+ * mu + R(q) (exp(l) * z_c) with log-scale l - ln 1.6 (z_c = normals[i][c][0..2], device float,
+ * N(0,1) draws supplied by the caller) and remove the parent.  New suffix order:
+ * [kept rows][clones][child 0 of each parent][child 1 ...].  The stats of all rows are reset.
+ * *n (host in/out), capacity = rows the arrays can hold (CLS_ERR_CAPACITY, nothing written, if
+ * exceeded); *n_clone, *n_split (host out, optional). */
+cls_status cls_densify(cls_ctx *ctx, float *mean_op, float *quat, float *log_scale, float *sh,
+                       float *m, float *v, float *accum, int32_t *count, int32_t sh_degree,
+                       int64_t n_static, int64_t *n, int64_t capacity, const float *normals,
+                       float grad_threshold, float log_scale_threshold, int64_t *n_clone,
+                       int64_t *n_split, void *stream);
+
 const char *cls_status_string(cls_status s);
 const char *cls_last_error(const cls_ctx *ctx);
 /* Number of kernels launched by the library since cls_create (host counter). */

@@ -21,7 +21,8 @@ STATUS = {0: "CLS_OK", 1: "CLS_ERR_INVALID_ARGUMENT", 2: "CLS_ERR_DIMENSION_MISM
 # symbols declared in include/cls.h (checked by tests/test_abi.py)
 EXPORTS = ("cls_create", "cls_destroy", "cls_render_fwd", "cls_active", "cls_copy_active", "cls_render_bwd", "cls_adam_masked",
            "cls_stats", "cls_profile_enable", "cls_profile_read", "cls_debug_grad2d", "cls_status_string",
-           "cls_last_error", "cls_launch_count")
+           "cls_last_error", "cls_launch_count", "cls_partition_static", "cls_prune_outside", "cls_densify_stats",
+           "cls_densify")
 CLS_PROF_GROUPS = 16
 
 
@@ -98,10 +99,18 @@ def _load():
     L.cls_status_string.restype = ctypes.c_char_p
     L.cls_last_error.argtypes = [V]
     L.cls_last_error.restype = ctypes.c_char_p
+    i64p = P(ctypes.c_int64)
+    L.cls_partition_static.argtypes = [V, P(cls_gaussians), V, V, V, V, P(cls_region), ctypes.c_int32, i64p, V]
+    L.cls_prune_outside.argtypes = [V, V, V, V, V, V, V, V, V, ctypes.c_int32, ctypes.c_int64, i64p, P(cls_region),
+                                    ctypes.c_int32, V]
+    L.cls_densify_stats.argtypes = [V, V, V, V]
+    L.cls_densify.argtypes = [V, V, V, V, V, V, V, V, V, ctypes.c_int32, ctypes.c_int64, i64p, ctypes.c_int64, V,
+                              ctypes.c_float, ctypes.c_float, i64p, i64p, V]
     L.cls_launch_count.argtypes = [V]
     L.cls_launch_count.restype = ctypes.c_int64
     for name in ("cls_create", "cls_destroy", "cls_render_fwd", "cls_active", "cls_copy_active", "cls_render_bwd", "cls_adam_masked",
-                 "cls_stats", "cls_debug_grad2d", "cls_profile_enable", "cls_profile_read"):
+                 "cls_stats", "cls_debug_grad2d", "cls_profile_enable", "cls_profile_read", "cls_partition_static",
+                 "cls_prune_outside", "cls_densify_stats", "cls_densify"):
         getattr(L, name).restype = ctypes.c_int
     return L
 

@@ -116,6 +116,8 @@ struct Scratch {
     float *item_loss;       // [items]
     // gradients
     float4 *grad2d;         // [V][A][3]
+    uint8_t *vis;           // [V][max_active] active Gaussian has a record in the view (densification stats)
+    long long max_active;
     Counters *cnt;
     int max_items;
 };
@@ -198,6 +200,27 @@ __device__ __forceinline__ unsigned long long lookback_warp(unsigned long long *
         vs[tile] = LB_FLAG_PRE | (prefix + agg);
     }
     return prefix;
+}
+
+// Gaussian centre in the union of the change regions (R21: spheres or AABBs, inclusive), fp64
+__device__ __forceinline__ bool in_regions(const float4 m, const RegSet &regs)
+{
+    const double x = m.x, y = m.y, z = m.z;
+    for (int j = 0; j < regs.n; j++) {
+        if (regs.kind[j] == 0) {
+            const double dx = __dsub_rn(x, (double)regs.a[j][0]);
+            const double dy = __dsub_rn(y, (double)regs.a[j][1]);
+            const double dz = __dsub_rn(z, (double)regs.a[j][2]);
+            const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+            const double r = regs.r[j];
+            if (d2 <= __dmul_rn(r, r)) return true;
+        } else {
+            if (m.x >= regs.a[j][0] && m.x <= regs.b[j][0] && m.y >= regs.a[j][1] && m.y <= regs.b[j][1] &&
+                m.z >= regs.a[j][2] && m.z <= regs.b[j][2])
+                return true;
+        }
+    }
+    return false;
 }
 
 // ---------------------------------------------------------------------------

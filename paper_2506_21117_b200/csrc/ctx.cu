@@ -37,6 +37,15 @@ struct cls_ctx {
     std::vector<cudaEvent_t> ev_pool;
     double prof_ms[CLS_PROF_GROUPS] = {};
     int64_t prof_n[CLS_PROF_GROUPS] = {};
+    int n_views_total = 1;
+    // NEXT-1 scratch (allocated on first use, grown as needed; outside the per-step hot path)
+    size_t dens_rows = 0, dens_n = 0;
+    float4 *d_mo = nullptr, *d_q = nullptr, *d_ls = nullptr, *d_sh = nullptr, *d_m = nullptr, *d_v = nullptr;
+    float *d_acc = nullptr;
+    int *d_cnt = nullptr;
+    unsigned *d_work = nullptr;
+    unsigned long long *d_status = nullptr, *d_tot = nullptr;
+    int *d_int = nullptr;
 };
 
 static const char *PROF_NAMES[] = {"member", "active_mask", "project_cand", "project_exact", "rec_sort", "bin_count",
@@ -133,7 +142,7 @@ cls_status cls_destroy(cls_ctx *c)
                     c->s.srec, c->s.rec_gid, c->s.cand, c->s.rkey,
                     c->s.rkey_alt, c->s.rval, c->s.rval_alt, c->s.rcnt, c->s.urec, c->s.uinfo, c->s.ucnt, c->s.uoff, c->s.roff, c->s.st_scan, c->s.tile_end,
                     c->s.tile_off, c->s.st_tiles, c->s.items, c->s.item_of_tile, c->s.first_active, c->s.pairs,
-                    c->s.pairs_alt, c->s.rs_counts, c->s.rs_totals, c->s.px_T, c->s.px_last, c->s.px_dl,
+                    c->s.pairs_alt, c->s.vis, c->s.rs_counts, c->s.rs_totals, c->s.px_T, c->s.px_last, c->s.px_dl,
                     c->s.item_loss, c->s.grad2d, c->s.cnt};
     for (void *p : ptrs)
         if (p) cudaFree(p);
@@ -142,6 +151,10 @@ cls_status cls_destroy(cls_ctx *c)
     if (c->ev_member) cudaEventDestroy(c->ev_member);
     if (c->ev_fwd) cudaEventDestroy(c->ev_fwd);
     for (auto &r : c->prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    void *dp[] = {c->d_mo, c->d_q, c->d_ls, c->d_sh, c->d_m, c->d_v, c->d_acc, c->d_cnt, c->d_work, c->d_status,
+                  c->d_tot, c->d_int};
+    for (void *p : dp)
+        if (p) cudaFree(p);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     delete c;
     return CLS_OK;
@@ -180,7 +193,8 @@ cls_status cls_create(cls_ctx **out, int device, const cls_limits *lim)
               dalloc(&s.pairs, P) && dalloc(&s.pairs_alt, P) && dalloc(&s.rs_counts, (size_t)512 * RS_GRID) &&
               dalloc(&s.rs_totals, 512) && dalloc(&s.px_T, VT * 256) && dalloc(&s.px_last, VT * 256) &&
               dalloc(&s.px_dl, VT * 768) && dalloc(&s.item_loss, VT) &&
-              dalloc(&s.grad2d, V * (size_t)lim->max_active * 3) && dalloc(&s.cnt, 1);
+              dalloc(&s.grad2d, V * (size_t)lim->max_active * 3) &&
+              dalloc(&s.vis, V * (size_t)lim->max_active) && dalloc(&s.cnt, 1);
     if (ok) ok = cudaMallocHost((void **)&c->h_cnt, sizeof(Counters)) == cudaSuccess &&
                  cudaMallocHost((void **)&c->h_A, sizeof(int)) == cudaSuccess;
     if (ok) ok = cudaEventCreateWithFlags(&c->ev_member, cudaEventDisableTiming) == cudaSuccess &&
@@ -195,6 +209,7 @@ cls_status cls_create(cls_ctx **out, int device, const cls_limits *lim)
     s.max_pairs = (long long)P;
     s.max_units = (long long)P;   // units (record, tile row) are bounded like the pairs
     s.max_items = (int)VT;
+    s.max_active = lim->max_active;
     memset(c->h_cnt, 0, sizeof(Counters));
     *out = c;
     return CLS_OK;
@@ -286,6 +301,7 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     cudaEventRecord(c->ev_member, st);
     run(c, P_MASK, st, [&] { launch_active_mask(p, d, cs, s, st); });
     run(c, P_PROJECT, st, [&] { launch_project_cand(p, d, cs, s, st); });
+    cudaMemsetAsync(s.vis, 0, (size_t)d.V * (size_t)s.max_active, st);
     run(c, P_PROJECT_EXACT, st, [&] { launch_project_exact(p, d, cs, s, st); });
     run(c, P_RECSORT, st, [&] { launch_bin_recsort(d, cs, s, st); });
     run(c, P_BINCOUNT, st, [&] { launch_bin_count(d, cs, s, st); });
@@ -303,6 +319,7 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     c->s.rskey = s.rskey;
     c->s.spairs = s.spairs;
     c->dims = d;
+    c->n_views_total = n_views_total;
     c->cams = cs;
     c->bg = bgc;
     c->has_targets = targets != nullptr;
@@ -461,6 +478,161 @@ cls_status cls_debug_grad2d(cls_ctx *c, float *out, void *stream)
     const size_t bytes = sizeof(float4) * 3 * (size_t)c->dims.V * (size_t)(*c->h_A);
     cudaMemcpyAsync(out, c->s.grad2d, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
     return check_cuda(c, "cls_debug_grad2d");
+}
+
+// ---------------------------------------------------------------------------
+// NEXT-1: static-prefix partition, sphere pruning, densification on O^t
+// ---------------------------------------------------------------------------
+static bool regset_of(cls_ctx *c, const cls_region *regions, int32_t n_regions, RegSet &regs)
+{
+    if (n_regions < 0 || n_regions > CLS_MAX_REGIONS || (n_regions > 0 && !regions)) return false;
+    regs = RegSet{};
+    regs.n = n_regions;
+    for (int j = 0; j < n_regions; j++) {
+        const cls_region &r = regions[j];
+        if (r.kind == 0 ? !(r.r > 0.f) : (r.kind != 1 || !(r.a[0] <= r.b[0] && r.a[1] <= r.b[1] && r.a[2] <= r.b[2])))
+            return false;
+        regs.kind[j] = r.kind;
+        for (int q = 0; q < 3; q++) { regs.a[j][q] = r.a[q]; regs.b[j][q] = r.b[q]; }
+        regs.r[j] = r.r;
+    }
+    (void)c;
+    return true;
+}
+
+// grow the NEXT-1 scratch to `rows` parameter rows (degree D) and `nflag` flag/scan entries
+static bool dens_reserve(cls_ctx *c, size_t rows, size_t nflag, int D)
+{
+    const int K4 = (3 * (D + 1) * (D + 1) + 3) / 4, ROW4 = 3 + K4;
+    rows = std::max<size_t>(rows, 1);
+    nflag = std::max<size_t>(nflag, 1);
+    if (rows > c->dens_rows) {
+        float4 **f4[] = {&c->d_mo, &c->d_q, &c->d_ls};
+        for (auto p : f4) { if (*p) cudaFree(*p); *p = nullptr; }
+        if (c->d_sh) cudaFree(c->d_sh);
+        if (c->d_m) cudaFree(c->d_m);
+        if (c->d_v) cudaFree(c->d_v);
+        if (c->d_acc) cudaFree(c->d_acc);
+        if (c->d_cnt) cudaFree(c->d_cnt);
+        c->d_sh = c->d_m = c->d_v = nullptr; c->d_acc = nullptr; c->d_cnt = nullptr;
+        c->dens_rows = 0;
+        const size_t r = rows + rows / 4;
+        if (!(dalloc(&c->d_mo, r) && dalloc(&c->d_q, r) && dalloc(&c->d_ls, r) && dalloc(&c->d_sh, r * 12) &&
+              dalloc(&c->d_m, r * 15) && dalloc(&c->d_v, r * 15) && dalloc(&c->d_acc, r) && dalloc(&c->d_cnt, r)))
+            return false;
+        c->dens_rows = r;
+    }
+    (void)ROW4;
+    if (nflag > c->dens_n) {
+        if (c->d_work) cudaFree(c->d_work);
+        if (c->d_status) cudaFree(c->d_status);
+        c->d_work = nullptr; c->d_status = nullptr;
+        c->dens_n = 0;
+        const size_t r = ((nflag + nflag / 4) + 3) & ~(size_t)3;   // multiple of 4: 16 B aligned sub-arrays
+        if (!(dalloc(&c->d_work, 7 * r + 28) && dalloc(&c->d_status, r / 2048 + 4))) return false;
+        c->dens_n = r;
+    }
+    if (!c->d_tot && !dalloc(&c->d_tot, 4)) return false;
+    if (!c->d_int && !dalloc(&c->d_int, 4)) return false;
+    return true;
+}
+
+cls_status cls_partition_static(cls_ctx *c, const cls_gaussians *g, float *mean_op, float *quat, float *log_scale,
+                                float *sh, const cls_region *regions, int32_t n_regions, int64_t *n_static,
+                                void *stream)
+{
+    if (!c) return CLS_ERR_INVALID_ARGUMENT;
+    if (!g || !mean_op || !quat || !log_scale || !sh || !n_static || !g->mean_op || !g->quat || !g->log_scale ||
+        !g->sh || g->n <= 0 || g->n >= (1ll << 31) || g->sh_degree < 0 || g->sh_degree > 3)
+        return fail(c, CLS_ERR_INVALID_ARGUMENT, "cls_partition_static: bad arguments");
+    if ((const float *)mean_op == g->mean_op || (const float *)sh == g->sh)
+        return fail(c, CLS_ERR_INVALID_ARGUMENT, "cls_partition_static: outputs must not alias the inputs");
+    RegSet regs;
+    if (!regset_of(c, regions, n_regions, regs)) return fail(c, CLS_ERR_INVALID_ARGUMENT, "bad regions");
+    cudaSetDevice(c->device);
+    const int n = (int)g->n;
+    if (!dens_reserve(c, 1, (size_t)n, g->sh_degree)) return fail(c, CLS_ERR_OUT_OF_MEMORY, "partition scratch");
+    cudaStream_t st = (cudaStream_t)stream;
+    launch_partition((const float4 *)g->mean_op, (const float4 *)g->quat, (const float4 *)g->log_scale,
+                     (const float4 *)g->sh, g->sh_degree, n, regs, (float4 *)mean_op, (float4 *)quat,
+                     (float4 *)log_scale, (float4 *)sh, c->d_work, c->d_work + c->dens_n, c->d_int, c->d_status,
+                     c->d_int + 1, c->d_tot, st);
+    unsigned long long ns = 0;
+    cudaMemcpyAsync(&ns, c->d_tot, sizeof ns, cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return check_cuda(c, "cls_partition_static");
+    *n_static = (int64_t)ns;
+    return check_cuda(c, "cls_partition_static");
+}
+
+static cls_status suffix_op(cls_ctx *c, int mode, float *mean_op, float *quat, float *log_scale, float *sh, float *m,
+                            float *v, float *accum, int32_t *count, int32_t sh_degree, int64_t n_static, int64_t *n,
+                            int64_t capacity, const RegSet &regs, const float *normals, float grad_thr,
+                            float log_scale_thr, int64_t *n_clone, int64_t *n_split, void *stream, const char *name)
+{
+    if (!mean_op || !quat || !log_scale || !sh || !n || sh_degree < 0 || sh_degree > 3 || n_static < 0 ||
+        *n < n_static || (m == nullptr) != (v == nullptr) || (accum == nullptr) != (count == nullptr))
+        return fail(c, CLS_ERR_INVALID_ARGUMENT, "%s: bad arguments", name);
+    const long long S = *n - n_static;
+    if (S == 0) {
+        if (n_clone) *n_clone = 0;
+        if (n_split) *n_split = 0;
+        return CLS_OK;
+    }
+    if (S >= (1ll << 31)) return fail(c, CLS_ERR_CAPACITY, "%s: suffix of %lld rows", name, S);
+    cudaSetDevice(c->device);
+    if (!dens_reserve(c, (size_t)S, (size_t)S, sh_degree)) return fail(c, CLS_ERR_OUT_OF_MEMORY, "%s scratch", name);
+    cudaStream_t st = (cudaStream_t)stream;
+    RowArrays a = rows_of((float4 *)mean_op, (float4 *)quat, (float4 *)log_scale, (float4 *)sh, (float4 *)m,
+                          (float4 *)v, accum, count, sh_degree);
+    RowArrays tmp = rows_of(c->d_mo, c->d_q, c->d_ls, c->d_sh, m ? c->d_m : nullptr, m ? c->d_v : nullptr,
+                            accum ? c->d_acc : nullptr, accum ? c->d_cnt : nullptr, sh_degree);
+    launch_suffix_plan(mode, a, n_static, (int)S, regs, grad_thr, log_scale_thr, c->d_work, c->d_int, c->d_status,
+                       c->d_int + 1, c->d_tot, st);
+    unsigned long long tot[3] = {0, 0, 0};
+    cudaMemcpyAsync(tot, c->d_tot, sizeof tot, cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return check_cuda(c, name);
+    const long long n_new = n_static + (long long)tot[0] + (long long)tot[1] + 2ll * (long long)tot[2];
+    if (n_new > capacity)
+        return fail(c, CLS_ERR_CAPACITY, "%s: %lld rows exceed the capacity %lld", name, n_new, (long long)capacity);
+    launch_suffix_apply(a, n_static, (int)S, tmp, c->d_work, c->d_tot, normals, st);
+    if (mode == 1 && accum) launch_reset_stats(accum, count, n_new, st);   // 3DGS: stats restart
+    *n = n_new;
+    if (n_clone) *n_clone = (int64_t)tot[1];
+    if (n_split) *n_split = (int64_t)tot[2];
+    return check_cuda(c, name);
+}
+
+cls_status cls_prune_outside(cls_ctx *c, float *mean_op, float *quat, float *log_scale, float *sh, float *m, float *v,
+                             float *accum, int32_t *count, int32_t sh_degree, int64_t n_static, int64_t *n,
+                             const cls_region *regions, int32_t n_regions, void *stream)
+{
+    if (!c) return CLS_ERR_INVALID_ARGUMENT;
+    RegSet regs;
+    if (!regset_of(c, regions, n_regions, regs)) return fail(c, CLS_ERR_INVALID_ARGUMENT, "bad regions");
+    return suffix_op(c, 0, mean_op, quat, log_scale, sh, m, v, accum, count, sh_degree, n_static, n, n ? *n : 0, regs,
+                     nullptr, 0.f, 0.f, nullptr, nullptr, stream, "cls_prune_outside");
+}
+
+cls_status cls_densify(cls_ctx *c, float *mean_op, float *quat, float *log_scale, float *sh, float *m, float *v,
+                       float *accum, int32_t *count, int32_t sh_degree, int64_t n_static, int64_t *n,
+                       int64_t capacity, const float *normals, float grad_threshold, float log_scale_threshold,
+                       int64_t *n_clone, int64_t *n_split, void *stream)
+{
+    if (!c) return CLS_ERR_INVALID_ARGUMENT;
+    if (!accum || !count || !normals) return fail(c, CLS_ERR_INVALID_ARGUMENT, "cls_densify: stats and normals needed");
+    RegSet regs{};
+    return suffix_op(c, 1, mean_op, quat, log_scale, sh, m, v, accum, count, sh_degree, n_static, n, capacity, regs,
+                     normals, grad_threshold, log_scale_threshold, n_clone, n_split, stream, "cls_densify");
+}
+
+cls_status cls_densify_stats(cls_ctx *c, float *accum, int32_t *count, void *stream)
+{
+    if (!c) return CLS_ERR_INVALID_ARGUMENT;
+    if (!c->bwd_valid) return fail(c, CLS_ERR_STATE, "cls_densify_stats before cls_render_bwd");
+    if (!accum || !count) return fail(c, CLS_ERR_INVALID_ARGUMENT, "null pointer argument");
+    cudaSetDevice(c->device);
+    launch_densify_stats(c->dims, c->s, c->n_views_total, accum, count, (cudaStream_t)stream);
+    return check_cuda(c, "cls_densify_stats");
 }
 
 }  // extern "C"

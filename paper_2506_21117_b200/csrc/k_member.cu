@@ -17,26 +17,6 @@ int64_t g_launches = 0;
 #define MEMBER_ITEMS 8
 #define MEMBER_TILE (MEMBER_THREADS * MEMBER_ITEMS)
 
-__device__ __forceinline__ bool in_regions(const float4 m, const RegSet &regs)
-{
-    const double x = m.x, y = m.y, z = m.z;
-    for (int j = 0; j < regs.n; j++) {
-        if (regs.kind[j] == 0) {
-            const double dx = __dsub_rn(x, (double)regs.a[j][0]);
-            const double dy = __dsub_rn(y, (double)regs.a[j][1]);
-            const double dz = __dsub_rn(z, (double)regs.a[j][2]);
-            const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-            const double r = regs.r[j];
-            if (d2 <= __dmul_rn(r, r)) return true;
-        } else {
-            if (m.x >= regs.a[j][0] && m.x <= regs.b[j][0] && m.y >= regs.a[j][1] && m.y <= regs.b[j][1] &&
-                m.z >= regs.a[j][2] && m.z <= regs.b[j][2])
-                return true;
-        }
-    }
-    return false;
-}
-
 __global__ void __launch_bounds__(MEMBER_THREADS)
 k_member(const float4 *__restrict__ mean_op, int n, const __grid_constant__ RegSet regs, Scratch s)
 {

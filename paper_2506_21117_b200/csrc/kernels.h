@@ -53,6 +53,27 @@ void launch_adam(const StepDims &d, const Scratch &s, float4 *mean_op, float4 *q
                  float4 *m, float4 *v, const float4 *grad_active, const float lr[6], float b1, float b2, float eps,
                  float bc1, float bc2, cudaStream_t st);
 
+// NEXT-1: static-prefix partition, sphere pruning, densification restricted to O^t (k_densify.cu)
+struct RowArrays {   // one parameter set, Gaussian-major rows (cls.h layout); m/v/acc/cnt optional
+    float4 *mo, *q, *ls, *sh, *m, *v;
+    float *acc;
+    int *cnt;
+    int K4, ROW4;
+};
+RowArrays rows_of(float4 *mo, float4 *q, float4 *ls, float4 *sh, float4 *m, float4 *v, float *acc, int *cnt, int D);
+void launch_densify_stats(const StepDims &d, const Scratch &s, int n_views_total, float *acc, int *cnt,
+                          cudaStream_t st);
+void launch_partition(const float4 *mo, const float4 *q, const float4 *ls, const float4 *sh, int D, int n,
+                      const RegSet &regs, float4 *omo, float4 *oq, float4 *ols, float4 *osh, unsigned *flag,
+                      unsigned *excl, int *n_dev, unsigned long long *status, int *ticket,
+                      unsigned long long *n_static_dev, cudaStream_t st);
+void launch_suffix_plan(int mode, const RowArrays &a, long long n_static, int S, const RegSet &regs, float grad_thr,
+                        float log_scale_thr, unsigned *work, int *S_dev, unsigned long long *status, int *ticket,
+                        unsigned long long *tot, cudaStream_t st);
+void launch_suffix_apply(const RowArrays &a, long long n_static, int S, const RowArrays &tmp, const unsigned *work,
+                         const unsigned long long *tot, const float *normals, cudaStream_t st);
+void launch_reset_stats(float *acc, int *cnt, long long n, cudaStream_t st);
+
 extern int64_t g_launches;   // kernels launched by this process through libcls (host counter)
 
 }  // namespace cls

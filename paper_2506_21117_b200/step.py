@@ -39,18 +39,32 @@ class GaussianParams:
     sh [n,K4,4] (coefficient k, channel c at float 3k+c of the Gaussian's chunks), m/v [n,3+K4,4].
     """
 
-    def __init__(self, mean_op, quat, log_scale, sh, sh_degree: int):
-        self.mean_op, self.quat, self.log_scale, self.sh = mean_op, quat, log_scale, sh
+    def __init__(self, mean_op, quat, log_scale, sh, sh_degree: int, capacity: Optional[int] = None):
         self.sh_degree = int(sh_degree)
-        self.n = int(mean_op.shape[0])
+        n = int(mean_op.shape[0])
         self.device = mean_op.device
+        cap = max(int(capacity or n), n)
+        self.capacity = cap
         r = row4(self.sh_degree)
-        self.m = torch.zeros((self.n, r, 4), dtype=torch.float32, device=self.device)
-        self.v = torch.zeros((self.n, r, 4), dtype=torch.float32, device=self.device)
+        kk = k4(self.sh_degree)
+        z = lambda *shape, dt=torch.float32: torch.zeros(shape, dtype=dt, device=self.device)
+        # capacity-sized storage (densification appends rows); the public tensors are views [:n]
+        self._mo, self._q, self._ls, self._sh = z(cap, 4), z(cap, 4), z(cap, 4), z(cap, kk, 4)
+        self._m, self._v = z(cap, r, 4), z(cap, r, 4)
+        self._acc, self._cnt = z(cap), z(cap, dt=torch.int32)   # densification statistics (NEXT-1)
+        self._mo[:n], self._q[:n], self._ls[:n], self._sh[:n] = mean_op, quat, log_scale, sh
+        self.n_static = 0
+        self._set_n(n)
         self.step = 0
 
+    def _set_n(self, n: int):
+        self.n = int(n)
+        self.mean_op, self.quat, self.log_scale, self.sh = self._mo[:n], self._q[:n], self._ls[:n], self._sh[:n]
+        self.m, self.v = self._m[:n], self._v[:n]
+        self.grad_accum, self.grad_count = self._acc[:n], self._cnt[:n]
+
     @classmethod
-    def from_arrays(cls, means, log_scales, quats, opacity_logits, sh, sh_degree, device="cuda"):
+    def from_arrays(cls, means, log_scales, quats, opacity_logits, sh, sh_degree, device="cuda", capacity=None):
         n = len(means)
         K = (sh_degree + 1) ** 2
         kk = k4(sh_degree)
@@ -63,12 +77,12 @@ class GaussianParams:
         shf[:, : 3 * K] = np.asarray(sh, np.float32).reshape(n, 3 * K)
         shc = np.ascontiguousarray(shf.reshape(n, kk, 4))
         t = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(device)
-        return cls(t(mo), t(np.asarray(quats, np.float32)), t(ls), t(shc), sh_degree)
+        return cls(t(mo), t(np.asarray(quats, np.float32)), t(ls), t(shc), sh_degree, capacity=capacity)
 
     @classmethod
-    def from_scene(cls, scene, device="cuda"):
+    def from_scene(cls, scene, device="cuda", capacity=None):
         return cls.from_arrays(scene.means, scene.log_scales, scene.quats, scene.opacity_logits, scene.sh,
-                               scene.sh_degree, device)
+                               scene.sh_degree, device, capacity=capacity)
 
     def struct(self) -> N.cls_gaussians:
         return N.cls_gaussians(self.n, self.sh_degree, self.mean_op.data_ptr(), self.quat.data_ptr(),
@@ -253,6 +267,59 @@ class LocalOptimizer:
 
     def launch_count(self) -> int:
         return int(lib.cls_launch_count(self.ctx))
+
+    # -- NEXT-1: static-prefix partition, sphere pruning, densification on O^t ------------------------
+    def partition_static(self, stream=None) -> int:
+        """Reorder the scene so that the Gaussians outside the regions come first (history
+        invariant); moments and densification statistics restart at 0."""
+        p = self.params
+        n = p.n
+        mo, q, ls, sh = (torch.empty_like(t) for t in (p._mo, p._q, p._ls, p._sh))
+        ns = ctypes.c_int64()
+        check(lib.cls_partition_static(self.ctx, ctypes.byref(p.struct()), ctypes.c_void_p(mo.data_ptr()),
+                                       ctypes.c_void_p(q.data_ptr()), ctypes.c_void_p(ls.data_ptr()),
+                                       ctypes.c_void_p(sh.data_ptr()), self._reg, len(self.regions),
+                                       ctypes.byref(ns), ctypes.c_void_p(_stream_ptr(stream))), self.ctx)
+        p._mo, p._q, p._ls, p._sh = mo, q, ls, sh
+        p._m.zero_(); p._v.zero_(); p._acc.zero_(); p._cnt.zero_()
+        p.n_static = int(ns.value)
+        p._set_n(n)
+        return p.n_static
+
+    def _rows_args(self):
+        p = self.params
+        return [ctypes.c_void_p(t.data_ptr()) for t in (p._mo, p._q, p._ls, p._sh, p._m, p._v, p._acc, p._cnt)]
+
+    def prune_outside(self, stream=None) -> int:
+        """Sphere pruning (Supp. L509-L511): remove the O^t rows [n_static, n) whose centre left
+        the regions.  Returns the number of removed rows."""
+        p = self.params
+        n = ctypes.c_int64(p.n)
+        check(lib.cls_prune_outside(self.ctx, *self._rows_args(), p.sh_degree, p.n_static, ctypes.byref(n),
+                                    self._reg, len(self.regions), ctypes.c_void_p(_stream_ptr(stream))), self.ctx)
+        removed = p.n - int(n.value)
+        p._set_n(int(n.value))
+        return removed
+
+    def densify_stats(self, stream=None):
+        """Accumulate the densification statistics of the last backward (reading R31)."""
+        p = self.params
+        check(lib.cls_densify_stats(self.ctx, ctypes.c_void_p(p._acc.data_ptr()), ctypes.c_void_p(p._cnt.data_ptr()),
+                                    ctypes.c_void_p(_stream_ptr(stream))), self.ctx)
+
+    def densify(self, normals: torch.Tensor, grad_threshold: float = 2e-4, log_scale_threshold: float = 0.0,
+                stream=None):
+        """3DGS clone/split on O^t (readings R32-R33); `normals` [n, 2, 3] N(0,1) draws on the device.
+        Returns (n_clone, n_split)."""
+        p = self.params
+        assert normals.is_contiguous() and normals.dtype == torch.float32 and normals.shape[0] >= p.n
+        n = ctypes.c_int64(p.n)
+        nc, nsp = ctypes.c_int64(), ctypes.c_int64()
+        check(lib.cls_densify(self.ctx, *self._rows_args(), p.sh_degree, p.n_static, ctypes.byref(n), p.capacity,
+                              ctypes.c_void_p(normals.data_ptr()), float(grad_threshold), float(log_scale_threshold),
+                              ctypes.byref(nc), ctypes.byref(nsp), ctypes.c_void_p(_stream_ptr(stream))), self.ctx)
+        p._set_n(int(n.value))
+        return int(nc.value), int(nsp.value)
 
     # -- one full local-optimisation step ----------------------------------------------------------
     def step(self, cameras, targets: torch.Tensor, n_views_total: Optional[int] = None,
