@@ -271,7 +271,7 @@ k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
 
 // ---- pass B: exact fp64 projection of the candidates, records for those touching active tiles ----
 template <int D>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
 k_project_exact(const float4 *__restrict__ mean_op, const float4 *__restrict__ quat,
                 const float4 *__restrict__ log_scale, const float4 *__restrict__ sh, int n,
                 const __grid_constant__ CamSet cams, Scratch s)
@@ -289,6 +289,7 @@ k_project_exact(const float4 *__restrict__ mean_op, const float4 *__restrict__ q
         Proj p;
         int i = 0, v = 0;
         float4 mo = make_float4(0, 0, 0, 0);
+        double o64 = 0.0, qcut = -1.0;   // opacity and the alpha >= 1/255 threshold 2 ln(255 o), computed once
         if (e < ncand) {
             const int2 cv = s.cand[e];
             i = cv.x;
@@ -297,8 +298,8 @@ k_project_exact(const float4 *__restrict__ mean_op, const float4 *__restrict__ q
             if (project_gaussian(mo, __ldg(quat + i), __ldg(log_scale + i), s_cams[v], W, H, TX, TY, p)) {
                 // emission rect = 3-sigma rect (support, R8) n bounding box of the alpha >= 1/255
                 // footprint (exact culling: outside it every pixel has alpha < 1/255)
-                const double o64 = 1.0 / (1.0 + exp(-(double)mo.w));
-                const double qcut = 2.0 * log(255.0 * o64) * (1.0 + 1e-6) + 2e-3;
+                o64 = 1.0 / (1.0 + exp(-(double)mo.w));
+                qcut = 2.0 * log(255.0 * o64) * (1.0 + 1e-6) + 2e-3;
                 if (qcut >= 0.0) {
                     const double hx = sqrt(qcut * p.A) + 1e-3, hy = sqrt(qcut * p.C) + 1e-3;
                     // pixel x is reached iff |u - x| <= hx; tile tx holds x in [16 tx, 16 tx + 15]
@@ -335,7 +336,6 @@ k_project_exact(const float4 *__restrict__ mean_op, const float4 *__restrict__ q
         sh_color_raw<D>(sh, n, i, dir, Y, col);
         // ---- record ----
         const float uh = __double2float_rn(p.u), vh = __double2float_rn(p.v);
-        const double o64 = 1.0 / (1.0 + exp(-(double)mo.w));
         // scaled LDL^T coefficients of the exponent (raster_q, reading R29): pivot on the larger
         // diagonal conic entry; conic a = C/det >= c = A/det  <=>  C >= A
         double a1, a2, b1, b2;
@@ -347,7 +347,7 @@ k_project_exact(const float4 *__restrict__ mean_op, const float4 *__restrict__ q
             a1 = k * (-p.B / p.A); a2 = k; b1 = sqrt(CLS_KAPPA / p.A); b2 = 0.0;
         }
         // pre-exponential test threshold: alpha >= 1/255 needs q <= 2 ln(255 o); margin covers fp32
-        const double qc = CLS_KAPPA * (2.0 * log(255.0 * o64) * (1.0 + 1e-6) + 2e-3);
+        const double qc = CLS_KAPPA * qcut;
         Rec R;
         R.xy = make_float4(uh, __double2float_rn(p.u - (double)uh), vh, __double2float_rn(p.v - (double)vh));
         R.co = make_float4(__double2float_rn(a1), __double2float_rn(a2), __double2float_rn(b1), __double2float_rn(b2));
