@@ -93,20 +93,20 @@ struct Scratch {
     const unsigned long long *rskey;   // the sorted keys (view in the high word)
     unsigned *rcnt, *roff;          // per sorted record: tile rows of its footprint rect, their exclusive offsets
     unsigned *urec;                 // per (record, tile row) unit: the sorted record
-    uint2 *uinfo;                   // per unit: (record | active << 31, ty | lo << 10 | hi << 20)
-    unsigned *ucnt, *uoff;          // per unit: active tiles reached, their exclusive offsets (pair positions)
+    // units sorted stably by their row segment (view, tile row): key = segment << 32 | lo | hi << 16
+    // (the footprint's tile columns in the row), value = sorted record | active << 31
+    unsigned long long *ukey, *ukey_alt;
+    unsigned *uval, *uval_alt;
+    const unsigned long long *sukey;        // sorted buffers
+    const unsigned *suval;
+    int *seg_off, *seg_end;                 // [V*TY] range of each row segment in the sorted units
     long long max_units;
     unsigned long long *st_scan;    // look-back status of the offsets scan
     // tiles
-    int *tile_end;          // [V*T] end of the tile's range in the sorted pairs (== tile_off if empty)
-    int *tile_off;          // [V*T] start of the tile's range
     unsigned long long *st_tiles;
     int *items;             // [V*T] (v*T + t) of active tiles, in (v, t) order
     int *item_of_tile;      // [V*T] item index or -1
-    int *first_active;      // [items] absolute position of the first pair holding an active Gaussian (INT_MAX if none)
-    // pairs: ((v*T + t) << 32) | record | active << 31, emitted in depth order, stably sorted by tile
-    unsigned long long *pairs, *pairs_alt;
-    const unsigned long long *spairs;   // the sorted buffer (pairs or pairs_alt)
+    int *first_active;      // [items] segment position of the first active entry the fwd staged (INT_MAX if none)
     long long max_pairs;
     unsigned *rs_counts, *rs_totals;    // radix sort scratch
     // per-pixel forward state, per item [items][256]

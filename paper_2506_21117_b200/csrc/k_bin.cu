@@ -9,10 +9,10 @@
 //   2. the records are gathered into that order (64 B each); the work units are (record, tile row)
 //      pairs: per unit the closed-form x-interval of the alpha >= 1/255 ellipse over the row band
 //      and the number of ACTIVE tiles in it (row bitmasks) -> order-preserving exclusive scan;
-//   3. emission at those ranges (no atomics): pair = (view*T + tile) << 32 | sorted record;
-//   4. a stable 2-pass LSD radix sort of the pairs by their (view, tile) key keeps the
-//      depth order inside every tile;
-//   5. tile ranges and the first active entry from the sorted keys.
+//   3. per unit the footprint's tile columns [lo, hi] in its row (dead if none is active);
+//   4. a stable 2-pass LSD radix sort of the units by their row segment (view, tile row) keeps
+//      the depth order inside every segment: a tile's depth-ordered list is the subsequence of
+//      its row segment whose [lo, hi] covers it, which the raster selects while staging.
 // The result is the unique total order (depth, index) per tile, so it is deterministic.
 #include "kernels.h"
 
@@ -131,12 +131,14 @@ __global__ void __launch_bounds__(256) k_fill_units(Scratch s)
     }
 }
 
-// per unit (record i, tile row ty): the footprint's tile columns [lo, hi] in that row and the
-// number of ACTIVE tiles among them; uinfo = (i | active << 31, ty | lo << 10 | hi << 20)
-__global__ void __launch_bounds__(256) k_unit_count(const __grid_constant__ CamSet cams, Scratch s)
+// per unit (record i, tile row ty): the footprint's tile columns [lo, hi] in that row; a unit whose
+// columns hold no ACTIVE tile is dead (its segment key sorts after every live one)
+__global__ void __launch_bounds__(256) k_unit_build(const __grid_constant__ CamSet cams, Scratch s)
 {
     const int U = s.cnt->overflow ? 0 : s.cnt->n_units32;
     const int TY = cams.TY, W32 = (cams.TX + 31) >> 5;
+    const unsigned long long dead = (unsigned long long)(cams.n * TY) << 32;
+    unsigned long long pairs = 0;
     for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < U; u += gridDim.x * blockDim.x) {
         const unsigned i = s.urec[u];
         const FootRec f = foot_load(s, i);
@@ -146,72 +148,26 @@ __global__ void __launch_bounds__(256) k_unit_count(const __grid_constant__ CamS
         if (foot_row(f, ty, lo, hi)) {
             const unsigned *rm = s.rowmask + ((size_t)f.view * TY + ty) * W32;
             for (int w = lo >> 5; w <= (hi >> 5); w++) cnt += __popc(row_bits(rm, w, lo, hi));
-        } else {
-            lo = 1; hi = 0;
         }
-        s.ucnt[u] = cnt;
-        s.uinfo[u] = make_uint2(f.w, (unsigned)ty | ((unsigned)lo << 10) | ((unsigned)(hi & 1023) << 20));
+        pairs += cnt;
+        s.ukey[u] = cnt ? ((unsigned long long)(f.view * TY + ty) << 32) | (unsigned)lo | ((unsigned)hi << 16) : dead;
+        s.uval[u] = f.w;
     }
+    for (int o = 16; o > 0; o >>= 1) pairs += __shfl_xor_sync(0xffffffffu, pairs, o);
+    if ((threadIdx.x & 31) == 0 && pairs) atomicAdd(&s.cnt->n_pairs, pairs);
 }
 
-// 3. emission: unit u's pairs at uoff[u] .. + ucnt[u]; units are in (sorted record, row) order, so
-// consecutive threads write consecutive ranges (coalesced) and the pairs come out in record order.
-__global__ void __launch_bounds__(256) k_emit(const __grid_constant__ CamSet cams, Scratch s)
+// row-segment ranges of the sorted units (dead units excluded)
+__global__ void __launch_bounds__(256) k_seg_ranges(Scratch s, int n_seg)
 {
-    if (s.cnt->overflow) return;
-    const int U = s.cnt->n_units32;
-    const unsigned long long total = s.cnt->n_pairs;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        if ((long long)total > s.max_pairs) atomicOr(&s.cnt->overflow, 2);
-        s.cnt->n_pairs32 = (int)min((unsigned long long)s.max_pairs, total);
-    }
-    if ((long long)total > s.max_pairs) return;
-    const int TX = cams.TX, TY = cams.TY, T = cams.T, W32 = (TX + 31) >> 5;
-    for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < U; u += gridDim.x * blockDim.x) {
-        if (s.ucnt[u] == 0u) continue;
-        const uint2 inf = s.uinfo[u];
-        const unsigned i = inf.x & 0x7fffffffu;
-        const int ty = (int)(inf.y & 1023u), lo = (int)((inf.y >> 10) & 1023u), hi = (int)(inf.y >> 20);
-        const int view = (int)(s.rskey[i] >> 32);
-        const unsigned *rm = s.rowmask + ((size_t)view * TY + ty) * W32;
-        const unsigned long long kb = ((unsigned long long)view * T + (unsigned long long)ty * TX) << 32;
-        unsigned long long *out = s.pairs + s.uoff[u];
-        for (int w = lo >> 5; w <= (hi >> 5); w++) {
-            unsigned bits = row_bits(rm, w, lo, hi);
-            while (bits) {
-                const int tx = 32 * w + __ffs(bits) - 1;
-                bits &= bits - 1;
-                *out++ = (kb + ((unsigned long long)tx << 32)) | inf.x;
-            }
-        }
-    }
-}
-
-// 5. tile ranges of the sorted pairs and the first active entry (absolute position)
-__global__ void __launch_bounds__(256) k_ranges(Scratch s)
-{
-    const int n = s.cnt->overflow ? 0 : s.cnt->n_pairs32;
-    const unsigned long long *p = s.spairs;
+    const int n = s.cnt->overflow ? 0 : s.cnt->n_units32;
+    const unsigned long long *k = s.sukey;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const unsigned long long pi = p[i];
-        const unsigned e = (unsigned)(pi >> 32);
-        if (i == 0 || (unsigned)(p[i - 1] >> 32) != e) s.tile_off[e] = i;
-        if (i == n - 1 || (unsigned)(p[i + 1] >> 32) != e) s.tile_end[e] = i + 1;
-        if ((unsigned)pi >> 31) atomicMin(&s.first_active[s.item_of_tile[e]], i);
+        const unsigned e = (unsigned)(k[i] >> 32);
+        if (e >= (unsigned)n_seg) continue;
+        if (i == 0 || (unsigned)(k[i - 1] >> 32) != e) s.seg_off[e] = i;
+        if (i == n - 1 || (unsigned)(k[i + 1] >> 32) != e) s.seg_end[e] = i + 1;
     }
-}
-
-// longest list (diagnostics)
-__global__ void k_max_list(Scratch s)
-{
-    const int n_items = s.cnt->n_items;
-    int mx = 0;
-    for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < n_items; it += gridDim.x * blockDim.x) {
-        const int e = s.items[it];
-        mx = max(mx, s.tile_end[e] - s.tile_off[e]);
-    }
-    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((threadIdx.x & 31) == 0 && mx) atomicMax(&s.cnt->max_list, mx);
 }
 
 static int bits_for(long long x)   // bits to represent 0..x
@@ -240,7 +196,7 @@ void launch_bin_recsort(const StepDims &d, const CamSet &cams, Scratch &s, cudaS
     g_launches += 2;
 }
 
-// 2. sorted records, their (record, tile row) units, exact per-unit pair counts and offsets
+// 2. sorted records, their (record, tile row) units
 void launch_bin_count(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st)
 {
     const int R = (int)s.max_records;
@@ -248,33 +204,29 @@ void launch_bin_count(const StepDims &d, const CamSet &cams, Scratch &s, cudaStr
     scan_excl_u32(s.rcnt, s.roff, &s.cnt->n_records, R, s.st_scan, &s.cnt->scan_ticket, &s.cnt->n_units,
                   &s.cnt->overflow, st);
     k_fill_units<<<148 * 8, 256, 0, st>>>(s);
-    k_unit_count<<<148 * 8, 256, 0, st>>>(cams, s);
-    scan_excl_u32(s.ucnt, s.uoff, &s.cnt->n_units32, (int)s.max_units, s.st_scan, &s.cnt->scan_ticket2,
-                  &s.cnt->n_pairs, &s.cnt->overflow, st);
-    g_launches += 3;
+    g_launches += 2;
 }
 
-// 3. emission
+// 3. per unit: footprint columns and segment key
 void launch_bin_emit(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st)
 {
-    k_emit<<<148 * 8, 256, 0, st>>>(cams, s);
+    k_unit_build<<<148 * 8, 256, 0, st>>>(cams, s);
     g_launches += 1;
 }
 
-// 4. stable sort of the pairs by (view, tile), 5. ranges
+// 4. stable sort of the units by row segment (view, tile row); 5. segment ranges
 void launch_bin_pairsort(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st)
 {
-    const int VT = d.V * d.T;
-    const int tbits = std::max(bits_for(VT - 1), 1);
-    const int w2 = radix_sort_u64(s.pairs, s.pairs_alt, nullptr, nullptr, &s.cnt->n_pairs32, (int)s.max_pairs, 32,
-                                  32 + tbits, 9, s.rs_counts, s.rs_totals, &s.cnt->overflow, st);
-    s.spairs = w2 ? s.pairs_alt : s.pairs;
-    cudaMemsetAsync(s.tile_off, 0, sizeof(int) * (size_t)VT, st);
-    cudaMemsetAsync(s.tile_end, 0, sizeof(int) * (size_t)VT, st);
-    cudaMemsetAsync(s.first_active, 0x7f, sizeof(int) * (size_t)VT, st);
-    k_ranges<<<148 * 8, 256, 0, st>>>(s);
-    k_max_list<<<148, 256, 0, st>>>(s);
-    g_launches += 2;
+    const int n_seg = d.V * d.TY;
+    const int sbits = std::max(bits_for(n_seg), 1);   // n_seg itself marks the dead units
+    const int w = radix_sort_u64(s.ukey, s.ukey_alt, s.uval, s.uval_alt, &s.cnt->n_units32, (int)s.max_units, 32,
+                                 32 + sbits, 8, s.rs_counts, s.rs_totals, &s.cnt->overflow, st);
+    s.sukey = w ? s.ukey_alt : s.ukey;
+    s.suval = w ? s.uval_alt : s.uval;
+    cudaMemsetAsync(s.seg_off, 0, sizeof(int) * (size_t)n_seg, st);
+    cudaMemsetAsync(s.seg_end, 0, sizeof(int) * (size_t)n_seg, st);
+    k_seg_ranges<<<148 * 8, 256, 0, st>>>(s, n_seg);
+    g_launches += 1;
 }
 
 }  // namespace cls

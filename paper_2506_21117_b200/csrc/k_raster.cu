@@ -43,6 +43,77 @@ __device__ __forceinline__ void stage(const Scratch &s, unsigned val, int tx, in
     sc = make_float4(rgb.x, rgb.y, rgb.z, ax.y);
 }
 
+
+// ---------------------------------------------------------------------------
+// Staging from a row segment.  The units of the tile's row segment (view, tile row) are in depth
+// order; the tile's list is the subsequence whose column interval [lo, hi] covers tx.  One round
+// tests 256 consecutive units (4 per thread, coalesced 8 B key loads), ranks the covering ones in
+// segment order with warp ballots and stages them; a round that would overflow the batch stops
+// exactly at the first unstaged covering unit.  DIR = +1 scans forward from `cur` (< end),
+// DIR = -1 backward from `cur` (exclusive) down to `end` (inclusive), staging in descending order.
+// Returns the number of staged entries; s_pos[j] = segment position of staged entry j.
+// ---------------------------------------------------------------------------
+#define RT_SCAN 8    // units tested per thread per round (512 per round): few rounds, one latency each
+
+template <int DIR, bool BWD>
+__device__ __forceinline__ int fill_batch(const Scratch &s, int &cur, int end, int tx, int ty, float4 *sa, float4 *sb,
+                                          float4 *sc, float2 *sd, int *s_pos, int *s_wc, int *s_next, int *s_first)
+{
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned *cols = reinterpret_cast<const unsigned *>(s.sukey);   // low word: lo | hi << 16
+    int nst = 0;
+    while (nst < RT_BATCH && (DIR > 0 ? cur < end : cur > end)) {
+        unsigned cw[RT_SCAN];
+#pragma unroll
+        for (int k = 0; k < RT_SCAN; k++) {   // all loads first: one memory latency per round
+            const int u = DIR > 0 ? cur + k * RT_THREADS + tid : cur - 1 - (k * RT_THREADS + tid);
+            cw[k] = (DIR > 0 ? u < end : u >= end) ? __ldg(cols + 2 * (size_t)u) : 0xffffu;   // empty if outside
+        }
+        unsigned cov = 0u;
+#pragma unroll
+        for (int k = 0; k < RT_SCAN; k++) {
+            const int lo = (int)(cw[k] & 0xffffu), hi = (int)(cw[k] >> 16);
+            const bool c = lo <= tx && tx <= hi;
+            const unsigned b = __ballot_sync(0xffffffffu, c);
+            cov |= (c ? 1u : 0u) << k;
+            if (lane == 0) s_wc[2 * k + warp] = __popc(b);
+            cw[k] = b;   // reuse: the warp's ballot of round k
+        }
+        __syncthreads();
+        int total = 0;
+        int pre_mine = 0;
+#pragma unroll
+        for (int k = 0; k < RT_SCAN; k++) {
+            const int c0 = s_wc[2 * k], c1 = s_wc[2 * k + 1];
+            if ((cov >> k) & 1u) {
+                const int u = DIR > 0 ? cur + k * RT_THREADS + tid : cur - 1 - (k * RT_THREADS + tid);
+                const int slot = nst + total + (warp ? c0 : 0) + __popc(cw[k] & lt);
+                if (slot < RT_BATCH) {
+                    const unsigned val = s.suval[u];
+                    stage(s, val, tx, ty, sa[slot], sb[slot], sc[slot]);
+                    if (BWD) {
+                        const float4 xy = s.srec[val & 0x7fffffffu].xy;
+                        sd[slot] = make_float2(__double2float_rn(((double)xy.x - (double)(CLS_TILE * tx)) + (double)xy.y),
+                                               __double2float_rn(((double)xy.z - (double)(CLS_TILE * ty)) + (double)xy.w));
+                    }
+                    if (!BWD && (val >> 31)) atomicMin(s_first, u);
+                    s_pos[slot] = u;
+                } else if (slot == RT_BATCH) {
+                    *s_next = DIR > 0 ? u : u + 1;   // resume exactly at the first unstaged covering unit
+                }
+            }
+            total += c0 + c1;
+        }
+        (void)pre_mine;
+        __syncthreads();
+        cur = nst + total > RT_BATCH ? *s_next : (DIR > 0 ? cur + RT_SCAN * RT_THREADS : cur - RT_SCAN * RT_THREADS);
+        nst = min(nst + total, RT_BATCH);
+        __syncthreads();
+    }
+    return nst;
+}
+
 // alpha = min(0.99, o 2^-q') of a (pixel, Gaussian) with q' <= qcut'; G = 2^-q' = exp(-q/2)
 __device__ __forceinline__ float alpha_of(float qk, float o, float &G)
 {
@@ -74,7 +145,7 @@ __device__ __forceinline__ float block_sum(float v, float *red)
 // composites again -- no per-pixel "done" flags, the warp stays converged.
 // ---------------------------------------------------------------------------
 template <bool TARGET, bool IMAGE>
-__global__ void __launch_bounds__(RT_THREADS)
+__global__ void __launch_bounds__(RT_THREADS, 12)
 k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ targets, float *__restrict__ images,
       float loss_scale, float3 bg)
 {
@@ -82,7 +153,7 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
     __shared__ float4 sb[RT_BATCH];
     __shared__ float4 sc[RT_BATCH];
     __shared__ float red[RT_THREADS / 32];
-    __shared__ int s_item;
+    __shared__ int s_item, s_pos[RT_BATCH], s_wc[2 * RT_SCAN], s_next, s_first, s_lastp[CLS_BLOCK_PIX];
     if (s.cnt->overflow) return;
     const int n_items = s.cnt->n_items;
     const int tid = threadIdx.x;
@@ -99,25 +170,26 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         const int e = s.items[item];
         const int v = e / T, t = e - v * T;
         const int tx = t % TX, ty = t / TX;
-        const int off = s.tile_off[e];
-        const int n = s.tile_end[e] - off;
+        const int seg = v * cams.TY + ty;
+        int cur = s.seg_off[seg];
+        const int se = s.seg_end[seg];
+        if (tid == 0) s_first = 0x7fffffff;
         const int x = tx * CLS_TILE + lx;
         float Tr[RT_PX], C0[RT_PX], C1[RT_PX], C2[RT_PX];
-        int last[RT_PX];
+        int last[RT_PX];   // last composited entry: list index (its segment position goes to s_lastp)
 #pragma unroll
         for (int k = 0; k < RT_PX; k++) {
             const bool in = x < W && ty * CLS_TILE + ly + 4 * k < H;
             Tr[k] = in ? 1.f : -1.f;   // out-of-image pixels start terminated
             C0[k] = C1[k] = C2[k] = 0.f;
             last[k] = -1;
+            s_lastp[tid + k * RT_THREADS] = -1;
         }
-        for (int b0 = 0; b0 < n; b0 += RT_BATCH) {
+        int lbase = 0;   // list index of the batch's first entry
+        while (true) {
             const bool live = Tr[0] > 0.f || Tr[1] > 0.f || Tr[2] > 0.f || Tr[3] > 0.f;
-            if (__syncthreads_count(live) == 0) break;
-            for (int j = tid; j < RT_BATCH && b0 + j < n; j += RT_THREADS)
-                stage(s, (unsigned)s.spairs[off + b0 + j], tx, ty, sa[j], sb[j], sc[j]);
-            __syncthreads();
-            const int cnt = min(RT_BATCH, n - b0);
+            if (__syncthreads_count(live) == 0 || cur >= se) break;
+            const int cnt = fill_batch<1, false>(s, cur, se, tx, ty, sa, sb, sc, nullptr, s_pos, s_wc, &s_next, &s_first);
             for (int k = 0; k < cnt; k++) {
                 // warp-level exit once all its pixels terminated (checked every 4 entries)
                 if ((k & 3) == 0 &&
@@ -125,7 +197,7 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
                     break;
                 const float4 A = sa[k], B = sb[k], Cc = sc[k];
                 const float sx = __fmaf_rn(-A.y, flx, A.x), txx = __fmaf_rn(-B.x, flx, A.w);
-                const int pos = b0 + k;
+                const int pos = lbase + k;
 #pragma unroll
                 for (int p = 0; p < RT_PX; p++) {
                     // The exponential is cheaper than a branch around it; beyond qcut' the alpha test
@@ -147,6 +219,15 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
                     Tr[p] = ok ? Tn : -fabsf(Tr[p]);
                 }
             }
+#pragma unroll
+            for (int p = 0; p < RT_PX; p++)   // segment position of a last entry of this batch
+                if (last[p] >= lbase) s_lastp[tid + p * RT_THREADS] = s_pos[last[p] - lbase];
+            lbase += cnt;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            s.first_active[item] = s_first;
+            atomicMax(&s.cnt->max_list, lbase);
         }
         float l1 = 0.f;
 #pragma unroll
@@ -158,7 +239,7 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
             const int pl = tid + p * RT_THREADS;          // pixel slot (ly + 4p) * 16 + lx
             const size_t px = (size_t)item * CLS_BLOCK_PIX + pl;
             s.px_T[px] = Tf;
-            s.px_last[px] = last[p];
+            s.px_last[px] = s_lastp[tid + p * RT_THREADS];
             float *dl = s.px_dl + (size_t)item * 3 * CLS_BLOCK_PIX + pl;
             if (in) {
                 const float o0 = C0[p] + Tf * bg.x, o1 = C1[p] + Tf * bg.y, o2 = C2[p] + Tf * bg.z;
@@ -272,7 +353,7 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
     __shared__ float4 sb[RT_BATCH];
     __shared__ float4 sc[RT_BATCH];
     __shared__ float2 sd[RT_BATCH];    // tile-local 2D mean (dx0, dy0) in fp32
-    __shared__ int s_item, s_maxlast;
+    __shared__ int s_item, s_maxlast, s_pos[RT_BATCH], s_wc[2 * RT_SCAN], s_next;
     if (s.cnt->overflow) return;
     const int n_items = s.cnt->n_items;
     const int A = s.cnt->A;
@@ -293,8 +374,7 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         const int e = s.items[item];
         const int v = e / T, t = e - v * T;
         const int tx = t % TX, ty = t / TX;
-        const int off = s.tile_off[e];
-        const int first = min(s.first_active[item] - off, s.tile_end[e] - off);   // absolute -> list position
+        const int first = s.first_active[item];   // segment position of the first active entry (fwd)
         const int x = tx * CLS_TILE + lx;
         PixB P[RT_PX];
         int ml = -1;
@@ -325,19 +405,13 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         __syncthreads();
         const int end = s_maxlast + 1;   // exclusive
         float4 *gbase = s.grad2d + (size_t)v * A * 3;
-        for (int bend = end; bend > first; bend -= RT_BATCH) {
-            const int bstart = max(bend - RT_BATCH, first);
+        // reverse walk over the row segment [first, end): batches of covering units, descending
+        int cur = end;
+        while (cur > first) {
             __syncthreads();
-            for (int j = tid; j < bend - bstart; j += RT_THREADS) {
-                const unsigned val = (unsigned)s.spairs[off + bstart + j];
-                stage(s, val, tx, ty, sa[j], sb[j], sc[j]);
-                const float4 xy = s.srec[val & 0x7fffffffu].xy;
-                sd[j] = make_float2(__double2float_rn(((double)xy.x - (double)(CLS_TILE * tx)) + (double)xy.y),
-                                    __double2float_rn(((double)xy.z - (double)(CLS_TILE * ty)) + (double)xy.w));
-            }
-            __syncthreads();
-            for (int k = bend - 1 - bstart; k >= 0; k--) {
-                const int jj = bstart + k;
+            const int cnt = fill_batch<-1, true>(s, cur, first, tx, ty, sa, sb, sc, sd, s_pos, s_wc, &s_next, nullptr);
+            for (int k = 0; k < cnt; k++) {
+                const int jj = s_pos[k];
                 const float4 Aa = sa[k], Bb = sb[k], Cc = sc[k];
                 const int ordk = __float_as_int(Cc.w);
                 const bool active = ordk >= 0;   // uniform over the CTA
