@@ -104,7 +104,7 @@ class ClockSampler:
 def limits_for(cfg: str, n: int, n_views: int, W: int, H: int, all_tiles: bool):
     from paper_2506_21117_b200 import default_limits
     TX, TY = -(-W // 16), -(-H // 16)
-    rec = n // 2 if not all_tiles else n
+    rec = n if (all_tiles or n <= 200_000) else n // 2   # records per view (capacity)
     pairs = min(TX * TY * 2048, 8_000_000 if not all_tiles else 24_000_000)
     pairs = min(pairs, (2**31 - 2) // max(n_views, 1))
     return default_limits(n, n_views, W, H, records_per_view=min(rec, (2**31 - 1) // max(n_views, 1)),
@@ -237,6 +237,10 @@ def run_ours(args):
                         "frac": round(ach / hbm, 4), "traffic": None,
                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)", "bytes_per_launch": int(amount)}
             roof["share_of_step"] = round(per[dom]["ms"] / max(step_ms_sum, 1e-9), 3)
+            tr = ncu_traffic(args.config, dom)
+            if tr is not None and world == 1 and not args.all_tiles:
+                roof["traffic"] = tr["bytes"]
+                roof["traffic_source"] = f"dram__bytes_read.sum + dram__bytes_write.sum, {tr['source']}"
         out = {
             "metric": "local-opt steps/s (fwd+bwd+masked Adam)",
             "value": round(value, 4), "unit": "steps/s", "n_gpus": world, "steps": args.steps,
@@ -263,6 +267,25 @@ def run_ours(args):
         dist.destroy_process_group()
     opt.close()
     return out
+
+
+# kernel names of the profile groups in the ncu captures committed under profiles/
+GROUP_KERNELS = {"fwd_raster": "k_fwd<1, 0>", "project_cand": "k_project_cand<1>", "project_exact": "k_project_exact<3>",
+                 "bwd_raster": "k_bwd", "emit": "k_unit_build", "bin_count": "k_permute"}
+
+
+def ncu_traffic(config: str, group: str):
+    """DRAM bytes per launch of the group's kernel from the newest committed ncu --set full capture of
+    this workload (profiles/r*_<config>_ncu_traffic.json), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_{config}_ncu_traffic.json")))
+    if not files or group not in GROUP_KERNELS:
+        return None
+    try:
+        rec = json.load(open(files[-1])).get(GROUP_KERNELS[group])
+        return None if rec is None else {"bytes": int(rec["dram_bytes"]), "source": os.path.basename(files[-1])}
+    except Exception:
+        return None
 
 
 def algorithmic_work(sc, n_views, st):
