@@ -113,6 +113,7 @@ struct Scratch {
     float *px_T;
     int *px_last;
     float *px_dl;           // [items][3][256] fused-L1 dL/dC
+    float *tgt;             // [items][3][256] target pixels gathered from host memory (k_gather_targets)
     float *item_loss;       // [items]
     // gradients
     float4 *grad2d;         // [V][A][3]

@@ -23,6 +23,8 @@ struct cls_ctx {
     Counters *h_cnt = nullptr;   // pinned copy of the counters of the last fwd
     int *h_A = nullptr;          // pinned
     cudaEvent_t ev_member = nullptr, ev_fwd = nullptr;
+    cudaStream_t side = nullptr;                              // host-target gather stream
+    cudaEvent_t ev_items = nullptr, ev_gather = nullptr;
     bool fwd_valid = false, has_targets = false, bwd_valid = false;
     StepDims dims{};
     CamSet cams{};
@@ -142,7 +144,7 @@ cls_status cls_destroy(cls_ctx *c)
                     c->s.srec, c->s.rec_gid, c->s.cand, c->s.rkey,
                     c->s.rkey_alt, c->s.rval, c->s.rval_alt, c->s.rcnt, c->s.urec, c->s.ukey, c->s.ukey_alt, c->s.uval, c->s.uval_alt,
                     c->s.roff, c->s.st_scan, c->s.seg_off, c->s.seg_end, c->s.st_tiles, c->s.items, c->s.item_of_tile,
-                    c->s.first_active, c->s.vis, c->s.rs_counts, c->s.rs_totals, c->s.px_T, c->s.px_last, c->s.px_dl,
+                    c->s.first_active, c->s.vis, c->s.rs_counts, c->s.rs_totals, c->s.px_T, c->s.px_last, c->s.px_dl, c->s.tgt,
                     c->s.item_loss, c->s.grad2d, c->s.cnt};
     for (void *p : ptrs)
         if (p) cudaFree(p);
@@ -150,6 +152,9 @@ cls_status cls_destroy(cls_ctx *c)
     if (c->h_A) cudaFreeHost(c->h_A);
     if (c->ev_member) cudaEventDestroy(c->ev_member);
     if (c->ev_fwd) cudaEventDestroy(c->ev_fwd);
+    if (c->ev_items) cudaEventDestroy(c->ev_items);
+    if (c->ev_gather) cudaEventDestroy(c->ev_gather);
+    if (c->side) cudaStreamDestroy(c->side);
     for (auto &r : c->prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     void *dp[] = {c->d_mo, c->d_q, c->d_ls, c->d_sh, c->d_m, c->d_v, c->d_acc, c->d_cnt, c->d_work, c->d_status,
                   c->d_tot, c->d_int};
@@ -193,13 +198,16 @@ cls_status cls_create(cls_ctx **out, int device, const cls_limits *lim)
               dalloc(&s.items, VT) && dalloc(&s.item_of_tile, VT) && dalloc(&s.first_active, VT) &&
               dalloc(&s.rs_counts, (size_t)512 * RS_GRID) &&
               dalloc(&s.rs_totals, 512) && dalloc(&s.px_T, VT * 256) && dalloc(&s.px_last, VT * 256) &&
-              dalloc(&s.px_dl, VT * 768) && dalloc(&s.item_loss, VT) &&
+              dalloc(&s.px_dl, VT * 768) && dalloc(&s.tgt, VT * 768) && dalloc(&s.item_loss, VT) &&
               dalloc(&s.grad2d, V * (size_t)lim->max_active * 3) &&
               dalloc(&s.vis, V * (size_t)lim->max_active) && dalloc(&s.cnt, 1);
     if (ok) ok = cudaMallocHost((void **)&c->h_cnt, sizeof(Counters)) == cudaSuccess &&
                  cudaMallocHost((void **)&c->h_A, sizeof(int)) == cudaSuccess;
     if (ok) ok = cudaEventCreateWithFlags(&c->ev_member, cudaEventDisableTiming) == cudaSuccess &&
-                 cudaEventCreateWithFlags(&c->ev_fwd, cudaEventDisableTiming) == cudaSuccess;
+                 cudaEventCreateWithFlags(&c->ev_fwd, cudaEventDisableTiming) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&c->ev_items, cudaEventDisableTiming) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&c->ev_gather, cudaEventDisableTiming) == cudaSuccess &&
+                 cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
         cls_destroy(c);
@@ -300,7 +308,26 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     run(c, P_MEMBER, st, [&] { launch_member(p, d, regs, s, st); });
     cudaMemcpyAsync(c->h_A, &s.cnt->A, sizeof(int), cudaMemcpyDeviceToHost, st);
     cudaEventRecord(c->ev_member, st);
-    run(c, P_MASK, st, [&] { launch_active_mask(p, d, cs, s, st); });
+    run(c, P_MASK, st, [&] {
+        launch_active_mask(p, d, cs, s, st);
+        launch_bin_items(d, s, st);
+    });
+    // host-resident (pinned, mapped) targets: gather only the active tiles' pixels on the side
+    // stream, overlapped with projection and binning; the fwd waits for it
+    bool staged = false;
+    if (targets) {
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, targets) == cudaSuccess && pa.type == cudaMemoryTypeHost) {
+            if (!pa.devicePointer) return fail(c, CLS_ERR_INVALID_ARGUMENT, "host targets must be pinned and mapped");
+            cudaEventRecord(c->ev_items, st);
+            cudaStreamWaitEvent(c->side, c->ev_items, 0);
+            launch_gather_targets(d, cs, s, (const float *)pa.devicePointer, c->side);
+            cudaEventRecord(c->ev_gather, c->side);
+            staged = true;
+        } else {
+            cudaGetLastError();   // unregistered pointers report an error on some drivers: device memory
+        }
+    }
     run(c, P_PROJECT, st, [&] { launch_project_cand(p, d, cs, s, st); });
     cudaMemsetAsync(s.vis, 0, (size_t)d.V * (size_t)s.max_active, st);
     run(c, P_PROJECT_EXACT, st, [&] { launch_project_exact(p, d, cs, s, st); });
@@ -308,7 +335,8 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     run(c, P_BINCOUNT, st, [&] { launch_bin_count(d, cs, s, st); });
     run(c, P_EMIT, st, [&] { launch_bin_emit(d, cs, s, st); });
     run(c, P_PAIRSORT, st, [&] { launch_bin_pairsort(d, cs, s, st); });
-    run(c, P_FWD, st, [&] { launch_fwd(d, cs, s, targets, images, loss_scale, bgc, st); });
+    if (staged) cudaStreamWaitEvent(st, c->ev_gather, 0);
+    run(c, P_FWD, st, [&] { launch_fwd(d, cs, s, targets, staged, images, loss_scale, bgc, st); });
     if (images) run(c, P_FILL, st, [&] { launch_fill_bg(d, s, images, bgc, st); });
     if (targets && loss) run(c, P_LOSS, st, [&] { launch_loss(s, loss_scale, loss, st); });
     if (tile_mask) cudaMemcpyAsync(tile_mask, s.mask, (size_t)d.V * d.T, cudaMemcpyDeviceToDevice, st);

@@ -177,13 +177,51 @@ static int bits_for(long long x)   // bits to represent 0..x
     return b;
 }
 
-// 1. items + record depth sort + ties
-void launch_bin_recsort(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st)
+// 0. items: the active (view, tile)s in (view, tile) order (right after the tile mask)
+void launch_bin_items(const StepDims &d, Scratch &s, cudaStream_t st)
 {
     const int VT = d.V * d.T;
     const int blocks = (VT + TSCAN_TILE - 1) / TSCAN_TILE;
     cudaMemsetAsync(s.st_tiles, 0, sizeof(unsigned long long) * blocks, st);
     k_tiles_scan<<<blocks, TSCAN_THREADS, 0, st>>>(VT, s);
+    g_launches++;
+}
+
+// target pixels of the active tiles, gathered from (mapped, pinned) host memory into the
+// per-item layout [item][3][256] that k_fwd reads: only the pixels the local step needs cross
+// the host link.  One warp per (item, channel); lanes cover 16-pixel rows.
+__global__ void __launch_bounds__(256) k_gather_targets(const __grid_constant__ CamSet cams, Scratch s,
+                                                        const float *__restrict__ host_targets)
+{
+    const int n_items = s.cnt->overflow ? 0 : s.cnt->n_items;
+    const int W = cams.W, H = cams.H, TX = cams.TX, T = cams.T;
+    const size_t HW = (size_t)H * W;
+    const int lane = threadIdx.x & 31;
+    for (int wk = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wk < n_items * 3; wk += (gridDim.x * blockDim.x) >> 5) {
+        const int item = wk / 3, ch = wk - 3 * item;
+        const int e = s.items[item];
+        const int v = e / T, t = e - v * T;
+        const int x0 = (t % TX) * CLS_TILE, y0 = (t / TX) * CLS_TILE;
+        const float *src = host_targets + (size_t)v * 3 * HW + (size_t)ch * HW;
+        float *dst = s.tgt + ((size_t)item * 3 + ch) * CLS_BLOCK_PIX;
+#pragma unroll
+        for (int k = 0; k < CLS_BLOCK_PIX / 32; k++) {
+            const int pl = k * 32 + lane, x = x0 + (pl & 15), y = y0 + (pl >> 4);
+            dst[pl] = (x < W && y < H) ? src[(size_t)y * W + x] : 0.f;
+        }
+    }
+}
+
+void launch_gather_targets(const StepDims &d, const CamSet &cams, const Scratch &s, const float *host_targets,
+                           cudaStream_t st)
+{
+    k_gather_targets<<<148 * 4, 256, 0, st>>>(cams, s, host_targets);
+    g_launches++;
+}
+
+// 1. record depth sort + ties
+void launch_bin_recsort(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st)
+{
     const int rbits = 32 + bits_for(d.V - 1);
     const int R = (int)s.max_records;
     const int w = radix_sort_u64(s.rkey, s.rkey_alt, s.rval, s.rval_alt, &s.cnt->n_records, R, 0, rbits, 8,
@@ -193,7 +231,7 @@ void launch_bin_recsort(const StepDims &d, const CamSet &cams, Scratch &s, cudaS
     s.rsorted = rv;
     s.rskey = rk;
     k_rec_ties<<<148 * 4, 256, 0, st>>>(s, rk, rv);
-    g_launches += 2;
+    g_launches += 1;
 }
 
 // 2. sorted records, their (record, tile row) units

@@ -146,8 +146,8 @@ __device__ __forceinline__ float block_sum(float v, float *red)
 // ---------------------------------------------------------------------------
 template <bool TARGET, bool IMAGE>
 __global__ void __launch_bounds__(RT_THREADS, 12)
-k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ targets, float *__restrict__ images,
-      float loss_scale, float3 bg)
+k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ targets, bool staged,
+      float *__restrict__ images, float loss_scale, float3 bg)
 {
     __shared__ float4 sa[RT_BATCH];
     __shared__ float4 sb[RT_BATCH];
@@ -251,7 +251,14 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
                     images[pix + 2 * HW] = o2;
                 }
                 if (TARGET) {
-                    const float r0 = o0 - targets[pix], r1 = o1 - targets[pix + HW], r2 = o2 - targets[pix + 2 * HW];
+                    float t0, t1, t2;
+                    if (staged) {   // gathered per item (host-resident targets)
+                        const float *tg = s.tgt + (size_t)item * 3 * CLS_BLOCK_PIX + pl;
+                        t0 = tg[0]; t1 = tg[CLS_BLOCK_PIX]; t2 = tg[2 * CLS_BLOCK_PIX];
+                    } else {
+                        t0 = targets[pix]; t1 = targets[pix + HW]; t2 = targets[pix + 2 * HW];
+                    }
+                    const float r0 = o0 - t0, r1 = o1 - t1, r2 = o2 - t2;
                     l1 += fabsf(r0) + fabsf(r1) + fabsf(r2);
                     dl[0] = r0 > 0.f ? loss_scale : (r0 < 0.f ? -loss_scale : 0.f);
                     dl[CLS_BLOCK_PIX] = r1 > 0.f ? loss_scale : (r1 < 0.f ? -loss_scale : 0.f);
@@ -270,14 +277,14 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
     if ((tid & 31) == 0 && evals) atomicAdd(&s.cnt->fwd_evals, evals);
 }
 
-void launch_fwd(const StepDims &d, const CamSet &cams, const Scratch &s, const float *targets, float *images,
-                float loss_scale, float3 bg, cudaStream_t st)
+void launch_fwd(const StepDims &d, const CamSet &cams, const Scratch &s, const float *targets, bool staged,
+                float *images, float loss_scale, float3 bg, cudaStream_t st)
 {
     const int grid = 148 * 16;
-    if (targets && images) k_fwd<true, true><<<grid, RT_THREADS, 0, st>>>(cams, s, targets, images, loss_scale, bg);
-    else if (targets) k_fwd<true, false><<<grid, RT_THREADS, 0, st>>>(cams, s, targets, images, loss_scale, bg);
-    else if (images) k_fwd<false, true><<<grid, RT_THREADS, 0, st>>>(cams, s, targets, images, loss_scale, bg);
-    else k_fwd<false, false><<<grid, RT_THREADS, 0, st>>>(cams, s, targets, images, loss_scale, bg);
+    if (targets && images) k_fwd<true, true><<<grid, RT_THREADS, 0, st>>>(cams, s, targets, staged, images, loss_scale, bg);
+    else if (targets) k_fwd<true, false><<<grid, RT_THREADS, 0, st>>>(cams, s, targets, staged, images, loss_scale, bg);
+    else if (images) k_fwd<false, true><<<grid, RT_THREADS, 0, st>>>(cams, s, targets, staged, images, loss_scale, bg);
+    else k_fwd<false, false><<<grid, RT_THREADS, 0, st>>>(cams, s, targets, staged, images, loss_scale, bg);
     g_launches++;
 }
 

@@ -238,3 +238,27 @@ def test_full_size_c4_sampled_views(torch_cuda):
         H.assert_images(g["images"][v], r)
     r = H.compare_grads(g["grad"], H.oracle_rows(fb, sub.sh_degree))
     assert r["n_bad"] == 0, r
+
+
+def test_host_resident_targets_match_device_targets(torch_cuda):
+    """Targets in pinned host memory (only the active tiles' pixels are gathered on the device,
+    DESIGN.md "End to end") give bit-identical loss and images; the gradients agree up to the
+    order of the float atomics of the backward (not bit-reproducible run to run)."""
+    torch = torch_cuda
+    from paper_2506_21117_b200 import GaussianParams, LocalOptimizer, default_limits
+    sc = SCENES["c2r"]()
+    out = []
+    for host in (False, True):
+        p = GaussianParams.from_scene(sc)
+        opt = LocalOptimizer(p, sc.regions, limits=default_limits(sc.n, len(sc.cameras), sc.width, sc.height))
+        tg = torch.from_numpy(np.ascontiguousarray(sc.targets))
+        tg = tg.pin_memory() if host else tg.cuda()
+        res = opt.forward(sc.cameras, tg, images=True)
+        g = opt.backward()
+        torch.cuda.synchronize()
+        out.append((res.loss.item(), res.images.cpu().numpy(), g.cpu().numpy()))
+        opt.close()
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1], out[1][1])
+    g0, g1 = out[0][2].astype(np.float64), out[1][2].astype(np.float64)
+    assert np.all(np.abs(g0 - g1) <= 1e-5 * np.abs(g0) + 1e-6 * np.abs(g0).max())
