@@ -76,6 +76,7 @@ struct Scratch {
     // masks
     uint8_t *mask;          // [V][T]
     int *sat;               // [V][(TY+1)(TX+1)]
+    int *mdiff;             // [V][(TY+1)(TX+1)]  corner differences of the active rects (tile mask)
     unsigned *rowmask;      // [V][TY][ceil(TX/32)] active-tile row bitmasks
     int4 *view_bbox;        // [V] tile bbox of the active tiles
     int *diff;              // [V][(TY+1)(TX+1)]  corner differences of record rects

@@ -140,7 +140,7 @@ cls_status cls_destroy(cls_ctx *c)
 {
     if (!c) return CLS_ERR_INVALID_ARGUMENT;
     cudaSetDevice(c->device);
-    void *ptrs[] = {c->s.idx, c->s.ord, c->s.st_member, c->s.mask, c->s.sat, c->s.rowmask, c->s.view_bbox, c->s.rec,
+    void *ptrs[] = {c->s.idx, c->s.ord, c->s.st_member, c->s.mask, c->s.sat, c->s.mdiff, c->s.rowmask, c->s.view_bbox, c->s.rec,
                     c->s.srec, c->s.rec_gid, c->s.cand, c->s.rkey,
                     c->s.rkey_alt, c->s.rval, c->s.rval_alt, c->s.rcnt, c->s.urec, c->s.ukey, c->s.ukey_alt, c->s.uval, c->s.uval_alt,
                     c->s.roff, c->s.st_scan, c->s.seg_off, c->s.seg_end, c->s.st_tiles, c->s.items, c->s.item_of_tile,
@@ -188,7 +188,7 @@ cls_status cls_create(cls_ctx **out, int device, const cls_limits *lim)
     const size_t SAT = V * (c->maxTY + 1) * (c->maxTX + 1);
     Scratch &s = c->s;
     bool ok = dalloc(&s.idx, N) && dalloc(&s.ord, N) && dalloc(&s.st_member, N / 2048 + 2) && dalloc(&s.mask, VT) &&
-              dalloc(&s.sat, SAT) && dalloc(&s.rowmask, V * c->maxTY * ((c->maxTX + 31) / 32)) &&
+              dalloc(&s.sat, SAT) && dalloc(&s.mdiff, SAT) && dalloc(&s.rowmask, V * c->maxTY * ((c->maxTX + 31) / 32)) &&
               dalloc(&s.view_bbox, V) && dalloc(&s.rec, R) && dalloc(&s.srec, R) && dalloc(&s.rec_gid, R) &&
               dalloc(&s.cand, R + R / 2 + 1024) && dalloc(&s.rkey, R) && dalloc(&s.rkey_alt, R) && dalloc(&s.rval, R) &&
               dalloc(&s.rval_alt, R) && dalloc(&s.rcnt, R) && dalloc(&s.urec, P) && dalloc(&s.ukey, P) &&

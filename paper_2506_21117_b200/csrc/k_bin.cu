@@ -5,7 +5,7 @@
 // (view | tile) and each tile's list is ordered by depth, ties by Gaussian index (reading
 // R13).  B200 design: no per-pair depth keys are sorted at all.
 //   1. the ~6M records are sorted ONCE by (view, fp32 depth) with a stable LSD radix sort
-//      (k_sort.cu); runs of equal keys are then ordered by Gaussian index (k_rec_ties);
+//      (k_sort.cu); runs of equal keys are ordered by Gaussian index while gathering (k_permute);
 //   2. the records are gathered into that order (64 B each); the work units are (record, tile row)
 //      pairs: per unit the closed-form x-interval of the alpha >= 1/255 ellipse over the row band
 //      and the number of ACTIVE tiles in it (row bitmasks) -> order-preserving exclusive scan;
@@ -58,8 +58,8 @@ __global__ void __launch_bounds__(TSCAN_THREADS) k_tiles_scan(int total, Scratch
         }
         if (lane < TSCAN_THREADS / 32) s_warp[lane] = wi - w;
         const unsigned agg = __shfl_sync(0xffffffffu, wi, TSCAN_THREADS / 32 - 1);
+        const unsigned long long pre = lookback_warp(s.st_tiles, tile, (unsigned long long)agg);
         if (lane == 0) {
-            const unsigned long long pre = lookback(s.st_tiles, tile, (unsigned long long)agg);
             s_prefix = (unsigned)pre;
             if (tile == (int)gridDim.x - 1) s.cnt->n_items = (int)(pre + agg);
         }
@@ -80,36 +80,31 @@ __global__ void __launch_bounds__(TSCAN_THREADS) k_tiles_scan(int total, Scratch
     }
 }
 
-// -------- records: ties of the (view, depth) sort ordered by Gaussian index (R13) --------
-__global__ void k_rec_ties(Scratch s, const unsigned long long *__restrict__ key, unsigned *val)
-{
-    const int n = s.cnt->overflow ? 0 : min(s.cnt->n_records, (int)s.max_records);
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i + 1 < n; i += gridDim.x * blockDim.x) {
-        const unsigned long long k = key[i];
-        if (key[i + 1] != k || (i > 0 && key[i - 1] == k)) continue;   // not the start of a run
-        int end = i + 2;
-        while (end < n && key[end] == k) end++;
-        for (int a = i + 1; a < end; a++) {   // insertion sort of the run by Gaussian index
-            const unsigned va = val[a];
-            const int ga = s.rec_gid[va];
-            int b = a - 1;
-            while (b >= i && s.rec_gid[val[b]] > ga) {
-                val[b + 1] = val[b];
-                b--;
-            }
-            val[b + 1] = va;
-        }
-    }
-}
-
 // 2. records gathered into (view, depth, index) order (one 64 B record per access) and the
 // number of tile rows of each footprint rect: the work units of the binning are (record, tile row)
 // pairs, so every thread does the same small amount of work however tall a footprint is.
 __global__ void __launch_bounds__(256) k_permute(Scratch s)
 {
     const int n = s.cnt->overflow ? 0 : min(s.cnt->n_records, (int)s.max_records);
+    const unsigned long long *key = s.rskey;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const Rec R = s.rec[s.rsorted[i]];
+        // ties of the (view, depth) key are ordered by Gaussian index (R13): inside a run of equal
+        // keys (rare, short) position i takes the run member of rank i - start in index order
+        const unsigned long long k = key[i];
+        unsigned r = s.rsorted[i];
+        if ((i > 0 && key[i - 1] == k) || (i + 1 < n && key[i + 1] == k)) {
+            int a = i, b = i + 1;
+            while (a > 0 && key[a - 1] == k) a--;
+            while (b < n && key[b] == k) b++;
+            for (int j = a; j < b; j++) {
+                const unsigned rj = s.rsorted[j];
+                const int gj = s.rec_gid[rj];
+                int rank = 0;
+                for (int q = a; q < b; q++) rank += s.rec_gid[s.rsorted[q]] < gj;
+                if (rank == i - a) { r = rj; break; }
+            }
+        }
+        const Rec R = s.rec[r];
         s.srec[i] = R;
         s.rcnt[i] = (unsigned)((__float_as_int(R.aux.w) >> 16) - (__float_as_int(R.aux.z) >> 16));
     }
@@ -229,9 +224,7 @@ void launch_bin_recsort(const StepDims &d, const CamSet &cams, Scratch &s, cudaS
     unsigned long long *rk = w ? s.rkey_alt : s.rkey;
     unsigned *rv = w ? s.rval_alt : s.rval;
     s.rsorted = rv;
-    s.rskey = rk;
-    k_rec_ties<<<148 * 4, 256, 0, st>>>(s, rk, rv);
-    g_launches += 1;
+    s.rskey = rk;   // ties are resolved by k_permute
 }
 
 // 2. sorted records, their (record, tile row) units

@@ -55,8 +55,8 @@ k_member(const float4 *__restrict__ mean_op, int n, const __grid_constant__ RegS
         if (lane < total_cells) s_wcnt[lane / nw][lane % nw] = inc0 - v0;
         if (lane + 32 < total_cells) s_wcnt[(lane + 32) / nw][(lane + 32) % nw] = inc1 - v1;
         const int agg = __shfl_sync(0xffffffffu, inc1, 31);
+        const unsigned long long pre = lookback_warp(s.st_member, tile, (unsigned long long)agg);
         if (lane == 0) {
-            unsigned long long pre = lookback(s.st_member, tile, (unsigned long long)agg);
             s_prefix = pre;
             if (tile == (int)gridDim.x - 1) s.cnt->A = (int)(pre + agg);
         }
@@ -102,18 +102,42 @@ k_active_rects(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
         if (!project_gaussian(__ldg(mean_op + i), __ldg(quat + i), __ldg(log_scale + i), cams.c[v], cams.W, cams.H,
                               cams.TX, cams.TY, p))
             continue;
-        uint8_t *mk = s.mask + (size_t)v * cams.T;
-        for (int ty = p.y0; ty < p.y1; ty++)
-            for (int tx = p.x0; tx < p.x1; tx++) mk[ty * cams.TX + tx] = 1;
+        // rect corners into the view's difference array; k_sat integrates it (O(1) per rect)
+        const int P = cams.TX + 1;
+        int *D = s.mdiff + (size_t)v * (cams.TY + 1) * P;
+        atomicAdd(D + p.y0 * P + p.x0, 1);
+        atomicAdd(D + p.y0 * P + p.x1, -1);
+        atomicAdd(D + p.y1 * P + p.x0, -1);
+        atomicAdd(D + p.y1 * P + p.x1, 1);
     }
 }
 
-// summed-area table of each view's mask, one block per view
-__global__ void __launch_bounds__(256) k_sat(const __grid_constant__ CamSet cams, Scratch s)
+// mask of each view from the rect-corner differences (2D prefix sum > 0: the tile lies in some
+// active rect), then its summed-area table; one block per view
+__global__ void __launch_bounds__(256) k_sat(const __grid_constant__ CamSet cams, Scratch s, int all_tiles)
 {
     const int v = blockIdx.x;
     const int TX = cams.TX, TY = cams.TY, P = TX + 1;
-    const uint8_t *mk = s.mask + (size_t)v * cams.T;
+    uint8_t *mk = s.mask + (size_t)v * cams.T;
+    if (!all_tiles) {
+        int *D = s.mdiff + (size_t)v * (TY + 1) * P;
+        for (int y = threadIdx.x; y < TY; y += blockDim.x) {   // row prefix
+            int acc = 0;
+            for (int x = 0; x < TX; x++) {
+                acc += D[y * P + x];
+                D[y * P + x] = acc;
+            }
+        }
+        __syncthreads();
+        for (int x = threadIdx.x; x < TX; x += blockDim.x) {   // column prefix -> mask
+            int acc = 0;
+            for (int y = 0; y < TY; y++) {
+                acc += D[y * P + x];
+                mk[y * TX + x] = acc > 0 ? 1 : 0;
+            }
+        }
+        __syncthreads();
+    }
     int *S = s.sat + (size_t)v * (TY + 1) * P;
     for (int x = threadIdx.x; x < P; x += blockDim.x) S[x] = 0;
     // row prefix sums
@@ -170,13 +194,13 @@ void launch_active_mask(const Params &g, const StepDims &d, const CamSet &cams, 
     if (d.all_tiles) {
         cudaMemsetAsync(s.mask, 1, (size_t)d.V * d.T, st);
     } else {
-        cudaMemsetAsync(s.mask, 0, (size_t)d.V * d.T, st);
+        cudaMemsetAsync(s.mdiff, 0, sizeof(int) * (size_t)d.V * (d.TY + 1) * (d.TX + 1), st);
         int blocks = (int)std::min<long long>(((long long)d.n * d.V + 255) / 256, 148LL * 8);
         if (blocks < 1) blocks = 1;
         k_active_rects<<<blocks, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, cams, s);
         g_launches++;
     }
-    k_sat<<<d.V, 256, 0, st>>>(cams, s);
+    k_sat<<<d.V, 256, 0, st>>>(cams, s, d.all_tiles);
     g_launches++;
 }
 
