@@ -250,6 +250,29 @@ cls_status cls_densify(cls_ctx *ctx, float *mean_op, float *quat, float *log_sca
                        float grad_threshold, float log_scale_threshold, int64_t *n_clone,
                        int64_t *n_split, void *stream);
 
+/* ---------------------------------------------------------------------------------------
+ * NEXT-2: lifting 2D change masks to O^t (PAPER.md Supp. L458-L469).
+ * ------------------------------------------------------------------------------------- */
+
+/* Majority voting (L460-L463): for every Gaussian centre (mean_op, device float4[n]) and each of
+ * the n_views posed cameras (host), c = views whose binary mask (device uint8[n_views][H][W],
+ * nonzero = changed) contains the projected centre, o = views where the centre projects outside
+ * the image (reading R34: pixel (x, y) covers [x, x+1) x [y, y+1) in intrinsics coordinates; a
+ * centre behind the camera is outside).  member[i] (device uint8[n] out) = 1 iff
+ * (4/3) o < n_views < 2 c (evaluated exactly in integers).  c_out, o_out (device int32[n]) optional. */
+cls_status cls_majority_vote(cls_ctx *ctx, const float *mean_op, int64_t n, const cls_camera *cams,
+                             int32_t n_views, const uint8_t *masks, int32_t *c_out, int32_t *o_out,
+                             uint8_t *member, void *stream);
+
+/* Sphere fitting (L468-L469): for each cluster k in [0, n_clusters) of the points mean_op[i] with
+ * labels[i] == k (device int32[n]; -1 or >= n_clusters = not clustered -- the clustering itself,
+ * HDBSCAN, is outside this library): centre = member mean, radius = 1.1 x the 98th percentile of
+ * the member distances to the centre, linear interpolation between order statistics (R35).
+ * centres (device float[n_clusters][3]) and radii (device float[n_clusters]) out; empty clusters
+ * get radius 0. */
+cls_status cls_fit_spheres(cls_ctx *ctx, const float *mean_op, int64_t n, const int32_t *labels,
+                           int32_t n_clusters, float *centres, float *radii, void *stream);
+
 const char *cls_status_string(cls_status s);
 const char *cls_last_error(const cls_ctx *ctx);
 /* Number of kernels launched by the library since cls_create (host counter). */

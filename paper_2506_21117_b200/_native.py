@@ -22,7 +22,7 @@ STATUS = {0: "CLS_OK", 1: "CLS_ERR_INVALID_ARGUMENT", 2: "CLS_ERR_DIMENSION_MISM
 EXPORTS = ("cls_create", "cls_destroy", "cls_render_fwd", "cls_active", "cls_copy_active", "cls_render_bwd", "cls_adam_masked",
            "cls_stats", "cls_profile_enable", "cls_profile_read", "cls_debug_grad2d", "cls_status_string",
            "cls_last_error", "cls_launch_count", "cls_partition_static", "cls_prune_outside", "cls_densify_stats",
-           "cls_densify")
+           "cls_densify", "cls_majority_vote", "cls_fit_spheres")
 CLS_PROF_GROUPS = 16
 
 
@@ -106,11 +106,13 @@ def _load():
     L.cls_densify_stats.argtypes = [V, V, V, V]
     L.cls_densify.argtypes = [V, V, V, V, V, V, V, V, V, ctypes.c_int32, ctypes.c_int64, i64p, ctypes.c_int64, V,
                               ctypes.c_float, ctypes.c_float, i64p, i64p, V]
+    L.cls_majority_vote.argtypes = [V, V, ctypes.c_int64, P(cls_camera), ctypes.c_int32, V, V, V, V, V]
+    L.cls_fit_spheres.argtypes = [V, V, ctypes.c_int64, V, ctypes.c_int32, V, V, V]
     L.cls_launch_count.argtypes = [V]
     L.cls_launch_count.restype = ctypes.c_int64
     for name in ("cls_create", "cls_destroy", "cls_render_fwd", "cls_active", "cls_copy_active", "cls_render_bwd", "cls_adam_masked",
                  "cls_stats", "cls_debug_grad2d", "cls_profile_enable", "cls_profile_read", "cls_partition_static",
-                 "cls_prune_outside", "cls_densify_stats", "cls_densify"):
+                 "cls_prune_outside", "cls_densify_stats", "cls_densify", "cls_majority_vote", "cls_fit_spheres"):
         getattr(L, name).restype = ctypes.c_int
     return L
 

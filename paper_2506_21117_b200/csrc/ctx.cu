@@ -48,6 +48,12 @@ struct cls_ctx {
     unsigned *d_work = nullptr;
     unsigned long long *d_status = nullptr, *d_tot = nullptr;
     int *d_int = nullptr;
+    // NEXT-2 scratch (sphere fit), grown as needed
+    size_t sph_n = 0, sph_k = 0;
+    double *d_sums = nullptr;
+    unsigned long long *d_k0 = nullptr, *d_k1 = nullptr;
+    unsigned *d_v0 = nullptr, *d_v1 = nullptr;
+    int *d_starts = nullptr;
 };
 
 static const char *PROF_NAMES[] = {"member", "active_mask", "project_cand", "project_exact", "rec_sort", "bin_count",
@@ -157,7 +163,7 @@ cls_status cls_destroy(cls_ctx *c)
     if (c->side) cudaStreamDestroy(c->side);
     for (auto &r : c->prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     void *dp[] = {c->d_mo, c->d_q, c->d_ls, c->d_sh, c->d_m, c->d_v, c->d_acc, c->d_cnt, c->d_work, c->d_status,
-                  c->d_tot, c->d_int};
+                  c->d_tot, c->d_int, c->d_sums, c->d_k0, c->d_k1, c->d_v0, c->d_v1, c->d_starts};
     for (void *p : dp)
         if (p) cudaFree(p);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -663,6 +669,62 @@ cls_status cls_densify_stats(cls_ctx *c, float *accum, int32_t *count, void *str
     cudaSetDevice(c->device);
     launch_densify_stats(c->dims, c->s, c->n_views_total, accum, count, (cudaStream_t)stream);
     return check_cuda(c, "cls_densify_stats");
+}
+
+// ---------------------------------------------------------------------------
+// NEXT-2: majority voting, sphere fitting
+// ---------------------------------------------------------------------------
+cls_status cls_majority_vote(cls_ctx *c, const float *mean_op, int64_t n, const cls_camera *cams, int32_t n_views,
+                             const uint8_t *masks, int32_t *c_out, int32_t *o_out, uint8_t *member, void *stream)
+{
+    if (!c) return CLS_ERR_INVALID_ARGUMENT;
+    if (!mean_op || !cams || !masks || !member || n <= 0 || n >= (1ll << 31) || n_views <= 0 ||
+        n_views > CLS_MAX_VIEWS)
+        return fail(c, CLS_ERR_INVALID_ARGUMENT, "cls_majority_vote: bad arguments");
+    CamSet cs{};
+    cs.n = n_views;
+    cs.W = cams[0].width;
+    cs.H = cams[0].height;
+    for (int v = 0; v < n_views; v++) {
+        const cls_camera &cm = cams[v];
+        if (cm.width != cs.W || cm.height != cs.H || cm.width < 1 || cm.height < 1 || !(cm.fx > 0.f) || !(cm.fy > 0.f))
+            return fail(c, CLS_ERR_DIMENSION_MISMATCH, "cls_majority_vote: view %d", v);
+        GCam &g = cs.c[v];
+        memcpy(g.R, cm.R, sizeof g.R);
+        memcpy(g.t, cm.t, sizeof g.t);
+        g.fx = cm.fx; g.fy = cm.fy; g.cx = cm.cx; g.cy = cm.cy;
+    }
+    cudaSetDevice(c->device);
+    launch_vote((const float4 *)mean_op, (int)n, cs, masks, c_out, o_out, member, (cudaStream_t)stream);
+    return check_cuda(c, "cls_majority_vote");
+}
+
+cls_status cls_fit_spheres(cls_ctx *c, const float *mean_op, int64_t n, const int32_t *labels, int32_t n_clusters,
+                           float *centres, float *radii, void *stream)
+{
+    if (!c) return CLS_ERR_INVALID_ARGUMENT;
+    if (!mean_op || !labels || !centres || !radii || n <= 0 || n >= (1ll << 31) || n_clusters <= 0 ||
+        n_clusters >= (1 << 24))
+        return fail(c, CLS_ERR_INVALID_ARGUMENT, "cls_fit_spheres: bad arguments");
+    cudaSetDevice(c->device);
+    if ((size_t)n > c->sph_n || (size_t)n_clusters + 1 > c->sph_k) {
+        void *old[] = {c->d_sums, c->d_k0, c->d_k1, c->d_v0, c->d_v1, c->d_starts};
+        for (void *p : old)
+            if (p) cudaFree(p);
+        c->d_sums = nullptr; c->d_k0 = c->d_k1 = nullptr; c->d_v0 = c->d_v1 = nullptr; c->d_starts = nullptr;
+        c->sph_n = c->sph_k = 0;
+        const size_t N = (size_t)n + 4, K = (size_t)n_clusters + 2;
+        if (!(dalloc(&c->d_sums, 4 * K) && dalloc(&c->d_k0, N) && dalloc(&c->d_k1, N) && dalloc(&c->d_v0, N) &&
+              dalloc(&c->d_v1, N) && dalloc(&c->d_starts, K)))
+            return fail(c, CLS_ERR_OUT_OF_MEMORY, "cls_fit_spheres scratch");
+        c->sph_n = N;
+        c->sph_k = K;
+    }
+    if (!c->d_int && !dalloc(&c->d_int, 4)) return fail(c, CLS_ERR_OUT_OF_MEMORY, "cls_fit_spheres scratch");
+    launch_fit_spheres((const float4 *)mean_op, (int)n, labels, n_clusters, c->d_sums, c->d_k0, c->d_k1, c->d_v0,
+                       c->d_v1, c->d_starts, c->d_int, c->s.rs_counts, c->s.rs_totals, centres, radii,
+                       (cudaStream_t)stream);
+    return check_cuda(c, "cls_fit_spheres");
 }
 
 }  // extern "C"

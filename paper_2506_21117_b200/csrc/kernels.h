@@ -77,6 +77,13 @@ void launch_suffix_apply(const RowArrays &a, long long n_static, int S, const Ro
                          const unsigned long long *tot, const float *normals, cudaStream_t st);
 void launch_reset_stats(float *acc, int *cnt, long long n, cudaStream_t st);
 
+// NEXT-2: majority voting and sphere fitting (k_voting.cu)
+void launch_vote(const float4 *mean_op, int n, const CamSet &cams, const uint8_t *masks, int *c_out, int *o_out,
+                 uint8_t *member, cudaStream_t st);
+void launch_fit_spheres(const float4 *mean_op, int n, const int *labels, int K, double *sums, unsigned long long *keys,
+                        unsigned long long *keys_alt, unsigned *vals, unsigned *vals_alt, int *starts, int *n_dev,
+                        unsigned *counts, unsigned *totals, float *centres, float *radii, cudaStream_t st);
+
 extern int64_t g_launches;   // kernels launched by this process through libcls (host counter)
 
 }  // namespace cls

@@ -321,6 +321,35 @@ class LocalOptimizer:
         p._set_n(int(n.value))
         return int(nc.value), int(nsp.value)
 
+    # -- NEXT-2: majority voting, sphere fitting -------------------------------------------------------
+    def majority_vote(self, mean_op: torch.Tensor, cameras, masks: torch.Tensor, stream=None):
+        """Majority voting of the centres `mean_op` [n, 4] over the posed binary
+        change masks `masks` [V, H, W] (uint8, device).  Returns (member bool [n], c int32 [n], o int32 [n])."""
+        n = int(mean_op.shape[0])
+        assert masks.dtype == torch.uint8 and masks.is_contiguous() and masks.shape[0] == len(cameras)
+        dev = mean_op.device
+        member = torch.empty(n, dtype=torch.uint8, device=dev)
+        c = torch.empty(n, dtype=torch.int32, device=dev)
+        o = torch.empty(n, dtype=torch.int32, device=dev)
+        cams = camera_structs(cameras)
+        check(lib.cls_majority_vote(self.ctx, ctypes.c_void_p(mean_op.data_ptr()), n, cams, len(cameras),
+                                    ctypes.c_void_p(masks.data_ptr()), ctypes.c_void_p(c.data_ptr()),
+                                    ctypes.c_void_p(o.data_ptr()), ctypes.c_void_p(member.data_ptr()),
+                                    ctypes.c_void_p(_stream_ptr(stream))), self.ctx)
+        return member.bool(), c, o
+
+    def fit_spheres(self, mean_op: torch.Tensor, labels: torch.Tensor, n_clusters: int, stream=None):
+        """One sphere per cluster (L468-L469): centre = member mean, radius = 1.1 x 98th percentile of
+        the member distances.  `labels` int32 [n] (-1 = unclustered).  Returns (centres [K, 3], radii [K])."""
+        n = int(mean_op.shape[0])
+        assert labels.dtype == torch.int32 and labels.is_contiguous() and labels.shape[0] == n
+        centres = torch.empty((n_clusters, 3), dtype=torch.float32, device=mean_op.device)
+        radii = torch.empty(n_clusters, dtype=torch.float32, device=mean_op.device)
+        check(lib.cls_fit_spheres(self.ctx, ctypes.c_void_p(mean_op.data_ptr()), n, ctypes.c_void_p(labels.data_ptr()),
+                                  int(n_clusters), ctypes.c_void_p(centres.data_ptr()),
+                                  ctypes.c_void_p(radii.data_ptr()), ctypes.c_void_p(_stream_ptr(stream))), self.ctx)
+        return centres, radii
+
     # -- one full local-optimisation step ----------------------------------------------------------
     def step(self, cameras, targets: torch.Tensor, n_views_total: Optional[int] = None,
              allreduce: Optional[Callable[[torch.Tensor, torch.Tensor], None]] = None, stream=None):

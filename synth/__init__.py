@@ -318,3 +318,47 @@ def scene_from_arrays(means, log_scales, quats, opacity_logits, sh, sh_degree, c
                  np.asarray(quats, np.float32), np.asarray(opacity_logits, np.float32),
                  np.asarray(sh, np.float32).reshape(len(means), (sh_degree + 1) ** 2, 3), sh_degree,
                  list(cameras), list(regions), None if targets is None else np.asarray(targets, np.float32))
+
+
+def change_masks(scene: Scene, cameras=None, noise: float = 0.002, seed: int = 17) -> np.ndarray:
+    """Synthetic binary 2D change masks [V][H][W] (uint8) standing in for the DINOv2 change
+    detection of PAPER.md L450-L456 (unavailable here): each change region is drawn as the disk
+    (sphere) or rectangle (box corners) its bounds project to, dilated by 2 % of the width
+    (L456), then a seeded fraction `noise` of the pixels is flipped (imperfect 2D detection).
+    Input synthesis only -- none of the method's arithmetic."""
+    cams = scene.cameras if cameras is None else cameras
+    rng = np.random.default_rng(seed)
+    out = []
+    for cam in cams:
+        W, H = cam.width, cam.height
+        m = np.zeros((H, W), np.uint8)
+        yy, xx = np.mgrid[0:H, 0:W]
+        R = np.asarray(cam.R, np.float64)
+        t = np.asarray(cam.t, np.float64)
+        dil = 0.02 * W
+        for r in scene.regions:
+            if r.kind == REGION_SPHERE:
+                pts, rad = [np.asarray(r.a, np.float64)], float(r.r)
+            else:
+                lo, hi = np.asarray(r.a, np.float64), np.asarray(r.b, np.float64)
+                pts = [np.array([a, b, c]) for a in (lo[0], hi[0]) for b in (lo[1], hi[1]) for c in (lo[2], hi[2])]
+                rad = 0.0
+            uv = []
+            for p in pts:
+                pc = R @ p + t
+                if pc[2] <= 0.05:
+                    continue
+                uv.append((cam.fx * pc[0] / pc[2] + cam.cx, cam.fy * pc[1] / pc[2] + cam.cy, cam.fx * rad / pc[2]))
+            if not uv:
+                continue
+            uv = np.array(uv)
+            if r.kind == REGION_SPHERE:
+                u, v, rr = uv[0]
+                m |= ((xx + 0.5 - u) ** 2 + (yy + 0.5 - v) ** 2 <= (rr + dil) ** 2).astype(np.uint8)
+            else:
+                u0, u1 = uv[:, 0].min() - dil, uv[:, 0].max() + dil
+                v0, v1 = uv[:, 1].min() - dil, uv[:, 1].max() + dil
+                m |= ((xx + 0.5 >= u0) & (xx + 0.5 <= u1) & (yy + 0.5 >= v0) & (yy + 0.5 <= v1)).astype(np.uint8)
+        flip = rng.random((H, W)) < noise
+        out.append(np.where(flip, 1 - m, m).astype(np.uint8))
+    return np.stack(out)
