@@ -273,6 +273,33 @@ cls_status cls_majority_vote(cls_ctx *ctx, const float *mean_op, int64_t n, cons
 cls_status cls_fit_spheres(cls_ctx *ctx, const float *mean_op, int64_t n, const int32_t *labels,
                            int32_t n_clusters, float *centres, float *radii, void *stream);
 
+/* ---------------------------------------------------------------------------------------
+ * NEXT-3/4: history record / recover (PAPER.md Supp. L651-L701) and the merge of
+ * batched updates (L642-L648).  Gaussian sets are cls_gaussians (device rows; n = row count or
+ * capacity as documented); each call synchronises `stream` once.
+ * ------------------------------------------------------------------------------------- */
+
+/* "we store O^t and I^t immediately after computing O^t, before any optimization" (L665): I
+ * (device uint8[g->n] out) = 1 for the rows of g whose centre lies in the regions (O^t, R21);
+ * those rows are copied in order into O (capacity O_capacity rows); *n_changed (host) = |O^t|. */
+cls_status cls_history_record(cls_ctx *ctx, const cls_gaussians *g, const cls_region *regions,
+                              int32_t n_regions, uint8_t *I, const cls_gaussians *O,
+                              int64_t O_capacity, int64_t *n_changed, void *stream);
+
+/* One RecoverState step (Alg. "History Recovery", L684-L701): G^{t-1} (out, >= n_prev rows) from
+ * G^t (cur: its first |not I| rows are the static rows of G^{t-1}, the partition invariant of
+ * L666), the stored O^t (O->n rows) and I^t (device uint8[n_prev]):
+ * out[j] = I[j] ? O[rank among ones] : cur[rank among zeros].  Repeat per stored step to walk back. */
+cls_status cls_history_recover(cls_ctx *ctx, const cls_gaussians *cur, const cls_gaussians *O,
+                               const uint8_t *I, int64_t n_prev, const cls_gaussians *out,
+                               void *stream);
+
+/* Batched updates (L645, reading R36): out = [prev rows with I1 = I2 = 0, in order][O1][O2];
+ * I1, I2 device uint8[prev->n]; out->n = capacity; *n_out (host) = rows written. */
+cls_status cls_merge_updates(cls_ctx *ctx, const cls_gaussians *prev, const uint8_t *I1,
+                             const uint8_t *I2, const cls_gaussians *O1, const cls_gaussians *O2,
+                             const cls_gaussians *out, int64_t *n_out, void *stream);
+
 const char *cls_status_string(cls_status s);
 const char *cls_last_error(const cls_ctx *ctx);
 /* Number of kernels launched by the library since cls_create (host counter). */

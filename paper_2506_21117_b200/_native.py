@@ -22,7 +22,8 @@ STATUS = {0: "CLS_OK", 1: "CLS_ERR_INVALID_ARGUMENT", 2: "CLS_ERR_DIMENSION_MISM
 EXPORTS = ("cls_create", "cls_destroy", "cls_render_fwd", "cls_active", "cls_copy_active", "cls_render_bwd", "cls_adam_masked",
            "cls_stats", "cls_profile_enable", "cls_profile_read", "cls_debug_grad2d", "cls_status_string",
            "cls_last_error", "cls_launch_count", "cls_partition_static", "cls_prune_outside", "cls_densify_stats",
-           "cls_densify", "cls_majority_vote", "cls_fit_spheres")
+           "cls_densify", "cls_majority_vote", "cls_fit_spheres", "cls_history_record", "cls_history_recover",
+           "cls_merge_updates")
 CLS_PROF_GROUPS = 16
 
 
@@ -108,11 +109,16 @@ def _load():
                               ctypes.c_float, ctypes.c_float, i64p, i64p, V]
     L.cls_majority_vote.argtypes = [V, V, ctypes.c_int64, P(cls_camera), ctypes.c_int32, V, V, V, V, V]
     L.cls_fit_spheres.argtypes = [V, V, ctypes.c_int64, V, ctypes.c_int32, V, V, V]
+    G = P(cls_gaussians)
+    L.cls_history_record.argtypes = [V, G, P(cls_region), ctypes.c_int32, V, G, ctypes.c_int64, i64p, V]
+    L.cls_history_recover.argtypes = [V, G, G, V, ctypes.c_int64, G, V]
+    L.cls_merge_updates.argtypes = [V, G, V, V, G, G, G, i64p, V]
     L.cls_launch_count.argtypes = [V]
     L.cls_launch_count.restype = ctypes.c_int64
     for name in ("cls_create", "cls_destroy", "cls_render_fwd", "cls_active", "cls_copy_active", "cls_render_bwd", "cls_adam_masked",
                  "cls_stats", "cls_debug_grad2d", "cls_profile_enable", "cls_profile_read", "cls_partition_static",
-                 "cls_prune_outside", "cls_densify_stats", "cls_densify", "cls_majority_vote", "cls_fit_spheres"):
+                 "cls_prune_outside", "cls_densify_stats", "cls_densify", "cls_majority_vote", "cls_fit_spheres",
+                 "cls_history_record", "cls_history_recover", "cls_merge_updates"):
         getattr(L, name).restype = ctypes.c_int
     return L
 

@@ -672,6 +672,111 @@ cls_status cls_densify_stats(cls_ctx *c, float *accum, int32_t *count, void *str
 }
 
 // ---------------------------------------------------------------------------
+// NEXT-3/4: history record / recover, batched-update merge
+// ---------------------------------------------------------------------------
+static RowArrays g_rows(const cls_gaussians *g)
+{
+    return rows_of((float4 *)g->mean_op, (float4 *)g->quat, (float4 *)g->log_scale, (float4 *)g->sh, nullptr, nullptr,
+                   nullptr, nullptr, g->sh_degree);
+}
+
+static bool g_valid(const cls_gaussians *g, bool allow_empty = false)
+{
+    return g && g->mean_op && g->quat && g->log_scale && g->sh && g->sh_degree >= 0 && g->sh_degree <= 3 &&
+           (allow_empty ? g->n >= 0 : g->n > 0) && g->n < (1ll << 31);
+}
+
+cls_status cls_history_record(cls_ctx *c, const cls_gaussians *g, const cls_region *regions, int32_t n_regions,
+                              uint8_t *I, const cls_gaussians *O, int64_t O_capacity, int64_t *n_changed,
+                              void *stream)
+{
+    if (!c) return CLS_ERR_INVALID_ARGUMENT;
+    if (!g_valid(g) || !I || !g_valid(O, true) || O->sh_degree != g->sh_degree || !n_changed)
+        return fail(c, CLS_ERR_INVALID_ARGUMENT, "cls_history_record: bad arguments");
+    RegSet regs;
+    if (!regset_of(c, regions, n_regions, regs)) return fail(c, CLS_ERR_INVALID_ARGUMENT, "bad regions");
+    cudaSetDevice(c->device);
+    const int n = (int)g->n;
+    if (!dens_reserve(c, 1, (size_t)n, g->sh_degree)) return fail(c, CLS_ERR_OUT_OF_MEMORY, "record scratch");
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned *flag = c->d_work, *excl = c->d_work + c->dens_n;
+    launch_flags_regions((const float4 *)g->mean_op, n, regs, flag, I, st);
+    cudaMemcpyAsync(c->d_int, &n, sizeof(int), cudaMemcpyHostToDevice, st);
+    scan_excl_u32(flag, excl, c->d_int, n, c->d_status, c->d_int + 1, c->d_tot, nullptr, st);
+    unsigned long long k = 0;
+    cudaMemcpyAsync(&k, c->d_tot, sizeof k, cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return check_cuda(c, "cls_history_record");
+    if ((long long)k > O_capacity) return fail(c, CLS_ERR_CAPACITY, "O^t has %llu rows > capacity", k);
+    launch_compact_rows(g_rows(g), g_rows(O), n, flag, excl, 0, st);
+    *n_changed = (int64_t)k;
+    return check_cuda(c, "cls_history_record");
+}
+
+cls_status cls_history_recover(cls_ctx *c, const cls_gaussians *cur, const cls_gaussians *O, const uint8_t *I,
+                               int64_t n_prev, const cls_gaussians *out, void *stream)
+{
+    if (!c) return CLS_ERR_INVALID_ARGUMENT;
+    if (!g_valid(cur) || !g_valid(O, true) || !g_valid(out, true) || !I || n_prev <= 0 || n_prev >= (1ll << 31) ||
+        O->sh_degree != cur->sh_degree || out->sh_degree != cur->sh_degree || out->n < n_prev)
+        return fail(c, CLS_ERR_INVALID_ARGUMENT, "cls_history_recover: bad arguments");
+    cudaSetDevice(c->device);
+    const int n = (int)n_prev;
+    if (!dens_reserve(c, 1, (size_t)n, cur->sh_degree)) return fail(c, CLS_ERR_OUT_OF_MEMORY, "recover scratch");
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned *flag = c->d_work, *excl = c->d_work + c->dens_n;
+    launch_flags_u8(I, nullptr, n, flag, 0, st);
+    cudaMemcpyAsync(c->d_int, &n, sizeof(int), cudaMemcpyHostToDevice, st);
+    scan_excl_u32(flag, excl, c->d_int, n, c->d_status, c->d_int + 1, c->d_tot, nullptr, st);
+    unsigned long long k = 0;
+    cudaMemcpyAsync(&k, c->d_tot, sizeof k, cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return check_cuda(c, "cls_history_recover");
+    if ((long long)k != O->n || n_prev - (long long)k > cur->n)
+        return fail(c, CLS_ERR_DIMENSION_MISMATCH, "I^t has %llu ones for %lld stored rows", k, (long long)O->n);
+    launch_recover_rows(g_rows(cur), g_rows(O), g_rows(out), n, flag, excl, st);
+    return check_cuda(c, "cls_history_recover");
+}
+
+cls_status cls_merge_updates(cls_ctx *c, const cls_gaussians *prev, const uint8_t *I1, const uint8_t *I2,
+                             const cls_gaussians *O1, const cls_gaussians *O2, const cls_gaussians *out,
+                             int64_t *n_out, void *stream)
+{
+    if (!c) return CLS_ERR_INVALID_ARGUMENT;
+    if (!g_valid(prev) || !I1 || !I2 || !g_valid(O1, true) || !g_valid(O2, true) || !g_valid(out, true) || !n_out ||
+        O1->sh_degree != prev->sh_degree || O2->sh_degree != prev->sh_degree || out->sh_degree != prev->sh_degree)
+        return fail(c, CLS_ERR_INVALID_ARGUMENT, "cls_merge_updates: bad arguments");
+    cudaSetDevice(c->device);
+    const int n = (int)prev->n;
+    if (!dens_reserve(c, 1, (size_t)n, prev->sh_degree)) return fail(c, CLS_ERR_OUT_OF_MEMORY, "merge scratch");
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned *flag = c->d_work, *excl = c->d_work + c->dens_n;
+    launch_flags_u8(I1, I2, n, flag, 1, st);
+    cudaMemcpyAsync(c->d_int, &n, sizeof(int), cudaMemcpyHostToDevice, st);
+    scan_excl_u32(flag, excl, c->d_int, n, c->d_status, c->d_int + 1, c->d_tot, nullptr, st);
+    unsigned long long k = 0;
+    cudaMemcpyAsync(&k, c->d_tot, sizeof k, cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return check_cuda(c, "cls_merge_updates");
+    const long long total = (long long)k + O1->n + O2->n;
+    if (total > out->n) return fail(c, CLS_ERR_CAPACITY, "merged scene of %lld rows > out capacity", total);
+    launch_compact_rows(g_rows(prev), g_rows(out), n, flag, excl, 0, st);
+    RowArrays o = g_rows(out);
+    const size_t K4 = (size_t)o.K4;
+    const size_t b1 = (size_t)k, b2 = (size_t)k + (size_t)O1->n;
+    const cls_gaussians *parts[2] = {O1, O2};
+    const size_t bases[2] = {b1, b2};
+    for (int q = 0; q < 2; q++) {
+        const cls_gaussians *P = parts[q];
+        if (P->n == 0) continue;
+        const size_t b = bases[q], m = (size_t)P->n;
+        cudaMemcpyAsync((float4 *)out->mean_op + b, P->mean_op, 16 * m, cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync((float4 *)out->quat + b, P->quat, 16 * m, cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync((float4 *)out->log_scale + b, P->log_scale, 16 * m, cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync((float4 *)out->sh + b * K4, P->sh, 16 * m * K4, cudaMemcpyDeviceToDevice, st);
+    }
+    *n_out = total;
+    return check_cuda(c, "cls_merge_updates");
+}
+
+// ---------------------------------------------------------------------------
 // NEXT-2: majority voting, sphere fitting
 // ---------------------------------------------------------------------------
 cls_status cls_majority_vote(cls_ctx *c, const float *mean_op, int64_t n, const cls_camera *cams, int32_t n_views,

@@ -227,6 +227,70 @@ void launch_suffix_apply(const RowArrays &a, long long n_static, int S, const Ro
     g_launches += 2;
 }
 
+// ---------------- history record / recover, batched-update merge (NEXT-3/4) ----------------
+__global__ void k_flags_regions(const float4 *__restrict__ mean_op, int n, const __grid_constant__ RegSet regs,
+                                unsigned *flag, uint8_t *I)
+{
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const bool in = in_regions(mean_op[i], regs);
+        flag[i] = in ? 1u : 0u;
+        if (I) I[i] = in ? 1 : 0;
+    }
+}
+
+__global__ void k_flags_u8(const uint8_t *__restrict__ a, const uint8_t *__restrict__ b, int n, unsigned *flag,
+                           int mode)
+{
+    // mode 0: flag = a != 0; mode 1: flag = (a == 0 && b == 0)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        flag[i] = mode == 0 ? (a[i] != 0) : (a[i] == 0 && b[i] == 0);
+}
+
+// dst[off + excl[i]] = src[i] for flagged rows (stable compaction)
+__global__ void k_compact_rows(RowArrays src, RowArrays dst, int n, const unsigned *__restrict__ flag,
+                               const unsigned *__restrict__ excl, long long off)
+{
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        if (flag[i]) copy_row(src, i, dst, off + excl[i], false);
+}
+
+// RecoverState step (Alg. "History Recovery"): out[j] = I[j] ? O[rank1(j)] : cur[rank0(j)]
+__global__ void k_recover_rows(RowArrays cur, RowArrays O, RowArrays out, int n, const unsigned *__restrict__ flag,
+                               const unsigned *__restrict__ excl)
+{
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const unsigned r1 = excl[j];
+        if (flag[j]) copy_row(O, r1, out, j, false);
+        else copy_row(cur, (long long)j - r1, out, j, false);
+    }
+}
+
+void launch_flags_regions(const float4 *mo, int n, const RegSet &regs, unsigned *flag, uint8_t *I, cudaStream_t st)
+{
+    k_flags_regions<<<std::max(1, std::min((n + 255) / 256, 148 * 8)), 256, 0, st>>>(mo, n, regs, flag, I);
+    g_launches++;
+}
+
+void launch_flags_u8(const uint8_t *a, const uint8_t *b, int n, unsigned *flag, int mode, cudaStream_t st)
+{
+    k_flags_u8<<<std::max(1, std::min((n + 255) / 256, 148 * 8)), 256, 0, st>>>(a, b, n, flag, mode);
+    g_launches++;
+}
+
+void launch_compact_rows(const RowArrays &src, const RowArrays &dst, int n, const unsigned *flag, const unsigned *excl,
+                         long long off, cudaStream_t st)
+{
+    k_compact_rows<<<std::max(1, std::min((n + 255) / 256, 148 * 8)), 256, 0, st>>>(src, dst, n, flag, excl, off);
+    g_launches++;
+}
+
+void launch_recover_rows(const RowArrays &cur, const RowArrays &O, const RowArrays &out, int n, const unsigned *flag,
+                         const unsigned *excl, cudaStream_t st)
+{
+    k_recover_rows<<<std::max(1, std::min((n + 255) / 256, 148 * 8)), 256, 0, st>>>(cur, O, out, n, flag, excl);
+    g_launches++;
+}
+
 void launch_reset_stats(float *acc, int *cnt, long long n, cudaStream_t st)
 {
     k_reset_stats<<<148 * 4, 256, 0, st>>>(acc, cnt, n);

@@ -76,6 +76,12 @@ void launch_suffix_plan(int mode, const RowArrays &a, long long n_static, int S,
 void launch_suffix_apply(const RowArrays &a, long long n_static, int S, const RowArrays &tmp, const unsigned *work,
                          const unsigned long long *tot, const float *normals, cudaStream_t st);
 void launch_reset_stats(float *acc, int *cnt, long long n, cudaStream_t st);
+void launch_flags_regions(const float4 *mo, int n, const RegSet &regs, unsigned *flag, uint8_t *I, cudaStream_t st);
+void launch_flags_u8(const uint8_t *a, const uint8_t *b, int n, unsigned *flag, int mode, cudaStream_t st);
+void launch_compact_rows(const RowArrays &src, const RowArrays &dst, int n, const unsigned *flag, const unsigned *excl,
+                         long long off, cudaStream_t st);
+void launch_recover_rows(const RowArrays &cur, const RowArrays &O, const RowArrays &out, int n, const unsigned *flag,
+                         const unsigned *excl, cudaStream_t st);
 
 // NEXT-2: majority voting and sphere fitting (k_voting.cu)
 void launch_vote(const float4 *mean_op, int n, const CamSet &cams, const uint8_t *masks, int *c_out, int *o_out,

@@ -108,6 +108,37 @@ class GaussianParams:
                 mo[:, 3].copy(), shf.copy())
 
 
+@dataclass
+class Rows:
+    """A set of Gaussian rows in the C-ABI layout (no moments): the stored history O^t, a
+    recovered past state, a merged scene.  mean_op/quat/log_scale [n, 4], sh [n, K4, 4] (device)."""
+    mean_op: torch.Tensor
+    quat: torch.Tensor
+    log_scale: torch.Tensor
+    sh: torch.Tensor
+    sh_degree: int
+
+    @property
+    def n(self) -> int:
+        return int(self.mean_op.shape[0])
+
+    @classmethod
+    def empty(cls, n: int, sh_degree: int, device) -> "Rows":
+        z = lambda *shape: torch.zeros(shape, dtype=torch.float32, device=device)
+        return cls(z(n, 4), z(n, 4), z(n, 4), z(n, k4(sh_degree), 4), sh_degree)
+
+    @classmethod
+    def of(cls, p) -> "Rows":
+        return cls(p.mean_op, p.quat, p.log_scale, p.sh, p.sh_degree)
+
+    def head(self, n: int) -> "Rows":
+        return Rows(self.mean_op[:n], self.quat[:n], self.log_scale[:n], self.sh[:n], self.sh_degree)
+
+    def struct(self) -> N.cls_gaussians:
+        return N.cls_gaussians(self.n, self.sh_degree, self.mean_op.data_ptr(), self.quat.data_ptr(),
+                               self.log_scale.data_ptr(), self.sh.data_ptr())
+
+
 def camera_structs(cameras) -> ctypes.Array:
     arr = (N.cls_camera * len(cameras))()
     for j, c in enumerate(cameras):
@@ -349,6 +380,36 @@ class LocalOptimizer:
                                   int(n_clusters), ctypes.c_void_p(centres.data_ptr()),
                                   ctypes.c_void_p(radii.data_ptr()), ctypes.c_void_p(_stream_ptr(stream))), self.ctx)
         return centres, radii
+
+    # -- NEXT-3/4: history record / recover, batched-update merge ------------------------------------
+    def history_record(self, stream=None):
+        """Store O^t and I^t before the optimisation.  Returns (I uint8 [n], O: Rows)."""
+        p = self.params
+        I = torch.empty(p.n, dtype=torch.uint8, device=p.device)
+        O = Rows.empty(p.n, p.sh_degree, p.device)
+        k = ctypes.c_int64()
+        check(lib.cls_history_record(self.ctx, ctypes.byref(p.struct()), self._reg, len(self.regions),
+                                     ctypes.c_void_p(I.data_ptr()), ctypes.byref(O.struct()), p.n, ctypes.byref(k),
+                                     ctypes.c_void_p(_stream_ptr(stream))), self.ctx)
+        return I, O.head(int(k.value))
+
+    def history_recover(self, cur: Rows, O: Rows, I: torch.Tensor, stream=None) -> Rows:
+        """One RecoverState step (Alg. "History Recovery"): G^{t-1} from G^t, O^t and I^t."""
+        out = Rows.empty(int(I.shape[0]), cur.sh_degree, cur.mean_op.device)
+        check(lib.cls_history_recover(self.ctx, ctypes.byref(cur.struct()), ctypes.byref(O.struct()),
+                                      ctypes.c_void_p(I.data_ptr()), int(I.shape[0]), ctypes.byref(out.struct()),
+                                      ctypes.c_void_p(_stream_ptr(stream))), self.ctx)
+        return out
+
+    def merge_updates(self, prev: Rows, I1: torch.Tensor, O1: Rows, I2: torch.Tensor, O2: Rows, stream=None) -> Rows:
+        """Batched updates (L645, reading R36): [unchanged rows of prev][O1][O2]."""
+        out = Rows.empty(prev.n + O1.n + O2.n, prev.sh_degree, prev.mean_op.device)
+        k = ctypes.c_int64()
+        check(lib.cls_merge_updates(self.ctx, ctypes.byref(prev.struct()), ctypes.c_void_p(I1.data_ptr()),
+                                    ctypes.c_void_p(I2.data_ptr()), ctypes.byref(O1.struct()), ctypes.byref(O2.struct()),
+                                    ctypes.byref(out.struct()), ctypes.byref(k), ctypes.c_void_p(_stream_ptr(stream))),
+              self.ctx)
+        return out.head(int(k.value))
 
     # -- one full local-optimisation step ----------------------------------------------------------
     def step(self, cameras, targets: torch.Tensor, n_views_total: Optional[int] = None,
