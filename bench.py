@@ -11,7 +11,9 @@ Gaussians, strong in the views: the total work per step is fixed)
 
 Prints ONE JSON line (rank 0).  `value` = steps/s of the whole job, timed with CUDA events
 on the launching stream over exactly K steps bracketed by barrier + synchronize, max over
-ranks.  The roofline of the dominant kernel uses the library's own CUDA-event timing of
+ranks.  At N = 1 the step (fwd + bwd + masked Adam) is captured once as a CUDA graph and
+replayed (`--eager` launches every kernel instead); the per-kernel breakdown then comes from
+K eager steps run right after.  The roofline of the dominant kernel uses the library's own CUDA-event timing of
 each kernel group over the same timed region.  `--impl reference` times the CPU oracle
 (oracle/, fp64) on a bounded sample of the same workload on the host cores.
 """
@@ -143,6 +145,12 @@ def run_ours(args):
         opt.adam(grad)
         return res.loss
 
+    gstep = None
+    if not args.eager and world == 1 and not args.all_tiles:
+        from paper_2506_21117_b200 import GraphStep
+        gstep = GraphStep(opt, cams, tg, n_views_total=V)   # fwd + bwd + masked Adam captured once
+        step_eager = step
+        step = lambda targets=None: gstep.replay()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -166,6 +174,15 @@ def run_ours(args):
     ms_total = e0.elapsed_time(e1)
     launches = opt.launch_count() - launches0
     prof = opt.profile_read()
+    if gstep is not None:
+        # graph replays carry no per-kernel events and no host launches: the kernel breakdown and the
+        # per-step kernel count come from K eager steps right after (same workload)
+        l0 = opt.launch_count()
+        for _ in range(args.steps):
+            step_eager()
+        torch.cuda.synchronize()
+        launches = opt.launch_count() - l0      # kernels per K steps (each replay runs the same set)
+        prof = opt.profile_read()
     opt.profile(False)
     stats = opt.stats()
     t = torch.tensor([ms_total], dtype=torch.float64, device=f"cuda:{local}")
@@ -182,13 +199,19 @@ def run_ours(args):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        w0 = time.perf_counter()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        # eager: the host-target gather runs on a side stream overlapped with projection/binning
+        # (measured faster end to end than the same step replayed as a CUDA graph)
+        step_host = (lambda: step_eager(tg_host)) if gstep is not None else (lambda: step(tg_host))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        w0 = time.perf_counter()
         f0.record(stream)
         for _ in range(args.steps):
             # this step's inputs: the views' target images stay in pinned host memory; the library
             # moves only the pixels of the active tiles to the device (k_gather_targets, overlapped)
-            loss = step(tg_host)
+            loss = step_host()
             loss_host.copy_(loss, non_blocking=True)         # the step's result
         f1.record(stream)
         torch.cuda.synchronize()
@@ -263,6 +286,8 @@ def run_ours(args):
             "mpix_per_s": {"rendered": round(sum(stats["n_active_tiles"]) * 256 * world * value / 1e6, 2),
                            "frame_equivalent": round(V * W * H * value / 1e6, 2)},
             "e2e": e2e, "gpu_launches": int(launches), "roofline": roof, "clocks": clocks,
+            "step_mode": ("CUDA graph replay (kernel breakdown from K eager steps; e2e eager)" if gstep is not None
+                          else "eager"),
             "kernels_ms_per_step": {k: round(v["ms"] / args.steps, 4) for k, v in per.items()},
             "kernel_rates": groups,
             "counts": {k: stats[k] for k in ("n_records", "n_pairs", "n_items", "max_list", "n_units",
@@ -386,6 +411,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-views", type=int, default=1)
+    ap.add_argument("--eager", action="store_true",
+                    help="launch every kernel per step instead of replaying the step as one CUDA graph (N = 1)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

@@ -191,6 +191,14 @@ cls_status cls_adam_masked(cls_ctx *ctx, float *mean_op, float *quat, float *log
                            float *m, float *v, const float *grad_active, const float *lr,
                            float beta1, float beta2, float eps, int32_t step, void *stream);
 
+/* cls_adam_masked with the step t read on the device from *step_device (>= 1) and incremented
+ * there afterwards: a CUDA graph of fwd + bwd + Adam captured once replays with the right bias
+ * correction every step (no host argument changes between replays). */
+cls_status cls_adam_masked_devstep(cls_ctx *ctx, float *mean_op, float *quat, float *log_scale, float *sh,
+                                   float *m, float *v, const float *grad_active, const float *lr,
+                                   float beta1, float beta2, float eps, int32_t *step_device,
+                                   void *stream);
+
 /* Counters of the last fwd (host struct out).  Synchronises the ctx's last stream.
  * Returns CLS_ERR_CAPACITY if a capacity overflowed during that fwd. */
 cls_status cls_stats(cls_ctx *ctx, cls_stats_t *out);

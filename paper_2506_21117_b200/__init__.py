@@ -10,7 +10,7 @@ Importing a name from this package loads libcls.so; if it is not built, that rai
 (there is no CPU fallback).  ``paper_2506_21117_b200.build`` compiles it.
 """
 _LAZY = {"GaussianParams": "step", "LocalOptimizer": "step", "default_limits": "step", "k4": "step",
-         "row4": "step", "Rows": "step"}
+         "row4": "step", "Rows": "step", "GraphStep": "step"}
 
 __all__ = list(_LAZY)
 

@@ -23,7 +23,7 @@ EXPORTS = ("cls_create", "cls_destroy", "cls_render_fwd", "cls_active", "cls_cop
            "cls_stats", "cls_profile_enable", "cls_profile_read", "cls_debug_grad2d", "cls_status_string",
            "cls_last_error", "cls_launch_count", "cls_partition_static", "cls_prune_outside", "cls_densify_stats",
            "cls_densify", "cls_majority_vote", "cls_fit_spheres", "cls_history_record", "cls_history_recover",
-           "cls_merge_updates")
+           "cls_merge_updates", "cls_adam_masked_devstep")
 CLS_PROF_GROUPS = 16
 
 
@@ -113,12 +113,14 @@ def _load():
     L.cls_history_record.argtypes = [V, G, P(cls_region), ctypes.c_int32, V, G, ctypes.c_int64, i64p, V]
     L.cls_history_recover.argtypes = [V, G, G, V, ctypes.c_int64, G, V]
     L.cls_merge_updates.argtypes = [V, G, V, V, G, G, G, i64p, V]
+    L.cls_adam_masked_devstep.argtypes = [V, V, V, V, V, V, V, V, P(ctypes.c_float), ctypes.c_float, ctypes.c_float,
+                                          ctypes.c_float, V, V]
     L.cls_launch_count.argtypes = [V]
     L.cls_launch_count.restype = ctypes.c_int64
     for name in ("cls_create", "cls_destroy", "cls_render_fwd", "cls_active", "cls_copy_active", "cls_render_bwd", "cls_adam_masked",
                  "cls_stats", "cls_debug_grad2d", "cls_profile_enable", "cls_profile_read", "cls_partition_static",
                  "cls_prune_outside", "cls_densify_stats", "cls_densify", "cls_majority_vote", "cls_fit_spheres",
-                 "cls_history_record", "cls_history_recover", "cls_merge_updates"):
+                 "cls_history_record", "cls_history_recover", "cls_merge_updates", "cls_adam_masked_devstep"):
         getattr(L, name).restype = ctypes.c_int
     return L
 

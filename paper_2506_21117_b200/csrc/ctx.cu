@@ -26,6 +26,7 @@ struct cls_ctx {
     cudaStream_t side = nullptr;                              // host-target gather stream
     cudaEvent_t ev_items = nullptr, ev_gather = nullptr;
     bool fwd_valid = false, has_targets = false, bwd_valid = false;
+    bool captured = false;   // the last fwd was recorded into a CUDA graph: its events are not usable
     StepDims dims{};
     CamSet cams{};
     float3 bg{};
@@ -310,10 +311,15 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     Scratch s = c->s;
     s.max_items = d.V * d.T;
 
+    {
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(st, &cap);
+        c->captured = cap != cudaStreamCaptureStatusNone;
+    }
     cudaMemsetAsync(s.cnt, 0, sizeof(Counters), st);
     run(c, P_MEMBER, st, [&] { launch_member(p, d, regs, s, st); });
     cudaMemcpyAsync(c->h_A, &s.cnt->A, sizeof(int), cudaMemcpyDeviceToHost, st);
-    cudaEventRecord(c->ev_member, st);
+    if (!c->captured) cudaEventRecord(c->ev_member, st);
     run(c, P_MASK, st, [&] {
         launch_active_mask(p, d, cs, s, st);
         launch_bin_items(d, s, st);
@@ -347,7 +353,7 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     if (targets && loss) run(c, P_LOSS, st, [&] { launch_loss(s, loss_scale, loss, st); });
     if (tile_mask) cudaMemcpyAsync(tile_mask, s.mask, (size_t)d.V * d.T, cudaMemcpyDeviceToDevice, st);
     cudaMemcpyAsync(c->h_cnt, s.cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st);
-    cudaEventRecord(c->ev_fwd, st);
+    if (!c->captured) cudaEventRecord(c->ev_fwd, st);
     cls_status e = check_cuda(c, "cls_render_fwd");
     if (e != CLS_OK) return e;
     c->s.rsorted = s.rsorted;
@@ -368,7 +374,7 @@ cls_status cls_active(cls_ctx *c, int64_t *A, const int32_t **idx)
 {
     if (!c || !A) return CLS_ERR_INVALID_ARGUMENT;
     if (!c->fwd_valid) return fail(c, CLS_ERR_STATE, "cls_active before cls_render_fwd");
-    if (cudaEventSynchronize(c->ev_member) != cudaSuccess)
+    if ((c->captured ? cudaDeviceSynchronize() : cudaEventSynchronize(c->ev_member)) != cudaSuccess)
         return fail(c, CLS_ERR_CUDA, "membership event: %s", cudaGetErrorString(cudaGetLastError()));
     *A = *c->h_A;
     if (idx) *idx = c->s.idx;
@@ -382,7 +388,8 @@ cls_status cls_copy_active(cls_ctx *c, int32_t *dst, void *stream)
 {
     if (!c || !dst) return CLS_ERR_INVALID_ARGUMENT;
     if (!c->fwd_valid) return fail(c, CLS_ERR_STATE, "cls_copy_active before cls_render_fwd");
-    if (cudaEventSynchronize(c->ev_member) != cudaSuccess) return fail(c, CLS_ERR_CUDA, "membership event");
+    if ((c->captured ? cudaDeviceSynchronize() : cudaEventSynchronize(c->ev_member)) != cudaSuccess)
+        return fail(c, CLS_ERR_CUDA, "membership event");
     const int A = *c->h_A;
     if (A > 0) cudaMemcpyAsync(dst, c->s.idx, sizeof(int) * (size_t)A, cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
     return check_cuda(c, "cls_copy_active");
@@ -414,36 +421,51 @@ cls_status cls_render_bwd(cls_ctx *c, const cls_gaussians *g, const float *dL_di
     return CLS_OK;
 }
 
-cls_status cls_adam_masked(cls_ctx *c, float *mean_op, float *quat, float *log_scale, float *sh, float *m, float *v,
-                           const float *grad_active, const float *lr, float beta1, float beta2, float eps,
-                           int32_t step, void *stream)
+static cls_status adam_impl(cls_ctx *c, float *mean_op, float *quat, float *log_scale, float *sh, float *m, float *v,
+                            const float *grad_active, const float *lr, float beta1, float beta2, float eps,
+                            int32_t step, int32_t *step_dev, void *stream)
 {
     if (!c) return CLS_ERR_INVALID_ARGUMENT;
     if (!c->fwd_valid) return fail(c, CLS_ERR_STATE, "cls_adam_masked without a preceding cls_render_fwd");
     if (!mean_op || !quat || !log_scale || !sh || !m || !v || !grad_active || !lr)
         return fail(c, CLS_ERR_INVALID_ARGUMENT, "null pointer argument");
-    if (step < 1 || !(beta1 >= 0.f && beta1 < 1.f) || !(beta2 >= 0.f && beta2 < 1.f) || !(eps >= 0.f))
+    if ((!step_dev && step < 1) || !(beta1 >= 0.f && beta1 < 1.f) || !(beta2 >= 0.f && beta2 < 1.f) || !(eps >= 0.f))
         return fail(c, CLS_ERR_INVALID_ARGUMENT, "bad Adam hyper-parameters (step=%d)", step);
     if (!aligned16(mean_op) || !aligned16(quat) || !aligned16(log_scale) || !aligned16(sh) || !aligned16(m) ||
         !aligned16(v) || !aligned16(grad_active))
         return fail(c, CLS_ERR_INVALID_ARGUMENT, "float4 arrays must be 16-byte aligned");
     cudaSetDevice(c->device);
     cudaStream_t st = (cudaStream_t)stream;
-    const float bc1 = (float)(1.0 - pow((double)beta1, (double)step));
-    const float bc2 = (float)(1.0 - pow((double)beta2, (double)step));
+    const float bc1 = step_dev ? 1.f : (float)(1.0 - pow((double)beta1, (double)step));
+    const float bc2 = step_dev ? 1.f : (float)(1.0 - pow((double)beta2, (double)step));
     run(c, P_ADAM, st, [&] {
         launch_adam(c->dims, c->s, (float4 *)mean_op, (float4 *)quat, (float4 *)log_scale, (float4 *)sh, (float4 *)m,
-                    (float4 *)v, (const float4 *)grad_active, lr, beta1, beta2, eps, bc1, bc2, st);
+                    (float4 *)v, (const float4 *)grad_active, lr, beta1, beta2, eps, bc1, bc2, step_dev, st);
     });
     c->last_stream = st;
     return check_cuda(c, "cls_adam_masked");
+}
+
+cls_status cls_adam_masked(cls_ctx *c, float *mean_op, float *quat, float *log_scale, float *sh, float *m, float *v,
+                           const float *grad_active, const float *lr, float beta1, float beta2, float eps,
+                           int32_t step, void *stream)
+{
+    return adam_impl(c, mean_op, quat, log_scale, sh, m, v, grad_active, lr, beta1, beta2, eps, step, nullptr, stream);
+}
+
+cls_status cls_adam_masked_devstep(cls_ctx *c, float *mean_op, float *quat, float *log_scale, float *sh, float *m,
+                                   float *v, const float *grad_active, const float *lr, float beta1, float beta2,
+                                   float eps, int32_t *step_device, void *stream)
+{
+    if (!step_device) return fail(c, CLS_ERR_INVALID_ARGUMENT, "null step_device");
+    return adam_impl(c, mean_op, quat, log_scale, sh, m, v, grad_active, lr, beta1, beta2, eps, 0, step_device, stream);
 }
 
 cls_status cls_stats(cls_ctx *c, cls_stats_t *out)
 {
     if (!c || !out) return CLS_ERR_INVALID_ARGUMENT;
     if (!c->fwd_valid) return fail(c, CLS_ERR_STATE, "cls_stats before cls_render_fwd");
-    if (cudaEventSynchronize(c->ev_fwd) != cudaSuccess)
+    if ((c->captured ? cudaDeviceSynchronize() : cudaEventSynchronize(c->ev_fwd)) != cudaSuccess)
         return fail(c, CLS_ERR_CUDA, "fwd event: %s", cudaGetErrorString(cudaGetLastError()));
     if (c->last_stream) cudaStreamSynchronize(c->last_stream);
     // refresh the overflow bit (bwd may have set bit 2)
@@ -510,7 +532,8 @@ cls_status cls_debug_grad2d(cls_ctx *c, float *out, void *stream)
 {
     if (!c || !out) return CLS_ERR_INVALID_ARGUMENT;
     if (!c->bwd_valid) return fail(c, CLS_ERR_STATE, "cls_debug_grad2d before cls_render_bwd");
-    cudaEventSynchronize(c->ev_member);
+    if (c->captured) cudaDeviceSynchronize();
+    else cudaEventSynchronize(c->ev_member);
     const size_t bytes = sizeof(float4) * 3 * (size_t)c->dims.V * (size_t)(*c->h_A);
     cudaMemcpyAsync(out, c->s.grad2d, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
     return check_cuda(c, "cls_debug_grad2d");

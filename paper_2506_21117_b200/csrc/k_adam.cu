@@ -17,21 +17,29 @@ struct AdamArgs {
     const float4 *g;
     float lr[6];
     float b1, b2, eps, bc1, bc2;
+    const int *step_dev;   // if set: the step t is read on the device (CUDA-graph replays), bc from it
     int n, K4, ROW4, n_sh_floats;
 };
 
-__device__ __forceinline__ void adam_lane(float &p, float &m, float &v, float g, float lr, const AdamArgs &a)
+__device__ __forceinline__ void adam_lane(float &p, float &m, float &v, float g, float lr, const AdamArgs &a,
+                                          float bc1, float bc2)
 {
     m = a.b1 * m + (1.0f - a.b1) * g;
     v = a.b2 * v + (1.0f - a.b2) * g * g;
-    const float mh = m / a.bc1;
-    const float vh = v / a.bc2;
+    const float mh = m / bc1;
+    const float vh = v / bc2;
     p = p - lr * mh / (sqrtf(vh) + a.eps);
 }
 
 __global__ void __launch_bounds__(256) k_adam(const __grid_constant__ AdamArgs a, Scratch s)
 {
     const int A = s.cnt->A;
+    float bc1 = a.bc1, bc2 = a.bc2;
+    if (a.step_dev) {   // same double-precision bias correction as the host path
+        const int t = *a.step_dev;
+        bc1 = (float)(1.0 - pow((double)a.b1, (double)t));
+        bc2 = (float)(1.0 - pow((double)a.b2, (double)t));
+    }
     const long long total = (long long)A * a.ROW4;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x) {
@@ -62,21 +70,24 @@ __global__ void __launch_bounds__(256) k_adam(const __grid_constant__ AdamArgs a
         float4 m = a.m[(size_t)i * a.ROW4 + c];
         float4 v = a.v[(size_t)i * a.ROW4 + c];
         const float4 g = a.g[(size_t)k * a.ROW4 + c];
-        if (lr4[0] >= 0.f) adam_lane(p.x, m.x, v.x, g.x, lr4[0], a);
-        if (lr4[1] >= 0.f) adam_lane(p.y, m.y, v.y, g.y, lr4[1], a);
-        if (lr4[2] >= 0.f) adam_lane(p.z, m.z, v.z, g.z, lr4[2], a);
-        if (lr4[3] >= 0.f) adam_lane(p.w, m.w, v.w, g.w, lr4[3], a);
+        if (lr4[0] >= 0.f) adam_lane(p.x, m.x, v.x, g.x, lr4[0], a, bc1, bc2);
+        if (lr4[1] >= 0.f) adam_lane(p.y, m.y, v.y, g.y, lr4[1], a, bc1, bc2);
+        if (lr4[2] >= 0.f) adam_lane(p.z, m.z, v.z, g.z, lr4[2], a, bc1, bc2);
+        if (lr4[3] >= 0.f) adam_lane(p.w, m.w, v.w, g.w, lr4[3], a, bc1, bc2);
         *pp = p;
         a.m[(size_t)i * a.ROW4 + c] = m;
         a.v[(size_t)i * a.ROW4 + c] = v;
     }
 }
 
+__global__ void k_step_inc(int *step_dev) { *step_dev += 1; }
+
 void launch_adam(const StepDims &d, const Scratch &s, float4 *mean_op, float4 *quat, float4 *log_scale, float4 *sh,
                  float4 *m, float4 *v, const float4 *grad_active, const float lr[6], float b1, float b2, float eps,
-                 float bc1, float bc2, cudaStream_t st)
+                 float bc1, float bc2, int *step_dev, cudaStream_t st)
 {
     AdamArgs a;
+    a.step_dev = step_dev;
     a.mean_op = mean_op; a.quat = quat; a.log_scale = log_scale; a.sh = sh;
     a.m = m; a.v = v; a.g = grad_active;
     for (int q = 0; q < 6; q++) a.lr[q] = lr[q];
@@ -86,6 +97,10 @@ void launch_adam(const StepDims &d, const Scratch &s, float4 *mean_op, float4 *q
     const int blocks = (int)std::min<long long>((upper + 255) / 256, 148LL * 16);
     k_adam<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(a, s);
     g_launches++;
+    if (step_dev) {   // the next replay uses the next step
+        k_step_inc<<<1, 1, 0, st>>>(step_dev);
+        g_launches++;
+    }
 }
 
 }  // namespace cls

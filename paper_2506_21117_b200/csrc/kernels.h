@@ -54,7 +54,7 @@ void launch_bwd_project(const Params &g, const StepDims &d, const CamSet &cams, 
 // (6) masked Adam                                              (k_adam.cu)
 void launch_adam(const StepDims &d, const Scratch &s, float4 *mean_op, float4 *quat, float4 *log_scale, float4 *sh,
                  float4 *m, float4 *v, const float4 *grad_active, const float lr[6], float b1, float b2, float eps,
-                 float bc1, float bc2, cudaStream_t st);
+                 float bc1, float bc2, int *step_dev, cudaStream_t st);
 
 // NEXT-1: static-prefix partition, sphere pruning, densification restricted to O^t (k_densify.cu)
 struct RowArrays {   // one parameter set, Gaussian-major rows (cls.h layout); m/v/acc/cnt optional

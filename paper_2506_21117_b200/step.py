@@ -422,3 +422,59 @@ class LocalOptimizer:
             allreduce(grad, res.loss)
         self.adam(grad, stream=stream)
         return res.loss
+
+
+class GraphStep:
+    """One local-optimisation step (fwd + fused L1 + bwd + masked Adam) captured ONCE as a CUDA graph
+    and replayed every step: no per-step host work beyond the replay (the small configs are
+    launch-bound otherwise).  Everything the step needs on the host is fixed at capture: the views,
+    the static `targets` tensor (device, or pinned host memory from which each replay gathers the
+    active tiles' pixels; copy new data into it between replays if needed), a
+    capacity-sized gradient buffer (rows >= the active count; the kernels read |O^t| on the device)
+    and the Adam step, which lives on the device (cls_adam_masked_devstep).  Single GPU."""
+
+    def __init__(self, opt: "LocalOptimizer", cameras, targets: torch.Tensor, n_views_total: Optional[int] = None):
+        p = opt.params
+        self.opt = opt
+        self.cams = camera_structs(cameras)
+        self.nv = len(cameras)
+        self.nvt = int(n_views_total or self.nv)
+        self.targets = targets   # device tensor, or pinned host memory (only active tiles' pixels are read)
+        assert (targets.is_cuda or targets.is_pinned()) and targets.is_contiguous() and targets.dtype == torch.float32
+        dev = p.device
+        self.loss = torch.zeros(1, dtype=torch.float32, device=dev)
+        self.grad = torch.zeros((max(int(opt.limits.max_active), 1), row4(p.sh_degree), 4), dtype=torch.float32,
+                                device=dev)
+        self.step_dev = torch.tensor([p.step + 1], dtype=torch.int32, device=dev)
+        self.stream = torch.cuda.Stream(device=dev)
+        self.stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self.stream):
+            self._fwd_bwd()                      # warm-up (one-time kernel attribute set-up), no update
+        self.stream.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            self._fwd_bwd()
+            self._adam()
+
+    def _fwd_bwd(self):
+        o, p = self.opt, self.opt.params
+        st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        g = p.struct()
+        check(lib.cls_render_fwd(o.ctx, ctypes.byref(g), self.cams, self.nv, self.nvt, o._reg, len(o.regions), o.bg,
+                                 ctypes.c_void_p(self.targets.data_ptr()), None, None,
+                                 ctypes.c_void_p(self.loss.data_ptr()), 0, st), o.ctx)
+        check(lib.cls_render_bwd(o.ctx, ctypes.byref(g), None, ctypes.c_void_p(self.grad.data_ptr()), st), o.ctx)
+
+    def _adam(self):
+        o, p = self.opt, self.opt.params
+        st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        check(lib.cls_adam_masked_devstep(o.ctx, *(ctypes.c_void_p(t.data_ptr()) for t in
+                                                   (p.mean_op, p.quat, p.log_scale, p.sh, p.m, p.v, self.grad)),
+                                          o.lr, float(o.betas[0]), float(o.betas[1]), o.eps,
+                                          ctypes.c_void_p(self.step_dev.data_ptr()), st), o.ctx)
+
+    def replay(self) -> torch.Tensor:
+        """Run one step; returns the (device) loss tensor of this step."""
+        self.graph.replay()
+        self.opt.params.step += 1
+        return self.loss

@@ -262,3 +262,31 @@ def test_host_resident_targets_match_device_targets(torch_cuda):
     assert np.array_equal(out[0][1], out[1][1])
     g0, g1 = out[0][2].astype(np.float64), out[1][2].astype(np.float64)
     assert np.all(np.abs(g0 - g1) <= 1e-5 * np.abs(g0) + 1e-6 * np.abs(g0).max())
+
+
+def test_cuda_graph_step_matches_eager(torch_cuda):
+    """GraphStep (fwd + bwd + masked Adam captured once, replayed) follows the eager steps: same
+    losses and parameters after 4 steps (up to the order of the backward's float atomics)."""
+    torch = torch_cuda
+    from paper_2506_21117_b200 import GaussianParams, GraphStep, LocalOptimizer, default_limits
+    sc = SCENES["c1"]()
+    res = []
+    for graph in (False, True):
+        p = GaussianParams.from_scene(sc)
+        opt = LocalOptimizer(p, sc.regions, limits=default_limits(sc.n, 1, sc.width, sc.height))
+        tg = torch.from_numpy(np.ascontiguousarray(sc.targets)).cuda()
+        losses = []
+        if graph:
+            gs = GraphStep(opt, sc.cameras, tg)
+            for _ in range(4):
+                losses.append(gs.replay().item())
+        else:
+            for _ in range(4):
+                losses.append(opt.step(sc.cameras, tg).item())
+        torch.cuda.synchronize()
+        res.append((np.array(losses), p.mean_op.cpu().numpy().copy(), p.sh.cpu().numpy().copy(), p.step))
+        opt.close()
+    assert res[0][3] == res[1][3] == 4
+    assert np.allclose(res[0][0], res[1][0], rtol=1e-6)
+    assert np.allclose(res[0][1], res[1][1], rtol=1e-5, atol=1e-6)
+    assert np.allclose(res[0][2], res[1][2], rtol=1e-5, atol=1e-6)
