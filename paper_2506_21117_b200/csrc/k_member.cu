@@ -113,34 +113,40 @@ k_active_rects(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
 }
 
 // mask of each view from the rect-corner differences (2D prefix sum > 0: the tile lies in some
-// active rect), then its summed-area table; one block per view
+// active rect), then its summed-area table, tile bbox and row bitmasks; one block per view.  The
+// prefix sums run in shared memory (SMEM) when the (TY+1)(TX+1) table fits, else in global memory.
+template <bool SMEM>
 __global__ void __launch_bounds__(256) k_sat(const __grid_constant__ CamSet cams, Scratch s, int all_tiles)
 {
+    extern __shared__ int sm_sat[];
     const int v = blockIdx.x;
     const int TX = cams.TX, TY = cams.TY, P = TX + 1;
     uint8_t *mk = s.mask + (size_t)v * cams.T;
+    int *Sg = s.sat + (size_t)v * (TY + 1) * P;
+    int *S = SMEM ? sm_sat : Sg;
     if (!all_tiles) {
-        int *D = s.mdiff + (size_t)v * (TY + 1) * P;
+        const int *D = s.mdiff + (size_t)v * (TY + 1) * P;
+        for (int k = threadIdx.x; k < (TY + 1) * P; k += blockDim.x) S[k] = D[k];
+        __syncthreads();
         for (int y = threadIdx.x; y < TY; y += blockDim.x) {   // row prefix
             int acc = 0;
             for (int x = 0; x < TX; x++) {
-                acc += D[y * P + x];
-                D[y * P + x] = acc;
+                acc += S[y * P + x];
+                S[y * P + x] = acc;
             }
         }
         __syncthreads();
         for (int x = threadIdx.x; x < TX; x += blockDim.x) {   // column prefix -> mask
             int acc = 0;
             for (int y = 0; y < TY; y++) {
-                acc += D[y * P + x];
+                acc += S[y * P + x];
                 mk[y * TX + x] = acc > 0 ? 1 : 0;
             }
         }
         __syncthreads();
     }
-    int *S = s.sat + (size_t)v * (TY + 1) * P;
+    // summed-area table of the mask: S[(y+1) P + x + 1] = active tiles in [0, x] x [0, y]
     for (int x = threadIdx.x; x < P; x += blockDim.x) S[x] = 0;
-    // row prefix sums
     for (int y = threadIdx.x; y < TY; y += blockDim.x) {
         int acc = 0;
         S[(y + 1) * P] = 0;
@@ -150,7 +156,6 @@ __global__ void __launch_bounds__(256) k_sat(const __grid_constant__ CamSet cams
         }
     }
     __syncthreads();
-    // column prefix sums
     for (int x = threadIdx.x; x < P; x += blockDim.x) {
         int acc = 0;
         for (int y = 1; y <= TY; y++) {
@@ -159,6 +164,8 @@ __global__ void __launch_bounds__(256) k_sat(const __grid_constant__ CamSet cams
         }
     }
     __syncthreads();
+    if (SMEM)
+        for (int k = threadIdx.x; k < (TY + 1) * P; k += blockDim.x) Sg[k] = S[k];
     if (threadIdx.x == 0) s.cnt->active_tiles[v] = S[TY * P + TX];
     // tile bbox of the active tiles (x0, y0, x1, y1 exclusive; empty: x1 <= x0)
     __shared__ int s_bb[4];
@@ -200,7 +207,9 @@ void launch_active_mask(const Params &g, const StepDims &d, const CamSet &cams, 
         k_active_rects<<<blocks, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, cams, s);
         g_launches++;
     }
-    k_sat<<<d.V, 256, 0, st>>>(cams, s, d.all_tiles);
+    const size_t smem = sizeof(int) * (size_t)(d.TY + 1) * (d.TX + 1);
+    if (smem <= 48 * 1024) k_sat<true><<<d.V, 256, smem, st>>>(cams, s, d.all_tiles);
+    else k_sat<false><<<d.V, 256, 0, st>>>(cams, s, d.all_tiles);
     g_launches++;
 }
 
