@@ -56,19 +56,22 @@ __device__ __forceinline__ void stage(const Scratch &s, unsigned val, int tx, in
 #define RT_SCAN 8    // units tested per thread per round (512 per round): few rounds, one latency each
 
 template <int DIR, bool BWD>
-__device__ __forceinline__ int fill_batch(const Scratch &s, int &cur, int end, int tx, int ty, float4 *sa, float4 *sb,
-                                          float4 *sc, float2 *sd, int *s_pos, int *s_wc, int *s_next, int *s_first)
+__device__ __forceinline__ int fill_batch(const Scratch &s, int &cur, int end, int tx, int ty, float4 *ent, float2 *sd,
+                                          int *s_pos, int *s_wc, int *s_next, int *s_first, int *s_clamp)
 {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (!BWD && tid == 0) *s_clamp = 0;
     const unsigned lt = (1u << lane) - 1u;
     const unsigned *cols = reinterpret_cast<const unsigned *>(s.sukey);   // low word: lo | hi << 16
     int nst = 0;
     while (nst < RT_BATCH && (DIR > 0 ? cur < end : cur > end)) {
-        unsigned cw[RT_SCAN];
+        unsigned cw[RT_SCAN], uv[RT_SCAN];
 #pragma unroll
-        for (int k = 0; k < RT_SCAN; k++) {   // all loads first: one memory latency per round
+        for (int k = 0; k < RT_SCAN; k++) {   // all loads first (columns AND record ids): one memory latency per round
             const int u = DIR > 0 ? cur + k * RT_THREADS + tid : cur - 1 - (k * RT_THREADS + tid);
-            cw[k] = (DIR > 0 ? u < end : u >= end) ? __ldg(cols + 2 * (size_t)u) : 0xffffu;   // empty if outside
+            const bool in = DIR > 0 ? u < end : u >= end;
+            cw[k] = in ? __ldg(cols + 2 * (size_t)u) : 0xffffu;   // empty if outside
+            uv[k] = in ? __ldg(s.suval + u) : 0u;
         }
         unsigned cov = 0u;
 #pragma unroll
@@ -90,8 +93,9 @@ __device__ __forceinline__ int fill_batch(const Scratch &s, int &cur, int end, i
                 const int u = DIR > 0 ? cur + k * RT_THREADS + tid : cur - 1 - (k * RT_THREADS + tid);
                 const int slot = nst + total + (warp ? c0 : 0) + __popc(cw[k] & lt);
                 if (slot < RT_BATCH) {
-                    const unsigned val = s.suval[u];
-                    stage(s, val, tx, ty, sa[slot], sb[slot], sc[slot]);
+                    const unsigned val = uv[k];
+                    stage(s, val, tx, ty, ent[3 * slot], ent[3 * slot + 1], ent[3 * slot + 2]);
+                    if (!BWD && ent[3 * slot + 1].z > 0.98999f) *s_clamp = 1;   // alpha's 0.99 clamp may bind
                     if (BWD) {
                         const float4 xy = s.srec[val & 0x7fffffffu].xy;
                         sd[slot] = make_float2(__double2float_rn(((double)xy.x - (double)(CLS_TILE * tx)) + (double)xy.y),
@@ -111,6 +115,10 @@ __device__ __forceinline__ int fill_batch(const Scratch &s, int &cur, int end, i
         nst = min(nst + total, RT_BATCH);
         __syncthreads();
     }
+    if (!BWD && (nst & 1)) {   // the forward composites entries in pairs: pad with a no-op entry (o = 0)
+        if (tid < 3) ent[3 * nst + tid] = make_float4(0.f, 0.f, 0.f, 0.f);
+        __syncthreads();
+    }
     return nst;
 }
 
@@ -121,6 +129,133 @@ __device__ __forceinline__ float alpha_of(float qk, float o, float &G)
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-qk));
     G = e;
     return fminf(0.99f, __fmul_rn(o, e));
+}
+
+__device__ __forceinline__ unsigned long long pack2(float a, float b)
+{
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void unpack2(unsigned long long r, float &a, float &b)
+{
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ float tmax4(unsigned long long p, unsigned long long q)
+{
+    float a, b, c, d;
+    unpack2(p, a, b);
+    unpack2(q, c, d);
+    return fmaxf(fmaxf(a, b), fmaxf(c, d));
+}
+
+// ---------------------------------------------------------------------------
+// Forward compositing of one staged entry into a PAIR of pixels (same column, rows fy.x, fy.y).
+// sm_100 has packed fp32x2 FMA/MUL (FFMA2/FMUL2, IEEE RN per lane: bit-identical to the scalar
+// ops) with a broadcast operand; the pipe that limits this loop is the ALU pipe (FSETP/FSEL/FMNMX
+// issue at half the FFMA rate, tools/microbench/alu.cu), so the per-pixel decisions are predicates:
+//   an = -(o 2^-q)  [max(an, -0.99) when o may exceed 0.99: CLAMP]     -- -alpha, exactly negated
+//   h  = an <= -1/255;  an = h ? an : 0                                 -- alpha >= 1/255, else 0
+//   tn = an T + T,  wn = an T                                           -- T (1 - alpha), -alpha T
+//   k  = tn >= 1e-4;  @k: Cn += wn c (negated colour sums), last = h ? pos : last
+//   T  = k ? tn : -|T|                                                  -- -|T| marks termination
+// A skipped entry leaves tn = T (>= 1e-4 while live, so T is unchanged and Cn gains +-0); a
+// terminated pixel keeps T < 0, so tn < 0, k is false and -|T| = T.  All values equal the scalar
+// form alpha = min(0.99, o e), Tn = fma(-alpha, T, T), w = alpha T, C = fma(w, c, C)
+// bit for bit (RN rounding is sign-symmetric).
+// ---------------------------------------------------------------------------
+#define CP_PRE                                                                                   \
+    "{\n\t"                                                                                      \
+    ".reg .b64 s, t, q, e, an, tn, wn, na, nb, sxx, txx, no2;\n\t"                              \
+    ".reg .f32 q0, q1, e0, e1, a0, a1, tn0, tn1, w0, w1, T0, T1;\n\t"                           \
+    ".reg .pred h0, h1, k0, k1;\n\t"                                                          \
+    "mov.b64 na, {%10, %10};\n\t"                                                               \
+    "mov.b64 nb, {%11, %11};\n\t"                                                               \
+    "mov.b64 sxx, {%12, %12};\n\t"                                                              \
+    "mov.b64 txx, {%13, %13};\n\t"                                                              \
+    "mov.b64 no2, {%14, %14};\n\t"                                                              \
+    "fma.rn.f32x2 s, na, %9, sxx;\n\t"                                                          \
+    "fma.rn.f32x2 t, nb, %9, txx;\n\t"                                                          \
+    "mul.rn.f32x2 t, t, t;\n\t"                                                                 \
+    "fma.rn.f32x2 q, s, s, t;\n\t"                                                              \
+    "mov.b64 {q0, q1}, q;\n\t"                                                                  \
+    "neg.f32 q0, q0;\n\t"                                                                       \
+    "neg.f32 q1, q1;\n\t"                                                                       \
+    "ex2.approx.ftz.f32 e0, q0;\n\t"                                                            \
+    "ex2.approx.ftz.f32 e1, q1;\n\t"                                                            \
+    "mov.b64 e, {e0, e1};\n\t"                                                                  \
+    "mul.rn.f32x2 an, no2, e;\n\t"                                                              \
+    "mov.b64 {a0, a1}, an;\n\t"
+#define CP_CLAMP                                                                                 \
+    "max.f32 a0, a0, 0fBF7D70A4;\n\t"                                                           \
+    "max.f32 a1, a1, 0fBF7D70A4;\n\t"                                                           \
+    "mov.b64 an, {a0, a1};\n\t"
+#define CP_SUF                                                                                   \
+    "setp.le.f32 h0, a0, 0fBB808081;\n\t"                                                       \
+    "setp.le.f32 h1, a1, 0fBB808081;\n\t"                                                       \
+    "selp.f32 a0, a0, 0f00000000, h0;\n\t"                                                      \
+    "selp.f32 a1, a1, 0f00000000, h1;\n\t"                                                      \
+    "mov.b64 an, {a0, a1};\n\t"                                                                 \
+    "fma.rn.f32x2 tn, an, %0, %0;\n\t"                                                          \
+    "mul.rn.f32x2 wn, an, %0;\n\t"                                                              \
+    "mov.b64 {tn0, tn1}, tn;\n\t"                                                               \
+    "mov.b64 {w0, w1}, wn;\n\t"                                                                 \
+    "mov.b64 {T0, T1}, %0;\n\t"                                                                 \
+    "setp.ge.f32 k0, tn0, 0f38D1B717;\n\t"                                                      \
+    "setp.ge.f32 k1, tn1, 0f38D1B717;\n\t"                                                      \
+    "@k0 fma.rn.f32 %1, w0, %15, %1;\n\t"                                                       \
+    "@k0 fma.rn.f32 %2, w0, %16, %2;\n\t"                                                       \
+    "@k0 fma.rn.f32 %3, w0, %17, %3;\n\t"                                                       \
+    "@k1 fma.rn.f32 %4, w1, %15, %4;\n\t"                                                       \
+    "@k1 fma.rn.f32 %5, w1, %16, %5;\n\t"                                                       \
+    "@k1 fma.rn.f32 %6, w1, %17, %6;\n\t"                                                       \
+    "@k0 selp.b32 %7, %18, %7, h0;\n\t"                                                         \
+    "@k1 selp.b32 %8, %18, %8, h1;\n\t"                                                         \
+    "abs.f32 T0, T0;\n\t"                                                                       \
+    "abs.f32 T1, T1;\n\t"                                                                       \
+    "neg.f32 T0, T0;\n\t"                                                                       \
+    "neg.f32 T1, T1;\n\t"                                                                       \
+    "selp.f32 T0, tn0, T0, k0;\n\t"                                                             \
+    "selp.f32 T1, tn1, T1, k1;\n\t"                                                             \
+    "mov.b64 %0, {T0, T1};\n\t"                                                                 \
+    "}"
+#define CP_OPS                                                                                            \
+    : "+l"(T), "+f"(Ca0), "+f"(Ca1), "+f"(Ca2), "+f"(Cb0), "+f"(Cb1), "+f"(Cb2), "+r"(la), "+r"(lb)         \
+    : "l"(fy), "f"(na2), "f"(nb2), "f"(sx), "f"(tx), "f"(no), "f"(c0), "f"(c1), "f"(c2), "r"(pos)
+template <bool CLAMP>
+__device__ __forceinline__ void comp_pair(unsigned long long fy, float na2, float nb2, float sx, float tx, float no,
+                                          float c0, float c1, float c2, int pos, unsigned long long &T, float &Ca0,
+                                          float &Ca1, float &Ca2, float &Cb0, float &Cb1, float &Cb2, int &la, int &lb)
+{
+    if (CLAMP) asm(CP_PRE CP_CLAMP CP_SUF CP_OPS);
+    else asm(CP_PRE CP_SUF CP_OPS);
+}
+#undef CP_PRE
+#undef CP_CLAMP
+#undef CP_SUF
+#undef CP_OPS
+
+// one staged batch into the thread's 4 pixels, entries in pairs (the batch is padded to even length)
+template <bool CLAMP>
+__device__ __forceinline__ void comp_batch(const float4 *ent, int cnt, int lbase, float flx, unsigned long long fy01,
+                                           unsigned long long fy23, unsigned long long &T01, unsigned long long &T23,
+                                           float (&C0)[RT_PX], float (&C1)[RT_PX], float (&C2)[RT_PX],
+                                           int (&last)[RT_PX])
+{
+    for (int k = 0; k < cnt; k += 2) {
+        // warp-level exit once all its pixels terminated (checked every 4 entries)
+        if ((k & 3) == 0 && !__any_sync(0xffffffffu, tmax4(T01, T23) > 0.f)) break;
+#pragma unroll
+        for (int j = 0; j < 2; j++) {
+            const float4 A = ent[3 * (k + j)], B = ent[3 * (k + j) + 1], Cc = ent[3 * (k + j) + 2];
+            const float sx = __fmaf_rn(-A.y, flx, A.x), txx = __fmaf_rn(-B.x, flx, A.w);
+            const int pos = lbase + k + j;
+            comp_pair<CLAMP>(fy01, -A.z, -B.y, sx, txx, -B.z, Cc.x, Cc.y, Cc.z, pos, T01, C0[0], C1[0], C2[0], C0[1],
+                             C1[1], C2[1], last[0], last[1]);
+            comp_pair<CLAMP>(fy23, -A.z, -B.y, sx, txx, -B.z, Cc.x, Cc.y, Cc.z, pos, T23, C0[2], C1[2], C2[2], C0[3],
+                             C1[3], C2[3], last[2], last[3]);
+        }
+    }
 }
 
 __device__ __forceinline__ float block_sum(float v, float *red)
@@ -149,16 +284,15 @@ __global__ void __launch_bounds__(RT_THREADS, 12)
 k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ targets, bool staged,
       float *__restrict__ images, float loss_scale, float3 bg)
 {
-    __shared__ float4 sa[RT_BATCH];
-    __shared__ float4 sb[RT_BATCH];
-    __shared__ float4 sc[RT_BATCH];
+    __shared__ float4 ent[3 * (RT_BATCH + 1)];   // staged entries (sa, sb, sc) + one pad
     __shared__ float red[RT_THREADS / 32];
-    __shared__ int s_item, s_pos[RT_BATCH], s_wc[2 * RT_SCAN], s_next, s_first, s_lastp[CLS_BLOCK_PIX];
+    __shared__ int s_item, s_pos[RT_BATCH], s_wc[2 * RT_SCAN], s_next, s_first, s_clamp, s_lastp[CLS_BLOCK_PIX];
     if (s.cnt->overflow) return;
     const int n_items = s.cnt->n_items;
     const int tid = threadIdx.x;
     const int lx = tid & 15, ly = tid >> 4;   // pixels (lx, ly + 4k)
     const float flx = (float)lx;
+    const unsigned long long fy01 = pack2((float)ly, (float)(ly + 4)), fy23 = pack2((float)(ly + 8), (float)(ly + 12));
     const int W = cams.W, H = cams.H, TX = cams.TX, T = cams.T;
     unsigned long long evals = 0;
     while (true) {
@@ -175,50 +309,30 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         const int se = s.seg_end[seg];
         if (tid == 0) s_first = 0x7fffffff;
         const int x = tx * CLS_TILE + lx;
-        float Tr[RT_PX], C0[RT_PX], C1[RT_PX], C2[RT_PX];
+        // T of pixel pairs (p0, p1), (p2, p3) packed for the fp32x2 ops; C* hold the NEGATED colour sums
+        unsigned long long T01, T23;
+        float C0[RT_PX], C1[RT_PX], C2[RT_PX];
         int last[RT_PX];   // last composited entry: list index (its segment position goes to s_lastp)
+        {
+            float Ti[RT_PX];
 #pragma unroll
-        for (int k = 0; k < RT_PX; k++) {
-            const bool in = x < W && ty * CLS_TILE + ly + 4 * k < H;
-            Tr[k] = in ? 1.f : -1.f;   // out-of-image pixels start terminated
-            C0[k] = C1[k] = C2[k] = 0.f;
-            last[k] = -1;
-            s_lastp[tid + k * RT_THREADS] = -1;
+            for (int k = 0; k < RT_PX; k++) {
+                const bool in = x < W && ty * CLS_TILE + ly + 4 * k < H;
+                Ti[k] = in ? 1.f : -1.f;   // out-of-image pixels start terminated
+                C0[k] = C1[k] = C2[k] = 0.f;
+                last[k] = -1;
+                s_lastp[tid + k * RT_THREADS] = -1;
+            }
+            T01 = pack2(Ti[0], Ti[1]);
+            T23 = pack2(Ti[2], Ti[3]);
         }
         int lbase = 0;   // list index of the batch's first entry
         while (true) {
-            const bool live = Tr[0] > 0.f || Tr[1] > 0.f || Tr[2] > 0.f || Tr[3] > 0.f;
+            const bool live = tmax4(T01, T23) > 0.f;
             if (__syncthreads_count(live) == 0 || cur >= se) break;
-            const int cnt = fill_batch<1, false>(s, cur, se, tx, ty, sa, sb, sc, nullptr, s_pos, s_wc, &s_next, &s_first);
-            for (int k = 0; k < cnt; k++) {
-                // warp-level exit once all its pixels terminated (checked every 4 entries)
-                if ((k & 3) == 0 &&
-                    !__any_sync(0xffffffffu, fmaxf(fmaxf(Tr[0], Tr[1]), fmaxf(Tr[2], Tr[3])) > 0.f))
-                    break;
-                const float4 A = sa[k], B = sb[k], Cc = sc[k];
-                const float sx = __fmaf_rn(-A.y, flx, A.x), txx = __fmaf_rn(-B.x, flx, A.w);
-                const int pos = lbase + k;
-#pragma unroll
-                for (int p = 0; p < RT_PX; p++) {
-                    // The exponential is cheaper than a branch around it; beyond qcut' the alpha test
-                    // rejects anyway (ex2 -> 0), so results equal the pre-tested form.  A skipped entry
-                    // (alpha < 1/255) gets alpha = 0, so Tn = T exactly; then Tn < 1e-4 happens exactly at
-                    // the terminating entry or on an already terminated pixel (T < 0).  Branch-free.
-                    float ss, tt, G;
-                    const float qk = raster_q(sx, txx, A.z, B.y, (float)(ly + 4 * p), ss, tt);
-                    float alpha = alpha_of(qk, B.z, G);
-                    const bool hit = alpha >= (1.0f / 255.0f);
-                    alpha = hit ? alpha : 0.f;
-                    const float Tn = __fmaf_rn(-alpha, Tr[p], Tr[p]);   // T (1 - alpha), one rounding
-                    const bool ok = Tn >= 1e-4f;
-                    const float w = ok ? alpha * Tr[p] : 0.f;
-                    C0[p] = __fmaf_rn(w, Cc.x, C0[p]);
-                    C1[p] = __fmaf_rn(w, Cc.y, C1[p]);
-                    C2[p] = __fmaf_rn(w, Cc.z, C2[p]);
-                    if (ok && hit) last[p] = pos;
-                    Tr[p] = ok ? Tn : -fabsf(Tr[p]);
-                }
-            }
+            const int cnt = fill_batch<1, false>(s, cur, se, tx, ty, ent, nullptr, s_pos, s_wc, &s_next, &s_first, &s_clamp);
+            if (s_clamp) comp_batch<true>(ent, cnt, lbase, flx, fy01, fy23, T01, T23, C0, C1, C2, last);
+            else comp_batch<false>(ent, cnt, lbase, flx, fy01, fy23, T01, T23, C0, C1, C2, last);
 #pragma unroll
             for (int p = 0; p < RT_PX; p++)   // segment position of a last entry of this batch
                 if (last[p] >= lbase) s_lastp[tid + p * RT_THREADS] = s_pos[last[p] - lbase];
@@ -230,11 +344,17 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
             atomicMax(&s.cnt->max_list, lbase);
         }
         float l1 = 0.f;
+        float Tr[RT_PX];
+        unpack2(T01, Tr[0], Tr[1]);
+        unpack2(T23, Tr[2], Tr[3]);
 #pragma unroll
         for (int p = 0; p < RT_PX; p++) {
             const int yy = ty * CLS_TILE + ly + 4 * p;
             const bool in = x < W && yy < H;
             const float Tf = fabsf(Tr[p]);
+            C0[p] = -C0[p];   // the loop kept the negated sums
+            C1[p] = -C1[p];
+            C2[p] = -C2[p];
             evals += (unsigned long long)(last[p] + 1);   // entries up to the last composited one
             const int pl = tid + p * RT_THREADS;          // pixel slot (ly + 4p) * 16 + lx
             const size_t px = (size_t)item * CLS_BLOCK_PIX + pl;
@@ -356,9 +476,7 @@ struct PixB {   // backward state of one pixel
 __global__ void __launch_bounds__(RT_THREADS)
 k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ dL_dimg, float3 bg)
 {
-    __shared__ float4 sa[RT_BATCH];
-    __shared__ float4 sb[RT_BATCH];
-    __shared__ float4 sc[RT_BATCH];
+    __shared__ float4 ent[3 * (RT_BATCH + 1)];
     __shared__ float2 sd[RT_BATCH];    // tile-local 2D mean (dx0, dy0) in fp32
     __shared__ int s_item, s_maxlast, s_pos[RT_BATCH], s_wc[2 * RT_SCAN], s_next;
     if (s.cnt->overflow) return;
@@ -416,10 +534,10 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         int cur = end;
         while (cur > first) {
             __syncthreads();
-            const int cnt = fill_batch<-1, true>(s, cur, first, tx, ty, sa, sb, sc, sd, s_pos, s_wc, &s_next, nullptr);
+            const int cnt = fill_batch<-1, true>(s, cur, first, tx, ty, ent, sd, s_pos, s_wc, &s_next, nullptr, nullptr);
             for (int k = 0; k < cnt; k++) {
                 const int jj = s_pos[k];
-                const float4 Aa = sa[k], Bb = sb[k], Cc = sc[k];
+                const float4 Aa = ent[3 * k], Bb = ent[3 * k + 1], Cc = ent[3 * k + 2];
                 const int ordk = __float_as_int(Cc.w);
                 const bool active = ordk >= 0;   // uniform over the CTA
                 const float sx = __fmaf_rn(-Aa.y, flx, Aa.x), txx = __fmaf_rn(-Bb.x, flx, Aa.w);
