@@ -57,10 +57,10 @@ __device__ __forceinline__ void stage(const Scratch &s, unsigned val, int tx, in
 
 template <int DIR, bool BWD>
 __device__ __forceinline__ int fill_batch(const Scratch &s, int &cur, int end, int tx, int ty, float4 *ent, float2 *sd,
-                                          int *s_pos, int *s_wc, int *s_next, int *s_first, int *s_clamp)
+                                          int *s_pos, unsigned *s_rid, int *s_wc, int *s_next, int *s_first,
+                                          int *s_clamp)
 {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (!BWD && tid == 0) *s_clamp = 0;
     const unsigned lt = (1u << lane) - 1u;
     const unsigned *cols = reinterpret_cast<const unsigned *>(s.sukey);   // low word: lo | hi << 16
     int nst = 0;
@@ -85,40 +85,54 @@ __device__ __forceinline__ int fill_batch(const Scratch &s, int &cur, int end, i
         }
         __syncthreads();
         int total = 0;
-        int pre_mine = 0;
 #pragma unroll
-        for (int k = 0; k < RT_SCAN; k++) {
+        for (int k = 0; k < RT_SCAN; k++) {   // rank: slots in segment order; staging comes after the batch is complete
             const int c0 = s_wc[2 * k], c1 = s_wc[2 * k + 1];
             if ((cov >> k) & 1u) {
                 const int u = DIR > 0 ? cur + k * RT_THREADS + tid : cur - 1 - (k * RT_THREADS + tid);
                 const int slot = nst + total + (warp ? c0 : 0) + __popc(cw[k] & lt);
                 if (slot < RT_BATCH) {
-                    const unsigned val = uv[k];
-                    stage(s, val, tx, ty, ent[3 * slot], ent[3 * slot + 1], ent[3 * slot + 2]);
-                    if (!BWD && ent[3 * slot + 1].z > 0.98999f) *s_clamp = 1;   // alpha's 0.99 clamp may bind
-                    if (BWD) {
-                        const float4 xy = s.srec[val & 0x7fffffffu].xy;
-                        sd[slot] = make_float2(__double2float_rn(((double)xy.x - (double)(CLS_TILE * tx)) + (double)xy.y),
-                                               __double2float_rn(((double)xy.z - (double)(CLS_TILE * ty)) + (double)xy.w));
-                    }
-                    if (!BWD && (val >> 31)) atomicMin(s_first, u);
                     s_pos[slot] = u;
+                    s_rid[slot] = uv[k];
                 } else if (slot == RT_BATCH) {
                     *s_next = DIR > 0 ? u : u + 1;   // resume exactly at the first unstaged covering unit
                 }
             }
             total += c0 + c1;
         }
-        (void)pre_mine;
         __syncthreads();
         cur = nst + total > RT_BATCH ? *s_next : (DIR > 0 ? cur + RT_SCAN * RT_THREADS : cur - RT_SCAN * RT_THREADS);
         nst = min(nst + total, RT_BATCH);
         __syncthreads();
     }
-    if (!BWD && (nst & 1)) {   // the forward composites entries in pairs: pad with a no-op entry (o = 0)
-        if (tid < 3) ent[3 * nst + tid] = make_float4(0.f, 0.f, 0.f, 0.f);
-        __syncthreads();
+    // stage the batch: RT_BATCH / RT_THREADS independent record loads per thread, issued together
+    bool cl = false;
+    int fmin = 0x7fffffff;
+#pragma unroll
+    for (int r = 0; r < RT_BATCH / RT_THREADS; r++) {
+        const int slot = tid + r * RT_THREADS;
+        if (slot < nst) {
+            const unsigned val = s_rid[slot];
+            stage(s, val, tx, ty, ent[3 * slot], ent[3 * slot + 1], ent[3 * slot + 2]);
+            if (!BWD) {
+                cl |= ent[3 * slot + 1].z > 0.98999f;   // alpha's 0.99 clamp may bind
+                if (val >> 31) fmin = min(fmin, s_pos[slot]);
+            } else {
+                const float4 xy = s.srec[val & 0x7fffffffu].xy;
+                sd[slot] = make_float2(__double2float_rn(((double)xy.x - (double)(CLS_TILE * tx)) + (double)xy.y),
+                                       __double2float_rn(((double)xy.z - (double)(CLS_TILE * ty)) + (double)xy.w));
+            }
+        }
     }
+    if (!BWD) {
+        if (tid == 0) *s_clamp = 0;
+        if ((nst & 1) && tid < 3) ent[3 * nst + tid] = make_float4(0.f, 0.f, 0.f, 0.f);   // pad to pairs (o = 0)
+        __syncthreads();
+        if (cl) *s_clamp = 1;
+        fmin = __reduce_min_sync(0xffffffffu, fmin);
+        if (lane == 0 && fmin != 0x7fffffff) atomicMin(s_first, fmin);
+    }
+    __syncthreads();
     return nst;
 }
 
@@ -287,6 +301,7 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
     __shared__ float4 ent[3 * (RT_BATCH + 1)];   // staged entries (sa, sb, sc) + one pad
     __shared__ float red[RT_THREADS / 32];
     __shared__ int s_item, s_pos[RT_BATCH], s_wc[2 * RT_SCAN], s_next, s_first, s_clamp, s_lastp[CLS_BLOCK_PIX];
+    __shared__ unsigned s_rid[RT_BATCH];
     if (s.cnt->overflow) return;
     const int n_items = s.cnt->n_items;
     const int tid = threadIdx.x;
@@ -330,7 +345,7 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         while (true) {
             const bool live = tmax4(T01, T23) > 0.f;
             if (__syncthreads_count(live) == 0 || cur >= se) break;
-            const int cnt = fill_batch<1, false>(s, cur, se, tx, ty, ent, nullptr, s_pos, s_wc, &s_next, &s_first, &s_clamp);
+            const int cnt = fill_batch<1, false>(s, cur, se, tx, ty, ent, nullptr, s_pos, s_rid, s_wc, &s_next, &s_first, &s_clamp);
             if (s_clamp) comp_batch<true>(ent, cnt, lbase, flx, fy01, fy23, T01, T23, C0, C1, C2, last);
             else comp_batch<false>(ent, cnt, lbase, flx, fy01, fy23, T01, T23, C0, C1, C2, last);
 #pragma unroll
@@ -479,6 +494,7 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
     __shared__ float4 ent[3 * (RT_BATCH + 1)];
     __shared__ float2 sd[RT_BATCH];    // tile-local 2D mean (dx0, dy0) in fp32
     __shared__ int s_item, s_maxlast, s_pos[RT_BATCH], s_wc[2 * RT_SCAN], s_next;
+    __shared__ unsigned s_rid[RT_BATCH];
     if (s.cnt->overflow) return;
     const int n_items = s.cnt->n_items;
     const int A = s.cnt->A;
@@ -534,7 +550,7 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         int cur = end;
         while (cur > first) {
             __syncthreads();
-            const int cnt = fill_batch<-1, true>(s, cur, first, tx, ty, ent, sd, s_pos, s_wc, &s_next, nullptr, nullptr);
+            const int cnt = fill_batch<-1, true>(s, cur, first, tx, ty, ent, sd, s_pos, s_rid, s_wc, &s_next, nullptr, nullptr);
             for (int k = 0; k < cnt; k++) {
                 const int jj = s_pos[k];
                 const float4 Aa = ent[3 * k], Bb = ent[3 * k + 1], Cc = ent[3 * k + 2];
