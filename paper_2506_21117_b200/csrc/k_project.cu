@@ -125,6 +125,21 @@ __device__ __forceinline__ float rcp_approx(float x)
     return r;
 }
 
+// append the warp's kept (Gaussian, view) pairs to the candidate list (one atomic per warp)
+__device__ __forceinline__ void push_cand(const Scratch &s, bool keep, int gi, int gv, int lane)
+{
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (!bal) return;
+    int wb = 0;
+    if (lane == 0) wb = atomicAdd(&s.cnt->n_cand, __popc(bal));
+    wb = __shfl_sync(0xffffffffu, wb, 0);
+    if (keep) {
+        const long long slot = (long long)wb + __popc(bal & ((1u << lane) - 1u));
+        if (slot < s.max_cand) s.cand[slot] = make_int2(gi, gv);
+        else atomicOr(&s.cnt->overflow, 1);
+    }
+}
+
 template <bool SMEM_ROWS>
 __global__ void __launch_bounds__(PC_THREADS)
 k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ quat,
@@ -133,7 +148,7 @@ k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
     extern __shared__ unsigned s_rows[];   // [V][TY][W32] active-tile row bitmasks (if they fit)
     __shared__ CamSoA C;
     __shared__ float gM[PC_WARPS][9][32];   // M = R(q^) diag(exp(l)) of the warp's 32 Gaussians
-    __shared__ float gP[PC_WARPS][4][32];   // (x, y, z, qcut)
+    __shared__ float gP[PC_WARPS][6][32];   // (x, y, z, qcut, s_max^2, sqrt(qcut))
     __shared__ unsigned short q[PC_WARPS][PC_Q];   // queued (lane | view << 5)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int W = cams.W, H = cams.H, TX = cams.TX, TY = cams.TY, V = cams.n;
@@ -151,59 +166,79 @@ k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
     if (SMEM_ROWS)
         for (int k = threadIdx.x; k < V * per_view; k += blockDim.x) s_rows[k] = s.rowmask[k];
     __syncthreads();
+    // stage-1 lane layout: VP lanes per Gaussian (one view each, the camera in registers), GPW = 32 / VP
+    // Gaussians per step; VP = the smallest power of two >= V, at most 32 (more views: chunks of 32)
+    int lvp = 0;
+    while ((1 << lvp) < V && lvp < 5) lvp++;
+    const int VP = 1 << lvp, GPW = 32 >> lvp;
     unsigned short *qw = q[wid];
     const int nwarps = gridDim.x * PC_WARPS;
     unsigned long long n_s1 = 0;
     for (int base = (blockIdx.x * PC_WARPS + wid) * 32; base < n; base += nwarps * 32) {
-        const int i = base + lane;
-        const bool valid = i < n;
-        float4 mo = make_float4(0, 0, 0, 0), qq = make_float4(1, 0, 0, 0), ls = make_float4(0, 0, 0, 0);
-        if (valid) {
-            mo = __ldg(mean_op + i);
-            qq = __ldg(quat + i);
-            ls = __ldg(log_scale + i);
+        {   // per-Gaussian terms, one Gaussian per lane
+            const int i = base + lane;
+            const bool valid = i < n;
+            float4 mo = make_float4(0, 0, 0, 0), qq = make_float4(1, 0, 0, 0), ls = make_float4(0, 0, 0, 0);
+            if (valid) {
+                mo = __ldg(mean_op + i);
+                qq = __ldg(quat + i);
+                ls = __ldg(log_scale + i);
+            }
+            // M = R(q^) diag(exp(l)) in fp32, view independent
+            const float qn = rsqrtf(qq.x * qq.x + qq.y * qq.y + qq.z * qq.z + qq.w * qq.w);
+            const float w = qq.x * qn, x = qq.y * qn, y = qq.z * qn, z = qq.w * qn;
+            const float s0 = __expf(ls.x), s1 = __expf(ls.y), s2 = __expf(ls.z);
+            const float smx = fmaxf(s0, fmaxf(s1, s2)) * 1.001f;
+            gM[wid][0][lane] = (1.f - 2.f * (y * y + z * z)) * s0;
+            gM[wid][1][lane] = 2.f * (x * y - w * z) * s1;
+            gM[wid][2][lane] = 2.f * (x * z + w * y) * s2;
+            gM[wid][3][lane] = 2.f * (x * y + w * z) * s0;
+            gM[wid][4][lane] = (1.f - 2.f * (x * x + z * z)) * s1;
+            gM[wid][5][lane] = 2.f * (y * z - w * x) * s2;
+            gM[wid][6][lane] = 2.f * (x * z - w * y) * s0;
+            gM[wid][7][lane] = 2.f * (y * z + w * x) * s1;
+            gM[wid][8][lane] = (1.f - 2.f * (x * x + y * y)) * s2;
+            // 2 ln(255 o) (+ margin): no pixel has alpha >= 1/255 beyond q > qcut
+            const float op = 1.0f / (1.0f + __expf(-mo.w));
+            const float qcut = valid ? 2.0f * __logf(255.0f * op) * 1.001f + 0.05f : -1.0f;
+            gP[wid][0][lane] = mo.x; gP[wid][1][lane] = mo.y; gP[wid][2][lane] = mo.z; gP[wid][3][lane] = qcut;
+            gP[wid][4][lane] = smx * smx;
+            // isotropic extent factor of the kept footprint: min(3 sqrt(lb) + 1, sqrt(qcut lb))
+            gP[wid][5][lane] = sqrtf(fmaxf(qcut, 0.f)) * 1.002f;
         }
-        // M = R(q^) diag(exp(l)) in fp32, view independent
-        const float qn = rsqrtf(qq.x * qq.x + qq.y * qq.y + qq.z * qq.z + qq.w * qq.w);
-        const float w = qq.x * qn, x = qq.y * qn, y = qq.z * qn, z = qq.w * qn;
-        const float s0 = __expf(ls.x), s1 = __expf(ls.y), s2 = __expf(ls.z);
-        const float smx = fmaxf(s0, fmaxf(s1, s2)) * 1.001f;
-        const float smax2 = smx * smx;
-        gM[wid][0][lane] = (1.f - 2.f * (y * y + z * z)) * s0;
-        gM[wid][1][lane] = 2.f * (x * y - w * z) * s1;
-        gM[wid][2][lane] = 2.f * (x * z + w * y) * s2;
-        gM[wid][3][lane] = 2.f * (x * y + w * z) * s0;
-        gM[wid][4][lane] = (1.f - 2.f * (x * x + z * z)) * s1;
-        gM[wid][5][lane] = 2.f * (y * z - w * x) * s2;
-        gM[wid][6][lane] = 2.f * (x * z - w * y) * s0;
-        gM[wid][7][lane] = 2.f * (y * z + w * x) * s1;
-        gM[wid][8][lane] = (1.f - 2.f * (x * x + y * y)) * s2;
-        // 2 ln(255 o) (+ margin): no pixel has alpha >= 1/255 beyond q > qcut
-        const float op = 1.0f / (1.0f + __expf(-mo.w));
-        const float qcut = valid ? 2.0f * __logf(255.0f * op) * 1.001f + 0.05f : -1.0f;
-        gP[wid][0][lane] = mo.x; gP[wid][1][lane] = mo.y; gP[wid][2][lane] = mo.z; gP[wid][3][lane] = qcut;
-        // isotropic extent factor of the kept footprint: min(3 sqrt(lb) + 1, sqrt(qcut lb))
-        const float kq = sqrtf(fmaxf(qcut, 0.f)) * 1.002f;
         __syncwarp();
         int head = 0, tail = 0;   // ring buffer [head, tail) of queued pairs, warp-uniform
-        for (int v = 0; v <= V; v++) {
-            if (v < V) {
-                // ---- stage 1 (uniform view v; camera reads are smem broadcasts) ----
+        for (int vc = 0; vc < V; vc += VP) {
+            const int v = vc + (lane & (VP - 1));
+            const bool vok = v < V;
+            const int vv_ = vok ? v : 0;
+            // this lane's camera, in registers for all the warp's Gaussians
+            const float R0 = C.R[0][vv_], R1 = C.R[1][vv_], R2 = C.R[2][vv_], R3 = C.R[3][vv_], R4 = C.R[4][vv_],
+                        R5 = C.R[5][vv_], R6 = C.R[6][vv_], R7 = C.R[7][vv_], R8 = C.R[8][vv_];
+            const float t0 = C.t[0][vv_], t1 = C.t[1][vv_], t2 = C.t[2][vv_];
+            const float cfx = C.fx[vv_], cfy = C.fy[vv_], ccx = C.cx[vv_], ccy = C.cy[vv_];
+            const float limx = C.limx[vv_], limy = C.limy[vv_];
+            const float fx2 = cfx * cfx, fy2 = cfy * cfy;
+            const unsigned *rv = rows + vv_ * per_view;
+            for (int gg = 0; gg < 32; gg += GPW) {
+                // ---- stage 1: (Gaussian g, view v) per lane ----
+                const int g = gg + (lane >> lvp);
+                const float mx = gP[wid][0][g], my = gP[wid][1][g], mz = gP[wid][2][g], qcut = gP[wid][3][g];
                 bool pass = false;
-                const float tz = C.R[6][v] * mo.x + C.R[7][v] * mo.y + C.R[8][v] * mo.z + C.t[2][v];
-                if (qcut >= 0.f && tz >= 0.199f) {   // exact culls t_z <= 0.2 (R5)
-                    const float tx = C.R[0][v] * mo.x + C.R[1][v] * mo.y + C.R[2][v] * mo.z + C.t[0][v];
-                    const float ty = C.R[3][v] * mo.x + C.R[4][v] * mo.y + C.R[5][v] * mo.z + C.t[1][v];
+                const float tz = R6 * mx + R7 * my + R8 * mz + t2;
+                if (vok && qcut >= 0.f && tz >= 0.199f) {   // exact culls t_z <= 0.2 (R5)
+                    const float smax2 = gP[wid][4][g], kq = gP[wid][5][g];
+                    const float tx = R0 * mx + R1 * my + R2 * mz + t0;
+                    const float ty = R3 * mx + R4 * my + R5 * mz + t1;
                     const float iz = rcp_approx(tz);   // tz >= 0.199; the margins absorb the approximation
                     const float xr = tx * iz, yr = ty * iz;
-                    const float u = C.fx[v] * xr + C.cx[v] - 0.5f, vv = C.fy[v] * yr + C.cy[v] - 0.5f;
-                    const float xz = fminf(fmaxf(xr, -C.limx[v]), C.limx[v]);
-                    const float yz = fminf(fmaxf(yr, -C.limy[v]), C.limy[v]);
-                    const float fx2 = C.fx[v] * C.fx[v], fy2 = C.fy[v] * C.fy[v];
+                    const float u = cfx * xr + ccx - 0.5f, vv = cfy * yr + ccy - 0.5f;
+                    const float xz = fminf(fmaxf(xr, -limx), limx);
+                    const float yz = fminf(fmaxf(yr, -limy), limy);
                     const float jf2 = (fx2 * (1.0f + xz * xz) + fy2 * (1.0f + yz * yz)) * iz * iz;
                     const float lb = jf2 * smax2 * 1.002f + 0.301f;
                     const float sl = lb * rsqrtf(lb) * 1.0001f;
-                    const float em = 0.5f + 1e-3f * fabsf(u - C.cx[v]) + 1e-3f * fabsf(vv - C.cy[v]);
+                    const float em = 0.5f + 1e-3f * fabsf(u - ccx) + 1e-3f * fabsf(vv - ccy);
                     const float R = fminf(3.0f * sl * 1.001f + 1.01f, kq * sl) + em + 0.01f;
                     // tiles holding a pixel within R of the centre (the exact rect n footprint lies inside)
                     const float inv = 1.0f / CLS_TILE;
@@ -220,7 +255,6 @@ k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
                             const unsigned m0 = 0xffffffffu << (tx0 & 31);
                             const unsigned m1 = 0xffffffffu >> (31 - ((tx1 - 1) & 31));
                             const unsigned mA = w0 == w1 ? (m0 & m1) : m0, mB = w0 == w1 ? 0u : m1;
-                            const unsigned *rv = rows + v * per_view;
                             unsigned acc = 0u;
 #pragma unroll
                             for (int r = 0; r < 3; r++) {
@@ -233,36 +267,34 @@ k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
                 }
                 const unsigned bal = __ballot_sync(0xffffffffu, pass);
                 n_s1 += __popc(bal);
-                if (pass) qw[(tail + __popc(bal & ((1u << lane) - 1u))) & (PC_Q - 1)] = (unsigned short)(lane | (v << 5));
+                if (pass) qw[(tail + __popc(bal & ((1u << lane) - 1u))) & (PC_Q - 1)] = (unsigned short)(g | (v << 5));
                 tail += __popc(bal);
                 __syncwarp();
-            }
-            // ---- stage 2: full chunks of 32 (and the rest after the last view) ----
-            while (tail - head >= 32 || (v == V && tail > head)) {
-                const int cnt = min(32, tail - head);
-                bool keep = false;
-                int gi = 0, gv = 0;
-                if (lane < cnt) {
+                // ---- stage 2: full chunks of 32 ----
+                while (tail - head >= 32) {
                     const unsigned e = qw[(head + lane) & (PC_Q - 1)];
-                    const int gl = e & 31;
-                    gv = e >> 5;
-                    gi = base + gl;
-                    keep = cand_exact32(gM[wid], gP[wid], gl, gv, C, s.sat, TX, TY);
-                }
-                head += cnt;
-                __syncwarp();
-                const unsigned bal = __ballot_sync(0xffffffffu, keep);
-                if (bal) {
-                    int wb = 0;
-                    if (lane == 0) wb = atomicAdd(&s.cnt->n_cand, __popc(bal));
-                    wb = __shfl_sync(0xffffffffu, wb, 0);
-                    if (keep) {
-                        const long long slot = (long long)wb + __popc(bal & ((1u << lane) - 1u));
-                        if (slot < s.max_cand) s.cand[slot] = make_int2(gi, gv);
-                        else atomicOr(&s.cnt->overflow, 1);
-                    }
+                    const int gl = e & 31, gv = e >> 5;
+                    const bool keep = cand_exact32(gM[wid], gP[wid], gl, gv, C, s.sat, TX, TY);
+                    head += 32;
+                    __syncwarp();
+                    push_cand(s, keep, base + gl, gv, lane);
                 }
             }
+        }
+        // ---- stage 2: the rest ----
+        while (tail > head) {
+            const int cnt = min(32, tail - head);
+            bool keep = false;
+            int gl = 0, gv = 0;
+            if (lane < cnt) {
+                const unsigned e = qw[(head + lane) & (PC_Q - 1)];
+                gl = e & 31;
+                gv = e >> 5;
+                keep = cand_exact32(gM[wid], gP[wid], gl, gv, C, s.sat, TX, TY);
+            }
+            head += cnt;
+            __syncwarp();
+            push_cand(s, keep, base + gl, gv, lane);
         }
         __syncwarp();
     }
