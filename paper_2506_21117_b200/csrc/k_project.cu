@@ -236,6 +236,7 @@ k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
             const float limx = C.limx[vv_], limy = C.limy[vv_];
             const float fx2 = cfx * cfx, fy2 = cfy * cfy;
             const unsigned *rv = rows + vv_ * per_view;
+            const int4 bb = s.view_bbox[vv_];   // tile bbox of the view's active tiles (empty: x1 <= x0)
             for (int gg = 0; gg < 32; gg += GPW) {
                 // ---- stage 1: (Gaussian g, view v) per lane ----
                 const int g = gg + (lane >> lvp);
@@ -258,9 +259,9 @@ k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
                     const float R = fminf(3.0f * sl * 1.001f + 1.01f, kq * sl) + em + 0.01f;
                     // tiles holding a pixel within R of the centre (the exact rect n footprint lies inside)
                     const float inv = 1.0f / CLS_TILE;
-                    const int tx0 = max((int)floorf((u - R) * inv), 0), tx1 = min((int)floorf((u + R) * inv) + 1, TX);
-                    const int ty0 = max((int)floorf((vv - R) * inv), 0), ty1 = min((int)floorf((vv + R) * inv) + 1, TY);
-                    // small rects (at most 3 rows, 2 bitmask words: the common case) test the row
+                    const int tx0 = max((int)floorf((u - R) * inv), bb.x), tx1 = min((int)floorf((u + R) * inv) + 1, bb.z);
+                    const int ty0 = max((int)floorf((vv - R) * inv), bb.y), ty1 = min((int)floorf((vv + R) * inv) + 1, bb.w);
+                    // (clipped to the active bbox, which lies inside the image) small rects (at most 3 rows, 2 bitmask words: the common case) test the row
                     // bitmasks here, branch-free; larger ones pass on to stage 2's O(1) summed-area
                     // table test, so no lane loops
                     if (tx0 < tx1 && ty0 < ty1) {
