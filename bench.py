@@ -134,6 +134,8 @@ def run_ours(args):
     params = GaussianParams.from_scene(sc, device=f"cuda:{local}")
     lim = limits_for(args.config, sc.n, len(cams), W, H, args.all_tiles)
     opt = LocalOptimizer(params, sc.regions, limits=lim)
+    if not args.no_spatial_order:
+        opt.spatial_order()   # scene layout, once at load (not part of a step): Morton-ordered rows
     tg_host = torch.from_numpy(np.ascontiguousarray(sc.targets[my_views])).pin_memory()
     tg = tg_host.to(f"cuda:{local}")
     stream = torch.cuda.current_stream()
@@ -281,7 +283,9 @@ def run_ours(args):
             "config": {"workload": args.config, "gaussians": sc.n, "views": V, "width": W, "height": H,
                        "sh_degree": sc.sh_degree, "active": int(stats["n_active"]),
                        "mode": "all-tiles (w/o kernel)" if args.all_tiles else "masked (local kernel)",
-                       "parallelism": f"views/dp{world}", "l2": "inputs larger than L2 (params+moments "
+                       "parallelism": f"views/dp{world}",
+                       "row_order": "generator order" if args.no_spatial_order else "Morton (cls_spatial_order at load)",
+                       "l2": "inputs larger than L2 (params+moments "
                        f"{sc.n * (12 + 3 * 4 * 4) * 4 * 3 / 1e9:.2f} GB)"},
             "mpix_per_s": {"rendered": round(sum(stats["n_active_tiles"]) * 256 * world * value / 1e6, 2),
                            "frame_equivalent": round(V * W * H * value / 1e6, 2)},
@@ -291,7 +295,7 @@ def run_ours(args):
             "kernels_ms_per_step": {k: round(v["ms"] / args.steps, 4) for k, v in per.items()},
             "kernel_rates": groups,
             "counts": {k: stats[k] for k in ("n_records", "n_pairs", "n_items", "max_list", "n_units",
-                                             "n_fwd_evals", "n_bwd_evals", "n_candidates", "n_kept_pairs", "n_stage1")},
+                                             "n_fwd_evals", "n_bwd_evals", "n_candidates", "n_kept_pairs", "n_stage1", "n_tested")},
         }
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(sc, args.cpu_views)
@@ -409,6 +413,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--all-tiles", action="store_true", help="full-frame step (P:347 'w/o Kernel')")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-spatial-order", action="store_true",
+                    help="keep the synthetic generator's row order (no cls_spatial_order at load)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-views", type=int, default=1)
     ap.add_argument("--eager", action="store_true",

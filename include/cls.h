@@ -111,6 +111,7 @@ typedef struct {
     int64_t n_candidates;      /* (Gaussian, view) pairs passing the fp32 projection pre-test */
     int64_t n_kept_pairs;      /* pairs kept after the exact alpha-footprint culling (<= n_pairs) */
     int64_t n_stage1;          /* (Gaussian, view) pairs passing the projection isotropic pre-test */
+    int64_t n_tested;          /* (Gaussian, view) pairs the pre-test examined (after the warp-level cull) */
 } cls_stats_t;
 
 #define CLS_PROF_GROUPS 16
@@ -229,6 +230,16 @@ cls_status cls_debug_grad2d(cls_ctx *ctx, float *out, void *stream);
 cls_status cls_partition_static(cls_ctx *ctx, const cls_gaussians *g, float *mean_op, float *quat,
                                 float *log_scale, float *sh, const cls_region *regions,
                                 int32_t n_regions, int64_t *n_static, void *stream);
+
+/* Scene layout (not a step of the method; run once when a scene is loaded, before
+ * cls_partition_static): permutes the n rows of `g` into Morton (Z-curve) order of their centres
+ * over the scene's bounding box (10 bits per axis, ties by the original row index), so that
+ * consecutive rows hold nearby Gaussians and the projection culls whole warps of them per view
+ * (DESIGN.md "Scene layout").  Outputs (device, caller-owned, must not alias the inputs) get the
+ * permuted rows.  A permutation changes no rendered value except the order of exactly equal
+ * depths (broken by row index, R12).  Synchronises `stream`; allocates and frees its scratch. */
+cls_status cls_spatial_order(cls_ctx *ctx, const cls_gaussians *g, float *mean_op, float *quat,
+                             float *log_scale, float *sh, void *stream);
 
 /* Sphere pruning (Supp. L509-L511, §3.3): rows [n_static, n) -- O^t after the partition --
  * whose centre lies outside the union of the regions are removed (stable compaction of the

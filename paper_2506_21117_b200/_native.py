@@ -23,7 +23,7 @@ EXPORTS = ("cls_create", "cls_destroy", "cls_render_fwd", "cls_active", "cls_cop
            "cls_stats", "cls_profile_enable", "cls_profile_read", "cls_debug_grad2d", "cls_status_string",
            "cls_last_error", "cls_launch_count", "cls_partition_static", "cls_prune_outside", "cls_densify_stats",
            "cls_densify", "cls_majority_vote", "cls_fit_spheres", "cls_history_record", "cls_history_recover",
-           "cls_merge_updates", "cls_adam_masked_devstep")
+           "cls_merge_updates", "cls_adam_masked_devstep", "cls_spatial_order")
 CLS_PROF_GROUPS = 16
 
 
@@ -59,14 +59,15 @@ class cls_stats_t(ctypes.Structure):
                 ("n_items", ctypes.c_int64), ("n_active_tiles", ctypes.c_int64 * CLS_MAX_VIEWS),
                 ("overflow", ctypes.c_int32), ("n_views", ctypes.c_int32), ("max_list", ctypes.c_int64),
                 ("n_units", ctypes.c_int64), ("n_fwd_evals", ctypes.c_int64), ("n_bwd_evals", ctypes.c_int64),
-                ("n_candidates", ctypes.c_int64), ("n_kept_pairs", ctypes.c_int64), ("n_stage1", ctypes.c_int64)]
+                ("n_candidates", ctypes.c_int64), ("n_kept_pairs", ctypes.c_int64), ("n_stage1", ctypes.c_int64),
+                ("n_tested", ctypes.c_int64)]
 
     def as_dict(self):
         return dict(n_active=self.n_active, n_records=self.n_records, n_pairs=self.n_pairs, n_items=self.n_items,
                     n_active_tiles=list(self.n_active_tiles[: self.n_views]), overflow=self.overflow,
                     max_list=self.max_list, n_units=self.n_units, n_fwd_evals=self.n_fwd_evals,
                     n_bwd_evals=self.n_bwd_evals, n_candidates=self.n_candidates,
-                    n_kept_pairs=self.n_kept_pairs, n_stage1=self.n_stage1)
+                    n_kept_pairs=self.n_kept_pairs, n_stage1=self.n_stage1, n_tested=self.n_tested)
 
 
 class cls_profile_t(ctypes.Structure):
@@ -102,6 +103,7 @@ def _load():
     L.cls_last_error.restype = ctypes.c_char_p
     i64p = P(ctypes.c_int64)
     L.cls_partition_static.argtypes = [V, P(cls_gaussians), V, V, V, V, P(cls_region), ctypes.c_int32, i64p, V]
+    L.cls_spatial_order.argtypes = [V, P(cls_gaussians), V, V, V, V, V]
     L.cls_prune_outside.argtypes = [V, V, V, V, V, V, V, V, V, ctypes.c_int32, ctypes.c_int64, i64p, P(cls_region),
                                     ctypes.c_int32, V]
     L.cls_densify_stats.argtypes = [V, V, V, V]
@@ -120,7 +122,8 @@ def _load():
     for name in ("cls_create", "cls_destroy", "cls_render_fwd", "cls_active", "cls_copy_active", "cls_render_bwd", "cls_adam_masked",
                  "cls_stats", "cls_debug_grad2d", "cls_profile_enable", "cls_profile_read", "cls_partition_static",
                  "cls_prune_outside", "cls_densify_stats", "cls_densify", "cls_majority_vote", "cls_fit_spheres",
-                 "cls_history_record", "cls_history_recover", "cls_merge_updates", "cls_adam_masked_devstep"):
+                 "cls_history_record", "cls_history_recover", "cls_merge_updates", "cls_adam_masked_devstep",
+                 "cls_spatial_order"):
         getattr(L, name).restype = ctypes.c_int
     return L
 

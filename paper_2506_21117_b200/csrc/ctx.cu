@@ -485,6 +485,7 @@ cls_status cls_stats(cls_ctx *c, cls_stats_t *out)
     out->n_candidates = h.n_cand;
     out->n_kept_pairs = (int64_t)h.n_pairs;
     out->n_stage1 = (int64_t)h.n_stage1;
+    out->n_tested = (int64_t)h.n_tested;
     out->n_fwd_evals = (int64_t)h.fwd_evals;
     unsigned long long bev = 0;
     cudaMemcpy(&bev, &c->s.cnt->bwd_evals, sizeof bev, cudaMemcpyDeviceToHost);
@@ -621,6 +622,45 @@ cls_status cls_partition_static(cls_ctx *c, const cls_gaussians *g, float *mean_
     if (cudaStreamSynchronize(st) != cudaSuccess) return check_cuda(c, "cls_partition_static");
     *n_static = (int64_t)ns;
     return check_cuda(c, "cls_partition_static");
+}
+
+cls_status cls_spatial_order(cls_ctx *c, const cls_gaussians *g, float *mean_op, float *quat, float *log_scale,
+                             float *sh, void *stream)
+{
+    if (!c) return CLS_ERR_INVALID_ARGUMENT;
+    if (!g || !mean_op || !quat || !log_scale || !sh || !g->mean_op || !g->quat || !g->log_scale || !g->sh ||
+        g->n <= 0 || g->n >= (1ll << 31) || g->sh_degree < 0 || g->sh_degree > 3)
+        return fail(c, CLS_ERR_INVALID_ARGUMENT, "cls_spatial_order: bad arguments");
+    if ((const float *)mean_op == g->mean_op || (const float *)quat == g->quat ||
+        (const float *)log_scale == g->log_scale || (const float *)sh == g->sh)
+        return fail(c, CLS_ERR_INVALID_ARGUMENT, "cls_spatial_order: outputs must not alias the inputs");
+    cudaSetDevice(c->device);
+    const int n = (int)g->n;
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned long long *keys = nullptr, *keys_alt = nullptr;
+    unsigned *vals = nullptr, *vals_alt = nullptr, *bb = nullptr, *counts = nullptr, *totals = nullptr;
+    int *n_dev = nullptr;
+    bool ok = cudaMalloc(&keys, sizeof(*keys) * n) == cudaSuccess && cudaMalloc(&keys_alt, sizeof(*keys) * n) == cudaSuccess &&
+              cudaMalloc(&vals, sizeof(*vals) * n) == cudaSuccess && cudaMalloc(&vals_alt, sizeof(*vals) * n) == cudaSuccess &&
+              cudaMalloc(&bb, sizeof(unsigned) * 6) == cudaSuccess &&
+              cudaMalloc(&counts, sizeof(unsigned) * 512 * RS_GRID) == cudaSuccess &&
+              cudaMalloc(&totals, sizeof(unsigned) * 512) == cudaSuccess && cudaMalloc(&n_dev, sizeof(int)) == cudaSuccess;
+    if (ok) {
+        const RowArrays src = rows_of((float4 *)g->mean_op, (float4 *)g->quat, (float4 *)g->log_scale, (float4 *)g->sh,
+                                      nullptr, nullptr, nullptr, nullptr, g->sh_degree);
+        const RowArrays dst = rows_of((float4 *)mean_op, (float4 *)quat, (float4 *)log_scale, (float4 *)sh, nullptr,
+                                      nullptr, nullptr, nullptr, g->sh_degree);
+        launch_spatial_order(src, dst, n, bb, keys, keys_alt, vals, vals_alt, n_dev, counts, totals, st);
+    }
+    const cudaError_t e = cudaStreamSynchronize(st);
+    cudaFree(keys); cudaFree(keys_alt); cudaFree(vals); cudaFree(vals_alt); cudaFree(bb); cudaFree(counts);
+    cudaFree(totals); cudaFree(n_dev);
+    if (!ok) {
+        cudaGetLastError();
+        return fail(c, CLS_ERR_OUT_OF_MEMORY, "cls_spatial_order: scratch");
+    }
+    if (e != cudaSuccess) return check_cuda(c, "cls_spatial_order");
+    return check_cuda(c, "cls_spatial_order");
 }
 
 static cls_status suffix_op(cls_ctx *c, int mode, float *mean_op, float *quat, float *log_scale, float *sh, float *m,

@@ -298,3 +298,97 @@ void launch_reset_stats(float *acc, int *cnt, long long n, cudaStream_t st)
 }
 
 }  // namespace cls
+
+namespace cls {
+
+// ---------------- spatial order (scene layout, once per loaded scene) ----------------
+// Rows are permuted into Morton (Z-curve) order of their centres over the scene's bounding box
+// (10 bits per axis, ties by the original index): consecutive rows -- one warp of projection --
+// then hold nearby Gaussians, so a warp-level bound on their footprints culls whole
+// (warp, view) pairs (k_project_cand).  A permutation of the rows changes no rendered value
+// except the order of exactly equal depths, which the depth key breaks by row index.
+__device__ __forceinline__ unsigned f2ord(float f)
+{
+    const unsigned u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(unsigned u) { return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u); }
+
+__global__ void k_bbox(const float4 *__restrict__ mo, int n, unsigned *bb)
+{
+    unsigned lo[3] = {0xffffffffu, 0xffffffffu, 0xffffffffu}, hi[3] = {0u, 0u, 0u};
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const float4 m = mo[i];
+        const unsigned k[3] = {f2ord(m.x), f2ord(m.y), f2ord(m.z)};
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+            lo[a] = min(lo[a], k[a]);
+            hi[a] = max(hi[a], k[a]);
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        lo[a] = __reduce_min_sync(0xffffffffu, lo[a]);
+        hi[a] = __reduce_max_sync(0xffffffffu, hi[a]);
+    }
+    if ((threadIdx.x & 31) == 0)
+        for (int a = 0; a < 3; a++) {
+            atomicMin(bb + a, lo[a]);
+            atomicMax(bb + 3 + a, hi[a]);
+        }
+}
+
+__device__ __forceinline__ unsigned spread10(unsigned x)   // 10 bits -> every third bit
+{
+    x &= 0x3ffu;
+    x = (x | (x << 16)) & 0x030000ffu;
+    x = (x | (x << 8)) & 0x0300f00fu;
+    x = (x | (x << 4)) & 0x030c30c3u;
+    x = (x | (x << 2)) & 0x09249249u;
+    return x;
+}
+
+__global__ void k_morton(const float4 *__restrict__ mo, int n, const unsigned *bb, unsigned long long *keys,
+                         unsigned *vals)
+{
+    float lo[3], sc[3];
+    for (int a = 0; a < 3; a++) {
+        lo[a] = ord2f(bb[a]);
+        const float ext = ord2f(bb[3 + a]) - lo[a];
+        sc[a] = ext > 0.f ? 1023.0f / ext : 0.f;
+    }
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const float4 m = mo[i];
+        const float p[3] = {m.x, m.y, m.z};
+        unsigned c[3];
+        for (int a = 0; a < 3; a++) {
+            const float t = (p[a] - lo[a]) * sc[a];
+            c[a] = t >= 0.f ? min((unsigned)t, 1023u) : 0u;   // NaN -> 0
+        }
+        keys[i] = (unsigned long long)(spread10(c[0]) | (spread10(c[1]) << 1) | (spread10(c[2]) << 2));
+        vals[i] = (unsigned)i;
+    }
+}
+
+__global__ void k_gather_rows(RowArrays src, RowArrays dst, int n, const unsigned *__restrict__ perm)
+{
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+        copy_row(src, perm[j], dst, j, false);
+}
+
+void launch_spatial_order(const RowArrays &src, const RowArrays &dst, int n, unsigned *bb, unsigned long long *keys,
+                          unsigned long long *keys_alt, unsigned *vals, unsigned *vals_alt, int *n_dev,
+                          unsigned *counts, unsigned *totals, cudaStream_t st)
+{
+    const int blocks = std::max(1, std::min((n + 255) / 256, 148 * 8));
+    cudaMemsetAsync(bb, 0xff, 3 * sizeof(unsigned), st);
+    cudaMemsetAsync(bb + 3, 0, 3 * sizeof(unsigned), st);
+    k_bbox<<<blocks, 256, 0, st>>>(src.mo, n, bb);
+    k_morton<<<blocks, 256, 0, st>>>(src.mo, n, bb, keys, vals);
+    cudaMemcpyAsync(n_dev, &n, sizeof(int), cudaMemcpyHostToDevice, st);
+    const int w = radix_sort_u64(keys, keys_alt, vals, vals_alt, n_dev, n, 0, 30, 8, counts, totals, nullptr, st);
+    k_gather_rows<<<blocks, 256, 0, st>>>(src, dst, n, w ? vals_alt : vals);
+    g_launches += 3;
+}
+
+}  // namespace cls

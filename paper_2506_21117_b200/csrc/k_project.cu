@@ -182,15 +182,12 @@ k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
     if (SMEM_ROWS)
         for (int k = threadIdx.x; k < V * per_view; k += blockDim.x) s_rows[k] = s.rowmask[k];
     __syncthreads();
-    // stage-1 lane layout: VP lanes per Gaussian (one view each, the camera in registers), GPW = 32 / VP
-    // Gaussians per step; VP = the smallest power of two >= V, at most 32 (more views: chunks of 32)
-    int lvp = 0;
-    while ((1 << lvp) < V && lvp < 5) lvp++;
-    const int VP = 1 << lvp, GPW = 32 >> lvp;
     unsigned short *qw = q[wid];
     const int nwarps = gridDim.x * PC_WARPS;
-    unsigned long long n_s1 = 0;
+    unsigned long long n_s1 = 0, n_tested = 0;
     for (int base = (blockIdx.x * PC_WARPS + wid) * 32; base < n; base += nwarps * 32) {
+        float wc[3], wrs, wsm2, wkq;
+        bool wb_any;
         {   // per-Gaussian terms, one Gaussian per lane
             const int i = base + lane;
             const bool valid = i < n;
@@ -221,13 +218,81 @@ k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
             gP[wid][4][lane] = smx * smx;
             // isotropic extent factor of the kept footprint: min(3 sqrt(lb) + 1, sqrt(qcut lb))
             gP[wid][5][lane] = sqrtf(fmaxf(qcut, 0.f)) * 1.002f;
+            // warp bound: a sphere (c, rs) holding the centres of the warp's kept Gaussians (qcut >= 0),
+            // their largest scale and opacity factor.  Rows in spatial order (cls_spatial_order) make it tight.
+            const bool kept = qcut >= 0.f;
+            wb_any = __any_sync(0xffffffffu, kept);
+            float lo3[3] = {mo.x, mo.y, mo.z}, hi3[3] = {mo.x, mo.y, mo.z};
+#pragma unroll
+            for (int a = 0; a < 3; a++) {
+                if (!kept) { lo3[a] = INFINITY; hi3[a] = -INFINITY; }
+                for (int o = 16; o > 0; o >>= 1) {
+                    lo3[a] = fminf(lo3[a], __shfl_xor_sync(0xffffffffu, lo3[a], o));
+                    hi3[a] = fmaxf(hi3[a], __shfl_xor_sync(0xffffffffu, hi3[a], o));
+                }
+                wc[a] = 0.5f * (lo3[a] + hi3[a]);
+            }
+            const float dx = mo.x - wc[0], dy = mo.y - wc[1], dz = mo.z - wc[2];
+            float r2 = kept ? dx * dx + dy * dy + dz * dz : 0.f, sm2 = kept ? smx * smx : 0.f,
+                  kqm = kept ? sqrtf(qcut) * 1.002f : 0.f;
+            for (int o = 16; o > 0; o >>= 1) {
+                r2 = fmaxf(r2, __shfl_xor_sync(0xffffffffu, r2, o));
+                sm2 = fmaxf(sm2, __shfl_xor_sync(0xffffffffu, sm2, o));
+                kqm = fmaxf(kqm, __shfl_xor_sync(0xffffffffu, kqm, o));
+            }
+            wrs = sqrtf(r2) * 1.0001f + 1e-6f;
+            wsm2 = sm2;
+            wkq = kqm;
         }
         __syncwarp();
+        if (!wb_any) continue;
         int head = 0, tail = 0;   // ring buffer [head, tail) of queued pairs, warp-uniform
-        for (int vc = 0; vc < V; vc += VP) {
-            const int v = vc + (lane & (VP - 1));
-            const bool vok = v < V;
-            const int vv_ = vok ? v : 0;
+        for (int vc = 0; vc < V; vc += 32) {
+            // ---- warp-level cull, lane = view vc + lane: can ANY of the warp's Gaussians reach an
+            // active tile of the view?  Conservative bound on the centres' projections (the box
+            // [c +- rs] in camera space, depth >= 0.199) widened by the largest stage-1 radius. ----
+            bool wpass = false;
+            {
+                const int v = vc + lane;
+                if (v < V) {
+                    const float zc = C.R[6][v] * wc[0] + C.R[7][v] * wc[1] + C.R[8][v] * wc[2] + C.t[2][v];
+                    const int4 bb = s.view_bbox[v];
+                    if (zc + wrs >= 0.199f && bb.z > bb.x && bb.w > bb.y) {
+                        const float xc = C.R[0][v] * wc[0] + C.R[1][v] * wc[1] + C.R[2][v] * wc[2] + C.t[0][v];
+                        const float yc = C.R[3][v] * wc[0] + C.R[4][v] * wc[1] + C.R[5][v] * wc[2] + C.t[1][v];
+                        const float izl = 1.0f / fmaxf(zc - wrs, 0.199f), izh = 1.0f / (zc + wrs);
+                        const float nx0 = fminf((xc - wrs) * izl, (xc - wrs) * izh), nx1 = fmaxf((xc + wrs) * izl, (xc + wrs) * izh);
+                        const float ny0 = fminf((yc - wrs) * izl, (yc - wrs) * izh), ny1 = fmaxf((yc + wrs) * izl, (yc + wrs) * izh);
+                        const float fx = C.fx[v], fy = C.fy[v], cx = C.cx[v], cy = C.cy[v];
+                        const float u0 = fx * nx0 + cx - 0.5f, u1 = fx * nx1 + cx - 0.5f;
+                        const float v0 = fy * ny0 + cy - 0.5f, v1 = fy * ny1 + cy - 0.5f;
+                        const float ax = fminf(fmaxf(fabsf(nx0), fabsf(nx1)), C.limx[v]);
+                        const float ay = fminf(fmaxf(fabsf(ny0), fabsf(ny1)), C.limy[v]);
+                        const float jf2 = (fx * fx * (1.0f + ax * ax) + fy * fy * (1.0f + ay * ay)) * izl * izl;
+                        const float sl = sqrtf(jf2 * wsm2 * 1.002f + 0.301f) * 1.0001f;
+                        const float em = 0.5f + 1e-3f * fmaxf(fabsf(u0 - cx), fabsf(u1 - cx)) +
+                                         1e-3f * fmaxf(fabsf(v0 - cy), fabsf(v1 - cy));
+                        const float R = (fminf(3.0f * sl * 1.001f + 1.01f, wkq * sl) + em + 0.01f) * 1.01f + 1.0f;
+                        const float inv = 1.0f / CLS_TILE;
+                        const float fx0 = fmaxf(floorf((u0 - R) * inv), (float)bb.x), fx1 = fminf(floorf((u1 + R) * inv) + 1.0f, (float)bb.z);
+                        const float fy0 = fmaxf(floorf((v0 - R) * inv), (float)bb.y), fy1 = fminf(floorf((v1 + R) * inv) + 1.0f, (float)bb.w);
+                        wpass = !(fx0 >= fx1 || fy0 >= fy1);   // NaN bounds keep the view
+                    }
+                }
+            }
+            const unsigned vmask = __ballot_sync(0xffffffffu, wpass);
+            if (!vmask) continue;
+            // stage-1 lane layout over the kept views: VP lanes per Gaussian (one view each, the camera
+            // in registers), GPW = 32 / VP Gaussians per step; VP = the smallest power of two >= #views
+            const int nvk = __popc(vmask);
+            n_tested += 32ull * (unsigned long long)nvk;   // counted on lane 0 only (below)
+            int lvp = 0;
+            while ((1 << lvp) < nvk) lvp++;
+            const int VP = 1 << lvp, GPW = 32 >> lvp;
+            const int slotv = lane & (VP - 1);
+            const bool vok = slotv < nvk;
+            const int v = vok ? vc + (int)__fns(vmask, 0, slotv + 1) : 0;
+            const int vv_ = v;
             // this lane's camera, in registers for all the warp's Gaussians
             const float R0 = C.R[0][vv_], R1 = C.R[1][vv_], R2 = C.R[2][vv_], R3 = C.R[3][vv_], R4 = C.R[4][vv_],
                         R5 = C.R[5][vv_], R6 = C.R[6][vv_], R7 = C.R[7][vv_], R8 = C.R[8][vv_];
@@ -317,6 +382,7 @@ k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
     }
     flush_cand(s, ob, ocnt, lane);
     if (lane == 0 && n_s1) atomicAdd(&s.cnt->n_stage1, n_s1);
+    if (lane == 0 && n_tested) atomicAdd(&s.cnt->n_tested, n_tested);
 }
 
 // ---- pass B: exact fp64 projection of the candidates, records for those touching active tiles ----

@@ -76,6 +76,9 @@ void launch_suffix_plan(int mode, const RowArrays &a, long long n_static, int S,
 void launch_suffix_apply(const RowArrays &a, long long n_static, int S, const RowArrays &tmp, const unsigned *work,
                          const unsigned long long *tot, const float *normals, cudaStream_t st);
 void launch_reset_stats(float *acc, int *cnt, long long n, cudaStream_t st);
+void launch_spatial_order(const RowArrays &src, const RowArrays &dst, int n, unsigned *bb, unsigned long long *keys,
+                          unsigned long long *keys_alt, unsigned *vals, unsigned *vals_alt, int *n_dev,
+                          unsigned *counts, unsigned *totals, cudaStream_t st);
 void launch_flags_regions(const float4 *mo, int n, const RegSet &regs, unsigned *flag, uint8_t *I, cudaStream_t st);
 void launch_flags_u8(const uint8_t *a, const uint8_t *b, int n, unsigned *flag, int mode, cudaStream_t st);
 void launch_compact_rows(const RowArrays &src, const RowArrays &dst, int n, const unsigned *flag, const unsigned *excl,

@@ -300,6 +300,18 @@ class LocalOptimizer:
         return int(lib.cls_launch_count(self.ctx))
 
     # -- NEXT-1: static-prefix partition, sphere pruning, densification on O^t ------------------------
+    def spatial_order(self, stream=None) -> None:
+        """Scene layout, once after loading (include/cls.h cls_spatial_order): rows in Morton order of
+        their centres, so projection warps hold nearby Gaussians; moments and statistics restart."""
+        p = self.params
+        mo, q, ls, sh = (torch.empty_like(t) for t in (p._mo, p._q, p._ls, p._sh))
+        check(lib.cls_spatial_order(self.ctx, ctypes.byref(p.struct()), ctypes.c_void_p(mo.data_ptr()),
+                                    ctypes.c_void_p(q.data_ptr()), ctypes.c_void_p(ls.data_ptr()),
+                                    ctypes.c_void_p(sh.data_ptr()), ctypes.c_void_p(_stream_ptr(stream))), self.ctx)
+        p._mo, p._q, p._ls, p._sh = mo, q, ls, sh
+        p._m.zero_(); p._v.zero_(); p._acc.zero_(); p._cnt.zero_()
+        p._set_n(p.n)
+
     def partition_static(self, stream=None) -> int:
         """Reorder the scene so that the Gaussians outside the regions come first (history
         invariant); moments and densification statistics restart at 0."""
