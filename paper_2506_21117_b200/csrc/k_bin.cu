@@ -217,10 +217,10 @@ void launch_gather_targets(const StepDims &d, const CamSet &cams, const Scratch 
 // 1. record depth sort + ties
 void launch_bin_recsort(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st)
 {
-    const int rbits = 32 + bits_for(d.V - 1);
+    const int rbits = 31 + bits_for(d.V - 1);
     const int R = (int)s.max_records;
-    const int w = radix_sort_u64(s.rkey, s.rkey_alt, s.rval, s.rval_alt, &s.cnt->n_records, R, 0, rbits, 8,
-                                 s.rs_counts, s.rs_totals, &s.cnt->overflow, st);
+    const int w = radix_sort_u64(s.rkey, s.rkey_alt, s.rval, s.rval_alt, &s.cnt->n_records, R, 0, rbits,
+                                 rbits <= 32 ? 8 : 9, s.rs_counts, s.rs_totals, &s.cnt->overflow, st);
     unsigned long long *rk = w ? s.rkey_alt : s.rkey;
     unsigned *rv = w ? s.rval_alt : s.rval;
     s.rsorted = rv;
