@@ -83,7 +83,7 @@ typedef struct {
 /* Capacities fixed at cls_create; scratch is sized from them once. */
 typedef struct {
     int64_t max_gaussians;     /* n of every call <= this */
-    int64_t max_records;       /* sum over views of (Gaussian, view) records overlapping active tiles */
+    int64_t max_records;       /* sum over views of (Gaussian, view) records overlapping active tiles, <= 2^27 */
     int64_t max_pairs;         /* sum over views of (Gaussian, active tile) pairs, < 2^31 */
     int64_t max_active;        /* |O^t| (sizes the per-view 2D gradient buffer) */
     int32_t max_views;         /* views per call, <= CLS_MAX_VIEWS */

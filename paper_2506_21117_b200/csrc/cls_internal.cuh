@@ -7,6 +7,8 @@
 #include "../../include/cls.h"
 
 #define CLS_TILE 16
+#define RK_IDX_BITS 27   // record id in the low bits of the record sort key (max_records <= 2^27)
+#define RK_IDX_MASK ((1ull << RK_IDX_BITS) - 1ull)
 #define CLS_BLOCK_PIX 256
 
 namespace cls {
@@ -90,9 +92,7 @@ struct Scratch {
     long long max_cand;
     // record depth sort: key (view << 32 | fp32 depth bits), value record id
     unsigned long long *rkey, *rkey_alt;
-    unsigned *rval, *rval_alt;
-    const unsigned *rsorted;        // record ids in (view, depth, Gaussian index) order (rval or rval_alt)
-    const unsigned long long *rskey;   // the sorted keys (view << 31 | depth bits - bits(0.125))
+    const unsigned long long *rskey;   // the sorted keys: view | depth bits - bits(0.125) | record id
     unsigned *rcnt, *roff;          // per sorted record: tile rows of its footprint rect, their exclusive offsets
     unsigned *urec;                 // per (record, tile row) unit: the sorted record
     // units sorted stably by their row segment (view, tile row): key = segment << 32 | lo | hi << 16
@@ -461,7 +461,7 @@ __device__ __forceinline__ bool foot_row(const FootRec &f, int ty, int &lo, int 
 __device__ __forceinline__ FootRec foot_load(const Scratch &s, unsigned i)
 {
     const Rec R = s.srec[i];
-    return foot_make(R, (int)(s.rskey[i] >> 31), i | (__float_as_int(R.aux.y) < 0 ? 0u : 0x80000000u));
+    return foot_make(R, (int)(s.rskey[i] >> (31 + RK_IDX_BITS)), i | (__float_as_int(R.aux.y) < 0 ? 0u : 0x80000000u));
 }
 
 // active tiles of row bitmask `rm` (W32 words) in columns [lo, hi] of word w

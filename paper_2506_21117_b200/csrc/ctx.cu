@@ -149,7 +149,7 @@ cls_status cls_destroy(cls_ctx *c)
     cudaSetDevice(c->device);
     void *ptrs[] = {c->s.idx, c->s.ord, c->s.st_member, c->s.mask, c->s.sat, c->s.mdiff, c->s.rowmask, c->s.view_bbox, c->s.rec,
                     c->s.srec, c->s.rec_gid, c->s.cand, c->s.rkey,
-                    c->s.rkey_alt, c->s.rval, c->s.rval_alt, c->s.rcnt, c->s.urec, c->s.ukey, c->s.ukey_alt, c->s.uval, c->s.uval_alt,
+                    c->s.rkey_alt, c->s.rcnt, c->s.urec, c->s.ukey, c->s.ukey_alt, c->s.uval, c->s.uval_alt,
                     c->s.roff, c->s.st_scan, c->s.seg_off, c->s.seg_end, c->s.st_tiles, c->s.items, c->s.item_of_tile,
                     c->s.first_active, c->s.vis, c->s.rs_counts, c->s.rs_totals, c->s.px_T, c->s.px_last, c->s.px_dl, c->s.tgt,
                     c->s.item_loss, c->s.grad2d, c->s.cnt};
@@ -178,7 +178,7 @@ cls_status cls_create(cls_ctx **out, int device, const cls_limits *lim)
     *out = nullptr;
     if (lim->max_gaussians <= 0 || lim->max_views <= 0 || lim->max_views > CLS_MAX_VIEWS || lim->max_width < 16 ||
         lim->max_height < 16 || lim->max_records <= 0 || lim->max_pairs <= 0 || lim->max_pairs >= (1ll << 31) ||
-        lim->max_active <= 0 || lim->max_gaussians >= (1ll << 31) || lim->max_records >= (1ll << 31) ||
+        lim->max_active <= 0 || lim->max_gaussians >= (1ll << 31) || lim->max_records > (1ll << RK_IDX_BITS) ||
         lim->max_width > 16384 || lim->max_height > 16384)
         return CLS_ERR_INVALID_ARGUMENT;
     if (cudaSetDevice(device) != cudaSuccess) return CLS_ERR_CUDA;
@@ -197,8 +197,8 @@ cls_status cls_create(cls_ctx **out, int device, const cls_limits *lim)
     bool ok = dalloc(&s.idx, N) && dalloc(&s.ord, N) && dalloc(&s.st_member, N / 2048 + 2) && dalloc(&s.mask, VT) &&
               dalloc(&s.sat, SAT) && dalloc(&s.mdiff, SAT) && dalloc(&s.rowmask, V * c->maxTY * ((c->maxTX + 31) / 32)) &&
               dalloc(&s.view_bbox, V) && dalloc(&s.rec, R) && dalloc(&s.srec, R) && dalloc(&s.rec_gid, R) &&
-              dalloc(&s.cand, R + R / 2 + 1024) && dalloc(&s.rkey, R) && dalloc(&s.rkey_alt, R) && dalloc(&s.rval, R) &&
-              dalloc(&s.rval_alt, R) && dalloc(&s.rcnt, R) && dalloc(&s.urec, P) && dalloc(&s.ukey, P) &&
+              dalloc(&s.cand, R + R / 2 + 1024) && dalloc(&s.rkey, R) && dalloc(&s.rkey_alt, R) &&
+              dalloc(&s.rcnt, R) && dalloc(&s.urec, P) && dalloc(&s.ukey, P) &&
               dalloc(&s.ukey_alt, P) && dalloc(&s.uval, P) && dalloc(&s.uval_alt, P) && dalloc(&s.roff, R) &&
               dalloc(&s.st_scan, std::max(R, P) / 2048 + 2) && dalloc(&s.seg_off, V * c->maxTY) &&
               dalloc(&s.seg_end, V * c->maxTY) && dalloc(&s.st_tiles, VT / 2048 + 2) &&
@@ -356,7 +356,6 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     if (!c->captured) cudaEventRecord(c->ev_fwd, st);
     cls_status e = check_cuda(c, "cls_render_fwd");
     if (e != CLS_OK) return e;
-    c->s.rsorted = s.rsorted;
     c->s.rskey = s.rskey;
     c->s.sukey = s.sukey;
     c->s.suval = s.suval;

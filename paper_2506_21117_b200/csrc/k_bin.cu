@@ -90,17 +90,17 @@ __global__ void __launch_bounds__(256) k_permute(Scratch s)
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         // ties of the (view, depth) key are ordered by Gaussian index (R13): inside a run of equal
         // keys (rare, short) position i takes the run member of rank i - start in index order
-        const unsigned long long k = key[i];
-        unsigned r = s.rsorted[i];
-        if ((i > 0 && key[i - 1] == k) || (i + 1 < n && key[i + 1] == k)) {
+        const unsigned long long k = key[i] >> RK_IDX_BITS;   // (view, depth); the low bits carry the record id
+        unsigned r = (unsigned)(key[i] & RK_IDX_MASK);
+        if ((i > 0 && (key[i - 1] >> RK_IDX_BITS) == k) || (i + 1 < n && (key[i + 1] >> RK_IDX_BITS) == k)) {
             int a = i, b = i + 1;
-            while (a > 0 && key[a - 1] == k) a--;
-            while (b < n && key[b] == k) b++;
+            while (a > 0 && (key[a - 1] >> RK_IDX_BITS) == k) a--;
+            while (b < n && (key[b] >> RK_IDX_BITS) == k) b++;
             for (int j = a; j < b; j++) {
-                const unsigned rj = s.rsorted[j];
+                const unsigned rj = (unsigned)(key[j] & RK_IDX_MASK);
                 const int gj = s.rec_gid[rj];
                 int rank = 0;
-                for (int q = a; q < b; q++) rank += s.rec_gid[s.rsorted[q]] < gj;
+                for (int q = a; q < b; q++) rank += s.rec_gid[(unsigned)(key[q] & RK_IDX_MASK)] < gj;
                 if (rank == i - a) { r = rj; break; }
             }
         }
@@ -217,13 +217,12 @@ void launch_gather_targets(const StepDims &d, const CamSet &cams, const Scratch 
 // 1. record depth sort + ties
 void launch_bin_recsort(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st)
 {
-    const int rbits = 31 + bits_for(d.V - 1);
+    const int rbits = 31 + bits_for(d.V - 1);   // (view, depth) above the carried record id
     const int R = (int)s.max_records;
-    const int w = radix_sort_u64(s.rkey, s.rkey_alt, s.rval, s.rval_alt, &s.cnt->n_records, R, 0, rbits,
-                                 rbits <= 32 ? 8 : 9, s.rs_counts, s.rs_totals, &s.cnt->overflow, st);
+    const int w = radix_sort_u64(s.rkey, s.rkey_alt, nullptr, nullptr, &s.cnt->n_records, R, RK_IDX_BITS,
+                                 RK_IDX_BITS + rbits, rbits <= 32 ? 8 : 9, s.rs_counts, s.rs_totals,
+                                 &s.cnt->overflow, st);
     unsigned long long *rk = w ? s.rkey_alt : s.rkey;
-    unsigned *rv = w ? s.rval_alt : s.rval;
-    s.rsorted = rv;
     s.rskey = rk;   // ties are resolved by k_permute
 }
 

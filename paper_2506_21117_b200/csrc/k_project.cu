@@ -475,9 +475,10 @@ k_project_exact(const float4 *__restrict__ mean_op, const float4 *__restrict__ q
         if (ordi >= 0 && ordi < s.max_active) s.vis[(size_t)v * s.max_active + ordi] = 1;   // densification stats
         // depth-sort key (reading R13): view, then fp32 round-to-nearest of the fp64 depth
         // (positive floats order as their bit patterns; depth > 0.2 here, so bits - bits(0.125) fits
-        // 31 bits: 36-bit keys for 32 views = four 9-bit radix passes); value: the record id
-        s.rkey[slot] = ((unsigned long long)v << 31) | (__float_as_uint(__double2float_rn(p.tz)) - 0x3E000000u);
-        s.rval[slot] = (unsigned)slot;
+        // 31 bits), then the record id in the low RK_IDX_BITS (carried, not sorted: no value array)
+        s.rkey[slot] = ((unsigned long long)v << (31 + RK_IDX_BITS)) |
+                       ((unsigned long long)(__float_as_uint(__double2float_rn(p.tz)) - 0x3E000000u) << RK_IDX_BITS) |
+                       (unsigned long long)slot;
     }
 }
 

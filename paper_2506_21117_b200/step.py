@@ -167,7 +167,7 @@ def default_limits(n, n_views, width, height, records_per_view=None, pairs_per_v
         pairs_per_view = min(TX * TY * 4096, 24 * records_per_view + 65536)
     lim = N.cls_limits()
     lim.max_gaussians = n
-    lim.max_records = min(int(records_per_view) * n_views, 2**31 - 1)
+    lim.max_records = min(int(records_per_view) * n_views, 2**27)   # record ids ride in 27 key bits
     lim.max_pairs = min(int(pairs_per_view) * n_views, 2**31 - 2)
     lim.max_active = max_active if max_active is not None else n
     lim.max_views = n_views
