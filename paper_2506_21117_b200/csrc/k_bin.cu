@@ -83,30 +83,58 @@ __global__ void __launch_bounds__(TSCAN_THREADS) k_tiles_scan(int total, Scratch
 // 2. records gathered into (view, depth, index) order (one 64 B record per access) and the
 // number of tile rows of each footprint rect: the work units of the binning are (record, tile row)
 // pairs, so every thread does the same small amount of work however tall a footprint is.
+// sorted position i -> record id; ties of the (view, depth) key are ordered by Gaussian index
+// (R13): inside a run of equal keys (rare, short) position i takes the run member of rank i - start
+__device__ __forceinline__ unsigned permute_source(const Scratch &s, const unsigned long long *key, int i, int n)
+{
+    const unsigned long long k = key[i] >> RK_IDX_BITS;   // (view, depth); the low bits carry the record id
+    unsigned r = (unsigned)(key[i] & RK_IDX_MASK);
+    if ((i > 0 && (key[i - 1] >> RK_IDX_BITS) == k) || (i + 1 < n && (key[i + 1] >> RK_IDX_BITS) == k)) {
+        int a = i, b = i + 1;
+        while (a > 0 && (key[a - 1] >> RK_IDX_BITS) == k) a--;
+        while (b < n && (key[b] >> RK_IDX_BITS) == k) b++;
+        for (int j = a; j < b; j++) {
+            const unsigned rj = (unsigned)(key[j] & RK_IDX_MASK);
+            const int gj = s.rec_gid[rj];
+            int rank = 0;
+            for (int q = a; q < b; q++) rank += s.rec_gid[(unsigned)(key[q] & RK_IDX_MASK)] < gj;
+            if (rank == i - a) {
+                r = rj;
+                break;
+            }
+        }
+    }
+    return r;
+}
+
+// Warp-cooperative gather: 32 sorted positions per warp iteration; each 64 B record is moved by 4
+// lanes (16 B each), so every load instruction reads 8 whole records (fully used sectors) and the
+// 4 groups' loads are in flight together.
 __global__ void __launch_bounds__(256) k_permute(Scratch s)
 {
     const int n = s.cnt->overflow ? 0 : min(s.cnt->n_records, (int)s.max_records);
     const unsigned long long *key = s.rskey;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        // ties of the (view, depth) key are ordered by Gaussian index (R13): inside a run of equal
-        // keys (rare, short) position i takes the run member of rank i - start in index order
-        const unsigned long long k = key[i] >> RK_IDX_BITS;   // (view, depth); the low bits carry the record id
-        unsigned r = (unsigned)(key[i] & RK_IDX_MASK);
-        if ((i > 0 && (key[i - 1] >> RK_IDX_BITS) == k) || (i + 1 < n && (key[i + 1] >> RK_IDX_BITS) == k)) {
-            int a = i, b = i + 1;
-            while (a > 0 && (key[a - 1] >> RK_IDX_BITS) == k) a--;
-            while (b < n && (key[b] >> RK_IDX_BITS) == k) b++;
-            for (int j = a; j < b; j++) {
-                const unsigned rj = (unsigned)(key[j] & RK_IDX_MASK);
-                const int gj = s.rec_gid[rj];
-                int rank = 0;
-                for (int q = a; q < b; q++) rank += s.rec_gid[(unsigned)(key[q] & RK_IDX_MASK)] < gj;
-                if (rank == i - a) { r = rj; break; }
+    const int lane = threadIdx.x & 31, q = lane & 3;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int base = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; base < n; base += nwarps * 32) {
+        const int i = base + lane;
+        const unsigned r = i < n ? permute_source(s, key, i, n) : 0u;
+        float4 v[4];
+#pragma unroll
+        for (int g = 0; g < 4; g++) {
+            const int j = g * 8 + (lane >> 2);
+            const unsigned rj = __shfl_sync(0xffffffffu, r, j);
+            if (base + j < n) v[g] = reinterpret_cast<const float4 *>(s.rec + rj)[q];
+        }
+#pragma unroll
+        for (int g = 0; g < 4; g++) {
+            const int j = g * 8 + (lane >> 2), ij = base + j;
+            if (ij < n) {
+                reinterpret_cast<float4 *>(s.srec + ij)[q] = v[g];
+                if (q == 3)   // aux: (qcut', ord, x0 | y0 << 16, x1 | y1 << 16) -> tile rows of the rect
+                    s.rcnt[ij] = (unsigned)((__float_as_int(v[g].w) >> 16) - (__float_as_int(v[g].z) >> 16));
             }
         }
-        const Rec R = s.rec[r];
-        s.srec[i] = R;
-        s.rcnt[i] = (unsigned)((__float_as_int(R.aux.w) >> 16) - (__float_as_int(R.aux.z) >> 16));
     }
 }
 
