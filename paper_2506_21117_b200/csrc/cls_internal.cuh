@@ -246,24 +246,29 @@ __device__ __forceinline__ void quat_rot(double w, double x, double y, double z,
     Rq[6] = 2.0 * (x * z - w * y);       Rq[7] = 2.0 * (y * z + w * x);       Rq[8] = 1.0 - 2.0 * (x * x + y * y);
 }
 
-// returns false if culled (near plane, det <= 0, empty rect)
-__device__ __forceinline__ bool project_gaussian(const float4 mo, const float4 q, const float4 ls, const GCam &c,
-                                                 int W, int H, int TX, int TY, Proj &p)
+// M = R(q^) diag(exp(l)) in fp64: the view-independent part of the projection (Sigma = M M^T)
+__device__ __forceinline__ void gauss_m64(const float4 q, const float4 ls, double M[9])
 {
-    const double mx = mo.x, my = mo.y, mz = mo.z;
-    p.tx = (double)c.R[0] * mx + (double)c.R[1] * my + (double)c.R[2] * mz + (double)c.t[0];
-    p.ty = (double)c.R[3] * mx + (double)c.R[4] * my + (double)c.R[5] * mz + (double)c.t[1];
-    p.tz = (double)c.R[6] * mx + (double)c.R[7] * my + (double)c.R[8] * mz + (double)c.t[2];
-    if (!(p.tz > 0.2)) return false;
-    // Sigma = M M^T, M = R(q^) diag(exp(l))
     double qw = q.x, qx = q.y, qy = q.z, qz = q.w;
     double qn = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
     qw /= qn; qx /= qn; qy /= qn; qz /= qn;
     double Rq[9];
     quat_rot(qw, qx, qy, qz, Rq);
     double s0 = exp((double)ls.x), s1 = exp((double)ls.y), s2 = exp((double)ls.z);
-    double M[9] = {Rq[0] * s0, Rq[1] * s1, Rq[2] * s2, Rq[3] * s0, Rq[4] * s1, Rq[5] * s2,
-                   Rq[6] * s0, Rq[7] * s1, Rq[8] * s2};
+    M[0] = Rq[0] * s0; M[1] = Rq[1] * s1; M[2] = Rq[2] * s2;
+    M[3] = Rq[3] * s0; M[4] = Rq[4] * s1; M[5] = Rq[5] * s2;
+    M[6] = Rq[6] * s0; M[7] = Rq[7] * s1; M[8] = Rq[8] * s2;
+}
+
+// the view-dependent part; returns false if culled (near plane, det <= 0, empty rect)
+__device__ __forceinline__ bool project_view(const float4 mo, const double M[9], const GCam &c, int W, int H, int TX,
+                                             int TY, Proj &p)
+{
+    const double mx = mo.x, my = mo.y, mz = mo.z;
+    p.tx = (double)c.R[0] * mx + (double)c.R[1] * my + (double)c.R[2] * mz + (double)c.t[0];
+    p.ty = (double)c.R[3] * mx + (double)c.R[4] * my + (double)c.R[5] * mz + (double)c.t[1];
+    p.tz = (double)c.R[6] * mx + (double)c.R[7] * my + (double)c.R[8] * mz + (double)c.t[2];
+    if (!(p.tz > 0.2)) return false;
     // J with the frustum clamp (R10)
     const double fx = c.fx, fy = c.fy;
     const double limx = 1.3 * ((double)W / (2.0 * fx)), limy = 1.3 * ((double)H / (2.0 * fy));
@@ -304,6 +309,14 @@ __device__ __forceinline__ bool project_gaussian(const float4 mo, const float4 q
     p.x0 = min(max(x0, 0), TX); p.x1 = min(max(x1, 0), TX);
     p.y0 = min(max(y0, 0), TY); p.y1 = min(max(y1, 0), TY);
     return (p.x1 - p.x0) * (p.y1 - p.y0) != 0;
+}
+
+__device__ __forceinline__ bool project_gaussian(const float4 mo, const float4 q, const float4 ls, const GCam &c,
+                                                 int W, int H, int TX, int TY, Proj &p)
+{
+    double M[9];
+    gauss_m64(q, ls, M);
+    return project_view(mo, M, c, W, H, TX, TY, p);
 }
 
 // number of active tiles in [x0,x1) x [y0,y1) from a summed-area table with row pitch TX+1

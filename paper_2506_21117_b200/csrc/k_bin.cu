@@ -213,32 +213,65 @@ void launch_bin_items(const StepDims &d, Scratch &s, cudaStream_t st)
 // target pixels of the active tiles, gathered from (mapped, pinned) host memory into the
 // per-item layout [item][3][256] that k_fwd reads: only the pixels the local step needs cross
 // the host link.  One warp per (item, channel); lanes cover 16-pixel rows.
+// host-resident targets: the pixels of the ACTIVE tiles only, read over the host link (zero-copy,
+// pinned + mapped) into a per-item staging buffer.  A warp reads one pixel row of 8 consecutive
+// items (16 B per lane, 4 lanes per 64 B tile row): the items are in tile order, so neighbouring
+// active tiles make one contiguous 512 B read -- the link is efficient for long reads only
+// (tools/microbench/h2d.cu: 51 GB/s sequential).  GT_U independent loads per thread stay in flight.
+#define GT_U 8
 __global__ void __launch_bounds__(256) k_gather_targets(const __grid_constant__ CamSet cams, Scratch s,
                                                         const float *__restrict__ host_targets)
 {
     const int n_items = s.cnt->overflow ? 0 : s.cnt->n_items;
     const int W = cams.W, H = cams.H, TX = cams.TX, T = cams.T;
     const size_t HW = (size_t)H * W;
-    const int lane = threadIdx.x & 31;
-    for (int wk = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wk < n_items * 3; wk += (gridDim.x * blockDim.x) >> 5) {
-        const int item = wk / 3, ch = wk - 3 * item;
-        const int e = s.items[item];
-        const int v = e / T, t = e - v * T;
-        const int x0 = (t % TX) * CLS_TILE, y0 = (t / TX) * CLS_TILE;
-        const float *src = host_targets + (size_t)v * 3 * HW + (size_t)ch * HW;
-        float *dst = s.tgt + ((size_t)item * 3 + ch) * CLS_BLOCK_PIX;
+    const bool vec = (W & 3) == 0 && (reinterpret_cast<size_t>(host_targets) & 15) == 0;
+    const long long total = (long long)((n_items + 7) / 8) * 3 * 16 * 32;   // (group, ch, row, item-in-group, quarter)
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long f0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; f0 < total; f0 += stride * GT_U) {
+        float4 val[GT_U];
+        long long dst[GT_U];
 #pragma unroll
-        for (int k = 0; k < CLS_BLOCK_PIX / 32; k++) {
-            const int pl = k * 32 + lane, x = x0 + (pl & 15), y = y0 + (pl >> 4);
-            dst[pl] = (x < W && y < H) ? src[(size_t)y * W + x] : 0.f;
+        for (int u = 0; u < GT_U; u++) {
+            const long long f = f0 + u * stride;
+            val[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            dst[u] = -1;
+            if (f < total) {
+                const int qd = (int)(f & 3), j = (int)((f >> 2) & 7);
+                const long long r2 = f >> 5;
+                const int row = (int)(r2 & 15);
+                const long long r3 = r2 >> 4;
+                const int ch = (int)(r3 % 3);
+                const int item = (int)(r3 / 3) * 8 + j;
+                if (item < n_items) {
+                    const int e = s.items[item];
+                    const int v = e / T, t = e - v * T;
+                    const int x = (t % TX) * CLS_TILE + 4 * qd, y = (t / TX) * CLS_TILE + row;
+                    const float *src = host_targets + (size_t)v * 3 * HW + (size_t)ch * HW + (size_t)y * W + x;
+                    if (y < H) {
+                        if (vec && x + 3 < W) {
+                            val[u] = *reinterpret_cast<const float4 *>(src);
+                        } else {
+                            val[u].x = x < W ? src[0] : 0.f;
+                            val[u].y = x + 1 < W ? src[1] : 0.f;
+                            val[u].z = x + 2 < W ? src[2] : 0.f;
+                            val[u].w = x + 3 < W ? src[3] : 0.f;
+                        }
+                    }
+                    dst[u] = ((long long)item * 3 + ch) * 64 + row * 4 + qd;   // (item, ch, row, quarter)
+                }
+            }
         }
+#pragma unroll
+        for (int u = 0; u < GT_U; u++)
+            if (dst[u] >= 0) reinterpret_cast<float4 *>(s.tgt)[dst[u]] = val[u];
     }
 }
 
 void launch_gather_targets(const StepDims &d, const CamSet &cams, const Scratch &s, const float *host_targets,
                            cudaStream_t st)
 {
-    k_gather_targets<<<148 * 4, 256, 0, st>>>(cams, s, host_targets);
+    k_gather_targets<<<148 * 8, 256, 0, st>>>(cams, s, host_targets);
     g_launches++;
 }
 
