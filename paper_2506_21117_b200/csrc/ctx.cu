@@ -172,6 +172,16 @@ cls_status cls_destroy(cls_ctx *c)
     return CLS_OK;
 }
 
+// the host-target gather stream runs at the greatest priority: its blocks (link-bound reads) are
+// scheduled ahead of the main stream's projection/binning blocks, so the transfer starts as soon as
+// the active tiles are known instead of waiting for free SMs
+static cudaError_t create_side_stream(cudaStream_t *st)
+{
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    return cudaStreamCreateWithPriority(st, cudaStreamNonBlocking, hi);
+}
+
 cls_status cls_create(cls_ctx **out, int device, const cls_limits *lim)
 {
     if (!out || !lim) return CLS_ERR_INVALID_ARGUMENT;
@@ -214,7 +224,7 @@ cls_status cls_create(cls_ctx **out, int device, const cls_limits *lim)
                  cudaEventCreateWithFlags(&c->ev_fwd, cudaEventDisableTiming) == cudaSuccess &&
                  cudaEventCreateWithFlags(&c->ev_items, cudaEventDisableTiming) == cudaSuccess &&
                  cudaEventCreateWithFlags(&c->ev_gather, cudaEventDisableTiming) == cudaSuccess &&
-                 cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) == cudaSuccess;
+                 create_side_stream(&c->side) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
         cls_destroy(c);

@@ -271,7 +271,9 @@ __global__ void __launch_bounds__(256) k_gather_targets(const __grid_constant__ 
 void launch_gather_targets(const StepDims &d, const CamSet &cams, const Scratch &s, const float *host_targets,
                            cudaStream_t st)
 {
-    k_gather_targets<<<148 * 8, 256, 0, st>>>(cams, s, host_targets);
+    // a small grid: 32 x 256 threads x GT_U 16 B reads keep ~1 MB in flight, far above the link's
+    // bandwidth-delay product (~0.1 MB), while leaving the SMs to the concurrent projection/binning
+    k_gather_targets<<<32, 256, 0, st>>>(cams, s, host_targets);
     g_launches++;
 }
 
