@@ -332,17 +332,19 @@ def algorithmic_work(sc, n_views, st):
     K4 = -(-3 * (sc.sh_degree + 1) ** 2 // 4)
     A, R, P = st["n_active"], st["n_records"], st["n_pairs"]
     C = st.get("n_candidates", R)
-    rpasses = -(-(32 + max(V - 1, 1).bit_length()) // 8)
-    T = -(-sc.width // 16) * -(-sc.height // 16)
-    ppasses = -(-max(V * T - 1, 1).bit_length() // 9)
+    U = st.get("n_units", P)
+    rbits = 31 + max(V - 1, 1).bit_length()            # (view, depth) bits above the carried record id
+    rpasses = -(-rbits // (8 if rbits <= 32 else 9))
+    TY = -(-sc.height // 16)
+    upasses = -(-max(V * TY, 1).bit_length() // 8)      # row segments (view, tile row), 8-bit digits
     return {
         "member": ("hbm", n * 16 + n * 4 + A * 4),
         "project_cand": ("hbm", n * 48 + C * 8),
-        "project_exact": ("hbm", C * 8 + R * (48 + 16 * K4 + 64 + 4 + 12)),
-        "rec_sort": ("hbm", rpasses * R * 24),
-        "bin_count": ("hbm", R * (4 + 8 + 64 + 64 + 4 + 8)),
-        "emit": ("hbm", R * (64 + 8 + 4 + 4) + P * 8),
-        "pair_sort": ("hbm", ppasses * P * 16 + P * 8),
+        "project_exact": ("hbm", C * 8 + R * (48 + 16 * K4 + 64 + 4 + 8)),
+        "rec_sort": ("hbm", rpasses * R * 16),          # key-only passes: read + write 8 B
+        "bin_count": ("hbm", R * (8 + 64 + 64 + 4 + 4) + U * 4),
+        "emit": ("hbm", R * 64 + U * (4 + 12)),
+        "pair_sort": ("hbm", upasses * U * 24 + U * 8),  # key 8 B + value 4 B, read + write
         "fwd_raster": ("alu", st["n_fwd_evals"] * FWD_FLOPS_PER_EVAL),
         "bwd_raster": ("alu", st["n_bwd_evals"] * BWD_FLOPS_PER_EVAL),
         "bwd_project": ("hbm", A * V * 48 + A * (48 + 16 * K4) + A * 16 * (3 + K4)),
