@@ -86,7 +86,7 @@ struct Scratch {
     // records
     Rec *rec;               // records in creation order (k_project_exact)
     int *rec_gid;           // their Gaussian index (ties of the depth order, R13)
-    Rec *srec;              // records in (view, depth, index) order: the binning and the raster read these
+    unsigned *srid;         // record ids in (view, depth, Gaussian index) order (records stay in place)
     long long max_records;
     int2 *cand;             // (Gaussian, view) candidates of the fp32 pre-test
     long long max_cand;
@@ -473,8 +473,9 @@ __device__ __forceinline__ bool foot_row(const FootRec &f, int ty, int &lo, int 
 // sorted record i (pair value: i | active << 31)
 __device__ __forceinline__ FootRec foot_load(const Scratch &s, unsigned i)
 {
-    const Rec R = s.srec[i];
-    return foot_make(R, (int)(s.rskey[i] >> (31 + RK_IDX_BITS)), i | (__float_as_int(R.aux.y) < 0 ? 0u : 0x80000000u));
+    const unsigned rid = s.srid[i];
+    const Rec R = s.rec[rid];
+    return foot_make(R, (int)(s.rskey[i] >> (31 + RK_IDX_BITS)), rid | (__float_as_int(R.aux.y) < 0 ? 0u : 0x80000000u));
 }
 
 // active tiles of row bitmask `rm` (W32 words) in columns [lo, hi] of word w

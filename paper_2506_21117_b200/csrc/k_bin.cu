@@ -107,34 +107,18 @@ __device__ __forceinline__ unsigned permute_source(const Scratch &s, const unsig
     return r;
 }
 
-// Warp-cooperative gather: 32 sorted positions per warp iteration; each 64 B record is moved by 4
-// lanes (16 B each), so every load instruction reads 8 whole records (fully used sectors) and the
-// 4 groups' loads are in flight together.
+// sorted position i -> record id (ties re-ordered by Gaussian index) and the record's number of
+// tile rows; the records themselves stay where k_project_exact wrote them (units and the raster
+// address them by id: no 64 B record copy)
 __global__ void __launch_bounds__(256) k_permute(Scratch s)
 {
     const int n = s.cnt->overflow ? 0 : min(s.cnt->n_records, (int)s.max_records);
     const unsigned long long *key = s.rskey;
-    const int lane = threadIdx.x & 31, q = lane & 3;
-    const int nwarps = (gridDim.x * blockDim.x) >> 5;
-    for (int base = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; base < n; base += nwarps * 32) {
-        const int i = base + lane;
-        const unsigned r = i < n ? permute_source(s, key, i, n) : 0u;
-        float4 v[4];
-#pragma unroll
-        for (int g = 0; g < 4; g++) {
-            const int j = g * 8 + (lane >> 2);
-            const unsigned rj = __shfl_sync(0xffffffffu, r, j);
-            if (base + j < n) v[g] = reinterpret_cast<const float4 *>(s.rec + rj)[q];
-        }
-#pragma unroll
-        for (int g = 0; g < 4; g++) {
-            const int j = g * 8 + (lane >> 2), ij = base + j;
-            if (ij < n) {
-                reinterpret_cast<float4 *>(s.srec + ij)[q] = v[g];
-                if (q == 3)   // aux: (qcut', ord, x0 | y0 << 16, x1 | y1 << 16) -> tile rows of the rect
-                    s.rcnt[ij] = (unsigned)((__float_as_int(v[g].w) >> 16) - (__float_as_int(v[g].z) >> 16));
-            }
-        }
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const unsigned r = permute_source(s, key, i, n);
+        const float4 aux = reinterpret_cast<const float4 *>(s.rec + r)[3];   // (qcut', ord, x0|y0<<16, x1|y1<<16)
+        s.srid[i] = r;
+        s.rcnt[i] = (unsigned)((__float_as_int(aux.w) >> 16) - (__float_as_int(aux.z) >> 16));
     }
 }
 

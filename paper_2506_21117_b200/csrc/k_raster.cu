@@ -31,7 +31,7 @@ namespace cls {
 __device__ __forceinline__ void stage(const Scratch &s, unsigned val, int tx, int ty, float4 &sa, float4 &sb,
                                       float4 &sc)
 {
-    const Rec &R = s.srec[val & 0x7fffffffu];
+    const Rec &R = s.rec[val & 0x7fffffffu];
     const float4 xy = R.xy, co = R.co, rgb = R.rgb;
     const float2 ax = make_float2(R.aux.x, R.aux.y);
     const double dx0 = ((double)xy.x - (double)(CLS_TILE * tx)) + (double)xy.y;
@@ -118,7 +118,7 @@ __device__ __forceinline__ int fill_batch(const Scratch &s, int &cur, int end, i
                 cl |= ent[3 * slot + 1].z > 0.98999f;   // alpha's 0.99 clamp may bind
                 if (val >> 31) fmin = min(fmin, s_pos[slot]);
             } else {
-                const float4 xy = s.srec[val & 0x7fffffffu].xy;
+                const float4 xy = s.rec[val & 0x7fffffffu].xy;
                 sd[slot] = make_float2(__double2float_rn(((double)xy.x - (double)(CLS_TILE * tx)) + (double)xy.y),
                                        __double2float_rn(((double)xy.z - (double)(CLS_TILE * ty)) + (double)xy.w));
             }
