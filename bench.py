@@ -343,8 +343,8 @@ def algorithmic_work(sc, n_views, st):
         "project_exact": ("hbm", C * 8 + R * (48 + 16 * K4 + 64 + 4 + 8)),
         "rec_sort": ("hbm", rpasses * R * 16),          # key-only passes: read + write 8 B
         "bin_count": ("hbm", R * (8 + 64 + 64 + 4 + 4) + U * 4),
-        "emit": ("hbm", R * 64 + U * (4 + 12)),
-        "pair_sort": ("hbm", upasses * U * 24 + U * 8),  # key 8 B + value 4 B, read + write
+        "emit": ("hbm", R * 64 + U * (4 + 8)),
+        "pair_sort": ("hbm", upasses * U * 16 + U * 8),  # key-only passes (record id packed in the key)
         "fwd_raster": ("alu", st["n_fwd_evals"] * FWD_FLOPS_PER_EVAL),
         "bwd_raster": ("alu", st["n_bwd_evals"] * BWD_FLOPS_PER_EVAL),
         "bwd_project": ("hbm", A * V * 48 + A * (48 + 16 * K4) + A * 16 * (3 + K4)),

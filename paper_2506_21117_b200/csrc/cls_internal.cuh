@@ -9,6 +9,11 @@
 #define CLS_TILE 16
 #define RK_IDX_BITS 27   // record id in the low bits of the record sort key (max_records <= 2^27)
 #define RK_IDX_MASK ((1ull << RK_IDX_BITS) - 1ull)
+// unit key (one u64, sorted by its top bits only): row segment (view * TY + ty, 17 bits; V * TY = dead)
+// << 47 | hi << 37 | lo << 27 | record id (27 bits); lo, hi = the footprint's tile columns (TX <= 1024)
+#define UK_SEG_SHIFT 47
+#define UK_LO_SHIFT 27
+#define UK_HI_SHIFT 37
 #define CLS_BLOCK_PIX 256
 
 namespace cls {
@@ -98,9 +103,7 @@ struct Scratch {
     // units sorted stably by their row segment (view, tile row): key = segment << 32 | lo | hi << 16
     // (the footprint's tile columns in the row), value = sorted record | active << 31
     unsigned long long *ukey, *ukey_alt;
-    unsigned *uval, *uval_alt;
-    const unsigned long long *sukey;        // sorted buffers
-    const unsigned *suval;
+    const unsigned long long *sukey;        // sorted units
     int *seg_off, *seg_end;                 // [V*TY] range of each row segment in the sorted units
     long long max_units;
     unsigned long long *st_scan;    // look-back status of the offsets scan

@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(256) k_unit_build(const __grid_constant__ CamS
 {
     const int U = s.cnt->overflow ? 0 : s.cnt->n_units32;
     const int TY = cams.TY, W32 = (cams.TX + 31) >> 5;
-    const unsigned long long dead = (unsigned long long)(cams.n * TY) << 32;
+    const unsigned long long dead = (unsigned long long)(cams.n * TY) << UK_SEG_SHIFT;
     unsigned long long pairs = 0;
     for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < U; u += gridDim.x * blockDim.x) {
         const unsigned i = s.urec[u];
@@ -157,8 +157,10 @@ __global__ void __launch_bounds__(256) k_unit_build(const __grid_constant__ CamS
             for (int w = lo >> 5; w <= (hi >> 5); w++) cnt += __popc(row_bits(rm, w, lo, hi));
         }
         pairs += cnt;
-        s.ukey[u] = cnt ? ((unsigned long long)(f.view * TY + ty) << 32) | (unsigned)lo | ((unsigned)hi << 16) : dead;
-        s.uval[u] = f.w;
+        const unsigned long long rid = f.w & 0x7fffffffu;
+        s.ukey[u] = (cnt ? ((unsigned long long)(f.view * TY + ty) << UK_SEG_SHIFT) |
+                               ((unsigned long long)lo << UK_LO_SHIFT) | ((unsigned long long)hi << UK_HI_SHIFT)
+                         : dead) | rid;
     }
     for (int o = 16; o > 0; o >>= 1) pairs += __shfl_xor_sync(0xffffffffu, pairs, o);
     if ((threadIdx.x & 31) == 0 && pairs) atomicAdd(&s.cnt->n_pairs, pairs);
@@ -170,10 +172,10 @@ __global__ void __launch_bounds__(256) k_seg_ranges(Scratch s, int n_seg)
     const int n = s.cnt->overflow ? 0 : s.cnt->n_units32;
     const unsigned long long *k = s.sukey;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const unsigned e = (unsigned)(k[i] >> 32);
+        const unsigned e = (unsigned)(k[i] >> UK_SEG_SHIFT);
         if (e >= (unsigned)n_seg) continue;
-        if (i == 0 || (unsigned)(k[i - 1] >> 32) != e) s.seg_off[e] = i;
-        if (i == n - 1 || (unsigned)(k[i + 1] >> 32) != e) s.seg_end[e] = i + 1;
+        if (i == 0 || (unsigned)(k[i - 1] >> UK_SEG_SHIFT) != e) s.seg_off[e] = i;
+        if (i == n - 1 || (unsigned)(k[i + 1] >> UK_SEG_SHIFT) != e) s.seg_end[e] = i + 1;
     }
 }
 
@@ -296,10 +298,9 @@ void launch_bin_pairsort(const StepDims &d, const CamSet &cams, Scratch &s, cuda
 {
     const int n_seg = d.V * d.TY;
     const int sbits = std::max(bits_for(n_seg), 1);   // n_seg itself marks the dead units
-    const int w = radix_sort_u64(s.ukey, s.ukey_alt, s.uval, s.uval_alt, &s.cnt->n_units32, (int)s.max_units, 32,
-                                 32 + sbits, 8, s.rs_counts, s.rs_totals, &s.cnt->overflow, st);
+    const int w = radix_sort_u64(s.ukey, s.ukey_alt, nullptr, nullptr, &s.cnt->n_units32, (int)s.max_units,
+                                 UK_SEG_SHIFT, UK_SEG_SHIFT + sbits, 8, s.rs_counts, s.rs_totals, &s.cnt->overflow, st);
     s.sukey = w ? s.ukey_alt : s.ukey;
-    s.suval = w ? s.uval_alt : s.uval;
     cudaMemsetAsync(s.seg_off, 0, sizeof(int) * (size_t)n_seg, st);
     cudaMemsetAsync(s.seg_end, 0, sizeof(int) * (size_t)n_seg, st);
     k_seg_ranges<<<148 * 8, 256, 0, st>>>(s, n_seg);

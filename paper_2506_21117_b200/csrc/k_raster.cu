@@ -31,7 +31,7 @@ namespace cls {
 __device__ __forceinline__ void stage(const Scratch &s, unsigned val, int tx, int ty, float4 &sa, float4 &sb,
                                       float4 &sc)
 {
-    const Rec &R = s.rec[val & 0x7fffffffu];
+    const Rec &R = s.rec[val];
     const float4 xy = R.xy, co = R.co, rgb = R.rgb;
     const float2 ax = make_float2(R.aux.x, R.aux.y);
     const double dx0 = ((double)xy.x - (double)(CLS_TILE * tx)) + (double)xy.y;
@@ -62,7 +62,6 @@ __device__ __forceinline__ int fill_batch(const Scratch &s, int &cur, int end, i
 {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned lt = (1u << lane) - 1u;
-    const unsigned *cols = reinterpret_cast<const unsigned *>(s.sukey);   // low word: lo | hi << 16
     int nst = 0;
     while (nst < RT_BATCH && (DIR > 0 ? cur < end : cur > end)) {
         unsigned cw[RT_SCAN], uv[RT_SCAN];
@@ -70,13 +69,14 @@ __device__ __forceinline__ int fill_batch(const Scratch &s, int &cur, int end, i
         for (int k = 0; k < RT_SCAN; k++) {   // all loads first (columns AND record ids): one memory latency per round
             const int u = DIR > 0 ? cur + k * RT_THREADS + tid : cur - 1 - (k * RT_THREADS + tid);
             const bool in = DIR > 0 ? u < end : u >= end;
-            cw[k] = in ? __ldg(cols + 2 * (size_t)u) : 0xffffu;   // empty if outside
-            uv[k] = in ? __ldg(s.suval + u) : 0u;
+            const unsigned long long key = in ? __ldg(s.sukey + u) : (0x3ffull << UK_LO_SHIFT);   // empty if outside
+            cw[k] = (unsigned)(key >> UK_LO_SHIFT) & 0xfffffu;   // lo | hi << 10
+            uv[k] = (unsigned)(key & RK_IDX_MASK);               // record id
         }
         unsigned cov = 0u;
 #pragma unroll
         for (int k = 0; k < RT_SCAN; k++) {
-            const int lo = (int)(cw[k] & 0xffffu), hi = (int)(cw[k] >> 16);
+            const int lo = (int)(cw[k] & 0x3ffu), hi = (int)(cw[k] >> 10);
             const bool c = lo <= tx && tx <= hi;
             const unsigned b = __ballot_sync(0xffffffffu, c);
             cov |= (c ? 1u : 0u) << k;
@@ -116,9 +116,9 @@ __device__ __forceinline__ int fill_batch(const Scratch &s, int &cur, int end, i
             stage(s, val, tx, ty, ent[3 * slot], ent[3 * slot + 1], ent[3 * slot + 2]);
             if (!BWD) {
                 cl |= ent[3 * slot + 1].z > 0.98999f;   // alpha's 0.99 clamp may bind
-                if (val >> 31) fmin = min(fmin, s_pos[slot]);
+                if (__float_as_int(ent[3 * slot + 2].w) >= 0) fmin = min(fmin, s_pos[slot]);   // active ordinal
             } else {
-                const float4 xy = s.rec[val & 0x7fffffffu].xy;
+                const float4 xy = s.rec[val].xy;
                 sd[slot] = make_float2(__double2float_rn(((double)xy.x - (double)(CLS_TILE * tx)) + (double)xy.y),
                                        __double2float_rn(((double)xy.z - (double)(CLS_TILE * ty)) + (double)xy.w));
             }
