@@ -106,7 +106,9 @@ typedef struct {
     int32_t n_views;
     int64_t max_list;          /* longest per-tile list */
     int64_t n_units;           /* (record, tile row) work units of the binning */
-    int64_t n_fwd_evals;       /* (pixel, list entry) evaluations of the forward compositing */
+    int64_t n_fwd_evals;       /* (pixel, list entry) evaluations of the forward compositing: the list
+                                  length for pixels that never terminate, last composited entry + 1
+                                  for the others (a lower bound) */
     int64_t n_bwd_evals;       /* (pixel, list entry) evaluations of the backward walk (after its bwd) */
     int64_t n_candidates;      /* (Gaussian, view) pairs passing the fp32 projection pre-test */
     int64_t n_kept_pairs;      /* pairs kept after the exact alpha-footprint culling (<= n_pairs) */

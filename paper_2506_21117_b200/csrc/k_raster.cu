@@ -370,7 +370,10 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
             C0[p] = -C0[p];   // the loop kept the negated sums
             C1[p] = -C1[p];
             C2[p] = -C2[p];
-            evals += (unsigned long long)(last[p] + 1);   // entries up to the last composited one
+            // (pixel, entry) evaluations the method performs: the whole list for a pixel that never
+            // terminated, entries up to its last composited one otherwise (a lower bound: the
+            // terminating entry and the non-hits before it are not counted)
+            evals += Tr[p] > 0.f ? (unsigned long long)lbase : (unsigned long long)(last[p] + 1);
             const int pl = tid + p * RT_THREADS;          // pixel slot (ly + 4p) * 16 + lx
             const size_t px = (size_t)item * CLS_BLOCK_PIX + pl;
             s.px_T[px] = Tf;
