@@ -357,9 +357,12 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     run(c, P_BINCOUNT, st, [&] { launch_bin_count(d, cs, s, st); });
     run(c, P_EMIT, st, [&] { launch_bin_emit(d, cs, s, st); });
     run(c, P_PAIRSORT, st, [&] { launch_bin_pairsort(d, cs, s, st); });
-    if (staged) cudaStreamWaitEvent(st, c->ev_gather, 0);
     run(c, P_FWD, st, [&] { launch_fwd(d, cs, s, targets, staged, images, loss_scale, bgc, st); });
     if (images) run(c, P_FILL, st, [&] { launch_fill_bg(d, s, images, bgc, st); });
+    if (staged) {   // the loss terms need the gathered targets; the compositing above did not
+        cudaStreamWaitEvent(st, c->ev_gather, 0);
+        run(c, P_LOSS, st, [&] { launch_loss_staged(d, cs, s, loss_scale, st); });
+    }
     if (targets && loss) run(c, P_LOSS, st, [&] { launch_loss(s, loss_scale, loss, st); });
     if (tile_mask) cudaMemcpyAsync(tile_mask, s.mask, (size_t)d.V * d.T, cudaMemcpyDeviceToDevice, st);
     cudaMemcpyAsync(c->h_cnt, s.cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st);

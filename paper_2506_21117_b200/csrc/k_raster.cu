@@ -388,14 +388,12 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
                     images[pix + HW] = o1;
                     images[pix + 2 * HW] = o2;
                 }
-                if (TARGET) {
-                    float t0, t1, t2;
-                    if (staged) {   // gathered per item (host-resident targets)
-                        const float *tg = s.tgt + (size_t)item * 3 * CLS_BLOCK_PIX + pl;
-                        t0 = tg[0]; t1 = tg[CLS_BLOCK_PIX]; t2 = tg[2 * CLS_BLOCK_PIX];
-                    } else {
-                        t0 = targets[pix]; t1 = targets[pix + HW]; t2 = targets[pix + 2 * HW];
-                    }
+                if (TARGET && staged) {   // host-resident targets still in flight: keep the colour,
+                    dl[0] = o0;           // k_loss_staged forms the loss terms once they arrive
+                    dl[CLS_BLOCK_PIX] = o1;
+                    dl[2 * CLS_BLOCK_PIX] = o2;
+                } else if (TARGET) {
+                    const float t0 = targets[pix], t1 = targets[pix + HW], t2 = targets[pix + 2 * HW];
                     const float r0 = o0 - t0, r1 = o1 - t1, r2 = o2 - t2;
                     l1 += fabsf(r0) + fabsf(r1) + fabsf(r2);
                     dl[0] = r0 > 0.f ? loss_scale : (r0 < 0.f ? -loss_scale : 0.f);
@@ -406,13 +404,56 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
                 dl[0] = dl[CLS_BLOCK_PIX] = dl[2 * CLS_BLOCK_PIX] = 0.f;
             }
         }
-        if (TARGET) {
+        if (TARGET && !staged) {
             const float tot = block_sum(l1, red);
             if (tid == 0) s.item_loss[item] = tot;
         }
     }
     for (int o = 16; o > 0; o >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, o);
     if ((tid & 31) == 0 && evals) atomicAdd(&s.cnt->fwd_evals, evals);
+}
+
+// host-resident targets: the fused-L1 epilogue of k_fwd, run once the gathered targets arrived
+// (the forward compositing itself does not wait for the host link).  Same thread <-> pixel map,
+// per-thread order and block reduction as k_fwd's epilogue: bit-identical loss and dL/dC.
+__global__ void __launch_bounds__(RT_THREADS) k_loss_staged(const __grid_constant__ CamSet cams, Scratch s,
+                                                            float loss_scale)
+{
+    __shared__ float red[RT_THREADS / 32];
+    if (s.cnt->overflow) return;
+    const int n_items = s.cnt->n_items;
+    const int tid = threadIdx.x;
+    const int lx = tid & 15, ly = tid >> 4;
+    const int W = cams.W, H = cams.H, TX = cams.TX, T = cams.T;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int e = s.items[item];
+        const int t = e % T;
+        const int x = (t % TX) * CLS_TILE + lx, y0 = (t / TX) * CLS_TILE;
+        float l1 = 0.f;
+#pragma unroll
+        for (int p = 0; p < RT_PX; p++) {
+            const int yy = y0 + ly + 4 * p;
+            if (x < W && yy < H) {
+                const int pl = tid + p * RT_THREADS;
+                float *dl = s.px_dl + (size_t)item * 3 * CLS_BLOCK_PIX + pl;
+                const float *tg = s.tgt + (size_t)item * 3 * CLS_BLOCK_PIX + pl;
+                const float r0 = dl[0] - tg[0], r1 = dl[CLS_BLOCK_PIX] - tg[CLS_BLOCK_PIX],
+                            r2 = dl[2 * CLS_BLOCK_PIX] - tg[2 * CLS_BLOCK_PIX];
+                l1 += fabsf(r0) + fabsf(r1) + fabsf(r2);
+                dl[0] = r0 > 0.f ? loss_scale : (r0 < 0.f ? -loss_scale : 0.f);
+                dl[CLS_BLOCK_PIX] = r1 > 0.f ? loss_scale : (r1 < 0.f ? -loss_scale : 0.f);
+                dl[2 * CLS_BLOCK_PIX] = r2 > 0.f ? loss_scale : (r2 < 0.f ? -loss_scale : 0.f);
+            }
+        }
+        const float tot = block_sum(l1, red);
+        if (tid == 0) s.item_loss[item] = tot;
+    }
+}
+
+void launch_loss_staged(const StepDims &d, const CamSet &cams, const Scratch &s, float loss_scale, cudaStream_t st)
+{
+    k_loss_staged<<<148 * 16, RT_THREADS, 0, st>>>(cams, s, loss_scale);
+    g_launches++;
 }
 
 void launch_fwd(const StepDims &d, const CamSet &cams, const Scratch &s, const float *targets, bool staged,

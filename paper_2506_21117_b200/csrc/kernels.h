@@ -46,6 +46,7 @@ void launch_fwd(const StepDims &d, const CamSet &cams, const Scratch &s, const f
                 float *images, float loss_scale, float3 bg, cudaStream_t st);
 void launch_fill_bg(const StepDims &d, const Scratch &s, float *images, float3 bg, cudaStream_t st);
 void launch_loss(const Scratch &s, float loss_scale, float *loss, cudaStream_t st);
+void launch_loss_staged(const StepDims &d, const CamSet &cams, const Scratch &s, float loss_scale, cudaStream_t st);
 // (5) backward raster + backward projection                    (k_raster.cu, k_bwd_project.cu)
 void launch_zero_grad2d(const StepDims &d, const Scratch &s, long long cap, cudaStream_t st);
 void launch_bwd_raster(const StepDims &d, const Scratch &s, const float *dL_dimages, float3 bg, cudaStream_t st);
