@@ -295,7 +295,7 @@ def run_ours(args):
             "kernels_ms_per_step": {k: round(v["ms"] / args.steps, 4) for k, v in per.items()},
             "kernel_rates": groups,
             "counts": {k: stats[k] for k in ("n_records", "n_pairs", "n_items", "max_list", "n_units",
-                                             "n_fwd_evals", "n_bwd_evals", "n_candidates", "n_kept_pairs", "n_stage1", "n_tested")},
+                                             "n_fwd_evals", "n_bwd_evals", "n_candidates", "n_kept_pairs", "n_stage1", "n_tested", "n_live_units")},
         }
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(sc, args.cpu_views)

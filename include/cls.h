@@ -114,6 +114,7 @@ typedef struct {
     int64_t n_kept_pairs;      /* pairs kept after the exact alpha-footprint culling (<= n_pairs) */
     int64_t n_stage1;          /* (Gaussian, view) pairs passing the projection isotropic pre-test */
     int64_t n_tested;          /* (Gaussian, view) pairs the pre-test examined (after the warp-level cull) */
+    int64_t n_live_units;      /* binning units (record, tile row) that reach an active tile */
 } cls_stats_t;
 
 #define CLS_PROF_GROUPS 16

@@ -60,14 +60,15 @@ class cls_stats_t(ctypes.Structure):
                 ("overflow", ctypes.c_int32), ("n_views", ctypes.c_int32), ("max_list", ctypes.c_int64),
                 ("n_units", ctypes.c_int64), ("n_fwd_evals", ctypes.c_int64), ("n_bwd_evals", ctypes.c_int64),
                 ("n_candidates", ctypes.c_int64), ("n_kept_pairs", ctypes.c_int64), ("n_stage1", ctypes.c_int64),
-                ("n_tested", ctypes.c_int64)]
+                ("n_tested", ctypes.c_int64), ("n_live_units", ctypes.c_int64)]
 
     def as_dict(self):
         return dict(n_active=self.n_active, n_records=self.n_records, n_pairs=self.n_pairs, n_items=self.n_items,
                     n_active_tiles=list(self.n_active_tiles[: self.n_views]), overflow=self.overflow,
                     max_list=self.max_list, n_units=self.n_units, n_fwd_evals=self.n_fwd_evals,
                     n_bwd_evals=self.n_bwd_evals, n_candidates=self.n_candidates,
-                    n_kept_pairs=self.n_kept_pairs, n_stage1=self.n_stage1, n_tested=self.n_tested)
+                    n_kept_pairs=self.n_kept_pairs, n_stage1=self.n_stage1, n_tested=self.n_tested,
+                    n_live_units=self.n_live_units)
 
 
 class cls_profile_t(ctypes.Structure):

@@ -51,6 +51,7 @@ struct Counters {
     int n_cand;
     unsigned long long n_stage1;    // (Gaussian, view) pairs passing the isotropic stage-1 test
     unsigned long long n_tested;    // (Gaussian, view) pairs tested by stage 1 (after the warp-level cull)
+    unsigned long long n_live_units;   // units reaching an active tile (the others sort to the end)
     int tiles_scan_tiles;   // look-back ticket (tile scan)
     unsigned long long n_pairs;     // (record, active tile) pairs kept by the exact footprint culling
     int n_pairs32;          // min(n_pairs, max_pairs): element count of the pair sort

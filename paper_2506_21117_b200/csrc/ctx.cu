@@ -497,6 +497,7 @@ cls_status cls_stats(cls_ctx *c, cls_stats_t *out)
     out->n_kept_pairs = (int64_t)h.n_pairs;
     out->n_stage1 = (int64_t)h.n_stage1;
     out->n_tested = (int64_t)h.n_tested;
+    out->n_live_units = (int64_t)h.n_live_units;
     out->n_fwd_evals = (int64_t)h.fwd_evals;
     unsigned long long bev = 0;
     cudaMemcpy(&bev, &c->s.cnt->bwd_evals, sizeof bev, cudaMemcpyDeviceToHost);

@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(256) k_unit_build(const __grid_constant__ CamS
     const int U = s.cnt->overflow ? 0 : s.cnt->n_units32;
     const int TY = cams.TY, W32 = (cams.TX + 31) >> 5;
     const unsigned long long dead = (unsigned long long)(cams.n * TY) << UK_SEG_SHIFT;
-    unsigned long long pairs = 0;
+    unsigned long long pairs = 0, live = 0;
     for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < U; u += gridDim.x * blockDim.x) {
         const unsigned i = s.urec[u];
         const FootRec f = foot_load(s, i);
@@ -157,13 +157,18 @@ __global__ void __launch_bounds__(256) k_unit_build(const __grid_constant__ CamS
             for (int w = lo >> 5; w <= (hi >> 5); w++) cnt += __popc(row_bits(rm, w, lo, hi));
         }
         pairs += cnt;
+        live += cnt ? 1u : 0u;
         const unsigned long long rid = f.w & 0x7fffffffu;
         s.ukey[u] = (cnt ? ((unsigned long long)(f.view * TY + ty) << UK_SEG_SHIFT) |
                                ((unsigned long long)lo << UK_LO_SHIFT) | ((unsigned long long)hi << UK_HI_SHIFT)
                          : dead) | rid;
     }
-    for (int o = 16; o > 0; o >>= 1) pairs += __shfl_xor_sync(0xffffffffu, pairs, o);
+    for (int o = 16; o > 0; o >>= 1) {
+        pairs += __shfl_xor_sync(0xffffffffu, pairs, o);
+        live += __shfl_xor_sync(0xffffffffu, live, o);
+    }
     if ((threadIdx.x & 31) == 0 && pairs) atomicAdd(&s.cnt->n_pairs, pairs);
+    if ((threadIdx.x & 31) == 0 && live) atomicAdd(&s.cnt->n_live_units, live);
 }
 
 // row-segment ranges of the sorted units (dead units excluded)
