@@ -122,7 +122,8 @@ __global__ void __launch_bounds__(256) k_permute(Scratch s)
     }
 }
 
-// unit -> record map: urec[roff[i] + k] = i for the record's k-th tile row
+// unit -> record map: urec[roff[i] + k] = (record id, view << 16 | k) for the k-th tile row of the
+// record at sorted position i (the unit build then needs one dependent load, not three)
 __global__ void __launch_bounds__(256) k_fill_units(Scratch s)
 {
     const int n = s.cnt->overflow ? 0 : min(s.cnt->n_records, (int)s.max_records);
@@ -134,7 +135,8 @@ __global__ void __launch_bounds__(256) k_fill_units(Scratch s)
     if ((long long)U > s.max_units) return;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const unsigned o = s.roff[i], c = s.rcnt[i];
-        for (unsigned k = 0; k < c; k++) s.urec[o + k] = (unsigned)i;
+        const unsigned rid = s.srid[i], vw = (unsigned)(s.rskey[i] >> (31 + RK_IDX_BITS)) << 16;
+        for (unsigned k = 0; k < c; k++) s.urec[o + k] = make_uint2(rid, vw | k);
     }
 }
 
@@ -147,9 +149,10 @@ __global__ void __launch_bounds__(256) k_unit_build(const __grid_constant__ CamS
     const unsigned long long dead = (unsigned long long)(cams.n * TY) << UK_SEG_SHIFT;
     unsigned long long pairs = 0, live = 0;
     for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < U; u += gridDim.x * blockDim.x) {
-        const unsigned i = s.urec[u];
-        const FootRec f = foot_load(s, i);
-        const int ty = f.y0 + (int)((unsigned)u - s.roff[i]);
+        const uint2 ur = s.urec[u];
+        const Rec R = s.rec[ur.x];
+        const FootRec f = foot_make(R, (int)(ur.y >> 16), ur.x | (__float_as_int(R.aux.y) < 0 ? 0u : 0x80000000u));
+        const int ty = f.y0 + (int)(ur.y & 0xffffu);
         int lo, hi;
         unsigned cnt = 0u;
         if (foot_row(f, ty, lo, hi)) {
