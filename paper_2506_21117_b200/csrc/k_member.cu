@@ -112,57 +112,67 @@ k_active_rects(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
     }
 }
 
+// inclusive prefix sum of n ints at stride st (one warp; 32 elements per step with a carried total)
+__device__ __forceinline__ void warp_prefix(int *a, int n, int st)
+{
+    const int lane = threadIdx.x & 31;
+    int carry = 0;
+    for (int b = 0; b < n; b += 32) {
+        const int i = b + lane;
+        int v = i < n ? a[i * st] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += t;
+        }
+        v += carry;
+        if (i < n) a[i * st] = v;
+        carry = __shfl_sync(0xffffffffu, v, 31);
+    }
+}
+
 // mask of each view from the rect-corner differences (2D prefix sum > 0: the tile lies in some
-// active rect), then its summed-area table, tile bbox and row bitmasks; one block per view.  The
-// prefix sums run in shared memory (SMEM) when the (TY+1)(TX+1) table fits, else in global memory.
+// active rect), then its summed-area table, tile bbox and row bitmasks; one block per view, one warp
+// per row / column prefix (warp scans).  The tables and the mask live in shared memory (SMEM) when
+// they fit, else in global memory.
+#define SAT_THREADS 512
 template <bool SMEM>
-__global__ void __launch_bounds__(256) k_sat(const __grid_constant__ CamSet cams, Scratch s, int all_tiles)
+__global__ void __launch_bounds__(SAT_THREADS) k_sat(const __grid_constant__ CamSet cams, Scratch s, int all_tiles)
 {
     extern __shared__ int sm_sat[];
     const int v = blockIdx.x;
     const int TX = cams.TX, TY = cams.TY, P = TX + 1;
-    uint8_t *mk = s.mask + (size_t)v * cams.T;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = SAT_THREADS / 32;
+    uint8_t *mkg = s.mask + (size_t)v * cams.T;
     int *Sg = s.sat + (size_t)v * (TY + 1) * P;
     int *S = SMEM ? sm_sat : Sg;
+    uint8_t *mk = SMEM ? reinterpret_cast<uint8_t *>(sm_sat + (TY + 1) * P) : mkg;
     if (!all_tiles) {
         const int *D = s.mdiff + (size_t)v * (TY + 1) * P;
         for (int k = threadIdx.x; k < (TY + 1) * P; k += blockDim.x) S[k] = D[k];
         __syncthreads();
-        for (int y = threadIdx.x; y < TY; y += blockDim.x) {   // row prefix
-            int acc = 0;
-            for (int x = 0; x < TX; x++) {
-                acc += S[y * P + x];
-                S[y * P + x] = acc;
-            }
-        }
+        for (int y = warp; y < TY; y += nw) warp_prefix(S + y * P, TX, 1);   // row prefix
         __syncthreads();
-        for (int x = threadIdx.x; x < TX; x += blockDim.x) {   // column prefix -> mask
-            int acc = 0;
-            for (int y = 0; y < TY; y++) {
-                acc += S[y * P + x];
-                mk[y * TX + x] = acc > 0 ? 1 : 0;
-            }
-        }
+        for (int x = warp; x < TX; x += nw) warp_prefix(S + x, TY, P);       // column prefix
         __syncthreads();
-    }
-    // summed-area table of the mask: S[(y+1) P + x + 1] = active tiles in [0, x] x [0, y]
-    for (int x = threadIdx.x; x < P; x += blockDim.x) S[x] = 0;
-    for (int y = threadIdx.x; y < TY; y += blockDim.x) {
-        int acc = 0;
-        S[(y + 1) * P] = 0;
-        for (int x = 0; x < TX; x++) {
-            acc += mk[y * TX + x];
-            S[(y + 1) * P + x + 1] = acc;
+        for (int t = threadIdx.x; t < TX * TY; t += blockDim.x) {
+            const uint8_t m = S[(t / TX) * P + t % TX] > 0 ? 1 : 0;
+            mk[t] = m;
+            if (SMEM) mkg[t] = m;
         }
+    } else if (SMEM) {
+        for (int t = threadIdx.x; t < TX * TY; t += blockDim.x) mk[t] = mkg[t];
     }
     __syncthreads();
-    for (int x = threadIdx.x; x < P; x += blockDim.x) {
-        int acc = 0;
-        for (int y = 1; y <= TY; y++) {
-            acc += S[y * P + x];
-            S[y * P + x] = acc;
-        }
+    // summed-area table of the mask: S[(y+1) P + x + 1] = active tiles in [0, x] x [0, y]
+    for (int k = threadIdx.x; k < (TY + 1) * P; k += blockDim.x) {
+        const int y = k / P, x = k - y * P;
+        S[k] = (y > 0 && x > 0) ? mk[(y - 1) * TX + x - 1] : 0;
     }
+    __syncthreads();
+    for (int y = warp; y < TY; y += nw) warp_prefix(S + (y + 1) * P + 1, TX, 1);
+    __syncthreads();
+    for (int x = warp; x < TX; x += nw) warp_prefix(S + P + x + 1, TY, P);
     __syncthreads();
     if (SMEM)
         for (int k = threadIdx.x; k < (TY + 1) * P; k += blockDim.x) Sg[k] = S[k];
@@ -171,29 +181,20 @@ __global__ void __launch_bounds__(256) k_sat(const __grid_constant__ CamSet cams
     __shared__ int s_bb[4];
     if (threadIdx.x == 0) { s_bb[0] = TX; s_bb[1] = TY; s_bb[2] = 0; s_bb[3] = 0; }
     __syncthreads();
-    {
-        int x0 = TX, y0 = TY, x1 = 0, y1 = 0;
-        for (int t = threadIdx.x; t < TX * TY; t += blockDim.x)
-            if (mk[t]) {
-                const int x = t % TX, y = t / TX;
-                x0 = min(x0, x); y0 = min(y0, y); x1 = max(x1, x + 1); y1 = max(y1, y + 1);
-            }
-        atomicMin(&s_bb[0], x0); atomicMin(&s_bb[1], y0); atomicMax(&s_bb[2], x1); atomicMax(&s_bb[3], y1);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) s.view_bbox[v] = make_int4(s_bb[0], s_bb[1], s_bb[2], s_bb[3]);
-    // row bitmasks of the active tiles (projection pass A)
+    // row bitmasks of the active tiles (projection pass A): one ballot per 32 tiles of a row
     const int W32 = (TX + 31) >> 5;
     unsigned *rm = s.rowmask + (size_t)v * TY * W32;
-    for (int k = threadIdx.x; k < TY * W32; k += blockDim.x) {
-        const int y = k / W32, w = k % W32;
-        unsigned bits = 0u;
-        for (int b = 0; b < 32; b++) {
-            const int x = w * 32 + b;
-            if (x < TX && mk[y * TX + x]) bits |= 1u << b;
-        }
-        rm[k] = bits;
+    int x0 = TX, y0 = TY, x1 = 0, y1 = 0;
+    for (int k = warp; k < TY * W32; k += nw) {
+        const int y = k / W32, x = (k % W32) * 32 + lane;
+        const bool m = x < TX && mk[y * TX + x];
+        const unsigned bits = __ballot_sync(0xffffffffu, m);
+        if (lane == 0) rm[k] = bits;
+        if (m) { x0 = min(x0, x); y0 = min(y0, y); x1 = max(x1, x + 1); y1 = max(y1, y + 1); }
     }
+    atomicMin(&s_bb[0], x0); atomicMin(&s_bb[1], y0); atomicMax(&s_bb[2], x1); atomicMax(&s_bb[3], y1);
+    __syncthreads();
+    if (threadIdx.x == 0) s.view_bbox[v] = make_int4(s_bb[0], s_bb[1], s_bb[2], s_bb[3]);
 }
 
 void launch_active_mask(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st)
@@ -207,9 +208,14 @@ void launch_active_mask(const Params &g, const StepDims &d, const CamSet &cams, 
         k_active_rects<<<blocks, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, cams, s);
         g_launches++;
     }
-    const size_t smem = sizeof(int) * (size_t)(d.TY + 1) * (d.TX + 1);
-    if (smem <= 48 * 1024) k_sat<true><<<d.V, 256, smem, st>>>(cams, s, d.all_tiles);
-    else k_sat<false><<<d.V, 256, 0, st>>>(cams, s, d.all_tiles);
+    const size_t smem = sizeof(int) * (size_t)(d.TY + 1) * (d.TX + 1) + (size_t)d.TX * d.TY;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_sat<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    if (smem <= 200 * 1024) k_sat<true><<<d.V, SAT_THREADS, smem, st>>>(cams, s, d.all_tiles);
+    else k_sat<false><<<d.V, SAT_THREADS, 0, st>>>(cams, s, d.all_tiles);
     g_launches++;
 }
 
