@@ -527,6 +527,37 @@ void launch_loss(const Scratch &s, float loss_scale, float *loss, cudaStream_t s
 // added into grad2d[v][ordinal] with float4 atomics.  Frozen entries only update T and S.
 // The alpha of every (pixel, entry) is recomputed with exactly the forward's operations.
 // ---------------------------------------------------------------------------
+// reduce-scatter over a warp of 9 per-lane values (padded to 16); returns, in lane l, the warp total
+// of value (l >> 1) & 15 (values 9..15 are zero)
+__device__ __forceinline__ float warp_reduce_scatter9(const float (&r)[9], int lane)
+{
+    float a8[8];
+    const bool b4 = lane & 16;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+        const float lo = r[j], hi = j + 8 < 9 ? r[j + 8] : 0.f;
+        const float recv = __shfl_xor_sync(0xffffffffu, b4 ? lo : hi, 16);
+        a8[j] = (b4 ? hi : lo) + recv;
+    }
+    float a4[4];
+    const bool b3 = lane & 8;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        const float recv = __shfl_xor_sync(0xffffffffu, b3 ? a8[j] : a8[j + 4], 8);
+        a4[j] = (b3 ? a8[j + 4] : a8[j]) + recv;
+    }
+    float a2[2];
+    const bool b2 = lane & 4;
+#pragma unroll
+    for (int j = 0; j < 2; j++) {
+        const float recv = __shfl_xor_sync(0xffffffffu, b2 ? a4[j] : a4[j + 2], 4);
+        a2[j] = (b2 ? a4[j + 2] : a4[j]) + recv;
+    }
+    const bool b1 = lane & 2;
+    float a1 = (b1 ? a2[1] : a2[0]) + __shfl_xor_sync(0xffffffffu, b1 ? a2[0] : a2[1], 2);
+    return a1 + __shfl_xor_sync(0xffffffffu, a1, 1);
+}
+
 struct PixB {   // backward state of one pixel
     float T, Tf, S0, S1, S2, g0, g1, g2;
     int last;
@@ -601,6 +632,10 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
                 const int ordk = __float_as_int(Cc.w);
                 const bool active = ordk >= 0;   // uniform over the CTA
                 const float sx = __fmaf_rn(-Aa.y, flx, Aa.x), txx = __fmaf_rn(-Bb.x, flx, Aa.w);
+                // the entry's conic (a, b, c) / kappa and tile-local mean (per entry, not per pixel)
+                const float ca = (Aa.y * Aa.y + Bb.x * Bb.x) * ik, cb = (Aa.y * Aa.z + Bb.x * Bb.y) * ik,
+                            cc = (Aa.z * Aa.z + Bb.y * Bb.y) * ik;
+                const float2 d0 = sd[k];
                 float r[9];
 #pragma unroll
                 for (int q = 0; q < 9; q++) r[q] = 0.f;
@@ -615,11 +650,11 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
                     const float alpha = alpha_of(qk, Bb.z, G);
                     if (alpha < (1.0f / 255.0f)) continue;
                     const float omi = __fsub_rn(1.0f, alpha);
-                    P[p].T = __fdiv_rn(P[p].T, omi);   // transmittance in front of entry jj
+                    const float inv = __frcp_rn(omi);   // one rounded reciprocal for T and dL/dalpha
+                    P[p].T = P[p].T * inv;              // transmittance in front of entry jj
                     const float w = alpha * P[p].T;
                     if (active) {
                         any = true;
-                        const float inv = 1.0f / omi;
                         const float dLda = P[p].g0 * (Cc.x * P[p].T - (P[p].S0 + P[p].Tf * bg.x) * inv) +
                                            P[p].g1 * (Cc.y * P[p].T - (P[p].S1 + P[p].Tf * bg.y) * inv) +
                                            P[p].g2 * (Cc.z * P[p].T - (P[p].S2 + P[p].Tf * bg.z) * inv);
@@ -629,10 +664,7 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
                         if (Bb.z * G < 0.99f) {
                             const float dLdp = alpha * dLda;
                             r[5] += G * dLda;
-                            const float2 d0 = sd[k];
                             const float dx = d0.x - flx, dy = d0.y - (float)(ly + 4 * p);
-                            const float ca = (Aa.y * Aa.y + Bb.x * Bb.x) * ik, cb = (Aa.y * Aa.z + Bb.x * Bb.y) * ik,
-                                        cc = (Aa.z * Aa.z + Bb.y * Bb.y) * ik;
                             r[0] += -dLdp * (ca * dx + cb * dy);
                             r[1] += -dLdp * (cb * dx + cc * dy);
                             r[2] += -0.5f * dLdp * dx * dx;
@@ -645,18 +677,13 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
                     P[p].S2 += Cc.z * w;
                 }
                 if (active && __any_sync(0xffffffffu, any)) {
-#pragma unroll
-                    for (int q = 0; q < 9; q++) {
-                        float a = r[q];
-                        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-                        r[q] = a;
-                    }
-                    if (lane == 0) {
-                        float4 *gp = gbase + (size_t)ordk * 3;
-                        atomicAdd(gp, make_float4(r[0], r[1], r[2], r[3]));
-                        atomicAdd(gp + 1, make_float4(r[4], r[5], r[6], r[7]));
-                        atomicAdd(gp + 2, make_float4(r[8], 0.f, 0.f, 0.f));
-                    }
+                    // warp reduce-scatter of the 9 sums (padded to 16): at each butterfly level a
+                    // lane keeps half of its values and receives its partner's copy of that half, so
+                    // 16 shuffles replace 9 x 5; lane l ends with the total of value l >> 1
+                    const float tot = warp_reduce_scatter9(r, lane);
+                    const int q = lane >> 1;
+                    if ((lane & 1) == 0 && q < 9)
+                        atomicAdd(reinterpret_cast<float *>(gbase + (size_t)ordk * 3) + q, tot);
                 }
             }
         }
