@@ -163,6 +163,30 @@ __device__ __forceinline__ float tmax4(unsigned long long p, unsigned long long 
     return fmaxf(fmaxf(a, b), fmaxf(c, d));
 }
 
+// packed fp32x2 arithmetic (FFMA2 / FMUL2 / FADD2: IEEE round-to-nearest per lane)
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t bc2(float x) { return pack2(x, x); }
+__device__ __forceinline__ f2_t fma2(f2_t a, f2_t b, f2_t c)
+{
+    f2_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ f2_t mul2(f2_t a, f2_t b)
+{
+    f2_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f2_t add2(f2_t a, f2_t b)
+{
+    f2_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ float lo2(f2_t a) { float x, y; unpack2(a, x, y); return x; }
+__device__ __forceinline__ float hi2(f2_t a) { float x, y; unpack2(a, x, y); return y; }
+
 // ---------------------------------------------------------------------------
 // Forward compositing of one staged entry into a PAIR of pixels (same column, rows fy.x, fy.y).
 // sm_100 has packed fp32x2 FMA/MUL (FFMA2/FMUL2, IEEE RN per lane: bit-identical to the scalar
@@ -558,11 +582,6 @@ __device__ __forceinline__ float warp_reduce_scatter9(const float (&r)[9], int l
     return a1 + __shfl_xor_sync(0xffffffffu, a1, 1);
 }
 
-struct PixB {   // backward state of one pixel
-    float T, Tf, S0, S1, S2, g0, g1, g2;
-    int last;
-};
-
 __global__ void __launch_bounds__(RT_THREADS)
 k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ dL_dimg, float3 bg)
 {
@@ -592,101 +611,170 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         const int tx = t % TX, ty = t / TX;
         const int first = s.first_active[item];   // segment position of the first active entry (fwd)
         const int x = tx * CLS_TILE + lx;
-        PixB P[RT_PX];
+        // per-pixel state as fp32x2 pairs over the pixel pairs (p0, p1), (p2, p3) -- rows ly + 4p
+        f2_t Tp[2], Tfp[2], S0[2], S1[2], S2[2], G0[2], G1[2], G2[2];
+        int last[RT_PX];
         int ml = -1;
 #pragma unroll
-        for (int p = 0; p < RT_PX; p++) {
-            const int yy = ty * CLS_TILE + ly + 4 * p;
-            const int pl = tid + p * RT_THREADS;
-            const size_t px = (size_t)item * CLS_BLOCK_PIX + pl;
-            const bool in = x < W && yy < H;
-            P[p].last = in ? s.px_last[px] : -1;
-            P[p].Tf = s.px_T[px];
-            P[p].T = P[p].Tf;
-            P[p].S0 = P[p].S1 = P[p].S2 = 0.f;
-            P[p].g0 = P[p].g1 = P[p].g2 = 0.f;
-            if (in) {
-                if (dL_dimg) {
-                    const size_t HW = (size_t)H * W;
-                    const size_t pix = (size_t)v * 3 * HW + (size_t)yy * W + x;
-                    P[p].g0 = dL_dimg[pix]; P[p].g1 = dL_dimg[pix + HW]; P[p].g2 = dL_dimg[pix + 2 * HW];
-                } else {
-                    const float *dl = s.px_dl + (size_t)item * 3 * CLS_BLOCK_PIX + pl;
-                    P[p].g0 = dl[0]; P[p].g1 = dl[CLS_BLOCK_PIX]; P[p].g2 = dl[2 * CLS_BLOCK_PIX];
+        for (int h = 0; h < 2; h++) {
+            float tf[2], g0[2] = {0.f, 0.f}, g1[2] = {0.f, 0.f}, g2[2] = {0.f, 0.f};
+#pragma unroll
+            for (int j = 0; j < 2; j++) {
+                const int p = 2 * h + j;
+                const int yy = ty * CLS_TILE + ly + 4 * p;
+                const int pl = tid + p * RT_THREADS;
+                const size_t px = (size_t)item * CLS_BLOCK_PIX + pl;
+                const bool in = x < W && yy < H;
+                last[p] = in ? s.px_last[px] : -1;
+                tf[j] = s.px_T[px];
+                if (in) {
+                    if (dL_dimg) {
+                        const size_t HW = (size_t)H * W;
+                        const size_t pix = (size_t)v * 3 * HW + (size_t)yy * W + x;
+                        g0[j] = dL_dimg[pix]; g1[j] = dL_dimg[pix + HW]; g2[j] = dL_dimg[pix + 2 * HW];
+                    } else {
+                        const float *dl = s.px_dl + (size_t)item * 3 * CLS_BLOCK_PIX + pl;
+                        g0[j] = dl[0]; g1[j] = dl[CLS_BLOCK_PIX]; g2[j] = dl[2 * CLS_BLOCK_PIX];
+                    }
                 }
+                ml = max(ml, last[p]);
             }
-            ml = max(ml, P[p].last);
+            Tfp[h] = pack2(tf[0], tf[1]);
+            Tp[h] = Tfp[h];
+            S0[h] = S1[h] = S2[h] = 0ull;   // +0.0f pairs
+            G0[h] = pack2(g0[0], g0[1]); G1[h] = pack2(g1[0], g1[1]); G2[h] = pack2(g2[0], g2[1]);
+        }
+        // the colour behind starts with the background: X_ch = S_ch + T_final bg_ch is what dL/dalpha
+        // needs; it is kept directly (X_ch += c_ch w instead of S_ch += c_ch w)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            S0[h] = mul2(Tfp[h], bc2(bg.x));
+            S1[h] = mul2(Tfp[h], bc2(bg.y));
+            S2[h] = mul2(Tfp[h], bc2(bg.z));
         }
         if (ml >= first) atomicMax(&s_maxlast, ml);
         __syncthreads();
         const int end = s_maxlast + 1;   // exclusive
         float4 *gbase = s.grad2d + (size_t)v * A * 3;
+        const f2_t fyp[2] = {pack2((float)ly, (float)(ly + 4)), pack2((float)(ly + 8), (float)(ly + 12))};
         // reverse walk over the row segment [first, end): batches of covering units, descending
         int cur = end;
         while (cur > first) {
             __syncthreads();
             const int cnt = fill_batch<-1, true>(s, cur, first, tx, ty, ent, sd, s_pos, s_rid, s_wc, &s_next, nullptr, nullptr);
+            // walked (pixel, entry) pairs of this batch: s_pos is descending, so the entries above a
+            // pixel's last composited one form a prefix (binary search per pixel)
+#pragma unroll
+            for (int p = 0; p < RT_PX; p++) {
+                int lo = 0, hi = cnt;   // first k with s_pos[k] <= last[p]
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (s_pos[mid] > last[p]) lo = mid + 1;
+                    else hi = mid;
+                }
+                evals += (unsigned long long)(cnt - lo);
+            }
             for (int k = 0; k < cnt; k++) {
                 const int jj = s_pos[k];
                 const float4 Aa = ent[3 * k], Bb = ent[3 * k + 1], Cc = ent[3 * k + 2];
                 const int ordk = __float_as_int(Cc.w);
                 const bool active = ordk >= 0;   // uniform over the CTA
                 const float sx = __fmaf_rn(-Aa.y, flx, Aa.x), txx = __fmaf_rn(-Bb.x, flx, Aa.w);
-                // the entry's conic (a, b, c) / kappa and tile-local mean (per entry, not per pixel)
+                const float o = Bb.z;
+                if (!active) {
+                    // frozen entry: only T and the colour behind change (branch-free, per pixel pair)
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        const f2_t sp = fma2(bc2(-Aa.z), fyp[h], bc2(sx)), tp = fma2(bc2(-Bb.y), fyp[h], bc2(txx));
+                        const f2_t q = fma2(sp, sp, mul2(tp, tp));
+                        float al[2], in_[2];
+                        bool hit[2];
+#pragma unroll
+                        for (int j = 0; j < 2; j++) {
+                            float e;
+                            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-(j ? hi2(q) : lo2(q))));
+                            al[j] = fminf(0.99f, __fmul_rn(o, e));   // the forward's alpha, same operations
+                            hit[j] = jj <= last[2 * h + j] && al[j] >= (1.0f / 255.0f);
+                            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(in_[j]) : "f"(__fsub_rn(1.0f, al[j])));
+                        }
+                        const f2_t Tn = mul2(Tp[h], pack2(in_[0], in_[1]));   // transmittance in front of the entry
+                        float t0, t1, n0, n1;
+                        unpack2(Tp[h], t0, t1);
+                        unpack2(Tn, n0, n1);
+                        Tp[h] = pack2(hit[0] ? n0 : t0, hit[1] ? n1 : t1);
+                        const f2_t w = mul2(pack2(hit[0] ? al[0] : 0.f, hit[1] ? al[1] : 0.f), Tp[h]);
+                        S0[h] = fma2(bc2(Cc.x), w, S0[h]);
+                        S1[h] = fma2(bc2(Cc.y), w, S1[h]);
+                        S2[h] = fma2(bc2(Cc.z), w, S2[h]);
+                    }
+                    continue;
+                }
+                // active entry: the gradient terms too (positive partial sums, signs applied once)
                 const float ca = (Aa.y * Aa.y + Bb.x * Bb.x) * ik, cb = (Aa.y * Aa.z + Bb.x * Bb.y) * ik,
                             cc = (Aa.z * Aa.z + Bb.y * Bb.y) * ik;
                 const float2 d0 = sd[k];
-                float r[9];
+                const float dx = d0.x - flx;
+                f2_t R[9];
 #pragma unroll
-                for (int q = 0; q < 9; q++) r[q] = 0.f;
+                for (int qq = 0; qq < 9; qq++) R[qq] = 0ull;
                 bool any = false;
 #pragma unroll
-                for (int p = 0; p < RT_PX; p++) {
-                    if (jj > P[p].last) continue;
-                    ++evals;
-                    float ss, tt;
-                    const float qk = raster_q(sx, txx, Aa.z, Bb.y, (float)(ly + 4 * p), ss, tt);
-                    float G;   // same operations as the forward (no pre-test there either)
-                    const float alpha = alpha_of(qk, Bb.z, G);
-                    if (alpha < (1.0f / 255.0f)) continue;
-                    const float omi = __fsub_rn(1.0f, alpha);
-                    // one reciprocal (MUFU, ~1 ulp) for T and dL/dalpha: the reconstructed T drifts by
-                    // ~1e-7 per entry, far inside the 1e-3 gradient tolerance; omi >= 0.01
-                    float inv;
-                    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(omi));
-                    P[p].T = P[p].T * inv;              // transmittance in front of entry jj
-                    const float w = alpha * P[p].T;
-                    if (active) {
-                        any = true;
-                        const float dLda = P[p].g0 * (Cc.x * P[p].T - (P[p].S0 + P[p].Tf * bg.x) * inv) +
-                                           P[p].g1 * (Cc.y * P[p].T - (P[p].S1 + P[p].Tf * bg.y) * inv) +
-                                           P[p].g2 * (Cc.z * P[p].T - (P[p].S2 + P[p].Tf * bg.z) * inv);
-                        r[6] += w * P[p].g0;
-                        r[7] += w * P[p].g1;
-                        r[8] += w * P[p].g2;
-                        if (Bb.z * G < 0.99f) {
-                            const float dLdp = alpha * dLda;
-                            r[5] += G * dLda;
-                            const float dx = d0.x - flx, dy = d0.y - (float)(ly + 4 * p);
-                            r[0] += -dLdp * (ca * dx + cb * dy);
-                            r[1] += -dLdp * (cb * dx + cc * dy);
-                            r[2] += -0.5f * dLdp * dx * dx;
-                            r[3] += -dLdp * dx * dy;
-                            r[4] += -0.5f * dLdp * dy * dy;
-                        }
+                for (int h = 0; h < 2; h++) {
+                    const f2_t sp = fma2(bc2(-Aa.z), fyp[h], bc2(sx)), tp = fma2(bc2(-Bb.y), fyp[h], bc2(txx));
+                    const f2_t q = fma2(sp, sp, mul2(tp, tp));
+                    float al[2], in_[2], Gv[2], ninv[2];
+                    bool hit[2], geo[2];
+#pragma unroll
+                    for (int j = 0; j < 2; j++) {
+                        float e;
+                        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-(j ? hi2(q) : lo2(q))));
+                        Gv[j] = e;
+                        al[j] = fminf(0.99f, __fmul_rn(o, e));
+                        hit[j] = jj <= last[2 * h + j] && al[j] >= (1.0f / 255.0f);
+                        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(in_[j]) : "f"(__fsub_rn(1.0f, al[j])));
+                        ninv[j] = -in_[j];
+                        geo[j] = hit[j] && o * e < 0.99f;   // R4: the clamp does not bind
+                        any |= hit[j];
                     }
-                    P[p].S0 += Cc.x * w;
-                    P[p].S1 += Cc.y * w;
-                    P[p].S2 += Cc.z * w;
+                    const f2_t Tn = mul2(Tp[h], pack2(in_[0], in_[1]));
+                    float t0, t1, n0, n1;
+                    unpack2(Tp[h], t0, t1);
+                    unpack2(Tn, n0, n1);
+                    Tp[h] = pack2(hit[0] ? n0 : t0, hit[1] ? n1 : t1);
+                    const f2_t am = pack2(hit[0] ? al[0] : 0.f, hit[1] ? al[1] : 0.f);
+                    const f2_t w = mul2(am, Tp[h]);
+                    // dL/dalpha = T (sum_ch g_ch c_ch) - (sum_ch g_ch X_ch) / (1 - alpha), X = S + T_f bg
+                    const f2_t gc = fma2(G2[h], bc2(Cc.z), fma2(G1[h], bc2(Cc.y), mul2(G0[h], bc2(Cc.x))));
+                    const f2_t gx = fma2(G2[h], S2[h], fma2(G1[h], S1[h], mul2(G0[h], S0[h])));
+                    const f2_t dLda = fma2(Tp[h], gc, mul2(gx, pack2(ninv[0], ninv[1])));
+                    R[6] = fma2(w, G0[h], R[6]);
+                    R[7] = fma2(w, G1[h], R[7]);
+                    R[8] = fma2(w, G2[h], R[8]);
+                    float d0l, d0h;
+                    unpack2(dLda, d0l, d0h);
+                    const f2_t dg = pack2(geo[0] ? d0l : 0.f, geo[1] ? d0h : 0.f);   // dL/dalpha where R4 holds
+                    R[5] = fma2(pack2(Gv[0], Gv[1]), dg, R[5]);
+                    const f2_t dLdp = mul2(pack2(al[0], al[1]), dg);
+                    const f2_t dy = add2(bc2(d0.y), mul2(fyp[h], bc2(-1.0f)));
+                    R[0] = fma2(dLdp, fma2(bc2(cb), dy, bc2(ca * dx)), R[0]);
+                    R[1] = fma2(dLdp, fma2(bc2(cc), dy, bc2(cb * dx)), R[1]);
+                    R[2] = fma2(dLdp, bc2(dx * dx), R[2]);
+                    R[3] = fma2(dLdp, mul2(bc2(dx), dy), R[3]);
+                    R[4] = fma2(dLdp, mul2(dy, dy), R[4]);
+                    S0[h] = fma2(bc2(Cc.x), w, S0[h]);
+                    S1[h] = fma2(bc2(Cc.y), w, S1[h]);
+                    S2[h] = fma2(bc2(Cc.z), w, S2[h]);
                 }
-                if (active && __any_sync(0xffffffffu, any)) {
-                    // warp reduce-scatter of the 9 sums (padded to 16): at each butterfly level a
-                    // lane keeps half of its values and receives its partner's copy of that half, so
-                    // 16 shuffles replace 9 x 5; lane l ends with the total of value l >> 1
+                if (__any_sync(0xffffffffu, any)) {
+                    float r[9];
+#pragma unroll
+                    for (int qq = 0; qq < 9; qq++) r[qq] = lo2(R[qq]) + hi2(R[qq]);
+                    r[0] = -r[0]; r[1] = -r[1]; r[2] *= -0.5f; r[3] = -r[3]; r[4] *= -0.5f;
+                    // warp reduce-scatter of the 9 sums (padded to 16): lane l ends with value l >> 1
                     const float tot = warp_reduce_scatter9(r, lane);
-                    const int q = lane >> 1;
-                    if ((lane & 1) == 0 && q < 9)
-                        atomicAdd(reinterpret_cast<float *>(gbase + (size_t)ordk * 3) + q, tot);
+                    const int qi = lane >> 1;
+                    if ((lane & 1) == 0 && qi < 9)
+                        atomicAdd(reinterpret_cast<float *>(gbase + (size_t)ordk * 3) + qi, tot);
                 }
             }
         }
