@@ -8,10 +8,12 @@
 // ACTIVE (view, tile) work items from a device queue.  Each CTA stages its tile's
 // depth-ordered Gaussians in shared memory 128 at a time, forming the exponent's
 // tile-origin terms in fp64 once per (tile, Gaussian) from the record's hi/lo 2D mean
-// (H1, reading R29), and composites front to back (R1-R3) with ~20 fp32
-// instructions per (pixel, Gaussian).  Frozen Gaussians are composited but never differentiated: the
-// backward walk updates T and the colour-behind sum for them, and only ACTIVE entries
-// run the gradient math and the warp-reduced atomics.
+// (H1, reading R29), and composites front to back (R1-R3).  The two pixels of a
+// thread that share a column are processed as one packed fp32x2 pair (FFMA2/FMUL2, bit-identical
+// to the scalar operations), with the per-pixel decisions as predicates: ~13 instructions per
+// (pixel, Gaussian).  Frozen Gaussians are composited but never differentiated: the backward walk
+// updates T and the colour-behind sum for them, and only ACTIVE entries run the
+// gradient math and the warp-reduced atomics.
 #include "kernels.h"
 
 namespace cls {
@@ -134,15 +136,6 @@ __device__ __forceinline__ int fill_batch(const Scratch &s, int &cur, int end, i
     }
     __syncthreads();
     return nst;
-}
-
-// alpha = min(0.99, o 2^-q') of a (pixel, Gaussian) with q' <= qcut'; G = 2^-q' = exp(-q/2)
-__device__ __forceinline__ float alpha_of(float qk, float o, float &G)
-{
-    float e;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-qk));
-    G = e;
-    return fminf(0.99f, __fmul_rn(o, e));
 }
 
 __device__ __forceinline__ unsigned long long pack2(float a, float b)
