@@ -254,8 +254,9 @@ __device__ __forceinline__ void quat_rot(double w, double x, double y, double z,
 __device__ __forceinline__ void gauss_m64(const float4 q, const float4 ls, double M[9])
 {
     double qw = q.x, qx = q.y, qy = q.z, qz = q.w;
-    double qn = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
-    qw /= qn; qx /= qn; qy /= qn; qz /= qn;
+    // shared divisors as one reciprocal + products (<= 2 ulp from the quotients, R37)
+    const double iqn = 1.0 / sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+    qw *= iqn; qx *= iqn; qy *= iqn; qz *= iqn;
     double Rq[9];
     quat_rot(qw, qx, qy, qz, Rq);
     double s0 = exp((double)ls.x), s1 = exp((double)ls.y), s2 = exp((double)ls.z);
@@ -276,12 +277,13 @@ __device__ __forceinline__ bool project_view(const float4 mo, const double M[9],
     // J with the frustum clamp (R10)
     const double fx = c.fx, fy = c.fy;
     const double limx = 1.3 * ((double)W / (2.0 * fx)), limy = 1.3 * ((double)H / (2.0 * fy));
-    double xz = p.tx / p.tz, yz = p.ty / p.tz;
+    const double itz = 1.0 / p.tz, itz2 = itz * itz;
+    double xz = p.tx * itz, yz = p.ty * itz;
     xz = fmin(fmax(xz, -limx), limx);
     yz = fmin(fmax(yz, -limy), limy);
     const double xt = xz * p.tz, yt = yz * p.tz;
-    const double j00 = fx / p.tz, j02 = -(fx * xt) / (p.tz * p.tz);
-    const double j11 = fy / p.tz, j12 = -(fy * yt) / (p.tz * p.tz);
+    const double j00 = fx * itz, j02 = -(fx * xt) * itz2;
+    const double j11 = fy * itz, j12 = -(fy * yt) * itz2;
     // T = J W (2x3); then V = T M (2x3); Sigma' = V V^T + 0.3 I
     double T0[3], T1[3];
     for (int b = 0; b < 3; b++) {
@@ -298,15 +300,16 @@ __device__ __forceinline__ bool project_view(const float4 mo, const double M[9],
     p.C = V1[0] * V1[0] + V1[1] * V1[1] + V1[2] * V1[2] + 0.3;
     const double det = p.A * p.C - p.B * p.B;
     if (!(det > 0.0)) return false;
-    p.ca = p.C / det;
-    p.cb = -p.B / det;
-    p.cc = p.A / det;
+    const double idet = 1.0 / det;
+    p.ca = p.C * idet;
+    p.cb = -p.B * idet;
+    p.cc = p.A * idet;
     const double mid = 0.5 * (p.A + p.C);
     const double disc = mid * mid - det;
     const double lam = mid + sqrt(disc > 0.1 ? disc : 0.1);
     p.radius = (int)ceil(3.0 * sqrt(lam));
-    p.u = fx * p.tx / p.tz + (double)c.cx - 0.5;
-    p.v = fy * p.ty / p.tz + (double)c.cy - 0.5;
+    p.u = fx * p.tx * itz + (double)c.cx - 0.5;
+    p.v = fy * p.ty * itz + (double)c.cy - 0.5;
     const double r = (double)p.radius;
     int x0 = (int)((p.u - r) / CLS_TILE), y0 = (int)((p.v - r) / CLS_TILE);
     int x1 = (int)((p.u + r + CLS_TILE - 1) / CLS_TILE), y1 = (int)((p.v + r + CLS_TILE - 1) / CLS_TILE);
