@@ -266,7 +266,13 @@ __device__ __forceinline__ void gauss_m64(const float4 q, const float4 ls, doubl
 }
 
 // the view-dependent part; returns false if culled (near plane, det <= 0, empty rect)
-__device__ __forceinline__ bool project_view(const float4 mo, const double M[9], const GCam &c, int W, int H, int TX,
+// frustum-clamp limits of a view (R10): 1.3 (W / 2 fx), 1.3 (H / 2 fy), view constants
+__device__ __forceinline__ double2 view_lims(const GCam &c, int W, int H)
+{
+    return make_double2(1.3 * ((double)W / (2.0 * (double)c.fx)), 1.3 * ((double)H / (2.0 * (double)c.fy)));
+}
+
+__device__ __forceinline__ bool project_view(const float4 mo, const double M[9], const GCam &c, double2 lims, int TX,
                                              int TY, Proj &p)
 {
     const double mx = mo.x, my = mo.y, mz = mo.z;
@@ -276,7 +282,7 @@ __device__ __forceinline__ bool project_view(const float4 mo, const double M[9],
     if (!(p.tz > 0.2)) return false;
     // J with the frustum clamp (R10)
     const double fx = c.fx, fy = c.fy;
-    const double limx = 1.3 * ((double)W / (2.0 * fx)), limy = 1.3 * ((double)H / (2.0 * fy));
+    const double limx = lims.x, limy = lims.y;
     const double itz = 1.0 / p.tz, itz2 = itz * itz;
     double xz = p.tx * itz, yz = p.ty * itz;
     xz = fmin(fmax(xz, -limx), limx);
@@ -323,7 +329,7 @@ __device__ __forceinline__ bool project_gaussian(const float4 mo, const float4 q
 {
     double M[9];
     gauss_m64(q, ls, M);
-    return project_view(mo, M, c, W, H, TX, TY, p);
+    return project_view(mo, M, c, view_lims(c, W, H), TX, TY, p);
 }
 
 // number of active tiles in [x0,x1) x [y0,y1) from a summed-area table with row pitch TX+1

@@ -393,12 +393,14 @@ k_project_exact(const float4 *__restrict__ mean_op, const float4 *__restrict__ q
                 const __grid_constant__ CamSet cams, Scratch s)
 {
     __shared__ GCam s_cams[CLS_MAX_VIEWS];   // lanes index different views: no constant-bank serialisation
+    __shared__ double2 s_lims[CLS_MAX_VIEWS];   // per-view frustum-clamp limits (view constants)
     for (int k = threadIdx.x; k < cams.n * (int)(sizeof(GCam) / 4); k += blockDim.x)
         reinterpret_cast<float *>(s_cams)[k] = reinterpret_cast<const float *>(cams.c)[k];
+    for (int k = threadIdx.x; k < cams.n; k += blockDim.x) s_lims[k] = view_lims(cams.c[k], cams.W, cams.H);
     __syncthreads();
     const int ncand = min(s.cnt->n_cand, (int)s.max_cand);
     const int lane = threadIdx.x & 31;
-    const int W = cams.W, H = cams.H, TX = cams.TX, TY = cams.TY, P = TX + 1;
+    const int TX = cams.TX, TY = cams.TY, P = TX + 1;
     for (int base_e = blockIdx.x * blockDim.x; base_e < ncand; base_e += gridDim.x * blockDim.x) {
         const int e = base_e + threadIdx.x;
         bool keep = false;
@@ -411,7 +413,9 @@ k_project_exact(const float4 *__restrict__ mean_op, const float4 *__restrict__ q
             i = cv.x;
             v = cv.y;
             mo = __ldg(mean_op + i);
-            if (project_gaussian(mo, __ldg(quat + i), __ldg(log_scale + i), s_cams[v], W, H, TX, TY, p)) {
+            double M[9];
+            gauss_m64(__ldg(quat + i), __ldg(log_scale + i), M);
+            if (project_view(mo, M, s_cams[v], s_lims[v], TX, TY, p)) {
                 // emission rect = 3-sigma rect (support, R8) n bounding box of the alpha >= 1/255
                 // footprint (exact culling: outside it every pixel has alpha < 1/255)
                 o64 = 1.0 / (1.0 + exp(-(double)mo.w));
@@ -456,11 +460,11 @@ k_project_exact(const float4 *__restrict__ mean_op, const float4 *__restrict__ q
         // diagonal conic entry; conic a = C/det >= c = A/det  <=>  C >= A
         double a1, a2, b1, b2;
         if (p.C >= p.A) {   // pivot x: beta = b/a = -B/C, gamma = 1/C
-            const double k = sqrt(CLS_KAPPA * p.ca);
-            a1 = k; a2 = k * (-p.B / p.C); b1 = 0.0; b2 = sqrt(CLS_KAPPA / p.C);
+            const double k = sqrt(CLS_KAPPA * p.ca), iC = 1.0 / p.C;   // one reciprocal (R37)
+            a1 = k; a2 = k * (-p.B * iC); b1 = 0.0; b2 = sqrt(CLS_KAPPA * iC);
         } else {            // pivot y: beta = b/c = -B/A, gamma = 1/A
-            const double k = sqrt(CLS_KAPPA * p.cc);
-            a1 = k * (-p.B / p.A); a2 = k; b1 = sqrt(CLS_KAPPA / p.A); b2 = 0.0;
+            const double k = sqrt(CLS_KAPPA * p.cc), iA = 1.0 / p.A;
+            a1 = k * (-p.B * iA); a2 = k; b1 = sqrt(CLS_KAPPA * iA); b2 = 0.0;
         }
         // pre-exponential test threshold: alpha >= 1/255 needs q <= 2 ln(255 o); margin covers fp32
         const double qc = CLS_KAPPA * qcut;
