@@ -56,6 +56,19 @@ __device__ __forceinline__ bool rect_hits(const unsigned *rm, int W32, int x0, i
     return false;
 }
 
+__device__ __forceinline__ float rcp_approx(float x)
+{
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float sqrt_approx(float x)
+{
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // stage 2: fp32 EWA test of Gaussian gl of the warp's batch in view v
 __device__ __forceinline__ bool cand_exact32(const float (*gM)[32], const float (*gP)[32], int gl, int v,
                                              const CamSoA &C, const int *__restrict__ sat, int TX, int TY)
@@ -65,7 +78,7 @@ __device__ __forceinline__ bool cand_exact32(const float (*gM)[32], const float 
     const float tx = C.R[0][v] * mx + C.R[1][v] * my + C.R[2][v] * mz + C.t[0][v];
     const float ty = C.R[3][v] * mx + C.R[4][v] * my + C.R[5][v] * mz + C.t[1][v];
     const float fx = C.fx[v], fy = C.fy[v], limx = C.limx[v], limy = C.limy[v];
-    const float iz = __frcp_rn(tz);
+    const float iz = rcp_approx(tz);   // approximate MUFU ops here: the margins below are >= 1e-3 relative
     const float xz = fminf(fmaxf(tx * iz, -limx), limx), yz = fminf(fmaxf(ty * iz, -limy), limy);
     const float u = fx * tx * iz + C.cx[v] - 0.5f;
     const float vv = fy * ty * iz + C.cy[v] - 0.5f;
@@ -89,20 +102,20 @@ __device__ __forceinline__ bool cand_exact32(const float (*gM)[32], const float 
     const float mid = 0.5f * (A + Cc);
     // lambda_max via the cancellation-free form: mid^2 - det = ((A - C)/2)^2 + B^2
     const float hd = 0.5f * (A - Cc);
-    const float lam = mid + __fsqrt_rn(fmaxf(0.1f, hd * hd + B0 * B0));
+    const float lam = mid + sqrt_approx(fmaxf(0.1f, hd * hd + B0 * B0));
     // conservative mirrors (fp32 error margins) of the exact 3-sigma rect (R7/R8:
     // x0 = trunc((u - r)/16), x1 = trunc((u + r + 15)/16), r = ceil(3 sqrt(lambda))) and of
     // the exact alpha-footprint tile range; the candidate rect is their intersection.
     // margins: relative fp32 error of u, Sigma' grows like 1/t_z near the near plane
     // (cancellation in t = R mu + t0 ~ 3e-6 absolute): 1e-3 relative + 0.5 px covers t_z >= 0.199
-    const float r32 = ceilf(3.0f * __fsqrt_rn(lam) * 1.001f + 0.01f);
+    const float r32 = ceilf(3.0f * sqrt_approx(lam) * 1.001f + 0.01f);
     const float em = 0.5f + 1e-3f * fabsf(u - C.cx[v]) + 1e-3f * fabsf(vv - C.cy[v]);
     const float rx0 = floorf((u - r32 - em) * (1.0f / CLS_TILE));
     const float rx1 = floorf((u + r32 + em + CLS_TILE - 1) * (1.0f / CLS_TILE));
     const float ry0 = floorf((vv - r32 - em) * (1.0f / CLS_TILE));
     const float ry1 = floorf((vv + r32 + em + CLS_TILE - 1) * (1.0f / CLS_TILE));
-    const float hx = __fsqrt_rn(fmaxf(qcut, 0.f) * A) * 1.001f + em;
-    const float hy = __fsqrt_rn(fmaxf(qcut, 0.f) * Cc) * 1.001f + em;
+    const float hx = sqrt_approx(fmaxf(qcut, 0.f) * A) * 1.001f + em;
+    const float hy = sqrt_approx(fmaxf(qcut, 0.f) * Cc) * 1.001f + em;
     const float gx0 = floorf((u - hx - (CLS_TILE - 1)) * (1.0f / CLS_TILE)) + 1.0f;
     const float gx1 = floorf((u + hx) * (1.0f / CLS_TILE)) + 1.0f;
     const float gy0 = floorf((vv - hy - (CLS_TILE - 1)) * (1.0f / CLS_TILE)) + 1.0f;
@@ -118,12 +131,7 @@ __device__ __forceinline__ bool cand_exact32(const float (*gM)[32], const float 
     return sat_count(S, TX + 1, bx0, by0, bx1, by1) > 0;
 }
 
-__device__ __forceinline__ float rcp_approx(float x)
-{
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
+
 
 // append the warp's kept (Gaussian, view) pairs to its shared-memory output buffer; a buffer
 // close to full is flushed to the candidate list with ONE atomic (single-counter contention was
