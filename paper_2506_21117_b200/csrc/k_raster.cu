@@ -514,7 +514,18 @@ __global__ void __launch_bounds__(1024) k_loss(Scratch s, float loss_scale, floa
     __shared__ double red[32];
     const int n = s.cnt->overflow ? 0 : s.cnt->n_items;
     double acc = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) acc += (double)s.item_loss[i];
+    // the same summation order as a plain strided loop, with 8 loads in flight per thread
+    for (int i0 = threadIdx.x; i0 < n; i0 += 8 * blockDim.x) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const int i = i0 + u * blockDim.x;
+            v[u] = i < n ? s.item_loss[i] : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+            if (i0 + u * (int)blockDim.x < n) acc += (double)v[u];
+    }
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
     __syncthreads();
