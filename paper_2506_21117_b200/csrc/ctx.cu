@@ -59,9 +59,9 @@ struct cls_ctx {
 
 static const char *PROF_NAMES[] = {"member", "active_mask", "project_cand", "project_exact", "rec_sort", "bin_count",
                                    "emit", "pair_sort", "fwd_raster", "fill_bg", "loss", "zero_grad2d", "bwd_raster",
-                                   "bwd_project", "adam"};
+                                   "bwd_project", "adam", "gather_targets"};
 enum { P_MEMBER, P_MASK, P_PROJECT, P_PROJECT_EXACT, P_RECSORT, P_BINCOUNT, P_EMIT, P_PAIRSORT, P_FWD, P_FILL, P_LOSS,
-       P_ZERO, P_BWD_RASTER, P_BWD_PROJECT, P_ADAM, P_COUNT };
+       P_ZERO, P_BWD_RASTER, P_BWD_PROJECT, P_ADAM, P_GATHER, P_COUNT };
 static_assert(P_COUNT <= CLS_PROF_GROUPS, "profile groups");
 
 static cudaEvent_t prof_event(cls_ctx *c)
@@ -343,7 +343,7 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
             if (!pa.devicePointer) return fail(c, CLS_ERR_INVALID_ARGUMENT, "host targets must be pinned and mapped");
             cudaEventRecord(c->ev_items, st);
             cudaStreamWaitEvent(c->side, c->ev_items, 0);
-            launch_gather_targets(d, cs, s, (const float *)pa.devicePointer, c->side);
+            run(c, P_GATHER, c->side, [&] { launch_gather_targets(d, cs, s, (const float *)pa.devicePointer, c->side); });
             cudaEventRecord(c->ev_gather, c->side);
             staged = true;
         } else {
