@@ -292,7 +292,7 @@ int radix_sort_u64(unsigned long long *keys, unsigned long long *keys_alt, unsig
 // writes the total to *total.  The look-back status array must be zeroed before the launch.
 // ---------------------------------------------------------------------------
 #define SC_THREADS 256
-#define SC_ITEMS 8
+#define SC_ITEMS 32   // 8192 values per tile: the look-back chain has 4x fewer links than with 2048
 #define SC_TILE (SC_THREADS * SC_ITEMS)
 
 __global__ void __launch_bounds__(SC_THREADS)
@@ -317,10 +317,12 @@ k_scan_excl(const unsigned *__restrict__ in, unsigned *__restrict__ out, const i
         const int b = tile * SC_TILE + tid * SC_ITEMS;
         unsigned v[SC_ITEMS];
         unsigned long long sum = 0;
-        if (b + SC_ITEMS <= n) {   // two 16 B vector loads (the arrays are 16 B aligned, b is a multiple of 8)
-            const uint4 p0 = *reinterpret_cast<const uint4 *>(in + b);
-            const uint4 p1 = *reinterpret_cast<const uint4 *>(in + b + 4);
-            v[0] = p0.x; v[1] = p0.y; v[2] = p0.z; v[3] = p0.w; v[4] = p1.x; v[5] = p1.y; v[6] = p1.z; v[7] = p1.w;
+        if (b + SC_ITEMS <= n) {   // 16 B vector loads (the arrays are 16 B aligned, b is a multiple of 4)
+#pragma unroll
+            for (int k = 0; k < SC_ITEMS; k += 4) {
+                const uint4 p4 = *reinterpret_cast<const uint4 *>(in + b + k);
+                v[k] = p4.x; v[k + 1] = p4.y; v[k + 2] = p4.z; v[k + 3] = p4.w;
+            }
         } else {
 #pragma unroll
             for (int k = 0; k < SC_ITEMS; k++) v[k] = b + k < n ? in[b + k] : 0u;
@@ -360,8 +362,9 @@ k_scan_excl(const unsigned *__restrict__ in, unsigned *__restrict__ out, const i
             run += v[k];
         }
         if (b + SC_ITEMS <= n) {
-            *reinterpret_cast<uint4 *>(out + b) = make_uint4(o[0], o[1], o[2], o[3]);
-            *reinterpret_cast<uint4 *>(out + b + 4) = make_uint4(o[4], o[5], o[6], o[7]);
+#pragma unroll
+            for (int k = 0; k < SC_ITEMS; k += 4)
+                *reinterpret_cast<uint4 *>(out + b + k) = make_uint4(o[k], o[k + 1], o[k + 2], o[k + 3]);
         } else {
 #pragma unroll
             for (int k = 0; k < SC_ITEMS; k++)
