@@ -290,3 +290,21 @@ def test_cuda_graph_step_matches_eager(torch_cuda):
     assert np.allclose(res[0][0], res[1][0], rtol=1e-6)
     assert np.allclose(res[0][1], res[1][1], rtol=1e-5, atol=1e-6)
     assert np.allclose(res[0][2], res[1][2], rtol=1e-5, atol=1e-6)
+
+
+def test_more_than_32_views(torch_cuda):
+    """c5's 40 views (5 change sets x 8 views) in one call: the projection's warp-level view cull
+    and stage 1 run in two chunks of views (32 + 8), view ids up to 39 ride in the stage-2 queue
+    and the record keys; membership, masks, images, loss and gradients against the oracle."""
+    sc = synth.make_scene("c5", n=40000, width=160, height=104)
+    assert len(sc.cameras) > 32
+    up = _rand_upstream(sc, 5)
+    g = H.gpu_run(sc, dL=up)
+    fb = oracle.forward_backward(sc, dL_dC=up.astype(np.float64))
+    assert np.array_equal(g["idx"], fb["idx"])
+    for v, r in enumerate(fb["renders"]):
+        assert np.array_equal(g["tile_mask"][v], r["tile_mask"]), f"tile mask view {v}"
+        H.assert_images(g["images"][v], r)
+    r = H.compare_grads(g["grad"], H.oracle_rows(fb, sc.sh_degree))
+    assert r["n_bad"] == 0, r
+    g["opt"].close()
