@@ -308,3 +308,18 @@ def test_more_than_32_views(torch_cuda):
     r = H.compare_grads(g["grad"], H.oracle_rows(fb, sc.sh_degree))
     assert r["n_bad"] == 0, r
     g["opt"].close()
+
+
+def test_limits_64_views_and_16384_px_wide(torch_cuda):
+    """The ABI's maxima: 64 views in one call (6 view bits in the record and unit keys) and a
+    16384-pixel-wide image (1024 tile columns: the unit key's 10-bit column fields at their top)."""
+    for sc in (synth.make_scene("c2", n=3000, width=96, height=64, n_views=64),
+               synth.make_scene("c1", n=2000, width=16384, height=32)):
+        g = H.gpu_run(sc)
+        fb = oracle.forward_backward(sc, with_grad=False)
+        assert np.array_equal(g["idx"], fb["idx"])
+        for v, r in enumerate(fb["renders"]):
+            assert np.array_equal(g["tile_mask"][v], r["tile_mask"]), f"tile mask view {v}"
+            H.assert_images(g["images"][v], r)
+        assert g["loss"] == pytest.approx(fb["loss"], rel=2e-5)
+        g["opt"].close()
