@@ -49,23 +49,49 @@ __device__ __forceinline__ void stage(const Scratch &s, unsigned val, int tx, in
 // ---------------------------------------------------------------------------
 // Staging from a row segment.  The units of the tile's row segment (view, tile row) are in depth
 // order; the tile's list is the subsequence whose column interval [lo, hi] covers tx.  One round
-// tests 256 consecutive units (4 per thread, coalesced 8 B key loads), ranks the covering ones in
-// segment order with warp ballots and stages them; a round that would overflow the batch stops
-// exactly at the first unstaged covering unit.  DIR = +1 scans forward from `cur` (< end),
-// DIR = -1 backward from `cur` (exclusive) down to `end` (inclusive), staging in descending order.
-// Returns the number of staged entries; s_pos[j] = segment position of staged entry j.
+// tests 256 consecutive units (4 per thread, coalesced 8 B key loads) and ranks the covering ones in
+// segment order with warp ballots; the ranked units beyond the batch are CARRIED to the next batch
+// (slots RT_BATCH.. of s_pos / s_rid), so no unit is scanned twice.  DIR = +1 scans forward from
+// `cur` (< end), DIR = -1 backward from `cur` (exclusive) down to `end` (inclusive), staging in
+// descending order.  `carry` (uniform) = ranked units waiting in the carry slots.  Returns the
+// number of staged entries; s_pos[j] = segment position of staged entry j.
 // ---------------------------------------------------------------------------
-#define RT_SCAN 4    // units tested per thread per round (256 per round: a round overshooting a
-                     // 128-entry batch re-scans less than with 512; measured 0.73 -> 0.71 ms)
+#define RT_SCAN 4    // units tested per thread per round (256 per round)
+#define RT_SLOTS (RT_BATCH + RT_SCAN * RT_THREADS)   // batch + carry slots
 
 template <int DIR, bool BWD>
-__device__ __forceinline__ int fill_batch(const Scratch &s, int &cur, int end, int tx, int ty, float4 *ent, float2 *sd,
-                                          int *s_pos, unsigned *s_rid, int *s_wc, int *s_next, int *s_first,
+__device__ __forceinline__ int fill_batch(const Scratch &s, int &cur, int end, int &carry, int tx, int ty, float4 *ent,
+                                          float2 *sd, int *s_pos, unsigned *s_rid, int *s_wc, int *s_first,
                                           int *s_clamp)
 {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned lt = (1u << lane) - 1u;
     int nst = 0;
+    if (carry > 0) {   // the carried units go first, in order
+        constexpr int PER = (RT_SLOTS - RT_BATCH + RT_THREADS - 1) / RT_THREADS;
+        int cp[PER];
+        unsigned cr[PER];
+#pragma unroll
+        for (int r = 0; r < PER; r++) {
+            const int j = tid + r * RT_THREADS;
+            cp[r] = j < carry ? s_pos[RT_BATCH + j] : 0;
+            cr[r] = j < carry ? s_rid[RT_BATCH + j] : 0u;
+        }
+        __syncthreads();
+        const int m = min(carry, RT_BATCH);
+#pragma unroll
+        for (int r = 0; r < PER; r++) {
+            const int j = tid + r * RT_THREADS;
+            if (j < carry) {
+                const int d = j < m ? j : RT_BATCH + (j - m);   // the rest stays carried, moved to the front
+                s_pos[d] = cp[r];
+                s_rid[d] = cr[r];
+            }
+        }
+        __syncthreads();
+        nst = m;
+        carry -= m;
+    }
     while (nst < RT_BATCH && (DIR > 0 ? cur < end : cur > end)) {
         unsigned cw[RT_SCAN], uv[RT_SCAN];
 #pragma unroll
@@ -89,22 +115,18 @@ __device__ __forceinline__ int fill_batch(const Scratch &s, int &cur, int end, i
         __syncthreads();
         int total = 0;
 #pragma unroll
-        for (int k = 0; k < RT_SCAN; k++) {   // rank: slots in segment order; staging comes after the batch is complete
+        for (int k = 0; k < RT_SCAN; k++) {   // rank: slots in segment order (>= RT_BATCH: carried)
             const int c0 = s_wc[2 * k], c1 = s_wc[2 * k + 1];
             if ((cov >> k) & 1u) {
                 const int u = DIR > 0 ? cur + k * RT_THREADS + tid : cur - 1 - (k * RT_THREADS + tid);
                 const int slot = nst + total + (warp ? c0 : 0) + __popc(cw[k] & lt);
-                if (slot < RT_BATCH) {
-                    s_pos[slot] = u;
-                    s_rid[slot] = uv[k];
-                } else if (slot == RT_BATCH) {
-                    *s_next = DIR > 0 ? u : u + 1;   // resume exactly at the first unstaged covering unit
-                }
+                s_pos[slot] = u;
+                s_rid[slot] = uv[k];
             }
             total += c0 + c1;
         }
-        __syncthreads();
-        cur = nst + total > RT_BATCH ? *s_next : (DIR > 0 ? cur + RT_SCAN * RT_THREADS : cur - RT_SCAN * RT_THREADS);
+        cur = DIR > 0 ? cur + RT_SCAN * RT_THREADS : cur - RT_SCAN * RT_THREADS;
+        carry = max(nst + total - RT_BATCH, 0);
         nst = min(nst + total, RT_BATCH);
         __syncthreads();
     }
@@ -318,8 +340,8 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
 {
     __shared__ float4 ent[3 * (RT_BATCH + 1)];   // staged entries (sa, sb, sc) + one pad
     __shared__ float red[RT_THREADS / 32];
-    __shared__ int s_item, s_pos[RT_BATCH], s_wc[2 * RT_SCAN], s_next, s_first, s_clamp, s_lastp[CLS_BLOCK_PIX];
-    __shared__ unsigned s_rid[RT_BATCH];
+    __shared__ int s_item, s_pos[RT_SLOTS], s_wc[2 * RT_SCAN], s_first, s_clamp, s_lastp[CLS_BLOCK_PIX];
+    __shared__ unsigned s_rid[RT_SLOTS];
     if (s.cnt->overflow) return;
     const int n_items = s.cnt->n_items;
     const int tid = threadIdx.x;
@@ -360,10 +382,11 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
             T23 = pack2(Ti[2], Ti[3]);
         }
         int lbase = 0;   // list index of the batch's first entry
+        int carry = 0;   // ranked units carried to the next batch
         while (true) {
             const bool live = tmax4(T01, T23) > 0.f;
-            if (__syncthreads_count(live) == 0 || cur >= se) break;
-            const int cnt = fill_batch<1, false>(s, cur, se, tx, ty, ent, nullptr, s_pos, s_rid, s_wc, &s_next, &s_first, &s_clamp);
+            if (__syncthreads_count(live) == 0 || (cur >= se && carry == 0)) break;
+            const int cnt = fill_batch<1, false>(s, cur, se, carry, tx, ty, ent, nullptr, s_pos, s_rid, s_wc, &s_first, &s_clamp);
             if (s_clamp) comp_batch<true>(ent, cnt, lbase, flx, fy01, fy23, T01, T23, C0, C1, C2, last);
             else comp_batch<false>(ent, cnt, lbase, flx, fy01, fy23, T01, T23, C0, C1, C2, last);
 #pragma unroll
@@ -592,8 +615,8 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
 {
     __shared__ float4 ent[3 * (RT_BATCH + 1)];
     __shared__ float2 sd[RT_BATCH];    // tile-local 2D mean (dx0, dy0) in fp32
-    __shared__ int s_item, s_maxlast, s_pos[RT_BATCH], s_wc[2 * RT_SCAN], s_next;
-    __shared__ unsigned s_rid[RT_BATCH];
+    __shared__ int s_item, s_maxlast, s_pos[RT_SLOTS], s_wc[2 * RT_SCAN];
+    __shared__ unsigned s_rid[RT_SLOTS];
     if (s.cnt->overflow) return;
     const int n_items = s.cnt->n_items;
     const int A = s.cnt->A;
@@ -663,10 +686,10 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         float4 *gbase = s.grad2d + (size_t)v * A * 3;
         const f2_t fyp[2] = {pack2((float)ly, (float)(ly + 4)), pack2((float)(ly + 8), (float)(ly + 12))};
         // reverse walk over the row segment [first, end): batches of covering units, descending
-        int cur = end;
-        while (cur > first) {
+        int cur = end, carry = 0;
+        while (cur > first || carry > 0) {
             __syncthreads();
-            const int cnt = fill_batch<-1, true>(s, cur, first, tx, ty, ent, sd, s_pos, s_rid, s_wc, &s_next, nullptr, nullptr);
+            const int cnt = fill_batch<-1, true>(s, cur, first, carry, tx, ty, ent, sd, s_pos, s_rid, s_wc, nullptr, nullptr);
             // walked (pixel, entry) pairs of this batch: s_pos is descending, so the entries above a
             // pixel's last composited one form a prefix (binary search per pixel)
 #pragma unroll
