@@ -46,17 +46,14 @@ __device__ __forceinline__ void sh_basis_grad(int D, float x, float y, float z, 
 }
 
 template <int D>
-__global__ void __launch_bounds__(128)
-k_bwd_project(const float4 *__restrict__ mean_op, const float4 *__restrict__ quat,
-              const float4 *__restrict__ log_scale, const float4 *__restrict__ sh, int n,
-              const __grid_constant__ CamSet cams, Scratch s, float4 *__restrict__ out)
+__device__ __forceinline__ void bwd_project_row(const float4 *__restrict__ mean_op, const float4 *__restrict__ quat,
+                                                const float4 *__restrict__ log_scale, const float4 *__restrict__ sh,
+                                                int n, const CamSet &cams, const Scratch &s, float4 *__restrict__ out,
+                                                int A, int k)
 {
     constexpr int K = (D + 1) * (D + 1);
     constexpr int K4 = (3 * K + 3) / 4;
     constexpr int ROW4 = 3 + K4;
-    const int A = s.cnt->A;
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= A) return;
     const int i = s.idx[k];
     const float4 mo = mean_op[i], q4 = quat[i], ls = log_scale[i];
     // parameter-only quantities
@@ -214,10 +211,22 @@ k_bwd_project(const float4 *__restrict__ mean_op, const float4 *__restrict__ qua
     }
 }
 
+template <int D>
+__global__ void __launch_bounds__(128)
+k_bwd_project(const float4 *__restrict__ mean_op, const float4 *__restrict__ quat,
+              const float4 *__restrict__ log_scale, const float4 *__restrict__ sh, int n,
+              const __grid_constant__ CamSet cams, Scratch s, float4 *__restrict__ out)
+{
+    const int A = s.cnt->A;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < A; k += gridDim.x * blockDim.x)
+        bwd_project_row<D>(mean_op, quat, log_scale, sh, n, cams, s, out, A, k);
+}
+
+
 void launch_bwd_project(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s,
                         float *grad_active, cudaStream_t st)
 {
-    const int blocks = (d.n + 127) / 128;   // upper bound on A; threads k >= A exit
+    const int blocks = std::max(1, std::min((d.n + 127) / 128, 148 * 4));   // grid-stride over the A rows
     float4 *out = reinterpret_cast<float4 *>(grad_active);
     switch (d.D) {
     case 0: k_bwd_project<0><<<blocks, 128, 0, st>>>(g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s, out); break;
