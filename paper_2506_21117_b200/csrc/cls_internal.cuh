@@ -9,6 +9,8 @@
 #define CLS_TILE 16
 #define RK_IDX_BITS 27   // record id in the low bits of the record sort key (max_records <= 2^27)
 #define RK_IDX_MASK ((1ull << RK_IDX_BITS) - 1ull)
+#define RK_DEPTH_BITS 30  // depth field: fp32 bits of the depth minus bits(0.2f), clamped (ties beyond ~1e37)
+#define RK_VIEW_SHIFT (RK_DEPTH_BITS + RK_IDX_BITS)
 // unit key (one u64, sorted by its top bits only): row segment (view * TY + ty, 17 bits; V * TY = dead)
 // << 47 | hi << 37 | lo << 27 | record id (27 bits); lo, hi = the footprint's tile columns (TX <= 1024)
 #define UK_SEG_SHIFT 47
@@ -488,7 +490,7 @@ __device__ __forceinline__ FootRec foot_load(const Scratch &s, unsigned i)
 {
     const unsigned rid = s.srid[i];
     const Rec R = s.rec[rid];
-    return foot_make(R, (int)(s.rskey[i] >> (31 + RK_IDX_BITS)), rid | (__float_as_int(R.aux.y) < 0 ? 0u : 0x80000000u));
+    return foot_make(R, (int)(s.rskey[i] >> RK_VIEW_SHIFT), rid | (__float_as_int(R.aux.y) < 0 ? 0u : 0x80000000u));
 }
 
 // active tiles of row bitmask `rm` (W32 words) in columns [lo, hi] of word w

@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(256) k_fill_units(Scratch s)
     if ((long long)U > s.max_units) return;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const unsigned o = s.roff[i], c = s.rcnt[i];
-        const unsigned rid = s.srid[i], vw = (unsigned)(s.rskey[i] >> (31 + RK_IDX_BITS)) << 16;
+        const unsigned rid = s.srid[i], vw = (unsigned)(s.rskey[i] >> RK_VIEW_SHIFT) << 16;
         for (unsigned k = 0; k < c; k++) s.urec[o + k] = make_uint2(rid, vw | k);
     }
 }
@@ -274,7 +274,7 @@ void launch_gather_targets(const StepDims &d, const CamSet &cams, const Scratch 
 // 1. record depth sort + ties
 void launch_bin_recsort(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st)
 {
-    const int rbits = 31 + bits_for(d.V - 1);   // (view, depth) above the carried record id
+    const int rbits = RK_DEPTH_BITS + bits_for(d.V - 1);   // (view, depth) above the carried record id
     const int R = (int)s.max_records;
     const int w = radix_sort_u64(s.rkey, s.rkey_alt, nullptr, nullptr, &s.cnt->n_records, R, RK_IDX_BITS,
                                  RK_IDX_BITS + rbits, rbits <= 32 ? 8 : 9, s.rs_counts, s.rs_totals,

@@ -486,10 +486,11 @@ k_project_exact(const float4 *__restrict__ mean_op, const float4 *__restrict__ q
         s.rec_gid[slot] = i;
         if (ordi >= 0 && ordi < s.max_active) s.vis[(size_t)v * s.max_active + ordi] = 1;   // densification stats
         // depth-sort key (reading R13): view, then fp32 round-to-nearest of the fp64 depth
-        // (positive floats order as their bit patterns; depth > 0.2 here, so bits - bits(0.125) fits
-        // 31 bits), then the record id in the low RK_IDX_BITS (carried, not sorted: no value array)
-        s.rkey[slot] = ((unsigned long long)v << (31 + RK_IDX_BITS)) |
-                       ((unsigned long long)(__float_as_uint(__double2float_rn(p.tz)) - 0x3E000000u) << RK_IDX_BITS) |
+        // (positive floats order as their bit patterns; depth > 0.2 here, so bits - bits(0.2f) >= 0;
+        // clamped to 30 bits, which only merges depths beyond ~1e37), then the record id in the low
+        // RK_IDX_BITS (carried, not sorted: no value array).  36 key bits up to 64 views: 4 passes
+        const unsigned dk = min(__float_as_uint(__double2float_rn(p.tz)) - 0x3E4CCCCDu, (1u << RK_DEPTH_BITS) - 1u);
+        s.rkey[slot] = ((unsigned long long)v << RK_VIEW_SHIFT) | ((unsigned long long)dk << RK_IDX_BITS) |
                        (unsigned long long)slot;
     }
 }
