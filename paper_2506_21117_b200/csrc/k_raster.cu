@@ -610,7 +610,7 @@ __device__ __forceinline__ float warp_reduce_scatter9(const float (&r)[9], int l
     return a1 + __shfl_xor_sync(0xffffffffu, a1, 1);
 }
 
-__global__ void __launch_bounds__(RT_THREADS)
+__global__ void __launch_bounds__(RT_THREADS, 12)
 k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ dL_dimg, float3 bg)
 {
     __shared__ float4 ent[3 * (RT_BATCH + 1)];
