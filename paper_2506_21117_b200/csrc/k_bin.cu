@@ -142,15 +142,29 @@ __global__ void __launch_bounds__(256) k_fill_units(Scratch s)
 
 // per unit (record i, tile row ty): the footprint's tile columns [lo, hi] in that row; a unit whose
 // columns hold no ACTIVE tile is dead (its segment key sorts after every live one)
+#define UB_U 2   // units per thread per iteration (their load chains overlap; 4: too many registers)
 __global__ void __launch_bounds__(256) k_unit_build(const __grid_constant__ CamSet cams, Scratch s)
 {
     const int U = s.cnt->overflow ? 0 : s.cnt->n_units32;
     const int TY = cams.TY, W32 = (cams.TX + 31) >> 5;
     const unsigned long long dead = (unsigned long long)(cams.n * TY) << UK_SEG_SHIFT;
     unsigned long long pairs = 0, live = 0;
-    for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < U; u += gridDim.x * blockDim.x) {
-        const uint2 ur = s.urec[u];
-        const Rec R = s.rec[ur.x];
+    const int stride = gridDim.x * blockDim.x;
+    for (int u0 = blockIdx.x * blockDim.x + threadIdx.x; u0 < U; u0 += UB_U * stride) {
+        // UB_U units per iteration: their dependent load chains (unit map -> record) in flight together
+        uint2 urs[UB_U];
+        Rec Rs[UB_U];
+#pragma unroll
+        for (int h = 0; h < UB_U; h++) urs[h] = u0 + h * stride < U ? s.urec[u0 + h * stride] : make_uint2(0u, 0u);
+#pragma unroll
+        for (int h = 0; h < UB_U; h++)
+            if (u0 + h * stride < U) Rs[h] = s.rec[urs[h].x];
+#pragma unroll
+        for (int h = 0; h < UB_U; h++) {
+        const int u = u0 + h * stride;
+        if (u >= U) break;
+        const uint2 ur = urs[h];
+        const Rec &R = Rs[h];
         const FootRec f = foot_make(R, (int)(ur.y >> 16), ur.x | (__float_as_int(R.aux.y) < 0 ? 0u : 0x80000000u));
         const int ty = f.y0 + (int)(ur.y & 0xffffu);
         int lo, hi;
@@ -165,6 +179,7 @@ __global__ void __launch_bounds__(256) k_unit_build(const __grid_constant__ CamS
         s.ukey[u] = (cnt ? ((unsigned long long)(f.view * TY + ty) << UK_SEG_SHIFT) |
                                ((unsigned long long)lo << UK_LO_SHIFT) | ((unsigned long long)hi << UK_HI_SHIFT)
                          : dead) | rid;
+        }
     }
     for (int o = 16; o > 0; o >>= 1) {
         pairs += __shfl_xor_sync(0xffffffffu, pairs, o);
