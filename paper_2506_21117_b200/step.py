@@ -224,7 +224,8 @@ class LocalOptimizer:
         V = len(cameras)
         W, H = cameras[0].width, cameras[0].height
         dev = self.params.device
-        loss = torch.zeros(1, dtype=torch.float32, device=dev) if targets is not None else None
+        # written (not accumulated) by the call: no fill kernel
+        loss = torch.empty(1, dtype=torch.float32, device=dev) if targets is not None else None
         img = torch.empty((V, 3, H, W), dtype=torch.float32, device=dev) if images else None
         tm = torch.empty((V, -(-H // 16), -(-W // 16)), dtype=torch.uint8, device=dev) if tile_mask else None
         if targets is not None:
