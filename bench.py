@@ -342,7 +342,8 @@ def algorithmic_work(sc, n_views, st):
         "project_cand": ("hbm", n * 48 + C * 8),
         "project_exact": ("hbm", C * 8 + R * (48 + 16 * K4 + 64 + 4 + 8)),
         "rec_sort": ("hbm", rpasses * R * 16),          # key-only passes: read + write 8 B
-        "bin_count": ("hbm", R * (8 + 64 + 64 + 4 + 4) + U * 4),
+        # k_permute: key 8 + rrows 4 in, srid 4 + rcnt 4 out; scan: 4 + 4; k_fill_units: 20 in, U x 8 out
+        "bin_count": ("hbm", R * (20 + 8 + 20) + U * 8),
         "emit": ("hbm", R * 64 + U * (4 + 8)),
         "pair_sort": ("hbm", upasses * U * 16 + U * 8),  # key-only passes (record id packed in the key)
         "fwd_raster": ("alu", st["n_fwd_evals"] * FWD_FLOPS_PER_EVAL),

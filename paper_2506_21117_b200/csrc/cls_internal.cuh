@@ -94,6 +94,7 @@ struct Scratch {
     // records
     Rec *rec;               // records in creation order (k_project_exact)
     int *rec_gid;           // their Gaussian index (ties of the depth order, R13)
+    unsigned *rrows;        // their number of tile rows (a 4 B array k_permute gathers from L2)
     unsigned *srid;         // record ids in (view, depth, Gaussian index) order (records stay in place)
     long long max_records;
     int2 *cand;             // (Gaussian, view) candidates of the fp32 pre-test

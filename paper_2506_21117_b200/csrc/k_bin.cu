@@ -116,9 +116,8 @@ __global__ void __launch_bounds__(256) k_permute(Scratch s)
     const unsigned long long *key = s.rskey;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const unsigned r = permute_source(s, key, i, n);
-        const float4 aux = reinterpret_cast<const float4 *>(s.rec + r)[3];   // (qcut', ord, x0|y0<<16, x1|y1<<16)
         s.srid[i] = r;
-        s.rcnt[i] = (unsigned)((__float_as_int(aux.w) >> 16) - (__float_as_int(aux.z) >> 16));
+        s.rcnt[i] = s.rrows[r];   // y1 - y0 of the record (its 64 B row is not touched here)
     }
 }
 

@@ -484,6 +484,7 @@ k_project_exact(const float4 *__restrict__ mean_op, const float4 *__restrict__ q
                             __int_as_float(p.x1 | (p.y1 << 16)));
         s.rec[slot] = R;
         s.rec_gid[slot] = i;
+        s.rrows[slot] = (unsigned)(p.y1 - p.y0);
         if (ordi >= 0 && ordi < s.max_active) s.vis[(size_t)v * s.max_active + ordi] = 1;   // densification stats
         // depth-sort key (reading R13): view, then fp32 round-to-nearest of the fp64 depth
         // (positive floats order as their bit patterns; depth > 0.2 here, so bits - bits(0.2f) >= 0;
