@@ -308,7 +308,7 @@ def run_ours(args):
 
 # kernel names of the profile groups in the ncu captures committed under profiles/
 GROUP_KERNELS = {"fwd_raster": "k_fwd<1, 0>", "project_cand": "k_project_cand<1>", "project_exact": "k_project_exact<3>",
-                 "bwd_raster": "k_bwd", "emit": "k_unit_build", "bin_count": "k_permute"}
+                 "bwd_raster": "k_bwd", "emit": "k_units", "bin_count": "k_permute"}
 
 
 def ncu_traffic(config: str, group: str):
@@ -342,9 +342,11 @@ def algorithmic_work(sc, n_views, st):
         "project_cand": ("hbm", n * 48 + C * 8),
         "project_exact": ("hbm", C * 8 + R * (48 + 16 * K4 + 64 + 4 + 8)),
         "rec_sort": ("hbm", rpasses * R * 16),          # key-only passes: read + write 8 B
-        # k_permute: key 8 + rrows 4 in, srid 4 + rcnt 4 out; scan: 4 + 4; k_fill_units: 20 in, U x 8 out
-        "bin_count": ("hbm", R * (20 + 8 + 20) + U * 8),
-        "emit": ("hbm", R * 64 + U * (4 + 8)),
+        # k_permute: key 8 + rrows 4 in, srid 4 + rcnt 4 out; scan: 4 + 4
+        "bin_count": ("hbm", R * (20 + 8)),
+        # k_units: per record roff, rcnt, srid, key (20 B) + the 64 B record; per unit the row-mask
+        # word (4 B) and the 8 B key out
+        "emit": ("hbm", R * (20 + 64) + U * (4 + 8)),
         "pair_sort": ("hbm", upasses * U * 16 + U * 8),  # key-only passes (record id packed in the key)
         "fwd_raster": ("alu", st["n_fwd_evals"] * FWD_FLOPS_PER_EVAL),
         "bwd_raster": ("alu", st["n_bwd_evals"] * BWD_FLOPS_PER_EVAL),

@@ -103,7 +103,6 @@ struct Scratch {
     unsigned long long *rkey, *rkey_alt;
     const unsigned long long *rskey;   // the sorted keys: view | depth bits - bits(0.125) | record id
     unsigned *rcnt, *roff;          // per sorted record: tile rows of its footprint rect, their exclusive offsets
-    uint2 *urec;                    // per (record, tile row) unit: (record id, view << 16 | row in the rect)
     // units sorted stably by their row segment (view, tile row): key = segment << 32 | lo | hi << 16
     // (the footprint's tile columns in the row), value = sorted record | active << 31
     unsigned long long *ukey, *ukey_alt;

@@ -149,7 +149,7 @@ cls_status cls_destroy(cls_ctx *c)
     cudaSetDevice(c->device);
     void *ptrs[] = {c->s.idx, c->s.ord, c->s.st_member, c->s.mask, c->s.sat, c->s.mdiff, c->s.rowmask, c->s.view_bbox, c->s.rec,
                     c->s.srid, c->s.rec_gid, c->s.rrows, c->s.cand, c->s.rkey,
-                    c->s.rkey_alt, c->s.rcnt, c->s.urec, c->s.ukey, c->s.ukey_alt,
+                    c->s.rkey_alt, c->s.rcnt, c->s.ukey, c->s.ukey_alt,
                     c->s.roff, c->s.st_scan, c->s.seg_off, c->s.seg_end, c->s.st_tiles, c->s.items, c->s.item_of_tile,
                     c->s.first_active, c->s.vis, c->s.rs_counts, c->s.rs_totals, c->s.px_T, c->s.px_last, c->s.px_dl, c->s.tgt,
                     c->s.item_loss, c->s.grad2d, c->s.cnt};
@@ -208,7 +208,7 @@ cls_status cls_create(cls_ctx **out, int device, const cls_limits *lim)
               dalloc(&s.sat, SAT) && dalloc(&s.mdiff, SAT) && dalloc(&s.rowmask, V * c->maxTY * ((c->maxTX + 31) / 32)) &&
               dalloc(&s.view_bbox, V) && dalloc(&s.rec, R) && dalloc(&s.srid, R) && dalloc(&s.rec_gid, R) && dalloc(&s.rrows, R) &&
               dalloc(&s.cand, R + R / 2 + 1024) && dalloc(&s.rkey, R) && dalloc(&s.rkey_alt, R) &&
-              dalloc(&s.rcnt, R) && dalloc(&s.urec, P) && dalloc(&s.ukey, P) &&
+              dalloc(&s.rcnt, R) && dalloc(&s.ukey, P) &&
               dalloc(&s.ukey_alt, P) && dalloc(&s.roff, R) &&
               dalloc(&s.st_scan, std::max(R, P) / 2048 + 2) && dalloc(&s.seg_off, V * c->maxTY) &&
               dalloc(&s.seg_end, V * c->maxTY) && dalloc(&s.st_tiles, VT / 2048 + 2) &&

@@ -121,10 +121,19 @@ __global__ void __launch_bounds__(256) k_permute(Scratch s)
     }
 }
 
-// unit -> record map: urec[roff[i] + k] = (record id, view << 16 | k) for the k-th tile row of the
-// record at sorted position i (the unit build then needs one dependent load, not three)
-__global__ void __launch_bounds__(256) k_fill_units(Scratch s)
+// per unit (record i, tile row ty): the footprint's tile columns [lo, hi] in that row; a unit whose
+// columns hold no ACTIVE tile is dead (its segment key sorts after every live one).
+// A warp takes 32 consecutive sorted records (lane = record: one gather of the record, one
+// footprint setup each) and then their units, which are contiguous from roff[i0] (lane = unit:
+// coalesced key writes); a unit finds its record by a 5-step search over the warp's 32 unit
+// offsets and reads the footprint terms from shared memory.
+#define KU_THREADS 256
+#define KU_WARPS (KU_THREADS / 32)
+__global__ void __launch_bounds__(KU_THREADS) k_units(const __grid_constant__ CamSet cams, Scratch s)
 {
+    __shared__ float sf[KU_WARPS][9][32];      // u, v, ia, b, det, aQ, ey, dyr, mx
+    __shared__ unsigned si[KU_WARPS][4][32];   // x0 | x1 << 16, y0 | view << 16, record id, unit offset
+    __shared__ unsigned char sown[KU_WARPS][32];   // per unit of a chunk that starts a record: its lane
     const int n = s.cnt->overflow ? 0 : min(s.cnt->n_records, (int)s.max_records);
     const unsigned long long U = s.cnt->n_units;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -132,60 +141,93 @@ __global__ void __launch_bounds__(256) k_fill_units(Scratch s)
         s.cnt->n_units32 = (int)min((unsigned long long)s.max_units, U);
     }
     if ((long long)U > s.max_units) return;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const unsigned o = s.roff[i], c = s.rcnt[i];
-        const unsigned rid = s.srid[i], vw = (unsigned)(s.rskey[i] >> RK_VIEW_SHIFT) << 16;
-        for (unsigned k = 0; k < c; k++) s.urec[o + k] = make_uint2(rid, vw | k);
-    }
-}
-
-// per unit (record i, tile row ty): the footprint's tile columns [lo, hi] in that row; a unit whose
-// columns hold no ACTIVE tile is dead (its segment key sorts after every live one)
-#define UB_U 2   // units per thread per iteration (their load chains overlap; 4: too many registers)
-__global__ void __launch_bounds__(256) k_unit_build(const __grid_constant__ CamSet cams, Scratch s)
-{
-    const int U = s.cnt->overflow ? 0 : s.cnt->n_units32;
     const int TY = cams.TY, W32 = (cams.TX + 31) >> 5;
     const unsigned long long dead = (unsigned long long)(cams.n * TY) << UK_SEG_SHIFT;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    float (*F)[32] = sf[wid];
+    unsigned (*I)[32] = si[wid];
+    unsigned char *own = sown[wid];
     unsigned long long pairs = 0, live = 0;
-    const int stride = gridDim.x * blockDim.x;
-    for (int u0 = blockIdx.x * blockDim.x + threadIdx.x; u0 < U; u0 += UB_U * stride) {
-        // UB_U units per iteration: their dependent load chains (unit map -> record) in flight together
-        uint2 urs[UB_U];
-        Rec Rs[UB_U];
-#pragma unroll
-        for (int h = 0; h < UB_U; h++) urs[h] = u0 + h * stride < U ? s.urec[u0 + h * stride] : make_uint2(0u, 0u);
-#pragma unroll
-        for (int h = 0; h < UB_U; h++)
-            if (u0 + h * stride < U) Rs[h] = s.rec[urs[h].x];
-#pragma unroll
-        for (int h = 0; h < UB_U; h++) {
-        const int u = u0 + h * stride;
-        if (u >= U) break;
-        const uint2 ur = urs[h];
-        const Rec &R = Rs[h];
-        const FootRec f = foot_make(R, (int)(ur.y >> 16), ur.x | (__float_as_int(R.aux.y) < 0 ? 0u : 0x80000000u));
-        const int ty = f.y0 + (int)(ur.y & 0xffffu);
-        int lo, hi;
-        unsigned cnt = 0u;
-        if (foot_row(f, ty, lo, hi)) {
-            const unsigned *rm = s.rowmask + ((size_t)f.view * TY + ty) * W32;
-            for (int w = lo >> 5; w <= (hi >> 5); w++) cnt += __popc(row_bits(rm, w, lo, hi));
+    const int gstride = gridDim.x * KU_THREADS;
+    // the next batch's per-record words are loaded while the current batch's units are built
+    int i0 = (blockIdx.x * KU_WARPS + wid) * 32;
+    unsigned n_o = 0xffffffffu, n_c = 0u, n_rid = 0u;
+    int n_view = 0;
+    if (i0 + lane < n) {
+        n_o = s.roff[i0 + lane]; n_c = s.rcnt[i0 + lane]; n_rid = s.srid[i0 + lane];
+        n_view = (int)(s.rskey[i0 + lane] >> RK_VIEW_SHIFT);
+    }
+    for (; i0 < n; i0 += gstride) {
+        const int i = i0 + lane;
+        const unsigned o = n_o, c = n_c, rid = n_rid;   // invalid lanes: an offset beyond every unit
+        const int view = n_view;
+        Rec rec;
+        if (i < n) rec = s.rec[rid];
+        n_o = 0xffffffffu; n_c = 0u; n_rid = 0u; n_view = 0;
+        if (i + gstride < n) {
+            n_o = s.roff[i + gstride]; n_c = s.rcnt[i + gstride]; n_rid = s.srid[i + gstride];
+            n_view = (int)(s.rskey[i + gstride] >> RK_VIEW_SHIFT);
         }
-        pairs += cnt;
-        live += cnt ? 1u : 0u;
-        const unsigned long long rid = f.w & 0x7fffffffu;
-        s.ukey[u] = (cnt ? ((unsigned long long)(f.view * TY + ty) << UK_SEG_SHIFT) |
-                               ((unsigned long long)lo << UK_LO_SHIFT) | ((unsigned long long)hi << UK_HI_SHIFT)
-                         : dead) | rid;
+        if (i < n) {
+            const FootRec f = foot_make(rec, view, rid);
+            F[0][lane] = f.u; F[1][lane] = f.v; F[2][lane] = f.ia; F[3][lane] = f.b; F[4][lane] = f.det;
+            F[5][lane] = f.aQ; F[6][lane] = f.ey; F[7][lane] = f.dyr; F[8][lane] = f.mx;
+            I[0][lane] = (unsigned)f.x0 | ((unsigned)f.x1 << 16);
+            I[1][lane] = (unsigned)f.y0 | ((unsigned)view << 16);
+            I[2][lane] = rid;
         }
+        I[3][lane] = o;
+        __syncwarp();
+        const int last = min(31, n - 1 - i0);
+        const unsigned ubeg = __shfl_sync(0xffffffffu, o, 0);
+        const unsigned uend = __shfl_sync(0xffffffffu, o + c, last);
+        int carry = 0;   // record of the previous chunk's last unit
+        for (unsigned ub = ubeg; ub < uend; ub += 32) {
+            // records starting in this chunk of 32 units: a bit mask of their first units and, per
+            // start, the record's lane; unit lane l belongs to the nearest start at or before l
+            const bool st = c > 0u && o >= ub && o - ub < 32u;
+            __syncwarp();   // the previous chunk's reads of own[] are done
+            if (st) own[o - ub] = (unsigned char)lane;
+            const unsigned S = __reduce_or_sync(0xffffffffu, st ? 1u << (o - ub) : 0u);
+            __syncwarp();
+            const unsigned m = S & (0xffffffffu >> (31 - lane));
+            const int j = m ? (int)own[31 - __clz(m)] : carry;
+            carry = __shfl_sync(0xffffffffu, j, 31);
+            const unsigned u = ub + lane;
+            if (u >= uend) break;
+            FootRec f;
+            f.u = F[0][j]; f.v = F[1][j]; f.ia = F[2][j]; f.b = F[3][j]; f.det = F[4][j];
+            f.aQ = F[5][j]; f.ey = F[6][j]; f.dyr = F[7][j]; f.mx = F[8][j];
+            const unsigned xs = I[0][j], yv = I[1][j];
+            f.x0 = (int)(xs & 0xffffu); f.x1 = (int)(xs >> 16);
+            const int view = (int)(yv >> 16), ty = (int)(yv & 0xffffu) + (int)(u - I[3][j]);
+            int lo, hi;
+            unsigned cnt = 0u;
+            if (foot_row(f, ty, lo, hi)) {
+                const unsigned *rm = s.rowmask + ((size_t)view * TY + ty) * W32;
+                const int w0 = lo >> 5, w1 = hi >> 5;
+                if (w1 - w0 <= 1) {   // the common case, branch-free: columns within two mask words
+                    const unsigned m0 = 0xffffffffu << (lo & 31), m1 = 0xffffffffu >> (31 - (hi & 31));
+                    const unsigned a = rm[w0], b = rm[w1];
+                    cnt = w0 == w1 ? __popc(a & m0 & m1) : __popc(a & m0) + __popc(b & m1);
+                } else {
+                    for (int w = w0; w <= w1; w++) cnt += __popc(row_bits(rm, w, lo, hi));
+                }
+            }
+            pairs += cnt;
+            live += cnt ? 1u : 0u;
+            s.ukey[u] = (cnt ? ((unsigned long long)(view * TY + ty) << UK_SEG_SHIFT) |
+                                   ((unsigned long long)lo << UK_LO_SHIFT) | ((unsigned long long)hi << UK_HI_SHIFT)
+                             : dead) | (unsigned long long)I[2][j];
+        }
+        __syncwarp();
     }
     for (int o = 16; o > 0; o >>= 1) {
         pairs += __shfl_xor_sync(0xffffffffu, pairs, o);
         live += __shfl_xor_sync(0xffffffffu, live, o);
     }
-    if ((threadIdx.x & 31) == 0 && pairs) atomicAdd(&s.cnt->n_pairs, pairs);
-    if ((threadIdx.x & 31) == 0 && live) atomicAdd(&s.cnt->n_live_units, live);
+    if (lane == 0 && pairs) atomicAdd(&s.cnt->n_pairs, pairs);
+    if (lane == 0 && live) atomicAdd(&s.cnt->n_live_units, live);
 }
 
 // row-segment ranges of the sorted units (dead units excluded)
@@ -304,14 +346,13 @@ void launch_bin_count(const StepDims &d, const CamSet &cams, Scratch &s, cudaStr
     k_permute<<<148 * 8, 256, 0, st>>>(s);
     scan_excl_u32(s.rcnt, s.roff, &s.cnt->n_records, R, s.st_scan, &s.cnt->scan_ticket, &s.cnt->n_units,
                   &s.cnt->overflow, st);
-    k_fill_units<<<148 * 8, 256, 0, st>>>(s);
-    g_launches += 2;
+    g_launches += 1;
 }
 
 // 3. per unit: footprint columns and segment key
 void launch_bin_emit(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st)
 {
-    k_unit_build<<<148 * 8, 256, 0, st>>>(cams, s);
+    k_units<<<148 * 8, KU_THREADS, 0, st>>>(cams, s);
     g_launches += 1;
 }
 
