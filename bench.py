@@ -20,6 +20,7 @@ each kernel group over the same timed region.  `--impl reference` times the CPU 
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import statistics
@@ -126,7 +127,7 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2506_21117_b200.dist import allreduce_rows, shard_views
-    sc = synth.make_scene(args.config)
+    sc, u8 = bench_scene(args)
     V = len(sc.cameras)
     my_views = shard_views(V, world, rank)
     cams = [sc.cameras[v] for v in my_views]
@@ -136,7 +137,9 @@ def run_ours(args):
     opt = LocalOptimizer(params, sc.regions, limits=lim)
     if not args.no_spatial_order:
         opt.spatial_order()   # scene layout, once at load (not part of a step): Morton-ordered rows
-    tg_host = torch.from_numpy(np.ascontiguousarray(sc.targets[my_views])).pin_memory()
+    tg_np = u8[my_views] if u8 is not None else sc.targets[my_views]
+    tg_host = torch.from_numpy(np.ascontiguousarray(tg_np)).pin_memory()
+    tbytes = tg_host.element_size()
     tg = tg_host.to(f"cuda:{local}")
     stream = torch.cuda.current_stream()
 
@@ -202,9 +205,14 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        # eager: the host-target gather runs on a side stream overlapped with projection/binning
-        # (measured faster end to end than the same step replayed as a CUDA graph)
-        step_host = (lambda: step_eager(tg_host)) if gstep is not None else (lambda: step(tg_host))
+        # the host-target gather runs on a side stream overlapped with projection/binning, in a CUDA
+        # graph of the step over the pinned host targets (--e2e-mode graph) or launched eagerly
+        if gstep is not None and args.e2e_mode == "graph":
+            from paper_2506_21117_b200 import GraphStep
+            gstep_host = GraphStep(opt, cams, tg_host, n_views_total=V)
+            step_host = gstep_host.replay
+        else:
+            step_host = (lambda: step_eager(tg_host)) if gstep is not None else (lambda: step(tg_host))
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -222,15 +230,17 @@ def run_ours(args):
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         st_e = opt.stats()
-        h2d = torch.tensor([float(st_e["n_items"]) * 256 * 3 * 4], dtype=torch.float64, device=f"cuda:{local}")
+        h2d = torch.tensor([float(st_e["n_items"]) * 256 * 3 * tbytes], dtype=torch.float64, device=f"cuda:{local}")
         if world > 1:
             dist.all_reduce(h2d)
         e2e = {"value": 1000.0 * args.steps / float(te[1].item()), "unit": "steps/s",
                "h2d_bytes_per_step": int(h2d.item()), "d2h_bytes_per_step": 4 * world,
-               "h2d_note": "target pixels of the active tiles only (256 px x 3 ch x 4 B per active tile), read "
-                           "from pinned host memory inside the step; the full target set is "
-                           f"{int(tg_host.numel() * 4) * world} B",
-               "device_ms_per_step": float(te[0].item()) / args.steps}
+               "h2d_note": f"target pixels of the active tiles only (256 px x 3 ch x {tbytes} B per active tile), "
+                           "read from pinned host memory inside the step; the full target set is "
+                           f"{int(tg_host.numel() * tbytes) * world} B",
+               "device_ms_per_step": float(te[0].item()) / args.steps,
+               "mode": ("CUDA graph of the step over the pinned host targets"
+                        if gstep is not None and args.e2e_mode == "graph" else "eager launches")}
 
     out = None
     if rank == 0:
@@ -285,6 +295,8 @@ def run_ours(args):
                        "mode": "all-tiles (w/o kernel)" if args.all_tiles else "masked (local kernel)",
                        "parallelism": f"views/dp{world}",
                        "row_order": "generator order" if args.no_spatial_order else "Morton (cls_spatial_order at load)",
+                       "targets": ("u8 8-bit images (k / 255 in fp32, gathered per active tile)" if args.targets == "u8"
+                                   else "fp32"),
                        "l2": "inputs larger than L2 (params+moments "
                        f"{sc.n * (12 + 3 * 4 * 4) * 4 * 3 / 1e9:.2f} GB)"},
             "mpix_per_s": {"rendered": round(sum(stats["n_active_tiles"]) * 256 * world * value / 1e6, 2),
@@ -375,6 +387,17 @@ def cpu_baseline(sc, n_views):
                       f"Adam; {dt:.2f} s measured, scaled x{V / n_views:g} to one step"}
 
 
+def bench_scene(args):
+    """The workload's scene; with --targets u8 (default) its targets are 8-bit images (as captured)
+    and every consumer -- the kernels through CLS_FLAG_TARGETS_U8, the oracle's cpu baseline and the
+    reference arm -- sees the same fp32 values k / 255."""
+    sc = synth.make_scene(args.config)
+    if args.targets != "u8":
+        return sc, None
+    u8 = np.floor(np.asarray(sc.targets, np.float64) * 255.0 + 0.5).clip(0, 255).astype(np.uint8)
+    return dataclasses.replace(sc, targets=u8.astype(np.float32) / np.float32(255.0)), u8
+
+
 def run_reference(args):
     """Reference arm = the CPU oracle as it stands, on this arm's config and metric."""
     rank = int(os.environ.get("RANK", "0"))
@@ -382,7 +405,7 @@ def run_reference(args):
     if rank != 0:
         return None
     import oracle
-    sc = synth.make_scene(args.config)
+    sc, _ = bench_scene(args)
     V = len(sc.cameras)
     sub = synth.Scene(sc.name, sc.means, sc.log_scales, sc.quats, sc.opacity_logits, sc.sh, sc.sh_degree,
                       sc.cameras[:1], sc.regions, sc.targets[:1])
@@ -421,6 +444,9 @@ def main():
     ap.add_argument("--no-spatial-order", action="store_true",
                     help="keep the synthetic generator's row order (no cls_spatial_order at load)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-mode", default="graph", choices=("graph", "eager"))
+    ap.add_argument("--targets", default="u8", choices=("u8", "f32"),
+                    help="target images as 8-bit (k / 255, CLS_FLAG_TARGETS_U8) or fp32")
     ap.add_argument("--cpu-views", type=int, default=1)
     ap.add_argument("--eager", action="store_true",
                     help="launch every kernel per step instead of replaying the step as one CUDA graph (N = 1)")

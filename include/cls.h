@@ -95,6 +95,8 @@ typedef struct {
 
 /* flags of cls_render_fwd */
 #define CLS_FLAG_ALL_TILES 1u   /* every tile active: the full-frame 3DGS step ("w/o Kernel") */
+#define CLS_FLAG_TARGETS_U8 2u  /* targets are 8-bit images: uint8[n_views][3][H][W], value k stands for
+                                   the fp32 k / 255 (IEEE division, round to nearest) */
 
 typedef struct {
     int64_t n_active;          /* A = |O^t| of the last fwd */
@@ -147,16 +149,19 @@ cls_status cls_destroy(cls_ctx *ctx);
  *   n_views_total views of the whole step across ranks (>= n_views; loss normalisation)
  *   regions      (host) cls_region[n_regions], n_regions <= CLS_MAX_REGIONS (0 -> A = 0)
  *   bg           (host) float[3] background colour (R20: black in all configs)
- *   targets      (device) float[n_views][3][H][W] or NULL
+ *   targets      float[n_views][3][H][W] (or uint8, CLS_FLAG_TARGETS_U8) or NULL, in device memory
+ *                or in pinned, mapped host memory.  Only the active tiles' pixels are read: host
+ *                targets by a gather overlapped with projection and binning, device targets by
+ *                the forward's loss epilogue
  *   images       (device) float[n_views][3][H][W] out or NULL; pixels of inactive tiles = bg
  *   tile_mask    (device) uint8[n_views][ceil(H/16)][ceil(W/16)] out or NULL
  *   loss         (device) float scalar out or NULL (written only when targets != NULL)
- *   flags        CLS_FLAG_ALL_TILES or 0
+ *   flags        CLS_FLAG_ALL_TILES | CLS_FLAG_TARGETS_U8 or 0
  *   stream       cudaStream_t
  */
 cls_status cls_render_fwd(cls_ctx *ctx, const cls_gaussians *g, const cls_camera *cams, int32_t n_views,
                           int32_t n_views_total, const cls_region *regions, int32_t n_regions,
-                          const float *bg, const float *targets, float *images, uint8_t *tile_mask,
+                          const float *bg, const void *targets, float *images, uint8_t *tile_mask,
                           float *loss, uint32_t flags, void *stream);
 
 /* Size and device list of O^t from the last fwd.  Blocks the host only until the

@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(HERE, "libcls.so")
 CLS_MAX_VIEWS = 64
 CLS_MAX_REGIONS = 64
 CLS_FLAG_ALL_TILES = 1
+CLS_FLAG_TARGETS_U8 = 2
 
 STATUS = {0: "CLS_OK", 1: "CLS_ERR_INVALID_ARGUMENT", 2: "CLS_ERR_DIMENSION_MISMATCH", 3: "CLS_ERR_CAPACITY",
           4: "CLS_ERR_STATE", 5: "CLS_ERR_CUDA", 6: "CLS_ERR_OUT_OF_MEMORY"}

@@ -243,7 +243,7 @@ cls_status cls_create(cls_ctx **out, int device, const cls_limits *lim)
 
 cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *cams, int32_t n_views,
                           int32_t n_views_total, const cls_region *regions, int32_t n_regions, const float *bg,
-                          const float *targets, float *images, uint8_t *tile_mask, float *loss, uint32_t flags,
+                          const void *targets, float *images, uint8_t *tile_mask, float *loss, uint32_t flags,
                           void *stream)
 {
     if (!c) return CLS_ERR_INVALID_ARGUMENT;
@@ -336,18 +336,29 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     });
     // host-resident (pinned, mapped) targets: gather only the active tiles' pixels on the side
     // stream, overlapped with projection and binning; the fwd waits for it
+    // (8-bit targets, CLS_FLAG_TARGETS_U8: gathered and converted from host memory; read and
+    // converted by the forward's loss epilogue from device memory)
     bool staged = false;
     if (targets) {
         cudaPointerAttributes pa{};
+        const void *src = nullptr;
         if (cudaPointerGetAttributes(&pa, targets) == cudaSuccess && pa.type == cudaMemoryTypeHost) {
             if (!pa.devicePointer) return fail(c, CLS_ERR_INVALID_ARGUMENT, "host targets must be pinned and mapped");
-            cudaEventRecord(c->ev_items, st);
-            cudaStreamWaitEvent(c->side, c->ev_items, 0);
-            run(c, P_GATHER, c->side, [&] { launch_gather_targets(d, cs, s, (const float *)pa.devicePointer, c->side); });
-            cudaEventRecord(c->ev_gather, c->side);
-            staged = true;
+            src = pa.devicePointer;
         } else {
             cudaGetLastError();   // unregistered pointers report an error on some drivers: device memory
+        }
+        if (src) {
+            cudaEventRecord(c->ev_items, st);
+            cudaStreamWaitEvent(c->side, c->ev_items, 0);
+            run(c, P_GATHER, c->side, [&] {
+                if (flags & CLS_FLAG_TARGETS_U8)
+                    launch_gather_targets_u8(d, cs, s, (const unsigned char *)src, c->side);
+                else
+                    launch_gather_targets(d, cs, s, (const float *)src, c->side);
+            });
+            cudaEventRecord(c->ev_gather, c->side);
+            staged = true;
         }
     }
     run(c, P_PROJECT, st, [&] { launch_project_cand(p, d, cs, s, st); });
@@ -357,7 +368,7 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     run(c, P_BINCOUNT, st, [&] { launch_bin_count(d, cs, s, st); });
     run(c, P_EMIT, st, [&] { launch_bin_emit(d, cs, s, st); });
     run(c, P_PAIRSORT, st, [&] { launch_bin_pairsort(d, cs, s, st); });
-    run(c, P_FWD, st, [&] { launch_fwd(d, cs, s, targets, staged, images, loss_scale, bgc, st); });
+    run(c, P_FWD, st, [&] { launch_fwd(d, cs, s, targets, (flags & CLS_FLAG_TARGETS_U8) != 0, staged, images, loss_scale, bgc, st); });
     if (images) run(c, P_FILL, st, [&] { launch_fill_bg(d, s, images, bgc, st); });
     if (staged) {   // the loss terms need the gathered targets; the compositing above did not
         cudaStreamWaitEvent(st, c->ev_gather, 0);

@@ -327,6 +327,56 @@ void launch_gather_targets(const StepDims &d, const CamSet &cams, const Scratch 
     g_launches++;
 }
 
+// 8-bit targets (CLS_FLAG_TARGETS_U8): one lane per (active tile, channel, pixel row) reads the row's
+// 16 bytes; the 32 lanes of a warp take 32 consecutive items of one (channel, row), i.e. mostly
+// adjacent tiles: 512 contiguous bytes.  k stands for the fp32 k / 255 (round to nearest).
+__global__ void __launch_bounds__(256) k_gather_targets_u8(const __grid_constant__ CamSet cams, Scratch s,
+                                                           const unsigned char *__restrict__ targets)
+{
+    __shared__ float lut[256];   // k -> k / 255 (IEEE division, round to nearest)
+    lut[threadIdx.x] = __fdiv_rn((float)threadIdx.x, 255.0f);
+    __syncthreads();
+    const int n_items = s.cnt->overflow ? 0 : s.cnt->n_items;
+    const int W = cams.W, H = cams.H, TX = cams.TX, T = cams.T;
+    const size_t HW = (size_t)H * W;
+    const bool vec = (W & 15) == 0 && (reinterpret_cast<size_t>(targets) & 15) == 0;
+    const int total = ((n_items + 31) / 32) * 3 * 16 * 32;   // (group, ch, row, item-in-group)
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < total; f += gridDim.x * blockDim.x) {
+        const int j = f & 31, row = (f >> 5) & 15;
+        const int r3 = f >> 9;
+        const int g = r3 / 3, ch = r3 - 3 * g, item = g * 32 + j;
+        if (item >= n_items) continue;
+        const int e = s.items[item];
+        const int v = e / T, t = e - v * T;
+        const int x = (t % TX) * CLS_TILE, y = (t / TX) * CLS_TILE + row;
+        unsigned char b[16];
+        if (y < H) {
+            const unsigned char *src = targets + (size_t)v * 3 * HW + (size_t)ch * HW + (size_t)y * W + x;
+            if (vec) {
+                const uint4 q = *reinterpret_cast<const uint4 *>(src);
+                *reinterpret_cast<uint4 *>(b) = q;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 16; k++) b[k] = x + k < W ? src[k] : 0;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 16; k++) b[k] = 0;
+        }
+        float4 *dst = reinterpret_cast<float4 *>(s.tgt) + ((size_t)item * 3 + ch) * 64 + row * 4;
+#pragma unroll
+        for (int qd = 0; qd < 4; qd++)
+            dst[qd] = make_float4(lut[b[4 * qd]], lut[b[4 * qd + 1]], lut[b[4 * qd + 2]], lut[b[4 * qd + 3]]);
+    }
+}
+
+void launch_gather_targets_u8(const StepDims &d, const CamSet &cams, const Scratch &s, const unsigned char *targets,
+                              cudaStream_t st)
+{
+    k_gather_targets_u8<<<64, 256, 0, st>>>(cams, s, targets);
+    g_launches++;
+}
+
 // 1. record depth sort + ties
 void launch_bin_recsort(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st)
 {

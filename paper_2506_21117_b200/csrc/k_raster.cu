@@ -335,14 +335,17 @@ __device__ __forceinline__ float block_sum(float v, float *red)
 // ---------------------------------------------------------------------------
 template <bool TARGET, bool IMAGE>
 __global__ void __launch_bounds__(RT_THREADS, 12)
-k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ targets, bool staged,
-      float *__restrict__ images, float loss_scale, float3 bg)
+k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ targets,
+      const unsigned char *__restrict__ targets8, bool staged, float *__restrict__ images, float loss_scale, float3 bg)
 {
     __shared__ float4 ent[3 * (RT_BATCH + 1)];   // staged entries (sa, sb, sc) + one pad
     __shared__ float red[RT_THREADS / 32];
     __shared__ int s_item, s_pos[RT_SLOTS], s_wc[2 * RT_SCAN], s_first, s_clamp, s_lastp[CLS_BLOCK_PIX];
     __shared__ unsigned s_rid[RT_SLOTS];
+    __shared__ float s_u8[TARGET ? 256 : 1];   // k -> k / 255 (fp32, IEEE division) for 8-bit targets
     if (s.cnt->overflow) return;
+    if (TARGET && targets8)
+        for (int k = threadIdx.x; k < 256; k += blockDim.x) s_u8[k] = __fdiv_rn((float)k, 255.0f);
     const int n_items = s.cnt->n_items;
     const int tid = threadIdx.x;
     const int lx = tid & 15, ly = tid >> 4;   // pixels (lx, ly + 4k)
@@ -434,7 +437,14 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
                     dl[CLS_BLOCK_PIX] = o1;
                     dl[2 * CLS_BLOCK_PIX] = o2;
                 } else if (TARGET) {
-                    const float t0 = targets[pix], t1 = targets[pix + HW], t2 = targets[pix + 2 * HW];
+                    float t0, t1, t2;
+                    if (targets8) {   // 8-bit targets in device memory: k stands for k / 255 (fp32, IEEE)
+                        t0 = s_u8[targets8[pix]];
+                        t1 = s_u8[targets8[pix + HW]];
+                        t2 = s_u8[targets8[pix + 2 * HW]];
+                    } else {
+                        t0 = targets[pix]; t1 = targets[pix + HW]; t2 = targets[pix + 2 * HW];
+                    }
                     const float r0 = o0 - t0, r1 = o1 - t1, r2 = o2 - t2;
                     l1 += fabsf(r0) + fabsf(r1) + fabsf(r2);
                     dl[0] = r0 > 0.f ? loss_scale : (r0 < 0.f ? -loss_scale : 0.f);
@@ -497,14 +507,16 @@ void launch_loss_staged(const StepDims &d, const CamSet &cams, const Scratch &s,
     g_launches++;
 }
 
-void launch_fwd(const StepDims &d, const CamSet &cams, const Scratch &s, const float *targets, bool staged,
-                float *images, float loss_scale, float3 bg, cudaStream_t st)
+void launch_fwd(const StepDims &d, const CamSet &cams, const Scratch &s, const void *targets, bool targets_u8,
+                bool staged, float *images, float loss_scale, float3 bg, cudaStream_t st)
 {
     const int grid = 148 * 16;
-    if (targets && images) k_fwd<true, true><<<grid, RT_THREADS, 0, st>>>(cams, s, targets, staged, images, loss_scale, bg);
-    else if (targets) k_fwd<true, false><<<grid, RT_THREADS, 0, st>>>(cams, s, targets, staged, images, loss_scale, bg);
-    else if (images) k_fwd<false, true><<<grid, RT_THREADS, 0, st>>>(cams, s, targets, staged, images, loss_scale, bg);
-    else k_fwd<false, false><<<grid, RT_THREADS, 0, st>>>(cams, s, targets, staged, images, loss_scale, bg);
+    const float *t32 = targets_u8 ? nullptr : (const float *)targets;
+    const unsigned char *t8 = targets_u8 ? (const unsigned char *)targets : nullptr;
+    if (targets && images) k_fwd<true, true><<<grid, RT_THREADS, 0, st>>>(cams, s, t32, t8, staged, images, loss_scale, bg);
+    else if (targets) k_fwd<true, false><<<grid, RT_THREADS, 0, st>>>(cams, s, t32, t8, staged, images, loss_scale, bg);
+    else if (images) k_fwd<false, true><<<grid, RT_THREADS, 0, st>>>(cams, s, t32, t8, staged, images, loss_scale, bg);
+    else k_fwd<false, false><<<grid, RT_THREADS, 0, st>>>(cams, s, t32, t8, staged, images, loss_scale, bg);
     g_launches++;
 }
 

@@ -27,6 +27,8 @@ void launch_project_cand(const Params &g, const StepDims &d, const CamSet &cams,
 void launch_project_exact(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st);
 // (3) binning: record depth sort, exact pair counts, ordered emission, pair sort by tile (k_bin.cu)
 void launch_bin_items(const StepDims &d, Scratch &s, cudaStream_t st);
+void launch_gather_targets_u8(const StepDims &d, const CamSet &cams, const Scratch &s, const unsigned char *targets,
+                              cudaStream_t st);
 void launch_gather_targets(const StepDims &d, const CamSet &cams, const Scratch &s, const float *host_targets,
                            cudaStream_t st);
 void launch_bin_recsort(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st);
@@ -42,8 +44,8 @@ void scan_excl_u32(const unsigned *in, unsigned *out, const int *n_ptr, int max_
 #define RS_GRID (148 * 4)
 
 // (4) forward compositing + fused L1                           (k_raster.cu)
-void launch_fwd(const StepDims &d, const CamSet &cams, const Scratch &s, const float *targets, bool targets_staged,
-                float *images, float loss_scale, float3 bg, cudaStream_t st);
+void launch_fwd(const StepDims &d, const CamSet &cams, const Scratch &s, const void *targets, bool targets_u8,
+                bool targets_staged, float *images, float loss_scale, float3 bg, cudaStream_t st);
 void launch_fill_bg(const StepDims &d, const Scratch &s, float *images, float3 bg, cudaStream_t st);
 void launch_loss(const Scratch &s, float loss_scale, float *loss, cudaStream_t st);
 void launch_loss_staged(const StepDims &d, const CamSet &cams, const Scratch &s, float loss_scale, cudaStream_t st);

@@ -229,7 +229,9 @@ class LocalOptimizer:
         img = torch.empty((V, 3, H, W), dtype=torch.float32, device=dev) if images else None
         tm = torch.empty((V, -(-H // 16), -(-W // 16)), dtype=torch.uint8, device=dev) if tile_mask else None
         if targets is not None:
-            assert targets.is_contiguous() and targets.dtype == torch.float32 and tuple(targets.shape) == (V, 3, H, W)
+            # float32, or uint8 8-bit images (k stands for the fp32 k / 255; CLS_FLAG_TARGETS_U8)
+            assert targets.is_contiguous() and targets.dtype in (torch.float32, torch.uint8) and \
+                tuple(targets.shape) == (V, 3, H, W)
         g = self.params.struct()
         st = check(lib.cls_render_fwd(
             self.ctx, ctypes.byref(g), cams, V, int(n_views_total or V), self._reg, len(self.regions), self.bg,
@@ -237,7 +239,9 @@ class LocalOptimizer:
             ctypes.c_void_p(img.data_ptr() if img is not None else None),
             ctypes.c_void_p(tm.data_ptr() if tm is not None else None),
             ctypes.c_void_p(loss.data_ptr() if loss is not None else None),
-            N.CLS_FLAG_ALL_TILES if all_tiles else 0, ctypes.c_void_p(_stream_ptr(stream))), self.ctx)
+            (N.CLS_FLAG_ALL_TILES if all_tiles else 0) |
+            (N.CLS_FLAG_TARGETS_U8 if targets is not None and targets.dtype == torch.uint8 else 0),
+            ctypes.c_void_p(_stream_ptr(stream))), self.ctx)
         self._A = None
         self._fwd_views = V
         return ForwardResult(loss, img, tm)
@@ -453,7 +457,8 @@ class GraphStep:
         self.nv = len(cameras)
         self.nvt = int(n_views_total or self.nv)
         self.targets = targets   # device tensor, or pinned host memory (only active tiles' pixels are read)
-        assert (targets.is_cuda or targets.is_pinned()) and targets.is_contiguous() and targets.dtype == torch.float32
+        assert (targets.is_cuda or targets.is_pinned()) and targets.is_contiguous() and \
+            targets.dtype in (torch.float32, torch.uint8)
         dev = p.device
         self.loss = torch.zeros(1, dtype=torch.float32, device=dev)
         self.grad = torch.zeros((max(int(opt.limits.max_active), 1), row4(p.sh_degree), 4), dtype=torch.float32,
@@ -475,7 +480,8 @@ class GraphStep:
         g = p.struct()
         check(lib.cls_render_fwd(o.ctx, ctypes.byref(g), self.cams, self.nv, self.nvt, o._reg, len(o.regions), o.bg,
                                  ctypes.c_void_p(self.targets.data_ptr()), None, None,
-                                 ctypes.c_void_p(self.loss.data_ptr()), 0, st), o.ctx)
+                                 ctypes.c_void_p(self.loss.data_ptr()),
+                                 N.CLS_FLAG_TARGETS_U8 if self.targets.dtype == torch.uint8 else 0, st), o.ctx)
         check(lib.cls_render_bwd(o.ctx, ctypes.byref(g), None, ctypes.c_void_p(self.grad.data_ptr()), st), o.ctx)
 
     def _adam(self):

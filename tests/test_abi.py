@@ -36,6 +36,13 @@ def test_library_exports_every_declared_symbol(native):
     assert set(_declared()) == set(native.EXPORTS)
 
 
+def test_flag_constants_match_header(native):
+    src = open(os.path.join(ROOT, "include", "cls.h")).read()
+    flags = {k: int(v) for k, v in re.findall(r"#define (CLS_FLAG_\w+) (\d+)u", src)}
+    assert flags == {"CLS_FLAG_ALL_TILES": native.CLS_FLAG_ALL_TILES, "CLS_FLAG_TARGETS_U8": native.CLS_FLAG_TARGETS_U8}
+    assert len(set(flags.values())) == len(flags) and all(v & (v - 1) == 0 for v in flags.values())
+
+
 def test_status_strings(native):
     for code, name in native.STATUS.items():
         assert native.lib.cls_status_string(code).decode() == name

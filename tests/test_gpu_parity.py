@@ -2,6 +2,8 @@
 inputs.  Bars (BASELINE north_star): membership, tile masks
 exact; images within 1e-4 outside the ambiguity set; gradients within 1e-3 relative
 (or 1e-5 x column max); Adam within 1e-6 relative; frozen rows bit-identical."""
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -262,6 +264,56 @@ def test_host_resident_targets_match_device_targets(torch_cuda):
     assert np.array_equal(out[0][1], out[1][1])
     g0, g1 = out[0][2].astype(np.float64), out[1][2].astype(np.float64)
     assert np.all(np.abs(g0 - g1) <= 1e-5 * np.abs(g0) + 1e-6 * np.abs(g0).max())
+
+
+def _u8_targets(sc):
+    """8-bit versions of the scene's targets and the fp32 values they stand for (k / 255, IEEE)."""
+    u8 = np.floor(np.asarray(sc.targets, np.float64) * 255.0 + 0.5).clip(0, 255).astype(np.uint8)
+    return u8, u8.astype(np.float32) / np.float32(255.0)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2r"])   # width 128: 16 B row reads; 296: the byte path
+def test_u8_targets_match_fp32_targets(torch_cuda, name):
+    """8-bit targets (CLS_FLAG_TARGETS_U8; device memory and pinned host memory) are converted by
+    the gather to exactly the fp32 k / 255 the caller would pass: the loss and images are
+    bit-identical to those of the fp32 targets, and the loss matches the oracle's on k / 255."""
+    torch = torch_cuda
+    from paper_2506_21117_b200 import GaussianParams, LocalOptimizer, default_limits
+    sc = SCENES[name]()
+    u8, f32 = _u8_targets(sc)
+    out = []
+    for tg in (torch.from_numpy(f32).cuda(), torch.from_numpy(u8).cuda(), torch.from_numpy(u8).pin_memory()):
+        p = GaussianParams.from_scene(sc)
+        opt = LocalOptimizer(p, sc.regions, limits=default_limits(sc.n, len(sc.cameras), sc.width, sc.height))
+        res = opt.forward(sc.cameras, tg, images=True)
+        g = opt.backward()
+        torch.cuda.synchronize()
+        out.append((res.loss.item(), res.images.cpu().numpy(), g.cpu().numpy()))
+        opt.close()
+    for o in out[1:]:
+        assert o[0] == out[0][0]
+        assert np.array_equal(o[1], out[0][1])
+        g0, g1 = out[0][2].astype(np.float64), o[2].astype(np.float64)
+        assert np.all(np.abs(g0 - g1) <= 1e-5 * np.abs(g0) + 1e-6 * np.abs(g0).max())
+    fb = oracle.forward_backward(dataclasses.replace(sc, targets=f32), with_grad=False)
+    assert out[1][0] == pytest.approx(fb["loss"], rel=2e-5)
+
+
+def test_graph_step_with_u8_host_targets(torch_cuda):
+    """The bench's end-to-end form: GraphStep over 8-bit targets in pinned host memory gives the
+    loss of the eager step on the fp32 k / 255 targets."""
+    torch = torch_cuda
+    from paper_2506_21117_b200 import GaussianParams, GraphStep, LocalOptimizer, default_limits
+    sc = SCENES["c1"]()
+    u8, f32 = _u8_targets(sc)
+    p = GaussianParams.from_scene(sc)
+    opt = LocalOptimizer(p, sc.regions, limits=default_limits(sc.n, 1, sc.width, sc.height))
+    ref = opt.forward(sc.cameras, torch.from_numpy(f32).cuda()).loss.item()
+    opt.backward()
+    gs = GraphStep(opt, sc.cameras, torch.from_numpy(u8).pin_memory())
+    loss = gs.replay().item()
+    opt.close()
+    assert loss == ref
 
 
 def test_cuda_graph_step_matches_eager(torch_cuda):
