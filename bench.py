@@ -426,7 +426,8 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
             "config": {"workload": args.config, "gaussians": sc.n, "views": V, "width": sc.width,
-                       "height": sc.height},
+                       "height": sc.height, "sh_degree": sc.sh_degree,
+                       "targets": ("u8 8-bit images (k / 255 in fp32)" if args.targets == "u8" else "fp32")},
             "cpu_baseline": {"value": round(value, 6), "unit": "steps/s", "cores": oracle.num_threads(),
                              "kind": "oracle", "sample": sample},
             "e2e": {"value": round(value, 6), "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
