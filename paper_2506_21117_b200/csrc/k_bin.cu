@@ -402,7 +402,7 @@ void launch_bin_count(const StepDims &d, const CamSet &cams, Scratch &s, cudaStr
 // 3. per unit: footprint columns and segment key
 void launch_bin_emit(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st)
 {
-    k_units<<<148 * 8, KU_THREADS, 0, st>>>(cams, s);
+    k_units<<<148 * 4, KU_THREADS, 0, st>>>(cams, s);   // persistent: 4 CTAs per SM (64 registers)
     g_launches += 1;
 }
 

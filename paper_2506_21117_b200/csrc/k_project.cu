@@ -514,7 +514,7 @@ void launch_project_cand(const Params &g, const StepDims &d, const CamSet &cams,
 
 void launch_project_exact(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st)
 {
-    const int grid = 148 * 8;
+    const int grid = 148 * 3;   // persistent: the 3 CTAs per SM the register budget allows
     switch (d.D) {
     case 0: k_project_exact<0><<<grid, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s); break;
     case 1: k_project_exact<1><<<grid, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s); break;
