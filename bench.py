@@ -327,7 +327,13 @@ def ncu_traffic(config: str, group: str):
     """DRAM bytes per launch of the group's kernel from the newest committed ncu --set full capture of
     this workload (profiles/r*_<config>_ncu_traffic.json), or None."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_{config}_ncu_traffic.json")))
+    import re
+
+    def version(path):   # r<round>_v<n>_...: newest = highest (round, n), compared as numbers
+        m = re.match(r"r(\d+)_v(\d+)", os.path.basename(path))
+        return (int(m.group(1)), int(m.group(2))) if m else (-1, -1)
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_{config}_ncu_traffic.json")), key=version)
     if not files or group not in GROUP_KERNELS:
         return None
     try:

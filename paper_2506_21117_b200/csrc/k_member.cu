@@ -203,7 +203,8 @@ void launch_active_mask(const Params &g, const StepDims &d, const CamSet &cams, 
         cudaMemsetAsync(s.mask, 1, (size_t)d.V * d.T, st);
     } else {
         cudaMemsetAsync(s.mdiff, 0, sizeof(int) * (size_t)d.V * (d.TY + 1) * (d.TX + 1), st);
-        int blocks = (int)std::min<long long>(((long long)d.n * d.V + 255) / 256, 148LL * 8);
+        // persistent over the A x V (Gaussian, view) pairs: 3 CTAs per SM fit its 78 registers
+        int blocks = (int)std::min<long long>(((long long)d.n * d.V + 255) / 256, 148LL * 3);
         if (blocks < 1) blocks = 1;
         k_active_rects<<<blocks, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, cams, s);
         g_launches++;
