@@ -235,11 +235,29 @@ __global__ void __launch_bounds__(256) k_seg_ranges(Scratch s, int n_seg)
 {
     const int n = s.cnt->overflow ? 0 : s.cnt->n_units32;
     const unsigned long long *k = s.sukey;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const unsigned e = (unsigned)(k[i] >> UK_SEG_SHIFT);
-        if (e >= (unsigned)n_seg) continue;
-        if (i == 0 || (unsigned)(k[i - 1] >> UK_SEG_SHIFT) != e) s.seg_off[e] = i;
-        if (i == n - 1 || (unsigned)(k[i + 1] >> UK_SEG_SHIFT) != e) s.seg_end[e] = i + 1;
+    constexpr unsigned NONE = 0xffffffffu;   // the segment "before 0" and "after n - 1"
+    // four consecutive keys per thread (two 16 B loads) and their two neighbours
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; 4 * t < n; t += gridDim.x * blockDim.x) {
+        const int i0 = 4 * t;
+        unsigned e[6];
+        if (i0 + 3 < n) {
+            const ulonglong2 a = reinterpret_cast<const ulonglong2 *>(k)[2 * t];
+            const ulonglong2 b = reinterpret_cast<const ulonglong2 *>(k)[2 * t + 1];
+            e[1] = (unsigned)(a.x >> UK_SEG_SHIFT); e[2] = (unsigned)(a.y >> UK_SEG_SHIFT);
+            e[3] = (unsigned)(b.x >> UK_SEG_SHIFT); e[4] = (unsigned)(b.y >> UK_SEG_SHIFT);
+        } else {
+#pragma unroll
+            for (int j = 1; j <= 4; j++) e[j] = i0 + j - 1 < n ? (unsigned)(k[i0 + j - 1] >> UK_SEG_SHIFT) : NONE;
+        }
+        e[0] = i0 > 0 ? (unsigned)(k[i0 - 1] >> UK_SEG_SHIFT) : NONE;
+        e[5] = i0 + 4 < n ? (unsigned)(k[i0 + 4] >> UK_SEG_SHIFT) : NONE;
+#pragma unroll
+        for (int j = 1; j <= 4; j++) {
+            const int i = i0 + j - 1;
+            if (i >= n || e[j] >= (unsigned)n_seg) continue;
+            if (e[j - 1] != e[j]) s.seg_off[e[j]] = i;
+            if (e[j + 1] != e[j]) s.seg_end[e[j]] = i + 1;
+        }
     }
 }
 
