@@ -358,7 +358,7 @@ def algorithmic_work(sc, n_views, st):
     return {
         "member": ("hbm", n * 16 + n * 4 + A * 4),
         "project_cand": ("hbm", n * 48 + C * 8),
-        "project_exact": ("hbm", C * 8 + R * (48 + 16 * K4 + 64 + 4 + 8)),
+        "project_exact": ("hbm", C * 8 + R * (48 + 16 * K4 + 64 + 4 + 4 + 8)),   # record, gid, rows, key
         "rec_sort": ("hbm", rpasses * R * 16),          # key-only passes: read + write 8 B
         # k_permute: key 8 + rrows 4 in, srid 4 + rcnt 4 out; scan: 4 + 4
         "bin_count": ("hbm", R * (20 + 8)),
