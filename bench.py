@@ -302,7 +302,7 @@ def run_ours(args):
             "mpix_per_s": {"rendered": round(sum(stats["n_active_tiles"]) * 256 * world * value / 1e6, 2),
                            "frame_equivalent": round(V * W * H * value / 1e6, 2)},
             "e2e": e2e, "gpu_launches": int(launches), "roofline": roof, "clocks": clocks,
-            "step_mode": ("CUDA graph replay (kernel breakdown from K eager steps; e2e eager)" if gstep is not None
+            "step_mode": (f"CUDA graph replay (kernel breakdown from K eager steps; e2e {args.e2e_mode})" if gstep is not None
                           else "eager"),
             "kernels_ms_per_step": {k: round(v["ms"] / args.steps, 4) for k, v in per.items()},
             "kernel_rates": groups,
