@@ -78,6 +78,10 @@ typedef struct {
     const float *quat;         /* (device) float4[n] */
     const float *log_scale;    /* (device) float4[n] */
     const float *sh;           /* (device) float4[n][K4] */
+    int64_t generation;        /* caller-maintained content generation: change it whenever the
+                                  arrays' contents change outside this library.  cls_render_bwd returns
+                                  CLS_ERR_STATE unless it sees the same arrays, n, degree and generation as
+                                  the fwd it follows, with no cls_adam_masked on those arrays in between */
 } cls_gaussians;
 
 /* Capacities fixed at cls_create; scratch is sized from them once. */
@@ -144,7 +148,8 @@ cls_status cls_destroy(cls_ctx *ctx);
  *   5. if targets != NULL: fused L1 loss over active-tile pixels,
  *      L = sum |C - T*| / (3 H W n_views_total), and dL/dC kept for cls_render_bwd (R19)
  * Arguments:
- *   g            (host struct, device arrays) scene; unchanged until the matching bwd
+ *   g            (host struct, device arrays) scene; unchanged until the matching bwd (its pointers,
+ *                n, degree and generation are recorded and checked by cls_render_bwd)
  *   cams         (host) cls_camera[n_views]
  *   n_views_total views of the whole step across ranks (>= n_views; loss normalisation)
  *   regions      (host) cls_region[n_regions], n_regions <= CLS_MAX_REGIONS (0 -> A = 0)
@@ -181,6 +186,8 @@ cls_status cls_copy_active(cls_ctx *ctx, int32_t *dst, void *stream);
  *   dL_dimages   (device) float[n_views][3][H][W] upstream gradient, or NULL to use the
  *                fused-L1 gradient of the fwd (CLS_ERR_STATE if the fwd had no targets)
  *   grad_active  (device) float4[A][ROW4] out (fully overwritten; row k belongs to idx[k])
+ * CLS_ERR_STATE if g is not the fwd's scene: other arrays, n, degree or generation, or a
+ * cls_adam_masked has updated those arrays since the fwd (the saved forward state is stale).
  */
 cls_status cls_render_bwd(cls_ctx *ctx, const cls_gaussians *g, const float *dL_dimages,
                           float *grad_active, void *stream);
@@ -221,6 +228,11 @@ cls_status cls_profile_read(cls_ctx *ctx, cls_profile_t *out);
  * of the last bwd -- float[n_views][A][12] (u, v, conic a, b, c, opacity, r, g, b, 0, 0, 0) --
  * into `out` (device).  For stage-wise parity tests. */
 cls_status cls_debug_grad2d(cls_ctx *ctx, float *out, void *stream);
+
+/* Optional: after cls_render_fwd, the final transmittance T_final of every pixel of an active tile
+ * -- device float[n_views][H][W], NaN elsewhere -- into `T_out` (device).  For the parity protocol's
+ * measured error window. */
+cls_status cls_debug_pixels(cls_ctx *ctx, float *T_out, void *stream);
 
 /* ---------------------------------------------------------------------------------------
  * NEXT-1: static-prefix partition, sphere pruning, densification on O^t.

@@ -26,6 +26,12 @@ _lib = None
 
 TILE = 16
 
+# Ambiguity window of the parity protocol: (da, dt1, dtk) = relative
+# error bound of an fp32 alpha, and of an fp32 T per unit of sum alpha/(1-alpha) and per composited
+# Gaussian.  Test infrastructure only: these flag pixels whose fp64 decisions an fp32 renderer may
+# take the other way; they are measured (tools/parity_window.py), not part of the method.
+AMB_WINDOW = (1e-5, 1e-5, 1.2e-7)
+
 
 def build(force: bool = False) -> str:
     """Compile the oracle (gcc, fp64, OpenMP, no FP contraction)."""
@@ -48,8 +54,8 @@ def lib():
             L.orc_membership.argtypes = [i64, P, i32, P, P, P, P, P]
             L.orc_project.argtypes = [i64, i32, P, P, P, P, P, P, P, d, d, d, d, i32, i32] + [P] * 11
             L.orc_render_view.restype = ctypes.c_int
-            L.orc_render_view.argtypes = [i64, P, P, P, P, P, P, P, P, P, i32, i32, P, i32, i32, P, d, P, d,
-                                          P, P, P, P, P, P, P, P, P]
+            L.orc_render_view.argtypes = [i64, P, P, P, P, P, P, P, P, P, i32, i32, P, i32, i32, P, d, P, d, d, d,
+                                          P, P, P, P, P, P, P, P, P, P]
             L.orc_backward_project.argtypes = [i64, i32, P, P, P, P, P, P, P, d, d, d, d, i32, i32, P, P, P, P]
             L.orc_adam.argtypes = [i64, P, P, P, P, P, P, d, d, d, i32]
             L.orc_sh_basis.argtypes = [i32, d, d, d, P]
@@ -120,7 +126,7 @@ def project(scene, view: int) -> Dict[str, np.ndarray]:
 
 def render(scene, view: int, active: np.ndarray, proj=None, literal: bool = False, all_tiles: bool = False,
            dL_dC: Optional[np.ndarray] = None, with_grad: bool = True, loss_scale: Optional[float] = None,
-           delta: float = 1e-5, use_target: bool = True) -> Dict[str, np.ndarray]:
+           window=None, use_target: bool = True) -> Dict[str, np.ndarray]:
     """Forward (+ per-pixel backward into 2D gradients) of one view."""
     cam = scene.cameras[view]
     W, H = cam.width, cam.height
@@ -138,17 +144,18 @@ def render(scene, view: int, active: np.ndarray, proj=None, literal: bool = Fals
     out = dict(image=np.zeros((3, H, W)), T_final=np.zeros((H, W)), n_contrib=np.zeros((H, W), np.int32),
                tile_mask=np.zeros((TY, TX), np.uint8), ambiguous=np.zeros((H, W), np.uint8),
                dL_dC=np.zeros((3, H, W)), grad2d=np.zeros((n, 9)) if with_grad else None,
-               sig=np.zeros((H, W), np.uint64))
+               sig=np.zeros((H, W), np.uint64), path=np.zeros((H, W, 2)))
+    da, dt1, dtk = AMB_WINDOW if window is None else window
     loss_sum = ctypes.c_double(0.0)
     bg = _f64(scene.bg)
     ntiles = lib().orc_render_view(
         n, _p(proj["culled"]), _p(proj["uv"]), _p(proj["conic"]), _p(proj["opac"]), _p(proj["rect"]),
         _p(proj["depth_key"]), _p(proj["rgb"]), _p(proj["clamped"]), _p(act), W, H, _p(bg),
         int(literal), int(all_tiles), None if target is None else _p(target), float(loss_scale),
-        None if dl_in is None else _p(dl_in), float(delta),
+        None if dl_in is None else _p(dl_in), float(da), float(dt1), float(dtk),
         _p(out["image"]), _p(out["T_final"]), _p(out["n_contrib"]), _p(out["tile_mask"]),
         _p(out["ambiguous"]), ctypes.byref(loss_sum), _p(out["dL_dC"]),
-        None if out["grad2d"] is None else _p(out["grad2d"]), _p(out["sig"]))
+        None if out["grad2d"] is None else _p(out["grad2d"]), _p(out["sig"]), _p(out["path"]))
     out["loss_sum"] = loss_sum.value
     out["n_active_tiles"] = int(ntiles)
     out["tile_mask"] = out["tile_mask"].astype(bool)
@@ -180,7 +187,7 @@ def backward_project(scene, view: int, active: np.ndarray, proj, grad2d: np.ndar
 
 def forward_backward(scene, views: Optional[Sequence[int]] = None, active: Optional[np.ndarray] = None,
                      literal: bool = False, all_tiles: bool = False, dL_dC=None, n_views_total=None,
-                     delta: float = 1e-5, with_grad: bool = True):
+                     window=None, with_grad: bool = True):
     """One full forward + backward over ``views`` (default all).  Returns
     dict(active, idx, loss, renders[list], grad [N, stride])."""
     if views is None:
@@ -199,7 +206,7 @@ def forward_backward(scene, views: Optional[Sequence[int]] = None, active: Optio
         proj = project(scene, v)
         up = None if dL_dC is None else dL_dC[j]
         r = render(scene, v, active, proj, literal=literal, all_tiles=all_tiles, dL_dC=up,
-                   with_grad=with_grad, loss_scale=scale, delta=delta)
+                   with_grad=with_grad, loss_scale=scale, window=window)
         if with_grad:
             backward_project(scene, v, active, proj, r["grad2d"], grad)
         loss += r["loss_sum"] * scale

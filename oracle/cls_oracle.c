@@ -334,11 +334,12 @@ static inline int in_rect(const int32_t *rc, int tx, int ty)
  * non-culled Gaussians (support rule applied per pixel); literal = 0 builds per-tile
  * candidate lists by brute force.  Both evaluate the same operations in the same order.
  * all_tiles = 1 makes every tile active (full-frame 3DGS step, "w/o Kernel").
- * ambiguous[p] = 1 if a discrete decision along p's path lies within the fp32 error bound of
- * its threshold: with eps = delta the relative error bound of an
- * fp32 alpha, a skip is ambiguous if |255 alpha - 1| < eps + 1e-7, and a termination test is
- * ambiguous if |1e4 T' - 1| < E + eps alpha/(1 - alpha) + 1e-7, where E = sum over the already
- * composited Gaussians of (eps alpha/(1 - alpha) + 1.2e-7) bounds the relative error of fp32 T.
+ * ambiguous[p] = 1 if a discrete decision along p's path lies within the error window of an
+ * fp32 renderer (test infrastructure; the window's constants are
+ * measured, not part of the method): with r_j = alpha_j / (1 - alpha_j), S1 = sum of r_j over the
+ * Gaussians composited so far and K their number, a skip is ambiguous if |255 alpha - 1| < da, a
+ * termination test if |1e4 T' - 1| < da r + dt1 S1 + dtk (K + 1).
+ * path[p] (optional, 2 doubles) = (S1, sqrt(sum r_j^2)) over p's composited Gaussians.
  * sig[p] (optional) = FNV hash of p's composited index sequence (discrete state of the pixel).
  * Returns the number of active tiles.
  */
@@ -346,10 +347,10 @@ int orc_render_view(int64_t n, const int32_t *culled, const double *uv, const do
                     const double *opac, const int32_t *rect, const float *depth_key, const double *rgb,
                     const int32_t *clamped, const uint8_t *active, int W, int H, const double *bg,
                     int literal, int all_tiles, const float *target, double loss_scale,
-                    const double *dL_dC_in, double delta,
+                    const double *dL_dC_in, double da, double dt1, double dtk,
                     double *image, double *T_final, int32_t *n_contrib, uint8_t *tile_mask,
                     uint8_t *ambiguous, double *loss_sum, double *dL_dC_out, double *grad2d,
-                    uint64_t *sig)
+                    uint64_t *sig, double *path)
 {
     const int TX = (W + TILE - 1) / TILE, TY = (H + TILE - 1) / TILE;
     const int64_t HW = (int64_t)H * W;
@@ -434,12 +435,13 @@ int orc_render_view(int64_t n, const int32_t *culled, const double *uv, const do
                         }
                         T_final[pix] = 1.0; n_contrib[pix] = 0; ambiguous[pix] = 0;
                         if (sig) sig[pix] = 0;
+                        if (path) path[2 * pix] = path[2 * pix + 1] = 0.0;
                         continue;
                     }
                     double T = 1.0, C[3] = {0.0, 0.0, 0.0};
                     int64_t K = 0;
                     int amb = 0;
-                    double Erel = 0.0;   /* relative error bound of an fp32 T (ambiguity only) */
+                    double S1 = 0.0, S2 = 0.0;   /* sums of r_j, r_j^2 (ambiguity window only) */
                     int64_t len = literal ? nv : tile_start[tile + 1] - tile_start[tile];
                     for (int64_t s = 0; s < len; s++) {
                         int64_t i = literal ? order[s].idx : tile_list[tile_start[tile] + s];
@@ -451,13 +453,14 @@ int orc_render_view(int64_t n, const int32_t *culled, const double *uv, const do
                         double G = exp(p);
                         double a = opac[i] * G;
                         if (a > 0.99) a = 0.99;
-                        if (fabs(255.0 * a - 1.0) < delta + 1e-7) amb = 1;
+                        if (fabs(255.0 * a - 1.0) < da) amb = 1;
                         if (a < 1.0 / 255.0) continue;
                         double Tn = T * (1.0 - a);
-                        double ea = delta * a / (1.0 - a);
-                        if (fabs(1e4 * Tn - 1.0) < Erel + ea + 1e-7) amb = 1;
+                        double ra = a / (1.0 - a);
+                        if (fabs(1e4 * Tn - 1.0) < da * ra + dt1 * S1 + dtk * (double)(K + 1)) amb = 1;
                         if (Tn < 1e-4) break;
-                        Erel += ea + 1.2e-7;
+                        S1 += ra;
+                        S2 += ra * ra;
                         for (int ch = 0; ch < 3; ch++) C[ch] += a * T * rgb[3 * i + ch];
                         if (K == cap) {
                             cap *= 2;
@@ -478,6 +481,7 @@ int orc_render_view(int64_t n, const int32_t *culled, const double *uv, const do
                         image[ch * HW + pix] = out[ch];
                     }
                     T_final[pix] = T; n_contrib[pix] = (int32_t)K; ambiguous[pix] = (uint8_t)amb;
+                    if (path) { path[2 * pix] = S1; path[2 * pix + 1] = sqrt(S2); }
                     if (sig) {   /* decision signature: the composited index sequence (FD harness) */
                         uint64_t hsh = 1469598103934665603ull;
                         for (int64_t k = 0; k < K; k++) hsh = (hsh ^ (uint64_t)(cidx[k] + 1)) * 1099511628211ull;

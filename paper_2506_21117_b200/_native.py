@@ -24,7 +24,7 @@ EXPORTS = ("cls_create", "cls_destroy", "cls_render_fwd", "cls_active", "cls_cop
            "cls_stats", "cls_profile_enable", "cls_profile_read", "cls_debug_grad2d", "cls_status_string",
            "cls_last_error", "cls_launch_count", "cls_partition_static", "cls_prune_outside", "cls_densify_stats",
            "cls_densify", "cls_majority_vote", "cls_fit_spheres", "cls_history_record", "cls_history_recover",
-           "cls_merge_updates", "cls_adam_masked_devstep", "cls_spatial_order")
+           "cls_merge_updates", "cls_adam_masked_devstep", "cls_spatial_order", "cls_debug_pixels")
 CLS_PROF_GROUPS = 16
 
 
@@ -46,7 +46,8 @@ class cls_region(ctypes.Structure):
 
 class cls_gaussians(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("sh_degree", ctypes.c_int32), ("mean_op", ctypes.c_void_p),
-                ("quat", ctypes.c_void_p), ("log_scale", ctypes.c_void_p), ("sh", ctypes.c_void_p)]
+                ("quat", ctypes.c_void_p), ("log_scale", ctypes.c_void_p), ("sh", ctypes.c_void_p),
+                ("generation", ctypes.c_int64)]
 
 
 class cls_limits(ctypes.Structure):
@@ -97,6 +98,7 @@ def _load():
                                   ctypes.c_float, ctypes.c_int32, V]
     L.cls_stats.argtypes = [V, P(cls_stats_t)]
     L.cls_debug_grad2d.argtypes = [V, V, V]
+    L.cls_debug_pixels.argtypes = [V, V, V]
     L.cls_profile_enable.argtypes = [V, ctypes.c_int32]
     L.cls_profile_read.argtypes = [V, P(cls_profile_t)]
     L.cls_status_string.argtypes = [ctypes.c_int]
@@ -125,7 +127,7 @@ def _load():
                  "cls_stats", "cls_debug_grad2d", "cls_profile_enable", "cls_profile_read", "cls_partition_static",
                  "cls_prune_outside", "cls_densify_stats", "cls_densify", "cls_majority_vote", "cls_fit_spheres",
                  "cls_history_record", "cls_history_recover", "cls_merge_updates", "cls_adam_masked_devstep",
-                 "cls_spatial_order"):
+                 "cls_spatial_order", "cls_debug_pixels"):
         getattr(L, name).restype = ctypes.c_int
     return L
 

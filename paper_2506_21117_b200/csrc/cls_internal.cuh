@@ -61,6 +61,7 @@ struct Counters {
     int n_units32;
     int scan_ticket, scan_ticket2;  // tile tickets of the two order-preserving scans of the binning
     int n_items;
+    int n_long_runs;        // runs of > 32 equal (view, depth) record keys (ordered by k_long_runs)
     int fwd_work, bwd_work;
     int overflow;           // bit0 records, bit1 pairs, bit2 active set
     int max_list;
@@ -96,6 +97,7 @@ struct Scratch {
     int *rec_gid;           // their Gaussian index (ties of the depth order, R13)
     unsigned *rrows;        // their number of tile rows (a 4 B array k_permute gathers from L2)
     unsigned *srid;         // record ids in (view, depth, Gaussian index) order (records stay in place)
+    int *long_runs;         // first sorted position of each run of > 32 equal (view, depth) keys
     long long max_records;
     int2 *cand;             // (Gaussian, view) candidates of the fp32 pre-test
     long long max_cand;

@@ -27,6 +27,11 @@ struct cls_ctx {
     cudaEvent_t ev_items = nullptr, ev_gather = nullptr;
     bool fwd_valid = false, has_targets = false, bwd_valid = false;
     bool captured = false;   // the last fwd was recorded into a CUDA graph: its events are not usable
+    // the scene of the last fwd (SURVEY §8(b) generation check of cls_render_bwd)
+    const void *g_ptr[4] = {nullptr, nullptr, nullptr, nullptr};
+    int64_t g_n = 0, g_gen = 0;
+    int g_deg = -1;
+    bool adam_since_fwd = false;   // a cls_adam_masked updated the fwd's arrays after it
     StepDims dims{};
     CamSet cams{};
     float3 bg{};
@@ -148,7 +153,7 @@ cls_status cls_destroy(cls_ctx *c)
     if (!c) return CLS_ERR_INVALID_ARGUMENT;
     cudaSetDevice(c->device);
     void *ptrs[] = {c->s.idx, c->s.ord, c->s.st_member, c->s.mask, c->s.sat, c->s.mdiff, c->s.rowmask, c->s.view_bbox, c->s.rec,
-                    c->s.srid, c->s.rec_gid, c->s.rrows, c->s.cand, c->s.rkey,
+                    c->s.srid, c->s.long_runs, c->s.rec_gid, c->s.rrows, c->s.cand, c->s.rkey,
                     c->s.rkey_alt, c->s.rcnt, c->s.ukey, c->s.ukey_alt,
                     c->s.roff, c->s.st_scan, c->s.seg_off, c->s.seg_end, c->s.st_tiles, c->s.items, c->s.item_of_tile,
                     c->s.first_active, c->s.vis, c->s.rs_counts, c->s.rs_totals, c->s.px_T, c->s.px_last, c->s.px_dl, c->s.tgt,
@@ -206,10 +211,10 @@ cls_status cls_create(cls_ctx **out, int device, const cls_limits *lim)
     Scratch &s = c->s;
     bool ok = dalloc(&s.idx, N) && dalloc(&s.ord, N) && dalloc(&s.st_member, N / 2048 + 2) && dalloc(&s.mask, VT) &&
               dalloc(&s.sat, SAT) && dalloc(&s.mdiff, SAT) && dalloc(&s.rowmask, V * c->maxTY * ((c->maxTX + 31) / 32)) &&
-              dalloc(&s.view_bbox, V) && dalloc(&s.rec, R) && dalloc(&s.srid, R) && dalloc(&s.rec_gid, R) && dalloc(&s.rrows, R) &&
+              dalloc(&s.view_bbox, V) && dalloc(&s.rec, R) && dalloc(&s.srid, R) && dalloc(&s.long_runs, R / 33 + 1) && dalloc(&s.rec_gid, R) && dalloc(&s.rrows, R) &&
               dalloc(&s.cand, R + R / 2 + 1024) && dalloc(&s.rkey, R) && dalloc(&s.rkey_alt, R) &&
-              dalloc(&s.rcnt, R) && dalloc(&s.ukey, P) &&
-              dalloc(&s.ukey_alt, P) && dalloc(&s.roff, R) &&
+              dalloc(&s.rcnt, R) && dalloc(&s.ukey, std::max(P, R)) &&
+              dalloc(&s.ukey_alt, std::max(P, R)) && dalloc(&s.roff, R) &&
               dalloc(&s.st_scan, std::max(R, P) / 2048 + 2) && dalloc(&s.seg_off, V * c->maxTY) &&
               dalloc(&s.seg_end, V * c->maxTY) && dalloc(&s.st_tiles, VT / 2048 + 2) &&
               dalloc(&s.items, VT) && dalloc(&s.item_of_tile, VT) && dalloc(&s.first_active, VT) &&
@@ -321,6 +326,23 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     Scratch s = c->s;
     s.max_items = d.V * d.T;
 
+    // where the targets live, decided before any work is enqueued: device (or managed) memory is read
+    // by the forward's loss epilogue; pinned + mapped host memory is gathered over the link (below)
+    const void *tsrc = nullptr;
+    if (targets) {
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, targets) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(c, CLS_ERR_INVALID_ARGUMENT, "targets: not a CUDA-visible pointer");
+        }
+        if (pa.type == cudaMemoryTypeHost) {
+            if (!pa.devicePointer) return fail(c, CLS_ERR_INVALID_ARGUMENT, "host targets must be pinned and mapped");
+            tsrc = pa.devicePointer;
+        } else if (pa.type != cudaMemoryTypeDevice && pa.type != cudaMemoryTypeManaged) {
+            // pageable host memory (cudaMemoryTypeUnregistered): the kernels cannot read it
+            return fail(c, CLS_ERR_INVALID_ARGUMENT, "targets: pageable host memory (pin it or copy it to the device)");
+        }
+    }
     {
         cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
         cudaStreamIsCapturing(st, &cap);
@@ -339,27 +361,18 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     // (8-bit targets, CLS_FLAG_TARGETS_U8: gathered and converted from host memory; read and
     // converted by the forward's loss epilogue from device memory)
     bool staged = false;
-    if (targets) {
-        cudaPointerAttributes pa{};
-        const void *src = nullptr;
-        if (cudaPointerGetAttributes(&pa, targets) == cudaSuccess && pa.type == cudaMemoryTypeHost) {
-            if (!pa.devicePointer) return fail(c, CLS_ERR_INVALID_ARGUMENT, "host targets must be pinned and mapped");
-            src = pa.devicePointer;
-        } else {
-            cudaGetLastError();   // unregistered pointers report an error on some drivers: device memory
-        }
-        if (src) {
-            cudaEventRecord(c->ev_items, st);
-            cudaStreamWaitEvent(c->side, c->ev_items, 0);
-            run(c, P_GATHER, c->side, [&] {
-                if (flags & CLS_FLAG_TARGETS_U8)
-                    launch_gather_targets_u8(d, cs, s, (const unsigned char *)src, c->side);
-                else
-                    launch_gather_targets(d, cs, s, (const float *)src, c->side);
-            });
-            cudaEventRecord(c->ev_gather, c->side);
-            staged = true;
-        }
+    if (tsrc) {
+        const void *src = tsrc;
+        cudaEventRecord(c->ev_items, st);
+        cudaStreamWaitEvent(c->side, c->ev_items, 0);
+        run(c, P_GATHER, c->side, [&] {
+            if (flags & CLS_FLAG_TARGETS_U8)
+                launch_gather_targets_u8(d, cs, s, (const unsigned char *)src, c->side);
+            else
+                launch_gather_targets(d, cs, s, (const float *)src, c->side);
+        });
+        cudaEventRecord(c->ev_gather, c->side);
+        staged = true;
     }
     run(c, P_PROJECT, st, [&] { launch_project_cand(p, d, cs, s, st); });
     cudaMemsetAsync(s.vis, 0, (size_t)d.V * (size_t)s.max_active, st);
@@ -387,6 +400,9 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     c->cams = cs;
     c->bg = bgc;
     c->has_targets = targets != nullptr;
+    c->g_ptr[0] = g->mean_op; c->g_ptr[1] = g->quat; c->g_ptr[2] = g->log_scale; c->g_ptr[3] = g->sh;
+    c->g_n = g->n; c->g_deg = g->sh_degree; c->g_gen = g->generation;
+    c->adam_since_fwd = false;
     c->fwd_valid = true;
     c->last_stream = st;
     return CLS_OK;
@@ -423,8 +439,14 @@ cls_status cls_render_bwd(cls_ctx *c, const cls_gaussians *g, const float *dL_di
     if (!c) return CLS_ERR_INVALID_ARGUMENT;
     if (!c->fwd_valid) return fail(c, CLS_ERR_STATE, "cls_render_bwd without a preceding cls_render_fwd");
     if (!g || !grad_active) return fail(c, CLS_ERR_INVALID_ARGUMENT, "null pointer argument");
-    if (g->n != c->dims.n || g->sh_degree != c->dims.D)
+    if (g->n != c->g_n || g->sh_degree != c->g_deg || g->mean_op != c->g_ptr[0] || g->quat != c->g_ptr[1] ||
+        g->log_scale != c->g_ptr[2] || g->sh != c->g_ptr[3])
         return fail(c, CLS_ERR_STATE, "Gaussian set differs from the one of the fwd");
+    if (g->generation != c->g_gen)
+        return fail(c, CLS_ERR_STATE, "Gaussian set changed since the fwd (generation %lld, fwd saw %lld)",
+                    (long long)g->generation, (long long)c->g_gen);
+    if (c->adam_since_fwd)
+        return fail(c, CLS_ERR_STATE, "cls_adam_masked updated the scene after the fwd: run a new fwd");
     if (!dL_dimages && !c->has_targets)
         return fail(c, CLS_ERR_STATE, "no dL_dimages and the fwd had no targets (no fused L1 gradient)");
     if (!aligned16(grad_active)) return fail(c, CLS_ERR_INVALID_ARGUMENT, "grad_active must be 16-byte aligned");
@@ -464,6 +486,8 @@ static cls_status adam_impl(cls_ctx *c, float *mean_op, float *quat, float *log_
         launch_adam(c->dims, c->s, (float4 *)mean_op, (float4 *)quat, (float4 *)log_scale, (float4 *)sh, (float4 *)m,
                     (float4 *)v, (const float4 *)grad_active, lr, beta1, beta2, eps, bc1, bc2, step_dev, st);
     });
+    if (mean_op == c->g_ptr[0] || quat == c->g_ptr[1] || log_scale == c->g_ptr[2] || sh == c->g_ptr[3])
+        c->adam_since_fwd = true;   // the saved forward state no longer matches the parameters
     c->last_stream = st;
     return check_cuda(c, "cls_adam_masked");
 }
@@ -561,6 +585,17 @@ cls_status cls_debug_grad2d(cls_ctx *c, float *out, void *stream)
     const size_t bytes = sizeof(float4) * 3 * (size_t)c->dims.V * (size_t)(*c->h_A);
     cudaMemcpyAsync(out, c->s.grad2d, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
     return check_cuda(c, "cls_debug_grad2d");
+}
+
+cls_status cls_debug_pixels(cls_ctx *c, float *T_out, void *stream)
+{
+    if (!c || !T_out) return CLS_ERR_INVALID_ARGUMENT;
+    if (!c->fwd_valid) return fail(c, CLS_ERR_STATE, "cls_debug_pixels before cls_render_fwd");
+    cudaSetDevice(c->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaMemsetAsync(T_out, 0xff, sizeof(float) * (size_t)c->dims.V * c->dims.H * c->dims.W, st);   // NaN: not rendered
+    launch_debug_pixels(c->dims, c->cams, c->s, T_out, st);
+    return check_cuda(c, "cls_debug_pixels");
 }
 
 // ---------------------------------------------------------------------------

@@ -33,6 +33,7 @@ __device__ __forceinline__ void adam_lane(float &p, float &m, float &v, float g,
 
 __global__ void __launch_bounds__(256) k_adam(const __grid_constant__ AdamArgs a, Scratch s)
 {
+    if (s.cnt->overflow) return;   // capacity overflow: the gradient rows are not valid, nothing is updated
     const int A = s.cnt->A;
     float bc1 = a.bc1, bc2 = a.bc2;
     if (a.step_dev) {   // same double-precision bias correction as the host path
@@ -80,7 +81,10 @@ __global__ void __launch_bounds__(256) k_adam(const __grid_constant__ AdamArgs a
     }
 }
 
-__global__ void k_step_inc(int *step_dev) { *step_dev += 1; }
+__global__ void k_step_inc(Scratch s, int *step_dev)
+{
+    if (!s.cnt->overflow) *step_dev += 1;   // a skipped update does not advance t
+}
 
 void launch_adam(const StepDims &d, const Scratch &s, float4 *mean_op, float4 *quat, float4 *log_scale, float4 *sh,
                  float4 *m, float4 *v, const float4 *grad_active, const float lr[6], float b1, float b2, float eps,
@@ -98,7 +102,7 @@ void launch_adam(const StepDims &d, const Scratch &s, float4 *mean_op, float4 *q
     k_adam<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(a, s);
     g_launches++;
     if (step_dev) {   // the next replay uses the next step
-        k_step_inc<<<1, 1, 0, st>>>(step_dev);
+        k_step_inc<<<1, 1, 0, st>>>(s, step_dev);
         g_launches++;
     }
 }

@@ -80,44 +80,113 @@ __global__ void __launch_bounds__(TSCAN_THREADS) k_tiles_scan(int total, Scratch
     }
 }
 
-// 2. records gathered into (view, depth, index) order (one 64 B record per access) and the
-// number of tile rows of each footprint rect: the work units of the binning are (record, tile row)
-// pairs, so every thread does the same small amount of work however tall a footprint is.
-// sorted position i -> record id; ties of the (view, depth) key are ordered by Gaussian index
-// (R13): inside a run of equal keys (rare, short) position i takes the run member of rank i - start
-__device__ __forceinline__ unsigned permute_source(const Scratch &s, const unsigned long long *key, int i, int n)
-{
-    const unsigned long long k = key[i] >> RK_IDX_BITS;   // (view, depth); the low bits carry the record id
-    unsigned r = (unsigned)(key[i] & RK_IDX_MASK);
-    if ((i > 0 && (key[i - 1] >> RK_IDX_BITS) == k) || (i + 1 < n && (key[i + 1] >> RK_IDX_BITS) == k)) {
-        int a = i, b = i + 1;
-        while (a > 0 && (key[a - 1] >> RK_IDX_BITS) == k) a--;
-        while (b < n && (key[b] >> RK_IDX_BITS) == k) b++;
-        for (int j = a; j < b; j++) {
-            const unsigned rj = (unsigned)(key[j] & RK_IDX_MASK);
-            const int gj = s.rec_gid[rj];
-            int rank = 0;
-            for (int q = a; q < b; q++) rank += s.rec_gid[(unsigned)(key[q] & RK_IDX_MASK)] < gj;
-            if (rank == i - a) {
-                r = rj;
-                break;
-            }
-        }
-    }
-    return r;
-}
-
-// sorted position i -> record id (ties re-ordered by Gaussian index) and the record's number of
-// tile rows; the records themselves stay where k_project_exact wrote them (units and the raster
-// address them by id: no 64 B record copy)
+// 2. sorted position i -> record id, with ties of the (view, depth) key ordered by Gaussian index
+// (R13).  The radix sort is stable in creation order, which is not index order, so every run of
+// equal keys is re-ordered here: a run of at most 32 records by its first thread (insertion sort
+// of (Gaussian index, record id)), a longer run by one CTA of k_long_runs (merge sort in global
+// memory, O(L log^2 L)) -- coplanar Gaussians seen by an axis-aligned camera make runs of thousands.
+// Positions outside runs map directly.  The records themselves stay where k_project_exact wrote
+// them (units and the raster address them by id: no 64 B record copy).
+#define SHORT_RUN 32
 __global__ void __launch_bounds__(256) k_permute(Scratch s)
 {
     const int n = s.cnt->overflow ? 0 : min(s.cnt->n_records, (int)s.max_records);
     const unsigned long long *key = s.rskey;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const unsigned r = permute_source(s, key, i, n);
-        s.srid[i] = r;
-        s.rcnt[i] = s.rrows[r];   // y1 - y0 of the record (its 64 B row is not touched here)
+        const unsigned long long k = key[i] >> RK_IDX_BITS;   // (view, depth); the low bits carry the record id
+        const unsigned r = (unsigned)(key[i] & RK_IDX_MASK);
+        const bool eq_prev = i > 0 && (key[i - 1] >> RK_IDX_BITS) == k;
+        const bool eq_next = i + 1 < n && (key[i + 1] >> RK_IDX_BITS) == k;
+        if (!eq_prev && !eq_next) {
+            s.srid[i] = r;
+            s.rcnt[i] = s.rrows[r];   // y1 - y0 of the record (its 64 B row is not touched here)
+            continue;
+        }
+        if (eq_prev) continue;   // ordered by the run's first thread or CTA
+        if (i + SHORT_RUN < n && (key[i + SHORT_RUN] >> RK_IDX_BITS) == k) {   // longer than SHORT_RUN
+            const int slot = atomicAdd(&s.cnt->n_long_runs, 1);
+            s.long_runs[slot] = i;
+            continue;
+        }
+        unsigned long long p[SHORT_RUN];   // (Gaussian index << 32 | record id): distinct, ascending = R13
+        int L = 0;
+        while (i + L < n && L < SHORT_RUN && (key[i + L] >> RK_IDX_BITS) == k) {
+            const unsigned rj = (unsigned)(key[i + L] & RK_IDX_MASK);
+            const unsigned long long v = ((unsigned long long)(unsigned)s.rec_gid[rj] << 32) | rj;
+            int q = L++;
+            while (q > 0 && p[q - 1] > v) {
+                p[q] = p[q - 1];
+                q--;
+            }
+            p[q] = v;
+        }
+        for (int q = 0; q < L; q++) {
+            const unsigned rj = (unsigned)p[q];
+            s.srid[i + q] = rj;
+            s.rcnt[i + q] = s.rrows[rj];
+        }
+    }
+}
+
+// runs of more than SHORT_RUN equal keys: one CTA per run, bottom-up merge sort of the
+// (Gaussian index << 32 | record id) values through two global buffers (free at this point: the
+// unit keys are written later)
+__global__ void __launch_bounds__(256) k_long_runs(Scratch s, unsigned long long *bufa, unsigned long long *bufb)
+{
+    __shared__ int s_end;
+    const int n = s.cnt->overflow ? 0 : min(s.cnt->n_records, (int)s.max_records);
+    const int n_runs = s.cnt->n_long_runs;
+    const unsigned long long *key = s.rskey;
+    for (int e = blockIdx.x; e < n_runs; e += gridDim.x) {
+        const int a = s.long_runs[e];
+        const unsigned long long k = key[a] >> RK_IDX_BITS;
+        if (threadIdx.x == 0) {   // run end: exponential then binary search
+            int lo = a, step = 1;
+            while (lo + step < n && (key[lo + step] >> RK_IDX_BITS) == k) {
+                lo += step;
+                step <<= 1;
+            }
+            int hi = min(lo + step, n);   // key[lo] == k, key[hi] != k or hi == n
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if ((key[mid] >> RK_IDX_BITS) == k) lo = mid;
+                else hi = mid;
+            }
+            s_end = hi;
+        }
+        __syncthreads();
+        const int L = s_end - a;
+        unsigned long long *src = bufa + a, *dst = bufb + a;
+        for (int j = threadIdx.x; j < L; j += blockDim.x) {
+            const unsigned rj = (unsigned)(key[a + j] & RK_IDX_MASK);
+            src[j] = ((unsigned long long)(unsigned)s.rec_gid[rj] << 32) | rj;
+        }
+        __syncthreads();
+        for (int w = 1; w < L; w <<= 1) {
+            for (int j = threadIdx.x; j < L; j += blockDim.x) {
+                const int blk = j & ~(2 * w - 1), mid = min(blk + w, L), end = min(blk + 2 * w, L);
+                const unsigned long long x = src[j];
+                // position among the other half (values are distinct)
+                int lo = j < mid ? mid : blk, hi = j < mid ? end : mid;
+                while (lo < hi) {
+                    const int m = (lo + hi) >> 1;
+                    if (src[m] < x) lo = m + 1;
+                    else hi = m;
+                }
+                const int out = j < mid ? j + (lo - mid) : (j - mid) + lo;
+                dst[out] = x;
+            }
+            __syncthreads();
+            unsigned long long *t = src;
+            src = dst;
+            dst = t;
+        }
+        for (int j = threadIdx.x; j < L; j += blockDim.x) {
+            const unsigned rj = (unsigned)src[j];
+            s.srid[a + j] = rj;
+            s.rcnt[a + j] = s.rrows[rj];
+        }
+        __syncthreads();
     }
 }
 
@@ -358,11 +427,13 @@ __global__ void __launch_bounds__(256) k_gather_targets_u8(const __grid_constant
     const int W = cams.W, H = cams.H, TX = cams.TX, T = cams.T;
     const size_t HW = (size_t)H * W;
     const bool vec = (W & 15) == 0 && (reinterpret_cast<size_t>(targets) & 15) == 0;
-    const int total = ((n_items + 31) / 32) * 3 * 16 * 32;   // (group, ch, row, item-in-group)
-    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < total; f += gridDim.x * blockDim.x) {
-        const int j = f & 31, row = (f >> 5) & 15;
-        const int r3 = f >> 9;
-        const int g = r3 / 3, ch = r3 - 3 * g, item = g * 32 + j;
+    // 64-bit indices: 1536 lanes per 32 items overflow int beyond ~1.4M active tiles
+    const long long total = (long long)((n_items + 31) / 32) * 3 * 16 * 32;   // (group, ch, row, item-in-group)
+    for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < total;
+         f += (long long)gridDim.x * blockDim.x) {
+        const int j = (int)(f & 31), row = (int)((f >> 5) & 15);
+        const long long r3 = f >> 9;
+        const int g = (int)(r3 / 3), ch = (int)(r3 - 3ll * g), item = g * 32 + j;
         if (item >= n_items) continue;
         const int e = s.items[item];
         const int v = e / T, t = e - v * T;
@@ -414,9 +485,10 @@ void launch_bin_count(const StepDims &d, const CamSet &cams, Scratch &s, cudaStr
 {
     const int R = (int)s.max_records;
     k_permute<<<148 * 8, 256, 0, st>>>(s);
+    k_long_runs<<<148, 256, 0, st>>>(s, s.ukey, s.ukey_alt);   // exits at once without long runs
     scan_excl_u32(s.rcnt, s.roff, &s.cnt->n_records, R, s.st_scan, &s.cnt->scan_ticket, &s.cnt->n_units,
                   &s.cnt->overflow, st);
-    g_launches += 1;
+    g_launches += 2;
 }
 
 // 3. per unit: footprint columns and segment key

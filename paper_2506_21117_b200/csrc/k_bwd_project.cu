@@ -217,6 +217,7 @@ k_bwd_project(const float4 *__restrict__ mean_op, const float4 *__restrict__ qua
               const float4 *__restrict__ log_scale, const float4 *__restrict__ sh, int n,
               const __grid_constant__ CamSet cams, Scratch s, float4 *__restrict__ out)
 {
+    if (s.cnt->overflow) return;   // capacity overflow (records, pairs, A > max_active): no rows are valid
     const int A = s.cnt->A;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < A; k += gridDim.x * blockDim.x)
         bwd_project_row<D>(mean_op, quat, log_scale, sh, n, cams, s, out, A, k);

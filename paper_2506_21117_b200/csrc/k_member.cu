@@ -210,11 +210,8 @@ void launch_active_mask(const Params &g, const StepDims &d, const CamSet &cams, 
         g_launches++;
     }
     const size_t smem = sizeof(int) * (size_t)(d.TY + 1) * (d.TX + 1) + (size_t)d.TX * d.TY;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_sat<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-    }
+    static std::atomic<unsigned long long> attr{0};
+    per_device_once(attr, [] { cudaFuncSetAttribute(k_sat<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
     if (smem <= 200 * 1024) k_sat<true><<<d.V, SAT_THREADS, smem, st>>>(cams, s, d.all_tiles);
     else k_sat<false><<<d.V, SAT_THREADS, 0, st>>>(cams, s, d.all_tiles);
     g_launches++;

@@ -499,11 +499,10 @@ k_project_exact(const float4 *__restrict__ mean_op, const float4 *__restrict__ q
 void launch_project_cand(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st)
 {
     size_t smem = sizeof(unsigned) * (size_t)d.V * d.TY * ((d.TX + 31) / 32);
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};
+    per_device_once(attr, [] {
         cudaFuncSetAttribute(k_project_cand<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-        attr = true;
-    }
+    });
     const int blocks = std::min((d.n + PC_THREADS - 1) / PC_THREADS, 148 * 3);
     if (smem <= 96 * 1024)
         k_project_cand<true><<<blocks, PC_THREADS, smem, st>>>(g.mean_op, g.quat, g.log_scale, d.n, cams, s);

@@ -824,6 +824,29 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
     if (lane == 0 && evals) atomicAdd(&s.cnt->bwd_evals, evals);
 }
 
+// debug export (cls_debug_pixels): the forward's final transmittance |T| of every pixel of an active
+// tile into a [V][H][W] image (the caller pre-fills the rest)
+__global__ void k_debug_pixels(const __grid_constant__ CamSet cams, Scratch s, float *out)
+{
+    const int n_items = s.cnt->overflow ? 0 : s.cnt->n_items;
+    const int W = cams.W, H = cams.H, TX = cams.TX, T = cams.T;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)n_items * CLS_BLOCK_PIX;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int item = (int)(e / CLS_BLOCK_PIX), pl = (int)(e % CLS_BLOCK_PIX);
+        const int it = s.items[item];
+        const int v = it / T, t = it - v * T;
+        const int tid = pl % RT_THREADS, p = pl / RT_THREADS;   // pixel slot tid + p * RT_THREADS
+        const int x = (t % TX) * CLS_TILE + (tid & 15), y = (t / TX) * CLS_TILE + (tid >> 4) + 4 * p;
+        if (x < W && y < H) out[((size_t)v * H + y) * W + x] = s.px_T[e];
+    }
+}
+
+void launch_debug_pixels(const StepDims &d, const CamSet &cams, const Scratch &s, float *out, cudaStream_t st)
+{
+    k_debug_pixels<<<148 * 4, 256, 0, st>>>(cams, s, out);
+    g_launches++;
+}
+
 __global__ void k_zero_grad2d(Scratch s, int V, long long cap)
 {
     const long long A = s.cnt->A;

@@ -255,11 +255,10 @@ static void rs_pass(unsigned long long *kin, unsigned long long *kout, unsigned 
                     int max_n, int shift, unsigned *counts, unsigned *totals, const int *skip, cudaStream_t st)
 {
     constexpr size_t SM = rs_smem<BITS, VALS>();
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};
+    per_device_once(attr, [&] {
         cudaFuncSetAttribute(k_rs_downsweep<BITS, VALS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
-        attr = true;
-    }
+    });
     k_rs_upsweep<BITS><<<RS_GRID, RS_THREADS, 0, st>>>(kin, n_ptr, max_n, shift, counts, skip);
     k_rs_scan<<<((1 << BITS) + 7) / 8, 256, 0, st>>>(counts, totals, 1 << BITS, RS_GRID);
     k_rs_downsweep<BITS, VALS><<<RS_GRID, RS_THREADS, SM, st>>>(kin, kout, vin, vout, n_ptr, max_n, shift, counts,

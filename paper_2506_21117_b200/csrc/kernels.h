@@ -1,6 +1,7 @@
 // kernels.h -- host launchers of the step's kernels (one per subsystem of BASELINE north_star).
 #pragma once
 #include <algorithm>
+#include <atomic>
 
 #include "cls_internal.cuh"
 
@@ -50,6 +51,7 @@ void launch_fill_bg(const StepDims &d, const Scratch &s, float *images, float3 b
 void launch_loss(const Scratch &s, float loss_scale, float *loss, cudaStream_t st);
 void launch_loss_staged(const StepDims &d, const CamSet &cams, const Scratch &s, float loss_scale, cudaStream_t st);
 // (5) backward raster + backward projection                    (k_raster.cu, k_bwd_project.cu)
+void launch_debug_pixels(const StepDims &d, const CamSet &cams, const Scratch &s, float *out, cudaStream_t st);
 void launch_zero_grad2d(const StepDims &d, const Scratch &s, long long cap, cudaStream_t st);
 void launch_bwd_raster(const StepDims &d, const Scratch &s, const float *dL_dimages, float3 bg, cudaStream_t st);
 void launch_bwd_project(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s,
@@ -95,6 +97,20 @@ void launch_vote(const float4 *mean_op, int n, const CamSet &cams, const uint8_t
 void launch_fit_spheres(const float4 *mean_op, int n, const int *labels, int K, double *sums, unsigned long long *keys,
                         unsigned long long *keys_alt, unsigned *vals, unsigned *vals_alt, int *starts, int *n_dev,
                         unsigned *counts, unsigned *totals, float *centres, float *radii, cudaStream_t st);
+
+// once per (kernel attribute, device): cudaFuncSetAttribute applies to the current device only, so
+// a ctx on a second device sets it again.  Setting it twice is harmless; the bit is published only
+// after the attribute is set, so a thread that sees it set may launch.
+template <typename F>
+inline void per_device_once(std::atomic<unsigned long long> &done, F &&set_attr)
+{
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    set_attr();
+    done.fetch_or(bit, std::memory_order_release);
+}
 
 extern int64_t g_launches;   // kernels launched by this process through libcls (host counter)
 

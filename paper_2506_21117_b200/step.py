@@ -56,9 +56,15 @@ class GaussianParams:
         self.n_static = 0
         self._set_n(n)
         self.step = 0
+        self.generation = 0   # bumped by every host-side change of the rows (cls_gaussians.generation)
+
+    def touch(self):
+        """Record that the rows were changed outside libcls (a new content generation)."""
+        self.generation += 1
 
     def _set_n(self, n: int):
         self.n = int(n)
+        self.generation = getattr(self, "generation", 0) + 1
         self.mean_op, self.quat, self.log_scale, self.sh = self._mo[:n], self._q[:n], self._ls[:n], self._sh[:n]
         self.m, self.v = self._m[:n], self._v[:n]
         self.grad_accum, self.grad_count = self._acc[:n], self._cnt[:n]
@@ -86,7 +92,7 @@ class GaussianParams:
 
     def struct(self) -> N.cls_gaussians:
         return N.cls_gaussians(self.n, self.sh_degree, self.mean_op.data_ptr(), self.quat.data_ptr(),
-                               self.log_scale.data_ptr(), self.sh.data_ptr())
+                               self.log_scale.data_ptr(), self.sh.data_ptr(), self.generation)
 
     def rows(self, idx: torch.Tensor) -> torch.Tensor:
         """Gather ABI rows [len(idx), ROW4, 4] of the parameters (layout helper for tests)."""
@@ -232,6 +238,7 @@ class LocalOptimizer:
             # float32, or uint8 8-bit images (k stands for the fp32 k / 255; CLS_FLAG_TARGETS_U8)
             assert targets.is_contiguous() and targets.dtype in (torch.float32, torch.uint8) and \
                 tuple(targets.shape) == (V, 3, H, W)
+            assert targets.is_cuda or targets.is_pinned(), "targets: device or pinned host memory"
         g = self.params.struct()
         st = check(lib.cls_render_fwd(
             self.ctx, ctypes.byref(g), cams, V, int(n_views_total or V), self._reg, len(self.regions), self.bg,
@@ -244,6 +251,7 @@ class LocalOptimizer:
             ctypes.c_void_p(_stream_ptr(stream))), self.ctx)
         self._A = None
         self._fwd_views = V
+        self._dims = (V, H, W)
         return ForwardResult(loss, img, tm)
 
     def active_count(self) -> int:
@@ -287,6 +295,14 @@ class LocalOptimizer:
         check(lib.cls_debug_grad2d(self.ctx, ctypes.c_void_p(out.data_ptr()),
                                    ctypes.c_void_p(_stream_ptr(None))), self.ctx)
         return out[:, :A]
+
+    def debug_pixels(self) -> torch.Tensor:
+        """T_final [V, H, W] of the last fwd (NaN outside the active tiles): parity diagnostics."""
+        d = self._dims
+        out = torch.empty(d, dtype=torch.float32, device=self.params.device)
+        check(lib.cls_debug_pixels(self.ctx, ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(_stream_ptr(None))),
+              self.ctx)
+        return out
 
     def stats(self) -> dict:
         st = N.cls_stats_t()

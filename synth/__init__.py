@@ -312,6 +312,36 @@ def tiny_scene(seed: int, n: int = 8, width: int = 32, height: int = 32, sh_degr
                  sh.astype(np.float32), sh_degree, cams, regions, targets)
 
 
+def coplanar_scene(seed: int = 3, grid=(50, 40), n_random: int = 600, width: int = 160, height: int = 128,
+                   sh_degree: int = 1) -> Scene:
+    """Depth-tie stress scene (reading R13): an axis-aligned camera at the origin (R = I, t = 0)
+    looking along +z at a grid of Gaussians on the plane z = 3 -- every grid Gaussian has exactly the
+    same view depth, one run of grid[0] x grid[1] equal depth keys -- plus a few on the plane z = 4
+    (a short run) and random ones in front of and behind them.  Rows are shuffled, so the index
+    order that breaks the ties is unrelated to the spatial order."""
+    rng = np.random.default_rng(seed)
+    gx, gy = grid
+    xs, ys = np.meshgrid(np.linspace(-1.1, 1.1, gx), np.linspace(-0.85, 0.85, gy))
+    plane = np.stack([xs.ravel(), ys.ravel(), np.full(gx * gy, 3.0)], 1)
+    short = np.stack([rng.uniform(-0.5, 0.5, 20), rng.uniform(-0.4, 0.4, 20), np.full(20, 4.0)], 1)
+    rand = np.stack([rng.uniform(-1.2, 1.2, n_random), rng.uniform(-0.9, 0.9, n_random),
+                     rng.uniform(2.0, 5.0, n_random)], 1)
+    means = np.concatenate([plane, short, rand]).astype(np.float32)
+    n = len(means)
+    perm = rng.permutation(n)
+    means = means[perm]
+    ls = rng.normal(-3.3, 0.3, (n, 3)).astype(np.float32)
+    q = _unit_quats(rng, n)
+    op = rng.normal(0.0, 1.0, n).astype(np.float32)
+    sh = _sh(rng, n, sh_degree)
+    focal = (width / 2.0) / math.tan(math.radians(60.0) / 2.0)
+    cam = Camera(np.eye(3, dtype=np.float32), np.zeros(3, np.float32), float(focal), float(focal),
+                 width / 2.0, height / 2.0, int(width), int(height))
+    regions = [Region(REGION_SPHERE, np.array([0.2, 0.1, 3.0], np.float32), np.zeros(3, np.float32), 0.45)]
+    targets = rng.random((1, 3, height, width), dtype=np.float32)
+    return Scene("coplanar", means, ls, q, op, sh, sh_degree, [cam], regions, targets)
+
+
 def scene_from_arrays(means, log_scales, quats, opacity_logits, sh, sh_degree, cameras, regions,
                       targets=None, name="custom") -> Scene:
     return Scene(name, np.asarray(means, np.float32), np.asarray(log_scales, np.float32),

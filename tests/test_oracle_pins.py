@@ -416,3 +416,125 @@ def test_sh_orthonormal(oracle_lib):
             Y = oracle.sh_basis(3, [st * math.cos(ph), st * math.sin(ph), ct])
             G += wt * (2 * np.pi / len(phis)) * np.outer(Y, Y)
     assert np.allclose(G, np.eye(16), atol=1e-12)
+
+
+# ---------------------------------------------------------------------------
+# R5 near plane, R10 frustum clamp of J, R13 depth ties (previously unpinned)
+# ---------------------------------------------------------------------------
+
+def test_r5_near_plane_threshold(oracle_lib):
+    """3DGS near plane (R5): culled iff t_z <= 0.2.  Camera R = I, t = 0, so t_z = z exactly
+    (fp64 means)."""
+    cam = _one_cam()
+    zs = np.array([0.19, 0.2, 0.2 + 1e-12, 0.21, 0.5])
+    means = np.stack([np.zeros(5), np.zeros(5), zs], 1)
+    sc = _scene(means, np.log(np.full((5, 3), 0.002)), [[1, 0, 0, 0]] * 5, np.zeros(5), np.zeros((5, 1, 3)), 0,
+                [cam])
+    sc.means = means
+    p = oracle.project(sc, 0)
+    assert list(p["culled"]) == [1, 1, 0, 0, 0]
+    assert p["tcam"][:, 2] == pytest.approx(zs, abs=0)
+
+
+def _clamp_cam():
+    # W = H = 64, f = 100: tan(fov_x / 2) = W / (2 f) = 0.32, clamp limit L = 1.3 * 0.32 = 0.416
+    return _one_cam(W=64, H=64, f=100.0, cx=32.0, cy=32.0)
+
+
+@pytest.mark.parametrize("xz,yz", [(0.5, 0.0), (-0.5, 0.0), (0.0, 0.47), (0.45, -0.46), (0.2, 0.1)])
+def test_r10_frustum_clamp_closed_form(oracle_lib, xz, yz):
+    """R10: J uses x/z, y/z clamped to +-1.3 tan(fov/2).  For an isotropic Gaussian (Sigma = s^2 I)
+    seen by R = I the closed form is Sigma' = s^2 J J^T + 0.3 I with
+    J = [[f/z, 0, -f xc/z], [0, f/z, -f yc/z]], xc = clamp(x/z, -L, L): A = (f s / z)^2 (1 + xc^2) + 0.3,
+    B = (f s / z)^2 xc yc, C = (f s / z)^2 (1 + yc^2) + 0.3.  The centre u, v uses the UNclamped x/z."""
+    L = 1.3 * 64 / (2 * 100.0)
+    z, s = 2.0, 0.4                                   # a large splat: its footprint reaches the image
+    means = np.array([[xz * z, yz * z, z]])
+    sc = _scene(means, np.log([[s] * 3]), [[1, 0, 0, 0]], [0.0], np.zeros((1, 1, 3)), 0, [_clamp_cam()])
+    sc.means = means
+    sc.log_scales = np.log([[s] * 3])
+    p = oracle.project(sc, 0)
+    assert p["culled"][0] == 0
+    xc, yc = min(max(xz, -L), L), min(max(yz, -L), L)
+    k = (100.0 * s / z) ** 2
+    assert p["cov2d"][0] == pytest.approx([k * (1 + xc * xc) + 0.3, k * xc * yc, k * (1 + yc * yc) + 0.3],
+                                          rel=1e-12, abs=1e-9)
+    assert p["uv"][0] == pytest.approx([100.0 * xz + 32.0 - 0.5, 100.0 * yz + 32.0 - 0.5], rel=1e-12)
+
+
+def test_r13_depth_ties_by_index(oracle_lib):
+    """R13: the depth key is the fp32 rounding of the fp64 view depth and equal keys are ordered by
+    ascending Gaussian index -- even when the true (fp64) depths differ below fp32 resolution.
+    Two coincident splats (opacity 0.5 red, 0.6 green): the transmittance product of V2 in index
+    order, C = (0.5, 0.6 (1 - 0.5), 0) = (0.5, 0.3, 0); with the rows swapped, (0.5 (1 - 0.6), 0.6, 0)."""
+    cam = _one_cam()
+    for behind0 in (1e-9, 0.0):           # row 0 slightly BEHIND row 1 in fp64, same fp32 key; or exactly tied
+        means = np.array([[0.0, 0.0, 2.0 + behind0], [0.0, 0.0, 2.0]])
+        ops = np.log(np.array([0.5, 0.6]) / (1 - np.array([0.5, 0.6])))
+        sh = _dc(np.array([[1.0, 0, 0], [0, 1.0, 0]])).reshape(2, 1, 3)
+        for order in ((0, 1), (1, 0)):
+            o = list(order)
+            sc = _scene(means[o], np.log(np.full((2, 3), 0.05)), [[1, 0, 0, 0]] * 2, ops[o], sh[o], 0, [cam])
+            sc.means, sc.opacity_logits, sc.sh = means[o], ops[o], sh[o]
+            sc.log_scales = np.log(np.full((2, 3), 0.05))
+            p = oracle.project(sc, 0)
+            assert p["depth_key"][0] == p["depth_key"][1]
+            r = oracle.render(sc, 0, np.ones(2, bool), p, use_target=False, with_grad=False)
+            first_red = order == (0, 1)       # index 0 holds the red splat
+            expect = [0.5, 0.3, 0.0] if first_red else [0.2, 0.6, 0.0]
+            assert r["image"][:, 32, 32] == pytest.approx(expect, abs=1e-12)
+
+
+def test_p7_finite_differences_clamped_jacobian(oracle_lib):
+    """P7 on Gaussians whose J is frustum-clamped (R10) in x, in y and in both, next to an unclamped
+    one: the clamped-branch derivative (dJ02/dt_x = 0, dJ02/dt_z = +-f L / t_z^2) against central
+    finite differences of the smooth probe loss.  Every clamped Gaussian sits >= 0.05 beyond the limit
+    and every unclamped one >= 0.05 inside it, so no +-1e-4 perturbation changes a clamp decision."""
+    W = H = 32
+    f = 40.0                                          # L = 1.3 * 32 / 80 = 0.52
+    cam = synth.Camera(np.eye(3, dtype=np.float32), np.zeros(3, np.float32), f, f, 16.0, 16.0, W, H)
+    L = 1.3 * W / (2 * f)
+    z = np.array([3.0, 3.2, 3.4, 3.6])
+    xz = np.array([0.60, 0.0, -0.62, 0.10])
+    yz = np.array([0.0, 0.61, -0.60, 0.05])
+    means = np.stack([xz * z, yz * z, z], 1)
+    rng = np.random.default_rng(31)
+    ls = np.log(rng.uniform(0.25, 0.4, (4, 3)))
+    q = rng.standard_normal((4, 4))
+    ops = np.log(np.array([0.5, 0.45, 0.55, 0.4]) / (1 - np.array([0.5, 0.45, 0.55, 0.4])))
+    sh = rng.normal(0.0, 0.3, (4, 4, 3))
+    sh[:, 0, :] = (rng.uniform(0.3, 0.7, (4, 3)) - 0.5) / C0
+    sc = _f64_scene(_scene(means, ls, q, ops, sh, 1, [cam]))
+    sc.means, sc.log_scales, sc.quats, sc.opacity_logits, sc.sh = means, ls, q, ops, sh
+    p = oracle.project(sc, 0)
+    assert np.all(p["culled"] == 0)
+    tc = p["tcam"]
+    rx, ry = np.abs(tc[:, 0] / tc[:, 2]), np.abs(tc[:, 1] / tc[:, 2])
+    assert np.all(np.abs(rx - L) >= 0.05) and np.all(np.abs(ry - L) >= 0.05)
+    assert (rx > L).sum() == 2 and (ry > L).sum() == 2      # x clamped twice, y clamped twice
+    act = np.ones(4, bool)
+    w = np.random.default_rng(32).standard_normal((1, 3, H, W))
+    g = oracle.forward_backward(sc, active=act, dL_dC=w)["grad"]
+    eps = 1e-4
+    worst, checked = 0.0, 0
+    for i in range(4):
+        for name, count, col in (("means", 3, 0), ("quats", 4, 3), ("log_scales", 3, 7)):
+            arr = getattr(sc, name)
+            for j in range(count):
+                x0 = arr[i, j]
+                fds = []
+                for h in (eps, eps / 2):
+                    arr[i, j] = x0 + h
+                    lp = _probe(sc, w, act)
+                    arr[i, j] = x0 - h
+                    lm = _probe(sc, w, act)
+                    arr[i, j] = x0
+                    assert _same_decisions(lp, lm)
+                    fds.append((lp[0] - lm[0]) / (2 * h))
+                fd = (4.0 * fds[1] - fds[0]) / 3.0
+                an = g[i, col + j]
+                err = abs(fd - an) / max(abs(fd), abs(an), 1e-8)
+                worst = max(worst, err)
+                checked += 1
+                assert err < 1e-5, (name, i, j, fd, an)
+    assert checked == 40
