@@ -101,6 +101,17 @@ typedef struct {
 #define CLS_FLAG_ALL_TILES 1u   /* every tile active: the full-frame 3DGS step ("w/o Kernel") */
 #define CLS_FLAG_TARGETS_U8 2u  /* targets are 8-bit images: uint8[n_views][3][H][W], value k stands for
                                    the fp32 k / 255 (IEEE division, round to nearest) */
+#define CLS_FLAG_STATIC_CACHE 4u /* static cache: the records
+                                   and binning units of the rows OUTSIDE the regions at the cache's build -- rows
+                                   the local optimisation never changes -- are built once against the active
+                                   mask dilated by 2 tiles and reused; each step projects and bins only the rows
+                                   that were ever active and merges them in (depth, index) order.  Results are
+                                   those of the uncached step.  The build is redone on the device when the
+                                   active mask leaves the dilated mask or a row outside the cached set becomes
+                                   active, and from scratch when the arrays, n, degree, generation, views or
+                                   regions differ from the previous call.  Contract: rows outside the regions
+                                   change only through a new generation.  The first call with this flag must
+                                   not be stream-captured (it allocates).  Ignored with CLS_FLAG_ALL_TILES. */
 
 typedef struct {
     int64_t n_active;          /* A = |O^t| of the last fwd */
@@ -108,7 +119,7 @@ typedef struct {
     int64_t n_pairs;           /* (Gaussian, active tile) pairs sorted */
     int64_t n_items;           /* active (view, tile) work items rendered */
     int64_t n_active_tiles[CLS_MAX_VIEWS];
-    int32_t overflow;          /* bit 0 records, bit 1 pairs, bit 2 active set */
+    int32_t overflow;          /* bit 0 records, bit 1 pairs/units, bit 2 active set, bit 3 static cache build */
     int32_t n_views;
     int64_t max_list;          /* longest per-tile list */
     int64_t n_units;           /* (record, tile row) work units of the binning */
@@ -121,9 +132,18 @@ typedef struct {
     int64_t n_stage1;          /* (Gaussian, view) pairs passing the projection isotropic pre-test */
     int64_t n_tested;          /* (Gaussian, view) pairs the pre-test examined (after the warp-level cull) */
     int64_t n_live_units;      /* binning units (record, tile row) that reach an active tile */
+    /* static cache (CLS_FLAG_STATIC_CACHE), as of the last fwd */
+    int32_t cache_mode;        /* that fwd: 0 reused, 1 rebuilt for a new dilated mask, 2 rebuilt with a new row set */
+    int32_t cache_valid;
+    int64_t cache_builds;      /* builds since the ctx was created (mask-only rebuilds in cache_mask_builds) */
+    int64_t cache_mask_builds;
+    int64_t cache_records;     /* frozen records of the current build */
+    int64_t cache_units;       /* their live (record, tile row) units */
+    int64_t cache_rows;        /* rows projected every step (S0) */
+    int64_t n_tie_runs;        /* runs of > 32 records with equal (view, depth) keys, ordered by index (R13) */
 } cls_stats_t;
 
-#define CLS_PROF_GROUPS 16
+#define CLS_PROF_GROUPS 20
 /* Per-kernel-group device time accumulated while profiling is enabled (CUDA events recorded
  * on the launching stream around each group of launches). */
 typedef struct {
@@ -161,7 +181,7 @@ cls_status cls_destroy(cls_ctx *ctx);
  *   images       (device) float[n_views][3][H][W] out or NULL; pixels of inactive tiles = bg
  *   tile_mask    (device) uint8[n_views][ceil(H/16)][ceil(W/16)] out or NULL
  *   loss         (device) float scalar out or NULL (written only when targets != NULL)
- *   flags        CLS_FLAG_ALL_TILES | CLS_FLAG_TARGETS_U8 or 0
+ *   flags        CLS_FLAG_ALL_TILES | CLS_FLAG_TARGETS_U8 | CLS_FLAG_STATIC_CACHE or 0
  *   stream       cudaStream_t
  */
 cls_status cls_render_fwd(cls_ctx *ctx, const cls_gaussians *g, const cls_camera *cams, int32_t n_views,

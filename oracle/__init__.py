@@ -144,7 +144,7 @@ def render(scene, view: int, active: np.ndarray, proj=None, literal: bool = Fals
     out = dict(image=np.zeros((3, H, W)), T_final=np.zeros((H, W)), n_contrib=np.zeros((H, W), np.int32),
                tile_mask=np.zeros((TY, TX), np.uint8), ambiguous=np.zeros((H, W), np.uint8),
                dL_dC=np.zeros((3, H, W)), grad2d=np.zeros((n, 9)) if with_grad else None,
-               sig=np.zeros((H, W), np.uint64), path=np.zeros((H, W, 2)))
+               sig=np.zeros((H, W), np.uint64), path=np.zeros((H, W, 3)))
     da, dt1, dtk = AMB_WINDOW if window is None else window
     loss_sum = ctypes.c_double(0.0)
     bg = _f64(scene.bg)

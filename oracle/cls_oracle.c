@@ -339,7 +339,9 @@ static inline int in_rect(const int32_t *rc, int tx, int ty)
  * measured, not part of the method): with r_j = alpha_j / (1 - alpha_j), S1 = sum of r_j over the
  * Gaussians composited so far and K their number, a skip is ambiguous if |255 alpha - 1| < da, a
  * termination test if |1e4 T' - 1| < da r + dt1 S1 + dtk (K + 1).
- * path[p] (optional, 2 doubles) = (S1, sqrt(sum r_j^2)) over p's composited Gaussians.
+ * path[p] (optional, 3 doubles) = (S1, sqrt(sum r_j^2)) over p's composited Gaussians and the
+ * pixel's smallest decision margin: min over its skip / termination tests of |255 alpha - 1| / da and
+ * |1e4 T' - 1| / (da r + dt1 S1 + dtk (K + 1)) (ambiguous iff < 1; +inf without tests).
  * sig[p] (optional) = FNV hash of p's composited index sequence (discrete state of the pixel).
  * Returns the number of active tiles.
  */
@@ -435,13 +437,14 @@ int orc_render_view(int64_t n, const int32_t *culled, const double *uv, const do
                         }
                         T_final[pix] = 1.0; n_contrib[pix] = 0; ambiguous[pix] = 0;
                         if (sig) sig[pix] = 0;
-                        if (path) path[2 * pix] = path[2 * pix + 1] = 0.0;
+                        if (path) path[3 * pix] = path[3 * pix + 1] = 0.0, path[3 * pix + 2] = INFINITY;
                         continue;
                     }
                     double T = 1.0, C[3] = {0.0, 0.0, 0.0};
                     int64_t K = 0;
                     int amb = 0;
                     double S1 = 0.0, S2 = 0.0;   /* sums of r_j, r_j^2 (ambiguity window only) */
+                    double margin = INFINITY;
                     int64_t len = literal ? nv : tile_start[tile + 1] - tile_start[tile];
                     for (int64_t s = 0; s < len; s++) {
                         int64_t i = literal ? order[s].idx : tile_list[tile_start[tile] + s];
@@ -454,10 +457,13 @@ int orc_render_view(int64_t n, const int32_t *culled, const double *uv, const do
                         double a = opac[i] * G;
                         if (a > 0.99) a = 0.99;
                         if (fabs(255.0 * a - 1.0) < da) amb = 1;
+                        margin = fmin(margin, fabs(255.0 * a - 1.0) / da);
                         if (a < 1.0 / 255.0) continue;
                         double Tn = T * (1.0 - a);
                         double ra = a / (1.0 - a);
-                        if (fabs(1e4 * Tn - 1.0) < da * ra + dt1 * S1 + dtk * (double)(K + 1)) amb = 1;
+                        const double wt = da * ra + dt1 * S1 + dtk * (double)(K + 1);
+                        if (fabs(1e4 * Tn - 1.0) < wt) amb = 1;
+                        margin = fmin(margin, fabs(1e4 * Tn - 1.0) / wt);
                         if (Tn < 1e-4) break;
                         S1 += ra;
                         S2 += ra * ra;
@@ -481,7 +487,7 @@ int orc_render_view(int64_t n, const int32_t *culled, const double *uv, const do
                         image[ch * HW + pix] = out[ch];
                     }
                     T_final[pix] = T; n_contrib[pix] = (int32_t)K; ambiguous[pix] = (uint8_t)amb;
-                    if (path) { path[2 * pix] = S1; path[2 * pix + 1] = sqrt(S2); }
+                    if (path) { path[3 * pix] = S1; path[3 * pix + 1] = sqrt(S2); path[3 * pix + 2] = margin; }
                     if (sig) {   /* decision signature: the composited index sequence (FD harness) */
                         uint64_t hsh = 1469598103934665603ull;
                         for (int64_t k = 0; k < K; k++) hsh = (hsh ^ (uint64_t)(cidx[k] + 1)) * 1099511628211ull;

@@ -15,6 +15,7 @@ CLS_MAX_VIEWS = 64
 CLS_MAX_REGIONS = 64
 CLS_FLAG_ALL_TILES = 1
 CLS_FLAG_TARGETS_U8 = 2
+CLS_FLAG_STATIC_CACHE = 4
 
 STATUS = {0: "CLS_OK", 1: "CLS_ERR_INVALID_ARGUMENT", 2: "CLS_ERR_DIMENSION_MISMATCH", 3: "CLS_ERR_CAPACITY",
           4: "CLS_ERR_STATE", 5: "CLS_ERR_CUDA", 6: "CLS_ERR_OUT_OF_MEMORY"}
@@ -25,7 +26,7 @@ EXPORTS = ("cls_create", "cls_destroy", "cls_render_fwd", "cls_active", "cls_cop
            "cls_last_error", "cls_launch_count", "cls_partition_static", "cls_prune_outside", "cls_densify_stats",
            "cls_densify", "cls_majority_vote", "cls_fit_spheres", "cls_history_record", "cls_history_recover",
            "cls_merge_updates", "cls_adam_masked_devstep", "cls_spatial_order", "cls_debug_pixels")
-CLS_PROF_GROUPS = 16
+CLS_PROF_GROUPS = 20
 
 
 class ClsError(RuntimeError):
@@ -62,7 +63,10 @@ class cls_stats_t(ctypes.Structure):
                 ("overflow", ctypes.c_int32), ("n_views", ctypes.c_int32), ("max_list", ctypes.c_int64),
                 ("n_units", ctypes.c_int64), ("n_fwd_evals", ctypes.c_int64), ("n_bwd_evals", ctypes.c_int64),
                 ("n_candidates", ctypes.c_int64), ("n_kept_pairs", ctypes.c_int64), ("n_stage1", ctypes.c_int64),
-                ("n_tested", ctypes.c_int64), ("n_live_units", ctypes.c_int64)]
+                ("n_tested", ctypes.c_int64), ("n_live_units", ctypes.c_int64), ("cache_mode", ctypes.c_int32),
+                ("cache_valid", ctypes.c_int32), ("cache_builds", ctypes.c_int64), ("cache_mask_builds", ctypes.c_int64),
+                ("cache_records", ctypes.c_int64), ("cache_units", ctypes.c_int64), ("cache_rows", ctypes.c_int64),
+                ("n_tie_runs", ctypes.c_int64)]
 
     def as_dict(self):
         return dict(n_active=self.n_active, n_records=self.n_records, n_pairs=self.n_pairs, n_items=self.n_items,
@@ -70,12 +74,15 @@ class cls_stats_t(ctypes.Structure):
                     max_list=self.max_list, n_units=self.n_units, n_fwd_evals=self.n_fwd_evals,
                     n_bwd_evals=self.n_bwd_evals, n_candidates=self.n_candidates,
                     n_kept_pairs=self.n_kept_pairs, n_stage1=self.n_stage1, n_tested=self.n_tested,
-                    n_live_units=self.n_live_units)
+                    n_live_units=self.n_live_units, cache_mode=self.cache_mode, cache_valid=self.cache_valid,
+                    cache_builds=self.cache_builds, cache_mask_builds=self.cache_mask_builds,
+                    cache_records=self.cache_records, cache_units=self.cache_units, cache_rows=self.cache_rows,
+                    n_tie_runs=self.n_tie_runs)
 
 
 class cls_profile_t(ctypes.Structure):
-    _fields_ = [("n", ctypes.c_int32), ("name", (ctypes.c_char * 24) * 16), ("ms", ctypes.c_double * 16),
-                ("calls", ctypes.c_int64 * 16)]
+    _fields_ = [("n", ctypes.c_int32), ("name", (ctypes.c_char * 24) * CLS_PROF_GROUPS),
+                ("ms", ctypes.c_double * CLS_PROF_GROUPS), ("calls", ctypes.c_int64 * CLS_PROF_GROUPS)]
 
     def as_dict(self):
         return {self.name[i].value.decode(): dict(ms=self.ms[i], calls=self.calls[i]) for i in range(self.n)}

@@ -79,6 +79,47 @@ struct __align__(16) Rec {
                   //  rect x0 | y0 << 16 bits, rect x1 | y1 << 16 bits)
 };
 
+// static-prefix cache ("reuse the computed projection"):
+// device-side state, decided on the device every step so a captured step replays correctly
+#define CACHE_SKIP (1 << 30)   // Counters.overflow of the cache build on a warm step: every gated kernel returns
+struct CacheState {
+    int valid;          // a build exists for the current scene / views / regions (the host clears it)
+    int mode;           // this step: 0 warm, 1 rebuild for the mask (S0 kept), 2 rebuild with S0 := S0 u O^t
+    int need;           // checks of this step: bit 0 the mask left the dilated mask, bit 1 an active row is not in S0
+    int skip_full;      // 1 unless mode == 2 (scan skip flag of the S0 compaction)
+    int A0;             // |S0|: rows projected every step (the only rows whose parameters can change)
+    int F;              // frozen records of the build
+    int Uf;             // live frozen units of the build
+    int ovf;            // overflow bits of the last build (reported every step while it stands)
+    int builds, mask_builds, full_builds;
+    int skip_build;     // 1 on a warm step (gates the dilated-mask tables)
+    int n;              // rows of this step (the S0 compaction's element count)
+    int scan_ticket;
+    int n_mitems;       // work items of the frozen merge (chunks of one row segment)
+    unsigned long long A0_total;   // scan total of the S0 compaction
+};
+
+struct CacheBufs {      // the cache's device buffers (passed by value)
+    CacheState *st;
+    Counters *ccnt;     // counters of the build (CACHE_SKIP on warm steps)
+    int *dyn_of;        // [maxN] position of row i in S0, or -1
+    int *s0;            // [maxN] S0, ascending
+    unsigned *flag, *excl;            // [maxN] S0 compaction
+    unsigned long long *scan_status;  // its look-back status
+    uint8_t *dmask;     // [V][T] dilated mask (dmask/dsat/dmdiff/drowmask/dbbox: the build's mask tables)
+    int *dmdiff;
+    Rec *urec;          // [Fcap + Dcap] frozen records (id = (view, depth, index) rank), then the step's
+    unsigned long long *cfvd;   // [Fcap] (view, depth) key of each frozen record
+    int *cfgid;         // [Fcap] its Gaussian index
+    int *cseg_lb;       // [V*TY + 1] row-segment lower bounds of the sorted frozen units
+    unsigned *dpos;     // [Dcap] rank position of each dynamic record among the frozen ones
+    int *db;            // [V*TY + 1] row-segment lower bounds of the sorted dynamic units
+    unsigned *dq;       // [Dunits] rank position of each sorted dynamic unit's record
+    int2 *mitems;       // [max_units / MG_CHUNK + V*TY] (segment, first frozen unit) chunks of the merge
+    long long Fcap, Dcap, maxN, Dunits;
+    int dilate;         // tiles added around every active rect
+};
+
 // all scratch of a ctx (device pointers), passed by value to kernels
 struct Scratch {
     // membership

@@ -32,6 +32,18 @@ struct cls_ctx {
     int64_t g_n = 0, g_gen = 0;
     int g_deg = -1;
     bool adam_since_fwd = false;   // a cls_adam_masked updated the fwd's arrays after it
+    Scratch s_fwd{};               // the scratch view the last fwd's raster used (records, sorted units)
+    // static cache (CLS_FLAG_STATIC_CACHE, k_cache.cu), allocated at its first use
+    bool cache_alloc = false;
+    CacheBufs cb{};
+    int *d_dsat = nullptr;
+    unsigned *d_drowmask = nullptr;
+    int4 *d_dbbox = nullptr;
+    unsigned long long *d_cukey = nullptr, *d_cukey_alt = nullptr;
+    long long cache_P = 0;
+    CacheState *h_cst = nullptr;   // pinned copy of the cache state after the last fwd
+    std::vector<unsigned char> cache_sig;   // what the build depends on (host check -> invalidation)
+    int cache_dilate = 2;
     StepDims dims{};
     CamSet cams{};
     float3 bg{};
@@ -64,9 +76,10 @@ struct cls_ctx {
 
 static const char *PROF_NAMES[] = {"member", "active_mask", "project_cand", "project_exact", "rec_sort", "bin_count",
                                    "emit", "pair_sort", "fwd_raster", "fill_bg", "loss", "zero_grad2d", "bwd_raster",
-                                   "bwd_project", "adam", "gather_targets"};
+                                   "bwd_project", "adam", "gather_targets", "cache_check", "cache_build",
+                                   "cache_merge"};
 enum { P_MEMBER, P_MASK, P_PROJECT, P_PROJECT_EXACT, P_RECSORT, P_BINCOUNT, P_EMIT, P_PAIRSORT, P_FWD, P_FILL, P_LOSS,
-       P_ZERO, P_BWD_RASTER, P_BWD_PROJECT, P_ADAM, P_GATHER, P_COUNT };
+       P_ZERO, P_BWD_RASTER, P_BWD_PROJECT, P_ADAM, P_GATHER, P_CACHE_CHECK, P_CACHE_BUILD, P_CACHE_MERGE, P_COUNT };
 static_assert(P_COUNT <= CLS_PROF_GROUPS, "profile groups");
 
 static cudaEvent_t prof_event(cls_ctx *c)
@@ -173,6 +186,12 @@ cls_status cls_destroy(cls_ctx *c)
     for (void *p : dp)
         if (p) cudaFree(p);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
+    void *cp[] = {c->cb.st, c->cb.ccnt, c->cb.dyn_of, c->cb.s0, c->cb.flag, c->cb.excl, c->cb.scan_status, c->cb.dmask,
+                  c->cb.dmdiff, c->cb.urec, c->cb.cfvd, c->cb.cfgid, c->cb.cseg_lb, c->cb.dpos, c->cb.db, c->cb.dq, c->cb.mitems, c->d_dsat,
+                  c->d_drowmask, c->d_dbbox, c->d_cukey, c->d_cukey_alt};
+    for (void *p : cp)
+        if (p) cudaFree(p);
+    if (c->h_cst) cudaFreeHost(c->h_cst);
     delete c;
     return CLS_OK;
 }
@@ -244,6 +263,47 @@ cls_status cls_create(cls_ctx **out, int device, const cls_limits *lim)
     memset(c->h_cnt, 0, sizeof(Counters));
     *out = c;
     return CLS_OK;
+}
+
+// the static cache's buffers, sized from the ctx limits (frozen records: max_records; the step's own
+// records: max_active x max_views, at most max_records; ids of both share the 27 record-id key bits)
+static cls_status cache_allocate(cls_ctx *c)
+{
+    if (c->cache_alloc) return CLS_OK;
+    const size_t N = (size_t)c->lim.max_gaussians, V = (size_t)c->lim.max_views, VT = V * c->maxT;
+    const size_t SAT = V * (c->maxTY + 1) * (c->maxTX + 1), NSEG = V * c->maxTY + 1;
+    const long long R = c->lim.max_records;
+    const long long Dcap = std::max<long long>(std::min<long long>(c->lim.max_active * (long long)V, R), 1024);
+    if (R + Dcap > (1ll << RK_IDX_BITS))
+        return fail(c, CLS_ERR_CAPACITY, "static cache: max_records %lld + %lld step records exceed 2^27", R, Dcap);
+    const size_t P = std::max((size_t)c->lim.max_pairs, (size_t)R);
+    CacheBufs &cb = c->cb;
+    bool ok = dalloc(&cb.st, 1) && dalloc(&cb.ccnt, 1) && dalloc(&cb.dyn_of, N) && dalloc(&cb.s0, N) &&
+              dalloc(&cb.flag, N) && dalloc(&cb.excl, N) && dalloc(&cb.scan_status, N / 8192 + 4) &&
+              dalloc(&cb.dmask, VT) && dalloc(&cb.dmdiff, SAT) && dalloc(&cb.urec, (size_t)(R + Dcap)) &&
+              dalloc(&cb.cfvd, (size_t)R) && dalloc(&cb.cfgid, (size_t)R) && dalloc(&cb.cseg_lb, NSEG) &&
+              dalloc(&cb.dpos, (size_t)Dcap) && dalloc(&cb.db, NSEG) && dalloc(&c->d_dsat, SAT) &&
+              dalloc(&c->d_drowmask, V * c->maxTY * ((c->maxTX + 31) / 32)) && dalloc(&c->d_dbbox, V) &&
+              dalloc(&c->d_cukey, P) && dalloc(&c->d_cukey_alt, P) && dalloc(&cb.dq, P) &&
+              dalloc(&cb.mitems, P / 4096 + NSEG + 1) &&
+              cudaMallocHost((void **)&c->h_cst, sizeof(CacheState)) == cudaSuccess;
+    if (!ok) {
+        cudaGetLastError();
+        return fail(c, CLS_ERR_OUT_OF_MEMORY, "static cache buffers");
+    }
+    cudaMemset(cb.st, 0, sizeof(CacheState));
+    cudaMemset(cb.dmask, 0, VT);
+    cudaMemset(cb.dyn_of, 0xff, sizeof(int) * N);
+    memset(c->h_cst, 0, sizeof(CacheState));
+    cb.Fcap = R;
+    cb.Dcap = Dcap;
+    cb.maxN = (long long)N;
+    cb.Dunits = (long long)P;
+    c->cache_P = (long long)P;
+    if (const char *e = getenv("CLS_CACHE_DILATE")) c->cache_dilate = std::max(0, atoi(e));
+    cb.dilate = c->cache_dilate;
+    c->cache_alloc = true;
+    return check_cuda(c, "static cache allocation");
 }
 
 cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *cams, int32_t n_views,
@@ -348,6 +408,35 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
         cudaStreamIsCapturing(st, &cap);
         c->captured = cap != cudaStreamCaptureStatusNone;
     }
+    const bool cached = (flags & CLS_FLAG_STATIC_CACHE) && !d.all_tiles;
+    if (cached) {
+        if (!c->cache_alloc) {
+            if (c->captured)
+                return fail(c, CLS_ERR_STATE, "the first CLS_FLAG_STATIC_CACHE fwd must not be stream-captured");
+            cls_status e = cache_allocate(c);
+            if (e != CLS_OK) return e;
+        }
+        // what the frozen records depend on: the scene arrays and their generation, n, degree, views and
+        // regions.  A change clears the device-side valid flag; the next check rebuilds from scratch.
+        std::vector<unsigned char> sig;
+        auto put = [&sig](const void *p, size_t nb) {
+            const unsigned char *b = (const unsigned char *)p;
+            sig.insert(sig.end(), b, b + nb);
+        };
+        put(&g->n, sizeof g->n); put(&g->sh_degree, sizeof g->sh_degree); put(&g->generation, sizeof g->generation);
+        put(&g->mean_op, sizeof(void *)); put(&g->quat, sizeof(void *)); put(&g->log_scale, sizeof(void *));
+        put(&g->sh, sizeof(void *));
+        put(&n_views, sizeof n_views); put(&cs.W, sizeof(int)); put(&cs.H, sizeof(int));
+        put(cs.c, sizeof(GCam) * (size_t)n_views);
+        put(&regs.n, sizeof regs.n);
+        for (int j = 0; j < regs.n; j++) {
+            put(&regs.kind[j], sizeof(int)); put(regs.a[j], 12); put(regs.b[j], 12); put(&regs.r[j], 4);
+        }
+        if (sig != c->cache_sig) {
+            cudaMemsetAsync(&c->cb.st->valid, 0, sizeof(int), st);
+            c->cache_sig.swap(sig);
+        }
+    }
     cudaMemsetAsync(s.cnt, 0, sizeof(Counters), st);
     run(c, P_MEMBER, st, [&] { launch_member(p, d, regs, s, st); });
     cudaMemcpyAsync(c->h_A, &s.cnt->A, sizeof(int), cudaMemcpyDeviceToHost, st);
@@ -374,14 +463,51 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
         cudaEventRecord(c->ev_gather, c->side);
         staged = true;
     }
-    run(c, P_PROJECT, st, [&] { launch_project_cand(p, d, cs, s, st); });
-    cudaMemsetAsync(s.vis, 0, (size_t)d.V * (size_t)s.max_active, st);
-    run(c, P_PROJECT_EXACT, st, [&] { launch_project_exact(p, d, cs, s, st); });
-    run(c, P_RECSORT, st, [&] { launch_bin_recsort(d, cs, s, st); });
-    run(c, P_BINCOUNT, st, [&] { launch_bin_count(d, cs, s, st); });
-    run(c, P_EMIT, st, [&] { launch_bin_emit(d, cs, s, st); });
-    run(c, P_PAIRSORT, st, [&] { launch_bin_pairsort(d, cs, s, st); });
-    run(c, P_FWD, st, [&] { launch_fwd(d, cs, s, targets, (flags & CLS_FLAG_TARGETS_U8) != 0, staged, images, loss_scale, bgc, st); });
+    Scratch sr = s;   // what the raster reads (records, sorted units, segment ranges)
+    if (!cached) {
+        run(c, P_PROJECT, st, [&] { launch_project_cand(p, d, cs, s, st); });
+        cudaMemsetAsync(s.vis, 0, (size_t)d.V * (size_t)s.max_active, st);
+        run(c, P_PROJECT_EXACT, st, [&] { launch_project_exact(p, d, cs, s, st); });
+        run(c, P_RECSORT, st, [&] { launch_bin_recsort(d, cs, s, st); });
+        run(c, P_BINCOUNT, st, [&] { launch_bin_count(d, cs, s, st); });
+        run(c, P_EMIT, st, [&] { launch_bin_emit(d, cs, s, st); });
+        run(c, P_PAIRSORT, st, [&] { launch_bin_pairsort(d, cs, s, st); });
+        sr = s;
+    } else {
+        // static cache: the frozen rows' records and units are rebuilt on
+        // the device only when the check asks for it; every step projects and bins S0 alone and
+        // merges its units into the cached ones
+        CacheBufs cb = c->cb;
+        Scratch sb = s;   // the build: its own counters, the dilated mask tables, its own unit buffers
+        sb.cnt = cb.ccnt;
+        sb.mask = cb.dmask; sb.mdiff = cb.dmdiff; sb.sat = c->d_dsat; sb.rowmask = c->d_drowmask;
+        sb.view_bbox = c->d_dbbox;
+        sb.ukey = c->d_cukey; sb.ukey_alt = c->d_cukey_alt;
+        sb.max_records = cb.Fcap;
+        sb.max_units = c->cache_P;
+        unsigned long long *fsorted = nullptr;
+        run(c, P_CACHE_CHECK, st, [&] { launch_cache_check(cb, d, s, st); });
+        run(c, P_CACHE_BUILD, st, [&] { launch_cache_build(p, d, cs, cb, s, sb, &fsorted, st); });
+        Scratch sd = s;   // the step's own records: S0 x views, ids after the frozen ones
+        sd.rec = cb.urec + cb.Fcap;
+        sd.max_records = cb.Dcap;
+        run(c, P_PROJECT, st, [&] { launch_project_cand(p, d, cs, sd, st, cb.s0, &cb.st->A0, nullptr); });
+        cudaMemsetAsync(s.vis, 0, (size_t)d.V * (size_t)s.max_active, st);
+        run(c, P_PROJECT_EXACT, st, [&] { launch_project_exact(p, d, cs, sd, st); });
+        run(c, P_RECSORT, st, [&] { launch_bin_recsort(d, cs, sd, st); });
+        run(c, P_BINCOUNT, st, [&] { launch_bin_count(d, cs, sd, st); });
+        run(c, P_EMIT, st, [&] { launch_bin_emit(d, cs, sd, st); });
+        unsigned long long *dsorted = nullptr;
+        run(c, P_PAIRSORT, st, [&] { dsorted = launch_unit_sort(d, sd, st); });
+        unsigned long long *merged = dsorted == s.ukey ? s.ukey_alt : s.ukey;
+        run(c, P_CACHE_MERGE, st, [&] { launch_cache_merge(d, cb, sd, fsorted, dsorted, merged, st); });
+        sr = s;
+        sr.rec = cb.urec;
+        sr.rskey = sd.rskey;
+        sr.sukey = merged;
+        cudaMemcpyAsync(c->h_cst, cb.st, sizeof(CacheState), cudaMemcpyDeviceToHost, st);
+    }
+    run(c, P_FWD, st, [&] { launch_fwd(d, cs, sr, targets, (flags & CLS_FLAG_TARGETS_U8) != 0, staged, images, loss_scale, bgc, st); });
     if (images) run(c, P_FILL, st, [&] { launch_fill_bg(d, s, images, bgc, st); });
     if (staged) {   // the loss terms need the gathered targets; the compositing above did not
         cudaStreamWaitEvent(st, c->ev_gather, 0);
@@ -393,8 +519,7 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     if (!c->captured) cudaEventRecord(c->ev_fwd, st);
     cls_status e = check_cuda(c, "cls_render_fwd");
     if (e != CLS_OK) return e;
-    c->s.rskey = s.rskey;
-    c->s.sukey = s.sukey;
+    c->s_fwd = sr;
     c->dims = d;
     c->n_views_total = n_views_total;
     c->cams = cs;
@@ -454,7 +579,7 @@ cls_status cls_render_bwd(cls_ctx *c, const cls_gaussians *g, const float *dL_di
     cudaStream_t st = (cudaStream_t)stream;
     Params p{reinterpret_cast<const float4 *>(g->mean_op), reinterpret_cast<const float4 *>(g->quat),
              reinterpret_cast<const float4 *>(g->log_scale), reinterpret_cast<const float4 *>(g->sh)};
-    Scratch s = c->s;
+    Scratch s = c->s_fwd;
     run(c, P_ZERO, st, [&] { launch_zero_grad2d(c->dims, s, (long long)c->lim.max_active, st); });
     run(c, P_BWD_RASTER, st, [&] { launch_bwd_raster(c->dims, s, dL_dimages, c->bg, st); });
     run(c, P_BWD_PROJECT, st, [&] { launch_bwd_project(p, c->dims, c->cams, s, grad_active, st); });
@@ -537,6 +662,17 @@ cls_status cls_stats(cls_ctx *c, cls_stats_t *out)
     unsigned long long bev = 0;
     cudaMemcpy(&bev, &c->s.cnt->bwd_evals, sizeof bev, cudaMemcpyDeviceToHost);
     out->n_bwd_evals = (int64_t)bev;
+    out->n_tie_runs = h.n_long_runs;
+    if (c->cache_alloc) {
+        const CacheState &k = *c->h_cst;
+        out->cache_mode = k.mode;
+        out->cache_valid = k.valid;
+        out->cache_builds = k.builds;
+        out->cache_mask_builds = k.mask_builds;
+        out->cache_records = k.F;
+        out->cache_units = k.Uf;
+        out->cache_rows = k.A0;
+    }
     if (out->overflow)
         return fail(c, CLS_ERR_CAPACITY, "capacity overflow (bits %d): records %d/%lld pairs %llu/%lld A %d/%lld",
                     out->overflow, h.n_records, (long long)c->lim.max_records, h.n_pairs,

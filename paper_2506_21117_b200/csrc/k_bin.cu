@@ -134,7 +134,8 @@ __global__ void __launch_bounds__(256) k_permute(Scratch s)
 __global__ void __launch_bounds__(256) k_long_runs(Scratch s, unsigned long long *bufa, unsigned long long *bufb)
 {
     __shared__ int s_end;
-    const int n = s.cnt->overflow ? 0 : min(s.cnt->n_records, (int)s.max_records);
+    if (s.cnt->overflow) return;   // (also a skipped static-cache build, whose run count is stale)
+    const int n = min(s.cnt->n_records, (int)s.max_records);
     const int n_runs = s.cnt->n_long_runs;
     const unsigned long long *key = s.rskey;
     for (int e = blockIdx.x; e < n_runs; e += gridDim.x) {
@@ -496,6 +497,18 @@ void launch_bin_emit(const StepDims &d, const CamSet &cams, Scratch &s, cudaStre
 {
     k_units<<<148 * 4, KU_THREADS, 0, st>>>(cams, s);   // persistent: 4 CTAs per SM (64 registers)
     g_launches += 1;
+}
+
+// stable sort of the units by row segment only (the static cache merges the ranges itself); returns
+// the buffer holding the sorted units
+unsigned long long *launch_unit_sort(const StepDims &d, Scratch &s, cudaStream_t st)
+{
+    const int n_seg = d.V * d.TY;
+    const int sbits = std::max(bits_for(n_seg), 1);
+    const int w = radix_sort_u64(s.ukey, s.ukey_alt, nullptr, nullptr, &s.cnt->n_units32, (int)s.max_units,
+                                 UK_SEG_SHIFT, UK_SEG_SHIFT + sbits, 8, s.rs_counts, s.rs_totals, &s.cnt->overflow, st);
+    s.sukey = w ? s.ukey_alt : s.ukey;
+    return w ? s.ukey_alt : s.ukey;
 }
 
 // 4. stable sort of the units by row segment (view, tile row); 5. segment ranges

@@ -1,0 +1,404 @@
+// k_cache.cu -- the static cache of the projection and binning.
+//
+// PAPER.md Supp. L509: only the Gaussians of O^t are optimised -- every other row keeps its
+// parameters for the whole local optimisation -- and L539 "we reuse the computed projection to
+// create the per-tile depth ordering".  Rows outside the change regions at the cache's build
+// (the complement of S0) can never change or become active (a row becomes active only by moving
+// into a region, and only active rows move), so their records and (record, tile row) units are
+// built once, against a DILATED active-tile mask, and kept: the frozen part of every tile's
+// depth-ordered list.  Each step projects only S0 (~A rows x V views), sorts those few records
+// and units, and merges them into the frozen units of the segments that hold an active tile.
+//
+// Everything is decided on the device, so a CUDA graph of the step replays correctly:
+//   k_cache_check   the step's active mask inside the dilated mask?  every active row in S0?
+//   k_cache_decide  mode 0 (warm), 1 (rebuild for a new dilated mask), 2 (rebuild, S0 := S0 u O^t);
+//                   on a warm step the build's counters get CACHE_SKIP and every build kernel returns
+//   build           S0 compaction, dilated mask, projection of the rows outside S0, record sort,
+//                   physical reorder (frozen record id = its (view, depth, index) rank), units, unit sort
+//   per step        projection of S0, record sort, units, unit sort, then k_dyn_pos (each dynamic
+//                   record's rank among the frozen ones) and k_merge (both unit lists into one per
+//                   row segment, in (depth, index) order -- the order of R13, so results are unchanged)
+#include "kernels.h"
+
+namespace cls {
+
+// ---- checks and decision ----
+__global__ void __launch_bounds__(256) k_cache_check(CacheBufs cb, Scratch s, int VT)
+{
+    const int A = s.cnt->A;
+    const int valid = cb.st->valid;
+    const int total = max(VT, A);
+    int need = 0;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+        if (e < VT && s.mask[e] && !cb.dmask[e]) need |= 1;
+        if (valid && e < A && cb.dyn_of[s.idx[e]] < 0) need |= 2;
+    }
+    need = __reduce_or_sync(0xffffffffu, need);
+    if ((threadIdx.x & 31) == 0 && need) atomicOr(&cb.st->need, need);
+}
+
+__global__ void k_cache_decide(CacheBufs cb, int n)
+{
+    CacheState &c = *cb.st;
+    const int mode = !c.valid ? 2 : ((c.need & 2) ? 2 : ((c.need & 1) ? 1 : 0));
+    c.mode = mode;
+    c.skip_full = mode != 2;
+    c.skip_build = mode == 0;
+    c.n = n;
+    if (mode) {
+        int *w = reinterpret_cast<int *>(cb.ccnt);
+        for (int k = 0; k < (int)(sizeof(Counters) / sizeof(int)); k++) w[k] = 0;
+        c.builds++;
+        if (mode == 1) c.mask_builds++;
+        else c.full_builds++;
+    } else {
+        cb.ccnt->overflow = CACHE_SKIP;
+    }
+}
+
+// ---- S0 := (S0 if valid) u O^t, stable compaction ----
+__global__ void __launch_bounds__(256) k_s0_flags(CacheBufs cb, Scratch s, int n)
+{
+    if (cb.st->mode != 2) return;
+    const int valid = cb.st->valid;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        cb.flag[i] = ((valid && cb.dyn_of[i] >= 0) || s.ord[i] >= 0) ? 1u : 0u;
+}
+
+__global__ void __launch_bounds__(256) k_s0_scatter(CacheBufs cb, int n)
+{
+    if (cb.st->mode != 2) return;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const bool f = cb.flag[i] != 0u;
+        const int e = (int)cb.excl[i];
+        cb.dyn_of[i] = f ? e : -1;
+        if (f) cb.s0[e] = i;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) cb.st->A0 = (int)cb.st->A0_total;
+}
+
+// ---- dilated mask: the active rects grown by `dilate` tiles, into the dilated corner differences ----
+__global__ void __launch_bounds__(256) k_dzero(CacheBufs cb, int nd)
+{
+    if (cb.st->skip_build) return;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nd; k += gridDim.x * blockDim.x) cb.dmdiff[k] = 0;
+}
+
+__global__ void __launch_bounds__(256) k_dilated_rects(const float4 *__restrict__ mean_op,
+                                                       const float4 *__restrict__ quat,
+                                                       const float4 *__restrict__ log_scale,
+                                                       const __grid_constant__ CamSet cams, CacheBufs cb, Scratch s)
+{
+    if (cb.st->skip_build) return;
+    const int P = cams.TX + 1;
+    const int A = s.cnt->A;
+    const long long total = (long long)A * cams.n;
+    const int k = cb.dilate;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int a = (int)(e / cams.n), v = (int)(e % cams.n);
+        const int i = s.idx[a];
+        Proj p;
+        if (!project_gaussian(__ldg(mean_op + i), __ldg(quat + i), __ldg(log_scale + i), cams.c[v], cams.W, cams.H,
+                              cams.TX, cams.TY, p))
+            continue;
+        const int x0 = max(p.x0 - k, 0), y0 = max(p.y0 - k, 0);
+        const int x1 = min(p.x1 + k, cams.TX), y1 = min(p.y1 + k, cams.TY);
+        int *D = cb.dmdiff + (size_t)v * (cams.TY + 1) * P;
+        atomicAdd(D + y0 * P + x0, 1);
+        atomicAdd(D + y0 * P + x1, -1);
+        atomicAdd(D + y1 * P + x0, -1);
+        atomicAdd(D + y1 * P + x1, 1);
+    }
+}
+
+// ---- frozen records in (view, depth, index) order: record id = rank ----
+__global__ void __launch_bounds__(256) k_cache_reorder(CacheBufs cb, Scratch sb)
+{
+    if (sb.cnt->overflow) return;
+    const int F = min(sb.cnt->n_records, (int)sb.max_records);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < F; i += gridDim.x * blockDim.x) {
+        const unsigned rid = sb.srid[i];
+        cb.urec[i] = sb.rec[rid];
+        cb.cfvd[i] = sb.rskey[i] >> RK_IDX_BITS;
+        cb.cfgid[i] = sb.rec_gid[rid];
+        sb.srid[i] = (unsigned)i;
+    }
+}
+
+__device__ __forceinline__ int seg_lower_bound(const unsigned long long *k, int n, unsigned seg)
+{
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int m = (lo + hi) >> 1;
+        if ((unsigned)(k[m] >> UK_SEG_SHIFT) < seg) lo = m + 1;
+        else hi = m;
+    }
+    return lo;
+}
+
+// lower bound of every row segment in the sorted frozen units (n_seg + 1 entries; the last = live units)
+__global__ void __launch_bounds__(256) k_cache_seglb(CacheBufs cb, const unsigned long long *fsorted, int n_seg)
+{
+    if (cb.ccnt->overflow) return;
+    const int n = cb.ccnt->n_units32;
+    for (int sg = blockIdx.x * blockDim.x + threadIdx.x; sg <= n_seg; sg += gridDim.x * blockDim.x)
+        cb.cseg_lb[sg] = seg_lower_bound(fsorted, n, (unsigned)sg);
+}
+
+__global__ void k_cache_finalize(CacheBufs cb, Scratch s, int n_seg)
+{
+    CacheState &c = *cb.st;
+    if (c.mode) {
+        c.ovf = cb.ccnt->overflow;
+        c.F = min(cb.ccnt->n_records, (int)cb.Fcap);
+        c.Uf = c.ovf ? 0 : cb.cseg_lb[n_seg];
+        c.valid = 1;
+    }
+    c.need = 0;
+    if (c.ovf) atomicOr(&s.cnt->overflow, 8);
+}
+
+// ---- per step: dynamic records' ranks among the frozen ones, and the merge ----
+__global__ void __launch_bounds__(256) k_dyn_pos(CacheBufs cb, Scratch sd)
+{
+    if (sd.cnt->overflow) return;
+    const int D = min(sd.cnt->n_records, (int)sd.max_records);
+    const int F = cb.st->F;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D; i += gridDim.x * blockDim.x) {
+        const unsigned rid = sd.srid[i];
+        const unsigned long long key = sd.rskey[i] >> RK_IDX_BITS;   // (view, depth)
+        const int gid = sd.rec_gid[rid];
+        int lo = 0, hi = F;   // frozen records ordered before (view, depth, gid): (key, gid) strictly less
+        while (lo < hi) {
+            const int m = (lo + hi) >> 1;
+            const unsigned long long fk = cb.cfvd[m];
+            if (fk < key || (fk == key && cb.cfgid[m] < gid)) lo = m + 1;
+            else hi = m;
+        }
+        cb.dpos[rid] = (unsigned)lo;
+    }
+}
+
+// the rank position of each live dynamic unit's record, in unit order (the merge's search keys)
+__global__ void __launch_bounds__(256) k_dyn_q(CacheBufs cb, Scratch s, const unsigned long long *dsorted)
+{
+    if (s.cnt->overflow) return;
+    const int n = min(s.cnt->n_units32, (int)cb.Dunits);
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+        cb.dq[j] = cb.dpos[(unsigned)(dsorted[j] & RK_IDX_MASK)];
+}
+
+// merged row-segment ranges: segment sg holds the frozen units [lb_f(sg), lb_f(sg+1)) and the dynamic
+// units [lb_d(sg), lb_d(sg+1)), i.e. [lb_f(sg) + lb_d(sg), lb_f(sg+1) + lb_d(sg+1)) of the merge
+// lower bound of segment `seg` in k[0, n) by one warp: 32-ary search (each step probes 32 keys at once)
+__device__ __forceinline__ int seg_lower_bound_warp(const unsigned long long *k, int n, unsigned seg)
+{
+    const int lane = threadIdx.x & 31;
+    int lo = 0, hi = n;   // answer in [lo, hi]
+    while (hi - lo > 32) {
+        const long long span = hi - lo;
+        const int p = lo + (int)((span * (lane + 1)) / 33);   // 32 probes strictly inside (lo, hi)
+        const bool less = (unsigned)(k[p] >> UK_SEG_SHIFT) < seg;
+        const unsigned b = __ballot_sync(0xffffffffu, less);
+        const int c = __popc(b);   // probes below seg (a prefix, keys are sorted)
+        const int nlo = c ? __shfl_sync(0xffffffffu, p, c - 1) + 1 : lo;
+        const int nhi = c < 32 ? __shfl_sync(0xffffffffu, p, c) : hi;
+        lo = nlo;
+        hi = nhi;
+    }
+    const int p = lo + lane;
+    const bool less = p < hi && (unsigned)(k[p] >> UK_SEG_SHIFT) < seg;
+    return lo + __popc(__ballot_sync(0xffffffffu, less));
+}
+
+__global__ void __launch_bounds__(256) k_merge_bounds(CacheBufs cb, Scratch s, const unsigned long long *dsorted,
+                                                      int n_seg)
+{
+    if (s.cnt->overflow) return;
+    const int n = s.cnt->n_units32;
+    const int lane = threadIdx.x & 31;
+    for (int sg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; sg <= n_seg; sg += (gridDim.x * blockDim.x) >> 5) {
+        const int b0 = seg_lower_bound_warp(dsorted, n, (unsigned)sg);
+        if (lane == 0) cb.db[sg] = b0;
+        if (sg < n_seg) {
+            const int b1 = seg_lower_bound_warp(dsorted, n, (unsigned)sg + 1u);
+            if (lane == 0) {
+                s.seg_off[sg] = cb.cseg_lb[sg] + b0;
+                s.seg_end[sg] = cb.cseg_lb[sg + 1] + b1;
+            }
+        }
+    }
+}
+
+// Frozen units are merged in fixed chunks of MG_CHUNK consecutive units of one row segment (the work
+// list, built with the cache: segment sizes vary ~100x, so a CTA per segment would be unbalanced).
+#define MG_THREADS 256
+#define MG_SMEM 4096
+#define MG_CHUNK 4096
+__global__ void __launch_bounds__(1024) k_cache_items(CacheBufs cb, int n_seg)
+{
+    if (cb.ccnt->overflow) return;
+    __shared__ int s_carry;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (int b = 0; b < n_seg; b += blockDim.x) {
+        const int sg = b + threadIdx.x;
+        const int n = sg < n_seg ? (cb.cseg_lb[sg + 1] - cb.cseg_lb[sg] + MG_CHUNK - 1) / MG_CHUNK : 0;
+        // block-wide inclusive scan of n (warp scans + a pass over the warp totals)
+        __shared__ int s_w[32];
+        int v = n;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, v, o);
+            if ((threadIdx.x & 31) >= o) v += t;
+        }
+        if ((threadIdx.x & 31) == 31) s_w[threadIdx.x >> 5] = v;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            int w = threadIdx.x < (int)(blockDim.x >> 5) ? s_w[threadIdx.x] : 0;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, w, o);
+                if (threadIdx.x >= o) w += t;
+            }
+            s_w[threadIdx.x] = w;
+        }
+        __syncthreads();
+        const int excl = s_carry + v - n + ((threadIdx.x >> 5) ? s_w[(threadIdx.x >> 5) - 1] : 0);
+        for (int c = 0; c < n; c++) cb.mitems[excl + c] = make_int2(sg, cb.cseg_lb[sg] + c * MG_CHUNK);
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) s_carry = excl + n;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) cb.st->n_mitems = s_carry;
+}
+
+// every live unit of a segment with an active tile goes to its place in the (depth, index) order of
+// the segment: a frozen unit of rank r after the dynamic units whose rank position is <= r, a dynamic
+// unit of position p after the frozen units of rank < p (ranks are distinct, so this is a total order).
+// Frozen: one chunk of MG_CHUNK units per CTA iteration, the segment's dynamic positions staged in
+// shared memory, coalesced loads and stores, a shared-memory binary search per unit.
+__global__ void __launch_bounds__(MG_THREADS) k_merge_frozen(CacheBufs cb, Scratch s, const unsigned long long *fsorted,
+                                                             const unsigned long long *dsorted,
+                                                             unsigned long long *merged, int n_seg, int W32)
+{
+    __shared__ unsigned qd[MG_SMEM];
+    __shared__ int s_act;
+    if (s.cnt->overflow) return;
+    if ((long long)cb.cseg_lb[n_seg] + cb.db[n_seg] > s.max_units) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&s.cnt->overflow, 2);
+        return;
+    }
+    const int n_items = cb.st->n_mitems;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int2 w = cb.mitems[it];
+        const int sg = w.x;
+        if (threadIdx.x == 0) {
+            const unsigned *rm = s.rowmask + (size_t)sg * W32;
+            unsigned a = 0u;
+            for (int q = 0; q < W32; q++) a |= rm[q];
+            s_act = a != 0u;
+        }
+        __syncthreads();
+        if (s_act) {
+            const int f1 = min(w.y + MG_CHUNK, cb.cseg_lb[sg + 1]);
+            const int d0 = cb.db[sg], nd = cb.db[sg + 1] - d0;
+            const bool in_smem = nd <= MG_SMEM;
+            if (in_smem)
+                for (int j = threadIdx.x; j < nd; j += MG_THREADS) qd[j] = cb.dq[d0 + j];
+            __syncthreads();
+            for (int i = w.y + threadIdx.x; i < f1; i += MG_THREADS) {
+                const unsigned long long key = fsorted[i];
+                const unsigned r = (unsigned)(key & RK_IDX_MASK);
+                int lo = 0, hi = nd;   // dynamic units of the segment with position <= r
+                while (lo < hi) {
+                    const int m = (lo + hi) >> 1;
+                    if ((in_smem ? qd[m] : cb.dq[d0 + m]) <= r) lo = m + 1;
+                    else hi = m;
+                }
+                merged[i + d0 + lo] = key;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// dynamic units: their position among the segment's frozen ranks (binary search), then their place
+__global__ void __launch_bounds__(256) k_merge_dyn(CacheBufs cb, Scratch s, const unsigned long long *fsorted,
+                                                   const unsigned long long *dsorted, unsigned long long *merged,
+                                                   int n_seg, int W32)
+{
+    if (s.cnt->overflow) return;
+    if ((long long)cb.cseg_lb[n_seg] + cb.db[n_seg] > s.max_units) return;
+    const int Ud = cb.db[n_seg];
+    const unsigned fbase = (unsigned)cb.Fcap;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < Ud; j += gridDim.x * blockDim.x) {
+        const unsigned long long key = dsorted[j];
+        const int sg = (int)(key >> UK_SEG_SHIFT);
+        const unsigned rid = (unsigned)(key & RK_IDX_MASK);
+        const unsigned p = cb.dq[j];
+        int lo = cb.cseg_lb[sg], hi = cb.cseg_lb[sg + 1];   // frozen units of the segment with rank < p
+        while (lo < hi) {
+            const int m = (lo + hi) >> 1;
+            if ((unsigned)(fsorted[m] & RK_IDX_MASK) < p) lo = m + 1;
+            else hi = m;
+        }
+        merged[j + lo] = (key & ~RK_IDX_MASK) | (unsigned long long)(rid + fbase);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------------------------
+void launch_cache_check(const CacheBufs &cb, const StepDims &d, const Scratch &s, cudaStream_t st)
+{
+    cudaMemsetAsync(&cb.st->need, 0, sizeof(int), st);
+    k_cache_check<<<148 * 2, 256, 0, st>>>(cb, s, d.V * d.T);
+    k_cache_decide<<<1, 1, 0, st>>>(cb, d.n);
+    g_launches += 2;
+}
+
+void launch_cache_build(const Params &g, const StepDims &d, const CamSet &cams, const CacheBufs &cb,
+                        const Scratch &s, Scratch &sb, unsigned long long **fsorted, cudaStream_t st)
+{
+    // S0 := (S0 if valid) u O^t
+    k_s0_flags<<<148 * 4, 256, 0, st>>>(cb, s, d.n);
+    scan_excl_u32(cb.flag, cb.excl, &cb.st->n, (int)cb.maxN, cb.scan_status, &cb.st->scan_ticket, &cb.st->A0_total,
+                  &cb.st->skip_full, st);
+    k_s0_scatter<<<148 * 4, 256, 0, st>>>(cb, d.n);
+    // dilated mask of the current active set and its tables
+    k_dzero<<<148, 256, 0, st>>>(cb, d.V * (d.TY + 1) * (d.TX + 1));
+    k_dilated_rects<<<148 * 3, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, cams, cb, s);
+    g_launches += 4;
+    launch_sat_only(d, cams, sb, &cb.st->skip_build, st);
+    // frozen records: every row outside S0 against the dilated mask
+    launch_project_cand(g, d, cams, sb, st, nullptr, nullptr, cb.dyn_of);
+    launch_project_exact(g, d, cams, sb, st);
+    launch_bin_recsort(d, cams, sb, st);
+    launch_bin_count(d, cams, sb, st);
+    k_cache_reorder<<<148 * 8, 256, 0, st>>>(cb, sb);
+    g_launches++;
+    Scratch su = sb;
+    su.rec = cb.urec;   // units read the reordered records (id = rank)
+    launch_bin_emit(d, cams, su, st);
+    const int n_seg = d.V * d.TY;
+    *fsorted = launch_unit_sort(d, su, st);
+    k_cache_seglb<<<(n_seg + 256) / 256, 256, 0, st>>>(cb, *fsorted, n_seg);
+    k_cache_items<<<1, 1024, 0, st>>>(cb, n_seg);
+    k_cache_finalize<<<1, 1, 0, st>>>(cb, s, n_seg);
+    g_launches += 3;
+}
+
+void launch_cache_merge(const StepDims &d, const CacheBufs &cb, const Scratch &sd, const unsigned long long *fsorted,
+                        const unsigned long long *dsorted, unsigned long long *merged, cudaStream_t st)
+{
+    const int n_seg = d.V * d.TY;
+    const int W32 = (d.TX + 31) / 32;
+    k_dyn_pos<<<148 * 4, 256, 0, st>>>(cb, sd);
+    k_dyn_q<<<148 * 4, 256, 0, st>>>(cb, sd, dsorted);
+    k_merge_bounds<<<(n_seg + 1 + 7) / 8, 256, 0, st>>>(cb, sd, dsorted, n_seg);
+    k_merge_frozen<<<148 * 8, MG_THREADS, 0, st>>>(cb, sd, fsorted, dsorted, merged, n_seg, W32);
+    k_merge_dyn<<<148 * 4, 256, 0, st>>>(cb, sd, fsorted, dsorted, merged, n_seg, W32);
+    g_launches += 5;
+}
+
+}  // namespace cls

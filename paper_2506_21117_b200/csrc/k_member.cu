@@ -137,9 +137,10 @@ __device__ __forceinline__ void warp_prefix(int *a, int n, int st)
 // they fit, else in global memory.
 #define SAT_THREADS 512
 template <bool SMEM>
-__global__ void __launch_bounds__(SAT_THREADS) k_sat(const __grid_constant__ CamSet cams, Scratch s, int all_tiles)
+__global__ void __launch_bounds__(SAT_THREADS) k_sat(const __grid_constant__ CamSet cams, Scratch s, int all_tiles, const int *__restrict__ skip)
 {
     extern __shared__ int sm_sat[];
+    if (skip && *skip) return;   // a gated (skipped) build of the static cache's dilated mask
     const int v = blockIdx.x;
     const int TX = cams.TX, TY = cams.TY, P = TX + 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = SAT_THREADS / 32;
@@ -212,8 +213,20 @@ void launch_active_mask(const Params &g, const StepDims &d, const CamSet &cams, 
     const size_t smem = sizeof(int) * (size_t)(d.TY + 1) * (d.TX + 1) + (size_t)d.TX * d.TY;
     static std::atomic<unsigned long long> attr{0};
     per_device_once(attr, [] { cudaFuncSetAttribute(k_sat<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
-    if (smem <= 200 * 1024) k_sat<true><<<d.V, SAT_THREADS, smem, st>>>(cams, s, d.all_tiles);
-    else k_sat<false><<<d.V, SAT_THREADS, 0, st>>>(cams, s, d.all_tiles);
+    if (smem <= 200 * 1024) k_sat<true><<<d.V, SAT_THREADS, smem, st>>>(cams, s, d.all_tiles, nullptr);
+    else k_sat<false><<<d.V, SAT_THREADS, 0, st>>>(cams, s, d.all_tiles, nullptr);
+    g_launches++;
+}
+
+// mask tables (summed-area table, row bitmasks, bbox) of the rect-corner differences already in s.mdiff;
+// skipped while *skip != 0 (the static cache's dilated mask, rebuilt only when the cache is)
+void launch_sat_only(const StepDims &d, const CamSet &cams, const Scratch &s, const int *skip, cudaStream_t st)
+{
+    const size_t smem = sizeof(int) * (size_t)(d.TY + 1) * (d.TX + 1) + (size_t)d.TX * d.TY;
+    static std::atomic<unsigned long long> attr{0};
+    per_device_once(attr, [] { cudaFuncSetAttribute(k_sat<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
+    if (smem <= 200 * 1024) k_sat<true><<<d.V, SAT_THREADS, smem, st>>>(cams, s, 0, skip);
+    else k_sat<false><<<d.V, SAT_THREADS, 0, st>>>(cams, s, 0, skip);
     g_launches++;
 }
 

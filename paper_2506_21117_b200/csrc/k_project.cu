@@ -164,8 +164,13 @@ __device__ __forceinline__ void push_cand(const Scratch &s, bool keep, int gi, i
 template <bool SMEM_ROWS>
 __global__ void __launch_bounds__(PC_THREADS)
 k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ quat,
-               const float4 *__restrict__ log_scale, int n, const __grid_constant__ CamSet cams, Scratch s)
+               const float4 *__restrict__ log_scale, int n, const __grid_constant__ CamSet cams, Scratch s,
+               const int *__restrict__ glist, const int *__restrict__ n_glist, const int *__restrict__ exclude)
 {
+    // glist (optional): project only the Gaussians glist[0 .. *n_glist) (the static cache's dynamic set);
+    // exclude (optional): skip Gaussian i where exclude[i] >= 0 (the cache's frozen build)
+    if (s.cnt->overflow) return;   // capacity overflow, or a skipped (gated) cache build
+    if (glist) n = *n_glist;
     extern __shared__ unsigned s_rows[];   // [V][TY][W32] active-tile row bitmasks (if they fit)
     __shared__ CamSoA C;
     __shared__ float gM[PC_WARPS][9][32];   // M = R(q^) diag(exp(l)) of the warp's 32 Gaussians
@@ -197,8 +202,8 @@ k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
         float wc[3], wrs, wsm2, wkq;
         bool wb_any;
         {   // per-Gaussian terms, one Gaussian per lane
-            const int i = base + lane;
-            const bool valid = i < n;
+            const int i = base + lane < n ? (glist ? __ldg(glist + base + lane) : base + lane) : 0;
+            const bool valid = base + lane < n && !(exclude && __ldg(exclude + i) >= 0);
             float4 mo = make_float4(0, 0, 0, 0), qq = make_float4(1, 0, 0, 0), ls = make_float4(0, 0, 0, 0);
             if (valid) {
                 mo = __ldg(mean_op + i);
@@ -367,7 +372,7 @@ k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
                     const bool keep = cand_exact32(gM[wid], gP[wid], gl, gv, C, s.sat, TX, TY);
                     head += 32;
                     __syncwarp();
-                    push_cand(s, keep, base + gl, gv, lane, ob, ocnt);
+                    push_cand(s, keep, glist && keep ? __ldg(glist + base + gl) : base + gl, gv, lane, ob, ocnt);
                 }
             }
         }
@@ -384,7 +389,7 @@ k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
             }
             head += cnt;
             __syncwarp();
-            push_cand(s, keep, base + gl, gv, lane, ob, ocnt);
+            push_cand(s, keep, glist && keep ? __ldg(glist + base + gl) : base + gl, gv, lane, ob, ocnt);
         }
         __syncwarp();
     }
@@ -406,6 +411,7 @@ k_project_exact(const float4 *__restrict__ mean_op, const float4 *__restrict__ q
         reinterpret_cast<float *>(s_cams)[k] = reinterpret_cast<const float *>(cams.c)[k];
     for (int k = threadIdx.x; k < cams.n; k += blockDim.x) s_lims[k] = view_lims(cams.c[k], cams.W, cams.H);
     __syncthreads();
+    if (s.cnt->overflow) return;   // capacity overflow, or a skipped (gated) cache build
     const int ncand = min(s.cnt->n_cand, (int)s.max_cand);
     const int lane = threadIdx.x & 31;
     const int TX = cams.TX, TY = cams.TY, P = TX + 1;
@@ -496,7 +502,8 @@ k_project_exact(const float4 *__restrict__ mean_op, const float4 *__restrict__ q
     }
 }
 
-void launch_project_cand(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st)
+void launch_project_cand(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st,
+                         const int *rows, const int *n_rows, const int *exclude)
 {
     size_t smem = sizeof(unsigned) * (size_t)d.V * d.TY * ((d.TX + 31) / 32);
     static std::atomic<unsigned long long> attr{0};
@@ -505,9 +512,11 @@ void launch_project_cand(const Params &g, const StepDims &d, const CamSet &cams,
     });
     const int blocks = std::min((d.n + PC_THREADS - 1) / PC_THREADS, 148 * 3);
     if (smem <= 96 * 1024)
-        k_project_cand<true><<<blocks, PC_THREADS, smem, st>>>(g.mean_op, g.quat, g.log_scale, d.n, cams, s);
+        k_project_cand<true><<<blocks, PC_THREADS, smem, st>>>(g.mean_op, g.quat, g.log_scale, d.n, cams, s, rows,
+                                                               n_rows, exclude);
     else
-        k_project_cand<false><<<blocks, PC_THREADS, 0, st>>>(g.mean_op, g.quat, g.log_scale, d.n, cams, s);
+        k_project_cand<false><<<blocks, PC_THREADS, 0, st>>>(g.mean_op, g.quat, g.log_scale, d.n, cams, s, rows,
+                                                             n_rows, exclude);
     g_launches++;
 }
 

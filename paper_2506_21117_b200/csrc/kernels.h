@@ -24,7 +24,8 @@ void launch_member(const Params &g, const StepDims &d, const RegSet &regs, const
 // (1b) active tile mask per view + summed-area tables       (k_member.cu)
 void launch_active_mask(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st);
 // (2) projection / cull of every Gaussian vs the mask -> records (k_project.cu)
-void launch_project_cand(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st);
+void launch_project_cand(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st,
+                         const int *rows = nullptr, const int *n_rows = nullptr, const int *exclude = nullptr);
 void launch_project_exact(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st);
 // (3) binning: record depth sort, exact pair counts, ordered emission, pair sort by tile (k_bin.cu)
 void launch_bin_items(const StepDims &d, Scratch &s, cudaStream_t st);
@@ -43,6 +44,15 @@ int radix_sort_u64(unsigned long long *keys, unsigned long long *keys_alt, unsig
 void scan_excl_u32(const unsigned *in, unsigned *out, const int *n_ptr, int max_n, unsigned long long *status,
                    int *ticket, unsigned long long *total, const int *skip, cudaStream_t st);
 #define RS_GRID (148 * 4)
+
+unsigned long long *launch_unit_sort(const StepDims &d, Scratch &s, cudaStream_t st);
+void launch_sat_only(const StepDims &d, const CamSet &cams, const Scratch &s, const int *skip, cudaStream_t st);
+// static cache of the frozen rows' records and units (k_cache.cu)
+void launch_cache_check(const CacheBufs &cb, const StepDims &d, const Scratch &s, cudaStream_t st);
+void launch_cache_build(const Params &g, const StepDims &d, const CamSet &cams, const CacheBufs &cb,
+                        const Scratch &s, Scratch &sb, unsigned long long **fsorted, cudaStream_t st);
+void launch_cache_merge(const StepDims &d, const CacheBufs &cb, const Scratch &sd, const unsigned long long *fsorted,
+                        const unsigned long long *dsorted, unsigned long long *merged, cudaStream_t st);
 
 // (4) forward compositing + fused L1                           (k_raster.cu)
 void launch_fwd(const StepDims &d, const CamSet &cams, const Scratch &s, const void *targets, bool targets_u8,

@@ -193,8 +193,10 @@ class LocalOptimizer:
 
     def __init__(self, params: GaussianParams, regions, limits: Optional[N.cls_limits] = None,
                  lr=(1e-3,) * 6, betas=(0.9, 0.999), eps=1e-15, bg=(0.0, 0.0, 0.0), max_views=None,
-                 width=None, height=None):
+                 width=None, height=None, static_cache: bool = False):
         self.params = params
+        # CLS_FLAG_STATIC_CACHE: the frozen rows' records/units are built once and reused (cls.h)
+        self.static_cache = bool(static_cache)
         self.regions = list(regions)
         self.lr = (ctypes.c_float * 6)(*[float(x) for x in lr])
         self.betas = betas
@@ -247,7 +249,8 @@ class LocalOptimizer:
             ctypes.c_void_p(tm.data_ptr() if tm is not None else None),
             ctypes.c_void_p(loss.data_ptr() if loss is not None else None),
             (N.CLS_FLAG_ALL_TILES if all_tiles else 0) |
-            (N.CLS_FLAG_TARGETS_U8 if targets is not None and targets.dtype == torch.uint8 else 0),
+            (N.CLS_FLAG_TARGETS_U8 if targets is not None and targets.dtype == torch.uint8 else 0) |
+            (N.CLS_FLAG_STATIC_CACHE if self.static_cache else 0),
             ctypes.c_void_p(_stream_ptr(stream))), self.ctx)
         self._A = None
         self._fwd_views = V
@@ -497,7 +500,8 @@ class GraphStep:
         check(lib.cls_render_fwd(o.ctx, ctypes.byref(g), self.cams, self.nv, self.nvt, o._reg, len(o.regions), o.bg,
                                  ctypes.c_void_p(self.targets.data_ptr()), None, None,
                                  ctypes.c_void_p(self.loss.data_ptr()),
-                                 N.CLS_FLAG_TARGETS_U8 if self.targets.dtype == torch.uint8 else 0, st), o.ctx)
+                                 (N.CLS_FLAG_TARGETS_U8 if self.targets.dtype == torch.uint8 else 0) |
+                                 (N.CLS_FLAG_STATIC_CACHE if o.static_cache else 0), st), o.ctx)
         check(lib.cls_render_bwd(o.ctx, ctypes.byref(g), None, ctypes.c_void_p(self.grad.data_ptr()), st), o.ctx)
 
     def _adam(self):

@@ -39,8 +39,22 @@ def test_library_exports_every_declared_symbol(native):
 def test_flag_constants_match_header(native):
     src = open(os.path.join(ROOT, "include", "cls.h")).read()
     flags = {k: int(v) for k, v in re.findall(r"#define (CLS_FLAG_\w+) (\d+)u", src)}
-    assert flags == {"CLS_FLAG_ALL_TILES": native.CLS_FLAG_ALL_TILES, "CLS_FLAG_TARGETS_U8": native.CLS_FLAG_TARGETS_U8}
+    assert flags == {"CLS_FLAG_ALL_TILES": native.CLS_FLAG_ALL_TILES, "CLS_FLAG_TARGETS_U8": native.CLS_FLAG_TARGETS_U8,
+                     "CLS_FLAG_STATIC_CACHE": native.CLS_FLAG_STATIC_CACHE}
     assert len(set(flags.values())) == len(flags) and all(v & (v - 1) == 0 for v in flags.values())
+
+
+def test_struct_layouts_match_header(native):
+    """The ctypes mirrors of the ABI structs have the header's sizes (C layout, x86-64)."""
+    import ctypes as C
+    assert C.sizeof(native.cls_gaussians) == 8 + 8 + 4 * 8 + 8          # n, degree (+pad), 4 pointers, generation
+    src = open(os.path.join(ROOT, "include", "cls.h")).read()
+    assert int(re.search(r"#define CLS_PROF_GROUPS (\d+)", src).group(1)) == native.CLS_PROF_GROUPS
+    end = src.index("} cls_stats_t;")
+    block = src[src.rindex("typedef struct {", 0, end):end]
+    block = re.sub(r"/\*.*?\*/", "", block, flags=re.S)
+    names = re.findall(r"\b(\w+)(?:\[\w+\])?;", block)
+    assert names == [f[0] for f in native.cls_stats_t._fields_]
 
 
 def test_status_strings(native):

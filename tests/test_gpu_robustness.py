@@ -33,7 +33,7 @@ def test_depth_ties_long_runs_by_index(torch_cuda):
     g = H.gpu_run(sc, dL=up)
     fb = oracle.forward_backward(sc, dL_dC=up.astype(np.float64))
     assert np.array_equal(g["idx"], fb["idx"])
-    assert g["stats"]["n_records"] > 2000
+    assert g["stats"]["n_tie_runs"] >= 1, g["stats"]   # the long-run path (k_long_runs) was taken
     r = H.assert_images(g["images"][0], fb["renders"][0])
     print("images", r)
     rg = H.compare_grads(g["grad"], H.oracle_rows(fb, sc.sh_degree))

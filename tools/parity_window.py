@@ -57,6 +57,9 @@ def main():
     import torch
     from paper_2506_21117_b200 import GaussianParams, LocalOptimizer, default_limits
     res = {}
+    margins_bad = []
+    # reference window for the margins: the survey's delta = 1e-5 on alpha, the linear T bound
+    W1 = (1e-5, 1e-5, 2.0 ** -24)
     all_rT, all_S1, all_S2, all_K, all_da = [], [], [], [], []
     rows = {}
     for nm, sc in scenes(a.scenes.split(",")).items():
@@ -73,6 +76,7 @@ def main():
             o = oracle.render(sc, v, oracle.membership(sc), with_grad=False, use_target=False, window=(0.0, 0.0, 0.0))
             comp = np.kron(o["tile_mask"], np.ones((16, 16), bool))[: sc.height, : sc.width]
             To, K, S1, S2 = o["T_final"], o["n_contrib"], o["path"][..., 0], o["path"][..., 1]
+            ow = oracle.render(sc, v, oracle.membership(sc), with_grad=False, use_target=False, window=W1)
             rT = np.abs(Tg[v] - To) / np.maximum(To, 1e-30)
             dimg = np.abs(img[v] - o["image"]).max(axis=0)
             same = comp & (rT < 1e-3)
@@ -80,8 +84,12 @@ def main():
             one = same & (K == 1)
             al = 1.0 - To[one]
             all_da.append(rT[one] * To[one] / np.maximum(al, 1e-30))   # |d alpha| / alpha
+            bad = comp & (dimg > 1e-4)
+            mg = ow["path"][..., 2]
+            margins_bad.append(mg[bad])
             per.append(dict(view=v, compared=int(comp.sum()), flipped=int((comp & (rT >= 1e-3)).sum()),
-                            bad_1e4=int((comp & (dimg > 1e-4)).sum()), max_K=int(K.max())))
+                            bad_1e4=int(bad.sum()), max_K=int(K.max()),
+                            max_margin_bad=float(mg[bad].max()) if bad.any() else None))
             rows.setdefault(nm, []).append((sc, v, comp, dimg))
         res[nm] = dict(views=per, seconds=round(time.time() - t0, 1))
         print(nm, per, flush=True)
@@ -98,12 +106,20 @@ def main():
         per_K_max={int(k): float(rT[K == k].max()) for k in (1, 2, 5, 10, 20, 40, 70, 100) if np.any(K == k)},
         rms_ratio_max=float(np.max(rT / np.maximum(S2, 1e-12) * (S2 > 0.05))),
     )
+    mb = np.concatenate(margins_bad) if margins_bad else np.zeros(0)
+    stats["bad_pixels"] = int(mb.size)
+    stats["bad_margin_vs_W1"] = dict(window=W1, max=float(mb.max()) if mb.size else None,
+                                     p99=float(np.percentile(mb, 99)) if mb.size else None,
+                                     p90=float(np.percentile(mb, 90)) if mb.size else None)
     print(json.dumps(stats, indent=1), flush=True)
     # candidate windows: (da, dt1, dtk)
     da_m = stats["dalpha_rel_K1"]["max"] or 1e-6
     cands = {"old_linear": (1e-5, 1e-5, 1.2e-7)}
-    for f in (2, 3, 5):
+    for f in (2, 3):
         cands[f"measured_x{f}"] = (f * da_m, f * max(stats["dt1_needed"], 0.0), f * u)
+    if mb.size:   # the window that flags every bad pixel, scaled from W1, with a factor 2 of headroom
+        f = 2.0 * float(mb.max())
+        cands["bad_margin_x2"] = (f * W1[0], f * W1[1], max(f, 1.0) * W1[2])
     scores = {}
     for cn, w in cands.items():
         tot_c = tot_a = tot_bad = 0
