@@ -554,6 +554,91 @@ int orc_render_view(int64_t n, const int32_t *culled, const double *uv, const do
 /* into grad[i][11 + 3K]:                                                     */
 /*   [0..2] mean, [3..6] quat (w,x,y,z), [7..9] log-scale, [10] opacity logit,*/
 /*   [11 + 3k + ch] SH coefficient k, channel ch.                            */
+/* Decision replay of ONE pixel (test infrastructure).  The pixel's
+ * depth-ordered list (every non-culled Gaussian whose rect holds the pixel's tile, (kappa, index)
+ * order, R8/R13) is composited as in orc_render_view; every skip or termination test of its path that
+ * lies inside the fp32 window (same test as the ambiguity flag) is a decision an fp32 renderer may
+ * take the other way.  The pixel is re-composited with each such decision inverted, and with each
+ * pair of them, up to 8 of them; returns the smallest max-over-channels |C - target| over the
+ * baseline and these alternatives (C includes T bg) and writes the number of window decisions to
+ * *n_window.  A renderer whose pixel is within tol of one of them took admissible decisions. */
+static void replay_one(const int64_t *list, int64_t L, const double *uv, const double *conic,
+                       const double *opac, const double *rgb, int x, int y, const double *bg,
+                       double da, double dt1, double dtk, int f0, int f1, int64_t *dec, int *n_dec,
+                       double out[3])
+{
+    double T = 1.0, C[3] = {0.0, 0.0, 0.0}, S1 = 0.0;
+    int64_t K = 0;
+    int di = 0;   /* index of the next test of the path */
+    for (int64_t s = 0; s < L; s++) {
+        const int64_t i = list[s];
+        double dx = uv[2 * i] - x, dy = uv[2 * i + 1] - y;
+        const double *q = conic + 3 * i;
+        double p = -0.5 * (q[0] * dx * dx + q[2] * dy * dy) - q[1] * dx * dy;
+        if (p > 0.0) continue;
+        double a = opac[i] * exp(p);
+        if (a > 0.99) a = 0.99;
+        int skip = a < 1.0 / 255.0;
+        if (fabs(255.0 * a - 1.0) < da) {
+            if (dec && *n_dec < 8) dec[(*n_dec)++] = di;
+            if (di == f0 || di == f1) skip = !skip;
+        }
+        di++;
+        if (skip) continue;
+        double Tn = T * (1.0 - a);
+        double ra = a / (1.0 - a);
+        int stop = Tn < 1e-4;
+        if (fabs(1e4 * Tn - 1.0) < da * ra + dt1 * S1 + dtk * (double)(K + 1)) {
+            if (dec && *n_dec < 8) dec[(*n_dec)++] = di;
+            if (di == f0 || di == f1) stop = !stop;
+        }
+        di++;
+        if (stop) break;
+        S1 += ra;
+        for (int ch = 0; ch < 3; ch++) C[ch] += a * T * rgb[3 * i + ch];
+        K++;
+        T = Tn;
+    }
+    for (int ch = 0; ch < 3; ch++) out[ch] = C[ch] + T * bg[ch];
+}
+
+static int key_cmp_idx(const void *pa, const void *pb)
+{
+    return ord_cmp(pa, pb);
+}
+
+double orc_pixel_replay(int64_t n, const int32_t *culled, const double *uv, const double *conic, const double *opac,
+                        const int32_t *rect, const float *depth_key, const double *rgb, const double *bg, int x,
+                        int y, double da, double dt1, double dtk, const double *target, int *n_window)
+{
+    const int tx = x / TILE, ty = y / TILE;
+    ord_t *o = malloc(sizeof(ord_t) * (n ? n : 1));
+    int64_t L = 0;
+    for (int64_t i = 0; i < n; i++)
+        if (!culled[i] && in_rect(rect + 4 * i, tx, ty)) { o[L].key = depth_key[i]; o[L].idx = i; L++; }
+    qsort(o, L, sizeof(ord_t), key_cmp_idx);
+    int64_t *list = malloc(sizeof(int64_t) * (L ? L : 1));
+    for (int64_t s = 0; s < L; s++) list[s] = o[s].idx;
+    free(o);
+    int64_t dec[8];
+    int nd = 0;
+    double c[3];
+    replay_one(list, L, uv, conic, opac, rgb, x, y, bg, da, dt1, dtk, -1, -1, dec, &nd, c);
+    double best = 0.0;
+    for (int ch = 0; ch < 3; ch++) best = fmax(best, fabs(c[ch] - target[ch]));
+    for (int a = 0; a < nd; a++)
+        for (int b = a; b < nd; b++) {
+            replay_one(list, L, uv, conic, opac, rgb, x, y, bg, da, dt1, dtk, (int)dec[a], b == a ? -1 : (int)dec[b],
+                       NULL, NULL, c);
+            double e = 0.0;
+            for (int ch = 0; ch < 3; ch++) e = fmax(e, fabs(c[ch] - target[ch]));
+            best = fmin(best, e);
+        }
+    free(list);
+    *n_window = nd;
+    return best;
+}
+
 /* ------------------------------------------------------------------------- */
 void orc_backward_project(int64_t n, int D, const double *mean, const double *log_scale,
                           const double *quat, const double *opacity_logit, const double *sh,

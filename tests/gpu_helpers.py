@@ -69,20 +69,38 @@ def _c_max(orc_render):
 
 
 def compare_images(gpu_img, orc_render, mask_tiles=True):
-    """Image parity: every compared pixel -- every pixel of an active
-    tile; the others are background on both sides and checked too -- within 1e-4 unless the oracle
-    flags it ambiguous; ambiguous pixels within one threshold flip and at most 1e-3 of the compared."""
+    """Image parity.  Every pixel -- the pixels of the active tiles
+    ("compared"), and the background of the others -- must be within 1e-4 of the fp64 oracle, except a
+    pixel whose path holds a decision inside the measured fp32 window (oracle flag "ambiguous"): that one
+    must be within 1e-4 of the oracle's DECISION REPLAY of the pixel (the fp64 composite with one or two
+    window decisions inverted, oracle.pixel_replay).  Such flipped pixels may be at most 1e-3 of the
+    compared ones."""
     o = orc_render["image"]
     amb = orc_render["ambiguous"]
     H, W = amb.shape
     comp = np.kron(orc_render["tile_mask"], np.ones((16, 16), bool))[:H, :W]
-    d = np.abs(gpu_img.astype(np.float64) - o).max(axis=0)
+    gimg = gpu_img.astype(np.float64)
+    d = np.abs(gimg - o).max(axis=0)
     n_amb = int((amb & comp).sum())
     ok = d[~amb]
     worst = float(ok.max()) if ok.size else 0.0
+    flip = amb & (d > IMG_TOL)
+    n_unexplained = 0
+    worst_replay = 0.0
+    can_replay = "scene" in orc_render and "proj" in orc_render
+    for y, x in zip(*np.nonzero(flip)):
+        if not can_replay:
+            n_unexplained += 1
+            continue
+        best, _ = oracle.pixel_replay(orc_render["scene"], orc_render["view"], orc_render["proj"], x, y,
+                                      gimg[:, y, x])
+        worst_replay = max(worst_replay, best)
+        n_unexplained += int(best > IMG_TOL)
     worst_amb = float(d[amb].max()) if n_amb else 0.0
     r = dict(worst=worst, worst_amb=worst_amb, n_amb=n_amb, compared=int(comp.sum()),
              amb_frac=n_amb / max(int(comp.sum()), 1), n_bad=int((ok > IMG_TOL).sum()),
+             n_flipped=int(flip.sum()), flip_frac=int(flip.sum()) / max(int(comp.sum()), 1),
+             n_unexplained=n_unexplained, worst_replay=worst_replay,
              amb_tol=AMB_FLIP * _c_max(orc_render) + IMG_TOL)
     log = os.environ.get("CLS_PARITY_LOG")
     if log:   # evidence for DESIGN.md: n_amb / compared of every image comparison
@@ -93,10 +111,12 @@ def compare_images(gpu_img, orc_render, mask_tiles=True):
 
 def assert_images(gpu_img, orc_render):
     r = compare_images(gpu_img, orc_render)
-    print("image parity:", {k: r[k] for k in ("n_amb", "compared", "amb_frac", "worst", "worst_amb", "n_bad")})
-    assert r["n_bad"] == 0, r
+    print("image parity:", {k: r[k] for k in ("compared", "n_amb", "n_flipped", "n_unexplained", "worst",
+                                              "worst_replay", "n_bad")})
+    assert r["n_bad"] == 0, r                      # unflagged pixels: within 1e-4
+    assert r["n_unexplained"] == 0, r              # flagged pixels off by > 1e-4: an admissible flip
     assert r["worst_amb"] <= r["amb_tol"], r
-    assert r["n_amb"] <= max(AMB_FRAC * r["compared"], 2), r
+    assert r["n_flipped"] <= max(AMB_FRAC * r["compared"], 2), r
     return r
 
 

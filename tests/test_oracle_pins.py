@@ -538,3 +538,56 @@ def test_p7_finite_differences_clamped_jacobian(oracle_lib):
                 checked += 1
                 assert err < 1e-5, (name, i, j, fd, an)
     assert checked == 40
+
+
+# ---------------------------------------------------------------------------
+# decision replay of the parity protocol (test infrastructure)
+# ---------------------------------------------------------------------------
+
+def test_pixel_replay_baseline_equals_render(oracle_lib):
+    """With no flip, the replay's per-pixel list (brute force over rects, (kappa, index) order)
+    composites exactly what orc_render_view does: a 0 distance to the rendered image."""
+    sc = synth.make_scene("c2", n=3000, width=96, height=80, n_views=1)
+    fb = oracle.forward_backward(sc, with_grad=False)
+    r = fb["renders"][0]
+    ys, xs = np.nonzero(np.kron(r["tile_mask"], np.ones((16, 16), bool))[: sc.height, : sc.width])
+    assert ys.size > 100
+    for k in range(0, ys.size, 37):
+        best, _ = oracle.pixel_replay(sc, 0, r["proj"], xs[k], ys[k], r["image"][:, ys[k], xs[k]])
+        assert best == 0.0
+
+
+def test_pixel_replay_skip_flip(oracle_lib):
+    """V1's splat with its opacity tuned so that alpha = (1/255)(1 + 5e-6) at 8 px from the centre:
+    the fp64 oracle composites it (C = c alpha), the pixel is flagged, and the replay explains a
+    renderer that skipped it (C = 0) -- but not an arbitrary value."""
+    cam = _one_cam()
+    sig2 = (100.0 * 0.05 / 2.0) ** 2 + 0.3
+    o = (1.0 / 255.0) * (1.0 + 5e-6) / math.exp(-0.5 * 64.0 / sig2)
+    sc = _scene(np.array([[0.0, 0.0, 2.0]]), np.log([[0.05] * 3]), [[1, 0, 0, 0]], [math.log(o / (1 - o))],
+                np.full((1, 1, 3), _dc(0.6)), 0, [cam])
+    sc.means = np.array([[0.0, 0.0, 2.0]])
+    sc.log_scales = np.log([[0.05] * 3])
+    sc.opacity_logits = np.array([math.log(o / (1 - o))])
+    p = oracle.project(sc, 0)
+    r = oracle.render(sc, 0, np.ones(1, bool), p, use_target=False, with_grad=False)
+    c = float(np.float32(_dc(0.6))) * C0 + 0.5
+    assert r["image"][0, 32, 40] == pytest.approx(c / 255.0, rel=1e-4)
+    assert r["ambiguous"][32, 40]
+    best, nw = oracle.pixel_replay(sc, 0, p, 40, 32, np.zeros(3))
+    assert nw >= 1 and best < 1e-12
+    best, _ = oracle.pixel_replay(sc, 0, p, 40, 32, np.full(3, 0.001))
+    assert best > 1e-4
+
+
+def test_pixel_replay_termination_flip(oracle_lib):
+    """Two coincident splats, alpha 0.99 then 0.989999: T' = 0.01 x 0.010001 = 1.0001e-4 >= 1e-4, so the
+    oracle composites the second (R3); the window flags the test and the replay explains a renderer
+    that terminated before it (C = 0.99 c1)."""
+    sc = _coincident([0.995, 0.989999], [[1, 0, 0], [0, 1, 0]])
+    r = oracle.render(sc, 0, np.ones(2, bool), use_target=False, with_grad=False)
+    assert r["n_contrib"][32, 32] == 2
+    assert r["ambiguous"][32, 32]
+    p = oracle.project(sc, 0)
+    best, nw = oracle.pixel_replay(sc, 0, p, 32, 32, np.array([0.99, 0.0, 0.0]))
+    assert nw >= 1 and best < 1e-12

@@ -93,6 +93,36 @@ def main():
             rows.setdefault(nm, []).append((sc, v, comp, dimg))
         res[nm] = dict(views=per, seconds=round(time.time() - t0, 1))
         print(nm, per, flush=True)
+    # alpha probe: the c4 scene thinned to isolated splats (same size / opacity / camera distributions),
+    # every tile rendered; pixels with ONE composited Gaussian give |d alpha| / alpha = |dT| (1 - alpha)... /
+    # alpha directly, over millions of samples (the tail alpha < 0.05 is where the skip test decides)
+    probe = dict(all=[], tail=[])
+    if "c4" in a.scenes.split(","):
+        sc4 = synth.make_scene("c4")
+        rng = np.random.default_rng(77)
+        keep = np.sort(rng.choice(sc4.n, 30000, replace=False))
+        views = [0, 1, 2, 3]
+        thin = synth.Scene("c4thin", sc4.means[keep], sc4.log_scales[keep], sc4.quats[keep],
+                           sc4.opacity_logits[keep], sc4.sh[keep], sc4.sh_degree, [sc4.cameras[v] for v in views],
+                           sc4.regions, None)
+        p = GaussianParams.from_scene(thin)
+        opt = LocalOptimizer(p, thin.regions, limits=default_limits(thin.n, len(views), thin.width, thin.height))
+        opt.forward(thin.cameras, None, images=False, all_tiles=True)
+        Tg = opt.debug_pixels().cpu().numpy().astype(np.float64)
+        torch.cuda.synchronize()
+        opt.close()
+        for v in range(len(views)):
+            o = oracle.render(thin, v, np.zeros(thin.n, bool), with_grad=False, use_target=False, all_tiles=True,
+                              window=(0.0, 0.0, 0.0))
+            To, K = o["T_final"], o["n_contrib"]
+            one = (K == 1) & np.isfinite(Tg[v])
+            one &= np.abs(Tg[v] - To) < 1e-3 * To          # no flip (a flip moves T by >= 1/255)
+            al = 1.0 - To[one]
+            rel = np.abs(Tg[v][one] - To[one]) / np.maximum(al, 1e-30)   # |d alpha| / alpha (T = 1 - alpha)
+            probe["all"].append(rel)
+            probe["tail"].append(rel[al < 0.05])
+    pa = np.concatenate(probe["all"]) if probe["all"] else np.zeros(0)
+    pt = np.concatenate(probe["tail"]) if probe["tail"] else np.zeros(0)
     rT = np.concatenate(all_rT); S1 = np.concatenate(all_S1); S2 = np.concatenate(all_S2)
     K = np.concatenate(all_K).astype(np.float64); da = np.concatenate(all_da)
     u = 2.0 ** -24
@@ -106,6 +136,12 @@ def main():
         per_K_max={int(k): float(rT[K == k].max()) for k in (1, 2, 5, 10, 20, 40, 70, 100) if np.any(K == k)},
         rms_ratio_max=float(np.max(rT / np.maximum(S2, 1e-12) * (S2 > 0.05))),
     )
+    stats["alpha_probe"] = dict(n=int(pa.size), n_tail=int(pt.size),
+                                p99=float(np.percentile(pa, 99)) if pa.size else None,
+                                p9999=float(np.percentile(pa, 99.99)) if pa.size else None,
+                                max=float(pa.max()) if pa.size else None,
+                                tail_p9999=float(np.percentile(pt, 99.99)) if pt.size else None,
+                                tail_max=float(pt.max()) if pt.size else None)
     mb = np.concatenate(margins_bad) if margins_bad else np.zeros(0)
     stats["bad_pixels"] = int(mb.size)
     stats["bad_margin_vs_W1"] = dict(window=W1, max=float(mb.max()) if mb.size else None,
@@ -115,8 +151,10 @@ def main():
     # candidate windows: (da, dt1, dtk)
     da_m = stats["dalpha_rel_K1"]["max"] or 1e-6
     cands = {"old_linear": (1e-5, 1e-5, 1.2e-7)}
-    for f in (2, 3):
-        cands[f"measured_x{f}"] = (f * da_m, f * max(stats["dt1_needed"], 0.0), f * u)
+    if pa.size:
+        da_m = max(float(pa.max()), da_m)
+    for f in (1, 2):
+        cands[f"measured_x{f}"] = (f * da_m, f * max(stats["dt1_needed"], 0.0), f * 2 * u)
     if mb.size:   # the window that flags every bad pixel, scaled from W1, with a factor 2 of headroom
         f = 2.0 * float(mb.max())
         cands["bad_margin_x2"] = (f * W1[0], f * W1[1], max(f, 1.0) * W1[2])
