@@ -254,6 +254,20 @@ cls_status cls_debug_grad2d(cls_ctx *ctx, float *out, void *stream);
  * measured error window. */
 cls_status cls_debug_pixels(cls_ctx *ctx, float *T_out, void *stream);
 
+/* Optional, synchronous (stage parity tests): the records of the last fwd
+ * -- with CLS_FLAG_STATIC_CACHE the cached frozen ones then the step's own -- as float[count][16]
+ * (u_hi, u_lo, v_hi, v_lo, a1, a2, b1, b2, r, g, b, opacity, qcut', ordinal bits, rect x0|y0<<16,
+ * rect x1|y1<<16; the exponent is 2^-(s'^2 + t'^2), s' = a1 dx + a2 dy, t' = b1 dx + b2 dy, i.e. the
+ * conic times log2(e)/2), their Gaussian index and view (device arrays of >= max entries);
+ * *count (host) = number of records (only min(count, max) are written). */
+cls_status cls_debug_records(cls_ctx *ctx, float *rec_out, int32_t *gid_out, int32_t *view_out, int64_t max,
+                             int64_t *count);
+
+/* Optional, synchronous: the depth-ordered list of tile `tile` (ty * TX + tx) of view `view` of the
+ * last fwd as Gaussian indices (device int32[>= max]); *count (host) = list length. */
+cls_status cls_debug_tile_list(cls_ctx *ctx, int32_t view, int32_t tile, int32_t *gid_out, int32_t max,
+                               int64_t *count);
+
 /* ---------------------------------------------------------------------------------------
  * NEXT-1: static-prefix partition, sphere pruning, densification on O^t.
  * These run between optimisation steps (not inside one); each synchronises `stream` once to

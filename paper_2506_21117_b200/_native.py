@@ -25,7 +25,7 @@ EXPORTS = ("cls_create", "cls_destroy", "cls_render_fwd", "cls_active", "cls_cop
            "cls_stats", "cls_profile_enable", "cls_profile_read", "cls_debug_grad2d", "cls_status_string",
            "cls_last_error", "cls_launch_count", "cls_partition_static", "cls_prune_outside", "cls_densify_stats",
            "cls_densify", "cls_majority_vote", "cls_fit_spheres", "cls_history_record", "cls_history_recover",
-           "cls_merge_updates", "cls_adam_masked_devstep", "cls_spatial_order", "cls_debug_pixels")
+           "cls_merge_updates", "cls_adam_masked_devstep", "cls_spatial_order", "cls_debug_pixels", "cls_debug_records", "cls_debug_tile_list")
 CLS_PROF_GROUPS = 20
 
 
@@ -106,6 +106,8 @@ def _load():
     L.cls_stats.argtypes = [V, P(cls_stats_t)]
     L.cls_debug_grad2d.argtypes = [V, V, V]
     L.cls_debug_pixels.argtypes = [V, V, V]
+    L.cls_debug_records.argtypes = [V, V, V, V, ctypes.c_int64, P(ctypes.c_int64)]
+    L.cls_debug_tile_list.argtypes = [V, ctypes.c_int32, ctypes.c_int32, V, ctypes.c_int32, P(ctypes.c_int64)]
     L.cls_profile_enable.argtypes = [V, ctypes.c_int32]
     L.cls_profile_read.argtypes = [V, P(cls_profile_t)]
     L.cls_status_string.argtypes = [ctypes.c_int]
@@ -134,7 +136,7 @@ def _load():
                  "cls_stats", "cls_debug_grad2d", "cls_profile_enable", "cls_profile_read", "cls_partition_static",
                  "cls_prune_outside", "cls_densify_stats", "cls_densify", "cls_majority_vote", "cls_fit_spheres",
                  "cls_history_record", "cls_history_recover", "cls_merge_updates", "cls_adam_masked_devstep",
-                 "cls_spatial_order", "cls_debug_pixels"):
+                 "cls_spatial_order", "cls_debug_pixels", "cls_debug_records", "cls_debug_tile_list"):
         getattr(L, name).restype = ctypes.c_int
     return L
 

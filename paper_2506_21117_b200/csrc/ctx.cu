@@ -33,6 +33,8 @@ struct cls_ctx {
     int g_deg = -1;
     bool adam_since_fwd = false;   // a cls_adam_masked updated the fwd's arrays after it
     Scratch s_fwd{};               // the scratch view the last fwd's raster used (records, sorted units)
+    Scratch s_rec{};               // ... and its record view (the step's own records when cached)
+    bool fwd_cached = false;
     // static cache (CLS_FLAG_STATIC_CACHE, k_cache.cu), allocated at its first use
     bool cache_alloc = false;
     CacheBufs cb{};
@@ -505,6 +507,7 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
         sr.rec = cb.urec;
         sr.rskey = sd.rskey;
         sr.sukey = merged;
+        c->s_rec = sd;
         cudaMemcpyAsync(c->h_cst, cb.st, sizeof(CacheState), cudaMemcpyDeviceToHost, st);
     }
     run(c, P_FWD, st, [&] { launch_fwd(d, cs, sr, targets, (flags & CLS_FLAG_TARGETS_U8) != 0, staged, images, loss_scale, bgc, st); });
@@ -520,6 +523,8 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     cls_status e = check_cuda(c, "cls_render_fwd");
     if (e != CLS_OK) return e;
     c->s_fwd = sr;
+    if (!cached) c->s_rec = sr;
+    c->fwd_cached = cached;
     c->dims = d;
     c->n_views_total = n_views_total;
     c->cams = cs;
@@ -732,6 +737,40 @@ cls_status cls_debug_pixels(cls_ctx *c, float *T_out, void *stream)
     cudaMemsetAsync(T_out, 0xff, sizeof(float) * (size_t)c->dims.V * c->dims.H * c->dims.W, st);   // NaN: not rendered
     launch_debug_pixels(c->dims, c->cams, c->s, T_out, st);
     return check_cuda(c, "cls_debug_pixels");
+}
+
+cls_status cls_debug_records(cls_ctx *c, float *rec_out, int32_t *gid_out, int32_t *view_out, int64_t max,
+                             int64_t *count)
+{
+    if (!c || !rec_out || !gid_out || !view_out || !count) return CLS_ERR_INVALID_ARGUMENT;
+    if (!c->fwd_valid) return fail(c, CLS_ERR_STATE, "cls_debug_records before cls_render_fwd");
+    cudaSetDevice(c->device);
+    int *d_n = nullptr;
+    if (cudaMalloc(&d_n, sizeof(int)) != cudaSuccess) return fail(c, CLS_ERR_OUT_OF_MEMORY, "debug count");
+    launch_debug_records(c->s_rec, c->cb, c->fwd_cached ? 1 : 0, rec_out, gid_out, view_out, max, d_n, 0);
+    int n = 0;
+    cudaMemcpy(&n, d_n, sizeof n, cudaMemcpyDeviceToHost);
+    cudaFree(d_n);
+    *count = n;
+    return check_cuda(c, "cls_debug_records");
+}
+
+cls_status cls_debug_tile_list(cls_ctx *c, int32_t view, int32_t tile, int32_t *gid_out, int32_t max, int64_t *count)
+{
+    if (!c || !gid_out || !count) return CLS_ERR_INVALID_ARGUMENT;
+    if (!c->fwd_valid) return fail(c, CLS_ERR_STATE, "cls_debug_tile_list before cls_render_fwd");
+    if (view < 0 || view >= c->dims.V || tile < 0 || tile >= c->dims.T)
+        return fail(c, CLS_ERR_INVALID_ARGUMENT, "view %d / tile %d out of range", view, tile);
+    cudaSetDevice(c->device);
+    int *d_n = nullptr;
+    if (cudaMalloc(&d_n, sizeof(int)) != cudaSuccess) return fail(c, CLS_ERR_OUT_OF_MEMORY, "debug count");
+    launch_debug_tile_list(c->s_fwd, c->cb, c->fwd_cached ? 1 : 0, c->dims.TY, c->dims.TX, view, tile, gid_out, max,
+                           d_n, 0);
+    int n = 0;
+    cudaMemcpy(&n, d_n, sizeof n, cudaMemcpyDeviceToHost);
+    cudaFree(d_n);
+    *count = n;
+    return check_cuda(c, "cls_debug_tile_list");
 }
 
 // ---------------------------------------------------------------------------

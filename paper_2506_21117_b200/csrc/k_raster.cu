@@ -847,6 +847,72 @@ void launch_debug_pixels(const StepDims &d, const CamSet &cams, const Scratch &s
     g_launches++;
 }
 
+// debug exports for the stage parity tests (cls_debug_records / cls_debug_tile_list): the records of
+// the last fwd with their Gaussian index and view, and one tile's depth-ordered list as Gaussian indices
+__device__ __forceinline__ int debug_gid(const Scratch &s, const CacheBufs &cb, bool cached, unsigned rid)
+{
+    if (!cached) return s.rec_gid[rid];
+    return rid < (unsigned)cb.Fcap ? cb.cfgid[rid] : s.rec_gid[rid - (unsigned)cb.Fcap];
+}
+
+__global__ void k_debug_records(Scratch s, CacheBufs cb, int cached, float4 *out, int *gid, int *view, long long max,
+                                int *count)
+{
+    const int F = cached ? cb.st->F : 0;
+    const int D = s.cnt->overflow ? 0 : min(s.cnt->n_records, (int)s.max_records);
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)F + D && e < max;
+         e += (long long)gridDim.x * blockDim.x) {
+        Rec r;
+        int g, v;
+        if (e < F) {
+            r = cb.urec[e];
+            g = cb.cfgid[e];
+            v = (int)(cb.cfvd[e] >> RK_DEPTH_BITS);
+        } else {
+            const unsigned long long key = s.rskey[e - F];
+            const unsigned rid = (unsigned)(key & RK_IDX_MASK);
+            r = s.rec[rid];   // (cached: s.rec already points at the step's own records)
+            g = s.rec_gid[rid];
+            v = (int)(key >> RK_VIEW_SHIFT);
+        }
+        out[4 * e] = r.xy; out[4 * e + 1] = r.co; out[4 * e + 2] = r.rgb; out[4 * e + 3] = r.aux;
+        gid[e] = g;
+        view[e] = v;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *count = F + D;
+}
+
+__global__ void k_debug_tile_list(Scratch s, CacheBufs cb, int cached, int TY, int TX, int view, int tile, int *out,
+                                  int max, int *count)
+{
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    const int tx = tile % TX, ty = tile / TX, seg = view * TY + ty;
+    int k = 0;
+    for (int u = s.seg_off[seg]; u < s.seg_end[seg]; u++) {
+        const unsigned long long key = s.sukey[u];
+        const int lo = (int)((key >> UK_LO_SHIFT) & 0x3ffu), hi = (int)((key >> UK_HI_SHIFT) & 0x3ffu);
+        if (lo <= tx && tx <= hi) {
+            if (k < max) out[k] = debug_gid(s, cb, cached != 0, (unsigned)(key & RK_IDX_MASK));
+            k++;
+        }
+    }
+    *count = k;
+}
+
+void launch_debug_records(const Scratch &s, const CacheBufs &cb, int cached, float *out, int *gid, int *view,
+                          long long max, int *count, cudaStream_t st)
+{
+    k_debug_records<<<148 * 4, 256, 0, st>>>(s, cb, cached, reinterpret_cast<float4 *>(out), gid, view, max, count);
+    g_launches++;
+}
+
+void launch_debug_tile_list(const Scratch &s, const CacheBufs &cb, int cached, int TY, int TX, int view, int tile,
+                            int *out, int max, int *count, cudaStream_t st)
+{
+    k_debug_tile_list<<<1, 32, 0, st>>>(s, cb, cached, TY, TX, view, tile, out, max, count);
+    g_launches++;
+}
+
 __global__ void k_zero_grad2d(Scratch s, int V, long long cap)
 {
     const long long A = s.cnt->A;

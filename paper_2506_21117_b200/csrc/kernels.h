@@ -62,6 +62,10 @@ void launch_loss(const Scratch &s, float loss_scale, float *loss, cudaStream_t s
 void launch_loss_staged(const StepDims &d, const CamSet &cams, const Scratch &s, float loss_scale, cudaStream_t st);
 // (5) backward raster + backward projection                    (k_raster.cu, k_bwd_project.cu)
 void launch_debug_pixels(const StepDims &d, const CamSet &cams, const Scratch &s, float *out, cudaStream_t st);
+void launch_debug_records(const Scratch &s, const CacheBufs &cb, int cached, float *out, int *gid, int *view,
+                          long long max, int *count, cudaStream_t st);
+void launch_debug_tile_list(const Scratch &s, const CacheBufs &cb, int cached, int TY, int TX, int view, int tile,
+                            int *out, int max, int *count, cudaStream_t st);
 void launch_zero_grad2d(const StepDims &d, const Scratch &s, long long cap, cudaStream_t st);
 void launch_bwd_raster(const StepDims &d, const Scratch &s, const float *dL_dimages, float3 bg, cudaStream_t st);
 void launch_bwd_project(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s,

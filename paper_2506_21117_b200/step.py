@@ -307,6 +307,28 @@ class LocalOptimizer:
               self.ctx)
         return out
 
+    def debug_records(self, max_records: int):
+        """Records of the last fwd: (rec float [k, 16], gid int32 [k], view int32 [k]) as numpy."""
+        dev = self.params.device
+        rec = torch.empty((max_records, 16), dtype=torch.float32, device=dev)
+        gid = torch.empty(max_records, dtype=torch.int32, device=dev)
+        view = torch.empty(max_records, dtype=torch.int32, device=dev)
+        cnt = ctypes.c_int64()
+        torch.cuda.synchronize()
+        check(lib.cls_debug_records(self.ctx, ctypes.c_void_p(rec.data_ptr()), ctypes.c_void_p(gid.data_ptr()),
+                                    ctypes.c_void_p(view.data_ptr()), int(max_records), ctypes.byref(cnt)), self.ctx)
+        k = min(int(cnt.value), max_records)
+        return rec[:k].cpu().numpy(), gid[:k].cpu().numpy(), view[:k].cpu().numpy(), int(cnt.value)
+
+    def debug_tile_list(self, view: int, tile: int, max_len: int = 1 << 16):
+        """The depth-ordered list of one tile of the last fwd, as Gaussian indices (numpy int32)."""
+        out = torch.empty(max_len, dtype=torch.int32, device=self.params.device)
+        cnt = ctypes.c_int64()
+        torch.cuda.synchronize()
+        check(lib.cls_debug_tile_list(self.ctx, int(view), int(tile), ctypes.c_void_p(out.data_ptr()), int(max_len),
+                                      ctypes.byref(cnt)), self.ctx)
+        return out[: min(int(cnt.value), max_len)].cpu().numpy()
+
     def stats(self) -> dict:
         st = N.cls_stats_t()
         check(lib.cls_stats(self.ctx, ctypes.byref(st)), self.ctx)
