@@ -96,6 +96,8 @@ struct CacheState {
     int n;              // rows of this step (the S0 compaction's element count)
     int scan_ticket;
     int n_mitems;       // work items of the frozen merge (chunks of one row segment)
+    int n_dyn_extra;    // rows of S0 that are not active this step (appended to the step's row list)
+    int n_dcand;        // the step's staged (row, view) record candidates
     unsigned long long A0_total;   // scan total of the S0 compaction
 };
 
@@ -116,6 +118,10 @@ struct CacheBufs {      // the cache's device buffers (passed by value)
     int *db;            // [V*TY + 1] row-segment lower bounds of the sorted dynamic units
     unsigned *dq;       // [Dunits] rank position of each sorted dynamic unit's record
     int2 *mitems;       // [max_units / MG_CHUNK + V*TY] (segment, first frozen unit) chunks of the merge
+    int *dlist;         // [maxN] the step's rows: O^t (idx order), then S0 \ O^t
+    double *dM;         // [maxN][12] per listed row: M = R(q^) diag(exp(l)) (9), opacity, qcut, pad
+    Rec *dcand;         // [Dcap] staged record candidates of the step (before the mask test)
+    int4 *dcinfo;       // [Dcap] (Gaussian index, view, depth key, tile rows)
     long long Fcap, Dcap, maxN, Dunits;
     int dilate;         // tiles added around every active rect
 };

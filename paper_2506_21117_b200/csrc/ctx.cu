@@ -46,6 +46,7 @@ struct cls_ctx {
     CacheState *h_cst = nullptr;   // pinned copy of the cache state after the last fwd
     std::vector<unsigned char> cache_sig;   // what the build depends on (host check -> invalidation)
     int cache_dilate = 2;
+    cudaStream_t body_stream = nullptr;   // captures the cache build into a conditional graph node
     StepDims dims{};
     CamSet cams{};
     float3 bg{};
@@ -189,11 +190,12 @@ cls_status cls_destroy(cls_ctx *c)
         if (p) cudaFree(p);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     void *cp[] = {c->cb.st, c->cb.ccnt, c->cb.dyn_of, c->cb.s0, c->cb.flag, c->cb.excl, c->cb.scan_status, c->cb.dmask,
-                  c->cb.dmdiff, c->cb.urec, c->cb.cfvd, c->cb.cfgid, c->cb.cseg_lb, c->cb.dpos, c->cb.db, c->cb.dq, c->cb.mitems, c->d_dsat,
+                  c->cb.dmdiff, c->cb.urec, c->cb.cfvd, c->cb.cfgid, c->cb.cseg_lb, c->cb.dpos, c->cb.db, c->cb.dq, c->cb.mitems, c->cb.dlist, c->cb.dM, c->cb.dcand, c->cb.dcinfo, c->d_dsat,
                   c->d_drowmask, c->d_dbbox, c->d_cukey, c->d_cukey_alt};
     for (void *p : cp)
         if (p) cudaFree(p);
     if (c->h_cst) cudaFreeHost(c->h_cst);
+    if (c->body_stream) cudaStreamDestroy(c->body_stream);
     delete c;
     return CLS_OK;
 }
@@ -286,7 +288,8 @@ static cls_status cache_allocate(cls_ctx *c)
               dalloc(&cb.cfvd, (size_t)R) && dalloc(&cb.cfgid, (size_t)R) && dalloc(&cb.cseg_lb, NSEG) &&
               dalloc(&cb.dpos, (size_t)Dcap) && dalloc(&cb.db, NSEG) && dalloc(&c->d_dsat, SAT) &&
               dalloc(&c->d_drowmask, V * c->maxTY * ((c->maxTX + 31) / 32)) && dalloc(&c->d_dbbox, V) &&
-              dalloc(&c->d_cukey, P) && dalloc(&c->d_cukey_alt, P) && dalloc(&cb.dq, P) &&
+              dalloc(&c->d_cukey, P) && dalloc(&c->d_cukey_alt, P) && dalloc(&cb.dq, P) && dalloc(&cb.dlist, N) &&
+              dalloc(&cb.dM, N * 12) && dalloc(&cb.dcand, (size_t)Dcap) && dalloc(&cb.dcinfo, (size_t)Dcap) &&
               dalloc(&cb.mitems, P / 4096 + NSEG + 1) &&
               cudaMallocHost((void **)&c->h_cst, sizeof(CacheState)) == cudaSuccess;
     if (!ok) {
@@ -304,6 +307,8 @@ static cls_status cache_allocate(cls_ctx *c)
     c->cache_P = (long long)P;
     if (const char *e = getenv("CLS_CACHE_DILATE")) c->cache_dilate = std::max(0, atoi(e));
     cb.dilate = c->cache_dilate;
+    if (cudaStreamCreateWithFlags(&c->body_stream, cudaStreamNonBlocking) != cudaSuccess)
+        return fail(c, CLS_ERR_CUDA, "static cache: body stream");
     c->cache_alloc = true;
     return check_cuda(c, "static cache allocation");
 }
@@ -444,7 +449,8 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     cudaMemcpyAsync(c->h_A, &s.cnt->A, sizeof(int), cudaMemcpyDeviceToHost, st);
     if (!c->captured) cudaEventRecord(c->ev_member, st);
     run(c, P_MASK, st, [&] {
-        launch_active_mask(p, d, cs, s, st);
+        if (cached) launch_dyn_mask(p, d, cs, c->cb, s, st);   // one projection of the step's rows (k_cache.cu)
+        else launch_active_mask(p, d, cs, s, st);
         launch_bin_items(d, s, st);
     });
     // host-resident (pinned, mapped) targets: gather only the active tiles' pixels on the side
@@ -488,14 +494,52 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
         sb.max_records = cb.Fcap;
         sb.max_units = c->cache_P;
         unsigned long long *fsorted = nullptr;
-        run(c, P_CACHE_CHECK, st, [&] { launch_cache_check(cb, d, s, st); });
-        run(c, P_CACHE_BUILD, st, [&] { launch_cache_build(p, d, cs, cb, s, sb, &fsorted, st); });
+        // captured into a CUDA graph: the build becomes the body of a conditional node set by
+        // k_cache_decide (warm replays skip it whole); eager: every build kernel returns at once
+        cudaGraph_t cap_graph = nullptr;
+        cudaGraphConditionalHandle cond = 0;
+        bool use_cond = false;
+        if (c->captured && !getenv("CLS_NO_COND_GRAPH")) {
+            cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+            if (cudaStreamGetCaptureInfo(st, &cst, nullptr, &cap_graph, nullptr, nullptr) == cudaSuccess &&
+                cst == cudaStreamCaptureStatusActive &&
+                cudaGraphConditionalHandleCreate(&cond, cap_graph, 0, cudaGraphCondAssignDefault) == cudaSuccess)
+                use_cond = true;
+            else
+                cudaGetLastError();
+        }
+        run(c, P_CACHE_CHECK, st, [&] { launch_cache_check(cb, d, s, st, cond, use_cond ? 1 : 0); });
+        if (use_cond) {
+            cudaStreamCaptureStatus cst;
+            const cudaGraphNode_t *deps = nullptr;
+            size_t nd = 0;
+            cudaStreamGetCaptureInfo(st, &cst, nullptr, nullptr, &deps, &nd);
+            cudaGraphNodeParams np = {};
+            np.type = cudaGraphNodeTypeConditional;
+            np.conditional.handle = cond;
+            np.conditional.type = cudaGraphCondTypeIf;
+            np.conditional.size = 1;
+            cudaGraphNode_t node;
+            if (cudaGraphAddNode(&node, cap_graph, deps, nd, &np) != cudaSuccess)
+                return fail(c, CLS_ERR_CUDA, "conditional node: %s", cudaGetErrorString(cudaGetLastError()));
+            cudaGraph_t body = np.conditional.phGraph_out[0];
+            if (cudaStreamBeginCaptureToGraph(c->body_stream, body, nullptr, nullptr, 0,
+                                              cudaStreamCaptureModeRelaxed) != cudaSuccess)
+                return fail(c, CLS_ERR_CUDA, "body capture: %s", cudaGetErrorString(cudaGetLastError()));
+            launch_cache_build(p, d, cs, cb, s, sb, &fsorted, c->body_stream);
+            cudaGraph_t out_body = nullptr;
+            if (cudaStreamEndCapture(c->body_stream, &out_body) != cudaSuccess)
+                return fail(c, CLS_ERR_CUDA, "body capture end: %s", cudaGetErrorString(cudaGetLastError()));
+            cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies);
+        } else {
+            run(c, P_CACHE_BUILD, st, [&] { launch_cache_build(p, d, cs, cb, s, sb, &fsorted, st); });
+        }
+        launch_cache_finalize(d, cb, s, st);
         Scratch sd = s;   // the step's own records: S0 x views, ids after the frozen ones
         sd.rec = cb.urec + cb.Fcap;
         sd.max_records = cb.Dcap;
-        run(c, P_PROJECT, st, [&] { launch_project_cand(p, d, cs, sd, st, cb.s0, &cb.st->A0, nullptr); });
         cudaMemsetAsync(s.vis, 0, (size_t)d.V * (size_t)s.max_active, st);
-        run(c, P_PROJECT_EXACT, st, [&] { launch_project_exact(p, d, cs, sd, st); });
+        run(c, P_PROJECT_EXACT, st, [&] { launch_dyn_emit(d, cb, sd, st); });   // the staged candidates vs the mask
         run(c, P_RECSORT, st, [&] { launch_bin_recsort(d, cs, sd, st); });
         run(c, P_BINCOUNT, st, [&] { launch_bin_count(d, cs, sd, st); });
         run(c, P_EMIT, st, [&] { launch_bin_emit(d, cs, sd, st); });

@@ -37,10 +37,12 @@ __global__ void __launch_bounds__(256) k_cache_check(CacheBufs cb, Scratch s, in
     if ((threadIdx.x & 31) == 0 && need) atomicOr(&cb.st->need, need);
 }
 
-__global__ void k_cache_decide(CacheBufs cb, int n)
+__global__ void k_cache_decide(CacheBufs cb, int n, cudaGraphConditionalHandle cond, int use_cond)
 {
     CacheState &c = *cb.st;
     const int mode = !c.valid ? 2 : ((c.need & 2) ? 2 : ((c.need & 1) ? 1 : 0));
+    // in a CUDA graph the build is the body of a conditional node: skipped whole on warm steps
+    if (use_cond) cudaGraphSetConditional(cond, mode != 0 ? 1u : 0u);
     c.mode = mode;
     c.skip_full = mode != 2;
     c.skip_build = mode == 0;
@@ -347,13 +349,220 @@ __global__ void __launch_bounds__(256) k_merge_dyn(CacheBufs cb, Scratch s, cons
 }
 
 // ---------------------------------------------------------------------------------------------
+// The step's own rows with the cache: ONE fp64 projection per (row, view), shared by the active mask
+// (rect corners of the active rows, modification 1) and the records ("reuse the computed
+// projection"), instead of one in k_active_rects and another in k_project_exact.
+//   k_dyn_list     rows: O^t (idx order), then the rows of the valid S0 that are not active this step
+//   k_dyn_rows     per row: M = R(q^) diag(exp l), opacity, the alpha >= 1/255 cut (fp64, once per row)
+//   k_dyn_project  per (row, view): the projection (same fp64 definitions as k_project_exact); active
+//                  rows add their rect to the mask's corner differences; every (row, view) with a
+//                  non-empty alpha-footprint rect is staged as a finished record candidate
+//   k_dyn_emit     after the mask tables: candidates whose rect holds an active tile become records
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_dyn_list(CacheBufs cb, Scratch s)
+{
+    const int A = s.cnt->A;
+    const int A0 = cb.st->valid ? cb.st->A0 : 0;
+    const int total = max(A, A0);
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+        if (e < A) cb.dlist[e] = s.idx[e];
+        bool extra = false;
+        int r = 0;
+        if (e < A0) {
+            r = cb.s0[e];
+            extra = s.ord[r] < 0;
+        }
+        const unsigned b = __ballot_sync(__activemask(), extra);
+        if (extra) {
+            const int lane = threadIdx.x & 31, leader = __ffs(b) - 1;
+            int base = 0;
+            if (lane == leader) base = atomicAdd(&cb.st->n_dyn_extra, __popc(b));
+            base = __shfl_sync(b, base, leader);
+            cb.dlist[A + base + __popc(b & ((1u << lane) - 1u))] = r;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_dyn_rows(CacheBufs cb, Scratch s, const float4 *__restrict__ mean_op,
+                                                  const float4 *__restrict__ quat, const float4 *__restrict__ log_scale)
+{
+    const int n = s.cnt->A + cb.st->n_dyn_extra;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const int i = cb.dlist[k];
+        double M[9];
+        gauss_m64(__ldg(quat + i), __ldg(log_scale + i), M);
+        double *o = cb.dM + (size_t)k * 12;
+        for (int q = 0; q < 9; q++) o[q] = M[q];
+        const double o64 = 1.0 / (1.0 + exp(-(double)__ldg(mean_op + i).w));
+        o[9] = o64;
+        o[10] = 2.0 * log(255.0 * o64) * (1.0 + 1e-6) + 2e-3;
+        o[11] = 0.0;
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256, 3) k_dyn_project(CacheBufs cb, Scratch s, const float4 *__restrict__ mean_op,
+                                                        const float4 *__restrict__ sh, int n,
+                                                        const __grid_constant__ CamSet cams)
+{
+    __shared__ GCam s_cams[CLS_MAX_VIEWS];
+    __shared__ double2 s_lims[CLS_MAX_VIEWS];
+    for (int k = threadIdx.x; k < cams.n * (int)(sizeof(GCam) / 4); k += blockDim.x)
+        reinterpret_cast<float *>(s_cams)[k] = reinterpret_cast<const float *>(cams.c)[k];
+    for (int k = threadIdx.x; k < cams.n; k += blockDim.x) s_lims[k] = view_lims(cams.c[k], cams.W, cams.H);
+    __syncthreads();
+    const int rows = s.cnt->A + cb.st->n_dyn_extra;
+    const int V = cams.n, TX = cams.TX, TY = cams.TY, P = TX + 1;
+    const int lane = threadIdx.x & 31;
+    const long long total = (long long)rows * V;
+    for (long long b0 = blockIdx.x * (long long)blockDim.x; b0 < total; b0 += (long long)gridDim.x * blockDim.x) {
+        const long long e = b0 + threadIdx.x;
+        bool keep = false;
+        Proj p;
+        int i = 0, v = 0, k = 0;
+        float4 mo = make_float4(0, 0, 0, 0);
+        double o64 = 0.0, qcut = -1.0;
+        if (e < total) {
+            k = (int)(e / V);
+            v = (int)(e - (long long)k * V);
+            i = cb.dlist[k];
+            const double *Mr = cb.dM + (size_t)k * 12;
+            double M[9];
+            for (int q = 0; q < 9; q++) M[q] = Mr[q];
+            o64 = Mr[9];
+            qcut = Mr[10];
+            mo = __ldg(mean_op + i);
+            if (project_view(mo, M, s_cams[v], s_lims[v], TX, TY, p)) {
+                if (s.ord[i] >= 0) {   // active: its rect joins the view's active tile mask (R9)
+                    int *Dd = s.mdiff + (size_t)v * (TY + 1) * P;
+                    atomicAdd(Dd + p.y0 * P + p.x0, 1);
+                    atomicAdd(Dd + p.y0 * P + p.x1, -1);
+                    atomicAdd(Dd + p.y1 * P + p.x0, -1);
+                    atomicAdd(Dd + p.y1 * P + p.x1, 1);
+                }
+                if (qcut >= 0.0) {   // the alpha-footprint rect, as in k_project_exact
+                    const double hx = sqrt(qcut * p.A) + 1e-3, hy = sqrt(qcut * p.C) + 1e-3;
+                    const int fx0 = (int)fmin(fmax(floor((p.u - hx - (CLS_TILE - 1)) / CLS_TILE) + 1.0, -1.0), TX + 1.0);
+                    const int fx1 = (int)fmin(fmax(floor((p.u + hx) / CLS_TILE) + 1.0, -1.0), TX + 1.0);
+                    const int fy0 = (int)fmin(fmax(floor((p.v - hy - (CLS_TILE - 1)) / CLS_TILE) + 1.0, -1.0), TY + 1.0);
+                    const int fy1 = (int)fmin(fmax(floor((p.v + hy) / CLS_TILE) + 1.0, -1.0), TY + 1.0);
+                    p.x0 = max(p.x0, fx0); p.x1 = min(p.x1, fx1);
+                    p.y0 = max(p.y0, fy0); p.y1 = min(p.y1, fy1);
+                    keep = p.x1 > p.x0 && p.y1 > p.y0;
+                }
+            }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (bal == 0u) continue;
+        int base = 0;
+        const int leader = __ffs(bal) - 1;
+        if (lane == leader) base = atomicAdd(&cb.st->n_dcand, __popc(bal));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (!keep) continue;
+        const long long slot = (long long)base + __popc(bal & ((1u << lane) - 1u));
+        if (slot >= cb.Dcap) {
+            atomicOr(&s.cnt->overflow, 1);
+            continue;
+        }
+        const GCam &c = s_cams[v];
+        float dir[3], Y[16], col[3];
+        view_dir(mo, c, dir);
+        sh_color_raw<D>(sh, n, i, dir, Y, col);
+        const float uh = __double2float_rn(p.u), vh = __double2float_rn(p.v);
+        double a1, a2, b1, b2;   // scaled LDL^T coefficients (raster_q, reading R29), as k_project_exact
+        if (p.C >= p.A) {
+            const double kk = sqrt(CLS_KAPPA * p.ca), iC = 1.0 / p.C;
+            a1 = kk; a2 = kk * (-p.B * iC); b1 = 0.0; b2 = sqrt(CLS_KAPPA * iC);
+        } else {
+            const double kk = sqrt(CLS_KAPPA * p.cc), iA = 1.0 / p.A;
+            a1 = kk * (-p.B * iA); a2 = kk; b1 = sqrt(CLS_KAPPA * iA); b2 = 0.0;
+        }
+        const double qc = CLS_KAPPA * qcut;
+        Rec R;
+        R.xy = make_float4(uh, __double2float_rn(p.u - (double)uh), vh, __double2float_rn(p.v - (double)vh));
+        R.co = make_float4(__double2float_rn(a1), __double2float_rn(a2), __double2float_rn(b1), __double2float_rn(b2));
+        R.rgb = make_float4(fmaxf(col[0], 0.0f), fmaxf(col[1], 0.0f), fmaxf(col[2], 0.0f), (float)o64);
+        R.aux = make_float4(__double2float_ru(qc), __int_as_float(s.ord[i]), __int_as_float(p.x0 | (p.y0 << 16)),
+                            __int_as_float(p.x1 | (p.y1 << 16)));
+        cb.dcand[slot] = R;
+        const unsigned dk = min(__float_as_uint(__double2float_rn(p.tz)) - 0x3E4CCCCDu, (1u << RK_DEPTH_BITS) - 1u);
+        cb.dcinfo[slot] = make_int4(i, v, (int)dk, p.y1 - p.y0);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_dyn_emit(CacheBufs cb, Scratch s, int TX, int TY)
+{
+    if (s.cnt->overflow) return;
+    const int nc = min(cb.st->n_dcand, (int)cb.Dcap);
+    const int lane = threadIdx.x & 31, P = TX + 1;
+    for (int b0 = blockIdx.x * blockDim.x; b0 < nc; b0 += gridDim.x * blockDim.x) {
+        const int e = b0 + threadIdx.x;
+        bool keep = false;
+        Rec R;
+        int4 inf = make_int4(0, 0, 0, 0);
+        if (e < nc) {
+            R = cb.dcand[e];
+            inf = cb.dcinfo[e];
+            const int ra = __float_as_int(R.aux.z), rb = __float_as_int(R.aux.w);
+            const int *S = s.sat + (size_t)inf.y * (TY + 1) * P;
+            keep = sat_count(S, P, ra & 0xffff, ra >> 16, rb & 0xffff, rb >> 16) > 0;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (bal == 0u) continue;
+        int base = 0;
+        const int leader = __ffs(bal) - 1;
+        if (lane == leader) base = atomicAdd(&s.cnt->n_records, __popc(bal));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (!keep) continue;
+        const long long slot = (long long)base + __popc(bal & ((1u << lane) - 1u));
+        if (slot >= s.max_records) {
+            atomicOr(&s.cnt->overflow, 1);
+            continue;
+        }
+        s.rec[slot] = R;
+        s.rec_gid[slot] = inf.x;
+        s.rrows[slot] = (unsigned)inf.w;
+        const int ordi = __float_as_int(R.aux.y);
+        if (ordi >= 0 && ordi < s.max_active) s.vis[(size_t)inf.y * s.max_active + ordi] = 1;
+        s.rkey[slot] = ((unsigned long long)inf.y << RK_VIEW_SHIFT) | ((unsigned long long)(unsigned)inf.z << RK_IDX_BITS) |
+                       (unsigned long long)slot;
+    }
+}
+
+void launch_dyn_mask(const Params &g, const StepDims &d, const CamSet &cams, const CacheBufs &cb, const Scratch &s,
+                     cudaStream_t st)
+{
+    cudaMemsetAsync(&cb.st->n_dyn_extra, 0, sizeof(int), st);
+    cudaMemsetAsync(&cb.st->n_dcand, 0, sizeof(int), st);
+    cudaMemsetAsync(s.mdiff, 0, sizeof(int) * (size_t)d.V * (d.TY + 1) * (d.TX + 1), st);
+    k_dyn_list<<<148 * 2, 256, 0, st>>>(cb, s);
+    k_dyn_rows<<<148 * 2, 256, 0, st>>>(cb, s, g.mean_op, g.quat, g.log_scale);
+    const int grid = 148 * 3;
+    switch (d.D) {
+    case 0: k_dyn_project<0><<<grid, 256, 0, st>>>(cb, s, g.mean_op, g.sh, d.n, cams); break;
+    case 1: k_dyn_project<1><<<grid, 256, 0, st>>>(cb, s, g.mean_op, g.sh, d.n, cams); break;
+    case 2: k_dyn_project<2><<<grid, 256, 0, st>>>(cb, s, g.mean_op, g.sh, d.n, cams); break;
+    default: k_dyn_project<3><<<grid, 256, 0, st>>>(cb, s, g.mean_op, g.sh, d.n, cams); break;
+    }
+    g_launches += 3;
+    launch_sat_only(d, cams, s, nullptr, st);
+}
+
+void launch_dyn_emit(const StepDims &d, const CacheBufs &cb, const Scratch &sd, cudaStream_t st)
+{
+    k_dyn_emit<<<148 * 4, 256, 0, st>>>(cb, sd, d.TX, d.TY);
+    g_launches++;
+}
+
+// ---------------------------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------------------------
-void launch_cache_check(const CacheBufs &cb, const StepDims &d, const Scratch &s, cudaStream_t st)
+void launch_cache_check(const CacheBufs &cb, const StepDims &d, const Scratch &s, cudaStream_t st,
+                        cudaGraphConditionalHandle cond, int use_cond)
 {
     cudaMemsetAsync(&cb.st->need, 0, sizeof(int), st);
     k_cache_check<<<148 * 2, 256, 0, st>>>(cb, s, d.V * d.T);
-    k_cache_decide<<<1, 1, 0, st>>>(cb, d.n);
+    k_cache_decide<<<1, 1, 0, st>>>(cb, d.n, cond, use_cond);
     g_launches += 2;
 }
 
@@ -384,8 +593,15 @@ void launch_cache_build(const Params &g, const StepDims &d, const CamSet &cams, 
     *fsorted = launch_unit_sort(d, su, st);
     k_cache_seglb<<<(n_seg + 256) / 256, 256, 0, st>>>(cb, *fsorted, n_seg);
     k_cache_items<<<1, 1024, 0, st>>>(cb, n_seg);
-    k_cache_finalize<<<1, 1, 0, st>>>(cb, s, n_seg);
-    g_launches += 3;
+    g_launches += 2;
+}
+
+// every step, after the (possibly skipped) build: the build's outcome into the cache state, and a
+// standing build overflow into the step's counters
+void launch_cache_finalize(const StepDims &d, const CacheBufs &cb, const Scratch &s, cudaStream_t st)
+{
+    k_cache_finalize<<<1, 1, 0, st>>>(cb, s, d.V * d.TY);
+    g_launches++;
 }
 
 void launch_cache_merge(const StepDims &d, const CacheBufs &cb, const Scratch &sd, const unsigned long long *fsorted,

@@ -48,9 +48,14 @@ void scan_excl_u32(const unsigned *in, unsigned *out, const int *n_ptr, int max_
 unsigned long long *launch_unit_sort(const StepDims &d, Scratch &s, cudaStream_t st);
 void launch_sat_only(const StepDims &d, const CamSet &cams, const Scratch &s, const int *skip, cudaStream_t st);
 // static cache of the frozen rows' records and units (k_cache.cu)
-void launch_cache_check(const CacheBufs &cb, const StepDims &d, const Scratch &s, cudaStream_t st);
+void launch_dyn_mask(const Params &g, const StepDims &d, const CamSet &cams, const CacheBufs &cb, const Scratch &s,
+                     cudaStream_t st);
+void launch_dyn_emit(const StepDims &d, const CacheBufs &cb, const Scratch &sd, cudaStream_t st);
+void launch_cache_check(const CacheBufs &cb, const StepDims &d, const Scratch &s, cudaStream_t st,
+                        cudaGraphConditionalHandle cond = 0, int use_cond = 0);
 void launch_cache_build(const Params &g, const StepDims &d, const CamSet &cams, const CacheBufs &cb,
                         const Scratch &s, Scratch &sb, unsigned long long **fsorted, cudaStream_t st);
+void launch_cache_finalize(const StepDims &d, const CacheBufs &cb, const Scratch &s, cudaStream_t st);
 void launch_cache_merge(const StepDims &d, const CacheBufs &cb, const Scratch &sd, const unsigned long long *fsorted,
                         const unsigned long long *dsorted, unsigned long long *merged, cudaStream_t st);
 

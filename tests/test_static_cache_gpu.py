@@ -136,3 +136,15 @@ def test_cached_graph_step_matches_uncached(torch_cuda):
     for k, x in enumerate(b):
         assert x["loss"] == x["ref_loss"], (k, x["loss"], x["ref_loss"])
     assert b[-1]["stats"]["cache_builds"] == 1
+
+
+def test_cached_graph_rebuild_inside_replay(torch_cuda, monkeypatch):
+    """A rebuild INSIDE a CUDA-graph replay: no dilation and a large learning rate, so the mask leaves
+    the cached one during the replays; the build runs as the body of the graph's conditional node and
+    every replay's loss still equals the uncached loss of the same parameters."""
+    monkeypatch.setenv("CLS_CACHE_DILATE", "0")
+    sc = SCENES["c2r"]()
+    b = _run_steps(sc, 8, lr=0.05, graph=True)
+    for k, x in enumerate(b):
+        assert x["loss"] == x["ref_loss"], (k, x["loss"], x["ref_loss"])
+    assert b[-1]["stats"]["cache_builds"] >= 2, b[-1]["stats"]   # the warm-up build + >= 1 inside a replay
