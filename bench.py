@@ -126,7 +126,7 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2506_21117_b200.dist import allreduce_rows, shard_views
+    from paper_2506_21117_b200.dist import allreduce_packed, shard_views
     sc, u8 = bench_scene(args)
     V = len(sc.cameras)
     my_views = shard_views(V, world, rank)
@@ -134,7 +134,17 @@ def run_ours(args):
     W, H = sc.width, sc.height
     params = GaussianParams.from_scene(sc, device=f"cuda:{local}")
     lim = limits_for(args.config, sc.n, len(cams), W, H, args.all_tiles)
-    opt = LocalOptimizer(params, sc.regions, limits=lim, static_cache=args.static_cache and not args.all_tiles)
+    cached = args.static_cache and not args.all_tiles
+    if world > 1:
+        # the all-reduce of a CUDA-graph step covers the gradient-row CAPACITY (max_active): size it from
+        # |O^t| of the scene (one membership pass through the library) with headroom; a larger active set
+        # is a reported overflow, never a silent truncation
+        probe = LocalOptimizer(params, sc.regions, limits=lim)
+        probe.forward(cams[:1], None)
+        A = probe.active_count()
+        probe.close()
+        lim.max_active = max(1024, int(A * 1.25) + 256)
+    opt = LocalOptimizer(params, sc.regions, limits=lim, static_cache=cached)
     if not args.no_spatial_order:
         opt.spatial_order()   # scene layout, once at load (not part of a step): Morton-ordered rows
     tg_np = u8[my_views] if u8 is not None else sc.targets[my_views]
@@ -144,9 +154,11 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
 
     def step(targets=None):
-        res = opt.forward(cams, tg if targets is None else targets, n_views_total=V, all_tiles=args.all_tiles)
+        t = tg if targets is None else targets
+        if world > 1:   # the step's only exchange: one NCCL all-reduce of the packed loss + active rows
+            return opt.step(cams, t, n_views_total=V, allreduce=allreduce_packed)
+        res = opt.forward(cams, t, n_views_total=V, all_tiles=args.all_tiles)
         grad = opt.backward()
-        allreduce_rows(grad, res.loss)          # the step's only exchange (N > 1): one NCCL all-reduce
         opt.adam(grad)
         return res.loss
 
@@ -159,11 +171,17 @@ def run_ours(args):
     torch.cuda.synchronize()
     cold_ms = c0.elapsed_time(c1)
     gstep = None
-    if not args.eager and world == 1 and not args.all_tiles:
+    graph_note = None
+    if not args.eager and not args.all_tiles:
         from paper_2506_21117_b200 import GraphStep
-        gstep = GraphStep(opt, cams, tg, n_views_total=V)   # fwd + bwd + masked Adam captured once
-        step_eager = step
-        step = lambda targets=None: gstep.replay()
+        try:   # fwd + bwd (+ NCCL all-reduce at N > 1) + masked Adam captured once
+            gstep = GraphStep(opt, cams, tg, n_views_total=V, allreduce=allreduce_packed if world > 1 else None)
+            step_eager = step
+            step = lambda targets=None: gstep.replay()
+        except Exception as e:   # e.g. a NCCL build that cannot be captured: eager steps, said in step_mode
+            torch.cuda.synchronize()
+            gstep = None
+            graph_note = f"graph capture failed ({type(e).__name__}: {str(e)[:120]}); eager steps"
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -217,7 +235,8 @@ def run_ours(args):
         # graph of the step over the pinned host targets (--e2e-mode graph) or launched eagerly
         if gstep is not None and args.e2e_mode == "graph":
             from paper_2506_21117_b200 import GraphStep
-            gstep_host = GraphStep(opt, cams, tg_host, n_views_total=V)
+            gstep_host = GraphStep(opt, cams, tg_host, n_views_total=V,
+                                   allreduce=allreduce_packed if world > 1 else None)
             step_host = gstep_host.replay
         else:
             step_host = (lambda: step_eager(tg_host)) if gstep is not None else (lambda: step(tg_host))
@@ -311,7 +330,7 @@ def run_ours(args):
                            "frame_equivalent": round(V * W * H * value / 1e6, 2)},
             "e2e": e2e, "gpu_launches": int(launches), "roofline": roof, "clocks": clocks,
             "step_mode": (f"CUDA graph replay (kernel breakdown from K eager steps; e2e {args.e2e_mode})" if gstep is not None
-                          else "eager"),
+                          else (graph_note or "eager")),
             "cold_step_ms": round(cold_ms, 4),
             "static_cache": ({"records": int(stats["cache_records"]), "units": int(stats["cache_units"]),
                               "rows_per_step": int(stats["cache_rows"]), "builds": int(stats["cache_builds"]),

@@ -55,6 +55,30 @@ def allreduce_rows(grad: torch.Tensor, loss: Optional[torch.Tensor], group=None)
         loss.copy_(flat[n:].view_as(loss))
 
 
+class PackedRows:
+    """One flat fp32 buffer holding the step's loss and its active-gradient rows, laid out so that the
+    loss and the first A rows are ONE contiguous prefix: [loss, 0, 0, 0][row 0][row 1]...  The C ABI
+    writes the loss and the rows straight into it (no torch.cat / copy_ around the collective), and the
+    all-reduce covers exactly the prefix of the live rows (eager) or of the row capacity (CUDA graph)."""
+
+    def __init__(self, capacity_rows: int, row_floats: int, device):
+        self.capacity = max(int(capacity_rows), 1)
+        self.row_floats = int(row_floats)
+        self.flat = torch.zeros(4 + self.capacity * self.row_floats, dtype=torch.float32, device=device)
+        self.loss = self.flat[:1]
+        self.rows = self.flat[4:].view(self.capacity, self.row_floats // 4, 4)
+
+    def prefix(self, n_rows: int) -> torch.Tensor:
+        return self.flat[: 4 + min(int(n_rows), self.capacity) * self.row_floats]
+
+
+def allreduce_packed(buf: torch.Tensor, group=None) -> None:
+    """The step's only exchange: one in-place sum over ranks of a PackedRows prefix."""
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return
+    dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+
+
 def checksum(t: torch.Tensor) -> int:
     """Bitwise checksum of a float tensor (cross-rank parameter identity checks)."""
     b = t.detach().contiguous().view(torch.int32).to(torch.int64)

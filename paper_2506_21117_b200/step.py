@@ -227,13 +227,15 @@ class LocalOptimizer:
     # -- the three C-ABI calls -------------------------------------------------------------------
     def forward(self, cameras, targets: Optional[torch.Tensor] = None, n_views_total: Optional[int] = None,
                 images: bool = False, tile_mask: bool = False, all_tiles: bool = False,
-                stream=None) -> ForwardResult:
+                stream=None, loss_out: Optional[torch.Tensor] = None) -> ForwardResult:
         cams = camera_structs(cameras)
         V = len(cameras)
         W, H = cameras[0].width, cameras[0].height
         dev = self.params.device
         # written (not accumulated) by the call: no fill kernel
-        loss = torch.empty(1, dtype=torch.float32, device=dev) if targets is not None else None
+        loss = None
+        if targets is not None:
+            loss = loss_out if loss_out is not None else torch.empty(1, dtype=torch.float32, device=dev)
         img = torch.empty((V, 3, H, W), dtype=torch.float32, device=dev) if images else None
         tm = torch.empty((V, -(-H // 16), -(-W // 16)), dtype=torch.uint8, device=dev) if tile_mask else None
         if targets is not None:
@@ -270,10 +272,15 @@ class LocalOptimizer:
               self.ctx)
         return out[:A]
 
-    def backward(self, dL_dimages: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    def backward(self, dL_dimages: Optional[torch.Tensor] = None, stream=None,
+                 out: Optional[torch.Tensor] = None) -> torch.Tensor:
         A = self.active_count() if self._A is None else self._A
-        grad = torch.empty((max(A, 1), row4(self.params.sh_degree), 4), dtype=torch.float32,
-                           device=self.params.device)
+        if out is not None:   # caller-provided rows (e.g. a PackedRows buffer): [>= A, ROW4, 4]
+            assert out.is_contiguous() and out.shape[0] >= A and out.shape[1] == row4(self.params.sh_degree)
+            grad = out
+        else:
+            grad = torch.empty((max(A, 1), row4(self.params.sh_degree), 4), dtype=torch.float32,
+                               device=self.params.device)
         g = self.params.struct()
         check(lib.cls_render_bwd(self.ctx, ctypes.byref(g),
                                  ctypes.c_void_p(dL_dimages.data_ptr() if dL_dimages is not None else None),
@@ -471,15 +478,29 @@ class LocalOptimizer:
 
     # -- one full local-optimisation step ----------------------------------------------------------
     def step(self, cameras, targets: torch.Tensor, n_views_total: Optional[int] = None,
-             allreduce: Optional[Callable[[torch.Tensor, torch.Tensor], None]] = None, stream=None):
-        """fwd -> |O^t| -> bwd -> (optional all-reduce of grad rows + loss) -> masked Adam.
-        Returns the device loss tensor (this rank's share unless all-reduced)."""
-        res = self.forward(cameras, targets, n_views_total=n_views_total, stream=stream)
-        grad = self.backward(stream=stream)
-        if allreduce is not None:
-            allreduce(grad, res.loss)
+             allreduce: Optional[Callable[[torch.Tensor], None]] = None, stream=None):
+        """fwd -> |O^t| -> bwd -> (optional all-reduce) -> masked Adam.  With `allreduce` (called with
+        one flat tensor, dist.allreduce_packed) the loss and the A gradient rows are written by the
+        library into one packed buffer and reduced as a single contiguous prefix.
+        Returns the device loss tensor (summed over ranks when all-reduced)."""
+        if allreduce is None:
+            res = self.forward(cameras, targets, n_views_total=n_views_total, stream=stream)
+            grad = self.backward(stream=stream)
+            self.adam(grad, stream=stream)
+            return res.loss
+        pk = self._packed()
+        self.forward(cameras, targets, n_views_total=n_views_total, stream=stream, loss_out=pk.loss)
+        A = self.active_count()
+        grad = self.backward(stream=stream, out=pk.rows)
+        allreduce(pk.prefix(A))
         self.adam(grad, stream=stream)
-        return res.loss
+        return pk.loss
+
+    def _packed(self):
+        from .dist import PackedRows
+        if getattr(self, "_pk", None) is None:
+            self._pk = PackedRows(int(self.limits.max_active), 4 * row4(self.params.sh_degree), self.params.device)
+        return self._pk
 
 
 class GraphStep:
@@ -491,7 +512,8 @@ class GraphStep:
     capacity-sized gradient buffer (rows >= the active count; the kernels read |O^t| on the device)
     and the Adam step, which lives on the device (cls_adam_masked_devstep).  Single GPU."""
 
-    def __init__(self, opt: "LocalOptimizer", cameras, targets: torch.Tensor, n_views_total: Optional[int] = None):
+    def __init__(self, opt: "LocalOptimizer", cameras, targets: torch.Tensor, n_views_total: Optional[int] = None,
+                 allreduce: Optional[Callable[[torch.Tensor], None]] = None):
         p = opt.params
         self.opt = opt
         self.cams = camera_structs(cameras)
@@ -501,9 +523,13 @@ class GraphStep:
         assert (targets.is_cuda or targets.is_pinned()) and targets.is_contiguous() and \
             targets.dtype in (torch.float32, torch.uint8)
         dev = p.device
-        self.loss = torch.zeros(1, dtype=torch.float32, device=dev)
-        self.grad = torch.zeros((max(int(opt.limits.max_active), 1), row4(p.sh_degree), 4), dtype=torch.float32,
-                                device=dev)
+        # loss and gradient rows in ONE packed buffer (dist.PackedRows): with `allreduce` (N > 1) the
+        # graph reduces its whole row capacity (max_active rows; A > max_active is a reported overflow)
+        from .dist import PackedRows
+        self.packed = PackedRows(int(opt.limits.max_active), 4 * row4(p.sh_degree), dev)
+        self.loss = self.packed.loss
+        self.grad = self.packed.rows
+        self.allreduce = allreduce
         self.step_dev = torch.tensor([p.step + 1], dtype=torch.int32, device=dev)
         self.stream = torch.cuda.Stream(device=dev)
         self.stream.wait_stream(torch.cuda.current_stream())
@@ -513,6 +539,8 @@ class GraphStep:
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph, stream=self.stream):
             self._fwd_bwd()
+            if self.allreduce is not None:
+                self.allreduce(self.packed.flat)
             self._adam()
 
     def _fwd_bwd(self):

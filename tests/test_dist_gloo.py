@@ -13,7 +13,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2506_21117_b200.dist import DataParallelStep, allreduce_rows, checksum, ranks_agree, shard_views
+from paper_2506_21117_b200.dist import (DataParallelStep, PackedRows, allreduce_packed, allreduce_rows, checksum,
+                                        ranks_agree, shard_views)
 
 
 def test_shard_views_contiguous_partition():
@@ -106,3 +107,30 @@ def test_allreduce_rows_is_noop_without_process_group():
     loss = torch.tensor([2.0])
     allreduce_rows(g, loss)
     assert torch.all(g == 1) and loss.item() == 2.0
+
+
+def _packed_worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    pk = PackedRows(capacity_rows=8, row_floats=16, device="cpu")
+    pk.loss.fill_(1.5 + rank)
+    pk.rows[:5] = torch.arange(5 * 16, dtype=torch.float32).view(5, 4, 4) * (rank + 1)
+    pk.rows[5:] = 7.0                      # rows beyond the live prefix (A = 5) are not reduced
+    allreduce_packed(pk.prefix(5))
+    np.savez(os.path.join(out_dir, f"p{rank}.npz"), flat=pk.flat.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_packed_rows_allreduce_prefix():
+    """PackedRows: the loss and the first A rows are one contiguous prefix, reduced in place by ONE
+    collective; the rows beyond A are untouched."""
+    with tempfile.TemporaryDirectory() as d:
+        mp.start_processes(_packed_worker, args=(2, _free_port(), d), nprocs=2, join=True, start_method="spawn")
+        f0, f1 = (np.load(os.path.join(d, f"p{r}.npz"))["flat"] for r in (0, 1))
+    assert f0[0] == 1.5 + 2.5 and f1[0] == 1.5 + 2.5
+    rows = f0[4:].reshape(8, 16)
+    assert np.array_equal(rows[:5].reshape(-1), np.arange(5 * 16, dtype=np.float32) * 3)
+    assert np.all(rows[5:] == 7.0)
+    assert np.array_equal(f0[:4 + 5 * 16], f1[:4 + 5 * 16])
