@@ -10,9 +10,10 @@ TAG=$1; CFG=${2:-c4}
 O=gpurun_out/${TAG}_${CFG}
 python bench.py --config $CFG > ${O}_bench.json 2> ${O}_bench.err
 tail -1 ${O}_bench.json
-python bench.py --config $CFG --eager --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > ${O}_eager.log 2>&1
+EAGER="--config $CFG --eager --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-local-full"
+python bench.py $EAGER > ${O}_eager.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file ${O}_launches.csv \
-    python bench.py --config $CFG --eager --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > ${O}_ncu_launches.log 2>&1
+    python bench.py $EAGER > ${O}_ncu_launches.log 2>&1
 # index of the 4th k_member launch = first kernel of the 4th eager step
 SKIP=$(python - "$O" <<'EOF'
 import csv, sys
@@ -31,6 +32,11 @@ print(member[3], member[4] - member[3])
 EOF
 )
 set -- $SKIP
-ncu --set full --clock-control none --import-source on --launch-skip $1 --launch-count $2 -o ${O}_full \
-    python bench.py --config $CFG --eager --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > ${O}_ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on --launch-skip $1 --launch-count $2 -o /tmp/${TAG}_${CFG}_full \
+    python bench.py $EAGER > ${O}_ncu_full.log 2>&1
+# the report itself stays on the box (gpurun copies back <= 64 MiB): its summaries come back
+ncu -i /tmp/${TAG}_${CFG}_full.ncu-rep --page raw --csv > /tmp/${TAG}_${CFG}_raw.csv
+python tools/ncu_full.py /tmp/${TAG}_${CFG}_raw.csv --header "${TAG} ${CFG} ncu --set full of one eager step" \
+    --summary ${O}_ncu_full_summary.txt --traffic ${O}_ncu_traffic.json
+ncu -i /tmp/${TAG}_${CFG}_full.ncu-rep --page source --csv --print-source sass -k regex:k_fwd > ${O}_kfwd_sass.csv 2>&1 || true
 ls -la ${O}_*
