@@ -445,7 +445,14 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
         }
     }
     cudaMemsetAsync(s.cnt, 0, sizeof(Counters), st);
-    run(c, P_MEMBER, st, [&] { launch_member(p, d, regs, s, st); });
+    run(c, P_MEMBER, st, [&] {
+        if (cached) {   // full membership only until the cache is valid; then only S0's rows can be active
+            launch_member(p, d, regs, s, st, &c->cb.st->valid);
+            launch_member_list(p, c->cb.s0, &c->cb.st->A0, &c->cb.st->valid, regs, s, st);
+        } else {
+            launch_member(p, d, regs, s, st);
+        }
+    });
     cudaMemcpyAsync(c->h_A, &s.cnt->A, sizeof(int), cudaMemcpyDeviceToHost, st);
     if (!c->captured) cudaEventRecord(c->ev_member, st);
     run(c, P_MASK, st, [&] {

@@ -308,16 +308,27 @@ __global__ void __launch_bounds__(MG_THREADS) k_merge_frozen(CacheBufs cb, Scrat
             if (in_smem)
                 for (int j = threadIdx.x; j < nd; j += MG_THREADS) qd[j] = cb.dq[d0 + j];
             __syncthreads();
-            for (int i = w.y + threadIdx.x; i < f1; i += MG_THREADS) {
-                const unsigned long long key = fsorted[i];
-                const unsigned r = (unsigned)(key & RK_IDX_MASK);
-                int lo = 0, hi = nd;   // dynamic units of the segment with position <= r
-                while (lo < hi) {
-                    const int m = (lo + hi) >> 1;
-                    if ((in_smem ? qd[m] : cb.dq[d0 + m]) <= r) lo = m + 1;
-                    else hi = m;
+            // four independent units per thread per iteration: four loads in flight (latency-bound otherwise)
+            for (int i0 = w.y + threadIdx.x; i0 < f1; i0 += 4 * MG_THREADS) {
+                unsigned long long key[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int i = i0 + u * MG_THREADS;
+                    key[u] = i < f1 ? fsorted[i] : 0ull;
                 }
-                merged[i + d0 + lo] = key;
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int i = i0 + u * MG_THREADS;
+                    if (i >= f1) break;
+                    const unsigned r = (unsigned)(key[u] & RK_IDX_MASK);
+                    int lo = 0, hi = nd;   // dynamic units of the segment with position <= r
+                    while (lo < hi) {
+                        const int m = (lo + hi) >> 1;
+                        if ((in_smem ? qd[m] : cb.dq[d0 + m]) <= r) lo = m + 1;
+                        else hi = m;
+                    }
+                    merged[i + d0 + lo] = key[u];
+                }
             }
         }
         __syncthreads();

@@ -18,9 +18,11 @@ int64_t g_launches = 0;
 #define MEMBER_TILE (MEMBER_THREADS * MEMBER_ITEMS)
 
 __global__ void __launch_bounds__(MEMBER_THREADS)
-k_member(const float4 *__restrict__ mean_op, int n, const __grid_constant__ RegSet regs, Scratch s)
+k_member(const float4 *__restrict__ mean_op, int n, const __grid_constant__ RegSet regs, Scratch s,
+         const int *__restrict__ skip)
 {
     __shared__ int s_tile;
+    if (skip && *skip) return;   // the static cache is valid: k_member_list tests its rows instead
     __shared__ int s_wcnt[MEMBER_ITEMS][MEMBER_THREADS / 32];
     __shared__ unsigned long long s_prefix;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -75,11 +77,90 @@ k_member(const float4 *__restrict__ mean_op, int n, const __grid_constant__ RegS
     }
 }
 
-void launch_member(const Params &g, const StepDims &d, const RegSet &regs, const Scratch &s, cudaStream_t st)
+void launch_member(const Params &g, const StepDims &d, const RegSet &regs, const Scratch &s, cudaStream_t st,
+                   const int *skip)
 {
     const int blocks = (d.n + MEMBER_TILE - 1) / MEMBER_TILE;
     cudaMemsetAsync(s.st_member, 0, sizeof(unsigned long long) * blocks, st);
-    k_member<<<blocks, MEMBER_THREADS, 0, st>>>(g.mean_op, d.n, regs, s);
+    k_member<<<blocks, MEMBER_THREADS, 0, st>>>(g.mean_op, d.n, regs, s, skip);
+    g_launches++;
+}
+
+// Membership of the rows of a list only (the static cache's S0, ascending), same stable compaction:
+// rows outside S0 never move and were outside the regions when S0 was formed (DESIGN.md "Static
+// cache"), so their ord stays -1 from the last full membership.  Persistent blocks claim tiles of the
+// list in ticket order (the look-back only waits on earlier tickets).  Runs only while the cache is
+// valid (*valid != 0); the full k_member runs otherwise.
+__global__ void __launch_bounds__(MEMBER_THREADS)
+k_member_list(const float4 *__restrict__ mean_op, const int *__restrict__ list, const int *__restrict__ n_list,
+              const int *__restrict__ valid, const __grid_constant__ RegSet regs, Scratch s)
+{
+    __shared__ int s_tile;
+    __shared__ int s_wcnt[MEMBER_ITEMS][MEMBER_THREADS / 32];
+    __shared__ unsigned long long s_prefix;
+    if (!*valid) return;
+    const int n = *n_list;
+    const int ntiles = (n + MEMBER_TILE - 1) / MEMBER_TILE;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    while (true) {
+        if (tid == 0) s_tile = atomicAdd(&s.cnt->member_tiles, 1);
+        __syncthreads();
+        const int tile = s_tile;
+        if (tile >= ntiles) break;
+        const int base = tile * MEMBER_TILE;
+        unsigned ballots[MEMBER_ITEMS];
+        int rows[MEMBER_ITEMS];
+#pragma unroll
+        for (int k = 0; k < MEMBER_ITEMS; k++) {
+            const int e = base + k * MEMBER_THREADS + tid;
+            bool in = false;
+            rows[k] = e < n ? list[e] : -1;
+            if (e < n) in = in_regions(__ldg(mean_op + rows[k]), regs);
+            ballots[k] = __ballot_sync(0xffffffffu, in);
+            if (lane == 0) s_wcnt[k][warp] = __popc(ballots[k]);
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const int nw = MEMBER_THREADS / 32;
+            const int total_cells = MEMBER_ITEMS * nw;
+            int v0 = lane < total_cells ? s_wcnt[lane / nw][lane % nw] : 0;
+            int v1 = lane + 32 < total_cells ? s_wcnt[(lane + 32) / nw][(lane + 32) % nw] : 0;
+            int inc0 = v0, inc1 = v1;
+            for (int o = 1; o < 32; o <<= 1) {
+                int t0 = __shfl_up_sync(0xffffffffu, inc0, o);
+                int t1 = __shfl_up_sync(0xffffffffu, inc1, o);
+                if (lane >= o) { inc0 += t0; inc1 += t1; }
+            }
+            const int tot0 = __shfl_sync(0xffffffffu, inc0, 31);
+            inc1 += tot0;
+            if (lane < total_cells) s_wcnt[lane / nw][lane % nw] = inc0 - v0;
+            if (lane + 32 < total_cells) s_wcnt[(lane + 32) / nw][(lane + 32) % nw] = inc1 - v1;
+            const int agg = __shfl_sync(0xffffffffu, inc1, 31);
+            const unsigned long long pre = lookback_warp(s.st_member, tile, (unsigned long long)agg);
+            if (lane == 0) {
+                s_prefix = pre;
+                if (tile == ntiles - 1) s.cnt->A = (int)(pre + agg);
+            }
+        }
+        __syncthreads();
+        const int prefix = (int)s_prefix;
+        const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+        for (int k = 0; k < MEMBER_ITEMS; k++) {
+            if (rows[k] < 0) continue;
+            const bool in = (ballots[k] >> lane) & 1u;
+            const int pos = prefix + s_wcnt[k][warp] + __popc(ballots[k] & lt);
+            if (in) s.idx[pos] = rows[k];
+            s.ord[rows[k]] = in ? pos : -1;
+        }
+        __syncthreads();
+    }
+}
+
+void launch_member_list(const Params &g, const int *list, const int *n_list, const int *valid, const RegSet &regs,
+                        const Scratch &s, cudaStream_t st)
+{
+    k_member_list<<<148 * 2, MEMBER_THREADS, 0, st>>>(g.mean_op, list, n_list, valid, regs, s);
     g_launches++;
 }
 

@@ -51,24 +51,31 @@ k_rs_upsweep(const unsigned long long *__restrict__ keys, const int *__restrict_
     for (int d = threadIdx.x; d < BINS; d += RS_THREADS) counts[(size_t)d * gridDim.x + blockIdx.x] = hist[d];
 }
 
-// one warp per digit: exclusive scan of counts[d][0..G) in place; totals[d] = sum
+// one warp per digit: exclusive scan of counts[d][0..G) in place; totals[d] = sum.  Only the blocks
+// that own a tile for this n are scanned (the others counted nothing and never scatter): a small sort
+// (the static cache's per-step records) does not pay for the whole persistent grid's table.
 __global__ void __launch_bounds__(256) k_rs_scan(unsigned *__restrict__ counts, unsigned *__restrict__ totals,
-                                                 int bins, int G)
+                                                 int bins, int G, const int *__restrict__ n_ptr, int max_n,
+                                                 const int *__restrict__ skip)
 {
     const int d = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (d >= bins) return;
+    const int n = (skip && *skip) ? 0 : min(*n_ptr, max_n);
+    const int ntiles = (n + RS_TILE - 1) / RS_TILE;
+    const int per = max((ntiles + G - 1) / G, 1);
+    const int used = min(G, (ntiles + per - 1) / per);   // blocks with t0 < t1 in rs_block_range
     unsigned *row = counts + (size_t)d * G;
     unsigned carry = 0u;
-    for (int b0 = 0; b0 < G; b0 += 32) {
+    for (int b0 = 0; b0 < used; b0 += 32) {
         const int b = b0 + lane;
-        const unsigned v = b < G ? row[b] : 0u;
+        const unsigned v = b < used ? row[b] : 0u;
         unsigned inc = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const unsigned t = __shfl_up_sync(0xffffffffu, inc, o);
             if (lane >= o) inc += t;
         }
-        if (b < G) row[b] = carry + inc - v;
+        if (b < used) row[b] = carry + inc - v;
         carry += __shfl_sync(0xffffffffu, inc, 31);
     }
     if (lane == 0) totals[d] = carry;
@@ -260,7 +267,7 @@ static void rs_pass(unsigned long long *kin, unsigned long long *kout, unsigned 
         cudaFuncSetAttribute(k_rs_downsweep<BITS, VALS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
     });
     k_rs_upsweep<BITS><<<RS_GRID, RS_THREADS, 0, st>>>(kin, n_ptr, max_n, shift, counts, skip);
-    k_rs_scan<<<((1 << BITS) + 7) / 8, 256, 0, st>>>(counts, totals, 1 << BITS, RS_GRID);
+    k_rs_scan<<<((1 << BITS) + 7) / 8, 256, 0, st>>>(counts, totals, 1 << BITS, RS_GRID, n_ptr, max_n, skip);
     k_rs_downsweep<BITS, VALS><<<RS_GRID, RS_THREADS, SM, st>>>(kin, kout, vin, vout, n_ptr, max_n, shift, counts,
                                                                 totals, skip);
     g_launches += 3;

@@ -20,7 +20,10 @@ struct Params {
 };
 
 // (1) membership + stable compaction -> idx, ord, A        (k_member.cu)
-void launch_member(const Params &g, const StepDims &d, const RegSet &regs, const Scratch &s, cudaStream_t st);
+void launch_member(const Params &g, const StepDims &d, const RegSet &regs, const Scratch &s, cudaStream_t st,
+                   const int *skip = nullptr);
+void launch_member_list(const Params &g, const int *list, const int *n_list, const int *valid, const RegSet &regs,
+                        const Scratch &s, cudaStream_t st);
 // (1b) active tile mask per view + summed-area tables       (k_member.cu)
 void launch_active_mask(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st);
 // (2) projection / cull of every Gaussian vs the mask -> records (k_project.cu)
