@@ -59,6 +59,7 @@ typedef struct {
     float R[9];
     float t[3];
     int32_t width, height;   /* >= 16 each */
+    int32_t set;             /* change set of the view, 0..31 (NEXT-3, see cls_region.set); 0 by default */
 } cls_camera;
 
 /* A change region (P:175-182 bounding spheres s_i = (m_i, 1.1 d_i)).
@@ -69,6 +70,10 @@ typedef struct {
     float a[3];
     float b[3];
     float r;
+    int32_t set;   /* change set 0..31 (concurrent updates; NEXT-3): a view of set s
+                      activates only the Gaussians inside a region of set s -- the others are composited
+                      in that view but get no gradient from it; O^t of the step is the union over sets.
+                      All 0 (default): one change set, the union of the regions (BASELINE c5). */
 } cls_region;
 
 typedef struct {

@@ -90,8 +90,11 @@ def sh_basis(degree: int, d) -> np.ndarray:
 # stage wrappers
 # ---------------------------------------------------------------------------
 
-def membership(scene) -> np.ndarray:
-    """bool[N]: centre inside the union of the change regions (R21)."""
+def membership(scene, regions=None) -> np.ndarray:
+    """bool[N]: centre inside the union of the change regions (R21) -- of `regions` if given."""
+    if regions is not None:
+        import dataclasses as _dc
+        scene = _dc.replace(scene, regions=list(regions))
     n = scene.n
     kinds = np.array([r.kind for r in scene.regions], np.int32)
     ra = _f64([r.a for r in scene.regions]).reshape(-1, 3) if scene.regions else np.zeros((0, 3))
@@ -205,9 +208,12 @@ def backward_project(scene, view: int, active: np.ndarray, proj, grad2d: np.ndar
 
 def forward_backward(scene, views: Optional[Sequence[int]] = None, active: Optional[np.ndarray] = None,
                      literal: bool = False, all_tiles: bool = False, dL_dC=None, n_views_total=None,
-                     window=None, with_grad: bool = True):
+                     window=None, with_grad: bool = True, per_set: bool = False):
     """One full forward + backward over ``views`` (default all).  Returns
-    dict(active, idx, loss, renders[list], grad [N, stride])."""
+    dict(active, idx, loss, renders[list], grad [N, stride]).
+    per_set (NEXT-3, "apply our method in parallel to each change"): view v activates
+    only the Gaussians inside the regions of its own change set (camera.set == region.set); O^t (idx) is
+    the union; every other Gaussian is composited in that view but gets no gradient from it."""
     if views is None:
         views = range(len(scene.cameras))
     views = list(views)
@@ -220,13 +226,20 @@ def forward_backward(scene, views: Optional[Sequence[int]] = None, active: Optio
     grad = np.zeros((scene.n, grad_stride(scene.sh_degree)))
     renders = []
     loss = 0.0
+    set_active = {}
     for j, v in enumerate(views):
         proj = project(scene, v)
         up = None if dL_dC is None else dL_dC[j]
-        r = render(scene, v, active, proj, literal=literal, all_tiles=all_tiles, dL_dC=up,
+        act_v = active
+        if per_set:
+            sv = int(getattr(scene.cameras[v], "set", 0))
+            if sv not in set_active:
+                set_active[sv] = membership(scene, [r for r in scene.regions if int(getattr(r, "set", 0)) == sv])
+            act_v = set_active[sv]
+        r = render(scene, v, act_v, proj, literal=literal, all_tiles=all_tiles, dL_dC=up,
                    with_grad=with_grad, loss_scale=scale, window=window)
         if with_grad:
-            backward_project(scene, v, active, proj, r["grad2d"], grad)
+            backward_project(scene, v, act_v, proj, r["grad2d"], grad)
         loss += r["loss_sum"] * scale
         r["proj"] = proj
         r["scene"], r["view"] = scene, v   # for the parity protocol's decision replay

@@ -38,11 +38,12 @@ class ClsError(RuntimeError):
 class cls_camera(ctypes.Structure):
     _fields_ = [("fx", ctypes.c_float), ("fy", ctypes.c_float), ("cx", ctypes.c_float), ("cy", ctypes.c_float),
                 ("R", ctypes.c_float * 9), ("t", ctypes.c_float * 3), ("width", ctypes.c_int32),
-                ("height", ctypes.c_int32)]
+                ("height", ctypes.c_int32), ("set", ctypes.c_int32)]
 
 
 class cls_region(ctypes.Structure):
-    _fields_ = [("kind", ctypes.c_int32), ("a", ctypes.c_float * 3), ("b", ctypes.c_float * 3), ("r", ctypes.c_float)]
+    _fields_ = [("kind", ctypes.c_int32), ("a", ctypes.c_float * 3), ("b", ctypes.c_float * 3), ("r", ctypes.c_float),
+                ("set", ctypes.c_int32)]
 
 
 class cls_gaussians(ctypes.Structure):

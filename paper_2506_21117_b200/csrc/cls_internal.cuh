@@ -28,7 +28,7 @@ struct GCam {
     float t[3];
     float fx, fy, cx, cy;
     float oc[3];   // camera centre -R^T t (for SH view directions)
-    float pad;
+    int set;       // change set of the view (NEXT-3 per-change-set activation; 0 in the union mode)
 };
 
 struct CamSet {
@@ -39,6 +39,7 @@ struct CamSet {
 
 struct RegSet {
     int n;
+    int set[CLS_MAX_REGIONS];   // change set of each region (0 .. 31)
     int kind[CLS_MAX_REGIONS];
     float a[CLS_MAX_REGIONS][3];
     float b[CLS_MAX_REGIONS][3];
@@ -131,6 +132,7 @@ struct Scratch {
     // membership
     int *idx;               // [maxN]   O^t, ascending
     int *ord;               // [maxN]   active ordinal or -1
+    unsigned *setmask;      // [maxN]   change sets holding the centre (bit s), valid where ord >= 0
     unsigned long long *st_member;  // look-back status
     // masks
     uint8_t *mask;          // [V][T]
@@ -260,6 +262,31 @@ __device__ __forceinline__ unsigned long long lookback_warp(unsigned long long *
     return prefix;
 }
 
+// change sets whose regions hold the Gaussian centre: bit s set iff the centre lies in a region of
+// set s (R21 per region, same fp64 tests as in_regions); 0 = frozen.  NEXT-3: a view of
+// change set s activates only the Gaussians of set s.
+__device__ __forceinline__ unsigned region_sets(const float4 m, const RegSet &regs)
+{
+    const double x = m.x, y = m.y, z = m.z;
+    unsigned mask = 0u;
+    for (int j = 0; j < regs.n; j++) {
+        bool in;
+        if (regs.kind[j] == 0) {
+            const double dx = __dsub_rn(x, (double)regs.a[j][0]);
+            const double dy = __dsub_rn(y, (double)regs.a[j][1]);
+            const double dz = __dsub_rn(z, (double)regs.a[j][2]);
+            const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+            const double r = regs.r[j];
+            in = d2 <= __dmul_rn(r, r);
+        } else {
+            in = m.x >= regs.a[j][0] && m.x <= regs.b[j][0] && m.y >= regs.a[j][1] && m.y <= regs.b[j][1] &&
+                 m.z >= regs.a[j][2] && m.z <= regs.b[j][2];
+        }
+        if (in) mask |= 1u << regs.set[j];
+    }
+    return mask;
+}
+
 // Gaussian centre in the union of the change regions (R21: spheres or AABBs, inclusive), fp64
 __device__ __forceinline__ bool in_regions(const float4 m, const RegSet &regs)
 {
@@ -381,6 +408,14 @@ __device__ __forceinline__ bool project_gaussian(const float4 mo, const float4 q
     double M[9];
     gauss_m64(q, ls, M);
     return project_view(mo, M, c, view_lims(c, W, H), TX, TY, p);
+}
+
+// active ordinal of row i in a view of change set `set` (NEXT-3): its ordinal in O^t if one of its
+// change sets is the view's, else -1 (composited in that view, never differentiated)
+__device__ __forceinline__ int view_ordinal(const Scratch &s, int i, int set)
+{
+    const int o = s.ord[i];
+    return (o >= 0 && ((s.setmask[i] >> set) & 1u)) ? o : -1;
 }
 
 // number of active tiles in [x0,x1) x [y0,y1) from a summed-area table with row pitch TX+1

@@ -168,7 +168,7 @@ cls_status cls_destroy(cls_ctx *c)
 {
     if (!c) return CLS_ERR_INVALID_ARGUMENT;
     cudaSetDevice(c->device);
-    void *ptrs[] = {c->s.idx, c->s.ord, c->s.st_member, c->s.mask, c->s.sat, c->s.mdiff, c->s.rowmask, c->s.view_bbox, c->s.rec,
+    void *ptrs[] = {c->s.idx, c->s.ord, c->s.setmask, c->s.st_member, c->s.mask, c->s.sat, c->s.mdiff, c->s.rowmask, c->s.view_bbox, c->s.rec,
                     c->s.srid, c->s.long_runs, c->s.rec_gid, c->s.rrows, c->s.cand, c->s.rkey,
                     c->s.rkey_alt, c->s.rcnt, c->s.ukey, c->s.ukey_alt,
                     c->s.roff, c->s.st_scan, c->s.seg_off, c->s.seg_end, c->s.st_tiles, c->s.items, c->s.item_of_tile,
@@ -232,7 +232,7 @@ cls_status cls_create(cls_ctx **out, int device, const cls_limits *lim)
     const size_t R = (size_t)lim->max_records, P = (size_t)lim->max_pairs;
     const size_t SAT = V * (c->maxTY + 1) * (c->maxTX + 1);
     Scratch &s = c->s;
-    bool ok = dalloc(&s.idx, N) && dalloc(&s.ord, N) && dalloc(&s.st_member, N / 2048 + 2) && dalloc(&s.mask, VT) &&
+    bool ok = dalloc(&s.idx, N) && dalloc(&s.ord, N) && dalloc(&s.setmask, N) && dalloc(&s.st_member, N / 2048 + 2) && dalloc(&s.mask, VT) &&
               dalloc(&s.sat, SAT) && dalloc(&s.mdiff, SAT) && dalloc(&s.rowmask, V * c->maxTY * ((c->maxTX + 31) / 32)) &&
               dalloc(&s.view_bbox, V) && dalloc(&s.rec, R) && dalloc(&s.srid, R) && dalloc(&s.long_runs, R / 33 + 1) && dalloc(&s.rec_gid, R) && dalloc(&s.rrows, R) &&
               dalloc(&s.cand, R + R / 2 + 1024) && dalloc(&s.rkey, R) && dalloc(&s.rkey_alt, R) &&
@@ -358,10 +358,15 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
         } else {
             return fail(c, CLS_ERR_INVALID_ARGUMENT, "region %d: unknown kind %d", j, r.kind);
         }
+        if (r.set < 0 || r.set > 31) return fail(c, CLS_ERR_INVALID_ARGUMENT, "region %d: change set %d", j, r.set);
         regs.kind[j] = r.kind;
+        regs.set[j] = r.set;
         for (int q = 0; q < 3; q++) { regs.a[j][q] = r.a[q]; regs.b[j][q] = r.b[q]; }
         regs.r[j] = r.r;
     }
+    for (int v = 0; v < n_views; v++)
+        if (cams[v].set < 0 || cams[v].set > 31)
+            return fail(c, CLS_ERR_INVALID_ARGUMENT, "view %d: change set %d", v, cams[v].set);
     if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, CLS_ERR_CUDA, "cudaSetDevice failed");
     cudaStream_t st = (cudaStream_t)stream;
     StepDims d{};
@@ -384,7 +389,7 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
         gc.fx = cm.fx; gc.fy = cm.fy; gc.cx = cm.cx; gc.cy = cm.cy;
         for (int q = 0; q < 3; q++)   // o_cam = -R^T t
             gc.oc[q] = (float)-((double)cm.R[q] * cm.t[0] + (double)cm.R[3 + q] * cm.t[1] + (double)cm.R[6 + q] * cm.t[2]);
-        gc.pad = 0.f;
+        gc.set = cm.set;
     }
     Params p{reinterpret_cast<const float4 *>(g->mean_op), reinterpret_cast<const float4 *>(g->quat),
              reinterpret_cast<const float4 *>(g->log_scale), reinterpret_cast<const float4 *>(g->sh)};
@@ -438,6 +443,7 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
         put(&regs.n, sizeof regs.n);
         for (int j = 0; j < regs.n; j++) {
             put(&regs.kind[j], sizeof(int)); put(regs.a[j], 12); put(regs.b[j], 12); put(&regs.r[j], 4);
+            put(&regs.set[j], sizeof(int));
         }
         if (sig != c->cache_sig) {
             cudaMemsetAsync(&c->cb.st->valid, 0, sizeof(int), st);
@@ -837,6 +843,7 @@ static bool regset_of(cls_ctx *c, const cls_region *regions, int32_t n_regions, 
         if (r.kind == 0 ? !(r.r > 0.f) : (r.kind != 1 || !(r.a[0] <= r.b[0] && r.a[1] <= r.b[1] && r.a[2] <= r.b[2])))
             return false;
         regs.kind[j] = r.kind;
+        regs.set[j] = (r.set >= 0 && r.set <= 31) ? r.set : 0;
         for (int q = 0; q < 3; q++) { regs.a[j][q] = r.a[q]; regs.b[j][q] = r.b[q]; }
         regs.r[j] = r.r;
     }

@@ -100,6 +100,7 @@ __global__ void __launch_bounds__(256) k_dilated_rects(const float4 *__restrict_
          e += (long long)gridDim.x * blockDim.x) {
         const int a = (int)(e / cams.n), v = (int)(e % cams.n);
         const int i = s.idx[a];
+        if (!((s.setmask[i] >> cams.c[v].set) & 1u)) continue;   // not active for this view's change set
         Proj p;
         if (!project_gaussian(__ldg(mean_op + i), __ldg(quat + i), __ldg(log_scale + i), cams.c[v], cams.W, cams.H,
                               cams.TX, cams.TY, p))
@@ -444,7 +445,7 @@ __global__ void __launch_bounds__(256, 3) k_dyn_project(CacheBufs cb, Scratch s,
             qcut = Mr[10];
             mo = __ldg(mean_op + i);
             if (project_view(mo, M, s_cams[v], s_lims[v], TX, TY, p)) {
-                if (s.ord[i] >= 0) {   // active: its rect joins the view's active tile mask (R9)
+                if (view_ordinal(s, i, s_cams[v].set) >= 0) {   // active here: its rect joins the mask (R9)
                     int *Dd = s.mdiff + (size_t)v * (TY + 1) * P;
                     atomicAdd(Dd + p.y0 * P + p.x0, 1);
                     atomicAdd(Dd + p.y0 * P + p.x1, -1);
@@ -493,8 +494,8 @@ __global__ void __launch_bounds__(256, 3) k_dyn_project(CacheBufs cb, Scratch s,
         R.xy = make_float4(uh, __double2float_rn(p.u - (double)uh), vh, __double2float_rn(p.v - (double)vh));
         R.co = make_float4(__double2float_rn(a1), __double2float_rn(a2), __double2float_rn(b1), __double2float_rn(b2));
         R.rgb = make_float4(fmaxf(col[0], 0.0f), fmaxf(col[1], 0.0f), fmaxf(col[2], 0.0f), (float)o64);
-        R.aux = make_float4(__double2float_ru(qc), __int_as_float(s.ord[i]), __int_as_float(p.x0 | (p.y0 << 16)),
-                            __int_as_float(p.x1 | (p.y1 << 16)));
+        R.aux = make_float4(__double2float_ru(qc), __int_as_float(view_ordinal(s, i, c.set)),
+                            __int_as_float(p.x0 | (p.y0 << 16)), __int_as_float(p.x1 | (p.y1 << 16)));
         cb.dcand[slot] = R;
         const unsigned dk = min(__float_as_uint(__double2float_rn(p.tz)) - 0x3E4CCCCDu, (1u << RK_DEPTH_BITS) - 1u);
         cb.dcinfo[slot] = make_int4(i, v, (int)dk, p.y1 - p.y0);

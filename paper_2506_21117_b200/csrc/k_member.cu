@@ -34,9 +34,10 @@ k_member(const float4 *__restrict__ mean_op, int n, const __grid_constant__ RegS
 #pragma unroll
     for (int k = 0; k < MEMBER_ITEMS; k++) {
         const int i = base + k * MEMBER_THREADS + tid;
-        bool in = false;
-        if (i < n) in = in_regions(__ldg(mean_op + i), regs);
-        ballots[k] = __ballot_sync(0xffffffffu, in);
+        unsigned sm = 0u;
+        if (i < n) sm = region_sets(__ldg(mean_op + i), regs);
+        if (i < n) s.setmask[i] = sm;
+        ballots[k] = __ballot_sync(0xffffffffu, sm != 0u);
         if (lane == 0) s_wcnt[k][warp] = __popc(ballots[k]);
     }
     __syncthreads();
@@ -113,10 +114,11 @@ k_member_list(const float4 *__restrict__ mean_op, const int *__restrict__ list, 
 #pragma unroll
         for (int k = 0; k < MEMBER_ITEMS; k++) {
             const int e = base + k * MEMBER_THREADS + tid;
-            bool in = false;
+            unsigned sm = 0u;
             rows[k] = e < n ? list[e] : -1;
-            if (e < n) in = in_regions(__ldg(mean_op + rows[k]), regs);
-            ballots[k] = __ballot_sync(0xffffffffu, in);
+            if (e < n) sm = region_sets(__ldg(mean_op + rows[k]), regs);
+            if (e < n) s.setmask[rows[k]] = sm;
+            ballots[k] = __ballot_sync(0xffffffffu, sm != 0u);
             if (lane == 0) s_wcnt[k][warp] = __popc(ballots[k]);
         }
         __syncthreads();
@@ -179,6 +181,7 @@ k_active_rects(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
          e += (long long)gridDim.x * blockDim.x) {
         const int k = (int)(e / cams.n), v = (int)(e % cams.n);
         const int i = s.idx[k];
+        if (!((s.setmask[i] >> cams.c[v].set) & 1u)) continue;   // active, but not for this view's change set
         Proj p;
         if (!project_gaussian(__ldg(mean_op + i), __ldg(quat + i), __ldg(log_scale + i), cams.c[v], cams.W, cams.H,
                               cams.TX, cams.TY, p))

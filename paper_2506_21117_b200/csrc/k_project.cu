@@ -463,7 +463,7 @@ k_project_exact(const float4 *__restrict__ mean_op, const float4 *__restrict__ q
             continue;
         }
         const GCam &c = s_cams[v];
-        const int ordi = s.ord[i];
+        const int ordi = view_ordinal(s, i, c.set);
         // ---- colour from SH at the viewing direction (R15), fp32 ----
         float dir[3], Y[16], col[3];
         view_dir(mo, c, dir);

@@ -151,7 +151,8 @@ __device__ __forceinline__ int fill_batch(const Scratch &s, int &cur, int end, i
     }
     if (!BWD) {
         if (tid == 0) *s_clamp = 0;
-        if ((nst & 1) && tid < 3) ent[3 * nst + tid] = make_float4(0.f, 0.f, 0.f, 0.f);   // pad to pairs (o = 0)
+        const int npad = (4 - (nst & 3)) & 3;   // pad to a multiple of 4 entries (opacity 0: never composited)
+        if (tid < 3 * npad) ent[3 * nst + tid] = make_float4(0.f, 0.f, 0.f, 0.f);
         __syncthreads();
         if (cl) *s_clamp = 1;
         fmin = __reduce_min_sync(0xffffffffu, fmin);
@@ -296,11 +297,11 @@ __device__ __forceinline__ void comp_batch(const float4 *ent, int cnt, int lbase
                                            float (&C0)[RT_PX], float (&C1)[RT_PX], float (&C2)[RT_PX],
                                            int (&last)[RT_PX])
 {
-    for (int k = 0; k < cnt; k += 2) {
+    for (int k = 0; k < cnt; k += 4) {   // 4 entries per iteration (the batch is padded to a multiple of 4)
         // warp-level exit once all its pixels terminated (checked every 4 entries)
-        if ((k & 3) == 0 && !__any_sync(0xffffffffu, tmax4(T01, T23) > 0.f)) break;
+        if (!__any_sync(0xffffffffu, tmax4(T01, T23) > 0.f)) break;
 #pragma unroll
-        for (int j = 0; j < 2; j++) {
+        for (int j = 0; j < 4; j++) {
             const float4 A = ent[3 * (k + j)], B = ent[3 * (k + j) + 1], Cc = ent[3 * (k + j) + 2];
             const float sx = __fmaf_rn(-A.y, flx, A.x), txx = __fmaf_rn(-B.x, flx, A.w);
             const int pos = lbase + k + j;
@@ -338,7 +339,7 @@ __global__ void __launch_bounds__(RT_THREADS, 12)
 k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ targets,
       const unsigned char *__restrict__ targets8, bool staged, float *__restrict__ images, float loss_scale, float3 bg)
 {
-    __shared__ float4 ent[3 * (RT_BATCH + 1)];   // staged entries (sa, sb, sc) + one pad
+    __shared__ float4 ent[3 * (RT_BATCH + 3)];   // staged entries (sa, sb, sc) + up to 3 pad entries
     __shared__ float red[RT_THREADS / 32];
     __shared__ int s_item, s_pos[RT_SLOTS], s_wc[2 * RT_SCAN], s_first, s_clamp, s_lastp[CLS_BLOCK_PIX];
     __shared__ unsigned s_rid[RT_SLOTS];

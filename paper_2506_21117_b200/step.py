@@ -145,9 +145,10 @@ class Rows:
                                self.log_scale.data_ptr(), self.sh.data_ptr())
 
 
-def camera_structs(cameras) -> ctypes.Array:
+def camera_structs(cameras, per_set: bool = False) -> ctypes.Array:
     arr = (N.cls_camera * len(cameras))()
     for j, c in enumerate(cameras):
+        arr[j].set = int(getattr(c, "set", 0)) if per_set else 0
         arr[j].fx, arr[j].fy, arr[j].cx, arr[j].cy = float(c.fx), float(c.fy), float(c.cx), float(c.cy)
         arr[j].R[:] = [float(x) for x in np.asarray(c.R, np.float32).reshape(9)]
         arr[j].t[:] = [float(x) for x in np.asarray(c.t, np.float32).reshape(3)]
@@ -155,9 +156,10 @@ def camera_structs(cameras) -> ctypes.Array:
     return arr
 
 
-def region_structs(regions) -> ctypes.Array:
+def region_structs(regions, per_set: bool = False) -> ctypes.Array:
     arr = (N.cls_region * max(len(regions), 1))()
     for j, r in enumerate(regions):
+        arr[j].set = int(getattr(r, "set", 0)) if per_set else 0
         arr[j].kind = int(r.kind)
         arr[j].a[:] = [float(x) for x in np.asarray(r.a, np.float32).reshape(3)]
         arr[j].b[:] = [float(x) for x in np.asarray(r.b, np.float32).reshape(3)]
@@ -193,8 +195,11 @@ class LocalOptimizer:
 
     def __init__(self, params: GaussianParams, regions, limits: Optional[N.cls_limits] = None,
                  lr=(1e-3,) * 6, betas=(0.9, 0.999), eps=1e-15, bg=(0.0, 0.0, 0.0), max_views=None,
-                 width=None, height=None, static_cache: bool = False):
+                 width=None, height=None, static_cache: bool = False, per_set: bool = False):
         self.params = params
+        # NEXT-3 per-change-set activation: regions and views carry their change set (`.set`); a view
+        # activates only its own set's Gaussians.  False: one change set, the union (BASELINE c5)
+        self.per_set = bool(per_set)
         # CLS_FLAG_STATIC_CACHE: the frozen rows' records/units are built once and reused (cls.h)
         self.static_cache = bool(static_cache)
         self.regions = list(regions)
@@ -209,7 +214,7 @@ class LocalOptimizer:
         h = ctypes.c_void_p()
         check(lib.cls_create(ctypes.byref(h), dev, ctypes.byref(limits)))
         self.ctx = h
-        self._reg = region_structs(self.regions)
+        self._reg = region_structs(self.regions, self.per_set)
         self._A = None
         self._fwd_views = 0
 
@@ -228,7 +233,7 @@ class LocalOptimizer:
     def forward(self, cameras, targets: Optional[torch.Tensor] = None, n_views_total: Optional[int] = None,
                 images: bool = False, tile_mask: bool = False, all_tiles: bool = False,
                 stream=None, loss_out: Optional[torch.Tensor] = None) -> ForwardResult:
-        cams = camera_structs(cameras)
+        cams = camera_structs(cameras, self.per_set)
         V = len(cameras)
         W, H = cameras[0].width, cameras[0].height
         dev = self.params.device
@@ -516,7 +521,7 @@ class GraphStep:
                  allreduce: Optional[Callable[[torch.Tensor], None]] = None):
         p = opt.params
         self.opt = opt
-        self.cams = camera_structs(cameras)
+        self.cams = camera_structs(cameras, opt.per_set)
         self.nv = len(cameras)
         self.nvt = int(n_views_total or self.nv)
         self.targets = targets   # device tensor, or pinned host memory (only active tiles' pixels are read)

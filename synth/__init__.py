@@ -41,6 +41,7 @@ class Camera:
     cy: float
     width: int
     height: int
+    set: int = 0           # change set the view belongs to (c5: 5 sets of 8 views; NEXT-3)
 
     @property
     def tiles(self):
@@ -53,6 +54,7 @@ class Region:
     a: np.ndarray          # sphere centre / AABB lo, (3,) float32
     b: np.ndarray          # AABB hi (unused for spheres), (3,) float32
     r: float               # sphere radius (unused for AABBs)
+    set: int = 0           # change set the region belongs to (c5: 5 sets of 1-3 spheres; NEXT-3)
 
 
 @dataclasses.dataclass
@@ -247,9 +249,14 @@ def make_scene(name: str, seed: Optional[int] = None, n: Optional[int] = None,
                 sets.append([Region(REGION_SPHERE, means[i].copy(), np.zeros(3, np.float32), float(r))
                              for i, r in zip(picks, radii)])
             per_set = 8 if n_views is None else max(1, n_views // 5)
-            for s in sets:
+            for si, s in enumerate(sets):
+                for r in s:
+                    r.set = si
                 regions.extend(s)
-                cams.extend(_inside_cameras(rng, per_set, box, [r.a for r in s], W, H, 65.0))
+                cs = _inside_cameras(rng, per_set, box, [r.a for r in s], W, H, 65.0)
+                for c in cs:
+                    c.set = si
+                cams.extend(cs)
             if n_views is not None:
                 cams = cams[:n_views]
     else:  # c4

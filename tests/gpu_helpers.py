@@ -18,7 +18,7 @@ GRAD_ABS_FRAC = 1e-5    # ... or 1e-5 x max|g| of the column (absolute floor)
 
 
 def gpu_run(scene, views=None, dL=None, all_tiles=False, images=True, limits=None, step_adam=False, lr=None,
-            static_cache=False):
+            static_cache=False, per_set=False):
     """Run fwd (+bwd) of the CUDA path. Returns numpy results."""
     import torch
     from paper_2506_21117_b200 import GaussianParams, LocalOptimizer, default_limits
@@ -29,7 +29,8 @@ def gpu_run(scene, views=None, dL=None, all_tiles=False, images=True, limits=Non
     params = GaussianParams.from_scene(scene)
     if limits is None:
         limits = default_limits(scene.n, max(len(cams), 1), W, H)
-    opt = LocalOptimizer(params, scene.regions, limits=limits, lr=lr or (1e-3,) * 6, static_cache=static_cache)
+    opt = LocalOptimizer(params, scene.regions, limits=limits, lr=lr or (1e-3,) * 6, static_cache=static_cache,
+                         per_set=per_set)
     tg = None
     if scene.targets is not None:
         tg = torch.from_numpy(np.ascontiguousarray(scene.targets[views])).cuda()

@@ -473,3 +473,29 @@ def test_multistep_resynchronised_adam(torch_cuda):
     assert np.allclose(p.moment_rows("m", idx).cpu().numpy().reshape(-1, F)[:, valid], m[:, valid], rtol=1e-6, atol=1e-30)
     assert np.allclose(p.moment_rows("v", idx).cpu().numpy().reshape(-1, F)[:, valid], v[:, valid], rtol=1e-5, atol=1e-38)
     opt.close()
+
+
+@pytest.mark.parametrize("cached", [False, True])
+def test_per_change_set_activation(torch_cuda, cached):
+    """NEXT-3: c5's batched update with each view activating only its own change
+    set.  Membership = the union; tile masks, images and gradients against the oracle's per_set mode;
+    fewer active tiles than the union mode (c5 rendered the union mask everywhere)."""
+    sc = synth.make_scene("c5", n=150000, n_views=10)
+    rng = np.random.default_rng(41)
+    up = rng.standard_normal((len(sc.cameras), 3, sc.height, sc.width)).astype(np.float32)
+    fb0 = oracle.forward_backward(sc, with_grad=False, per_set=True)
+    for v, r in enumerate(fb0["renders"]):
+        up[v][:, r["ambiguous"]] = 0.0
+    g = H.gpu_run(sc, dL=up, per_set=True, static_cache=cached)
+    gu = H.gpu_run(sc, per_set=False, static_cache=cached)
+    fb = oracle.forward_backward(sc, dL_dC=up.astype(np.float64), per_set=True)
+    assert np.array_equal(g["idx"], fb["idx"])
+    for v, r in enumerate(fb["renders"]):
+        assert np.array_equal(g["tile_mask"][v], r["tile_mask"]), f"tile mask view {v}"
+        H.assert_images(g["images"][v], r)
+    rg = H.compare_grads(g["grad"], H.oracle_rows(fb, sc.sh_degree))
+    assert rg["n_bad"] == 0, rg
+    assert sum(g["stats"]["n_active_tiles"]) < sum(gu["stats"]["n_active_tiles"])
+    print("active tiles per-set", sum(g["stats"]["n_active_tiles"]), "union", sum(gu["stats"]["n_active_tiles"]))
+    g["opt"].close()
+    gu["opt"].close()

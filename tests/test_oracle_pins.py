@@ -591,3 +591,35 @@ def test_pixel_replay_termination_flip(oracle_lib):
     p = oracle.project(sc, 0)
     best, nw = oracle.pixel_replay(sc, 0, p, 32, 32, np.array([0.99, 0.0, 0.0]))
     assert nw >= 1 and best < 1e-12
+
+
+# ---------------------------------------------------------------------------
+# NEXT-3 per-change-set activation: the oracle's per_set mode
+# ---------------------------------------------------------------------------
+
+def test_per_set_equals_independent_changes(oracle_lib):
+    """"Apply our method in parallel to each change" (L397): with two change sets (one region and one
+    view each), the per-set step's gradient is the SUM of the two single-change steps (each with its
+    own regions and views, the same loss normalisation) and its loss is the sum of their losses; with
+    every set id 0 it is the union step."""
+    import dataclasses
+    sc = synth.make_scene("c5", n=4000, width=96, height=64, n_views=10)
+    sets = sorted({c.set for c in sc.cameras})
+    assert len(sets) >= 2 and len({r.set for r in sc.regions}) >= 2
+    V = len(sc.cameras)
+    per = oracle.forward_backward(sc, per_set=True)
+    tot = np.zeros_like(per["grad"])
+    loss = 0.0
+    for s in sets:
+        views = [v for v in range(V) if sc.cameras[v].set == s]
+        sub = dataclasses.replace(sc, regions=[r for r in sc.regions if r.set == s])
+        fb = oracle.forward_backward(sub, views=views, n_views_total=V)
+        tot += fb["grad"]
+        loss += fb["loss"]
+    assert np.allclose(per["grad"], tot, rtol=1e-12, atol=1e-300)
+    assert per["loss"] == pytest.approx(loss, rel=1e-12)
+    assert np.array_equal(per["idx"], oracle.forward_backward(sc, with_grad=False)["idx"])   # O^t = the union
+    flat = dataclasses.replace(sc, cameras=[dataclasses.replace(c, set=0) for c in sc.cameras],
+                               regions=[dataclasses.replace(r, set=0) for r in sc.regions])
+    a, b = oracle.forward_backward(flat, per_set=True), oracle.forward_backward(sc)
+    assert np.array_equal(a["grad"], b["grad"]) and a["loss"] == b["loss"]
