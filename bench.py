@@ -548,6 +548,78 @@ def run_reference(args):
             "e2e": {"value": round(value, 6), "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+def run_loop(args):
+    """BASELINE config 5's batched multi-timestep update as the method runs it: `--steps` local-
+    optimisation steps (CUDA-graph replays of the cached step) with sphere pruning of O^t every
+    `--prune-every` steps (the scene partitioned into its static prefix first); a prune changes
+    the row count, so the step is re-captured after it.  Timed end to end on the device (prunes and
+    re-captures included).  --per-set: NEXT-3 per-change-set activation instead of the union."""
+    import torch
+
+    from paper_2506_21117_b200 import GaussianParams, GraphStep, LocalOptimizer
+    torch.cuda.set_device(0)
+    sc, u8 = bench_scene(args)
+    V = len(sc.cameras)
+    cams = sc.cameras
+    params = GaussianParams.from_scene(sc, device="cuda:0")
+    lim = limits_for(args.config, sc.n, V, sc.width, sc.height, False)
+    opt = LocalOptimizer(params, sc.regions, limits=lim, static_cache=True, per_set=args.per_set)
+    opt.spatial_order()
+    n_static = opt.partition_static()
+    tg = torch.from_numpy(np.ascontiguousarray(u8 if u8 is not None else sc.targets)).cuda()
+    for _ in range(args.warmup):            # warm-up steps (the first builds the static cache)
+        opt.step(cams, tg)
+    torch.cuda.synchronize()
+    n0 = params.n
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    prunes, removed, captures = 0, 0, 0
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        gs = None
+        for k in range(args.steps):
+            if k > 0 and k % args.prune_every == 0:
+                removed += opt.prune_outside()     # O^t rows whose centre left the spheres (P:509)
+                prunes += 1
+                gs = None                          # n changed: the captured step is stale
+            if gs is None:
+                gs = GraphStep(opt, cams, tg)
+                captures += 1
+            loss = gs.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    stats = opt.stats()
+    # per-kernel breakdown: K eager steps right after (same workload)
+    opt.profile(True)
+    opt.profile_read()
+    for _ in range(min(args.steps, 20)):
+        opt.step(cams, tg)
+    torch.cuda.synchronize()
+    prof = opt.profile_read()
+    opt.profile(False)
+    kk = min(args.steps, 20)
+    out = {"metric": "local-opt steps/s (fwd+bwd+masked Adam), 100-step batched loop with sphere pruning",
+           "value": round(1000.0 * args.steps / ms, 3), "unit": "steps/s", "n_gpus": 1, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+           "impl": "ours", "dtype": "f32", "data": "synthetic",
+           "config": {"workload": args.config, "gaussians": sc.n, "views": V, "width": sc.width,
+                      "height": sc.height, "activation": "per change set (NEXT-3)" if args.per_set else "union",
+                      "prune_every": args.prune_every, "n_static": int(n_static), "rows_at_start": int(n0),
+                      "rows_at_end": int(params.n)},
+           "loop": {"prunes": prunes, "rows_removed": int(removed), "graph_captures": captures,
+                    "timed": "device events around the whole loop (prunes and re-captures included)"},
+           "active": int(stats["n_active"]), "active_tiles": int(sum(stats["n_active_tiles"])),
+           "static_cache": {"builds": int(stats["cache_builds"]), "mask_rebuilds": int(stats["cache_mask_builds"]),
+                            "records": int(stats["cache_records"]),
+                            "note": "a prune changes the rows (full rebuild); the others follow the active mask"},
+           "kernels_ms_per_step": {k: round(v["ms"] / kk, 4) for k, v in prof.items() if v["calls"]},
+           "clocks": clk.summary()}
+    opt.close()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -570,10 +642,16 @@ def main():
     ap.add_argument("--no-static-cache", dest="static_cache", action="store_false")
     ap.add_argument("--eager", action="store_true",
                     help="launch every kernel per step instead of replaying the step as one CUDA graph (N = 1)")
+    ap.add_argument("--loop", action="store_true", help="the multi-step loop with pruning (BASELINE config 5)")
+    ap.add_argument("--prune-every", type=int, default=15)
+    ap.add_argument("--per-set", action="store_true", help="NEXT-3 per-change-set activation (with --loop)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
-    out = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if args.loop and args.impl == "ours":
+        out = run_loop(args)
+    else:
+        out = run_reference(args) if args.impl == "reference" else run_ours(args)
     if out is not None:
         print(json.dumps(out), flush=True)
 

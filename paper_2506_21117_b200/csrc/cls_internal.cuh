@@ -98,6 +98,7 @@ struct CacheState {
     int scan_ticket;
     int n_mitems;       // work items of the frozen merge (chunks of one row segment)
     int n_dyn_extra;    // rows of S0 that are not active this step (appended to the step's row list)
+    int dil;            // current dilation in tiles (grows by 2, up to 12, at every rebuild for the mask)
     int n_dcand;        // the step's staged (row, view) record candidates
     unsigned long long A0_total;   // scan total of the S0 compaction
 };

@@ -47,6 +47,10 @@ __global__ void k_cache_decide(CacheBufs cb, int n, cudaGraphConditionalHandle c
     c.skip_full = mode != 2;
     c.skip_build = mode == 0;
     c.n = n;
+    // the dilation adapts: a rebuild because the mask escaped means the active rects move faster than
+    // the margin, so the next build gets 2 more tiles (up to 12)
+    if (c.dil < cb.dilate) c.dil = cb.dilate;
+    if (mode == 1) c.dil = min(c.dil + 2, 12);
     if (mode) {
         int *w = reinterpret_cast<int *>(cb.ccnt);
         for (int k = 0; k < (int)(sizeof(Counters) / sizeof(int)); k++) w[k] = 0;
@@ -95,7 +99,7 @@ __global__ void __launch_bounds__(256) k_dilated_rects(const float4 *__restrict_
     const int P = cams.TX + 1;
     const int A = s.cnt->A;
     const long long total = (long long)A * cams.n;
-    const int k = cb.dilate;
+    const int k = cb.st->dil;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x) {
         const int a = (int)(e / cams.n), v = (int)(e % cams.n);
