@@ -33,6 +33,7 @@ __device__ __forceinline__ void adam_lane(float &p, float &m, float &v, float g,
 
 __global__ void __launch_bounds__(256) k_adam(const __grid_constant__ AdamArgs a, Scratch s)
 {
+    CLS_PDL_WAIT();
     if (s.cnt->overflow) return;   // capacity overflow: the gradient rows are not valid, nothing is updated
     const int A = s.cnt->A;
     float bc1 = a.bc1, bc2 = a.bc2;
@@ -83,6 +84,7 @@ __global__ void __launch_bounds__(256) k_adam(const __grid_constant__ AdamArgs a
 
 __global__ void k_step_inc(Scratch s, int *step_dev)
 {
+    CLS_PDL_WAIT();
     if (!s.cnt->overflow) *step_dev += 1;   // a skipped update does not advance t
 }
 
@@ -99,10 +101,10 @@ void launch_adam(const StepDims &d, const Scratch &s, float4 *mean_op, float4 *q
     a.n = d.n; a.K4 = d.K4; a.ROW4 = 3 + d.K4; a.n_sh_floats = 3 * (d.D + 1) * (d.D + 1);
     const long long upper = (long long)d.n * a.ROW4;
     const int blocks = (int)std::min<long long>((upper + 255) / 256, 148LL * 16);
-    k_adam<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(a, s);
+    cls_launch(k_adam, blocks > 0 ? blocks : 1, 256, 0, st, a, s);
     g_launches++;
     if (step_dev) {   // the next replay uses the next step
-        k_step_inc<<<1, 1, 0, st>>>(s, step_dev);
+        cls_launch(k_step_inc, 1, 1, 0, st, s, step_dev);
         g_launches++;
     }
 }

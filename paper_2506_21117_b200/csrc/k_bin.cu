@@ -25,6 +25,7 @@ namespace cls {
 
 __global__ void __launch_bounds__(TSCAN_THREADS) k_tiles_scan(int total, Scratch s)
 {
+    CLS_PDL_WAIT();
     __shared__ int s_tile;
     __shared__ unsigned s_warp[TSCAN_THREADS / 32];
     __shared__ unsigned s_prefix;
@@ -90,6 +91,7 @@ __global__ void __launch_bounds__(TSCAN_THREADS) k_tiles_scan(int total, Scratch
 #define SHORT_RUN 32
 __global__ void __launch_bounds__(256) k_permute(Scratch s)
 {
+    CLS_PDL_WAIT();
     const int n = s.cnt->overflow ? 0 : min(s.cnt->n_records, (int)s.max_records);
     const unsigned long long *key = s.rskey;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -133,6 +135,7 @@ __global__ void __launch_bounds__(256) k_permute(Scratch s)
 // unit keys are written later)
 __global__ void __launch_bounds__(256) k_long_runs(Scratch s, unsigned long long *bufa, unsigned long long *bufb)
 {
+    CLS_PDL_WAIT();
     __shared__ int s_end;
     if (s.cnt->overflow) return;   // (also a skipped static-cache build, whose run count is stale)
     const int n = min(s.cnt->n_records, (int)s.max_records);
@@ -201,6 +204,7 @@ __global__ void __launch_bounds__(256) k_long_runs(Scratch s, unsigned long long
 #define KU_WARPS (KU_THREADS / 32)
 __global__ void __launch_bounds__(KU_THREADS) k_units(const __grid_constant__ CamSet cams, Scratch s)
 {
+    CLS_PDL_WAIT();
     __shared__ float sf[KU_WARPS][9][32];      // u, v, ia, b, det, aQ, ey, dyr, mx
     __shared__ unsigned si[KU_WARPS][4][32];   // x0 | x1 << 16, y0 | view << 16, record id, unit offset
     __shared__ unsigned char sown[KU_WARPS][32];   // per unit of a chunk that starts a record: its lane
@@ -303,6 +307,7 @@ __global__ void __launch_bounds__(KU_THREADS) k_units(const __grid_constant__ Ca
 // row-segment ranges of the sorted units (dead units excluded)
 __global__ void __launch_bounds__(256) k_seg_ranges(Scratch s, int n_seg)
 {
+    CLS_PDL_WAIT();
     const int n = s.cnt->overflow ? 0 : s.cnt->n_units32;
     const unsigned long long *k = s.sukey;
     constexpr unsigned NONE = 0xffffffffu;   // the segment "before 0" and "after n - 1"
@@ -344,7 +349,7 @@ void launch_bin_items(const StepDims &d, Scratch &s, cudaStream_t st)
     const int VT = d.V * d.T;
     const int blocks = (VT + TSCAN_TILE - 1) / TSCAN_TILE;
     cudaMemsetAsync(s.st_tiles, 0, sizeof(unsigned long long) * blocks, st);
-    k_tiles_scan<<<blocks, TSCAN_THREADS, 0, st>>>(VT, s);
+    cls_launch(k_tiles_scan, blocks, TSCAN_THREADS, 0, st, VT, s);
     g_launches++;
 }
 
@@ -360,6 +365,7 @@ void launch_bin_items(const StepDims &d, Scratch &s, cudaStream_t st)
 __global__ void __launch_bounds__(256) k_gather_targets(const __grid_constant__ CamSet cams, Scratch s,
                                                         const float *__restrict__ host_targets)
 {
+    CLS_PDL_WAIT();
     const int n_items = s.cnt->overflow ? 0 : s.cnt->n_items;
     const int W = cams.W, H = cams.H, TX = cams.TX, T = cams.T;
     const size_t HW = (size_t)H * W;
@@ -411,7 +417,7 @@ void launch_gather_targets(const StepDims &d, const CamSet &cams, const Scratch 
 {
     // a small grid: 32 x 256 threads x GT_U 16 B reads keep ~1 MB in flight, far above the link's
     // bandwidth-delay product (~0.1 MB), while leaving the SMs to the concurrent projection/binning
-    k_gather_targets<<<32, 256, 0, st>>>(cams, s, host_targets);
+    cls_launch(k_gather_targets, 32, 256, 0, st, cams, s, host_targets);
     g_launches++;
 }
 
@@ -421,6 +427,7 @@ void launch_gather_targets(const StepDims &d, const CamSet &cams, const Scratch 
 __global__ void __launch_bounds__(256) k_gather_targets_u8(const __grid_constant__ CamSet cams, Scratch s,
                                                            const unsigned char *__restrict__ targets)
 {
+    CLS_PDL_WAIT();
     __shared__ float lut[256];   // k -> k / 255 (IEEE division, round to nearest)
     lut[threadIdx.x] = __fdiv_rn((float)threadIdx.x, 255.0f);
     __syncthreads();
@@ -465,7 +472,7 @@ void launch_gather_targets_u8(const StepDims &d, const CamSet &cams, const Scrat
 {
     // 32 CTAs (measured on c4 end to end: 16 -> 329, 32 -> 351, 64 -> 334, 128 -> 303 steps/s): enough
     // reads in flight for the link, few enough to leave the concurrent projection/binning its SMs
-    k_gather_targets_u8<<<32, 256, 0, st>>>(cams, s, targets);
+    cls_launch(k_gather_targets_u8, 32, 256, 0, st, cams, s, targets);
     g_launches++;
 }
 
@@ -485,8 +492,8 @@ void launch_bin_recsort(const StepDims &d, const CamSet &cams, Scratch &s, cudaS
 void launch_bin_count(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st)
 {
     const int R = (int)s.max_records;
-    k_permute<<<148 * 8, 256, 0, st>>>(s);
-    k_long_runs<<<148, 256, 0, st>>>(s, s.ukey, s.ukey_alt);   // exits at once without long runs
+    cls_launch(k_permute, 148 * 8, 256, 0, st, s);
+    cls_launch(k_long_runs, 148, 256, 0, st, s, s.ukey, s.ukey_alt);   // exits at once without long runs
     scan_excl_u32(s.rcnt, s.roff, &s.cnt->n_records, R, s.st_scan, &s.cnt->scan_ticket, &s.cnt->n_units,
                   &s.cnt->overflow, st);
     g_launches += 2;
@@ -495,7 +502,7 @@ void launch_bin_count(const StepDims &d, const CamSet &cams, Scratch &s, cudaStr
 // 3. per unit: footprint columns and segment key
 void launch_bin_emit(const StepDims &d, const CamSet &cams, Scratch &s, cudaStream_t st)
 {
-    k_units<<<148 * 4, KU_THREADS, 0, st>>>(cams, s);   // persistent: 4 CTAs per SM (64 registers)
+    cls_launch(k_units, 148 * 4, KU_THREADS, 0, st, cams, s);   // persistent: 4 CTAs per SM (64 registers)
     g_launches += 1;
 }
 
@@ -521,7 +528,7 @@ void launch_bin_pairsort(const StepDims &d, const CamSet &cams, Scratch &s, cuda
     s.sukey = w ? s.ukey_alt : s.ukey;
     cudaMemsetAsync(s.seg_off, 0, sizeof(int) * (size_t)n_seg, st);
     cudaMemsetAsync(s.seg_end, 0, sizeof(int) * (size_t)n_seg, st);
-    k_seg_ranges<<<148 * 8, 256, 0, st>>>(s, n_seg);
+    cls_launch(k_seg_ranges, 148 * 8, 256, 0, st, s, n_seg);
     g_launches += 1;
 }
 

@@ -217,6 +217,7 @@ k_bwd_project(const float4 *__restrict__ mean_op, const float4 *__restrict__ qua
               const float4 *__restrict__ log_scale, const float4 *__restrict__ sh, int n,
               const __grid_constant__ CamSet cams, Scratch s, float4 *__restrict__ out)
 {
+    CLS_PDL_WAIT();
     if (s.cnt->overflow) return;   // capacity overflow (records, pairs, A > max_active): no rows are valid
     const int A = s.cnt->A;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < A; k += gridDim.x * blockDim.x)
@@ -230,10 +231,10 @@ void launch_bwd_project(const Params &g, const StepDims &d, const CamSet &cams, 
     const int blocks = std::max(1, std::min((d.n + 127) / 128, 148 * 4));   // grid-stride over the A rows
     float4 *out = reinterpret_cast<float4 *>(grad_active);
     switch (d.D) {
-    case 0: k_bwd_project<0><<<blocks, 128, 0, st>>>(g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s, out); break;
-    case 1: k_bwd_project<1><<<blocks, 128, 0, st>>>(g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s, out); break;
-    case 2: k_bwd_project<2><<<blocks, 128, 0, st>>>(g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s, out); break;
-    default: k_bwd_project<3><<<blocks, 128, 0, st>>>(g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s, out); break;
+    case 0: cls_launch(k_bwd_project<0>, blocks, 128, 0, st, g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s, out); break;
+    case 1: cls_launch(k_bwd_project<1>, blocks, 128, 0, st, g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s, out); break;
+    case 2: cls_launch(k_bwd_project<2>, blocks, 128, 0, st, g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s, out); break;
+    default: cls_launch(k_bwd_project<3>, blocks, 128, 0, st, g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s, out); break;
     }
     g_launches++;
 }

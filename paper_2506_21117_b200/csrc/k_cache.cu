@@ -25,6 +25,7 @@ namespace cls {
 // ---- checks and decision ----
 __global__ void __launch_bounds__(256) k_cache_check(CacheBufs cb, Scratch s, int VT)
 {
+    CLS_PDL_WAIT();
     const int A = s.cnt->A;
     const int valid = cb.st->valid;
     const int total = max(VT, A);
@@ -39,6 +40,7 @@ __global__ void __launch_bounds__(256) k_cache_check(CacheBufs cb, Scratch s, in
 
 __global__ void k_cache_decide(CacheBufs cb, int n, cudaGraphConditionalHandle cond, int use_cond)
 {
+    CLS_PDL_WAIT();
     CacheState &c = *cb.st;
     const int mode = !c.valid ? 2 : ((c.need & 2) ? 2 : ((c.need & 1) ? 1 : 0));
     // in a CUDA graph the build is the body of a conditional node: skipped whole on warm steps
@@ -65,6 +67,7 @@ __global__ void k_cache_decide(CacheBufs cb, int n, cudaGraphConditionalHandle c
 // ---- S0 := (S0 if valid) u O^t, stable compaction ----
 __global__ void __launch_bounds__(256) k_s0_flags(CacheBufs cb, Scratch s, int n)
 {
+    CLS_PDL_WAIT();
     if (cb.st->mode != 2) return;
     const int valid = cb.st->valid;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
@@ -73,6 +76,7 @@ __global__ void __launch_bounds__(256) k_s0_flags(CacheBufs cb, Scratch s, int n
 
 __global__ void __launch_bounds__(256) k_s0_scatter(CacheBufs cb, int n)
 {
+    CLS_PDL_WAIT();
     if (cb.st->mode != 2) return;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const bool f = cb.flag[i] != 0u;
@@ -86,6 +90,7 @@ __global__ void __launch_bounds__(256) k_s0_scatter(CacheBufs cb, int n)
 // ---- dilated mask: the active rects grown by `dilate` tiles, into the dilated corner differences ----
 __global__ void __launch_bounds__(256) k_dzero(CacheBufs cb, int nd)
 {
+    CLS_PDL_WAIT();
     if (cb.st->skip_build) return;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nd; k += gridDim.x * blockDim.x) cb.dmdiff[k] = 0;
 }
@@ -95,6 +100,7 @@ __global__ void __launch_bounds__(256) k_dilated_rects(const float4 *__restrict_
                                                        const float4 *__restrict__ log_scale,
                                                        const __grid_constant__ CamSet cams, CacheBufs cb, Scratch s)
 {
+    CLS_PDL_WAIT();
     if (cb.st->skip_build) return;
     const int P = cams.TX + 1;
     const int A = s.cnt->A;
@@ -122,6 +128,7 @@ __global__ void __launch_bounds__(256) k_dilated_rects(const float4 *__restrict_
 // ---- frozen records in (view, depth, index) order: record id = rank ----
 __global__ void __launch_bounds__(256) k_cache_reorder(CacheBufs cb, Scratch sb)
 {
+    CLS_PDL_WAIT();
     if (sb.cnt->overflow) return;
     const int F = min(sb.cnt->n_records, (int)sb.max_records);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < F; i += gridDim.x * blockDim.x) {
@@ -147,6 +154,7 @@ __device__ __forceinline__ int seg_lower_bound(const unsigned long long *k, int 
 // lower bound of every row segment in the sorted frozen units (n_seg + 1 entries; the last = live units)
 __global__ void __launch_bounds__(256) k_cache_seglb(CacheBufs cb, const unsigned long long *fsorted, int n_seg)
 {
+    CLS_PDL_WAIT();
     if (cb.ccnt->overflow) return;
     const int n = cb.ccnt->n_units32;
     for (int sg = blockIdx.x * blockDim.x + threadIdx.x; sg <= n_seg; sg += gridDim.x * blockDim.x)
@@ -155,6 +163,7 @@ __global__ void __launch_bounds__(256) k_cache_seglb(CacheBufs cb, const unsigne
 
 __global__ void k_cache_finalize(CacheBufs cb, Scratch s, int n_seg)
 {
+    CLS_PDL_WAIT();
     CacheState &c = *cb.st;
     if (c.mode) {
         c.ovf = cb.ccnt->overflow;
@@ -169,6 +178,7 @@ __global__ void k_cache_finalize(CacheBufs cb, Scratch s, int n_seg)
 // ---- per step: dynamic records' ranks among the frozen ones, and the merge ----
 __global__ void __launch_bounds__(256) k_dyn_pos(CacheBufs cb, Scratch sd)
 {
+    CLS_PDL_WAIT();
     if (sd.cnt->overflow) return;
     const int D = min(sd.cnt->n_records, (int)sd.max_records);
     const int F = cb.st->F;
@@ -190,6 +200,7 @@ __global__ void __launch_bounds__(256) k_dyn_pos(CacheBufs cb, Scratch sd)
 // the rank position of each live dynamic unit's record, in unit order (the merge's search keys)
 __global__ void __launch_bounds__(256) k_dyn_q(CacheBufs cb, Scratch s, const unsigned long long *dsorted)
 {
+    CLS_PDL_WAIT();
     if (s.cnt->overflow) return;
     const int n = min(s.cnt->n_units32, (int)cb.Dunits);
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
@@ -222,6 +233,7 @@ __device__ __forceinline__ int seg_lower_bound_warp(const unsigned long long *k,
 __global__ void __launch_bounds__(256) k_merge_bounds(CacheBufs cb, Scratch s, const unsigned long long *dsorted,
                                                       int n_seg)
 {
+    CLS_PDL_WAIT();
     if (s.cnt->overflow) return;
     const int n = s.cnt->n_units32;
     const int lane = threadIdx.x & 31;
@@ -245,6 +257,7 @@ __global__ void __launch_bounds__(256) k_merge_bounds(CacheBufs cb, Scratch s, c
 #define MG_CHUNK 4096
 __global__ void __launch_bounds__(1024) k_cache_items(CacheBufs cb, int n_seg)
 {
+    CLS_PDL_WAIT();
     if (cb.ccnt->overflow) return;
     __shared__ int s_carry;
     if (threadIdx.x == 0) s_carry = 0;
@@ -288,6 +301,7 @@ __global__ void __launch_bounds__(MG_THREADS) k_merge_frozen(CacheBufs cb, Scrat
                                                              const unsigned long long *dsorted,
                                                              unsigned long long *merged, int n_seg, int W32)
 {
+    CLS_PDL_WAIT();
     __shared__ unsigned qd[MG_SMEM];
     __shared__ int s_act;
     if (s.cnt->overflow) return;
@@ -345,6 +359,7 @@ __global__ void __launch_bounds__(256) k_merge_dyn(CacheBufs cb, Scratch s, cons
                                                    const unsigned long long *dsorted, unsigned long long *merged,
                                                    int n_seg, int W32)
 {
+    CLS_PDL_WAIT();
     if (s.cnt->overflow) return;
     if ((long long)cb.cseg_lb[n_seg] + cb.db[n_seg] > s.max_units) return;
     const int Ud = cb.db[n_seg];
@@ -377,6 +392,7 @@ __global__ void __launch_bounds__(256) k_merge_dyn(CacheBufs cb, Scratch s, cons
 // ---------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_dyn_list(CacheBufs cb, Scratch s)
 {
+    CLS_PDL_WAIT();
     const int A = s.cnt->A;
     const int A0 = cb.st->valid ? cb.st->A0 : 0;
     const int total = max(A, A0);
@@ -402,6 +418,7 @@ __global__ void __launch_bounds__(256) k_dyn_list(CacheBufs cb, Scratch s)
 __global__ void __launch_bounds__(256) k_dyn_rows(CacheBufs cb, Scratch s, const float4 *__restrict__ mean_op,
                                                   const float4 *__restrict__ quat, const float4 *__restrict__ log_scale)
 {
+    CLS_PDL_WAIT();
     const int n = s.cnt->A + cb.st->n_dyn_extra;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         const int i = cb.dlist[k];
@@ -421,6 +438,7 @@ __global__ void __launch_bounds__(256, 3) k_dyn_project(CacheBufs cb, Scratch s,
                                                         const float4 *__restrict__ sh, int n,
                                                         const __grid_constant__ CamSet cams)
 {
+    CLS_PDL_WAIT();
     __shared__ GCam s_cams[CLS_MAX_VIEWS];
     __shared__ double2 s_lims[CLS_MAX_VIEWS];
     for (int k = threadIdx.x; k < cams.n * (int)(sizeof(GCam) / 4); k += blockDim.x)
@@ -508,6 +526,7 @@ __global__ void __launch_bounds__(256, 3) k_dyn_project(CacheBufs cb, Scratch s,
 
 __global__ void __launch_bounds__(256) k_dyn_emit(CacheBufs cb, Scratch s, int TX, int TY)
 {
+    CLS_PDL_WAIT();
     if (s.cnt->overflow) return;
     const int nc = min(cb.st->n_dcand, (int)cb.Dcap);
     const int lane = threadIdx.x & 31, P = TX + 1;
@@ -551,14 +570,14 @@ void launch_dyn_mask(const Params &g, const StepDims &d, const CamSet &cams, con
     cudaMemsetAsync(&cb.st->n_dyn_extra, 0, sizeof(int), st);
     cudaMemsetAsync(&cb.st->n_dcand, 0, sizeof(int), st);
     cudaMemsetAsync(s.mdiff, 0, sizeof(int) * (size_t)d.V * (d.TY + 1) * (d.TX + 1), st);
-    k_dyn_list<<<148 * 2, 256, 0, st>>>(cb, s);
-    k_dyn_rows<<<148 * 2, 256, 0, st>>>(cb, s, g.mean_op, g.quat, g.log_scale);
+    cls_launch(k_dyn_list, 148 * 2, 256, 0, st, cb, s);
+    cls_launch(k_dyn_rows, 148 * 2, 256, 0, st, cb, s, g.mean_op, g.quat, g.log_scale);
     const int grid = 148 * 3;
     switch (d.D) {
-    case 0: k_dyn_project<0><<<grid, 256, 0, st>>>(cb, s, g.mean_op, g.sh, d.n, cams); break;
-    case 1: k_dyn_project<1><<<grid, 256, 0, st>>>(cb, s, g.mean_op, g.sh, d.n, cams); break;
-    case 2: k_dyn_project<2><<<grid, 256, 0, st>>>(cb, s, g.mean_op, g.sh, d.n, cams); break;
-    default: k_dyn_project<3><<<grid, 256, 0, st>>>(cb, s, g.mean_op, g.sh, d.n, cams); break;
+    case 0: cls_launch(k_dyn_project<0>, grid, 256, 0, st, cb, s, g.mean_op, g.sh, d.n, cams); break;
+    case 1: cls_launch(k_dyn_project<1>, grid, 256, 0, st, cb, s, g.mean_op, g.sh, d.n, cams); break;
+    case 2: cls_launch(k_dyn_project<2>, grid, 256, 0, st, cb, s, g.mean_op, g.sh, d.n, cams); break;
+    default: cls_launch(k_dyn_project<3>, grid, 256, 0, st, cb, s, g.mean_op, g.sh, d.n, cams); break;
     }
     g_launches += 3;
     launch_sat_only(d, cams, s, nullptr, st);
@@ -566,7 +585,7 @@ void launch_dyn_mask(const Params &g, const StepDims &d, const CamSet &cams, con
 
 void launch_dyn_emit(const StepDims &d, const CacheBufs &cb, const Scratch &sd, cudaStream_t st)
 {
-    k_dyn_emit<<<148 * 4, 256, 0, st>>>(cb, sd, d.TX, d.TY);
+    cls_launch(k_dyn_emit, 148 * 4, 256, 0, st, cb, sd, d.TX, d.TY);
     g_launches++;
 }
 
@@ -577,8 +596,8 @@ void launch_cache_check(const CacheBufs &cb, const StepDims &d, const Scratch &s
                         cudaGraphConditionalHandle cond, int use_cond)
 {
     cudaMemsetAsync(&cb.st->need, 0, sizeof(int), st);
-    k_cache_check<<<148 * 2, 256, 0, st>>>(cb, s, d.V * d.T);
-    k_cache_decide<<<1, 1, 0, st>>>(cb, d.n, cond, use_cond);
+    cls_launch(k_cache_check, 148 * 2, 256, 0, st, cb, s, d.V * d.T);
+    cls_launch(k_cache_decide, 1, 1, 0, st, cb, d.n, cond, use_cond);
     g_launches += 2;
 }
 
@@ -586,13 +605,13 @@ void launch_cache_build(const Params &g, const StepDims &d, const CamSet &cams, 
                         const Scratch &s, Scratch &sb, unsigned long long **fsorted, cudaStream_t st)
 {
     // S0 := (S0 if valid) u O^t
-    k_s0_flags<<<148 * 4, 256, 0, st>>>(cb, s, d.n);
+    cls_launch(k_s0_flags, 148 * 4, 256, 0, st, cb, s, d.n);
     scan_excl_u32(cb.flag, cb.excl, &cb.st->n, (int)cb.maxN, cb.scan_status, &cb.st->scan_ticket, &cb.st->A0_total,
                   &cb.st->skip_full, st);
-    k_s0_scatter<<<148 * 4, 256, 0, st>>>(cb, d.n);
+    cls_launch(k_s0_scatter, 148 * 4, 256, 0, st, cb, d.n);
     // dilated mask of the current active set and its tables
-    k_dzero<<<148, 256, 0, st>>>(cb, d.V * (d.TY + 1) * (d.TX + 1));
-    k_dilated_rects<<<148 * 3, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, cams, cb, s);
+    cls_launch(k_dzero, 148, 256, 0, st, cb, d.V * (d.TY + 1) * (d.TX + 1));
+    cls_launch(k_dilated_rects, 148 * 3, 256, 0, st, g.mean_op, g.quat, g.log_scale, cams, cb, s);
     g_launches += 4;
     launch_sat_only(d, cams, sb, &cb.st->skip_build, st);
     // frozen records: every row outside S0 against the dilated mask
@@ -600,15 +619,15 @@ void launch_cache_build(const Params &g, const StepDims &d, const CamSet &cams, 
     launch_project_exact(g, d, cams, sb, st);
     launch_bin_recsort(d, cams, sb, st);
     launch_bin_count(d, cams, sb, st);
-    k_cache_reorder<<<148 * 8, 256, 0, st>>>(cb, sb);
+    cls_launch(k_cache_reorder, 148 * 8, 256, 0, st, cb, sb);
     g_launches++;
     Scratch su = sb;
     su.rec = cb.urec;   // units read the reordered records (id = rank)
     launch_bin_emit(d, cams, su, st);
     const int n_seg = d.V * d.TY;
     *fsorted = launch_unit_sort(d, su, st);
-    k_cache_seglb<<<(n_seg + 256) / 256, 256, 0, st>>>(cb, *fsorted, n_seg);
-    k_cache_items<<<1, 1024, 0, st>>>(cb, n_seg);
+    cls_launch(k_cache_seglb, (n_seg + 256) / 256, 256, 0, st, cb, *fsorted, n_seg);
+    cls_launch(k_cache_items, 1, 1024, 0, st, cb, n_seg);
     g_launches += 2;
 }
 
@@ -616,7 +635,7 @@ void launch_cache_build(const Params &g, const StepDims &d, const CamSet &cams, 
 // standing build overflow into the step's counters
 void launch_cache_finalize(const StepDims &d, const CacheBufs &cb, const Scratch &s, cudaStream_t st)
 {
-    k_cache_finalize<<<1, 1, 0, st>>>(cb, s, d.V * d.TY);
+    cls_launch(k_cache_finalize, 1, 1, 0, st, cb, s, d.V * d.TY);
     g_launches++;
 }
 
@@ -625,11 +644,11 @@ void launch_cache_merge(const StepDims &d, const CacheBufs &cb, const Scratch &s
 {
     const int n_seg = d.V * d.TY;
     const int W32 = (d.TX + 31) / 32;
-    k_dyn_pos<<<148 * 4, 256, 0, st>>>(cb, sd);
-    k_dyn_q<<<148 * 4, 256, 0, st>>>(cb, sd, dsorted);
-    k_merge_bounds<<<(n_seg + 1 + 7) / 8, 256, 0, st>>>(cb, sd, dsorted, n_seg);
-    k_merge_frozen<<<148 * 8, MG_THREADS, 0, st>>>(cb, sd, fsorted, dsorted, merged, n_seg, W32);
-    k_merge_dyn<<<148 * 4, 256, 0, st>>>(cb, sd, fsorted, dsorted, merged, n_seg, W32);
+    cls_launch(k_dyn_pos, 148 * 4, 256, 0, st, cb, sd);
+    cls_launch(k_dyn_q, 148 * 4, 256, 0, st, cb, sd, dsorted);
+    cls_launch(k_merge_bounds, (n_seg + 1 + 7) / 8, 256, 0, st, cb, sd, dsorted, n_seg);
+    cls_launch(k_merge_frozen, 148 * 8, MG_THREADS, 0, st, cb, sd, fsorted, dsorted, merged, n_seg, W32);
+    cls_launch(k_merge_dyn, 148 * 4, 256, 0, st, cb, sd, fsorted, dsorted, merged, n_seg, W32);
     g_launches += 5;
 }
 

@@ -42,6 +42,7 @@ __device__ __forceinline__ void copy_row(const RowArrays &src, long long i, cons
 __global__ void k_part_flags(const float4 *__restrict__ mean_op, int n, const __grid_constant__ RegSet regs,
                              unsigned *flag_static)
 {
+    CLS_PDL_WAIT();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
         flag_static[i] = in_regions(mean_op[i], regs) ? 0u : 1u;
 }
@@ -49,6 +50,7 @@ __global__ void k_part_flags(const float4 *__restrict__ mean_op, int n, const __
 __global__ void k_part_scatter(RowArrays src, RowArrays dst, int n, const unsigned *__restrict__ flag_static,
                                const unsigned *__restrict__ excl, const unsigned long long *n_static_p)
 {
+    CLS_PDL_WAIT();
     const long long ns = (long long)*n_static_p;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const long long j = flag_static[i] ? (long long)excl[i] : ns + (long long)(i - (long long)excl[i]);
@@ -61,6 +63,7 @@ __global__ void k_part_scatter(RowArrays src, RowArrays dst, int n, const unsign
 __global__ void k_prune_kind(RowArrays a, long long n_static, int S, const __grid_constant__ RegSet regs,
                              unsigned *kind, unsigned *keep, unsigned *clone, unsigned *split)
 {
+    CLS_PDL_WAIT();
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < S; r += gridDim.x * blockDim.x) {
         const bool in = in_regions(a.mo[n_static + r], regs);
         kind[r] = in ? 0u : 3u;
@@ -73,6 +76,7 @@ __global__ void k_prune_kind(RowArrays a, long long n_static, int S, const __gri
 __global__ void k_densify_kind(RowArrays a, long long n_static, int S, float grad_thr, float log_scale_thr,
                                unsigned *kind, unsigned *keep, unsigned *clone, unsigned *split)
 {
+    CLS_PDL_WAIT();
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < S; r += gridDim.x * blockDim.x) {
         const long long i = n_static + r;
         const int c = a.cnt[i];
@@ -90,6 +94,7 @@ __global__ void k_densify_kind(RowArrays a, long long n_static, int S, float gra
 
 __global__ void k_suffix_copy(RowArrays a, long long n_static, int S, RowArrays tmp)
 {
+    CLS_PDL_WAIT();
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < S; r += gridDim.x * blockDim.x)
         copy_row(a, n_static + r, tmp, r, false);
 }
@@ -99,6 +104,7 @@ __global__ void k_suffix_scatter(RowArrays tmp, RowArrays a, long long n_static,
                                  const unsigned *e_keep, const unsigned *e_clone, const unsigned *e_split,
                                  const unsigned long long *tot, const float *__restrict__ normals)
 {
+    CLS_PDL_WAIT();
     const long long K = (long long)tot[0], C = (long long)tot[1], P = (long long)tot[2];
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < S; r += gridDim.x * blockDim.x) {
         const unsigned k = kind[r];
@@ -129,6 +135,7 @@ __global__ void k_suffix_scatter(RowArrays tmp, RowArrays a, long long n_static,
 
 __global__ void k_reset_stats(float *acc, int *cnt, long long n)
 {
+    CLS_PDL_WAIT();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         acc[i] = 0.f;
         cnt[i] = 0;
@@ -140,6 +147,7 @@ __global__ void k_reset_stats(float *acc, int *cnt, long long n)
 // Gaussian has a record, || dL/d(u, v) * (W/2, H/2) || * V_total (reading R31)
 __global__ void k_densify_stats(Scratch s, int V, float sx, float sy, float *acc, int *cnt)
 {
+    CLS_PDL_WAIT();
     const int A = s.cnt->A;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < A; k += gridDim.x * blockDim.x) {
         float a = 0.f;
@@ -164,7 +172,7 @@ void launch_densify_stats(const StepDims &d, const Scratch &s, int n_views_total
                           cudaStream_t st)
 {
     const float sx = 0.5f * (float)d.W * (float)n_views_total, sy = 0.5f * (float)d.H * (float)n_views_total;
-    k_densify_stats<<<148 * 4, 256, 0, st>>>(s, d.V, sx, sy, acc, cnt);
+    cls_launch(k_densify_stats, 148 * 4, 256, 0, st, s, d.V, sx, sy, acc, cnt);
     g_launches++;
 }
 
@@ -185,12 +193,12 @@ void launch_partition(const float4 *mo, const float4 *q, const float4 *ls, const
                       unsigned long long *n_static_dev, cudaStream_t st)
 {
     const int blocks = std::max(1, std::min((n + 255) / 256, 148 * 8));
-    k_part_flags<<<blocks, 256, 0, st>>>(mo, n, regs, flag);
+    cls_launch(k_part_flags, blocks, 256, 0, st, mo, n, regs, flag);
     cudaMemcpyAsync(n_dev, &n, sizeof(int), cudaMemcpyHostToDevice, st);
     scan_excl_u32(flag, excl, n_dev, n, status, ticket, n_static_dev, nullptr, st);
     RowArrays src = rows_of((float4 *)mo, (float4 *)q, (float4 *)ls, (float4 *)sh, nullptr, nullptr, nullptr, nullptr, D);
     RowArrays dst = rows_of(omo, oq, ols, osh, nullptr, nullptr, nullptr, nullptr, D);
-    k_part_scatter<<<blocks, 256, 0, st>>>(src, dst, n, flag, excl, n_static_dev);
+    cls_launch(k_part_scatter, blocks, 256, 0, st, src, dst, n, flag, excl, n_static_dev);
     g_launches += 2;
 }
 
@@ -204,8 +212,8 @@ void launch_suffix_plan(int mode, const RowArrays &a, long long n_static, int S,
     unsigned *kind = work, *keep = work + S4, *clone = work + 2 * S4, *split = work + 3 * S4;
     unsigned *ek = work + 4 * S4, *ec = work + 5 * S4, *es = work + 6 * S4;
     const int blocks = std::max(1, std::min((S + 255) / 256, 148 * 8));
-    if (mode == 0) k_prune_kind<<<blocks, 256, 0, st>>>(a, n_static, S, regs, kind, keep, clone, split);
-    else k_densify_kind<<<blocks, 256, 0, st>>>(a, n_static, S, grad_thr, log_scale_thr, kind, keep, clone, split);
+    if (mode == 0) cls_launch(k_prune_kind, blocks, 256, 0, st, a, n_static, S, regs, kind, keep, clone, split);
+    else cls_launch(k_densify_kind, blocks, 256, 0, st, a, n_static, S, grad_thr, log_scale_thr, kind, keep, clone, split);
     cudaMemcpyAsync(S_dev, &S, sizeof(int), cudaMemcpyHostToDevice, st);
     scan_excl_u32(keep, ek, S_dev, S, status, ticket, tot + 0, nullptr, st);
     scan_excl_u32(clone, ec, S_dev, S, status, ticket, tot + 1, nullptr, st);
@@ -222,8 +230,8 @@ void launch_suffix_apply(const RowArrays &a, long long n_static, int S, const Ro
     const unsigned *kind = work;
     const unsigned *ek = work + 4 * S4, *ec = work + 5 * S4, *es = work + 6 * S4;
     const int blocks = std::max(1, std::min((S + 255) / 256, 148 * 8));
-    k_suffix_copy<<<blocks, 256, 0, st>>>(a, n_static, S, tmp);
-    k_suffix_scatter<<<blocks, 256, 0, st>>>(tmp, a, n_static, S, kind, ek, ec, es, tot, normals);
+    cls_launch(k_suffix_copy, blocks, 256, 0, st, a, n_static, S, tmp);
+    cls_launch(k_suffix_scatter, blocks, 256, 0, st, tmp, a, n_static, S, kind, ek, ec, es, tot, normals);
     g_launches += 2;
 }
 
@@ -231,6 +239,7 @@ void launch_suffix_apply(const RowArrays &a, long long n_static, int S, const Ro
 __global__ void k_flags_regions(const float4 *__restrict__ mean_op, int n, const __grid_constant__ RegSet regs,
                                 unsigned *flag, uint8_t *I)
 {
+    CLS_PDL_WAIT();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const bool in = in_regions(mean_op[i], regs);
         flag[i] = in ? 1u : 0u;
@@ -241,6 +250,7 @@ __global__ void k_flags_regions(const float4 *__restrict__ mean_op, int n, const
 __global__ void k_flags_u8(const uint8_t *__restrict__ a, const uint8_t *__restrict__ b, int n, unsigned *flag,
                            int mode)
 {
+    CLS_PDL_WAIT();
     // mode 0: flag = a != 0; mode 1: flag = (a == 0 && b == 0)
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
         flag[i] = mode == 0 ? (a[i] != 0) : (a[i] == 0 && b[i] == 0);
@@ -250,6 +260,7 @@ __global__ void k_flags_u8(const uint8_t *__restrict__ a, const uint8_t *__restr
 __global__ void k_compact_rows(RowArrays src, RowArrays dst, int n, const unsigned *__restrict__ flag,
                                const unsigned *__restrict__ excl, long long off)
 {
+    CLS_PDL_WAIT();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
         if (flag[i]) copy_row(src, i, dst, off + excl[i], false);
 }
@@ -258,6 +269,7 @@ __global__ void k_compact_rows(RowArrays src, RowArrays dst, int n, const unsign
 __global__ void k_recover_rows(RowArrays cur, RowArrays O, RowArrays out, int n, const unsigned *__restrict__ flag,
                                const unsigned *__restrict__ excl)
 {
+    CLS_PDL_WAIT();
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
         const unsigned r1 = excl[j];
         if (flag[j]) copy_row(O, r1, out, j, false);
@@ -267,33 +279,33 @@ __global__ void k_recover_rows(RowArrays cur, RowArrays O, RowArrays out, int n,
 
 void launch_flags_regions(const float4 *mo, int n, const RegSet &regs, unsigned *flag, uint8_t *I, cudaStream_t st)
 {
-    k_flags_regions<<<std::max(1, std::min((n + 255) / 256, 148 * 8)), 256, 0, st>>>(mo, n, regs, flag, I);
+    cls_launch(k_flags_regions, std::max(1, std::min((n + 255) / 256, 148 * 8)), 256, 0, st, mo, n, regs, flag, I);
     g_launches++;
 }
 
 void launch_flags_u8(const uint8_t *a, const uint8_t *b, int n, unsigned *flag, int mode, cudaStream_t st)
 {
-    k_flags_u8<<<std::max(1, std::min((n + 255) / 256, 148 * 8)), 256, 0, st>>>(a, b, n, flag, mode);
+    cls_launch(k_flags_u8, std::max(1, std::min((n + 255) / 256, 148 * 8)), 256, 0, st, a, b, n, flag, mode);
     g_launches++;
 }
 
 void launch_compact_rows(const RowArrays &src, const RowArrays &dst, int n, const unsigned *flag, const unsigned *excl,
                          long long off, cudaStream_t st)
 {
-    k_compact_rows<<<std::max(1, std::min((n + 255) / 256, 148 * 8)), 256, 0, st>>>(src, dst, n, flag, excl, off);
+    cls_launch(k_compact_rows, std::max(1, std::min((n + 255) / 256, 148 * 8)), 256, 0, st, src, dst, n, flag, excl, off);
     g_launches++;
 }
 
 void launch_recover_rows(const RowArrays &cur, const RowArrays &O, const RowArrays &out, int n, const unsigned *flag,
                          const unsigned *excl, cudaStream_t st)
 {
-    k_recover_rows<<<std::max(1, std::min((n + 255) / 256, 148 * 8)), 256, 0, st>>>(cur, O, out, n, flag, excl);
+    cls_launch(k_recover_rows, std::max(1, std::min((n + 255) / 256, 148 * 8)), 256, 0, st, cur, O, out, n, flag, excl);
     g_launches++;
 }
 
 void launch_reset_stats(float *acc, int *cnt, long long n, cudaStream_t st)
 {
-    k_reset_stats<<<148 * 4, 256, 0, st>>>(acc, cnt, n);
+    cls_launch(k_reset_stats, 148 * 4, 256, 0, st, acc, cnt, n);
     g_launches++;
 }
 
@@ -316,6 +328,7 @@ __device__ __forceinline__ float ord2f(unsigned u) { return __uint_as_float((u &
 
 __global__ void k_bbox(const float4 *__restrict__ mo, int n, unsigned *bb)
 {
+    CLS_PDL_WAIT();
     unsigned lo[3] = {0xffffffffu, 0xffffffffu, 0xffffffffu}, hi[3] = {0u, 0u, 0u};
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const float4 m = mo[i];
@@ -351,6 +364,7 @@ __device__ __forceinline__ unsigned spread10(unsigned x)   // 10 bits -> every t
 __global__ void k_morton(const float4 *__restrict__ mo, int n, const unsigned *bb, unsigned long long *keys,
                          unsigned *vals)
 {
+    CLS_PDL_WAIT();
     float lo[3], sc[3];
     for (int a = 0; a < 3; a++) {
         lo[a] = ord2f(bb[a]);
@@ -372,6 +386,7 @@ __global__ void k_morton(const float4 *__restrict__ mo, int n, const unsigned *b
 
 __global__ void k_gather_rows(RowArrays src, RowArrays dst, int n, const unsigned *__restrict__ perm)
 {
+    CLS_PDL_WAIT();
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
         copy_row(src, perm[j], dst, j, false);
 }
@@ -383,11 +398,11 @@ void launch_spatial_order(const RowArrays &src, const RowArrays &dst, int n, uns
     const int blocks = std::max(1, std::min((n + 255) / 256, 148 * 8));
     cudaMemsetAsync(bb, 0xff, 3 * sizeof(unsigned), st);
     cudaMemsetAsync(bb + 3, 0, 3 * sizeof(unsigned), st);
-    k_bbox<<<blocks, 256, 0, st>>>(src.mo, n, bb);
-    k_morton<<<blocks, 256, 0, st>>>(src.mo, n, bb, keys, vals);
+    cls_launch(k_bbox, blocks, 256, 0, st, src.mo, n, bb);
+    cls_launch(k_morton, blocks, 256, 0, st, src.mo, n, bb, keys, vals);
     cudaMemcpyAsync(n_dev, &n, sizeof(int), cudaMemcpyHostToDevice, st);
     const int w = radix_sort_u64(keys, keys_alt, vals, vals_alt, n_dev, n, 0, 30, 8, counts, totals, nullptr, st);
-    k_gather_rows<<<blocks, 256, 0, st>>>(src, dst, n, w ? vals_alt : vals);
+    cls_launch(k_gather_rows, blocks, 256, 0, st, src, dst, n, w ? vals_alt : vals);
     g_launches += 3;
 }
 

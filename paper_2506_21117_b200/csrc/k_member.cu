@@ -12,6 +12,7 @@
 namespace cls {
 
 int64_t g_launches = 0;
+bool g_pdl = getenv("CLS_NO_PDL") == nullptr;
 
 #define MEMBER_THREADS 256
 #define MEMBER_ITEMS 8
@@ -21,6 +22,7 @@ __global__ void __launch_bounds__(MEMBER_THREADS)
 k_member(const float4 *__restrict__ mean_op, int n, const __grid_constant__ RegSet regs, Scratch s,
          const int *__restrict__ skip)
 {
+    CLS_PDL_WAIT();
     __shared__ int s_tile;
     if (skip && *skip) return;   // the static cache is valid: k_member_list tests its rows instead
     __shared__ int s_wcnt[MEMBER_ITEMS][MEMBER_THREADS / 32];
@@ -83,7 +85,7 @@ void launch_member(const Params &g, const StepDims &d, const RegSet &regs, const
 {
     const int blocks = (d.n + MEMBER_TILE - 1) / MEMBER_TILE;
     cudaMemsetAsync(s.st_member, 0, sizeof(unsigned long long) * blocks, st);
-    k_member<<<blocks, MEMBER_THREADS, 0, st>>>(g.mean_op, d.n, regs, s, skip);
+    cls_launch(k_member, blocks, MEMBER_THREADS, 0, st, g.mean_op, d.n, regs, s, skip);
     g_launches++;
 }
 
@@ -96,6 +98,7 @@ __global__ void __launch_bounds__(MEMBER_THREADS)
 k_member_list(const float4 *__restrict__ mean_op, const int *__restrict__ list, const int *__restrict__ n_list,
               const int *__restrict__ valid, const __grid_constant__ RegSet regs, Scratch s)
 {
+    CLS_PDL_WAIT();
     __shared__ int s_tile;
     __shared__ int s_wcnt[MEMBER_ITEMS][MEMBER_THREADS / 32];
     __shared__ unsigned long long s_prefix;
@@ -162,7 +165,7 @@ k_member_list(const float4 *__restrict__ mean_op, const int *__restrict__ list, 
 void launch_member_list(const Params &g, const int *list, const int *n_list, const int *valid, const RegSet &regs,
                         const Scratch &s, cudaStream_t st)
 {
-    k_member_list<<<148 * 2, MEMBER_THREADS, 0, st>>>(g.mean_op, list, n_list, valid, regs, s);
+    cls_launch(k_member_list, 148 * 2, MEMBER_THREADS, 0, st, g.mean_op, list, n_list, valid, regs, s);
     g_launches++;
 }
 
@@ -175,6 +178,7 @@ __global__ void __launch_bounds__(256)
 k_active_rects(const float4 *__restrict__ mean_op, const float4 *__restrict__ quat,
                const float4 *__restrict__ log_scale, const __grid_constant__ CamSet cams, Scratch s)
 {
+    CLS_PDL_WAIT();
     const int A = s.cnt->A;
     const long long total = (long long)A * cams.n;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
@@ -223,6 +227,7 @@ __device__ __forceinline__ void warp_prefix(int *a, int n, int st)
 template <bool SMEM>
 __global__ void __launch_bounds__(SAT_THREADS) k_sat(const __grid_constant__ CamSet cams, Scratch s, int all_tiles, const int *__restrict__ skip)
 {
+    CLS_PDL_WAIT();
     extern __shared__ int sm_sat[];
     if (skip && *skip) return;   // a gated (skipped) build of the static cache's dilated mask
     const int v = blockIdx.x;
@@ -291,14 +296,14 @@ void launch_active_mask(const Params &g, const StepDims &d, const CamSet &cams, 
         // persistent over the A x V (Gaussian, view) pairs: 3 CTAs per SM fit its 78 registers
         int blocks = (int)std::min<long long>(((long long)d.n * d.V + 255) / 256, 148LL * 3);
         if (blocks < 1) blocks = 1;
-        k_active_rects<<<blocks, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, cams, s);
+        cls_launch(k_active_rects, blocks, 256, 0, st, g.mean_op, g.quat, g.log_scale, cams, s);
         g_launches++;
     }
     const size_t smem = sizeof(int) * (size_t)(d.TY + 1) * (d.TX + 1) + (size_t)d.TX * d.TY;
     static std::atomic<unsigned long long> attr{0};
     per_device_once(attr, [] { cudaFuncSetAttribute(k_sat<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
-    if (smem <= 200 * 1024) k_sat<true><<<d.V, SAT_THREADS, smem, st>>>(cams, s, d.all_tiles, nullptr);
-    else k_sat<false><<<d.V, SAT_THREADS, 0, st>>>(cams, s, d.all_tiles, nullptr);
+    if (smem <= 200 * 1024) cls_launch(k_sat<true>, d.V, SAT_THREADS, smem, st, cams, s, d.all_tiles, nullptr);
+    else cls_launch(k_sat<false>, d.V, SAT_THREADS, 0, st, cams, s, d.all_tiles, nullptr);
     g_launches++;
 }
 
@@ -309,8 +314,8 @@ void launch_sat_only(const StepDims &d, const CamSet &cams, const Scratch &s, co
     const size_t smem = sizeof(int) * (size_t)(d.TY + 1) * (d.TX + 1) + (size_t)d.TX * d.TY;
     static std::atomic<unsigned long long> attr{0};
     per_device_once(attr, [] { cudaFuncSetAttribute(k_sat<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
-    if (smem <= 200 * 1024) k_sat<true><<<d.V, SAT_THREADS, smem, st>>>(cams, s, 0, skip);
-    else k_sat<false><<<d.V, SAT_THREADS, 0, st>>>(cams, s, 0, skip);
+    if (smem <= 200 * 1024) cls_launch(k_sat<true>, d.V, SAT_THREADS, smem, st, cams, s, 0, skip);
+    else cls_launch(k_sat<false>, d.V, SAT_THREADS, 0, st, cams, s, 0, skip);
     g_launches++;
 }
 

@@ -167,6 +167,7 @@ k_project_cand(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
                const float4 *__restrict__ log_scale, int n, const __grid_constant__ CamSet cams, Scratch s,
                const int *__restrict__ glist, const int *__restrict__ n_glist, const int *__restrict__ exclude)
 {
+    CLS_PDL_WAIT();
     // glist (optional): project only the Gaussians glist[0 .. *n_glist) (the static cache's dynamic set);
     // exclude (optional): skip Gaussian i where exclude[i] >= 0 (the cache's frozen build)
     if (s.cnt->overflow) return;   // capacity overflow, or a skipped (gated) cache build
@@ -405,6 +406,7 @@ k_project_exact(const float4 *__restrict__ mean_op, const float4 *__restrict__ q
                 const float4 *__restrict__ log_scale, const float4 *__restrict__ sh, int n,
                 const __grid_constant__ CamSet cams, Scratch s)
 {
+    CLS_PDL_WAIT();
     __shared__ GCam s_cams[CLS_MAX_VIEWS];   // lanes index different views: no constant-bank serialisation
     __shared__ double2 s_lims[CLS_MAX_VIEWS];   // per-view frustum-clamp limits (view constants)
     for (int k = threadIdx.x; k < cams.n * (int)(sizeof(GCam) / 4); k += blockDim.x)
@@ -512,10 +514,10 @@ void launch_project_cand(const Params &g, const StepDims &d, const CamSet &cams,
     });
     const int blocks = std::min((d.n + PC_THREADS - 1) / PC_THREADS, 148 * 3);
     if (smem <= 96 * 1024)
-        k_project_cand<true><<<blocks, PC_THREADS, smem, st>>>(g.mean_op, g.quat, g.log_scale, d.n, cams, s, rows,
+        cls_launch(k_project_cand<true>, blocks, PC_THREADS, smem, st, g.mean_op, g.quat, g.log_scale, d.n, cams, s, rows,
                                                                n_rows, exclude);
     else
-        k_project_cand<false><<<blocks, PC_THREADS, 0, st>>>(g.mean_op, g.quat, g.log_scale, d.n, cams, s, rows,
+        cls_launch(k_project_cand<false>, blocks, PC_THREADS, 0, st, g.mean_op, g.quat, g.log_scale, d.n, cams, s, rows,
                                                              n_rows, exclude);
     g_launches++;
 }
@@ -524,10 +526,10 @@ void launch_project_exact(const Params &g, const StepDims &d, const CamSet &cams
 {
     const int grid = 148 * 3;   // persistent: the 3 CTAs per SM the register budget allows
     switch (d.D) {
-    case 0: k_project_exact<0><<<grid, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s); break;
-    case 1: k_project_exact<1><<<grid, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s); break;
-    case 2: k_project_exact<2><<<grid, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s); break;
-    default: k_project_exact<3><<<grid, 256, 0, st>>>(g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s); break;
+    case 0: cls_launch(k_project_exact<0>, grid, 256, 0, st, g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s); break;
+    case 1: cls_launch(k_project_exact<1>, grid, 256, 0, st, g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s); break;
+    case 2: cls_launch(k_project_exact<2>, grid, 256, 0, st, g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s); break;
+    default: cls_launch(k_project_exact<3>, grid, 256, 0, st, g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s); break;
     }
     g_launches++;
 }

@@ -339,6 +339,7 @@ __global__ void __launch_bounds__(RT_THREADS, 12)
 k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ targets,
       const unsigned char *__restrict__ targets8, bool staged, float *__restrict__ images, float loss_scale, float3 bg)
 {
+    CLS_PDL_WAIT();
     __shared__ float4 ent[3 * (RT_BATCH + 3)];   // staged entries (sa, sb, sc) + up to 3 pad entries
     __shared__ float red[RT_THREADS / 32];
     __shared__ int s_item, s_pos[RT_SLOTS], s_wc[2 * RT_SCAN], s_first, s_clamp, s_lastp[CLS_BLOCK_PIX];
@@ -471,6 +472,7 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
 __global__ void __launch_bounds__(RT_THREADS) k_loss_staged(const __grid_constant__ CamSet cams, Scratch s,
                                                             float loss_scale)
 {
+    CLS_PDL_WAIT();
     __shared__ float red[RT_THREADS / 32];
     if (s.cnt->overflow) return;
     const int n_items = s.cnt->n_items;
@@ -504,7 +506,7 @@ __global__ void __launch_bounds__(RT_THREADS) k_loss_staged(const __grid_constan
 
 void launch_loss_staged(const StepDims &d, const CamSet &cams, const Scratch &s, float loss_scale, cudaStream_t st)
 {
-    k_loss_staged<<<148 * 16, RT_THREADS, 0, st>>>(cams, s, loss_scale);
+    cls_launch(k_loss_staged, 148 * 16, RT_THREADS, 0, st, cams, s, loss_scale);
     g_launches++;
 }
 
@@ -514,10 +516,10 @@ void launch_fwd(const StepDims &d, const CamSet &cams, const Scratch &s, const v
     const int grid = 148 * 16;
     const float *t32 = targets_u8 ? nullptr : (const float *)targets;
     const unsigned char *t8 = targets_u8 ? (const unsigned char *)targets : nullptr;
-    if (targets && images) k_fwd<true, true><<<grid, RT_THREADS, 0, st>>>(cams, s, t32, t8, staged, images, loss_scale, bg);
-    else if (targets) k_fwd<true, false><<<grid, RT_THREADS, 0, st>>>(cams, s, t32, t8, staged, images, loss_scale, bg);
-    else if (images) k_fwd<false, true><<<grid, RT_THREADS, 0, st>>>(cams, s, t32, t8, staged, images, loss_scale, bg);
-    else k_fwd<false, false><<<grid, RT_THREADS, 0, st>>>(cams, s, t32, t8, staged, images, loss_scale, bg);
+    if (targets && images) cls_launch(k_fwd<true, true>, grid, RT_THREADS, 0, st, cams, s, t32, t8, staged, images, loss_scale, bg);
+    else if (targets) cls_launch(k_fwd<true, false>, grid, RT_THREADS, 0, st, cams, s, t32, t8, staged, images, loss_scale, bg);
+    else if (images) cls_launch(k_fwd<false, true>, grid, RT_THREADS, 0, st, cams, s, t32, t8, staged, images, loss_scale, bg);
+    else cls_launch(k_fwd<false, false>, grid, RT_THREADS, 0, st, cams, s, t32, t8, staged, images, loss_scale, bg);
     g_launches++;
 }
 
@@ -525,6 +527,7 @@ void launch_fwd(const StepDims &d, const CamSet &cams, const Scratch &s, const v
 __global__ void k_fill_bg(int V, int W, int H, int TX, int T, const uint8_t *__restrict__ mask, float *images,
                           float3 bg)
 {
+    CLS_PDL_WAIT();
     const size_t HW = (size_t)H * W;
     const size_t total = (size_t)V * HW;
     for (size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x; p < total; p += (size_t)gridDim.x * blockDim.x) {
@@ -541,13 +544,14 @@ __global__ void k_fill_bg(int V, int W, int H, int TX, int T, const uint8_t *__r
 
 void launch_fill_bg(const StepDims &d, const Scratch &s, float *images, float3 bg, cudaStream_t st)
 {
-    k_fill_bg<<<148 * 8, 256, 0, st>>>(d.V, d.W, d.H, d.TX, d.T, s.mask, images, bg);
+    cls_launch(k_fill_bg, 148 * 8, 256, 0, st, d.V, d.W, d.H, d.TX, d.T, s.mask, images, bg);
     g_launches++;
 }
 
 // deterministic loss: fixed-order reduction of the per-item partial sums (fp64 accumulate)
 __global__ void __launch_bounds__(1024) k_loss(Scratch s, float loss_scale, float *loss)
 {
+    CLS_PDL_WAIT();
     __shared__ double red[32];
     const int n = s.cnt->overflow ? 0 : s.cnt->n_items;
     double acc = 0.0;
@@ -575,7 +579,7 @@ __global__ void __launch_bounds__(1024) k_loss(Scratch s, float loss_scale, floa
 
 void launch_loss(const Scratch &s, float loss_scale, float *loss, cudaStream_t st)
 {
-    k_loss<<<1, 1024, 0, st>>>(s, loss_scale, loss);
+    cls_launch(k_loss, 1, 1024, 0, st, s, loss_scale, loss);
     g_launches++;
 }
 
@@ -626,6 +630,7 @@ __device__ __forceinline__ float warp_reduce_scatter9(const float (&r)[9], int l
 __global__ void __launch_bounds__(RT_THREADS, 12)
 k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ dL_dimg, float3 bg)
 {
+    CLS_PDL_WAIT();
     __shared__ float4 ent[3 * (RT_BATCH + 1)];
     __shared__ float2 sd[RT_BATCH];    // tile-local 2D mean (dx0, dy0) in fp32
     __shared__ int s_item, s_maxlast, s_pos[RT_SLOTS], s_wc[2 * RT_SCAN];
@@ -829,6 +834,7 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
 // tile into a [V][H][W] image (the caller pre-fills the rest)
 __global__ void k_debug_pixels(const __grid_constant__ CamSet cams, Scratch s, float *out)
 {
+    CLS_PDL_WAIT();
     const int n_items = s.cnt->overflow ? 0 : s.cnt->n_items;
     const int W = cams.W, H = cams.H, TX = cams.TX, T = cams.T;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)n_items * CLS_BLOCK_PIX;
@@ -844,7 +850,7 @@ __global__ void k_debug_pixels(const __grid_constant__ CamSet cams, Scratch s, f
 
 void launch_debug_pixels(const StepDims &d, const CamSet &cams, const Scratch &s, float *out, cudaStream_t st)
 {
-    k_debug_pixels<<<148 * 4, 256, 0, st>>>(cams, s, out);
+    cls_launch(k_debug_pixels, 148 * 4, 256, 0, st, cams, s, out);
     g_launches++;
 }
 
@@ -859,6 +865,7 @@ __device__ __forceinline__ int debug_gid(const Scratch &s, const CacheBufs &cb, 
 __global__ void k_debug_records(Scratch s, CacheBufs cb, int cached, float4 *out, int *gid, int *view, long long max,
                                 int *count)
 {
+    CLS_PDL_WAIT();
     const int F = cached ? cb.st->F : 0;
     const int D = s.cnt->overflow ? 0 : min(s.cnt->n_records, (int)s.max_records);
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)F + D && e < max;
@@ -886,6 +893,7 @@ __global__ void k_debug_records(Scratch s, CacheBufs cb, int cached, float4 *out
 __global__ void k_debug_tile_list(Scratch s, CacheBufs cb, int cached, int TY, int TX, int view, int tile, int *out,
                                   int max, int *count)
 {
+    CLS_PDL_WAIT();
     if (blockIdx.x != 0 || threadIdx.x != 0) return;
     const int tx = tile % TX, ty = tile / TX, seg = view * TY + ty;
     int k = 0;
@@ -903,19 +911,20 @@ __global__ void k_debug_tile_list(Scratch s, CacheBufs cb, int cached, int TY, i
 void launch_debug_records(const Scratch &s, const CacheBufs &cb, int cached, float *out, int *gid, int *view,
                           long long max, int *count, cudaStream_t st)
 {
-    k_debug_records<<<148 * 4, 256, 0, st>>>(s, cb, cached, reinterpret_cast<float4 *>(out), gid, view, max, count);
+    cls_launch(k_debug_records, 148 * 4, 256, 0, st, s, cb, cached, reinterpret_cast<float4 *>(out), gid, view, max, count);
     g_launches++;
 }
 
 void launch_debug_tile_list(const Scratch &s, const CacheBufs &cb, int cached, int TY, int TX, int view, int tile,
                             int *out, int max, int *count, cudaStream_t st)
 {
-    k_debug_tile_list<<<1, 32, 0, st>>>(s, cb, cached, TY, TX, view, tile, out, max, count);
+    cls_launch(k_debug_tile_list, 1, 32, 0, st, s, cb, cached, TY, TX, view, tile, out, max, count);
     g_launches++;
 }
 
 __global__ void k_zero_grad2d(Scratch s, int V, long long cap)
 {
+    CLS_PDL_WAIT();
     const long long A = s.cnt->A;
     if (A > cap) {
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&s.cnt->overflow, 4);
@@ -928,7 +937,7 @@ __global__ void k_zero_grad2d(Scratch s, int V, long long cap)
 
 void launch_zero_grad2d(const StepDims &d, const Scratch &s, long long cap, cudaStream_t st)
 {
-    k_zero_grad2d<<<148 * 4, 256, 0, st>>>(s, d.V, cap);
+    cls_launch(k_zero_grad2d, 148 * 4, 256, 0, st, s, d.V, cap);
     g_launches++;
 }
 
@@ -936,7 +945,7 @@ void launch_bwd_raster(const StepDims &d, const Scratch &s, const float *dL_dima
 {
     CamSet cams;
     cams.n = d.V; cams.W = d.W; cams.H = d.H; cams.TX = d.TX; cams.TY = d.TY; cams.T = d.T;
-    k_bwd<<<148 * 16, RT_THREADS, 0, st>>>(cams, s, dL_dimages, bg);
+    cls_launch(k_bwd, 148 * 16, RT_THREADS, 0, st, cams, s, dL_dimages, bg);
     g_launches++;
 }
 

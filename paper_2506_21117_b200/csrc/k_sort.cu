@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(RS_THREADS)
 k_rs_upsweep(const unsigned long long *__restrict__ keys, const int *__restrict__ n_ptr, int max_n, int shift,
              unsigned *__restrict__ counts, const int *__restrict__ skip)
 {
+    CLS_PDL_WAIT();
     constexpr int BINS = 1 << BITS;
     __shared__ unsigned hist[BINS];
     for (int d = threadIdx.x; d < BINS; d += RS_THREADS) hist[d] = 0u;
@@ -58,6 +59,7 @@ __global__ void __launch_bounds__(256) k_rs_scan(unsigned *__restrict__ counts, 
                                                  int bins, int G, const int *__restrict__ n_ptr, int max_n,
                                                  const int *__restrict__ skip)
 {
+    CLS_PDL_WAIT();
     const int d = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (d >= bins) return;
     const int n = (skip && *skip) ? 0 : min(*n_ptr, max_n);
@@ -102,6 +104,7 @@ k_rs_downsweep(const unsigned long long *__restrict__ kin, unsigned long long *_
                int shift, const unsigned *__restrict__ counts, const unsigned *__restrict__ totals,
                const int *__restrict__ skip)
 {
+    CLS_PDL_WAIT();
     constexpr int BINS = 1 << BITS;
     constexpr int WP = RS_WARPS + 1;
     constexpr int DPT = BINS / RS_THREADS;   // digits per thread in the table scan (1 or 2)
@@ -266,9 +269,9 @@ static void rs_pass(unsigned long long *kin, unsigned long long *kout, unsigned 
     per_device_once(attr, [&] {
         cudaFuncSetAttribute(k_rs_downsweep<BITS, VALS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
     });
-    k_rs_upsweep<BITS><<<RS_GRID, RS_THREADS, 0, st>>>(kin, n_ptr, max_n, shift, counts, skip);
-    k_rs_scan<<<((1 << BITS) + 7) / 8, 256, 0, st>>>(counts, totals, 1 << BITS, RS_GRID, n_ptr, max_n, skip);
-    k_rs_downsweep<BITS, VALS><<<RS_GRID, RS_THREADS, SM, st>>>(kin, kout, vin, vout, n_ptr, max_n, shift, counts,
+    cls_launch(k_rs_upsweep<BITS>, RS_GRID, RS_THREADS, 0, st, kin, n_ptr, max_n, shift, counts, skip);
+    cls_launch(k_rs_scan, ((1 << BITS) + 7) / 8, 256, 0, st, counts, totals, 1 << BITS, RS_GRID, n_ptr, max_n, skip);
+    cls_launch(k_rs_downsweep<BITS, VALS>, RS_GRID, RS_THREADS, SM, st, kin, kout, vin, vout, n_ptr, max_n, shift, counts,
                                                                 totals, skip);
     g_launches += 3;
 }
@@ -305,6 +308,7 @@ __global__ void __launch_bounds__(SC_THREADS)
 k_scan_excl(const unsigned *__restrict__ in, unsigned *__restrict__ out, const int *__restrict__ n_ptr, int max_n,
             unsigned long long *status, int *ticket, unsigned long long *total, const int *__restrict__ skip)
 {
+    CLS_PDL_WAIT();
     __shared__ int s_tile;
     __shared__ unsigned long long s_warp[SC_THREADS / 32];
     __shared__ unsigned long long s_prefix;
@@ -386,7 +390,7 @@ void scan_excl_u32(const unsigned *in, unsigned *out, const int *n_ptr, int max_
     const int tiles = (max_n + SC_TILE - 1) / SC_TILE;
     cudaMemsetAsync(status, 0, sizeof(unsigned long long) * (size_t)(tiles + 1), st);
     cudaMemsetAsync(ticket, 0, sizeof(int), st);
-    k_scan_excl<<<148 * 4, SC_THREADS, 0, st>>>(in, out, n_ptr, max_n, status, ticket, total, skip);
+    cls_launch(k_scan_excl, 148 * 4, SC_THREADS, 0, st, in, out, n_ptr, max_n, status, ticket, total, skip);
     g_launches++;
 }
 

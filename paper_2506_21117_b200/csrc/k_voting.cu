@@ -18,6 +18,7 @@ namespace cls {
 __global__ void __launch_bounds__(256) k_vote(const float4 *__restrict__ mean_op, int n, const __grid_constant__ CamSet cams,
                                               const uint8_t *__restrict__ masks, int *c_out, int *o_out, uint8_t *member)
 {
+    CLS_PDL_WAIT();
     __shared__ GCam s_cam[CLS_MAX_VIEWS];
     for (int k = threadIdx.x; k < cams.n * (int)(sizeof(GCam) / 4); k += blockDim.x)
         reinterpret_cast<float *>(s_cam)[k] = reinterpret_cast<const float *>(cams.c)[k];
@@ -59,7 +60,7 @@ void launch_vote(const float4 *mean_op, int n, const CamSet &cams, const uint8_t
                  uint8_t *member, cudaStream_t st)
 {
     const int blocks = std::max(1, std::min((n + 255) / 256, 148 * 8));
-    k_vote<<<blocks, 256, 0, st>>>(mean_op, n, cams, masks, c_out, o_out, member);
+    cls_launch(k_vote, blocks, 256, 0, st, mean_op, n, cams, masks, c_out, o_out, member);
     g_launches++;
 }
 
@@ -68,6 +69,7 @@ void launch_vote(const float4 *mean_op, int n, const CamSet &cams, const uint8_t
 __global__ void k_cluster_sums(const float4 *__restrict__ mean_op, int n, const int *__restrict__ labels, int K,
                                double *sums)
 {
+    CLS_PDL_WAIT();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const int k = labels[i];
         if (k < 0 || k >= K) continue;
@@ -91,6 +93,7 @@ __device__ __forceinline__ double member_dist(const float4 m, const double *sums
 __global__ void k_cluster_keys(const float4 *__restrict__ mean_op, int n, const int *__restrict__ labels, int K,
                                const double *sums, unsigned long long *keys, unsigned *vals, int *starts)
 {
+    CLS_PDL_WAIT();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const int k = labels[i];
         const bool mem = k >= 0 && k < K;
@@ -103,6 +106,7 @@ __global__ void k_cluster_keys(const float4 *__restrict__ mean_op, int n, const 
 
 __global__ void k_cluster_starts(const unsigned long long *keys, int n, int K, int *starts)
 {
+    CLS_PDL_WAIT();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const int k = (int)(keys[i] >> 32);
         if (k >= K) continue;
@@ -114,6 +118,7 @@ __global__ void k_cluster_starts(const unsigned long long *keys, int n, int K, i
 __global__ void k_cluster_spheres(const float4 *__restrict__ mean_op, const int *labels, int K, const double *sums,
                                   const int *starts, const unsigned *vals, float *centres, float *radii)
 {
+    CLS_PDL_WAIT();
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x) {
         const double cnt = sums[4 * k + 3];
         if (cnt < 1.0) {
@@ -139,16 +144,16 @@ void launch_fit_spheres(const float4 *mean_op, int n, const int *labels, int K, 
 {
     const int blocks = std::max(1, std::min((n + 255) / 256, 148 * 8));
     cudaMemsetAsync(sums, 0, sizeof(double) * 4 * (size_t)K, st);
-    k_cluster_sums<<<blocks, 256, 0, st>>>(mean_op, n, labels, K, sums);
-    k_cluster_keys<<<blocks, 256, 0, st>>>(mean_op, n, labels, K, sums, keys, vals, starts);
+    cls_launch(k_cluster_sums, blocks, 256, 0, st, mean_op, n, labels, K, sums);
+    cls_launch(k_cluster_keys, blocks, 256, 0, st, mean_op, n, labels, K, sums, keys, vals, starts);
     cudaMemcpyAsync(n_dev, &n, sizeof(int), cudaMemcpyHostToDevice, st);
     int kb = 1;
     while ((1ll << kb) <= (long long)K) kb++;
     const int w = radix_sort_u64(keys, keys_alt, vals, vals_alt, n_dev, n, 0, 32 + kb, 8, counts, totals, nullptr, st);
     const unsigned long long *sk = w ? keys_alt : keys;
     const unsigned *sv = w ? vals_alt : vals;
-    k_cluster_starts<<<blocks, 256, 0, st>>>(sk, n, K, starts);
-    k_cluster_spheres<<<std::max(1, (K + 255) / 256), 256, 0, st>>>(mean_op, labels, K, sums, starts, sv, centres, radii);
+    cls_launch(k_cluster_starts, blocks, 256, 0, st, sk, n, K, starts);
+    cls_launch(k_cluster_spheres, std::max(1, (K + 255) / 256), 256, 0, st, mean_op, labels, K, sums, starts, sv, centres, radii);
     g_launches += 5;
 }
 

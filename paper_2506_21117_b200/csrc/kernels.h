@@ -2,6 +2,8 @@
 #pragma once
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
+#include <utility>
 
 #include "cls_internal.cuh"
 
@@ -135,5 +137,30 @@ inline void per_device_once(std::atomic<unsigned long long> &done, F &&set_attr)
 }
 
 extern int64_t g_launches;   // kernels launched by this process through libcls (host counter)
+extern bool g_pdl;           // programmatic dependent launch on (CLS_NO_PDL=1 turns it off)
+
+// Every kernel of libcls starts with CLS_PDL_WAIT() and is launched by cls_launch with programmatic
+// stream serialization: a kernel's blocks may be scheduled while its predecessor in the stream drains,
+// and wait (griddepcontrol.wait) for the predecessor's completion and memory flush before touching any
+// data -- the launch latency of the ~55 small kernels of a step overlaps the previous kernel's tail.
+// Correctness needs only the wait at the very start of every kernel (each kernel waits for its
+// predecessor, which itself waited for its own), which CLS_PDL_WAIT provides.
+#define CLS_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+
+template <typename... KArgs, typename... Args>
+inline void cls_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 }  // namespace cls
