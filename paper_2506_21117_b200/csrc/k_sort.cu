@@ -3,15 +3,17 @@
 // device memory (no host synchronisation inside a step, H8).
 //
 // Used by the binning of subsystem (3) (PAPER.md Supp. L539, "per-tile depth ordering";
-// reading R13: depth, ties by Gaussian index): the records are sorted by (view, depth)
-// and the (tile, record) pairs -- emitted in that order -- by their (view, tile) key, so
-// every tile's list comes out in depth order without a per-tile sort.
+// reading R13: depth, ties by Gaussian index): the records are sorted by (view, depth) (key-only,
+// the record id rides in the low key bits; k_permute orders ties by index), and the (record, tile
+// row) units -- emitted in that order -- stably by their row segment (view, tile row), so every row
+// segment lists its units in depth order and a tile's list is the subsequence covering it, without a
+// per-tile sort.  Also the scene's Morton layout and the sphere fit's per-cluster sort.
 //
 // Design (B200): persistent grid of RS_GRID blocks; block b owns a contiguous range of
-// 4096-element tiles, so stability across blocks is by construction.  Per pass:
+// 2048-element tiles, so stability across blocks is by construction.  Per pass:
 //   upsweep    per-block digit histograms (shared-memory atomics) -> counts[digit][block]
-//   scan       one warp per digit scans counts[digit][*] (exclusive), totals[digit]
-//   downsweep  per tile: stable in-warp ranking with __match_any_sync in element order,
+//   scan       one warp per digit scans counts[digit][*] over the blocks that own tiles, totals[digit]
+//   downsweep  per tile: stable in-warp ranking with ballots of the digit bits in element order,
 //              a (digit, warp) table scan, staging in shared memory in sorted order, and
 //              coalesced scatter to digit_base[digit] + rank (runs of equal digits are
 //              contiguous in the output).
