@@ -119,6 +119,7 @@ struct CacheBufs {      // the cache's device buffers (passed by value)
     unsigned *dpos;     // [Dcap] rank position of each dynamic record among the frozen ones
     int *db;            // [V*TY + 1] row-segment lower bounds of the sorted dynamic units
     unsigned *dq;       // [Dunits] rank position of each sorted dynamic unit's record
+    unsigned *dmi;      // [Dunits] merged position of each sorted dynamic unit (virtual merge)
     int2 *mitems;       // [max_units / MG_CHUNK + V*TY] (segment, first frozen unit) chunks of the merge
     int *dlist;         // [maxN] the step's rows: O^t (idx order), then S0 \ O^t
     double *dM;         // [maxN][12] per listed row: M = R(q^) diag(exp(l)) (9), opacity, qcut, pad
@@ -181,6 +182,22 @@ struct Scratch {
     long long max_active;
     Counters *cnt;
     int max_items;
+    // static cache: the raster reads each row segment as a VIRTUAL merge of the cached frozen units and
+    // the step's own units (no merged copy): merged position u of segment s is the dynamic unit j if
+    // vm_dmi[j] == u, else the frozen unit vm_flb[s] + (u - seg_off[s]) - #(dynamic units before u)
+    int vm_on;
+    const unsigned long long *vm_f;     // frozen units, sorted by segment
+    const int *vm_flb;                  // [V*TY + 1] their segment lower bounds
+    const int *vm_db;                   // [V*TY + 1] the step's units' segment lower bounds
+    const unsigned *vm_dmi;             // merged position of each of the step's units
+    const unsigned long long *vm_dkey;  // the step's units with their global record ids
+};
+
+// per-tile cursor of the virtual merge (uniform over the CTA)
+struct VCur {
+    int m0, f0, d0, d1;   // segment start (merged position), its first frozen unit, its dynamic units [d0, d1)
+    int dc;               // dynamic units with merged position < the scan cursor
+    int nm;               // merged position of the next one in the scan direction (sentinel if none)
 };
 
 // ---------------------------------------------------------------------------

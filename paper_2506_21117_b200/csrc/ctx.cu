@@ -190,7 +190,7 @@ cls_status cls_destroy(cls_ctx *c)
         if (p) cudaFree(p);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     void *cp[] = {c->cb.st, c->cb.ccnt, c->cb.dyn_of, c->cb.s0, c->cb.flag, c->cb.excl, c->cb.scan_status, c->cb.dmask,
-                  c->cb.dmdiff, c->cb.urec, c->cb.cfvd, c->cb.cfgid, c->cb.cseg_lb, c->cb.dpos, c->cb.db, c->cb.dq, c->cb.mitems, c->cb.dlist, c->cb.dM, c->cb.dcand, c->cb.dcinfo, c->d_dsat,
+                  c->cb.dmdiff, c->cb.urec, c->cb.cfvd, c->cb.cfgid, c->cb.cseg_lb, c->cb.dpos, c->cb.db, c->cb.dq, c->cb.dmi, c->cb.mitems, c->cb.dlist, c->cb.dM, c->cb.dcand, c->cb.dcinfo, c->d_dsat,
                   c->d_drowmask, c->d_dbbox, c->d_cukey, c->d_cukey_alt};
     for (void *p : cp)
         if (p) cudaFree(p);
@@ -288,7 +288,7 @@ static cls_status cache_allocate(cls_ctx *c)
               dalloc(&cb.cfvd, (size_t)R) && dalloc(&cb.cfgid, (size_t)R) && dalloc(&cb.cseg_lb, NSEG) &&
               dalloc(&cb.dpos, (size_t)Dcap) && dalloc(&cb.db, NSEG) && dalloc(&c->d_dsat, SAT) &&
               dalloc(&c->d_drowmask, V * c->maxTY * ((c->maxTX + 31) / 32)) && dalloc(&c->d_dbbox, V) &&
-              dalloc(&c->d_cukey, P) && dalloc(&c->d_cukey_alt, P) && dalloc(&cb.dq, P) && dalloc(&cb.dlist, N) &&
+              dalloc(&c->d_cukey, P) && dalloc(&c->d_cukey_alt, P) && dalloc(&cb.dq, P) && dalloc(&cb.dmi, P) && dalloc(&cb.dlist, N) &&
               dalloc(&cb.dM, N * 12) && dalloc(&cb.dcand, (size_t)Dcap) && dalloc(&cb.dcinfo, (size_t)Dcap) &&
               dalloc(&cb.mitems, P / 4096 + NSEG + 1) &&
               cudaMallocHost((void **)&c->h_cst, sizeof(CacheState)) == cudaSuccess;
@@ -559,11 +559,19 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
         unsigned long long *dsorted = nullptr;
         run(c, P_PAIRSORT, st, [&] { dsorted = launch_unit_sort(d, sd, st); });
         unsigned long long *merged = dsorted == s.ukey ? s.ukey_alt : s.ukey;
-        run(c, P_CACHE_MERGE, st, [&] { launch_cache_merge(d, cb, sd, fsorted, dsorted, merged, st); });
+        run(c, P_CACHE_MERGE, st, [&] { launch_cache_merge(d, cb, sd, fsorted, dsorted, merged, g_vmerge, st); });
         sr = s;
         sr.rec = cb.urec;
         sr.rskey = sd.rskey;
         sr.sukey = merged;
+        if (g_vmerge) {   // the raster merges the frozen and the step's sorted units on the fly
+            sr.vm_on = 1;
+            sr.vm_f = fsorted;
+            sr.vm_flb = cb.cseg_lb;
+            sr.vm_db = cb.db;
+            sr.vm_dmi = cb.dmi;
+            sr.vm_dkey = merged;
+        }
         c->s_rec = sd;
         cudaMemcpyAsync(c->h_cst, cb.st, sizeof(CacheState), cudaMemcpyDeviceToHost, st);
     }

@@ -355,13 +355,15 @@ __global__ void __launch_bounds__(MG_THREADS) k_merge_frozen(CacheBufs cb, Scrat
 }
 
 // dynamic units: their position among the segment's frozen ranks (binary search), then their place
+// With the virtual merge (vm) the raster reads the two sorted lists in place: the dynamic unit keeps
+// index j in `merged` and records its merged position j + lo in cb.dmi; nothing frozen is copied.
 __global__ void __launch_bounds__(256) k_merge_dyn(CacheBufs cb, Scratch s, const unsigned long long *fsorted,
                                                    const unsigned long long *dsorted, unsigned long long *merged,
-                                                   int n_seg, int W32)
+                                                   int n_seg, int vm)
 {
     CLS_PDL_WAIT();
     if (s.cnt->overflow) return;
-    if ((long long)cb.cseg_lb[n_seg] + cb.db[n_seg] > s.max_units) return;
+    if (!vm && (long long)cb.cseg_lb[n_seg] + cb.db[n_seg] > s.max_units) return;
     const int Ud = cb.db[n_seg];
     const unsigned fbase = (unsigned)cb.Fcap;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < Ud; j += gridDim.x * blockDim.x) {
@@ -375,7 +377,13 @@ __global__ void __launch_bounds__(256) k_merge_dyn(CacheBufs cb, Scratch s, cons
             if ((unsigned)(fsorted[m] & RK_IDX_MASK) < p) lo = m + 1;
             else hi = m;
         }
-        merged[j + lo] = (key & ~RK_IDX_MASK) | (unsigned long long)(rid + fbase);
+        const unsigned long long gk = (key & ~RK_IDX_MASK) | (unsigned long long)(rid + fbase);
+        if (vm) {
+            merged[j] = gk;
+            cb.dmi[j] = (unsigned)(j + lo);
+        } else {
+            merged[j + lo] = gk;
+        }
     }
 }
 
@@ -640,16 +648,16 @@ void launch_cache_finalize(const StepDims &d, const CacheBufs &cb, const Scratch
 }
 
 void launch_cache_merge(const StepDims &d, const CacheBufs &cb, const Scratch &sd, const unsigned long long *fsorted,
-                        const unsigned long long *dsorted, unsigned long long *merged, cudaStream_t st)
+                        const unsigned long long *dsorted, unsigned long long *merged, bool vm, cudaStream_t st)
 {
     const int n_seg = d.V * d.TY;
     const int W32 = (d.TX + 31) / 32;
     cls_launch(k_dyn_pos, 148 * 4, 256, 0, st, cb, sd);
     cls_launch(k_dyn_q, 148 * 4, 256, 0, st, cb, sd, dsorted);
     cls_launch(k_merge_bounds, (n_seg + 1 + 7) / 8, 256, 0, st, cb, sd, dsorted, n_seg);
-    cls_launch(k_merge_frozen, 148 * 8, MG_THREADS, 0, st, cb, sd, fsorted, dsorted, merged, n_seg, W32);
-    cls_launch(k_merge_dyn, 148 * 4, 256, 0, st, cb, sd, fsorted, dsorted, merged, n_seg, W32);
-    g_launches += 5;
+    if (!vm) cls_launch(k_merge_frozen, 148 * 8, MG_THREADS, 0, st, cb, sd, fsorted, dsorted, merged, n_seg, W32);
+    cls_launch(k_merge_dyn, 148 * 4, 256, 0, st, cb, sd, fsorted, dsorted, merged, n_seg, vm ? 1 : 0);
+    g_launches += vm ? 4 : 5;
 }
 
 }  // namespace cls

@@ -59,10 +59,49 @@ __device__ __forceinline__ void stage(const Scratch &s, unsigned val, int tx, in
 #define RT_SCAN 4    // units tested per thread per round (256 per round)
 #define RT_SLOTS (RT_BATCH + RT_SCAN * RT_THREADS)   // batch + carry slots
 
+// virtual merge (static cache): for the scan window of a round -- [cur, cur + 256) forward, [cur - 256,
+// cur) backward -- the step's own units inside it are marked in a 256-bit map in shared memory (one
+// parallel pass: their merged positions increase with their index, so those inside the window are
+// the <= 256 next ones from the cursor vc.dc), after which each scanned position finds in O(1) whether
+// it is one of them and how many precede it.  pre[w] = marked positions in words < w of the window;
+// returns the index of the first of the step's units at or after the window's start.
+// the merged position of the next of the step's units in the scan direction (none: outside any window)
+template <int DIR>
+__device__ __forceinline__ void vm_next(const Scratch &s, VCur &vc)
+{
+    if (DIR > 0) vc.nm = vc.dc < vc.d1 ? (int)__ldg(s.vm_dmi + vc.dc) : 0x7fffffff;
+    else vc.nm = vc.dc > vc.d0 ? (int)__ldg(s.vm_dmi + vc.dc - 1) : -1;
+}
+
+template <int DIR>
+__device__ __forceinline__ int vm_window(const Scratch &s, VCur &vc, int wbase, const unsigned *s_bm_c, unsigned *s_bm,
+                                         int (&pre)[RT_SCAN * RT_THREADS / 32 + 1])
+{
+    const int tid = threadIdx.x;
+    const int whi = wbase + RT_SCAN * RT_THREADS;
+#pragma unroll
+    for (int r = 0; r < RT_SCAN; r++) {
+        const int j = DIR > 0 ? vc.dc + tid + r * RT_THREADS : vc.dc - 1 - (tid + r * RT_THREADS);
+        if (DIR > 0 ? j < vc.d1 : j >= vc.d0) {
+            const int m = (int)__ldg(s.vm_dmi + j);
+            if (m >= wbase && m < whi) atomicOr(s_bm + ((m - wbase) >> 5), 1u << ((m - wbase) & 31));
+        }
+    }
+    __syncthreads();
+    pre[0] = 0;
+#pragma unroll
+    for (int w = 0; w < RT_SCAN * RT_THREADS / 32; w++) pre[w + 1] = pre[w] + __popc(s_bm_c[w]);
+    const int n = pre[RT_SCAN * RT_THREADS / 32];
+    const int first = DIR > 0 ? vc.dc : vc.dc - n;
+    vc.dc = DIR > 0 ? vc.dc + n : vc.dc - n;
+    vm_next<DIR>(s, vc);
+    return first;
+}
+
 template <int DIR, bool BWD>
 __device__ __forceinline__ int fill_batch(const Scratch &s, int &cur, int end, int &carry, int tx, int ty, float4 *ent,
                                           float2 *sd, int *s_pos, unsigned *s_rid, int *s_wc, int *s_first,
-                                          int *s_clamp)
+                                          int *s_clamp, VCur *vc = nullptr, unsigned *s_bm = nullptr)
 {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned lt = (1u << lane) - 1u;
@@ -94,11 +133,37 @@ __device__ __forceinline__ int fill_batch(const Scratch &s, int &cur, int end, i
     }
     while (nst < RT_BATCH && (DIR > 0 ? cur < end : cur > end)) {
         unsigned cw[RT_SCAN], uv[RT_SCAN];
+        int dfirst = 0, pre[RT_SCAN * RT_THREADS / 32 + 1];
+        bool vdyn = false;   // the window holds some of the step's units (uniform)
+        if (s.vm_on) {
+            const int wbase = DIR > 0 ? cur : cur - RT_SCAN * RT_THREADS;
+            vdyn = DIR > 0 ? vc->nm < wbase + RT_SCAN * RT_THREADS : vc->nm >= wbase;
+            if (vdyn)   // mark them in s_bm (zeroed again at the end of the round)
+                dfirst = vm_window<DIR>(s, *vc, wbase, s_bm, s_bm, pre);
+            else
+                dfirst = vc->dc;
+        }
 #pragma unroll
         for (int k = 0; k < RT_SCAN; k++) {   // all loads first (columns AND record ids): one memory latency per round
             const int u = DIR > 0 ? cur + k * RT_THREADS + tid : cur - 1 - (k * RT_THREADS + tid);
             const bool in = DIR > 0 ? u < end : u >= end;
-            const unsigned long long key = in ? __ldg(s.sukey + u) : (0x3ffull << UK_LO_SHIFT);   // empty if outside
+            unsigned long long key = 0x3ffull << UK_LO_SHIFT;   // empty if outside
+            if (in) {
+                if (!s.vm_on) {
+                    key = __ldg(s.sukey + u);
+                } else if (!vdyn) {   // frozen units only
+                    key = __ldg(s.vm_f + vc->f0 + (u - vc->m0) - (dfirst - vc->d0));
+                } else {
+                    // window offset o = k*64 + tid (forward) or 255 - (k*64 + tid): word 2k + warp or 7 - 2k - warp
+                    const int o = DIR > 0 ? k * RT_THREADS + tid : RT_SCAN * RT_THREADS - 1 - (k * RT_THREADS + tid);
+                    const int w = o >> 5, b = o & 31;
+                    const int pw = DIR > 0 ? (warp ? pre[2 * k + 1] : pre[2 * k])
+                                           : (warp ? pre[RT_SCAN * 2 - 2 - 2 * k] : pre[RT_SCAN * 2 - 1 - 2 * k]);
+                    const unsigned word = s_bm[w];
+                    const int c = dfirst + pw + __popc(word & ((1u << b) - 1u));   // the step's units before u
+                    key = (word >> b) & 1u ? __ldg(s.vm_dkey + c) : __ldg(s.vm_f + vc->f0 + (u - vc->m0) - (c - vc->d0));
+                }
+            }
             cw[k] = (unsigned)(key >> UK_LO_SHIFT) & 0xfffffu;   // lo | hi << 10
             uv[k] = (unsigned)(key & RK_IDX_MASK);               // record id
         }
@@ -128,6 +193,7 @@ __device__ __forceinline__ int fill_batch(const Scratch &s, int &cur, int end, i
         cur = DIR > 0 ? cur + RT_SCAN * RT_THREADS : cur - RT_SCAN * RT_THREADS;
         carry = max(nst + total - RT_BATCH, 0);
         nst = min(nst + total, RT_BATCH);
+        if (vdyn && tid < (RT_SCAN * RT_THREADS) / 32) s_bm[tid] = 0u;   // every thread read it before the sync above
         __syncthreads();
     }
     // stage the batch: RT_BATCH / RT_THREADS independent record loads per thread, issued together
@@ -344,6 +410,7 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
     __shared__ float red[RT_THREADS / 32];
     __shared__ int s_item, s_pos[RT_SLOTS], s_wc[2 * RT_SCAN], s_first, s_clamp, s_lastp[CLS_BLOCK_PIX];
     __shared__ unsigned s_rid[RT_SLOTS];
+    __shared__ unsigned s_bm[(RT_SCAN * RT_THREADS) / 32];   // virtual merge: the window's own units of the step
     __shared__ float s_u8[TARGET ? 256 : 1];   // k -> k / 255 (fp32, IEEE division) for 8-bit targets
     if (s.cnt->overflow) return;
     if (TARGET && targets8)
@@ -354,6 +421,7 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
     const float flx = (float)lx;
     const unsigned long long fy01 = pack2((float)ly, (float)(ly + 4)), fy23 = pack2((float)(ly + 8), (float)(ly + 12));
     const int W = cams.W, H = cams.H, TX = cams.TX, T = cams.T;
+    if (tid < (RT_SCAN * RT_THREADS) / 32) s_bm[tid] = 0u;
     unsigned long long evals = 0;
     while (true) {
         if (tid == 0) s_item = atomicAdd(&s.cnt->fwd_work, 1);
@@ -367,6 +435,11 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         const int seg = v * cams.TY + ty;
         int cur = s.seg_off[seg];
         const int se = s.seg_end[seg];
+        VCur vc{};
+        if (s.vm_on) {
+            vc = VCur{cur, s.vm_flb[seg], s.vm_db[seg], s.vm_db[seg + 1], s.vm_db[seg], 0};
+            vm_next<1>(s, vc);
+        }
         if (tid == 0) s_first = 0x7fffffff;
         const int x = tx * CLS_TILE + lx;
         // T of pixel pairs (p0, p1), (p2, p3) packed for the fp32x2 ops; C* hold the NEGATED colour sums
@@ -391,7 +464,8 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         while (true) {
             const bool live = tmax4(T01, T23) > 0.f;
             if (__syncthreads_count(live) == 0 || (cur >= se && carry == 0)) break;
-            const int cnt = fill_batch<1, false>(s, cur, se, carry, tx, ty, ent, nullptr, s_pos, s_rid, s_wc, &s_first, &s_clamp);
+            const int cnt = fill_batch<1, false>(s, cur, se, carry, tx, ty, ent, nullptr, s_pos, s_rid, s_wc, &s_first,
+                                                 &s_clamp, &vc, s_bm);
             if (s_clamp) comp_batch<true>(ent, cnt, lbase, flx, fy01, fy23, T01, T23, C0, C1, C2, last);
             else comp_batch<false>(ent, cnt, lbase, flx, fy01, fy23, T01, T23, C0, C1, C2, last);
 #pragma unroll
@@ -635,6 +709,7 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
     __shared__ float2 sd[RT_BATCH];    // tile-local 2D mean (dx0, dy0) in fp32
     __shared__ int s_item, s_maxlast, s_pos[RT_SLOTS], s_wc[2 * RT_SCAN];
     __shared__ unsigned s_rid[RT_SLOTS];
+    __shared__ unsigned s_bm[(RT_SCAN * RT_THREADS) / 32];   // virtual merge window map
     if (s.cnt->overflow) return;
     const int n_items = s.cnt->n_items;
     const int A = s.cnt->A;
@@ -643,6 +718,7 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
     const float flx = (float)lx;
     const int W = cams.W, H = cams.H, TX = cams.TX, T = cams.T;
     const float ik = (float)(1.0 / CLS_KAPPA);
+    if (tid < (RT_SCAN * RT_THREADS) / 32) s_bm[tid] = 0u;
     unsigned long long evals = 0;
     while (true) {
         if (tid == 0) {
@@ -705,9 +781,28 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         const f2_t fyp[2] = {pack2((float)ly, (float)(ly + 4)), pack2((float)(ly + 8), (float)(ly + 12))};
         // reverse walk over the row segment [first, end): batches of covering units, descending
         int cur = end, carry = 0;
+        VCur vc{};
+        if (s.vm_on) {   // the dynamic cursor at `end`: the step's units with merged position < end
+            const int seg = v * cams.TY + ty;
+            vc = VCur{s.seg_off[seg], s.vm_flb[seg], s.vm_db[seg], s.vm_db[seg + 1], 0, 0};
+            int lo = vc.d0, hi = vc.d1;   // 32-ary search per warp: log32 of the segment's unit count rounds
+            while (hi - lo > 32) {
+                const int step = (hi - lo + 31) >> 5;
+                const int p = lo + lane * step;
+                const bool less = p < hi && (int)__ldg(s.vm_dmi + p) < end;
+                const int nb = __popc(__ballot_sync(0xffffffffu, less));   // probes below end
+                const int nlo = nb ? lo + (nb - 1) * step + 1 : lo;
+                hi = min(lo + nb * step, hi);
+                lo = nlo;
+            }
+            const int p = lo + lane;
+            vc.dc = lo + __popc(__ballot_sync(0xffffffffu, p < hi && (int)__ldg(s.vm_dmi + p) < end));
+            vm_next<-1>(s, vc);
+        }
         while (cur > first || carry > 0) {
             __syncthreads();
-            const int cnt = fill_batch<-1, true>(s, cur, first, carry, tx, ty, ent, sd, s_pos, s_rid, s_wc, nullptr, nullptr);
+            const int cnt = fill_batch<-1, true>(s, cur, first, carry, tx, ty, ent, sd, s_pos, s_rid, s_wc, nullptr, nullptr,
+                                                 &vc, s_bm);
             // walked (pixel, entry) pairs of this batch: s_pos is descending, so the entries above a
             // pixel's last composited one form a prefix (binary search per pixel)
 #pragma unroll
@@ -897,8 +992,16 @@ __global__ void k_debug_tile_list(Scratch s, CacheBufs cb, int cached, int TY, i
     if (blockIdx.x != 0 || threadIdx.x != 0) return;
     const int tx = tile % TX, ty = tile / TX, seg = view * TY + ty;
     int k = 0;
+    int c = s.vm_on ? s.vm_db[seg] : 0;   // virtual merge: the step's units before u
     for (int u = s.seg_off[seg]; u < s.seg_end[seg]; u++) {
-        const unsigned long long key = s.sukey[u];
+        unsigned long long key;
+        if (!s.vm_on) {
+            key = s.sukey[u];
+        } else if (c < s.vm_db[seg + 1] && (int)s.vm_dmi[c] == u) {
+            key = s.vm_dkey[c++];
+        } else {
+            key = s.vm_f[s.vm_flb[seg] + (u - s.seg_off[seg]) - (c - s.vm_db[seg])];
+        }
         const int lo = (int)((key >> UK_LO_SHIFT) & 0x3ffu), hi = (int)((key >> UK_HI_SHIFT) & 0x3ffu);
         if (lo <= tx && tx <= hi) {
             if (k < max) out[k] = debug_gid(s, cb, cached != 0, (unsigned)(key & RK_IDX_MASK));

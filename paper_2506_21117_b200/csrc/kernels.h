@@ -62,7 +62,7 @@ void launch_cache_build(const Params &g, const StepDims &d, const CamSet &cams, 
                         const Scratch &s, Scratch &sb, unsigned long long **fsorted, cudaStream_t st);
 void launch_cache_finalize(const StepDims &d, const CacheBufs &cb, const Scratch &s, cudaStream_t st);
 void launch_cache_merge(const StepDims &d, const CacheBufs &cb, const Scratch &sd, const unsigned long long *fsorted,
-                        const unsigned long long *dsorted, unsigned long long *merged, cudaStream_t st);
+                        const unsigned long long *dsorted, unsigned long long *merged, bool vm, cudaStream_t st);
 
 // (4) forward compositing + fused L1                           (k_raster.cu)
 void launch_fwd(const StepDims &d, const CamSet &cams, const Scratch &s, const void *targets, bool targets_u8,
@@ -138,6 +138,7 @@ inline void per_device_once(std::atomic<unsigned long long> &done, F &&set_attr)
 
 extern int64_t g_launches;   // kernels launched by this process through libcls (host counter)
 extern bool g_pdl;           // programmatic dependent launch on (CLS_NO_PDL=1 turns it off)
+extern bool g_vmerge;        // static cache: virtual merge in the raster (CLS_NO_VMERGE=1 materialises it)
 
 // Every kernel of libcls starts with CLS_PDL_WAIT() and is launched by cls_launch with programmatic
 // stream serialization: a kernel's blocks may be scheduled while its predecessor in the stream drains,
