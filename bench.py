@@ -384,6 +384,11 @@ def run_ours(args):
                 gbs = tr["bytes"] / t_s / 1e9
                 r.update({"hbm_gbs": round(gbs, 1), "hbm_frac": round(gbs / hbm, 4), "hbm_peak": hbm,
                           "hbm_source": f"ncu dram bytes per launch ({tr['source']}) / this run's event time"})
+            if grp == "fwd_raster" and stats.get("n_fwd_exec"):
+                # the (pixel, entry) evaluations executed: a warp walks on until all its pixels terminated;
+                # the roofline's unit stays the tile-list evaluation of SURVEY §8(d)
+                r["executed_evaluations"] = int(stats["n_fwd_exec"])
+                r["executed_frac"] = round(stats["n_fwd_exec"] / max(ev, 1.0), 4)
             raster[grp] = r
         out = {
             "metric": "local-opt steps/s (fwd+bwd+masked Adam)",
@@ -416,7 +421,7 @@ def run_ours(args):
             "kernels_ms_per_step": {k: round(v["ms"] / args.steps, 4) for k, v in per.items()},
             "kernel_rates": groups,
             "counts": {k: stats[k] for k in ("n_records", "n_pairs", "n_items", "max_list", "n_units",
-                                             "n_fwd_evals", "n_bwd_evals", "n_candidates", "n_kept_pairs", "n_stage1", "n_tested", "n_live_units")},
+                                             "n_fwd_evals", "n_fwd_exec", "n_bwd_evals", "n_candidates", "n_kept_pairs", "n_stage1", "n_tested", "n_live_units")},
         }
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(sc, args.cpu_views)

@@ -146,6 +146,9 @@ typedef struct {
     int64_t cache_units;       /* their live (record, tile row) units */
     int64_t cache_rows;        /* rows projected every step (S0) */
     int64_t n_tie_runs;        /* runs of > 32 records with equal (view, depth) keys, ordered by index (R13) */
+    int64_t n_fwd_exec;        /* (pixel, entry) evaluations the forward executed: entries walked by each
+                                  warp x its pixels (a warp walks on until all its pixels terminated;
+                                  compare n_fwd_evals) */
 } cls_stats_t;
 
 #define CLS_PROF_GROUPS 20

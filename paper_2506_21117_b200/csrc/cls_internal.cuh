@@ -69,6 +69,7 @@ struct Counters {
     int active_tiles[CLS_MAX_VIEWS];
     unsigned long long fwd_evals;   // (pixel, list entry) evaluations of the forward
     unsigned long long bwd_evals;   // (pixel, list entry) evaluations of the backward walk
+    unsigned long long fwd_exec;    // (pixel, entry) evaluations the forward executed (entries walked x the warp's pixels)
 };
 
 // One (Gaussian, view) record, 64 B = two full 32 B sectors per random access.

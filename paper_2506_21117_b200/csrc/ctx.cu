@@ -733,6 +733,7 @@ cls_status cls_stats(cls_ctx *c, cls_stats_t *out)
     cudaMemcpy(&bev, &c->s.cnt->bwd_evals, sizeof bev, cudaMemcpyDeviceToHost);
     out->n_bwd_evals = (int64_t)bev;
     out->n_tie_runs = h.n_long_runs;
+    out->n_fwd_exec = (int64_t)h.fwd_exec;
     if (c->cache_alloc) {
         const CacheState &k = *c->h_cst;
         out->cache_mode = k.mode;

@@ -358,12 +358,13 @@ __device__ __forceinline__ void comp_pair(unsigned long long fy, float na2, floa
 
 // one staged batch into the thread's 4 pixels, entries in pairs (the batch is padded to even length)
 template <bool CLAMP>
-__device__ __forceinline__ void comp_batch(const float4 *ent, int cnt, int lbase, float flx, unsigned long long fy01,
-                                           unsigned long long fy23, unsigned long long &T01, unsigned long long &T23,
-                                           float (&C0)[RT_PX], float (&C1)[RT_PX], float (&C2)[RT_PX],
-                                           int (&last)[RT_PX])
+__device__ __forceinline__ int comp_batch(const float4 *ent, int cnt, int lbase, float flx, unsigned long long fy01,
+                                          unsigned long long fy23, unsigned long long &T01, unsigned long long &T23,
+                                          float (&C0)[RT_PX], float (&C1)[RT_PX], float (&C2)[RT_PX],
+                                          int (&last)[RT_PX])
 {
-    for (int k = 0; k < cnt; k += 4) {   // 4 entries per iteration (the batch is padded to a multiple of 4)
+    int k = 0;
+    for (; k < cnt; k += 4) {   // 4 entries per iteration (the batch is padded to a multiple of 4)
         // warp-level exit once all its pixels terminated (checked every 4 entries)
         if (!__any_sync(0xffffffffu, tmax4(T01, T23) > 0.f)) break;
 #pragma unroll
@@ -377,6 +378,7 @@ __device__ __forceinline__ void comp_batch(const float4 *ent, int cnt, int lbase
                              C1[3], C2[3], last[2], last[3]);
         }
     }
+    return k;   // entries walked by the warp
 }
 
 __device__ __forceinline__ float block_sum(float v, float *red)
@@ -422,7 +424,7 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
     const unsigned long long fy01 = pack2((float)ly, (float)(ly + 4)), fy23 = pack2((float)(ly + 8), (float)(ly + 12));
     const int W = cams.W, H = cams.H, TX = cams.TX, T = cams.T;
     if (tid < (RT_SCAN * RT_THREADS) / 32) s_bm[tid] = 0u;
-    unsigned long long evals = 0;
+    unsigned long long evals = 0, walked = 0;
     while (true) {
         if (tid == 0) s_item = atomicAdd(&s.cnt->fwd_work, 1);
         __syncthreads();
@@ -466,8 +468,8 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
             if (__syncthreads_count(live) == 0 || (cur >= se && carry == 0)) break;
             const int cnt = fill_batch<1, false>(s, cur, se, carry, tx, ty, ent, nullptr, s_pos, s_rid, s_wc, &s_first,
                                                  &s_clamp, &vc, s_bm);
-            if (s_clamp) comp_batch<true>(ent, cnt, lbase, flx, fy01, fy23, T01, T23, C0, C1, C2, last);
-            else comp_batch<false>(ent, cnt, lbase, flx, fy01, fy23, T01, T23, C0, C1, C2, last);
+            walked += (unsigned)(s_clamp ? comp_batch<true>(ent, cnt, lbase, flx, fy01, fy23, T01, T23, C0, C1, C2, last)
+                                         : comp_batch<false>(ent, cnt, lbase, flx, fy01, fy23, T01, T23, C0, C1, C2, last));
 #pragma unroll
             for (int p = 0; p < RT_PX; p++)   // segment position of a last entry of this batch
                 if (last[p] >= lbase) s_lastp[tid + p * RT_THREADS] = s_pos[last[p] - lbase];
@@ -537,7 +539,10 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         }
     }
     for (int o = 16; o > 0; o >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, o);
-    if ((tid & 31) == 0 && evals) atomicAdd(&s.cnt->fwd_evals, evals);
+    if ((tid & 31) == 0) {
+        if (evals) atomicAdd(&s.cnt->fwd_evals, evals);
+        if (walked) atomicAdd(&s.cnt->fwd_exec, walked * (32ull * RT_PX));   // the warp's 128 pixels per entry walked
+    }
 }
 
 // host-resident targets: the fused-L1 epilogue of k_fwd, run once the gathered targets arrived
