@@ -128,6 +128,8 @@ struct CacheBufs {      // the cache's device buffers (passed by value)
     int4 *dcinfo;       // [Dcap] (Gaussian index, view, depth key, tile rows)
     long long Fcap, Dcap, maxN, Dunits;
     int dilate;         // tiles added around every active rect
+    int *tl_foff;       // [V*T + 1] per-tile ranges of the frozen tile lists
+    int2 *tl_drng;      // [max items] per-item ranges of the step's tile lists
 };
 
 // all scratch of a ctx (device pointers), passed by value to kernels
@@ -192,6 +194,15 @@ struct Scratch {
     const int *vm_db;                   // [V*TY + 1] the step's units' segment lower bounds
     const unsigned *vm_dmi;             // merged position of each of the step's units
     const unsigned long long *vm_dkey;  // the step's units with their global record ids
+    // static cache with exact per-tile lists (k_tiles.cu): a tile's list is the merge of its frozen list
+    // (record ids = ranks, ascending) and the step's list ((rank position among the frozen) << 32 | id);
+    // a step's entry of position p precedes the frozen record f iff p <= f.  List positions (px_last,
+    // first_active) are then list indices.
+    int tl_on;
+    const unsigned long long *tl_f;     // frozen pairs sorted by tile: (tile << 32 | frozen record id)
+    const int *tl_foff;                 // [V*T + 1] each tile's range of tl_f
+    const unsigned long long *tl_d;     // the step's pairs of the active tiles, sorted by tile
+    const int2 *tl_drng;                // [n_items] each work item's range of tl_d
 };
 
 // per-tile cursor of the virtual merge (uniform over the CTA)

@@ -42,6 +42,7 @@ struct cls_ctx {
     unsigned *d_drowmask = nullptr;
     int4 *d_dbbox = nullptr;
     unsigned long long *d_cukey = nullptr, *d_cukey_alt = nullptr;
+    const unsigned long long *tl_fsorted = nullptr;   // frozen tile-list pairs (one of d_cukey / d_cukey_alt)
     long long cache_P = 0;
     CacheState *h_cst = nullptr;   // pinned copy of the cache state after the last fwd
     std::vector<unsigned char> cache_sig;   // what the build depends on (host check -> invalidation)
@@ -190,7 +191,7 @@ cls_status cls_destroy(cls_ctx *c)
         if (p) cudaFree(p);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     void *cp[] = {c->cb.st, c->cb.ccnt, c->cb.dyn_of, c->cb.s0, c->cb.flag, c->cb.excl, c->cb.scan_status, c->cb.dmask,
-                  c->cb.dmdiff, c->cb.urec, c->cb.cfvd, c->cb.cfgid, c->cb.cseg_lb, c->cb.dpos, c->cb.db, c->cb.dq, c->cb.dmi, c->cb.mitems, c->cb.dlist, c->cb.dM, c->cb.dcand, c->cb.dcinfo, c->d_dsat,
+                  c->cb.dmdiff, c->cb.urec, c->cb.cfvd, c->cb.cfgid, c->cb.cseg_lb, c->cb.dpos, c->cb.db, c->cb.dq, c->cb.dmi, c->cb.mitems, c->cb.dlist, c->cb.dM, c->cb.dcand, c->cb.dcinfo, c->cb.tl_foff, c->cb.tl_drng, c->d_dsat,
                   c->d_drowmask, c->d_dbbox, c->d_cukey, c->d_cukey_alt};
     for (void *p : cp)
         if (p) cudaFree(p);
@@ -290,7 +291,7 @@ static cls_status cache_allocate(cls_ctx *c)
               dalloc(&c->d_drowmask, V * c->maxTY * ((c->maxTX + 31) / 32)) && dalloc(&c->d_dbbox, V) &&
               dalloc(&c->d_cukey, P) && dalloc(&c->d_cukey_alt, P) && dalloc(&cb.dq, P) && dalloc(&cb.dmi, P) && dalloc(&cb.dlist, N) &&
               dalloc(&cb.dM, N * 12) && dalloc(&cb.dcand, (size_t)Dcap) && dalloc(&cb.dcinfo, (size_t)Dcap) &&
-              dalloc(&cb.mitems, P / 4096 + NSEG + 1) &&
+              dalloc(&cb.mitems, P / 4096 + NSEG + 1) && dalloc(&cb.tl_foff, VT + 1) && dalloc(&cb.tl_drng, VT) &&
               cudaMallocHost((void **)&c->h_cst, sizeof(CacheState)) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
@@ -539,13 +540,15 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
             if (cudaStreamBeginCaptureToGraph(c->body_stream, body, nullptr, nullptr, 0,
                                               cudaStreamCaptureModeRelaxed) != cudaSuccess)
                 return fail(c, CLS_ERR_CUDA, "body capture: %s", cudaGetErrorString(cudaGetLastError()));
-            launch_cache_build(p, d, cs, cb, s, sb, &fsorted, c->body_stream);
+            launch_cache_build(p, d, cs, cb, s, sb, &fsorted, c->body_stream, g_tiles ? &c->tl_fsorted : nullptr);
             cudaGraph_t out_body = nullptr;
             if (cudaStreamEndCapture(c->body_stream, &out_body) != cudaSuccess)
                 return fail(c, CLS_ERR_CUDA, "body capture end: %s", cudaGetErrorString(cudaGetLastError()));
             cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies);
         } else {
-            run(c, P_CACHE_BUILD, st, [&] { launch_cache_build(p, d, cs, cb, s, sb, &fsorted, st); });
+            run(c, P_CACHE_BUILD, st, [&] {
+                launch_cache_build(p, d, cs, cb, s, sb, &fsorted, st, g_tiles ? &c->tl_fsorted : nullptr);
+            });
         }
         launch_cache_finalize(d, cb, s, st);
         Scratch sd = s;   // the step's own records: S0 x views, ids after the frozen ones
@@ -559,12 +562,28 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
         unsigned long long *dsorted = nullptr;
         run(c, P_PAIRSORT, st, [&] { dsorted = launch_unit_sort(d, sd, st); });
         unsigned long long *merged = dsorted == s.ukey ? s.ukey_alt : s.ukey;
-        run(c, P_CACHE_MERGE, st, [&] { launch_cache_merge(d, cb, sd, fsorted, dsorted, merged, g_vmerge, st); });
+        const unsigned long long *tl_d = nullptr;
+        if (g_tiles) {   // exact per-tile lists: the step's own pairs of the active tiles, merged in the raster
+            run(c, P_CACHE_MERGE, st, [&] {
+                launch_dyn_pos(cb, sd, st);
+                tl_d = launch_tile_lists(d, dsorted, &s.cnt->n_units32, s.rowmask, merged, dsorted, s.max_units,
+                                         (unsigned)cb.Fcap, s.cnt, cb.dq, cb.dmi, s.st_scan, s.rs_counts, s.rs_totals,
+                                         nullptr, s.items, &s.cnt->n_items, cb.tl_drng, cb.dpos, &s.cnt->overflow, st);
+            });
+        } else {
+            run(c, P_CACHE_MERGE, st, [&] { launch_cache_merge(d, cb, sd, fsorted, dsorted, merged, g_vmerge, st); });
+        }
         sr = s;
         sr.rec = cb.urec;
         sr.rskey = sd.rskey;
         sr.sukey = merged;
-        if (g_vmerge) {   // the raster merges the frozen and the step's sorted units on the fly
+        if (g_tiles) {
+            sr.tl_on = 1;
+            sr.tl_f = c->tl_fsorted;
+            sr.tl_foff = cb.tl_foff;
+            sr.tl_d = tl_d;
+            sr.tl_drng = cb.tl_drng;
+        } else if (g_vmerge) {   // the raster merges the frozen and the step's sorted units on the fly
             sr.vm_on = 1;
             sr.vm_f = fsorted;
             sr.vm_flb = cb.cseg_lb;

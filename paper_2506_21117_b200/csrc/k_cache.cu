@@ -610,7 +610,8 @@ void launch_cache_check(const CacheBufs &cb, const StepDims &d, const Scratch &s
 }
 
 void launch_cache_build(const Params &g, const StepDims &d, const CamSet &cams, const CacheBufs &cb,
-                        const Scratch &s, Scratch &sb, unsigned long long **fsorted, cudaStream_t st)
+                        const Scratch &s, Scratch &sb, unsigned long long **fsorted, cudaStream_t st,
+                        const unsigned long long **tl_sorted)
 {
     // S0 := (S0 if valid) u O^t
     cls_launch(k_s0_flags, 148 * 4, 256, 0, st, cb, s, d.n);
@@ -635,8 +636,16 @@ void launch_cache_build(const Params &g, const StepDims &d, const CamSet &cams, 
     const int n_seg = d.V * d.TY;
     *fsorted = launch_unit_sort(d, su, st);
     cls_launch(k_cache_seglb, (n_seg + 256) / 256, 256, 0, st, cb, *fsorted, n_seg);
-    cls_launch(k_cache_items, 1, 1024, 0, st, cb, n_seg);
-    g_launches += 2;
+    g_launches++;
+    if (tl_sorted) {   // exact per-tile frozen lists against the dilated mask (k_tiles.cu); the units are consumed
+        unsigned long long *other = *fsorted == su.ukey ? su.ukey_alt : su.ukey;
+        *tl_sorted = launch_tile_lists(d, *fsorted, &su.cnt->n_units32, su.rowmask, other, *fsorted, su.max_units, 0u,
+                                       su.cnt, cb.dq, cb.dmi, su.st_scan, su.rs_counts, su.rs_totals, cb.tl_foff, nullptr,
+                                       nullptr, nullptr, nullptr, &su.cnt->overflow, st);
+    } else {
+        cls_launch(k_cache_items, 1, 1024, 0, st, cb, n_seg);
+        g_launches++;
+    }
 }
 
 // every step, after the (possibly skipped) build: the build's outcome into the cache state, and a
@@ -644,6 +653,12 @@ void launch_cache_build(const Params &g, const StepDims &d, const CamSet &cams, 
 void launch_cache_finalize(const StepDims &d, const CacheBufs &cb, const Scratch &s, cudaStream_t st)
 {
     cls_launch(k_cache_finalize, 1, 1, 0, st, cb, s, d.V * d.TY);
+    g_launches++;
+}
+
+void launch_dyn_pos(const CacheBufs &cb, const Scratch &sd, cudaStream_t st)
+{
+    cls_launch(k_dyn_pos, 148 * 4, 256, 0, st, cb, sd);
     g_launches++;
 }
 

@@ -14,6 +14,7 @@ namespace cls {
 int64_t g_launches = 0;
 bool g_pdl = getenv("CLS_NO_PDL") == nullptr;
 bool g_vmerge = getenv("CLS_NO_VMERGE") == nullptr;
+bool g_tiles = getenv("CLS_NO_TL") == nullptr;
 
 #define MEMBER_THREADS 256
 #define MEMBER_ITEMS 8

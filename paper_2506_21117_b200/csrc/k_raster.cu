@@ -98,6 +98,43 @@ __device__ __forceinline__ int vm_window(const Scratch &s, VCur &vc, int wbase, 
     return first;
 }
 
+// stage the batch: RT_BATCH / RT_THREADS independent record loads per thread, issued together
+template <bool BWD>
+__device__ __forceinline__ int stage_batch(const Scratch &s, int nst, int tx, int ty, float4 *ent, float2 *sd,
+                                           const int *s_pos, const unsigned *s_rid, int *s_first, int *s_clamp)
+{
+    const int tid = threadIdx.x, lane = tid & 31;
+    bool cl = false;
+    int fmin = 0x7fffffff;
+#pragma unroll
+    for (int r = 0; r < RT_BATCH / RT_THREADS; r++) {
+        const int slot = tid + r * RT_THREADS;
+        if (slot < nst) {
+            const unsigned val = s_rid[slot];
+            stage(s, val, tx, ty, ent[3 * slot], ent[3 * slot + 1], ent[3 * slot + 2]);
+            if (!BWD) {
+                cl |= ent[3 * slot + 1].z > 0.98999f;   // alpha's 0.99 clamp may bind
+                if (__float_as_int(ent[3 * slot + 2].w) >= 0) fmin = min(fmin, s_pos[slot]);   // active ordinal
+            } else {
+                const float4 xy = s.rec[val].xy;
+                sd[slot] = make_float2(__double2float_rn(((double)xy.x - (double)(CLS_TILE * tx)) + (double)xy.y),
+                                       __double2float_rn(((double)xy.z - (double)(CLS_TILE * ty)) + (double)xy.w));
+            }
+        }
+    }
+    if (!BWD) {
+        if (tid == 0) *s_clamp = 0;
+        const int npad = (4 - (nst & 3)) & 3;   // pad to a multiple of 4 entries (opacity 0: never composited)
+        if (tid < 3 * npad) ent[3 * nst + tid] = make_float4(0.f, 0.f, 0.f, 0.f);
+        __syncthreads();
+        if (cl) *s_clamp = 1;
+        fmin = __reduce_min_sync(0xffffffffu, fmin);
+        if (lane == 0 && fmin != 0x7fffffff) atomicMin(s_first, fmin);
+    }
+    __syncthreads();
+    return nst;
+}
+
 template <int DIR, bool BWD>
 __device__ __forceinline__ int fill_batch(const Scratch &s, int &cur, int end, int &carry, int tx, int ty, float4 *ent,
                                           float2 *sd, int *s_pos, unsigned *s_rid, int *s_wc, int *s_first,
@@ -196,36 +233,120 @@ __device__ __forceinline__ int fill_batch(const Scratch &s, int &cur, int end, i
         if (vdyn && tid < (RT_SCAN * RT_THREADS) / 32) s_bm[tid] = 0u;   // every thread read it before the sync above
         __syncthreads();
     }
-    // stage the batch: RT_BATCH / RT_THREADS independent record loads per thread, issued together
-    bool cl = false;
-    int fmin = 0x7fffffff;
-#pragma unroll
-    for (int r = 0; r < RT_BATCH / RT_THREADS; r++) {
-        const int slot = tid + r * RT_THREADS;
-        if (slot < nst) {
-            const unsigned val = s_rid[slot];
-            stage(s, val, tx, ty, ent[3 * slot], ent[3 * slot + 1], ent[3 * slot + 2]);
-            if (!BWD) {
-                cl |= ent[3 * slot + 1].z > 0.98999f;   // alpha's 0.99 clamp may bind
-                if (__float_as_int(ent[3 * slot + 2].w) >= 0) fmin = min(fmin, s_pos[slot]);   // active ordinal
-            } else {
-                const float4 xy = s.rec[val].xy;
-                sd[slot] = make_float2(__double2float_rn(((double)xy.x - (double)(CLS_TILE * tx)) + (double)xy.y),
-                                       __double2float_rn(((double)xy.z - (double)(CLS_TILE * ty)) + (double)xy.w));
-            }
+    return stage_batch<BWD>(s, nst, tx, ty, ent, sd, s_pos, s_rid, s_first, s_clamp);
+}
+
+// ---------------------------------------------------------------------------
+// Exact per-tile lists (static cache, k_tiles.cu): the tile's frozen list F (record ids = ranks f,
+// ascending) and the step's list D (rank positions p, non-decreasing, with their record ids) are merged
+// on the fly: d precedes f iff p <= f, the (depth, index) order of R13.  A batch takes the next
+// RT_BATCH merged entries: the first RT_BATCH of the merge lie in the first RT_BATCH of each list, so
+// both windows are loaded and each element's merged rank inside them is its own index plus the number
+// of the other window's elements before it (a binary search in shared memory).  No scan, no carry:
+// s_pos holds list indices.  The windows sit in the upper slots of s_rid / s_pos.
+// ---------------------------------------------------------------------------
+template <int DIR>
+__device__ __forceinline__ int tl_merge(const Scratch &s, int fw0, int nf, int dw0, int nd, int nst, unsigned *s_rid,
+                                        int *s_pos, int *s_cnt)
+{
+    const int tid = threadIdx.x, lane = tid & 31;
+    unsigned *s_fw = s_rid + RT_BATCH, *s_dr = s_rid + 2 * RT_BATCH;
+    unsigned *s_dp = reinterpret_cast<unsigned *>(s_pos + RT_BATCH);
+    for (int r = tid; r < nf; r += RT_THREADS) s_fw[r] = (unsigned)__ldg(s.tl_f + fw0 + r);
+    for (int r = tid; r < nd; r += RT_THREADS) {
+        const unsigned long long k = __ldg(s.tl_d + dw0 + r);
+        s_dr[r] = (unsigned)k;
+        s_dp[r] = (unsigned)(k >> 32);
+    }
+    if (tid == 0) *s_cnt = 0;
+    __syncthreads();
+    int myf = 0;
+    for (int i = tid; i < nf; i += RT_THREADS) {
+        const unsigned f = s_fw[i];
+        int lo = 0, hi = nd;   // the step's entries with p <= f precede f
+        while (lo < hi) {
+            const int m = (lo + hi) >> 1;
+            if (s_dp[m] <= f) lo = m + 1;
+            else hi = m;
+        }
+        const int r = DIR > 0 ? i + lo : (nf - 1 - i) + (nd - lo);   // forward: rank; backward: rank from the top
+        if (r < nst) {
+            s_rid[r] = f;
+            myf++;
         }
     }
-    if (!BWD) {
-        if (tid == 0) *s_clamp = 0;
-        const int npad = (4 - (nst & 3)) & 3;   // pad to a multiple of 4 entries (opacity 0: never composited)
-        if (tid < 3 * npad) ent[3 * nst + tid] = make_float4(0.f, 0.f, 0.f, 0.f);
-        __syncthreads();
-        if (cl) *s_clamp = 1;
-        fmin = __reduce_min_sync(0xffffffffu, fmin);
-        if (lane == 0 && fmin != 0x7fffffff) atomicMin(s_first, fmin);
+    for (int j = tid; j < nd; j += RT_THREADS) {
+        const unsigned p = s_dp[j];
+        int lo = 0, hi = nf;   // frozen entries with f < p precede d
+        while (lo < hi) {
+            const int m = (lo + hi) >> 1;
+            if (s_fw[m] < p) lo = m + 1;
+            else hi = m;
+        }
+        const int r = DIR > 0 ? j + lo : (nd - 1 - j) + (nf - lo);
+        if (r < nst) s_rid[r] = s_dr[j];
     }
+    myf = __reduce_add_sync(0xffffffffu, myf);
+    if (lane == 0 && myf) atomicAdd(s_cnt, myf);
     __syncthreads();
-    return nst;
+    return *s_cnt;   // frozen entries among the staged ones
+}
+
+// forward: the next batch from cursors (fc, dc) of the lists ending at (fe, de); lbase = list index of fc + dc
+template <bool BWD>
+__device__ __forceinline__ int fill_tl(const Scratch &s, int &fc, int fe, int &dc, int de, int lbase, int tx, int ty,
+                                       float4 *ent, float2 *sd, int *s_pos, unsigned *s_rid, int *s_wc, int *s_first,
+                                       int *s_clamp)
+{
+    const int nf = min(RT_BATCH, fe - fc), nd = min(RT_BATCH, de - dc);
+    const int nst = min(RT_BATCH, nf + nd);
+    const int sf = tl_merge<1>(s, fc, nf, dc, nd, nst, s_rid, s_pos, s_wc);
+    for (int r = threadIdx.x; r < nst; r += RT_THREADS) s_pos[r] = lbase + r;
+    fc += sf;
+    dc += nst - sf;
+    return stage_batch<BWD>(s, nst, tx, ty, ent, sd, s_pos, s_rid, s_first, s_clamp);
+}
+
+// backward: the batch below list index cur (down to `first`, inclusive), cursors (fc, dc) at cur, lists
+// starting at (f0, d0); staged in descending list order
+__device__ __forceinline__ int fill_tl_bwd(const Scratch &s, int &fc, int f0, int &dc, int d0, int &cur, int first,
+                                           int tx, int ty, float4 *ent, float2 *sd, int *s_pos, unsigned *s_rid,
+                                           int *s_wc)
+{
+    const int nf = min(RT_BATCH, fc - f0), nd = min(RT_BATCH, dc - d0);
+    const int nst = min(RT_BATCH, cur - first);
+    const int sf = tl_merge<-1>(s, fc - nf, nf, dc - nd, nd, nst, s_rid, s_pos, s_wc);
+    for (int r = threadIdx.x; r < nst; r += RT_THREADS) s_pos[r] = cur - 1 - r;
+    fc -= sf;
+    dc -= nst - sf;
+    cur -= nst;
+    return stage_batch<true>(s, nst, tx, ty, ent, sd, s_pos, s_rid, nullptr, nullptr);
+}
+
+// the split of a tile's merged list at list index m: fi frozen and m - fi of the step's entries come
+// first.  Smallest fi in [max(0, m - nD), min(m, nF)] with (di = m - fi == 0 || fi == nF ||
+// p[di - 1] <= f[fi]) (monotone in fi); one warp, 32 probes per round.
+__device__ __forceinline__ int tl_split(const Scratch &s, int f0, int nF, int d0, int nD, int m)
+{
+    const int lane = threadIdx.x & 31;
+    int lo = max(0, m - nD), hi = min(m, nF);
+    while (lo < hi) {
+        const int x = lo + (int)(((long long)(hi - lo) * lane) >> 5);   // probes in [lo, hi)
+        const int di = m - x;
+        const bool ok = di == 0 || x == nF ||
+                        (unsigned)(__ldg(s.tl_d + d0 + di - 1) >> 32) <= (unsigned)__ldg(s.tl_f + f0 + x);
+        const unsigned b = __ballot_sync(0xffffffffu, ok);
+        if (b == 0u) {
+            lo = __shfl_sync(0xffffffffu, x, 31) + 1;
+        } else {
+            const int l1 = __ffs(b) - 1;
+            const int xl = __shfl_sync(0xffffffffu, x, l1);
+            const int xp = __shfl_sync(0xffffffffu, x, l1 > 0 ? l1 - 1 : 0);
+            hi = xl;
+            if (l1 > 0) lo = xp + 1;
+        }
+    }
+    return lo;
 }
 
 __device__ __forceinline__ unsigned long long pack2(float a, float b)
@@ -402,7 +523,7 @@ __device__ __forceinline__ float block_sum(float v, float *red)
 // every later T (1 - alpha) is negative, so it re-takes the termination branch and never
 // composites again -- no per-pixel "done" flags, the warp stays converged.
 // ---------------------------------------------------------------------------
-template <bool TARGET, bool IMAGE>
+template <bool TARGET, bool IMAGE, bool TL>
 __global__ void __launch_bounds__(RT_THREADS, 12)
 k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ targets,
       const unsigned char *__restrict__ targets8, bool staged, float *__restrict__ images, float loss_scale, float3 bg)
@@ -435,12 +556,22 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         const int v = e / T, t = e - v * T;
         const int tx = t % TX, ty = t / TX;
         const int seg = v * cams.TY + ty;
-        int cur = s.seg_off[seg];
-        const int se = s.seg_end[seg];
+        int cur = 0, se = 0;   // row-segment scan (or, TL: the two lists' cursors and ends)
+        int fc = 0, fe = 0, dc = 0, de = 0;
         VCur vc{};
-        if (s.vm_on) {
-            vc = VCur{cur, s.vm_flb[seg], s.vm_db[seg], s.vm_db[seg + 1], s.vm_db[seg], 0};
-            vm_next<1>(s, vc);
+        if (TL) {
+            fc = s.tl_foff[e];
+            fe = s.tl_foff[e + 1];
+            const int2 dr = s.tl_drng[item];
+            dc = dr.x;
+            de = dr.y;
+        } else {
+            cur = s.seg_off[seg];
+            se = s.seg_end[seg];
+            if (s.vm_on) {
+                vc = VCur{cur, s.vm_flb[seg], s.vm_db[seg], s.vm_db[seg + 1], s.vm_db[seg], 0};
+                vm_next<1>(s, vc);
+            }
         }
         if (tid == 0) s_first = 0x7fffffff;
         const int x = tx * CLS_TILE + lx;
@@ -465,13 +596,15 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         int carry = 0;   // ranked units carried to the next batch
         while (true) {
             const bool live = tmax4(T01, T23) > 0.f;
-            if (__syncthreads_count(live) == 0 || (cur >= se && carry == 0)) break;
-            const int cnt = fill_batch<1, false>(s, cur, se, carry, tx, ty, ent, nullptr, s_pos, s_rid, s_wc, &s_first,
-                                                 &s_clamp, &vc, s_bm);
+            if (__syncthreads_count(live) == 0 || (TL ? (fc >= fe && dc >= de) : (cur >= se && carry == 0))) break;
+            const int cnt = TL ? fill_tl<false>(s, fc, fe, dc, de, lbase, tx, ty, ent, nullptr, s_pos, s_rid, s_wc, &s_first,
+                                                &s_clamp)
+                               : fill_batch<1, false>(s, cur, se, carry, tx, ty, ent, nullptr, s_pos, s_rid, s_wc,
+                                                      &s_first, &s_clamp, &vc, s_bm);
             walked += (unsigned)(s_clamp ? comp_batch<true>(ent, cnt, lbase, flx, fy01, fy23, T01, T23, C0, C1, C2, last)
                                          : comp_batch<false>(ent, cnt, lbase, flx, fy01, fy23, T01, T23, C0, C1, C2, last));
 #pragma unroll
-            for (int p = 0; p < RT_PX; p++)   // segment position of a last entry of this batch
+            for (int p = 0; p < RT_PX; p++)   // segment position (TL: list index) of a last entry of this batch
                 if (last[p] >= lbase) s_lastp[tid + p * RT_THREADS] = s_pos[last[p] - lbase];
             lbase += cnt;
         }
@@ -589,16 +722,24 @@ void launch_loss_staged(const StepDims &d, const CamSet &cams, const Scratch &s,
     g_launches++;
 }
 
+template <bool TL>
+static void launch_fwd_t(const CamSet &cams, const Scratch &s, const float *t32, const unsigned char *t8, bool staged,
+                         float *images, float loss_scale, float3 bg, bool targets, cudaStream_t st)
+{
+    const int grid = 148 * 16;
+    if (targets && images) cls_launch(k_fwd<true, true, TL>, grid, RT_THREADS, 0, st, cams, s, t32, t8, staged, images, loss_scale, bg);
+    else if (targets) cls_launch(k_fwd<true, false, TL>, grid, RT_THREADS, 0, st, cams, s, t32, t8, staged, images, loss_scale, bg);
+    else if (images) cls_launch(k_fwd<false, true, TL>, grid, RT_THREADS, 0, st, cams, s, t32, t8, staged, images, loss_scale, bg);
+    else cls_launch(k_fwd<false, false, TL>, grid, RT_THREADS, 0, st, cams, s, t32, t8, staged, images, loss_scale, bg);
+}
+
 void launch_fwd(const StepDims &d, const CamSet &cams, const Scratch &s, const void *targets, bool targets_u8,
                 bool staged, float *images, float loss_scale, float3 bg, cudaStream_t st)
 {
-    const int grid = 148 * 16;
     const float *t32 = targets_u8 ? nullptr : (const float *)targets;
     const unsigned char *t8 = targets_u8 ? (const unsigned char *)targets : nullptr;
-    if (targets && images) cls_launch(k_fwd<true, true>, grid, RT_THREADS, 0, st, cams, s, t32, t8, staged, images, loss_scale, bg);
-    else if (targets) cls_launch(k_fwd<true, false>, grid, RT_THREADS, 0, st, cams, s, t32, t8, staged, images, loss_scale, bg);
-    else if (images) cls_launch(k_fwd<false, true>, grid, RT_THREADS, 0, st, cams, s, t32, t8, staged, images, loss_scale, bg);
-    else cls_launch(k_fwd<false, false>, grid, RT_THREADS, 0, st, cams, s, t32, t8, staged, images, loss_scale, bg);
+    if (s.tl_on) launch_fwd_t<true>(cams, s, t32, t8, staged, images, loss_scale, bg, targets != nullptr, st);
+    else launch_fwd_t<false>(cams, s, t32, t8, staged, images, loss_scale, bg, targets != nullptr, st);
     g_launches++;
 }
 
@@ -706,13 +847,14 @@ __device__ __forceinline__ float warp_reduce_scatter9(const float (&r)[9], int l
     return a1 + __shfl_xor_sync(0xffffffffu, a1, 1);
 }
 
+template <bool TL>
 __global__ void __launch_bounds__(RT_THREADS, 12)
 k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ dL_dimg, float3 bg)
 {
     CLS_PDL_WAIT();
     __shared__ float4 ent[3 * (RT_BATCH + 1)];
     __shared__ float2 sd[RT_BATCH];    // tile-local 2D mean (dx0, dy0) in fp32
-    __shared__ int s_item, s_maxlast, s_pos[RT_SLOTS], s_wc[2 * RT_SCAN];
+    __shared__ int s_item, s_maxlast, s_split, s_pos[RT_SLOTS], s_wc[2 * RT_SCAN];
     __shared__ unsigned s_rid[RT_SLOTS];
     __shared__ unsigned s_bm[(RT_SCAN * RT_THREADS) / 32];   // virtual merge window map
     if (s.cnt->overflow) return;
@@ -787,7 +929,22 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         // reverse walk over the row segment [first, end): batches of covering units, descending
         int cur = end, carry = 0;
         VCur vc{};
-        if (s.vm_on) {   // the dynamic cursor at `end`: the step's units with merged position < end
+        int fc = 0, f0 = 0, dc = 0, d0 = 0;   // TL: the two lists' cursors at `cur` and their starts
+        if (TL) {
+            f0 = s.tl_foff[e];
+            const int nF = s.tl_foff[e + 1] - f0;
+            const int2 dr = s.tl_drng[item];
+            d0 = dr.x;
+            if (end > first) {
+                if (tid < 32) {
+                    const int fi = tl_split(s, f0, nF, d0, dr.y - dr.x, end);
+                    if (tid == 0) s_split = fi;
+                }
+                __syncthreads();
+                fc = f0 + s_split;
+                dc = d0 + (end - s_split);
+            }
+        } else if (s.vm_on) {   // the dynamic cursor at `end`: the step's units with merged position < end
             const int seg = v * cams.TY + ty;
             vc = VCur{s.seg_off[seg], s.vm_flb[seg], s.vm_db[seg], s.vm_db[seg + 1], 0, 0};
             int lo = vc.d0, hi = vc.d1;   // 32-ary search per warp: log32 of the segment's unit count rounds
@@ -806,8 +963,9 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         }
         while (cur > first || carry > 0) {
             __syncthreads();
-            const int cnt = fill_batch<-1, true>(s, cur, first, carry, tx, ty, ent, sd, s_pos, s_rid, s_wc, nullptr, nullptr,
-                                                 &vc, s_bm);
+            const int cnt = TL ? fill_tl_bwd(s, fc, f0, dc, d0, cur, first, tx, ty, ent, sd, s_pos, s_rid, s_wc)
+                               : fill_batch<-1, true>(s, cur, first, carry, tx, ty, ent, sd, s_pos, s_rid, s_wc, nullptr,
+                                                      nullptr, &vc, s_bm);
             // walked (pixel, entry) pairs of this batch: s_pos is descending, so the entries above a
             // pixel's last composited one form a prefix (binary search per pixel)
 #pragma unroll
@@ -997,6 +1155,28 @@ __global__ void k_debug_tile_list(Scratch s, CacheBufs cb, int cached, int TY, i
     if (blockIdx.x != 0 || threadIdx.x != 0) return;
     const int tx = tile % TX, ty = tile / TX, seg = view * TY + ty;
     int k = 0;
+    if (s.tl_on) {   // exact per-tile lists: merge the frozen list and the step's list (p <= f: the step's first)
+        const int e = view * TX * TY + tile;
+        int item = -1;
+        for (int it = 0; it < s.cnt->n_items; it++)
+            if (s.items[it] == e) item = it;
+        int fc = s.tl_foff[e];
+        const int fe = s.tl_foff[e + 1];
+        int dc = 0, de = 0;
+        if (item >= 0) {
+            dc = s.tl_drng[item].x;
+            de = s.tl_drng[item].y;
+        }
+        while (fc < fe || dc < de) {
+            unsigned rid;
+            if (dc < de && (fc >= fe || (unsigned)(s.tl_d[dc] >> 32) <= (unsigned)s.tl_f[fc])) rid = (unsigned)s.tl_d[dc++];
+            else rid = (unsigned)s.tl_f[fc++];
+            if (k < max) out[k] = debug_gid(s, cb, cached != 0, rid);
+            k++;
+        }
+        *count = k;
+        return;
+    }
     int c = s.vm_on ? s.vm_db[seg] : 0;   // virtual merge: the step's units before u
     for (int u = s.seg_off[seg]; u < s.seg_end[seg]; u++) {
         unsigned long long key;
@@ -1053,7 +1233,8 @@ void launch_bwd_raster(const StepDims &d, const Scratch &s, const float *dL_dima
 {
     CamSet cams;
     cams.n = d.V; cams.W = d.W; cams.H = d.H; cams.TX = d.TX; cams.TY = d.TY; cams.T = d.T;
-    cls_launch(k_bwd, 148 * 16, RT_THREADS, 0, st, cams, s, dL_dimages, bg);
+    if (s.tl_on) cls_launch(k_bwd<true>, 148 * 16, RT_THREADS, 0, st, cams, s, dL_dimages, bg);
+    else cls_launch(k_bwd<false>, 148 * 16, RT_THREADS, 0, st, cams, s, dL_dimages, bg);
     g_launches++;
 }
 

@@ -59,10 +59,20 @@ void launch_dyn_emit(const StepDims &d, const CacheBufs &cb, const Scratch &sd, 
 void launch_cache_check(const CacheBufs &cb, const StepDims &d, const Scratch &s, cudaStream_t st,
                         cudaGraphConditionalHandle cond = 0, int use_cond = 0);
 void launch_cache_build(const Params &g, const StepDims &d, const CamSet &cams, const CacheBufs &cb,
-                        const Scratch &s, Scratch &sb, unsigned long long **fsorted, cudaStream_t st);
+                        const Scratch &s, Scratch &sb, unsigned long long **fsorted, cudaStream_t st,
+                        const unsigned long long **tl_sorted = nullptr);
 void launch_cache_finalize(const StepDims &d, const CacheBufs &cb, const Scratch &s, cudaStream_t st);
 void launch_cache_merge(const StepDims &d, const CacheBufs &cb, const Scratch &sd, const unsigned long long *fsorted,
                         const unsigned long long *dsorted, unsigned long long *merged, bool vm, cudaStream_t st);
+void launch_dyn_pos(const CacheBufs &cb, const Scratch &sd, cudaStream_t st);
+// exact per-tile lists of the static cache (k_tiles.cu)
+const unsigned long long *launch_tile_lists(const StepDims &d, const unsigned long long *units, const int *n_units,
+                                            const unsigned *rowmask, unsigned long long *buf_a,
+                                            unsigned long long *buf_b, long long cap, unsigned rid_add,
+                                            Counters *cnt, unsigned *ucnt, unsigned *uoff,
+                                            unsigned long long *st_scan, unsigned *rs_counts, unsigned *rs_totals,
+                                            int *off, const int *items, const int *n_items, int2 *rng,
+                                            const unsigned *dpos, const int *skip, cudaStream_t st);
 
 // (4) forward compositing + fused L1                           (k_raster.cu)
 void launch_fwd(const StepDims &d, const CamSet &cams, const Scratch &s, const void *targets, bool targets_u8,
@@ -139,6 +149,7 @@ inline void per_device_once(std::atomic<unsigned long long> &done, F &&set_attr)
 extern int64_t g_launches;   // kernels launched by this process through libcls (host counter)
 extern bool g_pdl;           // programmatic dependent launch on (CLS_NO_PDL=1 turns it off)
 extern bool g_vmerge;        // static cache: virtual merge in the raster (CLS_NO_VMERGE=1 materialises it)
+extern bool g_tiles;         // static cache: exact per-tile lists merged in the raster (CLS_NO_TL=1: row segments)
 
 // Every kernel of libcls starts with CLS_PDL_WAIT() and is launched by cls_launch with programmatic
 // stream serialization: a kernel's blocks may be scheduled while its predecessor in the stream drains,
