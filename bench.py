@@ -331,7 +331,8 @@ def run_ours(args):
         per = {k: v for k, v in prof.items() if v["calls"]}
         dom = max(per, key=lambda k: per[k]["ms"]) if per else None
         step_ms_sum = sum(v["ms"] for v in per.values())
-        work = algorithmic_work(sc, len(cams), stats)
+        work = algorithmic_work(sc, len(cams), stats,
+                                tiles=bool(args.static_cache) and not os.environ.get("CLS_NO_TL"))
         groups = {}
         for k, v in per.items():
             avg_ms = v["ms"] / v["calls"]
@@ -457,7 +458,7 @@ def ncu_traffic(config: str, group: str):
         return None
 
 
-def algorithmic_work(sc, n_views, st):
+def algorithmic_work(sc, n_views, st, tiles=False):
     """Per-launch algorithmic work of each kernel group: bytes the method must
     move for the HBM-bound groups, FP32 FLOPs for the compositing kernels."""
     n, V = sc.n, n_views
@@ -469,6 +470,8 @@ def algorithmic_work(sc, n_views, st):
     rpasses = -(-rbits // (8 if rbits <= 32 else 9))
     TY = -(-sc.height // 16)
     upasses = -(-max(V * TY, 1).bit_length() // 8)      # row segments (view, tile row), 8-bit digits
+    tbits = max(V * TY * (-(-sc.width // 16)), 1).bit_length()   # tiles (view, tile row, column)
+    tpasses = -(-tbits // (8 if tbits <= 16 else 9))
     return {
         "member": ("hbm", n * 16 + n * 4 + A * 4),
         "project_cand": ("hbm", n * 48 + C * 8),
@@ -479,7 +482,11 @@ def algorithmic_work(sc, n_views, st):
         # k_units: per record roff, rcnt, srid, key (20 B) + the 64 B record; per unit the row-mask
         # word (4 B) and the 8 B key out
         "emit": ("hbm", R * (20 + 64) + U * (4 + 8)),
-        "pair_sort": ("hbm", upasses * U * 16 + U * 8),  # key-only passes (record id packed in the key)
+        # key-only passes (record id packed in the key); with the static cache's exact tile lists (k_tiles.cu)
+        # the step's units are cut into (tile, record) pairs instead: count (8 in, 4 out), scan (4 + 4),
+        # emit (8 + 4 in, 8 out per pair), the key-only pair sort by tile, item ranges + merge keys
+        # (8 in, 4 dpos, 8 out per pair)
+        "pair_sort": ("hbm", (U * 28 + P * 8 + tpasses * P * 16 + P * 20) if tiles else (upasses * U * 16 + U * 8)),
         "fwd_raster": ("alu", st["n_fwd_evals"] * FWD_FLOPS_PER_EVAL),
         "bwd_raster": ("alu", st["n_bwd_evals"] * BWD_FLOPS_PER_EVAL),
         "bwd_project": ("hbm", A * V * 48 + A * (48 + 16 * K4) + A * 16 * (3 + K4)),

@@ -128,6 +128,8 @@ struct CacheBufs {      // the cache's device buffers (passed by value)
     int4 *dcinfo;       // [Dcap] (Gaussian index, view, depth key, tile rows)
     long long Fcap, Dcap, maxN, Dunits;
     int dilate;         // tiles added around every active rect
+    unsigned long long *smp_k;   // [Fcap / 1024 + 2] sampled frozen (view, depth) keys (k_dyn_pos)
+    int *smp_g;                  // ... and their Gaussian indices
     int *tl_foff;       // [V*T + 1] per-tile ranges of the frozen tile lists
     int2 *tl_drng;      // [max items] per-item ranges of the step's tile lists
 };

@@ -191,7 +191,7 @@ cls_status cls_destroy(cls_ctx *c)
         if (p) cudaFree(p);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     void *cp[] = {c->cb.st, c->cb.ccnt, c->cb.dyn_of, c->cb.s0, c->cb.flag, c->cb.excl, c->cb.scan_status, c->cb.dmask,
-                  c->cb.dmdiff, c->cb.urec, c->cb.cfvd, c->cb.cfgid, c->cb.cseg_lb, c->cb.dpos, c->cb.db, c->cb.dq, c->cb.dmi, c->cb.mitems, c->cb.dlist, c->cb.dM, c->cb.dcand, c->cb.dcinfo, c->cb.tl_foff, c->cb.tl_drng, c->d_dsat,
+                  c->cb.dmdiff, c->cb.urec, c->cb.cfvd, c->cb.cfgid, c->cb.cseg_lb, c->cb.dpos, c->cb.db, c->cb.dq, c->cb.dmi, c->cb.mitems, c->cb.dlist, c->cb.dM, c->cb.dcand, c->cb.dcinfo, c->cb.tl_foff, c->cb.tl_drng, c->cb.smp_k, c->cb.smp_g, c->d_dsat,
                   c->d_drowmask, c->d_dbbox, c->d_cukey, c->d_cukey_alt};
     for (void *p : cp)
         if (p) cudaFree(p);
@@ -292,6 +292,7 @@ static cls_status cache_allocate(cls_ctx *c)
               dalloc(&c->d_cukey, P) && dalloc(&c->d_cukey_alt, P) && dalloc(&cb.dq, P) && dalloc(&cb.dmi, P) && dalloc(&cb.dlist, N) &&
               dalloc(&cb.dM, N * 12) && dalloc(&cb.dcand, (size_t)Dcap) && dalloc(&cb.dcinfo, (size_t)Dcap) &&
               dalloc(&cb.mitems, P / 4096 + NSEG + 1) && dalloc(&cb.tl_foff, VT + 1) && dalloc(&cb.tl_drng, VT) &&
+              dalloc(&cb.smp_k, (size_t)R / 1024 + 2) && dalloc(&cb.smp_g, (size_t)R / 1024 + 2) &&
               cudaMallocHost((void **)&c->h_cst, sizeof(CacheState)) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
@@ -559,16 +560,18 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
         run(c, P_RECSORT, st, [&] { launch_bin_recsort(d, cs, sd, st); });
         run(c, P_BINCOUNT, st, [&] { launch_bin_count(d, cs, sd, st); });
         run(c, P_EMIT, st, [&] { launch_bin_emit(d, cs, sd, st); });
-        unsigned long long *dsorted = nullptr;
-        run(c, P_PAIRSORT, st, [&] { dsorted = launch_unit_sort(d, sd, st); });
+        // exact per-tile lists: the step's own pairs of the active tiles straight from its units (written in
+        // sorted-record order, so the stable pair sort by tile keeps each tile's pairs in depth order: no unit sort)
+        unsigned long long *dsorted = g_tiles ? s.ukey : nullptr;
+        if (!g_tiles) run(c, P_PAIRSORT, st, [&] { dsorted = launch_unit_sort(d, sd, st); });
         unsigned long long *merged = dsorted == s.ukey ? s.ukey_alt : s.ukey;
         const unsigned long long *tl_d = nullptr;
-        if (g_tiles) {   // exact per-tile lists: the step's own pairs of the active tiles, merged in the raster
-            run(c, P_CACHE_MERGE, st, [&] {
-                launch_dyn_pos(cb, sd, st);
+        if (g_tiles) {
+            run(c, P_CACHE_MERGE, st, [&] { launch_dyn_pos(cb, sd, st); });
+            run(c, P_PAIRSORT, st, [&] {
                 tl_d = launch_tile_lists(d, dsorted, &s.cnt->n_units32, s.rowmask, merged, dsorted, s.max_units,
                                          (unsigned)cb.Fcap, s.cnt, cb.dq, cb.dmi, s.st_scan, s.rs_counts, s.rs_totals,
-                                         nullptr, s.items, &s.cnt->n_items, cb.tl_drng, cb.dpos, &s.cnt->overflow, st);
+                                         nullptr, s.item_of_tile, cb.tl_drng, cb.dpos, &s.cnt->overflow, st);
             });
         } else {
             run(c, P_CACHE_MERGE, st, [&] { launch_cache_merge(d, cb, sd, fsorted, dsorted, merged, g_vmerge, st); });
@@ -598,7 +601,7 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     if (images) run(c, P_FILL, st, [&] { launch_fill_bg(d, s, images, bgc, st); });
     if (staged) {   // the loss terms need the gathered targets; the compositing above did not
         cudaStreamWaitEvent(st, c->ev_gather, 0);
-        run(c, P_LOSS, st, [&] { launch_loss_staged(d, cs, s, loss_scale, st); });
+        run(c, P_LOSS, st, [&] { launch_loss_staged(d, cs, sr, loss_scale, st); });
     }
     if (targets && loss) run(c, P_LOSS, st, [&] { launch_loss(s, loss_scale, loss, st); });
     if (tile_mask) cudaMemcpyAsync(tile_mask, s.mask, (size_t)d.V * d.T, cudaMemcpyDeviceToDevice, st);

@@ -176,17 +176,55 @@ __global__ void k_cache_finalize(CacheBufs cb, Scratch s, int n_seg)
 }
 
 // ---- per step: dynamic records' ranks among the frozen ones, and the merge ----
+// Every DYN_SMP_STRIDE(F)-th frozen (view, depth) key and Gaussian index, taken once per build: the rank
+// search of a step's record first bisects these samples in shared memory, then a range of one stride in
+// global memory (12 dependent global steps on c4 instead of 23).
+#define DYN_SMP_MAX 2048
+__host__ __device__ __forceinline__ int dyn_smp_stride(int F)
+{
+    int s = 1024;
+    while ((long long)s * DYN_SMP_MAX < (long long)F) s <<= 1;
+    return s;
+}
+
+__global__ void __launch_bounds__(256) k_cache_samples(CacheBufs cb)
+{
+    CLS_PDL_WAIT();
+    if (cb.ccnt->overflow) return;   // warm step (CACHE_SKIP) or a failed build
+    const int F = min(cb.ccnt->n_records, (int)cb.Fcap);
+    const int S = dyn_smp_stride(F), ns = (F + S - 1) / S;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < ns; j += gridDim.x * blockDim.x) {
+        cb.smp_k[j] = cb.cfvd[(size_t)j * S];
+        cb.smp_g[j] = cb.cfgid[(size_t)j * S];
+    }
+}
+
 __global__ void __launch_bounds__(256) k_dyn_pos(CacheBufs cb, Scratch sd)
 {
     CLS_PDL_WAIT();
+    __shared__ unsigned long long s_k[DYN_SMP_MAX];
+    __shared__ int s_g[DYN_SMP_MAX];
     if (sd.cnt->overflow) return;
     const int D = min(sd.cnt->n_records, (int)sd.max_records);
     const int F = cb.st->F;
+    const int S = dyn_smp_stride(F), ns = (F + S - 1) / S;
+    for (int j = threadIdx.x; j < ns; j += blockDim.x) {
+        s_k[j] = cb.smp_k[j];
+        s_g[j] = cb.smp_g[j];
+    }
+    __syncthreads();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D; i += gridDim.x * blockDim.x) {
         const unsigned rid = sd.srid[i];
         const unsigned long long key = sd.rskey[i] >> RK_IDX_BITS;   // (view, depth)
         const int gid = sd.rec_gid[rid];
-        int lo = 0, hi = F;   // frozen records ordered before (view, depth, gid): (key, gid) strictly less
+        // frozen records ordered before (view, depth, gid): (key, gid) strictly less
+        int c = 0, h = ns;   // samples strictly less
+        while (c < h) {
+            const int m = (c + h) >> 1;
+            if (s_k[m] < key || (s_k[m] == key && s_g[m] < gid)) c = m + 1;
+            else h = m;
+        }
+        int lo = c ? (c - 1) * S + 1 : 0, hi = c ? min(c * S, F) : 0;
         while (lo < hi) {
             const int m = (lo + hi) >> 1;
             const unsigned long long fk = cb.cfvd[m];
@@ -629,7 +667,8 @@ void launch_cache_build(const Params &g, const StepDims &d, const CamSet &cams, 
     launch_bin_recsort(d, cams, sb, st);
     launch_bin_count(d, cams, sb, st);
     cls_launch(k_cache_reorder, 148 * 8, 256, 0, st, cb, sb);
-    g_launches++;
+    cls_launch(k_cache_samples, 8, 256, 0, st, cb);
+    g_launches += 2;
     Scratch su = sb;
     su.rec = cb.urec;   // units read the reordered records (id = rank)
     launch_bin_emit(d, cams, su, st);
@@ -641,7 +680,7 @@ void launch_cache_build(const Params &g, const StepDims &d, const CamSet &cams, 
         unsigned long long *other = *fsorted == su.ukey ? su.ukey_alt : su.ukey;
         *tl_sorted = launch_tile_lists(d, *fsorted, &su.cnt->n_units32, su.rowmask, other, *fsorted, su.max_units, 0u,
                                        su.cnt, cb.dq, cb.dmi, su.st_scan, su.rs_counts, su.rs_totals, cb.tl_foff, nullptr,
-                                       nullptr, nullptr, nullptr, &su.cnt->overflow, st);
+                                       nullptr, nullptr, &su.cnt->overflow, st);
     } else {
         cls_launch(k_cache_items, 1, 1024, 0, st, cb, n_seg);
         g_launches++;

@@ -109,23 +109,28 @@ __global__ void __launch_bounds__(256) k_tl_offsets(const unsigned long long *__
         off[t] = tl_lower_bound(keys, n, (unsigned)t);
 }
 
-// the step's lists: the pair range of every active work item, and rw[i] = (rank position of the record
-// among the frozen ones) << 32 | global record id (the merge key next to the id)
+// the step's lists: the pair range of every active work item (rng zeroed beforehand: items without pairs
+// keep (0, 0)), and rw[i] = (rank position of the record among the frozen ones) << 32 | global record id
+// (the merge key next to the id)
 __global__ void __launch_bounds__(256) k_tl_items(const unsigned long long *__restrict__ keys, const int *n_ptr,
-                                                  const int *__restrict__ items, const int *n_items_ptr, int2 *rng,
+                                                  const int *__restrict__ item_of_tile, int2 *rng,
                                                   unsigned long long *rw, const unsigned *__restrict__ dpos,
                                                   unsigned fbase, const int *skip)
 {
     CLS_PDL_WAIT();
     if (skip && *skip) return;
-    const int n = *n_ptr, n_items = *n_items_ptr;
-    const int stride = gridDim.x * blockDim.x;
-    for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < n_items; it += stride) {
-        const unsigned e = (unsigned)items[it];
-        rng[it] = make_int2(tl_lower_bound(keys, n, e), tl_lower_bound(keys, n, e + 1u));
-    }
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const unsigned rid = (unsigned)keys[i];
+    const int n = *n_ptr;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const unsigned long long k = keys[i];
+        const unsigned t = (unsigned)(k >> 32);
+        const bool first = i == 0 || (unsigned)(keys[i - 1] >> 32) != t;
+        const bool last = i == n - 1 || (unsigned)(keys[i + 1] >> 32) != t;
+        if (first || last) {
+            const int it = item_of_tile[t];   // the step's pairs are cut against the active mask: an item
+            if (first) rng[it].x = i;
+            if (last) rng[it].y = i + 1;
+        }
+        const unsigned rid = (unsigned)k;
         rw[i] = ((unsigned long long)dpos[rid - fbase] << 32) | rid;
     }
 }
@@ -146,10 +151,11 @@ const unsigned long long *launch_tile_lists(const StepDims &d, const unsigned lo
                                             unsigned long long *buf_b, long long cap, unsigned rid_add,
                                             Counters *cnt, unsigned *ucnt, unsigned *uoff,
                                             unsigned long long *st_scan, unsigned *rs_counts, unsigned *rs_totals,
-                                            int *off, const int *items, const int *n_items, int2 *rng,
-                                            const unsigned *dpos, const int *skip, cudaStream_t st)
+                                            int *off, const int *item_of_tile, int2 *rng, const unsigned *dpos,
+                                            const int *skip, cudaStream_t st)
 {
     const int n_seg = d.V * d.TY, W32 = (d.TX + 31) / 32, nT = d.V * d.T;
+    if (!off) cudaMemsetAsync(rng, 0, sizeof(int2) * (size_t)nT, st);
     cls_launch(k_tl_count, 148 * 8, 256, 0, st, units, n_units, n_seg, rowmask, W32, ucnt, skip);
     scan_excl_u32(ucnt, uoff, n_units, (int)cap, st_scan, &cnt->scan_ticket2, &cnt->n_pairs, skip, st);
     cls_launch(k_tl_emit, 148 * 8, 256, 0, st, units, n_units, n_seg, rowmask, W32, d.TX, (const unsigned *)uoff,
@@ -163,8 +169,8 @@ const unsigned long long *launch_tile_lists(const StepDims &d, const unsigned lo
         cls_launch(k_tl_offsets, 148 * 8, 256, 0, st, sorted, (const int *)&cnt->n_pairs32, nT, off,
                    (const int *)&cnt->overflow);
     } else {
-        cls_launch(k_tl_items, 148 * 8, 256, 0, st, sorted, (const int *)&cnt->n_pairs32, items, n_items, rng, rw,
-                   dpos, rid_add, (const int *)&cnt->overflow);
+        cls_launch(k_tl_items, 148 * 8, 256, 0, st, sorted, (const int *)&cnt->n_pairs32, item_of_tile, rng, rw, dpos,
+                   rid_add, (const int *)&cnt->overflow);
     }
     g_launches += 3;
     return off ? sorted : rw;

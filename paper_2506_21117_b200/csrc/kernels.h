@@ -71,8 +71,8 @@ const unsigned long long *launch_tile_lists(const StepDims &d, const unsigned lo
                                             unsigned long long *buf_b, long long cap, unsigned rid_add,
                                             Counters *cnt, unsigned *ucnt, unsigned *uoff,
                                             unsigned long long *st_scan, unsigned *rs_counts, unsigned *rs_totals,
-                                            int *off, const int *items, const int *n_items, int2 *rng,
-                                            const unsigned *dpos, const int *skip, cudaStream_t st);
+                                            int *off, const int *item_of_tile, int2 *rng, const unsigned *dpos,
+                                            const int *skip, cudaStream_t st);
 
 // (4) forward compositing + fused L1                           (k_raster.cu)
 void launch_fwd(const StepDims &d, const CamSet &cams, const Scratch &s, const void *targets, bool targets_u8,
