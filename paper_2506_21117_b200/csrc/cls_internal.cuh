@@ -201,6 +201,7 @@ struct Scratch {
     // a step's entry of position p precedes the frozen record f iff p <= f.  List positions (px_last,
     // first_active) are then list indices.
     int tl_on;
+    unsigned *ucnt;                     // k_units also writes each unit's active-tile count here (or null)
     const unsigned long long *tl_f;     // frozen pairs sorted by tile: (tile << 32 | frozen record id)
     const int *tl_foff;                 // [V*T + 1] each tile's range of tl_f
     const unsigned long long *tl_d;     // the step's pairs of the active tiles, sorted by tile

@@ -559,7 +559,9 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
         run(c, P_PROJECT_EXACT, st, [&] { launch_dyn_emit(d, cb, sd, st); });   // the staged candidates vs the mask
         run(c, P_RECSORT, st, [&] { launch_bin_recsort(d, cs, sd, st); });
         run(c, P_BINCOUNT, st, [&] { launch_bin_count(d, cs, sd, st); });
+        if (g_tiles) sd.ucnt = cb.dq;   // k_units counts each unit's active tiles for the tile lists
         run(c, P_EMIT, st, [&] { launch_bin_emit(d, cs, sd, st); });
+        sd.ucnt = nullptr;
         // exact per-tile lists: the step's own pairs of the active tiles straight from its units (written in
         // sorted-record order, so the stable pair sort by tile keeps each tile's pairs in depth order: no unit sort)
         unsigned long long *dsorted = g_tiles ? s.ukey : nullptr;
@@ -571,7 +573,7 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
             run(c, P_PAIRSORT, st, [&] {
                 tl_d = launch_tile_lists(d, dsorted, &s.cnt->n_units32, s.rowmask, merged, dsorted, s.max_units,
                                          (unsigned)cb.Fcap, s.cnt, cb.dq, cb.dmi, s.st_scan, s.rs_counts, s.rs_totals,
-                                         nullptr, s.item_of_tile, cb.tl_drng, cb.dpos, &s.cnt->overflow, st);
+                                         nullptr, s.item_of_tile, cb.tl_drng, cb.dpos, &s.cnt->overflow, st, true);
             });
         } else {
             run(c, P_CACHE_MERGE, st, [&] { launch_cache_merge(d, cb, sd, fsorted, dsorted, merged, g_vmerge, st); });

@@ -290,6 +290,7 @@ __global__ void __launch_bounds__(KU_THREADS) k_units(const __grid_constant__ Ca
             }
             pairs += cnt;
             live += cnt ? 1u : 0u;
+            if (s.ucnt) s.ucnt[u] = cnt;   // the step's tile lists (k_tiles.cu) count no further
             s.ukey[u] = (cnt ? ((unsigned long long)(view * TY + ty) << UK_SEG_SHIFT) |
                                    ((unsigned long long)lo << UK_LO_SHIFT) | ((unsigned long long)hi << UK_HI_SHIFT)
                              : dead) | (unsigned long long)I[2][j];

@@ -202,22 +202,31 @@ k_active_rects(const float4 *__restrict__ mean_op, const float4 *__restrict__ qu
     }
 }
 
-// inclusive prefix sum of n ints at stride st (one warp; 32 elements per step with a carried total)
+// inclusive prefix sum of n ints at stride st (one warp): each lane takes 4 consecutive elements (a
+// local prefix), one warp scan of the lane totals per 128 elements, a carried total beyond
 __device__ __forceinline__ void warp_prefix(int *a, int n, int st)
 {
     const int lane = threadIdx.x & 31;
     int carry = 0;
-    for (int b = 0; b < n; b += 32) {
-        const int i = b + lane;
-        int v = i < n ? a[i * st] : 0;
+    for (int b = 0; b < n; b += 128) {
+        const int i0 = b + 4 * lane;
+        int v[4], sum = 0;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            sum += i0 + j < n ? a[(i0 + j) * st] : 0;
+            v[j] = sum;
+        }
+        int x = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, v, o);
-            if (lane >= o) v += t;
+            const int t = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += t;
         }
-        v += carry;
-        if (i < n) a[i * st] = v;
-        carry = __shfl_sync(0xffffffffu, v, 31);
+        const int excl = x - sum + carry;
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+            if (i0 + j < n) a[(i0 + j) * st] = v[j] + excl;
+        carry += __shfl_sync(0xffffffffu, x, 31);
     }
 }
 
@@ -225,7 +234,7 @@ __device__ __forceinline__ void warp_prefix(int *a, int n, int st)
 // active rect), then its summed-area table, tile bbox and row bitmasks; one block per view, one warp
 // per row / column prefix (warp scans).  The tables and the mask live in shared memory (SMEM) when
 // they fit, else in global memory.
-#define SAT_THREADS 512
+#define SAT_THREADS 1024
 template <bool SMEM>
 __global__ void __launch_bounds__(SAT_THREADS) k_sat(const __grid_constant__ CamSet cams, Scratch s, int all_tiles, const int *__restrict__ skip)
 {

@@ -142,7 +142,8 @@ static int tl_bits_for(long long x)
     return b;
 }
 
-// the tile lists of the sorted units `units` (count *n_units) against `rowmask`, emitted into buf_a and
+// the tile lists of the sorted units `units` (count *n_units) against `rowmask` (`counted`: k_units already
+// wrote each unit's count to ucnt), emitted into buf_a and
 // sorted through buf_b (`units` may live in buf_b: it is read before the sort).  Frozen (off != nullptr):
 // per-tile offsets, returns the sorted pairs.  The step's (off == nullptr): per-item ranges, returns the
 // rewritten (rank position << 32 | record id) pairs, written to whichever buffer the sort left free.
@@ -152,11 +153,14 @@ const unsigned long long *launch_tile_lists(const StepDims &d, const unsigned lo
                                             Counters *cnt, unsigned *ucnt, unsigned *uoff,
                                             unsigned long long *st_scan, unsigned *rs_counts, unsigned *rs_totals,
                                             int *off, const int *item_of_tile, int2 *rng, const unsigned *dpos,
-                                            const int *skip, cudaStream_t st)
+                                            const int *skip, cudaStream_t st, bool counted)
 {
     const int n_seg = d.V * d.TY, W32 = (d.TX + 31) / 32, nT = d.V * d.T;
     if (!off) cudaMemsetAsync(rng, 0, sizeof(int2) * (size_t)nT, st);
-    cls_launch(k_tl_count, 148 * 8, 256, 0, st, units, n_units, n_seg, rowmask, W32, ucnt, skip);
+    if (!counted) {
+        cls_launch(k_tl_count, 148 * 8, 256, 0, st, units, n_units, n_seg, rowmask, W32, ucnt, skip);
+        g_launches++;
+    }
     scan_excl_u32(ucnt, uoff, n_units, (int)cap, st_scan, &cnt->scan_ticket2, &cnt->n_pairs, skip, st);
     cls_launch(k_tl_emit, 148 * 8, 256, 0, st, units, n_units, n_seg, rowmask, W32, d.TX, (const unsigned *)uoff,
                (const unsigned long long *)&cnt->n_pairs, buf_a, cap, rid_add, &cnt->n_pairs32, &cnt->overflow, skip);
@@ -172,7 +176,7 @@ const unsigned long long *launch_tile_lists(const StepDims &d, const unsigned lo
         cls_launch(k_tl_items, 148 * 8, 256, 0, st, sorted, (const int *)&cnt->n_pairs32, item_of_tile, rng, rw, dpos,
                    rid_add, (const int *)&cnt->overflow);
     }
-    g_launches += 3;
+    g_launches += 2;
     return off ? sorted : rw;
 }
 

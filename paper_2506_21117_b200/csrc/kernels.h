@@ -72,7 +72,7 @@ const unsigned long long *launch_tile_lists(const StepDims &d, const unsigned lo
                                             Counters *cnt, unsigned *ucnt, unsigned *uoff,
                                             unsigned long long *st_scan, unsigned *rs_counts, unsigned *rs_totals,
                                             int *off, const int *item_of_tile, int2 *rng, const unsigned *dpos,
-                                            const int *skip, cudaStream_t st);
+                                            const int *skip, cudaStream_t st, bool counted = false);
 
 // (4) forward compositing + fused L1                           (k_raster.cu)
 void launch_fwd(const StepDims &d, const CamSet &cams, const Scratch &s, const void *targets, bool targets_u8,
