@@ -244,19 +244,25 @@ def run_ours(args):
             step_host = gstep_host.replay
         else:
             step_host = (lambda: step_eager(tg_host)) if gstep is not None else (lambda: step(tg_host))
+        for _ in range(max(args.warmup, 3)):   # untimed warm-up of this form of the step, like the device-target one
+            step_host()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
         w0 = time.perf_counter()
         f0.record(stream)
-        for _ in range(args.steps):
+        for k in range(args.steps):
             # this step's inputs: the views' target images stay in pinned host memory; the library
             # moves only the pixels of the active tiles to the device (k_gather_targets, overlapped)
+            ev[k].record(stream)
             loss = step_host()
             loss_host.copy_(loss, non_blocking=True)         # the step's result
+        ev[args.steps].record(stream)
         f1.record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - w0
+        per_step = sorted(ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps))
         te = torch.tensor([f0.elapsed_time(f1), wall * 1e3], dtype=torch.float64, device=f"cuda:{local}")
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -270,6 +276,8 @@ def run_ours(args):
                            "read from pinned host memory inside the step; the full target set is "
                            f"{int(tg_host.numel() * tbytes) * world} B",
                "device_ms_per_step": float(te[0].item()) / args.steps,
+               "device_step_ms_min_median_max": [round(per_step[0], 4), round(per_step[len(per_step) // 2], 4),
+                                                 round(per_step[-1], 4)],
                "mode": ("CUDA graph of the step over the pinned host targets"
                         if gstep is not None and args.e2e_mode == "graph" else "eager launches")}
 
