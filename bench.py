@@ -633,8 +633,10 @@ def run_loop(args):
                     "timed": "device events around the whole loop (prunes and re-captures included)"},
            "active": int(stats["n_active"]), "active_tiles": int(sum(stats["n_active_tiles"])),
            "static_cache": {"builds": int(stats["cache_builds"]), "mask_rebuilds": int(stats["cache_mask_builds"]),
-                            "records": int(stats["cache_records"]),
-                            "note": "a prune changes the rows (full rebuild); the others follow the active mask"},
+                            "refreshes": int(stats["cache_refreshes"]), "records": int(stats["cache_records"]),
+                            "note": "a prune changes only the rows >= n_static: S0 is re-formed and the frozen part "
+                                    "kept (refresh) when all frozen rows lie below n_static; the rebuilds follow "
+                                    "the active mask"},
            "kernels_ms_per_step": {k: round(v["ms"] / kk, 4) for k, v in prof.items() if v["calls"]},
            "clocks": clk.summary()}
     opt.close()

@@ -149,6 +149,8 @@ typedef struct {
     int64_t n_fwd_exec;        /* (pixel, entry) evaluations the forward executed: entries walked by each
                                   warp x its pixels (a warp walks on until all its pixels terminated;
                                   compare n_fwd_evals) */
+    int64_t cache_refreshes;   /* static cache: fwds that re-formed S0 after a cls_prune_outside / cls_densify
+                                  and kept the frozen part (all its rows below n_static) */
 } cls_stats_t;
 
 #define CLS_PROF_GROUPS 20

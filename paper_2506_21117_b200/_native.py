@@ -67,7 +67,8 @@ class cls_stats_t(ctypes.Structure):
                 ("n_tested", ctypes.c_int64), ("n_live_units", ctypes.c_int64), ("cache_mode", ctypes.c_int32),
                 ("cache_valid", ctypes.c_int32), ("cache_builds", ctypes.c_int64), ("cache_mask_builds", ctypes.c_int64),
                 ("cache_records", ctypes.c_int64), ("cache_units", ctypes.c_int64), ("cache_rows", ctypes.c_int64),
-                ("n_tie_runs", ctypes.c_int64), ("n_fwd_exec", ctypes.c_int64)]
+                ("n_tie_runs", ctypes.c_int64), ("n_fwd_exec", ctypes.c_int64),
+                ("cache_refreshes", ctypes.c_int64)]
 
     def as_dict(self):
         return dict(n_active=self.n_active, n_records=self.n_records, n_pairs=self.n_pairs, n_items=self.n_items,
@@ -78,7 +79,8 @@ class cls_stats_t(ctypes.Structure):
                     n_live_units=self.n_live_units, cache_mode=self.cache_mode, cache_valid=self.cache_valid,
                     cache_builds=self.cache_builds, cache_mask_builds=self.cache_mask_builds,
                     cache_records=self.cache_records, cache_units=self.cache_units, cache_rows=self.cache_rows,
-                    n_tie_runs=self.n_tie_runs, n_fwd_exec=self.n_fwd_exec)
+                    n_tie_runs=self.n_tie_runs, n_fwd_exec=self.n_fwd_exec,
+                    cache_refreshes=self.cache_refreshes)
 
 
 class cls_profile_t(ctypes.Structure):

@@ -86,7 +86,8 @@ struct __align__(16) Rec {
 #define CACHE_SKIP (1 << 30)   // Counters.overflow of the cache build on a warm step: every gated kernel returns
 struct CacheState {
     int valid;          // a build exists for the current scene / views / regions (the host clears it)
-    int mode;           // this step: 0 warm, 1 rebuild for the mask (S0 kept), 2 rebuild with S0 := S0 u O^t
+    int mode;           // this step: 0 warm, 1 rebuild for the mask (S0 kept), 2 rebuild with S0 := S0 u O^t,
+                        // 3 refresh after a suffix operation (S0 re-formed, frozen part kept)
     int need;           // checks of this step: bit 0 the mask left the dilated mask, bit 1 an active row is not in S0
     int skip_full;      // 1 unless mode == 2 (scan skip flag of the S0 compaction)
     int A0;             // |S0|: rows projected every step (the only rows whose parameters can change)
@@ -102,6 +103,17 @@ struct CacheState {
     int dil;            // current dilation in tiles (grows by 2, up to 12, at every rebuild for the mask)
     int n_dcand;        // the step's staged (row, view) record candidates
     unsigned long long A0_total;   // scan total of the S0 compaction
+    // a library suffix operation (cls_prune_outside / cls_densify) changed only the rows [n_static, n):
+    // if every frozen row is below n_static the frozen part stands and only S0 is re-formed (mode 3,
+    // S0 := [n_static, n) u O^t); refresh_req is set by the next fwd and consumed by k_cache_decide
+    int refresh_req, refresh_nstatic;
+    int refresh_step;   // this step follows a suffix operation: S0 := [n_static, n) u O^t (mode 3, or mode 2
+                        // if the frozen part cannot stay) -- the step's row list already holds that suffix
+    int list_ok;        // S0 is current: membership and the step's rows may be limited to it (cleared by an
+                        // invalidation or a refresh request, set again when the step's cache work finished)
+    int fmaxgid;        // largest Gaussian index of a frozen record of the current build
+    int s0_union;       // the S0 compaction keeps the old S0 (mode 2 on a valid cache)
+    int refreshes;
 };
 
 struct CacheBufs {      // the cache's device buffers (passed by value)

@@ -47,6 +47,7 @@ struct cls_ctx {
     CacheState *h_cst = nullptr;   // pinned copy of the cache state after the last fwd
     std::vector<unsigned char> cache_sig;   // what the build depends on (host check -> invalidation)
     int cache_dilate = 2;
+    int64_t cache_refresh = -1;   // n_static of a suffix operation since the last fwd (-1: none)
     cudaStream_t body_stream = nullptr;   // captures the cache build into a conditional graph node
     StepDims dims{};
     CamSet cams{};
@@ -437,7 +438,9 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
             const unsigned char *b = (const unsigned char *)p;
             sig.insert(sig.end(), b, b + nb);
         };
-        put(&g->n, sizeof g->n); put(&g->sh_degree, sizeof g->sh_degree); put(&g->generation, sizeof g->generation);
+        put(&g->n, sizeof g->n); put(&g->generation, sizeof g->generation);   // first: a suffix op changes only these
+        const size_t head = sig.size();
+        put(&g->sh_degree, sizeof g->sh_degree);
         put(&g->mean_op, sizeof(void *)); put(&g->quat, sizeof(void *)); put(&g->log_scale, sizeof(void *));
         put(&g->sh, sizeof(void *));
         put(&n_views, sizeof n_views); put(&cs.W, sizeof(int)); put(&cs.H, sizeof(int));
@@ -448,15 +451,25 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
             put(&regs.set[j], sizeof(int));
         }
         if (sig != c->cache_sig) {
-            cudaMemsetAsync(&c->cb.st->valid, 0, sizeof(int), st);
+            // a suffix operation of this library (prune / densify) since the last fwd, and nothing else
+            // changed: the device keeps the frozen part if all its rows lie below n_static (mode 3)
+            const bool suffix_only = c->cache_refresh >= 0 && c->cache_refresh <= g->n &&
+                                     sig.size() == c->cache_sig.size() &&
+                                     std::equal(sig.begin() + head, sig.end(), c->cache_sig.begin() + head);
+            if (suffix_only && !getenv("CLS_NO_REFRESH")) launch_cache_refresh(c->cb, (int)c->cache_refresh, st);
+            else {
+                cudaMemsetAsync(&c->cb.st->valid, 0, sizeof(int), st);
+                cudaMemsetAsync(&c->cb.st->list_ok, 0, sizeof(int), st);
+            }
             c->cache_sig.swap(sig);
         }
+        c->cache_refresh = -1;
     }
     cudaMemsetAsync(s.cnt, 0, sizeof(Counters), st);
     run(c, P_MEMBER, st, [&] {
         if (cached) {   // full membership only until the cache is valid; then only S0's rows can be active
-            launch_member(p, d, regs, s, st, &c->cb.st->valid);
-            launch_member_list(p, c->cb.s0, &c->cb.st->A0, &c->cb.st->valid, regs, s, st);
+            launch_member(p, d, regs, s, st, &c->cb.st->list_ok);
+            launch_member_list(p, c->cb.s0, &c->cb.st->A0, &c->cb.st->list_ok, regs, s, st);
         } else {
             launch_member(p, d, regs, s, st);
         }
@@ -767,6 +780,7 @@ cls_status cls_stats(cls_ctx *c, cls_stats_t *out)
         out->cache_records = k.F;
         out->cache_units = k.Uf;
         out->cache_rows = k.A0;
+        out->cache_refreshes = k.refreshes;
     }
     if (out->overflow)
         return fail(c, CLS_ERR_CAPACITY, "capacity overflow (bits %d): records %d/%lld pairs %llu/%lld A %d/%lld",
@@ -1020,6 +1034,8 @@ static cls_status suffix_op(cls_ctx *c, int mode, float *mean_op, float *quat, f
     launch_suffix_apply(a, n_static, (int)S, tmp, c->d_work, c->d_tot, normals, st);
     if (mode == 1 && accum) launch_reset_stats(accum, count, n_new, st);   // 3DGS: stats restart
     *n = n_new;
+    // only rows >= n_static changed: a valid static cache may keep its frozen part (next fwd, mode 3)
+    if (c->cache_alloc) c->cache_refresh = c->cache_refresh < 0 ? n_static : std::min<int64_t>(c->cache_refresh, n_static);
     if (n_clone) *n_clone = (int64_t)tot[1];
     if (n_split) *n_split = (int64_t)tot[2];
     return check_cuda(c, name);

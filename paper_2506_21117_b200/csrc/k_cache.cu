@@ -42,25 +42,34 @@ __global__ void k_cache_decide(CacheBufs cb, int n, cudaGraphConditionalHandle c
 {
     CLS_PDL_WAIT();
     CacheState &c = *cb.st;
-    const int mode = !c.valid ? 2 : ((c.need & 2) ? 2 : ((c.need & 1) ? 1 : 0));
+    const bool req = c.refresh_req != 0;
+    // a suffix operation changed rows >= n_static only: the frozen part stands if all its rows lie below
+    // (and the mask is still inside the dilated one); S0's old row indices are stale either way
+    const bool refresh = req && c.valid && !(c.need & 1) && c.fmaxgid < c.refresh_nstatic;
+    const int mode = refresh ? 3 : ((!c.valid || req) ? 2 : ((c.need & 2) ? 2 : ((c.need & 1) ? 1 : 0)));
+    c.s0_union = mode == 2 && c.valid && !req;
+    c.refresh_step = req;
+    c.refresh_req = 0;
     // in a CUDA graph the build is the body of a conditional node: skipped whole on warm steps
     if (use_cond) cudaGraphSetConditional(cond, mode != 0 ? 1u : 0u);
     c.mode = mode;
-    c.skip_full = mode != 2;
-    c.skip_build = mode == 0;
+    c.skip_full = mode != 2 && mode != 3;
+    c.skip_build = mode == 0 || mode == 3;
     c.n = n;
     // the dilation adapts: a rebuild because the mask escaped means the active rects move faster than
     // the margin, so the next build gets 2 more tiles (up to 12)
     if (c.dil < cb.dilate) c.dil = cb.dilate;
     if (mode == 1) c.dil = min(c.dil + 2, 12);
-    if (mode) {
+    if (mode == 1 || mode == 2) {
         int *w = reinterpret_cast<int *>(cb.ccnt);
         for (int k = 0; k < (int)(sizeof(Counters) / sizeof(int)); k++) w[k] = 0;
         c.builds++;
+        c.fmaxgid = -1;
         if (mode == 1) c.mask_builds++;
         else c.full_builds++;
     } else {
-        cb.ccnt->overflow = CACHE_SKIP;
+        cb.ccnt->overflow = CACHE_SKIP;   // warm step, or a refresh (only the S0 compaction runs)
+        if (mode == 3) c.refreshes++;
     }
 }
 
@@ -68,16 +77,18 @@ __global__ void k_cache_decide(CacheBufs cb, int n, cudaGraphConditionalHandle c
 __global__ void __launch_bounds__(256) k_s0_flags(CacheBufs cb, Scratch s, int n)
 {
     CLS_PDL_WAIT();
-    if (cb.st->mode != 2) return;
-    const int valid = cb.st->valid;
+    const int mode = cb.st->mode;
+    if (mode != 2 && mode != 3) return;
+    const int uni = cb.st->s0_union;
+    const int ns = cb.st->refresh_step ? cb.st->refresh_nstatic : 0x7fffffff;   // after a suffix op: rows >= n_static
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        cb.flag[i] = ((valid && cb.dyn_of[i] >= 0) || s.ord[i] >= 0) ? 1u : 0u;
+        cb.flag[i] = ((uni && cb.dyn_of[i] >= 0) || s.ord[i] >= 0 || i >= ns) ? 1u : 0u;
 }
 
 __global__ void __launch_bounds__(256) k_s0_scatter(CacheBufs cb, int n)
 {
     CLS_PDL_WAIT();
-    if (cb.st->mode != 2) return;
+    if (cb.st->mode != 2 && cb.st->mode != 3) return;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const bool f = cb.flag[i] != 0u;
         const int e = (int)cb.excl[i];
@@ -137,6 +148,7 @@ __global__ void __launch_bounds__(256) k_cache_reorder(CacheBufs cb, Scratch sb)
         cb.cfvd[i] = sb.rskey[i] >> RK_IDX_BITS;
         cb.cfgid[i] = sb.rec_gid[rid];
         sb.srid[i] = (unsigned)i;
+        atomicMax(&cb.st->fmaxgid, sb.rec_gid[rid]);
     }
 }
 
@@ -165,13 +177,14 @@ __global__ void k_cache_finalize(CacheBufs cb, Scratch s, int n_seg)
 {
     CLS_PDL_WAIT();
     CacheState &c = *cb.st;
-    if (c.mode) {
+    if (c.mode == 1 || c.mode == 2) {
         c.ovf = cb.ccnt->overflow;
         c.F = min(cb.ccnt->n_records, (int)cb.Fcap);
         c.Uf = c.ovf ? 0 : cb.cseg_lb[n_seg];
         c.valid = 1;
     }
     c.need = 0;
+    c.list_ok = c.valid;
     if (c.ovf) atomicOr(&s.cnt->overflow, 8);
 }
 
@@ -436,18 +449,22 @@ __global__ void __launch_bounds__(256) k_merge_dyn(CacheBufs cb, Scratch s, cons
 //                  non-empty alpha-footprint rect is staged as a finished record candidate
 //   k_dyn_emit     after the mask tables: candidates whose rect holds an active tile become records
 // ---------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_dyn_list(CacheBufs cb, Scratch s)
+__global__ void __launch_bounds__(256) k_dyn_list(CacheBufs cb, Scratch s, int n)
 {
     CLS_PDL_WAIT();
     const int A = s.cnt->A;
-    const int A0 = cb.st->valid ? cb.st->A0 : 0;
+    // the current S0; on a refresh step (suffix operation) S0 is re-formed later in this step as
+    // [n_static, n) u O^t, so its suffix rows are listed here instead
+    const bool refresh = !cb.st->list_ok && cb.st->refresh_req;
+    const int ns = refresh ? min(cb.st->refresh_nstatic, n) : n;
+    const int A0 = cb.st->list_ok ? cb.st->A0 : (refresh ? n - ns : 0);
     const int total = max(A, A0);
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
         if (e < A) cb.dlist[e] = s.idx[e];
         bool extra = false;
         int r = 0;
         if (e < A0) {
-            r = cb.s0[e];
+            r = refresh ? ns + e : cb.s0[e];
             extra = s.ord[r] < 0;
         }
         const unsigned b = __ballot_sync(__activemask(), extra);
@@ -616,7 +633,7 @@ void launch_dyn_mask(const Params &g, const StepDims &d, const CamSet &cams, con
     cudaMemsetAsync(&cb.st->n_dyn_extra, 0, sizeof(int), st);
     cudaMemsetAsync(&cb.st->n_dcand, 0, sizeof(int), st);
     cudaMemsetAsync(s.mdiff, 0, sizeof(int) * (size_t)d.V * (d.TY + 1) * (d.TX + 1), st);
-    cls_launch(k_dyn_list, 148 * 2, 256, 0, st, cb, s);
+    cls_launch(k_dyn_list, 148 * 2, 256, 0, st, cb, s, d.n);
     cls_launch(k_dyn_rows, 148 * 2, 256, 0, st, cb, s, g.mean_op, g.quat, g.log_scale);
     const int grid = 148 * 3;
     switch (d.D) {
@@ -692,6 +709,19 @@ void launch_cache_build(const Params &g, const StepDims &d, const CamSet &cams, 
 void launch_cache_finalize(const StepDims &d, const CacheBufs &cb, const Scratch &s, cudaStream_t st)
 {
     cls_launch(k_cache_finalize, 1, 1, 0, st, cb, s, d.V * d.TY);
+    g_launches++;
+}
+
+__global__ void k_cache_refresh(CacheBufs cb, int n_static)
+{
+    cb.st->refresh_req = 1;
+    cb.st->refresh_nstatic = n_static;
+    cb.st->list_ok = 0;   // S0's row indices are stale: full membership, and the suffix joins the step's rows
+}
+
+void launch_cache_refresh(const CacheBufs &cb, int n_static, cudaStream_t st)
+{
+    k_cache_refresh<<<1, 1, 0, st>>>(cb, n_static);
     g_launches++;
 }
 

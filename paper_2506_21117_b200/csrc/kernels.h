@@ -65,6 +65,7 @@ void launch_cache_finalize(const StepDims &d, const CacheBufs &cb, const Scratch
 void launch_cache_merge(const StepDims &d, const CacheBufs &cb, const Scratch &sd, const unsigned long long *fsorted,
                         const unsigned long long *dsorted, unsigned long long *merged, bool vm, cudaStream_t st);
 void launch_dyn_pos(const CacheBufs &cb, const Scratch &sd, cudaStream_t st);
+void launch_cache_refresh(const CacheBufs &cb, int n_static, cudaStream_t st);
 // exact per-tile lists of the static cache (k_tiles.cu)
 const unsigned long long *launch_tile_lists(const StepDims &d, const unsigned long long *units, const int *n_units,
                                             const unsigned *rowmask, unsigned long long *buf_a,

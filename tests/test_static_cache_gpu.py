@@ -148,3 +148,39 @@ def test_cached_graph_rebuild_inside_replay(torch_cuda, monkeypatch):
     for k, x in enumerate(b):
         assert x["loss"] == x["ref_loss"], (k, x["loss"], x["ref_loss"])
     assert b[-1]["stats"]["cache_builds"] >= 2, b[-1]["stats"]   # the warm-up build + >= 1 inside a replay
+
+
+def test_cached_prune_refresh_keeps_frozen_part(torch_cuda):
+    """The c5 loop's form (P:509 sphere pruning of O^t): partitioned scene, cached steps, a prune after
+    steps 2 and 5.  A prune changes only the rows >= n_static, so the next fwd re-forms S0 := [n_static, n)
+    u O^t and keeps the frozen part (mode 3, no rebuild); every step's images and loss stay bit-identical
+    to an uncached ctx on the same parameters."""
+    import torch
+    from paper_2506_21117_b200 import GaussianParams, LocalOptimizer, default_limits
+    sc = SCENES["c3s"]()
+    p = GaussianParams.from_scene(sc)
+    lim = default_limits(sc.n, len(sc.cameras), sc.width, sc.height)
+    opt = LocalOptimizer(p, sc.regions, limits=lim, lr=(0.02,) * 6, static_cache=True)
+    n_static = opt.partition_static()
+    ref = LocalOptimizer(p, sc.regions, limits=lim, lr=(0.02,) * 6)
+    tg = torch.from_numpy(np.ascontiguousarray(sc.targets)).cuda()
+    modes, removed = [], 0
+    for k in range(8):
+        if k in (3, 6):
+            removed += opt.prune_outside()
+        r0 = ref.forward(sc.cameras, tg, images=True)
+        res = opt.forward(sc.cameras, tg, images=True)
+        torch.cuda.synchronize()
+        assert np.array_equal(res.images.cpu().numpy(), r0.images.cpu().numpy()), f"step {k} images"
+        assert float(res.loss.item()) == float(r0.loss.item()), k
+        st = opt.stats()
+        modes.append(st["cache_mode"])
+        g = opt.backward()
+        opt.adam(g)
+    torch.cuda.synchronize()
+    assert modes[3] == 3 and modes[6] == 3, modes
+    # no full rebuild after the first (a large learning rate may move the mask: mode-1 rebuilds are allowed)
+    assert st["cache_builds"] - st["cache_mask_builds"] == 1 and st["cache_refreshes"] == 2, st
+    assert 0 < n_static < p.n
+    ref.close()
+    opt.close()
