@@ -146,6 +146,8 @@ struct CacheBufs {      // the cache's device buffers (passed by value)
     int2 *tl_drng;      // [max items] per-item ranges of the step's tile lists
 };
 
+#define G2D_STRIDE 10   // doubles per (view, active Gaussian) in Scratch::grad2d (9 used; 16 B aligned rows)
+
 // all scratch of a ctx (device pointers), passed by value to kernels
 struct Scratch {
     // membership
@@ -194,7 +196,8 @@ struct Scratch {
     float *tgt;             // [items][3][256] target pixels gathered from host memory (k_gather_targets)
     float *item_loss;       // [items]
     // gradients
-    float4 *grad2d;         // [V][A][3]
+    double *grad2d;         // [V][A][G2D_STRIDE]: the raster's 9 per-view sums (dL/du, dL/dv, dL/dconic (3),
+                            // dL/dopacity, dL/dcolour (3)), fp64-accumulated warp partials
     uint8_t *vis;           // [V][max_active] active Gaussian has a record in the view (densification stats)
     long long max_active;
     Counters *cnt;

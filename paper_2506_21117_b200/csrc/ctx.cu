@@ -246,7 +246,7 @@ cls_status cls_create(cls_ctx **out, int device, const cls_limits *lim)
               dalloc(&s.rs_counts, (size_t)512 * RS_GRID) &&
               dalloc(&s.rs_totals, 512) && dalloc(&s.px_T, VT * 256) && dalloc(&s.px_last, VT * 256) &&
               dalloc(&s.px_dl, VT * 768) && dalloc(&s.tgt, VT * 768) && dalloc(&s.item_loss, VT) &&
-              dalloc(&s.grad2d, V * (size_t)lim->max_active * 3) &&
+              dalloc(&s.grad2d, V * (size_t)lim->max_active * G2D_STRIDE) &&
               dalloc(&s.vis, V * (size_t)lim->max_active) && dalloc(&s.cnt, 1);
     if (ok) ok = cudaMallocHost((void **)&c->h_cnt, sizeof(Counters)) == cudaSuccess &&
                  cudaMallocHost((void **)&c->h_A, sizeof(int)) == cudaSuccess;
@@ -827,8 +827,7 @@ cls_status cls_debug_grad2d(cls_ctx *c, float *out, void *stream)
     if (!c->bwd_valid) return fail(c, CLS_ERR_STATE, "cls_debug_grad2d before cls_render_bwd");
     if (c->captured) cudaDeviceSynchronize();
     else cudaEventSynchronize(c->ev_member);
-    const size_t bytes = sizeof(float4) * 3 * (size_t)c->dims.V * (size_t)(*c->h_A);
-    cudaMemcpyAsync(out, c->s.grad2d, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
+    launch_debug_grad2d(c->s, c->dims.V, *c->h_A, out, (cudaStream_t)stream);
     return check_cuda(c, "cls_debug_grad2d");
 }
 

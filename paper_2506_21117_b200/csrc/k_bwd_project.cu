@@ -74,10 +74,14 @@ __device__ __forceinline__ void bwd_project_row(const float4 *__restrict__ mean_
     for (int e = 0; e < 3 * K; e++) gsh[e] = 0.f;
 
     for (int v = 0; v < cams.n; v++) {
-        const float4 *g2p = s.grad2d + ((size_t)v * A + k) * 3;
-        const float4 ga = g2p[0], gb = g2p[1], gc = g2p[2];
-        if (ga.x == 0.f && ga.y == 0.f && ga.z == 0.f && ga.w == 0.f && gb.x == 0.f && gb.y == 0.f && gb.z == 0.f &&
-            gb.w == 0.f && gc.x == 0.f)
+        // the raster's per-view sums (fp64 accumulation of its warp partials: order independent)
+        const double2 *g2p = reinterpret_cast<const double2 *>(s.grad2d + ((size_t)v * A + k) * G2D_STRIDE);
+        const double2 g01 = g2p[0], g23 = g2p[1], g45 = g2p[2], g67 = g2p[3];
+        const double g8 = s.grad2d[((size_t)v * A + k) * G2D_STRIDE + 8];
+        const double4 ga = make_double4(g01.x, g01.y, g23.x, g23.y), gb = make_double4(g45.x, g45.y, g67.x, g67.y);
+        const double2 gc = make_double2(g8, 0.0);
+        if (ga.x == 0.0 && ga.y == 0.0 && ga.z == 0.0 && ga.w == 0.0 && gb.x == 0.0 && gb.y == 0.0 && gb.z == 0.0 &&
+            gb.w == 0.0 && gc.x == 0.0)
             continue;   // not seen by this view (or zero gradient: contributes nothing)
         const GCam &c = cams.c[v];
         const double R[9] = {c.R[0], c.R[1], c.R[2], c.R[3], c.R[4], c.R[5], c.R[6], c.R[7], c.R[8]};
@@ -155,7 +159,8 @@ __device__ __forceinline__ void bwd_project_row(const float4 *__restrict__ mean_
         float dir[3], Y[16], col[3];
         const float inv_len = view_dir(mo, c, dir);
         sh_color_raw<D>(sh, n, i, dir, Y, col);
-        const float grgb[3] = {col[0] < 0.f ? 0.f : gb.z, col[1] < 0.f ? 0.f : gb.w, col[2] < 0.f ? 0.f : gc.x};
+        const float grgb[3] = {col[0] < 0.f ? 0.f : (float)gb.z, col[1] < 0.f ? 0.f : (float)gb.w,
+                               col[2] < 0.f ? 0.f : (float)gc.x};
 #pragma unroll
         for (int e = 0; e < 3 * K; e++) gsh[e] += Y[e / 3] * grgb[e % 3];
         if (D > 0) {

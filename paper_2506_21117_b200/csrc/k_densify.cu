@@ -154,8 +154,8 @@ __global__ void k_densify_stats(Scratch s, int V, float sx, float sy, float *acc
         int c = 0;
         for (int v = 0; v < V; v++) {
             if (!s.vis[(size_t)v * s.max_active + k]) continue;
-            const float4 g = s.grad2d[((size_t)v * A + k) * 3];
-            const float gx = g.x * sx, gy = g.y * sy;
+            const double *g = s.grad2d + ((size_t)v * A + k) * G2D_STRIDE;
+            const float gx = (float)g[0] * sx, gy = (float)g[1] * sy;
             a += sqrtf(gx * gx + gy * gy);
             c++;
         }

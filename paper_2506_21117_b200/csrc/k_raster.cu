@@ -813,7 +813,8 @@ void launch_loss(const Scratch &s, float loss_scale, float *loss, cudaStream_t s
 //   dp/du = -(a dx + b dy), dp/dv = -(b dx + c dy), dp/da = -dx^2/2, dp/db = -dx dy, dp/dc = -dy^2/2
 // with dx = u - x, dy = v - y and the conic (a, b, c) = (a1^2 + b1^2, a1 a2 + b1 b2, a2^2 + b2^2) / kappa
 // of the raster's own exponent; summed over the thread's 4 pixels and the warp (shuffles), then
-// added into grad2d[v][ordinal] with float4 atomics.  Frozen entries only update T and S.
+// added into grad2d[v][ordinal] with fp64 atomics (the sum of the fp32 warp partials does not depend on
+// the order the tiles finish in: the gradients are reproducible).  Frozen entries only update T and S.
 // The alpha of every (pixel, entry) is recomputed with exactly the forward's operations.
 // ---------------------------------------------------------------------------
 // reduce-scatter over a warp of 9 per-lane values (padded to 16); returns, in lane l, the warp total
@@ -924,7 +925,7 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         if (ml >= first) atomicMax(&s_maxlast, ml);
         __syncthreads();
         const int end = s_maxlast + 1;   // exclusive
-        float4 *gbase = s.grad2d + (size_t)v * A * 3;
+        double *gbase = s.grad2d + (size_t)v * A * G2D_STRIDE;
         const f2_t fyp[2] = {pack2((float)ly, (float)(ly + 4)), pack2((float)(ly + 8), (float)(ly + 12))};
         // reverse walk over the row segment [first, end): batches of covering units, descending
         int cur = end, carry = 0;
@@ -1078,7 +1079,7 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
                     const float tot = warp_reduce_scatter9(r, lane);
                     const int qi = lane >> 1;
                     if ((lane & 1) == 0 && qi < 9)
-                        atomicAdd(reinterpret_cast<float *>(gbase + (size_t)ordk * 3) + qi, tot);
+                        atomicAdd(gbase + (size_t)ordk * G2D_STRIDE + qi, (double)tot);   // fp64: order independent
                 }
             }
         }
@@ -1218,9 +1219,28 @@ __global__ void k_zero_grad2d(Scratch s, int V, long long cap)
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&s.cnt->overflow, 4);
         return;
     }
-    const long long total = (long long)V * A * 3;
+    const long long total = (long long)V * A * (G2D_STRIDE / 2);
+    double2 *g = reinterpret_cast<double2 *>(s.grad2d);
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x)
-        s.grad2d[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+        g[e] = make_double2(0.0, 0.0);
+}
+
+// debug export (cls_debug_grad2d): the fp64 sums as the ABI's fp32 [V][A][12] layout (9 used)
+__global__ void k_debug_grad2d(Scratch s, int V, int A, float *out)
+{
+    CLS_PDL_WAIT();
+    const long long total = (long long)V * A * 12;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+        const long long r = e / 12;
+        const int q = (int)(e - r * 12);
+        out[e] = q < 9 ? (float)s.grad2d[r * G2D_STRIDE + q] : 0.f;
+    }
+}
+
+void launch_debug_grad2d(const Scratch &s, int V, int A, float *out, cudaStream_t st)
+{
+    cls_launch(k_debug_grad2d, 148 * 4, 256, 0, st, s, V, A, out);
+    g_launches++;
 }
 
 void launch_zero_grad2d(const StepDims &d, const Scratch &s, long long cap, cudaStream_t st)

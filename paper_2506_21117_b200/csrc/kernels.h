@@ -88,6 +88,7 @@ void launch_debug_records(const Scratch &s, const CacheBufs &cb, int cached, flo
 void launch_debug_tile_list(const Scratch &s, const CacheBufs &cb, int cached, int TY, int TX, int view, int tile,
                             int *out, int max, int *count, cudaStream_t st);
 void launch_zero_grad2d(const StepDims &d, const Scratch &s, long long cap, cudaStream_t st);
+void launch_debug_grad2d(const Scratch &s, int V, int A, float *out, cudaStream_t st);
 void launch_bwd_raster(const StepDims &d, const Scratch &s, const float *dL_dimages, float3 bg, cudaStream_t st);
 void launch_bwd_project(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s,
                         float *grad_active, cudaStream_t st);
