@@ -46,7 +46,7 @@ struct cls_ctx {
     long long cache_P = 0;
     CacheState *h_cst = nullptr;   // pinned copy of the cache state after the last fwd
     std::vector<unsigned char> cache_sig;   // what the build depends on (host check -> invalidation)
-    int cache_dilate = 2;
+    int cache_dilate = 4;   // tiles added around the active rects at a build (CLS_CACHE_DILATE)
     int64_t cache_refresh = -1;   // n_static of a suffix operation since the last fwd (-1: none)
     cudaStream_t body_stream = nullptr;   // captures the cache build into a conditional graph node
     StepDims dims{};
