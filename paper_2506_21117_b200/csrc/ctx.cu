@@ -616,7 +616,9 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     if (images) run(c, P_FILL, st, [&] { launch_fill_bg(d, s, images, bgc, st); });
     if (staged) {   // the loss terms need the gathered targets; the compositing above did not
         cudaStreamWaitEvent(st, c->ev_gather, 0);
-        run(c, P_LOSS, st, [&] { launch_loss_staged(d, cs, sr, loss_scale, st); });
+        run(c, P_LOSS, st, [&] {
+            launch_loss_staged(d, cs, sr, loss_scale, (flags & CLS_FLAG_TARGETS_U8) != 0, st);
+        });
     }
     if (targets && loss) run(c, P_LOSS, st, [&] { launch_loss(s, loss_scale, loss, st); });
     if (tile_mask) cudaMemcpyAsync(tile_mask, s.mask, (size_t)d.V * d.T, cudaMemcpyDeviceToDevice, st);

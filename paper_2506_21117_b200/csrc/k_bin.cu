@@ -424,14 +424,12 @@ void launch_gather_targets(const StepDims &d, const CamSet &cams, const Scratch 
 
 // 8-bit targets (CLS_FLAG_TARGETS_U8): one lane per (active tile, channel, pixel row) reads the row's
 // 16 bytes; the 32 lanes of a warp take 32 consecutive items of one (channel, row), i.e. mostly
-// adjacent tiles: 512 contiguous bytes.  k stands for the fp32 k / 255 (round to nearest).
+// adjacent tiles: 512 contiguous bytes.  The bytes are staged as they are (a quarter of the fp32
+// traffic on the device, one store per lane); k stands for the fp32 k / 255 (round to nearest).
 __global__ void __launch_bounds__(256) k_gather_targets_u8(const __grid_constant__ CamSet cams, Scratch s,
                                                            const unsigned char *__restrict__ targets)
 {
     CLS_PDL_WAIT();
-    __shared__ float lut[256];   // k -> k / 255 (IEEE division, round to nearest)
-    lut[threadIdx.x] = __fdiv_rn((float)threadIdx.x, 255.0f);
-    __syncthreads();
     const int n_items = s.cnt->overflow ? 0 : s.cnt->n_items;
     const int W = cams.W, H = cams.H, TX = cams.TX, T = cams.T;
     const size_t HW = (size_t)H * W;
@@ -447,24 +445,19 @@ __global__ void __launch_bounds__(256) k_gather_targets_u8(const __grid_constant
         const int e = s.items[item];
         const int v = e / T, t = e - v * T;
         const int x = (t % TX) * CLS_TILE, y = (t / TX) * CLS_TILE + row;
-        unsigned char b[16];
+        uint4 q = make_uint4(0u, 0u, 0u, 0u);
         if (y < H) {
             const unsigned char *src = targets + (size_t)v * 3 * HW + (size_t)ch * HW + (size_t)y * W + x;
             if (vec) {
-                const uint4 q = *reinterpret_cast<const uint4 *>(src);
-                *reinterpret_cast<uint4 *>(b) = q;
+                q = *reinterpret_cast<const uint4 *>(src);
             } else {
+                unsigned char *b = reinterpret_cast<unsigned char *>(&q);
 #pragma unroll
                 for (int k = 0; k < 16; k++) b[k] = x + k < W ? src[k] : 0;
             }
-        } else {
-#pragma unroll
-            for (int k = 0; k < 16; k++) b[k] = 0;
         }
-        float4 *dst = reinterpret_cast<float4 *>(s.tgt) + ((size_t)item * 3 + ch) * 64 + row * 4;
-#pragma unroll
-        for (int qd = 0; qd < 4; qd++)
-            dst[qd] = make_float4(lut[b[4 * qd]], lut[b[4 * qd + 1]], lut[b[4 * qd + 2]], lut[b[4 * qd + 3]]);
+        // kept as bytes ([item][ch][256] u8): k_loss_staged converts k -> k / 255 with the forward's table
+        reinterpret_cast<uint4 *>(s.tgt)[((size_t)item * 3 + ch) * 16 + row] = q;
     }
 }
 
@@ -473,7 +466,8 @@ void launch_gather_targets_u8(const StepDims &d, const CamSet &cams, const Scrat
 {
     // 32 CTAs (measured on c4 end to end: 16 -> 329, 32 -> 351, 64 -> 334, 128 -> 303 steps/s): enough
     // reads in flight for the link, few enough to leave the concurrent projection/binning its SMs
-    cls_launch(k_gather_targets_u8, 32, 256, 0, st, cams, s, targets);
+    static const int ctas = getenv("CLS_GATHER_CTAS") ? std::max(1, atoi(getenv("CLS_GATHER_CTAS"))) : 32;
+    cls_launch(k_gather_targets_u8, ctas, 256, 0, st, cams, s, targets);
     g_launches++;
 }
 

@@ -681,11 +681,16 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
 // host-resident targets: the fused-L1 epilogue of k_fwd, run once the gathered targets arrived
 // (the forward compositing itself does not wait for the host link).  Same thread <-> pixel map,
 // per-thread order and block reduction as k_fwd's epilogue: bit-identical loss and dL/dC.
+template <bool U8>
 __global__ void __launch_bounds__(RT_THREADS) k_loss_staged(const __grid_constant__ CamSet cams, Scratch s,
                                                             float loss_scale)
 {
     CLS_PDL_WAIT();
     __shared__ float red[RT_THREADS / 32];
+    __shared__ float s_u8[U8 ? 256 : 1];   // k -> k / 255 (fp32, IEEE division), as in k_fwd
+    if (U8)
+        for (int k = threadIdx.x; k < 256; k += blockDim.x) s_u8[k] = __fdiv_rn((float)k, 255.0f);
+    __syncthreads();
     if (s.cnt->overflow) return;
     const int n_items = s.cnt->n_items;
     const int tid = threadIdx.x;
@@ -702,9 +707,16 @@ __global__ void __launch_bounds__(RT_THREADS) k_loss_staged(const __grid_constan
             if (x < W && yy < H) {
                 const int pl = tid + p * RT_THREADS;
                 float *dl = s.px_dl + (size_t)item * 3 * CLS_BLOCK_PIX + pl;
-                const float *tg = s.tgt + (size_t)item * 3 * CLS_BLOCK_PIX + pl;
-                const float r0 = dl[0] - tg[0], r1 = dl[CLS_BLOCK_PIX] - tg[CLS_BLOCK_PIX],
-                            r2 = dl[2 * CLS_BLOCK_PIX] - tg[2 * CLS_BLOCK_PIX];
+                float t0, t1, t2;
+                if (U8) {   // staged bytes ([item][ch][256] u8)
+                    const unsigned char *tg = reinterpret_cast<const unsigned char *>(s.tgt) +
+                                              (size_t)item * 3 * CLS_BLOCK_PIX + pl;
+                    t0 = s_u8[tg[0]]; t1 = s_u8[tg[CLS_BLOCK_PIX]]; t2 = s_u8[tg[2 * CLS_BLOCK_PIX]];
+                } else {
+                    const float *tg = s.tgt + (size_t)item * 3 * CLS_BLOCK_PIX + pl;
+                    t0 = tg[0]; t1 = tg[CLS_BLOCK_PIX]; t2 = tg[2 * CLS_BLOCK_PIX];
+                }
+                const float r0 = dl[0] - t0, r1 = dl[CLS_BLOCK_PIX] - t1, r2 = dl[2 * CLS_BLOCK_PIX] - t2;
                 l1 += fabsf(r0) + fabsf(r1) + fabsf(r2);
                 dl[0] = r0 > 0.f ? loss_scale : (r0 < 0.f ? -loss_scale : 0.f);
                 dl[CLS_BLOCK_PIX] = r1 > 0.f ? loss_scale : (r1 < 0.f ? -loss_scale : 0.f);
@@ -716,9 +728,11 @@ __global__ void __launch_bounds__(RT_THREADS) k_loss_staged(const __grid_constan
     }
 }
 
-void launch_loss_staged(const StepDims &d, const CamSet &cams, const Scratch &s, float loss_scale, cudaStream_t st)
+void launch_loss_staged(const StepDims &d, const CamSet &cams, const Scratch &s, float loss_scale, bool u8,
+                        cudaStream_t st)
 {
-    cls_launch(k_loss_staged, 148 * 16, RT_THREADS, 0, st, cams, s, loss_scale);
+    if (u8) cls_launch(k_loss_staged<true>, 148 * 16, RT_THREADS, 0, st, cams, s, loss_scale);
+    else cls_launch(k_loss_staged<false>, 148 * 16, RT_THREADS, 0, st, cams, s, loss_scale);
     g_launches++;
 }
 

@@ -80,7 +80,8 @@ void launch_fwd(const StepDims &d, const CamSet &cams, const Scratch &s, const v
                 bool targets_staged, float *images, float loss_scale, float3 bg, cudaStream_t st);
 void launch_fill_bg(const StepDims &d, const Scratch &s, float *images, float3 bg, cudaStream_t st);
 void launch_loss(const Scratch &s, float loss_scale, float *loss, cudaStream_t st);
-void launch_loss_staged(const StepDims &d, const CamSet &cams, const Scratch &s, float loss_scale, cudaStream_t st);
+void launch_loss_staged(const StepDims &d, const CamSet &cams, const Scratch &s, float loss_scale, bool u8,
+                        cudaStream_t st);
 // (5) backward raster + backward projection                    (k_raster.cu, k_bwd_project.cu)
 void launch_debug_pixels(const StepDims &d, const CamSet &cams, const Scratch &s, float *out, cudaStream_t st);
 void launch_debug_records(const Scratch &s, const CacheBufs &cb, int cached, float *out, int *gid, int *view,
