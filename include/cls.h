@@ -151,6 +151,7 @@ typedef struct {
                                   compare n_fwd_evals) */
     int64_t cache_refreshes;   /* static cache: fwds that re-formed S0 after a cls_prune_outside / cls_densify
                                   and kept the frozen part (all its rows below n_static) */
+    int64_t cache_dilation;    /* tiles the current build grew the active rects by (the dilated mask) */
 } cls_stats_t;
 
 #define CLS_PROF_GROUPS 20

@@ -68,7 +68,7 @@ class cls_stats_t(ctypes.Structure):
                 ("cache_valid", ctypes.c_int32), ("cache_builds", ctypes.c_int64), ("cache_mask_builds", ctypes.c_int64),
                 ("cache_records", ctypes.c_int64), ("cache_units", ctypes.c_int64), ("cache_rows", ctypes.c_int64),
                 ("n_tie_runs", ctypes.c_int64), ("n_fwd_exec", ctypes.c_int64),
-                ("cache_refreshes", ctypes.c_int64)]
+                ("cache_refreshes", ctypes.c_int64), ("cache_dilation", ctypes.c_int64)]
 
     def as_dict(self):
         return dict(n_active=self.n_active, n_records=self.n_records, n_pairs=self.n_pairs, n_items=self.n_items,
@@ -80,7 +80,7 @@ class cls_stats_t(ctypes.Structure):
                     cache_builds=self.cache_builds, cache_mask_builds=self.cache_mask_builds,
                     cache_records=self.cache_records, cache_units=self.cache_units, cache_rows=self.cache_rows,
                     n_tie_runs=self.n_tie_runs, n_fwd_exec=self.n_fwd_exec,
-                    cache_refreshes=self.cache_refreshes)
+                    cache_refreshes=self.cache_refreshes, cache_dilation=self.cache_dilation)
 
 
 class cls_profile_t(ctypes.Structure):

@@ -114,6 +114,7 @@ struct CacheState {
     int fmaxgid;        // largest Gaussian index of a frozen record of the current build
     int s0_union;       // the S0 compaction keeps the old S0 (mode 2 on a valid cache)
     int refreshes;
+    int check_done;     // blocks of k_cache_check that finished (the last one decides, then resets it)
 };
 
 struct CacheBufs {      // the cache's device buffers (passed by value)

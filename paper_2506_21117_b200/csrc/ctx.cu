@@ -783,6 +783,7 @@ cls_status cls_stats(cls_ctx *c, cls_stats_t *out)
         out->cache_units = k.Uf;
         out->cache_rows = k.A0;
         out->cache_refreshes = k.refreshes;
+        out->cache_dilation = k.dil;
     }
     if (out->overflow)
         return fail(c, CLS_ERR_CAPACITY, "capacity overflow (bits %d): records %d/%lld pairs %llu/%lld A %d/%lld",

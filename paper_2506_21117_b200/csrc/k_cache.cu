@@ -23,24 +23,9 @@
 namespace cls {
 
 // ---- checks and decision ----
-__global__ void __launch_bounds__(256) k_cache_check(CacheBufs cb, Scratch s, int VT)
-{
-    CLS_PDL_WAIT();
-    const int A = s.cnt->A;
-    const int valid = cb.st->valid;
-    const int total = max(VT, A);
-    int need = 0;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-        if (e < VT && s.mask[e] && !cb.dmask[e]) need |= 1;
-        if (valid && e < A && cb.dyn_of[s.idx[e]] < 0) need |= 2;
-    }
-    need = __reduce_or_sync(0xffffffffu, need);
-    if ((threadIdx.x & 31) == 0 && need) atomicOr(&cb.st->need, need);
-}
 
-__global__ void k_cache_decide(CacheBufs cb, int n, cudaGraphConditionalHandle cond, int use_cond)
+__device__ __forceinline__ void cache_decide(const CacheBufs &cb, int n, cudaGraphConditionalHandle cond, int use_cond)
 {
-    CLS_PDL_WAIT();
     CacheState &c = *cb.st;
     const bool req = c.refresh_req != 0;
     // a suffix operation changed rows >= n_static only: the frozen part stands if all its rows lie below
@@ -70,6 +55,34 @@ __global__ void k_cache_decide(CacheBufs cb, int n, cudaGraphConditionalHandle c
     } else {
         cb.ccnt->overflow = CACHE_SKIP;   // warm step, or a refresh (only the S0 compaction runs)
         if (mode == 3) c.refreshes++;
+    }
+}
+
+// the checks over the mask and the active rows; the last block to finish decides (k_cache_decide's work
+// without a launch of its own: a fence, a ticket, the decision by the block that draws the last one)
+__global__ void __launch_bounds__(256) k_cache_check(CacheBufs cb, Scratch s, int VT, int n,
+                                                     cudaGraphConditionalHandle cond, int use_cond)
+{
+    CLS_PDL_WAIT();
+    __shared__ int s_last;
+    const int A = s.cnt->A;
+    const int valid = cb.st->valid;
+    const int total = max(VT, A);
+    int need = 0;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+        if (e < VT && s.mask[e] && !cb.dmask[e]) need |= 1;
+        if (valid && e < A && cb.dyn_of[s.idx[e]] < 0) need |= 2;
+    }
+    need = __reduce_or_sync(0xffffffffu, need);
+    if ((threadIdx.x & 31) == 0 && need) atomicOr(&cb.st->need, need);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(&cb.st->check_done, 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        __threadfence();
+        cb.st->check_done = 0;
+        cache_decide(cb, n, cond, use_cond);
     }
 }
 
@@ -442,14 +455,31 @@ __global__ void __launch_bounds__(256) k_merge_dyn(CacheBufs cb, Scratch s, cons
 // The step's own rows with the cache: ONE fp64 projection per (row, view), shared by the active mask
 // (rect corners of the active rows, modification 1) and the records ("reuse the computed
 // projection"), instead of one in k_active_rects and another in k_project_exact.
-//   k_dyn_list     rows: O^t (idx order), then the rows of the valid S0 that are not active this step
-//   k_dyn_rows     per row: M = R(q^) diag(exp l), opacity, the alpha >= 1/255 cut (fp64, once per row)
+//   k_dyn_list     rows: O^t (idx order), then the rows of the valid S0 that are not active this step, and
+//                  per listed row M = R(q^) diag(exp l), opacity, the alpha >= 1/255 cut (fp64, once per row)
 //   k_dyn_project  per (row, view): the projection (same fp64 definitions as k_project_exact); active
 //                  rows add their rect to the mask's corner differences; every (row, view) with a
 //                  non-empty alpha-footprint rect is staged as a finished record candidate
 //   k_dyn_emit     after the mask tables: candidates whose rect holds an active tile become records
 // ---------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_dyn_list(CacheBufs cb, Scratch s, int n)
+// one listed row's per-row terms: M = R(q^) diag(exp l), opacity, the alpha >= 1/255 cut (fp64)
+__device__ __forceinline__ void dyn_row_terms(const CacheBufs &cb, int k, int i, const float4 *__restrict__ mean_op,
+                                              const float4 *__restrict__ quat, const float4 *__restrict__ log_scale)
+{
+    double M[9];
+    gauss_m64(__ldg(quat + i), __ldg(log_scale + i), M);
+    double *o = cb.dM + (size_t)k * 12;
+    for (int q = 0; q < 9; q++) o[q] = M[q];
+    const double o64 = 1.0 / (1.0 + exp(-(double)__ldg(mean_op + i).w));
+    o[9] = o64;
+    o[10] = 2.0 * log(255.0 * o64) * (1.0 + 1e-6) + 2e-3;
+    o[11] = 0.0;
+}
+
+// the step's rows (O^t in idx order, then the rows of S0 that are not active this step) and their per-row
+// terms, in one pass (each listed row's terms are computed by the thread that lists it)
+__global__ void __launch_bounds__(256) k_dyn_list(CacheBufs cb, Scratch s, int n, const float4 *__restrict__ mean_op,
+                                                  const float4 *__restrict__ quat, const float4 *__restrict__ log_scale)
 {
     CLS_PDL_WAIT();
     const int A = s.cnt->A;
@@ -460,7 +490,11 @@ __global__ void __launch_bounds__(256) k_dyn_list(CacheBufs cb, Scratch s, int n
     const int A0 = cb.st->list_ok ? cb.st->A0 : (refresh ? n - ns : 0);
     const int total = max(A, A0);
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-        if (e < A) cb.dlist[e] = s.idx[e];
+        if (e < A) {
+            const int i = s.idx[e];
+            cb.dlist[e] = i;
+            dyn_row_terms(cb, e, i, mean_op, quat, log_scale);
+        }
         bool extra = false;
         int r = 0;
         if (e < A0) {
@@ -473,28 +507,13 @@ __global__ void __launch_bounds__(256) k_dyn_list(CacheBufs cb, Scratch s, int n
             int base = 0;
             if (lane == leader) base = atomicAdd(&cb.st->n_dyn_extra, __popc(b));
             base = __shfl_sync(b, base, leader);
-            cb.dlist[A + base + __popc(b & ((1u << lane) - 1u))] = r;
+            const int k = A + base + __popc(b & ((1u << lane) - 1u));
+            cb.dlist[k] = r;
+            dyn_row_terms(cb, k, r, mean_op, quat, log_scale);
         }
     }
 }
 
-__global__ void __launch_bounds__(256) k_dyn_rows(CacheBufs cb, Scratch s, const float4 *__restrict__ mean_op,
-                                                  const float4 *__restrict__ quat, const float4 *__restrict__ log_scale)
-{
-    CLS_PDL_WAIT();
-    const int n = s.cnt->A + cb.st->n_dyn_extra;
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-        const int i = cb.dlist[k];
-        double M[9];
-        gauss_m64(__ldg(quat + i), __ldg(log_scale + i), M);
-        double *o = cb.dM + (size_t)k * 12;
-        for (int q = 0; q < 9; q++) o[q] = M[q];
-        const double o64 = 1.0 / (1.0 + exp(-(double)__ldg(mean_op + i).w));
-        o[9] = o64;
-        o[10] = 2.0 * log(255.0 * o64) * (1.0 + 1e-6) + 2e-3;
-        o[11] = 0.0;
-    }
-}
 
 template <int D>
 __global__ void __launch_bounds__(256, 3) k_dyn_project(CacheBufs cb, Scratch s, const float4 *__restrict__ mean_op,
@@ -633,8 +652,7 @@ void launch_dyn_mask(const Params &g, const StepDims &d, const CamSet &cams, con
     cudaMemsetAsync(&cb.st->n_dyn_extra, 0, sizeof(int), st);
     cudaMemsetAsync(&cb.st->n_dcand, 0, sizeof(int), st);
     cudaMemsetAsync(s.mdiff, 0, sizeof(int) * (size_t)d.V * (d.TY + 1) * (d.TX + 1), st);
-    cls_launch(k_dyn_list, 148 * 2, 256, 0, st, cb, s, d.n);
-    cls_launch(k_dyn_rows, 148 * 2, 256, 0, st, cb, s, g.mean_op, g.quat, g.log_scale);
+    cls_launch(k_dyn_list, 148 * 2, 256, 0, st, cb, s, d.n, g.mean_op, g.quat, g.log_scale);
     const int grid = 148 * 3;
     switch (d.D) {
     case 0: cls_launch(k_dyn_project<0>, grid, 256, 0, st, cb, s, g.mean_op, g.sh, d.n, cams); break;
@@ -642,7 +660,7 @@ void launch_dyn_mask(const Params &g, const StepDims &d, const CamSet &cams, con
     case 2: cls_launch(k_dyn_project<2>, grid, 256, 0, st, cb, s, g.mean_op, g.sh, d.n, cams); break;
     default: cls_launch(k_dyn_project<3>, grid, 256, 0, st, cb, s, g.mean_op, g.sh, d.n, cams); break;
     }
-    g_launches += 3;
+    g_launches += 2;
     launch_sat_only(d, cams, s, nullptr, st);
 }
 
@@ -658,10 +676,8 @@ void launch_dyn_emit(const StepDims &d, const CacheBufs &cb, const Scratch &sd, 
 void launch_cache_check(const CacheBufs &cb, const StepDims &d, const Scratch &s, cudaStream_t st,
                         cudaGraphConditionalHandle cond, int use_cond)
 {
-    cudaMemsetAsync(&cb.st->need, 0, sizeof(int), st);
-    cls_launch(k_cache_check, 148 * 2, 256, 0, st, cb, s, d.V * d.T);
-    cls_launch(k_cache_decide, 1, 1, 0, st, cb, d.n, cond, use_cond);
-    g_launches += 2;
+    cls_launch(k_cache_check, 148 * 2, 256, 0, st, cb, s, d.V * d.T, d.n, cond, use_cond);   // need: reset by finalize
+    g_launches += 1;
 }
 
 void launch_cache_build(const Params &g, const StepDims &d, const CamSet &cams, const CacheBufs &cb,

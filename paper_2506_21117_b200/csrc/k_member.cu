@@ -96,53 +96,60 @@ void launch_member(const Params &g, const StepDims &d, const RegSet &regs, const
 // cache"), so their ord stays -1 from the last full membership.  Persistent blocks claim tiles of the
 // list in ticket order (the look-back only waits on earlier tickets).  Runs only while the cache is
 // valid (*valid != 0); the full k_member runs otherwise.
-__global__ void __launch_bounds__(MEMBER_THREADS)
+#define MLIST_THREADS 1024   // the list version: 8192 rows per tile, so S0 (~12k rows on c4) is 2 tiles:
+                             // a look-back chain of 2 instead of 7 (the chain's latency is the kernel's time)
+__global__ void __launch_bounds__(MLIST_THREADS)
 k_member_list(const float4 *__restrict__ mean_op, const int *__restrict__ list, const int *__restrict__ n_list,
               const int *__restrict__ valid, const __grid_constant__ RegSet regs, Scratch s)
 {
     CLS_PDL_WAIT();
+    constexpr int NW = MLIST_THREADS / 32, CELLS = MEMBER_ITEMS * NW, CPL = CELLS / 32, TILE = MLIST_THREADS * MEMBER_ITEMS;
     __shared__ int s_tile;
-    __shared__ int s_wcnt[MEMBER_ITEMS][MEMBER_THREADS / 32];
+    __shared__ int s_wcnt[CELLS];   // cell k * NW + warp: element order base + k * MLIST_THREADS + tid
     __shared__ unsigned long long s_prefix;
     if (!*valid) return;
     const int n = *n_list;
-    const int ntiles = (n + MEMBER_TILE - 1) / MEMBER_TILE;
+    const int ntiles = (n + TILE - 1) / TILE;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     while (true) {
         if (tid == 0) s_tile = atomicAdd(&s.cnt->member_tiles, 1);
         __syncthreads();
         const int tile = s_tile;
         if (tile >= ntiles) break;
-        const int base = tile * MEMBER_TILE;
+        const int base = tile * TILE;
         unsigned ballots[MEMBER_ITEMS];
         int rows[MEMBER_ITEMS];
 #pragma unroll
         for (int k = 0; k < MEMBER_ITEMS; k++) {
-            const int e = base + k * MEMBER_THREADS + tid;
+            const int e = base + k * MLIST_THREADS + tid;
             unsigned sm = 0u;
             rows[k] = e < n ? list[e] : -1;
             if (e < n) sm = region_sets(__ldg(mean_op + rows[k]), regs);
             if (e < n) s.setmask[rows[k]] = sm;
             ballots[k] = __ballot_sync(0xffffffffu, sm != 0u);
-            if (lane == 0) s_wcnt[k][warp] = __popc(ballots[k]);
+            if (lane == 0) s_wcnt[k * NW + warp] = __popc(ballots[k]);
         }
         __syncthreads();
-        if (warp == 0) {
-            const int nw = MEMBER_THREADS / 32;
-            const int total_cells = MEMBER_ITEMS * nw;
-            int v0 = lane < total_cells ? s_wcnt[lane / nw][lane % nw] : 0;
-            int v1 = lane + 32 < total_cells ? s_wcnt[(lane + 32) / nw][(lane + 32) % nw] : 0;
-            int inc0 = v0, inc1 = v1;
-            for (int o = 1; o < 32; o <<= 1) {
-                int t0 = __shfl_up_sync(0xffffffffu, inc0, o);
-                int t1 = __shfl_up_sync(0xffffffffu, inc1, o);
-                if (lane >= o) { inc0 += t0; inc1 += t1; }
+        if (warp == 0) {   // exclusive scan of the cells (CPL consecutive cells per lane), then the look-back
+            int v[CPL], sum = 0;
+#pragma unroll
+            for (int q = 0; q < CPL; q++) {
+                v[q] = s_wcnt[lane * CPL + q];
+                sum += v[q];
             }
-            const int tot0 = __shfl_sync(0xffffffffu, inc0, 31);
-            inc1 += tot0;
-            if (lane < total_cells) s_wcnt[lane / nw][lane % nw] = inc0 - v0;
-            if (lane + 32 < total_cells) s_wcnt[(lane + 32) / nw][(lane + 32) % nw] = inc1 - v1;
-            const int agg = __shfl_sync(0xffffffffu, inc1, 31);
+            int inc = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += t;
+            }
+            int ex = inc - sum;
+#pragma unroll
+            for (int q = 0; q < CPL; q++) {
+                s_wcnt[lane * CPL + q] = ex;
+                ex += v[q];
+            }
+            const int agg = __shfl_sync(0xffffffffu, inc, 31);
             const unsigned long long pre = lookback_warp(s.st_member, tile, (unsigned long long)agg);
             if (lane == 0) {
                 s_prefix = pre;
@@ -156,7 +163,7 @@ k_member_list(const float4 *__restrict__ mean_op, const int *__restrict__ list, 
         for (int k = 0; k < MEMBER_ITEMS; k++) {
             if (rows[k] < 0) continue;
             const bool in = (ballots[k] >> lane) & 1u;
-            const int pos = prefix + s_wcnt[k][warp] + __popc(ballots[k] & lt);
+            const int pos = prefix + s_wcnt[k * NW + warp] + __popc(ballots[k] & lt);
             if (in) s.idx[pos] = rows[k];
             s.ord[rows[k]] = in ? pos : -1;
         }
@@ -167,7 +174,7 @@ k_member_list(const float4 *__restrict__ mean_op, const int *__restrict__ list, 
 void launch_member_list(const Params &g, const int *list, const int *n_list, const int *valid, const RegSet &regs,
                         const Scratch &s, cudaStream_t st)
 {
-    cls_launch(k_member_list, 148 * 2, MEMBER_THREADS, 0, st, g.mean_op, list, n_list, valid, regs, s);
+    cls_launch(k_member_list, 148, MLIST_THREADS, 0, st, g.mean_op, list, n_list, valid, regs, s);
     g_launches++;
 }
 

@@ -48,6 +48,7 @@ def test_record_stage_parity(torch_cuda, name, cached):
     sc = SCENES[name]()
     opt, mask = _run(sc, cached)
     rec, gid, view, count = opt.debug_records(4_000_000)
+    dil = int(opt.stats()["cache_dilation"]) if cached else 0
     opt.close()
     assert count == len(gid) and count > 0
     assert len(set(zip(view.tolist(), gid.tolist()))) == count, "one record per (view, Gaussian)"
@@ -76,13 +77,14 @@ def test_record_stage_parity(torch_cuda, name, cached):
         assert np.all((x0 >= orc[:, 0]) & (y0 >= orc[:, 1]) & (x1 <= orc[:, 2]) & (y1 <= orc[:, 3]))
         assert np.all((x1 > x0) & (y1 > y0))
         # each record's rect reaches an active tile (cached frozen records: a tile of the dilated mask
-        # they were built against, the active tiles grown by 2 tiles)
+        # they were built against, the active rects grown by the build's dilation)
         m = mask[v]
         if cached:
-            mp = np.pad(m, 2)
+            assert dil >= 1
+            mp = np.pad(m, dil)
             m = np.zeros_like(m)
-            for dy in range(5):
-                for dx in range(5):
+            for dy in range(2 * dil + 1):
+                for dx in range(2 * dil + 1):
                     m |= mp[dy:dy + mask.shape[1], dx:dx + mask.shape[2]]
         for k in range(0, len(g), max(1, len(g) // 400)):
             assert m[y0[k]:y1[k], x0[k]:x1[k]].any()
