@@ -69,6 +69,13 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # nvidia-smi's start-up (NVML init) can stall this process's driver calls for a long moment:
+            # let it finish before the timed region (the loop's host work -- prunes, re-captures -- would
+            # otherwise absorb it)
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 5.0:
+                time.sleep(0.02)
+            self.rows.clear()
         except Exception:
             self.proc = None
         return self
@@ -595,10 +602,11 @@ def run_loop(args):
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     prunes, removed, captures = 0, 0, 0
+    gs = GraphStep(opt, cams, tg)   # the first capture is set-up (its host time is not a step's)
+    captures += 1
     with ClockSampler(0) as clk:
         torch.cuda.synchronize()
         e0.record(stream)
-        gs = None
         for k in range(args.steps):
             if k > 0 and k % args.prune_every == 0:
                 removed += opt.prune_outside()     # O^t rows whose centre left the spheres
