@@ -449,8 +449,11 @@ def run_ours(args):
 
 
 # kernel names of the profile groups in the ncu captures committed under profiles/
-GROUP_KERNELS = {"fwd_raster": "k_fwd<1, 0>", "project_cand": "k_project_cand<1>", "project_exact": "k_project_exact<3>",
-                 "bwd_raster": "k_bwd", "emit": "k_units", "bin_count": "k_permute"}
+# the kernel names in the ncu summaries (with the static cache's exact tile lists the raster kernels
+# carry the TL template argument; the uncached names are the fallback)
+GROUP_KERNELS = {"fwd_raster": ("k_fwd<1, 0, 1>", "k_fwd<1, 0, 0>", "k_fwd<1, 0>"),
+                 "project_cand": ("k_project_cand<1>",), "project_exact": ("k_project_exact<3>",),
+                 "bwd_raster": ("k_bwd<1>", "k_bwd<0>", "k_bwd"), "emit": ("k_units",), "bin_count": ("k_permute",)}
 
 
 def ncu_traffic(config: str, group: str):
@@ -459,15 +462,18 @@ def ncu_traffic(config: str, group: str):
     import glob
     import re
 
-    def version(path):   # r<round>_v<n>_...: newest = highest (round, n), compared as numbers
-        m = re.match(r"r(\d+)_v(\d+)", os.path.basename(path))
-        return (int(m.group(1)), int(m.group(2))) if m else (-1, -1)
+    def version(path):   # r<round>_v<n>_... or r<round>_final_...: newest = highest (round, n), final last
+        m = re.match(r"r(\d+)_(?:v(\d+)|(final))", os.path.basename(path))
+        if not m:
+            return (-1, -1)
+        return (int(m.group(1)), 1 << 30 if m.group(3) else int(m.group(2)))
 
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_{config}_ncu_traffic.json")), key=version)
     if not files or group not in GROUP_KERNELS:
         return None
     try:
-        rec = json.load(open(files[-1])).get(GROUP_KERNELS[group])
+        table = json.load(open(files[-1]))
+        rec = next((table[k] for k in GROUP_KERNELS[group] if k in table), None)
         return None if rec is None else {"bytes": int(rec["dram_bytes"]), "source": os.path.basename(files[-1])}
     except Exception:
         return None
