@@ -347,7 +347,8 @@ def run_ours(args):
         dom = max(per, key=lambda k: per[k]["ms"]) if per else None
         step_ms_sum = sum(v["ms"] for v in per.values())
         work = algorithmic_work(sc, len(cams), stats,
-                                tiles=bool(args.static_cache) and not os.environ.get("CLS_NO_TL"))
+                                tiles=(bool(args.static_cache) and not os.environ.get("CLS_NO_TL")) and
+                                ("sort" if os.environ.get("CLS_TL_SORT") else "direct"))
         groups = {}
         for k, v in per.items():
             avg_ms = v["ms"] / v["calls"]
@@ -506,8 +507,13 @@ def algorithmic_work(sc, n_views, st, tiles=False):
         # key-only passes (record id packed in the key); with the static cache's exact tile lists (k_tiles.cu)
         # the step's units are cut into (tile, record) pairs instead: count (8 in, 4 out), scan (4 + 4),
         # emit (8 + 4 in, 8 out per pair), the key-only pair sort by tile, item ranges + merge keys
-        # (8 in, 4 dpos, 8 out per pair)
-        "pair_sort": ("hbm", (U * 28 + P * 8 + tpasses * P * 16 + P * 20) if tiles else (upasses * U * 16 + U * 8)),
+        # (8 in, 4 dpos, 8 out per pair).  Direct lists (default): the records' row counts scanned (4 + 4), two
+        # passes over the records (64 B each) and their units' row-mask words, a 4 B count per pair, the tiles'
+        # scan (4 + 4 per tile), 4 + 8 + 4 B per placed pair, then the per-tile order: 8 + 4 in, 4 rank
+        # position, 8 out per pair
+        "pair_sort": ("hbm", (R * 8 + 2 * (R * 64 + U * 4) + P * 4 + V * TY * (-(-sc.width // 16)) * 8 + P * 16 +
+                              P * 24) if tiles == "direct" else
+                      (U * 28 + P * 8 + tpasses * P * 16 + P * 20) if tiles else (upasses * U * 16 + U * 8)),
         "fwd_raster": ("alu", st["n_fwd_evals"] * FWD_FLOPS_PER_EVAL),
         "bwd_raster": ("alu", st["n_bwd_evals"] * BWD_FLOPS_PER_EVAL),
         "bwd_project": ("hbm", A * V * 48 + A * (48 + 16 * K4) + A * 16 * (3 + K4)),

@@ -70,6 +70,8 @@ struct Counters {
     unsigned long long fwd_evals;   // (pixel, list entry) evaluations of the forward
     unsigned long long bwd_evals;   // (pixel, list entry) evaluations of the backward walk
     unsigned long long fwd_exec;    // (pixel, entry) evaluations the forward executed (entries walked x the warp's pixels)
+    int n_big_items;        // direct tile lists: items queued for k_tl_dsort_big
+    int big_work;           // k_tl_dsort_big's item ticket
 };
 
 // One (Gaussian, view) record, 64 B = two full 32 B sectors per random access.
@@ -145,6 +147,9 @@ struct CacheBufs {      // the cache's device buffers (passed by value)
     int *smp_g;                  // ... and their Gaussian indices
     int *tl_foff;       // [V*T + 1] per-tile ranges of the frozen tile lists
     int2 *tl_drng;      // [max items] per-item ranges of the step's tile lists
+    unsigned *icnt;     // [V*T] direct lists: the step's pairs per work item
+    unsigned *ioff;     // [V*T] ... their exclusive offsets (end offsets after k_tl_dscatter)
+    int *ibig;          // [V*T][2] (offset, count) of the items of more than 64 pairs (k_tl_dsort_big)
 };
 
 #define G2D_STRIDE 10   // doubles per (view, active Gaussian) in Scratch::grad2d (9 used; 16 B aligned rows)

@@ -192,7 +192,7 @@ cls_status cls_destroy(cls_ctx *c)
         if (p) cudaFree(p);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     void *cp[] = {c->cb.st, c->cb.ccnt, c->cb.dyn_of, c->cb.s0, c->cb.flag, c->cb.excl, c->cb.scan_status, c->cb.dmask,
-                  c->cb.dmdiff, c->cb.urec, c->cb.cfvd, c->cb.cfgid, c->cb.cseg_lb, c->cb.dpos, c->cb.db, c->cb.dq, c->cb.dmi, c->cb.mitems, c->cb.dlist, c->cb.dM, c->cb.dcand, c->cb.dcinfo, c->cb.tl_foff, c->cb.tl_drng, c->cb.smp_k, c->cb.smp_g, c->d_dsat,
+                  c->cb.dmdiff, c->cb.urec, c->cb.cfvd, c->cb.cfgid, c->cb.cseg_lb, c->cb.dpos, c->cb.db, c->cb.dq, c->cb.dmi, c->cb.mitems, c->cb.dlist, c->cb.dM, c->cb.dcand, c->cb.dcinfo, c->cb.tl_foff, c->cb.tl_drng, c->cb.icnt, c->cb.ioff, c->cb.ibig, c->cb.smp_k, c->cb.smp_g, c->d_dsat,
                   c->d_drowmask, c->d_dbbox, c->d_cukey, c->d_cukey_alt};
     for (void *p : cp)
         if (p) cudaFree(p);
@@ -293,6 +293,7 @@ static cls_status cache_allocate(cls_ctx *c)
               dalloc(&c->d_cukey, P) && dalloc(&c->d_cukey_alt, P) && dalloc(&cb.dq, P) && dalloc(&cb.dmi, P) && dalloc(&cb.dlist, N) &&
               dalloc(&cb.dM, N * 12) && dalloc(&cb.dcand, (size_t)Dcap) && dalloc(&cb.dcinfo, (size_t)Dcap) &&
               dalloc(&cb.mitems, P / 4096 + NSEG + 1) && dalloc(&cb.tl_foff, VT + 1) && dalloc(&cb.tl_drng, VT) &&
+              dalloc(&cb.icnt, VT) && dalloc(&cb.ioff, VT) && dalloc(&cb.ibig, 2 * VT) &&
               dalloc(&cb.smp_k, (size_t)R / 1024 + 2) && dalloc(&cb.smp_g, (size_t)R / 1024 + 2) &&
               cudaMallocHost((void **)&c->h_cst, sizeof(CacheState)) == cudaSuccess;
     if (!ok) {
@@ -569,7 +570,19 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
         sd.rec = cb.urec + cb.Fcap;
         sd.max_records = cb.Dcap;
         cudaMemsetAsync(s.vis, 0, (size_t)d.V * (size_t)s.max_active, st);
-        run(c, P_PROJECT_EXACT, st, [&] { launch_dyn_emit(d, cb, sd, st); });   // the staged candidates vs the mask
+        // direct tile lists (default with the tile lists): the step's records are not sorted at all; their pairs
+        // are counted per tile and each tile's few entries are ordered on their own (k_cache.cu, k_tiles.cu)
+        const bool direct = g_tiles && !g_tl_sort;
+        // the staged candidates vs the mask
+        run(c, P_PROJECT_EXACT, st, [&] { launch_dyn_emit(d, cb, sd, st, false); });
+        const unsigned long long *tl_d = nullptr;
+        unsigned long long *dsorted = nullptr, *merged = s.ukey;
+        if (direct) {
+            sd.rskey = sd.rkey;   // unsorted (the debug exports read the record id from the key)
+            run(c, P_PAIRSORT, st, [&] {
+                tl_d = launch_dyn_tile_lists(d, cs, cb, sd, s.ukey_alt, cb.dq, s.ukey, cb.dmi, s.max_units, st);
+            });
+        } else {
         run(c, P_RECSORT, st, [&] { launch_bin_recsort(d, cs, sd, st); });
         run(c, P_BINCOUNT, st, [&] { launch_bin_count(d, cs, sd, st); });
         if (g_tiles) sd.ucnt = cb.dq;   // k_units counts each unit's active tiles for the tile lists
@@ -577,10 +590,9 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
         sd.ucnt = nullptr;
         // exact per-tile lists: the step's own pairs of the active tiles straight from its units (written in
         // sorted-record order, so the stable pair sort by tile keeps each tile's pairs in depth order: no unit sort)
-        unsigned long long *dsorted = g_tiles ? s.ukey : nullptr;
+        dsorted = g_tiles ? s.ukey : nullptr;
         if (!g_tiles) run(c, P_PAIRSORT, st, [&] { dsorted = launch_unit_sort(d, sd, st); });
-        unsigned long long *merged = dsorted == s.ukey ? s.ukey_alt : s.ukey;
-        const unsigned long long *tl_d = nullptr;
+        merged = dsorted == s.ukey ? s.ukey_alt : s.ukey;
         if (g_tiles) {
             run(c, P_CACHE_MERGE, st, [&] { launch_dyn_pos(cb, sd, st); });
             run(c, P_PAIRSORT, st, [&] {
@@ -590,6 +602,7 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
             });
         } else {
             run(c, P_CACHE_MERGE, st, [&] { launch_cache_merge(d, cb, sd, fsorted, dsorted, merged, g_vmerge, st); });
+        }
         }
         sr = s;
         sr.rec = cb.urec;

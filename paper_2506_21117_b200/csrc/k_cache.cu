@@ -225,6 +225,40 @@ __global__ void __launch_bounds__(256) k_cache_samples(CacheBufs cb)
     }
 }
 
+// frozen records ordered before (view, depth, gid) -- (key, gid) strictly less: the samples in shared
+// memory first, then one stride of the frozen keys
+__device__ __forceinline__ unsigned dyn_rank(const CacheBufs &cb, const unsigned long long *s_k, const int *s_g, int ns,
+                                             int S, int F, unsigned long long key, int gid)
+{
+    int c = 0, h = ns;   // samples strictly less
+    while (c < h) {
+        const int m = (c + h) >> 1;
+        if (s_k[m] < key || (s_k[m] == key && s_g[m] < gid)) c = m + 1;
+        else h = m;
+    }
+    int lo = c ? (c - 1) * S + 1 : 0, hi = c ? min(c * S, F) : 0;
+    while (lo < hi) {
+        const int m = (lo + hi) >> 1;
+        const unsigned long long fk = cb.cfvd[m];
+        if (fk < key || (fk == key && cb.cfgid[m] < gid)) lo = m + 1;
+        else hi = m;
+    }
+    return (unsigned)lo;
+}
+
+__device__ __forceinline__ int dyn_load_samples(const CacheBufs &cb, unsigned long long *s_k, int *s_g, int &S)
+{
+    const int F = cb.st->F;
+    S = dyn_smp_stride(F);
+    const int ns = (F + S - 1) / S;
+    for (int j = threadIdx.x; j < ns; j += blockDim.x) {
+        s_k[j] = cb.smp_k[j];
+        s_g[j] = cb.smp_g[j];
+    }
+    __syncthreads();
+    return ns;
+}
+
 __global__ void __launch_bounds__(256) k_dyn_pos(CacheBufs cb, Scratch sd)
 {
     CLS_PDL_WAIT();
@@ -233,32 +267,143 @@ __global__ void __launch_bounds__(256) k_dyn_pos(CacheBufs cb, Scratch sd)
     if (sd.cnt->overflow) return;
     const int D = min(sd.cnt->n_records, (int)sd.max_records);
     const int F = cb.st->F;
-    const int S = dyn_smp_stride(F), ns = (F + S - 1) / S;
-    for (int j = threadIdx.x; j < ns; j += blockDim.x) {
-        s_k[j] = cb.smp_k[j];
-        s_g[j] = cb.smp_g[j];
-    }
-    __syncthreads();
+    int S;
+    const int ns = dyn_load_samples(cb, s_k, s_g, S);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D; i += gridDim.x * blockDim.x) {
         const unsigned rid = sd.srid[i];
         const unsigned long long key = sd.rskey[i] >> RK_IDX_BITS;   // (view, depth)
-        const int gid = sd.rec_gid[rid];
-        // frozen records ordered before (view, depth, gid): (key, gid) strictly less
-        int c = 0, h = ns;   // samples strictly less
-        while (c < h) {
-            const int m = (c + h) >> 1;
-            if (s_k[m] < key || (s_k[m] == key && s_g[m] < gid)) c = m + 1;
-            else h = m;
-        }
-        int lo = c ? (c - 1) * S + 1 : 0, hi = c ? min(c * S, F) : 0;
-        while (lo < hi) {
-            const int m = (lo + hi) >> 1;
-            const unsigned long long fk = cb.cfvd[m];
-            if (fk < key || (fk == key && cb.cfgid[m] < gid)) lo = m + 1;
-            else hi = m;
-        }
-        cb.dpos[rid] = (unsigned)lo;
+        cb.dpos[rid] = dyn_rank(cb, s_k, s_g, ns, S, F, key, sd.rec_gid[rid]);
     }
+}
+
+// The step's own tile lists without sorting its records ("direct" lists).  The records of the
+// step stay in creation order; their (record, tile row) units are enumerated through an exclusive scan of
+// the records' row counts (as k_units does for the sorted records: a warp takes 32 records, then their
+// units, lane = unit).  Per unit the footprint's active tiles in that row, then per (record, active tile):
+//   MODE 1: count the tile's pairs (icnt[view tile]); per record also its rank position among the frozen
+//           records (as k_dyn_pos)
+//   MODE 2: one entry at the tile's next free slot (ioff, exclusive offsets of icnt): keys = depth << 32 | Gaussian
+//           index (R13 order within the view), vals = record id.  k_tl_dsort (k_tiles.cu) orders each tile.
+// Both passes run the same footprint code on the same records: the same tile sets.
+#define DU_THREADS 256
+#define DU_WARPS (DU_THREADS / 32)
+#define DU_BATCH 4
+template <int MODE>
+__global__ void __launch_bounds__(DU_THREADS) k_dyn_units(const __grid_constant__ CamSet cams, CacheBufs cb, Scratch s,
+                                                          unsigned long long *__restrict__ keys,
+                                                          unsigned *__restrict__ vals, long long cap)
+{
+    CLS_PDL_WAIT();
+    __shared__ unsigned long long s_k[MODE == 1 ? DYN_SMP_MAX : 1];
+    __shared__ int s_g[MODE == 1 ? DYN_SMP_MAX : 1];
+    __shared__ float sf[DU_WARPS][9][32];      // u, v, ia, b, det, aQ, ey, dyr, mx
+    __shared__ unsigned si[DU_WARPS][3][32];   // x0 | x1 << 16, y0 | view << 16, unit offset
+    __shared__ unsigned long long sk[DU_WARPS][MODE == 2 ? 32 : 1];   // the record's sort key
+    __shared__ unsigned char sown[DU_WARPS][32];
+    if (s.cnt->overflow) return;
+    if (MODE == 2) {
+        const unsigned long long P = s.cnt->n_pairs;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            if ((long long)P > cap) atomicOr(&s.cnt->overflow, 2);
+            s.cnt->n_pairs32 = (int)min((unsigned long long)cap, P);
+        }
+        if ((long long)P > cap) return;
+    }
+    int S = 1, ns = 0;
+    const int F = cb.st->F;
+    if (MODE == 1) ns = dyn_load_samples(cb, s_k, s_g, S);
+    const int n = min(s.cnt->n_records, (int)s.max_records);
+    const int TX = cams.TX, TY = cams.TY, T = TX * TY, W32 = (TX + 31) >> 5;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    float (*Fm)[32] = sf[wid];
+    unsigned (*I)[32] = si[wid];
+    unsigned char *own = sown[wid];
+    for (int i0 = (blockIdx.x * DU_WARPS + wid) * 32; i0 < n; i0 += gridDim.x * DU_THREADS) {
+        const int i = i0 + lane;
+        unsigned o = 0xffffffffu, c = 0u;   // invalid lanes: an offset beyond every unit
+        if (i < n) {
+            o = s.roff[i];
+            c = s.rrows[i];
+            const unsigned long long key = s.rkey[i] >> RK_IDX_BITS;   // (view, depth)
+            const int view = (int)(key >> RK_DEPTH_BITS);
+            const FootRec f = foot_make(s.rec[i], view, (unsigned)i);
+            Fm[0][lane] = f.u; Fm[1][lane] = f.v; Fm[2][lane] = f.ia; Fm[3][lane] = f.b; Fm[4][lane] = f.det;
+            Fm[5][lane] = f.aQ; Fm[6][lane] = f.ey; Fm[7][lane] = f.dyr; Fm[8][lane] = f.mx;
+            I[0][lane] = (unsigned)f.x0 | ((unsigned)f.x1 << 16);
+            I[1][lane] = (unsigned)f.y0 | ((unsigned)view << 16);
+            if (MODE == 1) cb.dpos[i] = dyn_rank(cb, s_k, s_g, ns, S, F, key, s.rec_gid[i]);
+            if (MODE == 2) sk[wid][lane] = ((key & ((1ull << RK_DEPTH_BITS) - 1ull)) << 32) | (unsigned)s.rec_gid[i];
+        }
+        I[2][lane] = o;
+        __syncwarp();
+        const int last = min(31, n - 1 - i0);
+        const unsigned ubeg = __shfl_sync(0xffffffffu, o, 0);
+        const unsigned uend = __shfl_sync(0xffffffffu, o + c, last);
+        int carry = 0;
+        for (unsigned ub = ubeg; ub < uend; ub += 32) {
+            const bool st = c > 0u && o >= ub && o - ub < 32u;
+            __syncwarp();
+            if (st) own[o - ub] = (unsigned char)lane;
+            const unsigned Sm = __reduce_or_sync(0xffffffffu, st ? 1u << (o - ub) : 0u);
+            __syncwarp();
+            const unsigned m = Sm & (0xffffffffu >> (31 - lane));
+            const int j = m ? (int)own[31 - __clz(m)] : carry;
+            carry = __shfl_sync(0xffffffffu, j, 31);
+            const unsigned u = ub + lane;
+            if (u >= uend) break;
+            FootRec f;
+            f.u = Fm[0][j]; f.v = Fm[1][j]; f.ia = Fm[2][j]; f.b = Fm[3][j]; f.det = Fm[4][j];
+            f.aQ = Fm[5][j]; f.ey = Fm[6][j]; f.dyr = Fm[7][j]; f.mx = Fm[8][j];
+            const unsigned xs = I[0][j], yv = I[1][j];
+            f.x0 = (int)(xs & 0xffffu); f.x1 = (int)(xs >> 16);
+            const int view = (int)(yv >> 16), ty = (int)(yv & 0xffffu) + (int)(u - I[2][j]);
+            int lo, hi;
+            if (!foot_row(f, ty, lo, hi)) continue;
+            const unsigned *rm = s.rowmask + ((size_t)view * TY + ty) * W32;
+            const unsigned tbase = (unsigned)(view * T + ty * TX);
+            const unsigned long long key = MODE == 2 ? sk[wid][j] : 0ull;
+            const unsigned rid = (unsigned)(i0 + j);
+            for (int w = lo >> 5; w <= (hi >> 5); w++) {
+                unsigned bits = row_bits(rm, w, lo, hi);
+                if (MODE == 1) {
+                    while (bits) {
+                        atomicAdd(&cb.icnt[tbase + (unsigned)(32 * w + __ffs(bits) - 1)], 1u);
+                        bits &= bits - 1u;
+                    }
+                } else {
+                    while (bits) {   // up to DU_BATCH slot requests in flight before their stores
+                        unsigned slot[DU_BATCH];
+                        int nb = 0;
+#pragma unroll
+                        for (int q = 0; q < DU_BATCH; q++) {
+                            if (bits) {
+                                slot[q] = atomicAdd(&cb.ioff[tbase + (unsigned)(32 * w + __ffs(bits) - 1)], 1u);
+                                bits &= bits - 1u;
+                                nb = q + 1;
+                            }
+                        }
+#pragma unroll
+                        for (int q = 0; q < DU_BATCH; q++) {
+                            if (q < nb) {
+                                keys[slot[q]] = key;
+                                vals[slot[q]] = rid;
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
+void launch_dyn_units(const StepDims &d, const CamSet &cams, const CacheBufs &cb, const Scratch &sd, int mode,
+                      long long cap, unsigned long long *keys, unsigned *vals, cudaStream_t st)
+{
+    static const int grid = getenv("CLS_DU_GRID") ? atoi(getenv("CLS_DU_GRID")) : 148 * 8;
+    if (mode == 1) cls_launch(k_dyn_units<1>, grid, DU_THREADS, 0, st, cams, cb, sd, keys, vals, cap);
+    else cls_launch(k_dyn_units<2>, grid, DU_THREADS, 0, st, cams, cb, sd, keys, vals, cap);
+    g_launches++;
 }
 
 // the rank position of each live dynamic unit's record, in unit order (the merge's search keys)
@@ -606,10 +751,17 @@ __global__ void __launch_bounds__(256, 3) k_dyn_project(CacheBufs cb, Scratch s,
     }
 }
 
+// RANK (direct tile lists): also each record's rank position among the frozen records (as k_dyn_pos)
+template <bool RANK>
 __global__ void __launch_bounds__(256) k_dyn_emit(CacheBufs cb, Scratch s, int TX, int TY)
 {
     CLS_PDL_WAIT();
+    __shared__ unsigned long long s_k[RANK ? DYN_SMP_MAX : 1];
+    __shared__ int s_g[RANK ? DYN_SMP_MAX : 1];
     if (s.cnt->overflow) return;
+    int S = 1, ns = 0;
+    const int F = cb.st->F;
+    if (RANK) ns = dyn_load_samples(cb, s_k, s_g, S);
     const int nc = min(cb.st->n_dcand, (int)cb.Dcap);
     const int lane = threadIdx.x & 31, P = TX + 1;
     for (int b0 = blockIdx.x * blockDim.x; b0 < nc; b0 += gridDim.x * blockDim.x) {
@@ -643,6 +795,9 @@ __global__ void __launch_bounds__(256) k_dyn_emit(CacheBufs cb, Scratch s, int T
         if (ordi >= 0 && ordi < s.max_active) s.vis[(size_t)inf.y * s.max_active + ordi] = 1;
         s.rkey[slot] = ((unsigned long long)inf.y << RK_VIEW_SHIFT) | ((unsigned long long)(unsigned)inf.z << RK_IDX_BITS) |
                        (unsigned long long)slot;
+        if (RANK)
+            cb.dpos[slot] = dyn_rank(cb, s_k, s_g, ns, S, F,
+                                     ((unsigned long long)inf.y << RK_DEPTH_BITS) | (unsigned)inf.z, inf.x);
     }
 }
 
@@ -664,9 +819,10 @@ void launch_dyn_mask(const Params &g, const StepDims &d, const CamSet &cams, con
     launch_sat_only(d, cams, s, nullptr, st);
 }
 
-void launch_dyn_emit(const StepDims &d, const CacheBufs &cb, const Scratch &sd, cudaStream_t st)
+void launch_dyn_emit(const StepDims &d, const CacheBufs &cb, const Scratch &sd, cudaStream_t st, bool rank)
 {
-    cls_launch(k_dyn_emit, 148 * 4, 256, 0, st, cb, sd, d.TX, d.TY);
+    if (rank) cls_launch(k_dyn_emit<true>, 148 * 4, 256, 0, st, cb, sd, d.TX, d.TY);
+    else cls_launch(k_dyn_emit<false>, 148 * 4, 256, 0, st, cb, sd, d.TX, d.TY);
     g_launches++;
 }
 

@@ -15,6 +15,7 @@ int64_t g_launches = 0;
 bool g_pdl = getenv("CLS_NO_PDL") == nullptr;
 bool g_vmerge = getenv("CLS_NO_VMERGE") == nullptr;
 bool g_tiles = getenv("CLS_NO_TL") == nullptr;
+bool g_tl_sort = getenv("CLS_TL_SORT") != nullptr;
 
 #define MEMBER_THREADS 256
 #define MEMBER_ITEMS 8

@@ -314,7 +314,7 @@ k_scan_excl(const unsigned *__restrict__ in, unsigned *__restrict__ out, const i
     __shared__ int s_tile;
     __shared__ unsigned long long s_warp[SC_THREADS / 32];
     __shared__ unsigned long long s_prefix;
-    const int n = (skip && *skip) ? 0 : min(*n_ptr, max_n);
+    const int n = (skip && *skip) ? 0 : (n_ptr ? min(*n_ptr, max_n) : max_n);   // no count: max_n elements
     const int ntiles = (n + SC_TILE - 1) / SC_TILE;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     while (true) {

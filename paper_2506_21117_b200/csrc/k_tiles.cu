@@ -135,6 +135,195 @@ __global__ void __launch_bounds__(256) k_tl_items(const unsigned long long *__re
     }
 }
 
+// ---- the step's lists, direct (no record sort): order every tile's entries ----
+// k_dyn_units<2> (k_cache.cu) left each active tile's entries (key = depth << 32 | Gaussian index, val = record
+// id) unordered in [ioff - icnt, ioff).  The keys are distinct (one record per Gaussian and view), so an
+// entry's position in the R13 order (depth, index) is its rank: the number of smaller keys of its tile.
+//   k_tl_dsort      one warp per item: <= 32 entries by a register bitonic sort over the lanes, <= 64 by
+//                   counting; longer items are queued
+//   k_tl_dsort_big  one CTA per queued item: every thread counts the smaller depth words of its entries against
+//                   all the item's in shared memory (broadcast reads, 2 instructions per comparison; a depth
+//                   tie -- two equal ranks -- adds the equal-depth keys of smaller index); items beyond
+//                   DS_BCAP entries (none in the configs) by a bottom-up merge sort in global memory
+// Each writes (rank position among the frozen records << 32 | global record id) at the entry's rank.
+#define DS_WARPS 4
+#define DS_BCAP 2048
+#define DS_BIG_THREADS 128
+__device__ __forceinline__ void ds_out(const CacheBufs &cb, unsigned long long *rw, int pos, unsigned v, unsigned fbase)
+{
+    rw[pos] = ((unsigned long long)__ldg(cb.dpos + v) << 32) | (v + fbase);
+}
+
+// bitonic sort of 32 (key, value) pairs across the lanes of a warp (ascending by lane)
+__device__ __forceinline__ void ds_bitonic32(unsigned long long &k, unsigned &v, int lane)
+{
+#pragma unroll
+    for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+            const unsigned long long ok = __shfl_xor_sync(0xffffffffu, k, j);
+            const unsigned ov = __shfl_xor_sync(0xffffffffu, v, j);
+            const bool up = (lane & kk) == 0, lower = (lane & j) == 0;
+            if (lower == up ? ok < k : ok > k) {
+                k = ok;
+                v = ov;
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(32 * DS_WARPS) k_tl_dsort(CacheBufs cb, Scratch s, const unsigned long long *keys,
+                                                          const unsigned *vals, unsigned long long *rw, unsigned fbase)
+{
+    CLS_PDL_WAIT();
+    if (s.cnt->overflow) return;
+    const int n_items = s.cnt->n_items;
+    const int lane = threadIdx.x & 31;
+    for (int item = blockIdx.x * DS_WARPS + (threadIdx.x >> 5); item < n_items; item += gridDim.x * DS_WARPS) {
+        const int e = s.items[item];
+        const int m = (int)cb.icnt[e], end = (int)cb.ioff[e], off = end - m;
+        if (lane == 0) cb.tl_drng[item] = make_int2(off, end);
+        if (m == 0) continue;
+        if (m <= 32) {
+            unsigned long long k = lane < m ? keys[off + lane] : ~0ull;
+            unsigned v = lane < m ? vals[off + lane] : 0u;
+            ds_bitonic32(k, v, lane);
+            if (lane < m) ds_out(cb, rw, off + lane, v, fbase);
+        } else if (m <= 64) {
+            const unsigned long long x0 = keys[off + lane], x1 = lane + 32 < m ? keys[off + lane + 32] : ~0ull;
+            int r0 = 0, r1 = 0;
+            for (int j = 0; j < m; j++) {
+                const unsigned long long y = __shfl_sync(0xffffffffu, j < 32 ? x0 : x1, j & 31);
+                r0 += y < x0;
+                r1 += y < x1;
+            }
+            ds_out(cb, rw, off + r0, vals[off + lane], fbase);
+            if (lane + 32 < m) ds_out(cb, rw, off + r1, vals[off + lane + 32], fbase);
+        } else if (lane == 0) {
+            reinterpret_cast<int2 *>(cb.ibig)[atomicAdd(&s.cnt->n_big_items, 1)] = make_int2(off, m);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(DS_BIG_THREADS) k_tl_dsort_big(CacheBufs cb, Scratch s, unsigned long long *keys,
+                                                                 unsigned *vals, unsigned long long *rw, unsigned *alt_v,
+                                                                 unsigned fbase)
+{
+    CLS_PDL_WAIT();
+    __shared__ __align__(16) unsigned KH[DS_BCAP + 4];
+    __shared__ unsigned KL[DS_BCAP];
+    __shared__ unsigned VV[DS_BCAP];
+    __shared__ unsigned seen[DS_BCAP / 32];
+    __shared__ int s_tie, s_b;
+    if (s.cnt->overflow) return;
+    const int nb = s.cnt->n_big_items;
+    while (true) {   // items handed out dynamically: their costs differ by 50x
+        if (threadIdx.x == 0) s_b = atomicAdd(&s.cnt->big_work, 1);
+        __syncthreads();
+        const int b = s_b;
+        __syncthreads();
+        if (b >= nb) break;
+        const int2 om = reinterpret_cast<const int2 *>(cb.ibig)[b];
+        const int off = om.x, m = om.y;
+        if (m <= DS_BCAP) {
+            // the depth words alone first (distinct in almost every item): rank = #{y < x} by the sign of y - x
+            // (depth words < 2^31); equal depth words show up as equal ranks, and then the full keys decide
+            for (int i = threadIdx.x; i < m; i += DS_BIG_THREADS) {
+                const unsigned long long k = keys[off + i];
+                KH[i] = (unsigned)(k >> 32);
+                KL[i] = (unsigned)k;
+                VV[i] = vals[off + i];
+            }
+            for (int i = m + threadIdx.x; i < ((m + 3) & ~3); i += DS_BIG_THREADS) KH[i] = 0x7fffffffu;
+            for (int i = threadIdx.x; i < (m + 31) / 32; i += DS_BIG_THREADS) seen[i] = 0u;
+            if (threadIdx.x == 0) s_tie = 0;
+            __syncthreads();
+            const int m4 = (m + 3) >> 2;
+            int rr[DS_BCAP / DS_BIG_THREADS];
+#pragma unroll
+            for (int q = 0; q < DS_BCAP / DS_BIG_THREADS; q++) {
+                const int i = threadIdx.x + q * DS_BIG_THREADS;
+                if (q * DS_BIG_THREADS >= m) break;
+                const unsigned x = i < m ? KH[i] : 0x7fffffffu;
+                unsigned r = 0;
+#pragma unroll 4
+                for (int j = 0; j < m4; j++) {
+                    const uint4 y = reinterpret_cast<const uint4 *>(KH)[j];
+                    r += ((y.x - x) >> 31) + ((y.y - x) >> 31) + ((y.z - x) >> 31) + ((y.w - x) >> 31);
+                }
+                rr[q] = (int)r;
+                if (i < m) atomicOr(seen + (r >> 5), 1u << (r & 31));
+            }
+            __syncthreads();
+            for (int i = threadIdx.x; i < (m + 31) / 32; i += DS_BIG_THREADS) {
+                const int nbits = min(32, m - 32 * i);
+                if (seen[i] != (nbits == 32 ? 0xffffffffu : (1u << nbits) - 1u)) s_tie = 1;
+            }
+            __syncthreads();
+            const bool tie = s_tie != 0;
+#pragma unroll
+            for (int q = 0; q < DS_BCAP / DS_BIG_THREADS; q++) {
+                const int i = threadIdx.x + q * DS_BIG_THREADS;
+                if (q * DS_BIG_THREADS >= m) break;
+                if (i >= m) continue;
+                int r = rr[q];
+                if (tie) {   // equal depth words: add the equal-depth keys of smaller Gaussian index
+                    const unsigned xh = KH[i], xl = KL[i];
+                    for (int j = 0; j < m; j++) r += (KH[j] == xh) & (KL[j] < xl);
+                }
+                ds_out(cb, rw, off + r, VV[i], fbase);
+            }
+            __syncthreads();
+            continue;
+        }
+        // (rare) merge sort: (keys, vals) <-> (rw as keys, alt_v) over [off, end)
+        unsigned long long *sk = keys + off, *dk = rw + off;
+        unsigned *sv = vals + off, *dv = alt_v + off;
+        for (int w = 1; w < m; w <<= 1) {
+            for (int j = threadIdx.x; j < m; j += blockDim.x) {
+                const int blk = j & ~(2 * w - 1), mid = min(blk + w, m), e2 = min(blk + 2 * w, m);
+                const unsigned long long x = sk[j];
+                int lo = j < mid ? mid : blk, hi = j < mid ? e2 : mid;   // position among the other half
+                while (lo < hi) {
+                    const int q = (lo + hi) >> 1;
+                    if (sk[q] < x) lo = q + 1;
+                    else hi = q;
+                }
+                const int o = j < mid ? j + (lo - mid) : (j - mid) + lo;
+                dk[o] = x;
+                dv[o] = sv[j];
+            }
+            __syncthreads();
+            unsigned long long *tk = sk; sk = dk; dk = tk;
+            unsigned *tv = sv; sv = dv; dv = tv;
+        }
+        // the sorted values are in sv (a u32 buffer); rw may hold the sorted keys, which are no longer needed
+        for (int j = threadIdx.x; j < m; j += blockDim.x) ds_out(cb, rw, off + j, sv[j], fbase);
+        __syncthreads();
+    }
+}
+
+// the step's tile lists, direct: units of the unsorted records (row counts scanned) -> per-tile counts ->
+// tile offsets -> entries -> per-tile order.  keys, out: [cap] u64; vals, alt_v: [cap] u32.  Returns out.
+const unsigned long long *launch_dyn_tile_lists(const StepDims &d, const CamSet &cams, const CacheBufs &cb,
+                                                const Scratch &sd, unsigned long long *keys, unsigned *vals,
+                                                unsigned long long *out, unsigned *alt_v, long long cap, cudaStream_t st)
+{
+    const int VT = d.V * d.T;
+    scan_excl_u32(sd.rrows, sd.roff, &sd.cnt->n_records, (int)sd.max_records, sd.st_scan, &sd.cnt->scan_ticket,
+                  &sd.cnt->n_units, &sd.cnt->overflow, st);
+    cudaMemsetAsync(cb.icnt, 0, sizeof(unsigned) * (size_t)VT, st);
+    launch_dyn_units(d, cams, cb, sd, 1, cap, keys, vals, st);
+    scan_excl_u32(cb.icnt, cb.ioff, nullptr, VT, sd.st_scan, &sd.cnt->scan_ticket2, &sd.cnt->n_pairs,
+                  &sd.cnt->overflow, st);
+    launch_dyn_units(d, cams, cb, sd, 2, cap, keys, vals, st);
+    cls_launch(k_tl_dsort, 148 * 8, 32 * DS_WARPS, 0, st, cb, sd, (const unsigned long long *)keys,
+               (const unsigned *)vals, out, (unsigned)cb.Fcap);
+    cls_launch(k_tl_dsort_big, 148 * 12, DS_BIG_THREADS, 0, st, cb, sd, keys, vals, out, alt_v, (unsigned)cb.Fcap);
+    g_launches += 2;
+    return out;
+}
+
 static int tl_bits_for(long long x)
 {
     int b = 0;

@@ -55,7 +55,12 @@ void launch_sat_only(const StepDims &d, const CamSet &cams, const Scratch &s, co
 // static cache of the frozen rows' records and units (k_cache.cu)
 void launch_dyn_mask(const Params &g, const StepDims &d, const CamSet &cams, const CacheBufs &cb, const Scratch &s,
                      cudaStream_t st);
-void launch_dyn_emit(const StepDims &d, const CacheBufs &cb, const Scratch &sd, cudaStream_t st);
+void launch_dyn_emit(const StepDims &d, const CacheBufs &cb, const Scratch &sd, cudaStream_t st, bool rank);
+void launch_dyn_units(const StepDims &d, const CamSet &cams, const CacheBufs &cb, const Scratch &sd, int mode,
+                      long long cap, unsigned long long *keys, unsigned *vals, cudaStream_t st);
+const unsigned long long *launch_dyn_tile_lists(const StepDims &d, const CamSet &cams, const CacheBufs &cb, const Scratch &sd,
+                                                unsigned long long *keys, unsigned *vals, unsigned long long *out,
+                                                unsigned *alt_v, long long cap, cudaStream_t st);
 void launch_cache_check(const CacheBufs &cb, const StepDims &d, const Scratch &s, cudaStream_t st,
                         cudaGraphConditionalHandle cond = 0, int use_cond = 0);
 void launch_cache_build(const Params &g, const StepDims &d, const CamSet &cams, const CacheBufs &cb,
@@ -153,6 +158,7 @@ extern int64_t g_launches;   // kernels launched by this process through libcls 
 extern bool g_pdl;           // programmatic dependent launch on (CLS_NO_PDL=1 turns it off)
 extern bool g_vmerge;        // static cache: virtual merge in the raster (CLS_NO_VMERGE=1 materialises it)
 extern bool g_tiles;         // static cache: exact per-tile lists merged in the raster (CLS_NO_TL=1: row segments)
+extern bool g_tl_sort;       // the step's own lists through the record and pair sorts (CLS_TL_SORT=1) instead of direct
 
 // Every kernel of libcls starts with CLS_PDL_WAIT() and is launched by cls_launch with programmatic
 // stream serialization: a kernel's blocks may be scheduled while its predecessor in the stream drains,

@@ -1,0 +1,24 @@
+"""A few eager static-cache steps of a config (argv[1], default c4) with device 8-bit targets (for ncu launch lists)."""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, '.')
+import bench  # noqa: E402
+import synth  # noqa: E402
+from paper_2506_21117_b200 import GaussianParams, LocalOptimizer  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "c4"
+n_steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+sc = synth.make_scene(cfg)
+u8 = np.floor(np.asarray(sc.targets, np.float64) * 255.0 + 0.5).clip(0, 255).astype(np.uint8)
+params = GaussianParams.from_scene(sc, device="cuda:0")
+lim = bench.limits_for(cfg, sc.n, len(sc.cameras), sc.width, sc.height, False)
+opt = LocalOptimizer(params, sc.regions, limits=lim, static_cache=True)
+opt.spatial_order()
+td = torch.from_numpy(u8).cuda()
+for _ in range(n_steps):
+    opt.step(sc.cameras, td)
+torch.cuda.synchronize()
+print("ok")

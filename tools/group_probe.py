@@ -1,0 +1,30 @@
+"""Eager per-group times (cls_profile events) of warm static-cache steps, argv[1] config (default c4)."""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, '.')
+import bench  # noqa: E402
+import synth  # noqa: E402
+from paper_2506_21117_b200 import GaussianParams, LocalOptimizer  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "c4"
+sc = synth.make_scene(cfg)
+u8 = np.floor(np.asarray(sc.targets, np.float64) * 255.0 + 0.5).clip(0, 255).astype(np.uint8)
+params = GaussianParams.from_scene(sc, device="cuda:0")
+lim = bench.limits_for(cfg, sc.n, len(sc.cameras), sc.width, sc.height, False)
+opt = LocalOptimizer(params, sc.regions, limits=lim, static_cache=True)
+opt.spatial_order()
+td = torch.from_numpy(u8).cuda()
+for _ in range(3):
+    opt.step(sc.cameras, td)
+torch.cuda.synchronize()
+opt.profile(True)
+opt.profile_read()
+for _ in range(10):
+    opt.step(sc.cameras, td)
+torch.cuda.synchronize()
+pr = opt.profile_read()
+g = {k: round(v["ms"] / max(v["calls"], 1), 4) for k, v in pr.items() if v["calls"]}
+print(cfg, g, "sum", round(sum(g.values()), 4))
