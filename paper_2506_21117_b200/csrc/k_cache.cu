@@ -763,7 +763,7 @@ __global__ void __launch_bounds__(256) k_dyn_emit(CacheBufs cb, Scratch s, int T
     const int F = cb.st->F;
     if (RANK) ns = dyn_load_samples(cb, s_k, s_g, S);
     const int nc = min(cb.st->n_dcand, (int)cb.Dcap);
-    const int lane = threadIdx.x & 31, P = TX + 1;
+    const int lane = threadIdx.x & 31;
     for (int b0 = blockIdx.x * blockDim.x; b0 < nc; b0 += gridDim.x * blockDim.x) {
         const int e = b0 + threadIdx.x;
         bool keep = false;
@@ -773,8 +773,11 @@ __global__ void __launch_bounds__(256) k_dyn_emit(CacheBufs cb, Scratch s, int T
             R = cb.dcand[e];
             inf = cb.dcinfo[e];
             const int ra = __float_as_int(R.aux.z), rb = __float_as_int(R.aux.w);
-            const int *S = s.sat + (size_t)inf.y * (TY + 1) * P;
-            keep = sat_count(S, P, ra & 0xffff, ra >> 16, rb & 0xffff, rb >> 16) > 0;
+            const int x0 = ra & 0xffff, y0 = ra >> 16, x1 = (rb & 0xffff) - 1, y1 = rb >> 16;   // x1 inclusive
+            const int W32 = (TX + 31) >> 5;
+            const unsigned *rm = s.rowmask + (size_t)inf.y * TY * W32;
+            for (int y = y0; y < y1 && !keep; y++)   // any active tile in the rect (row bitmasks)
+                for (int w = x0 >> 5; w <= (x1 >> 5) && !keep; w++) keep = row_bits(rm + y * W32, w, x0, x1) != 0u;
         }
         const unsigned bal = __ballot_sync(0xffffffffu, keep);
         if (bal == 0u) continue;
@@ -816,7 +819,7 @@ void launch_dyn_mask(const Params &g, const StepDims &d, const CamSet &cams, con
     default: cls_launch(k_dyn_project<3>, grid, 256, 0, st, cb, s, g.mean_op, g.sh, d.n, cams); break;
     }
     g_launches += 2;
-    launch_sat_only(d, cams, s, nullptr, st);
+    launch_sat_only(d, cams, s, nullptr, st, false);   // k_dyn_emit tests the records against the row bitmasks
 }
 
 void launch_dyn_emit(const StepDims &d, const CacheBufs &cb, const Scratch &sd, cudaStream_t st, bool rank)

@@ -243,7 +243,9 @@ __device__ __forceinline__ void warp_prefix(int *a, int n, int st)
 // per row / column prefix (warp scans).  The tables and the mask live in shared memory (SMEM) when
 // they fit, else in global memory.
 #define SAT_THREADS 1024
-template <bool SMEM>
+// SAT = false (the static cache's warm step: its records are tested against the row bitmasks, k_dyn_emit):
+// the mask, its row bitmasks, bbox and count only
+template <bool SMEM, bool SAT = true>
 __global__ void __launch_bounds__(SAT_THREADS) k_sat(const __grid_constant__ CamSet cams, Scratch s, int all_tiles, const int *__restrict__ skip)
 {
     CLS_PDL_WAIT();
@@ -273,22 +275,24 @@ __global__ void __launch_bounds__(SAT_THREADS) k_sat(const __grid_constant__ Cam
         for (int t = threadIdx.x; t < TX * TY; t += blockDim.x) mk[t] = mkg[t];
     }
     __syncthreads();
-    // summed-area table of the mask: S[(y+1) P + x + 1] = active tiles in [0, x] x [0, y]
-    for (int k = threadIdx.x; k < (TY + 1) * P; k += blockDim.x) {
-        const int y = k / P, x = k - y * P;
-        S[k] = (y > 0 && x > 0) ? mk[(y - 1) * TX + x - 1] : 0;
+    if (SAT) {
+        // summed-area table of the mask: S[(y+1) P + x + 1] = active tiles in [0, x] x [0, y]
+        for (int k = threadIdx.x; k < (TY + 1) * P; k += blockDim.x) {
+            const int y = k / P, x = k - y * P;
+            S[k] = (y > 0 && x > 0) ? mk[(y - 1) * TX + x - 1] : 0;
+        }
+        __syncthreads();
+        for (int y = warp; y < TY; y += nw) warp_prefix(S + (y + 1) * P + 1, TX, 1);
+        __syncthreads();
+        for (int x = warp; x < TX; x += nw) warp_prefix(S + P + x + 1, TY, P);
+        __syncthreads();
+        if (SMEM)
+            for (int k = threadIdx.x; k < (TY + 1) * P; k += blockDim.x) Sg[k] = S[k];
+        if (threadIdx.x == 0) s.cnt->active_tiles[v] = S[TY * P + TX];
     }
-    __syncthreads();
-    for (int y = warp; y < TY; y += nw) warp_prefix(S + (y + 1) * P + 1, TX, 1);
-    __syncthreads();
-    for (int x = warp; x < TX; x += nw) warp_prefix(S + P + x + 1, TY, P);
-    __syncthreads();
-    if (SMEM)
-        for (int k = threadIdx.x; k < (TY + 1) * P; k += blockDim.x) Sg[k] = S[k];
-    if (threadIdx.x == 0) s.cnt->active_tiles[v] = S[TY * P + TX];
     // tile bbox of the active tiles (x0, y0, x1, y1 exclusive; empty: x1 <= x0)
-    __shared__ int s_bb[4];
-    if (threadIdx.x == 0) { s_bb[0] = TX; s_bb[1] = TY; s_bb[2] = 0; s_bb[3] = 0; }
+    __shared__ int s_bb[4], s_n;
+    if (threadIdx.x == 0) { s_bb[0] = TX; s_bb[1] = TY; s_bb[2] = 0; s_bb[3] = 0; s_n = 0; }
     __syncthreads();
     // row bitmasks of the active tiles (projection pass A): one ballot per 32 tiles of a row
     const int W32 = (TX + 31) >> 5;
@@ -299,11 +303,15 @@ __global__ void __launch_bounds__(SAT_THREADS) k_sat(const __grid_constant__ Cam
         const bool m = x < TX && mk[y * TX + x];
         const unsigned bits = __ballot_sync(0xffffffffu, m);
         if (lane == 0) rm[k] = bits;
+        if (!SAT && lane == 0 && bits) atomicAdd(&s_n, __popc(bits));
         if (m) { x0 = min(x0, x); y0 = min(y0, y); x1 = max(x1, x + 1); y1 = max(y1, y + 1); }
     }
     atomicMin(&s_bb[0], x0); atomicMin(&s_bb[1], y0); atomicMax(&s_bb[2], x1); atomicMax(&s_bb[3], y1);
     __syncthreads();
-    if (threadIdx.x == 0) s.view_bbox[v] = make_int4(s_bb[0], s_bb[1], s_bb[2], s_bb[3]);
+    if (threadIdx.x == 0) {
+        s.view_bbox[v] = make_int4(s_bb[0], s_bb[1], s_bb[2], s_bb[3]);
+        if (!SAT) s.cnt->active_tiles[v] = s_n;
+    }
 }
 
 void launch_active_mask(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st)
@@ -328,13 +336,21 @@ void launch_active_mask(const Params &g, const StepDims &d, const CamSet &cams, 
 
 // mask tables (summed-area table, row bitmasks, bbox) of the rect-corner differences already in s.mdiff;
 // skipped while *skip != 0 (the static cache's dilated mask, rebuilt only when the cache is)
-void launch_sat_only(const StepDims &d, const CamSet &cams, const Scratch &s, const int *skip, cudaStream_t st)
+void launch_sat_only(const StepDims &d, const CamSet &cams, const Scratch &s, const int *skip, cudaStream_t st, bool sat)
 {
     const size_t smem = sizeof(int) * (size_t)(d.TY + 1) * (d.TX + 1) + (size_t)d.TX * d.TY;
     static std::atomic<unsigned long long> attr{0};
-    per_device_once(attr, [] { cudaFuncSetAttribute(k_sat<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
-    if (smem <= 200 * 1024) cls_launch(k_sat<true>, d.V, SAT_THREADS, smem, st, cams, s, 0, skip);
-    else cls_launch(k_sat<false>, d.V, SAT_THREADS, 0, st, cams, s, 0, skip);
+    per_device_once(attr, [] {
+        cudaFuncSetAttribute(k_sat<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_sat<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    });
+    if (smem <= 200 * 1024) {
+        if (sat) cls_launch(k_sat<true>, d.V, SAT_THREADS, smem, st, cams, s, 0, skip);
+        else cls_launch(k_sat<true, false>, d.V, SAT_THREADS, smem, st, cams, s, 0, skip);
+    } else {
+        if (sat) cls_launch(k_sat<false>, d.V, SAT_THREADS, 0, st, cams, s, 0, skip);
+        else cls_launch(k_sat<false, false>, d.V, SAT_THREADS, 0, st, cams, s, 0, skip);
+    }
     g_launches++;
 }
 

@@ -51,7 +51,8 @@ void scan_excl_u32(const unsigned *in, unsigned *out, const int *n_ptr, int max_
 #define RS_GRID (148 * 4)
 
 unsigned long long *launch_unit_sort(const StepDims &d, Scratch &s, cudaStream_t st);
-void launch_sat_only(const StepDims &d, const CamSet &cams, const Scratch &s, const int *skip, cudaStream_t st);
+void launch_sat_only(const StepDims &d, const CamSet &cams, const Scratch &s, const int *skip, cudaStream_t st,
+                     bool sat = true);
 // static cache of the frozen rows' records and units (k_cache.cu)
 void launch_dyn_mask(const Params &g, const StepDims &d, const CamSet &cams, const CacheBufs &cb, const Scratch &s,
                      cudaStream_t st);
