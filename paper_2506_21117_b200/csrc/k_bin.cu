@@ -464,9 +464,10 @@ __global__ void __launch_bounds__(256) k_gather_targets_u8(const __grid_constant
 void launch_gather_targets_u8(const StepDims &d, const CamSet &cams, const Scratch &s, const unsigned char *targets,
                               cudaStream_t st)
 {
-    // 32 CTAs (measured on c4 end to end: 16 -> 329, 32 -> 351, 64 -> 334, 128 -> 303 steps/s): enough
-    // reads in flight for the link, few enough to leave the concurrent projection/binning its SMs
-    static const int ctas = getenv("CLS_GATHER_CTAS") ? std::max(1, atoi(getenv("CLS_GATHER_CTAS"))) : 32;
+    // 20 CTAs (c4 end to end, graph step over pinned host targets, round 2 after the direct tile lists:
+    // 16 -> 1.262, 20 -> 1.241, 24 -> 1.247, 28 -> 1.261, 32 -> 1.279, 48 -> 1.350 ms): enough reads in
+    // flight for the link, few enough not to stretch the latency-bound kernels of the concurrent front end
+    static const int ctas = getenv("CLS_GATHER_CTAS") ? std::max(1, atoi(getenv("CLS_GATHER_CTAS"))) : 20;
     cls_launch(k_gather_targets_u8, ctas, 256, 0, st, cams, s, targets);
     g_launches++;
 }
