@@ -459,14 +459,14 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
                                      std::equal(sig.begin() + head, sig.end(), c->cache_sig.begin() + head);
             if (suffix_only && !getenv("CLS_NO_REFRESH")) launch_cache_refresh(c->cb, (int)c->cache_refresh, st);
             else {
-                cudaMemsetAsync(&c->cb.st->valid, 0, sizeof(int), st);
-                cudaMemsetAsync(&c->cb.st->list_ok, 0, sizeof(int), st);
+                cls_memset(&c->cb.st->valid, 0, sizeof(int), st);
+                cls_memset(&c->cb.st->list_ok, 0, sizeof(int), st);
             }
             c->cache_sig.swap(sig);
         }
         c->cache_refresh = -1;
     }
-    cudaMemsetAsync(s.cnt, 0, sizeof(Counters), st);
+    cls_memset(s.cnt, 0, sizeof(Counters), st);
     run(c, P_MEMBER, st, [&] {
         if (cached) {   // full membership only until the cache is valid; then only S0's rows can be active
             launch_member(p, d, regs, s, st, &c->cb.st->list_ok);
@@ -503,7 +503,7 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     Scratch sr = s;   // what the raster reads (records, sorted units, segment ranges)
     if (!cached) {
         run(c, P_PROJECT, st, [&] { launch_project_cand(p, d, cs, s, st); });
-        cudaMemsetAsync(s.vis, 0, (size_t)d.V * (size_t)s.max_active, st);
+        cls_memset(s.vis, 0, (size_t)d.V * (size_t)s.max_active, st);
         run(c, P_PROJECT_EXACT, st, [&] { launch_project_exact(p, d, cs, s, st); });
         run(c, P_RECSORT, st, [&] { launch_bin_recsort(d, cs, s, st); });
         run(c, P_BINCOUNT, st, [&] { launch_bin_count(d, cs, s, st); });
@@ -569,7 +569,7 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
         Scratch sd = s;   // the step's own records: S0 x views, ids after the frozen ones
         sd.rec = cb.urec + cb.Fcap;
         sd.max_records = cb.Dcap;
-        cudaMemsetAsync(s.vis, 0, (size_t)d.V * (size_t)s.max_active, st);
+        cls_memset(s.vis, 0, (size_t)d.V * (size_t)s.max_active, st);
         // direct tile lists (default with the tile lists): the step's records are not sorted at all; their pairs
         // are counted per tile and each tile's few entries are ordered on their own (k_cache.cu, k_tiles.cu)
         const bool direct = g_tiles && !g_tl_sort;
@@ -853,7 +853,7 @@ cls_status cls_debug_pixels(cls_ctx *c, float *T_out, void *stream)
     if (!c->fwd_valid) return fail(c, CLS_ERR_STATE, "cls_debug_pixels before cls_render_fwd");
     cudaSetDevice(c->device);
     cudaStream_t st = (cudaStream_t)stream;
-    cudaMemsetAsync(T_out, 0xff, sizeof(float) * (size_t)c->dims.V * c->dims.H * c->dims.W, st);   // NaN: not rendered
+    cls_memset(T_out, 0xff, sizeof(float) * (size_t)c->dims.V * c->dims.H * c->dims.W, st);   // NaN: not rendered
     launch_debug_pixels(c->dims, c->cams, c->s, T_out, st);
     return check_cuda(c, "cls_debug_pixels");
 }

@@ -349,7 +349,7 @@ void launch_bin_items(const StepDims &d, Scratch &s, cudaStream_t st)
 {
     const int VT = d.V * d.T;
     const int blocks = (VT + TSCAN_TILE - 1) / TSCAN_TILE;
-    cudaMemsetAsync(s.st_tiles, 0, sizeof(unsigned long long) * blocks, st);
+    cls_memset(s.st_tiles, 0, sizeof(unsigned long long) * blocks, st);
     cls_launch(k_tiles_scan, blocks, TSCAN_THREADS, 0, st, VT, s);
     g_launches++;
 }
@@ -522,8 +522,8 @@ void launch_bin_pairsort(const StepDims &d, const CamSet &cams, Scratch &s, cuda
     const int w = radix_sort_u64(s.ukey, s.ukey_alt, nullptr, nullptr, &s.cnt->n_units32, (int)s.max_units,
                                  UK_SEG_SHIFT, UK_SEG_SHIFT + sbits, 8, s.rs_counts, s.rs_totals, &s.cnt->overflow, st);
     s.sukey = w ? s.ukey_alt : s.ukey;
-    cudaMemsetAsync(s.seg_off, 0, sizeof(int) * (size_t)n_seg, st);
-    cudaMemsetAsync(s.seg_end, 0, sizeof(int) * (size_t)n_seg, st);
+    cls_memset(s.seg_off, 0, sizeof(int) * (size_t)n_seg, st);
+    cls_memset(s.seg_end, 0, sizeof(int) * (size_t)n_seg, st);
     cls_launch(k_seg_ranges, 148 * 8, 256, 0, st, s, n_seg);
     g_launches += 1;
 }

@@ -87,7 +87,7 @@ void launch_member(const Params &g, const StepDims &d, const RegSet &regs, const
                    const int *skip)
 {
     const int blocks = (d.n + MEMBER_TILE - 1) / MEMBER_TILE;
-    cudaMemsetAsync(s.st_member, 0, sizeof(unsigned long long) * blocks, st);
+    cls_memset(s.st_member, 0, sizeof(unsigned long long) * blocks, st);
     cls_launch(k_member, blocks, MEMBER_THREADS, 0, st, g.mean_op, d.n, regs, s, skip);
     g_launches++;
 }
@@ -317,9 +317,9 @@ __global__ void __launch_bounds__(SAT_THREADS) k_sat(const __grid_constant__ Cam
 void launch_active_mask(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st)
 {
     if (d.all_tiles) {
-        cudaMemsetAsync(s.mask, 1, (size_t)d.V * d.T, st);
+        cls_memset(s.mask, 1, (size_t)d.V * d.T, st);
     } else {
-        cudaMemsetAsync(s.mdiff, 0, sizeof(int) * (size_t)d.V * (d.TY + 1) * (d.TX + 1), st);
+        cls_memset(s.mdiff, 0, sizeof(int) * (size_t)d.V * (d.TY + 1) * (d.TX + 1), st);
         // persistent over the A x V (Gaussian, view) pairs: 3 CTAs per SM fit its 78 registers
         int blocks = (int)std::min<long long>(((long long)d.n * d.V + 255) / 256, 148LL * 3);
         if (blocks < 1) blocks = 1;

@@ -386,12 +386,39 @@ k_scan_excl(const unsigned *__restrict__ in, unsigned *__restrict__ out, const i
     }
 }
 
+__global__ void __launch_bounds__(256) k_fill(unsigned char *p, unsigned word, size_t bytes)
+{
+    CLS_PDL_WAIT();
+    const size_t head = min(bytes, (size_t)((16 - (reinterpret_cast<size_t>(p) & 15)) & 15));
+    const size_t nv = (bytes - head) / 16, tail0 = head + nv * 16;
+    const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x, nt = (size_t)gridDim.x * blockDim.x;
+    const uint4 w4 = make_uint4(word, word, word, word);
+    uint4 *v = reinterpret_cast<uint4 *>(p + head);
+    for (size_t i = tid; i < nv; i += nt) v[i] = w4;
+    if (tid < head) p[tid] = (unsigned char)word;
+    if (tid < bytes - tail0) p[tail0 + tid] = (unsigned char)word;
+}
+
+void cls_memset(void *p, int byte, size_t bytes, cudaStream_t st)
+{
+    static const bool nodes = getenv("CLS_MEMSET_NODES") != nullptr;
+    if (nodes) {
+        cudaMemsetAsync(p, byte, bytes, st);
+        return;
+    }
+    if (bytes == 0) return;
+    const unsigned b = (unsigned)byte & 0xffu, word = b | (b << 8) | (b << 16) | (b << 24);
+    const size_t blocks = std::min<size_t>(std::max<size_t>((bytes / 16 + 255) / 256, 1), 148 * 4);
+    cls_launch(k_fill, (unsigned)blocks, 256, 0, st, reinterpret_cast<unsigned char *>(p), word, bytes);
+    g_launches++;
+}
+
 void scan_excl_u32(const unsigned *in, unsigned *out, const int *n_ptr, int max_n, unsigned long long *status,
                    int *ticket, unsigned long long *total, const int *skip, cudaStream_t st)
 {
     const int tiles = (max_n + SC_TILE - 1) / SC_TILE;
-    cudaMemsetAsync(status, 0, sizeof(unsigned long long) * (size_t)(tiles + 1), st);
-    cudaMemsetAsync(ticket, 0, sizeof(int), st);
+    cls_memset(status, 0, sizeof(unsigned long long) * (size_t)(tiles + 1), st);
+    cls_memset(ticket, 0, sizeof(int), st);
     cls_launch(k_scan_excl, 148 * 4, SC_THREADS, 0, st, in, out, n_ptr, max_n, status, ticket, total, skip);
     g_launches++;
 }

@@ -312,7 +312,7 @@ const unsigned long long *launch_dyn_tile_lists(const StepDims &d, const CamSet 
     const int VT = d.V * d.T;
     scan_excl_u32(sd.rrows, sd.roff, &sd.cnt->n_records, (int)sd.max_records, sd.st_scan, &sd.cnt->scan_ticket,
                   &sd.cnt->n_units, &sd.cnt->overflow, st);
-    cudaMemsetAsync(cb.icnt, 0, sizeof(unsigned) * (size_t)VT, st);
+    cls_memset(cb.icnt, 0, sizeof(unsigned) * (size_t)VT, st);
     launch_dyn_units(d, cams, cb, sd, 1, cap, keys, vals, st);
     scan_excl_u32(cb.icnt, cb.ioff, nullptr, VT, sd.st_scan, &sd.cnt->scan_ticket2, &sd.cnt->n_pairs,
                   &sd.cnt->overflow, st);
@@ -345,7 +345,7 @@ const unsigned long long *launch_tile_lists(const StepDims &d, const unsigned lo
                                             const int *skip, cudaStream_t st, bool counted)
 {
     const int n_seg = d.V * d.TY, W32 = (d.TX + 31) / 32, nT = d.V * d.T;
-    if (!off) cudaMemsetAsync(rng, 0, sizeof(int2) * (size_t)nT, st);
+    if (!off) cls_memset(rng, 0, sizeof(int2) * (size_t)nT, st);
     if (!counted) {
         cls_launch(k_tl_count, 148 * 8, 256, 0, st, units, n_units, n_seg, rowmask, W32, ucnt, skip);
         g_launches++;

@@ -185,4 +185,8 @@ inline void cls_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
     cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// cudaMemsetAsync as a PDL kernel (k_fill, k_sort.cu): a memset node between two kernels of a captured step
+// would break their programmatic overlap (CLS_MEMSET_NODES=1 keeps the memset nodes)
+void cls_memset(void *p, int byte, size_t bytes, cudaStream_t st);
+
 }  // namespace cls
