@@ -24,6 +24,8 @@ struct cls_ctx {
     int *h_A = nullptr;          // pinned
     cudaEvent_t ev_member = nullptr, ev_fwd = nullptr;
     cudaStream_t side = nullptr;                              // host-target gather stream
+    cudaStream_t aux = nullptr;                               // device-to-host copies off the step's chain
+    cudaEvent_t ev_fork[2] = {}, ev_copied[2] = {};
     cudaEvent_t ev_items = nullptr, ev_gather = nullptr;
     bool fwd_valid = false, has_targets = false, bwd_valid = false;
     bool captured = false;   // the last fwd was recorded into a CUDA graph: its events are not usable
@@ -185,6 +187,11 @@ cls_status cls_destroy(cls_ctx *c)
     if (c->ev_items) cudaEventDestroy(c->ev_items);
     if (c->ev_gather) cudaEventDestroy(c->ev_gather);
     if (c->side) cudaStreamDestroy(c->side);
+    if (c->aux) cudaStreamDestroy(c->aux);
+    for (int k = 0; k < 2; k++) {
+        if (c->ev_fork[k]) cudaEventDestroy(c->ev_fork[k]);
+        if (c->ev_copied[k]) cudaEventDestroy(c->ev_copied[k]);
+    }
     for (auto &r : c->prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     void *dp[] = {c->d_mo, c->d_q, c->d_ls, c->d_sh, c->d_m, c->d_v, c->d_acc, c->d_cnt, c->d_work, c->d_status,
                   c->d_tot, c->d_int, c->d_sums, c->d_k0, c->d_k1, c->d_v0, c->d_v1, c->d_starts};
@@ -254,7 +261,11 @@ cls_status cls_create(cls_ctx **out, int device, const cls_limits *lim)
                  cudaEventCreateWithFlags(&c->ev_fwd, cudaEventDisableTiming) == cudaSuccess &&
                  cudaEventCreateWithFlags(&c->ev_items, cudaEventDisableTiming) == cudaSuccess &&
                  cudaEventCreateWithFlags(&c->ev_gather, cudaEventDisableTiming) == cudaSuccess &&
-                 create_side_stream(&c->side) == cudaSuccess;
+                 create_side_stream(&c->side) == cudaSuccess &&
+                 cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) == cudaSuccess;
+    for (int k = 0; ok && k < 2; k++)
+        ok = cudaEventCreateWithFlags(&c->ev_fork[k], cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&c->ev_copied[k], cudaEventDisableTiming) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
         cls_destroy(c);
@@ -475,8 +486,14 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
             launch_member(p, d, regs, s, st);
         }
     });
-    cudaMemcpyAsync(c->h_A, &s.cnt->A, sizeof(int), cudaMemcpyDeviceToHost, st);
-    if (!c->captured) cudaEventRecord(c->ev_member, st);
+    // |O^t| to the host on a branch (joined at the end of the fwd): a copy node in the chain would break the
+    // programmatic overlap of the kernels around it.  A is final once k_member ran.
+    cudaEventRecord(c->ev_fork[0], st);
+    cudaStreamWaitEvent(c->aux, c->ev_fork[0], 0);
+    cudaMemcpyAsync(c->h_A, &s.cnt->A, sizeof(int), cudaMemcpyDeviceToHost, c->aux);
+    if (!c->captured) cudaEventRecord(c->ev_member, c->aux);
+    cudaEventRecord(c->ev_copied[0], c->aux);
+    bool cst_copied = false;
     run(c, P_MASK, st, [&] {
         if (cached) launch_dyn_mask(p, d, cs, c->cb, s, st);   // one projection of the step's rows (k_cache.cu)
         else launch_active_mask(p, d, cs, s, st);
@@ -623,7 +640,12 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
             sr.vm_dkey = merged;
         }
         c->s_rec = sd;
-        cudaMemcpyAsync(c->h_cst, cb.st, sizeof(CacheState), cudaMemcpyDeviceToHost, st);
+        // the cache state to the host on the branch (no kernel of this fwd writes it any more)
+        cudaEventRecord(c->ev_fork[1], st);
+        cudaStreamWaitEvent(c->aux, c->ev_fork[1], 0);
+        cudaMemcpyAsync(c->h_cst, cb.st, sizeof(CacheState), cudaMemcpyDeviceToHost, c->aux);
+        cudaEventRecord(c->ev_copied[1], c->aux);
+        cst_copied = true;
     }
     run(c, P_FWD, st, [&] { launch_fwd(d, cs, sr, targets, (flags & CLS_FLAG_TARGETS_U8) != 0, staged, images, loss_scale, bgc, st); });
     if (images) run(c, P_FILL, st, [&] { launch_fill_bg(d, s, images, bgc, st); });
@@ -635,6 +657,8 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     }
     if (targets && loss) run(c, P_LOSS, st, [&] { launch_loss(s, loss_scale, loss, st); });
     if (tile_mask) cudaMemcpyAsync(tile_mask, s.mask, (size_t)d.V * d.T, cudaMemcpyDeviceToDevice, st);
+    cudaStreamWaitEvent(st, c->ev_copied[0], 0);   // join the copy branch
+    if (cst_copied) cudaStreamWaitEvent(st, c->ev_copied[1], 0);
     cudaMemcpyAsync(c->h_cnt, s.cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st);
     if (!c->captured) cudaEventRecord(c->ev_fwd, st);
     cls_status e = check_cuda(c, "cls_render_fwd");
