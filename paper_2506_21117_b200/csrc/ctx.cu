@@ -493,7 +493,6 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     cudaMemcpyAsync(c->h_A, &s.cnt->A, sizeof(int), cudaMemcpyDeviceToHost, c->aux);
     if (!c->captured) cudaEventRecord(c->ev_member, c->aux);
     cudaEventRecord(c->ev_copied[0], c->aux);
-    bool cst_copied = false;
     run(c, P_MASK, st, [&] {
         if (cached) launch_dyn_mask(p, d, cs, c->cb, s, st);   // one projection of the step's rows (k_cache.cu)
         else launch_active_mask(p, d, cs, s, st);
@@ -640,12 +639,6 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
             sr.vm_dkey = merged;
         }
         c->s_rec = sd;
-        // the cache state to the host on the branch (no kernel of this fwd writes it any more)
-        cudaEventRecord(c->ev_fork[1], st);
-        cudaStreamWaitEvent(c->aux, c->ev_fork[1], 0);
-        cudaMemcpyAsync(c->h_cst, cb.st, sizeof(CacheState), cudaMemcpyDeviceToHost, c->aux);
-        cudaEventRecord(c->ev_copied[1], c->aux);
-        cst_copied = true;
     }
     run(c, P_FWD, st, [&] { launch_fwd(d, cs, sr, targets, (flags & CLS_FLAG_TARGETS_U8) != 0, staged, images, loss_scale, bgc, st); });
     if (images) run(c, P_FILL, st, [&] { launch_fill_bg(d, s, images, bgc, st); });
@@ -658,8 +651,7 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     if (targets && loss) run(c, P_LOSS, st, [&] { launch_loss(s, loss_scale, loss, st); });
     if (tile_mask) cudaMemcpyAsync(tile_mask, s.mask, (size_t)d.V * d.T, cudaMemcpyDeviceToDevice, st);
     cudaStreamWaitEvent(st, c->ev_copied[0], 0);   // join the copy branch
-    if (cst_copied) cudaStreamWaitEvent(st, c->ev_copied[1], 0);
-    cudaMemcpyAsync(c->h_cnt, s.cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st);
+    // (the counters and the cache state reach the host in cls_stats, synchronously: no copy node here)
     if (!c->captured) cudaEventRecord(c->ev_fwd, st);
     cls_status e = check_cuda(c, "cls_render_fwd");
     if (e != CLS_OK) return e;
@@ -785,9 +777,10 @@ cls_status cls_stats(cls_ctx *c, cls_stats_t *out)
     if ((c->captured ? cudaDeviceSynchronize() : cudaEventSynchronize(c->ev_fwd)) != cudaSuccess)
         return fail(c, CLS_ERR_CUDA, "fwd event: %s", cudaGetErrorString(cudaGetLastError()));
     if (c->last_stream) cudaStreamSynchronize(c->last_stream);
-    // refresh the overflow bit (bwd may have set bit 2)
-    int ovf = 0;
-    cudaMemcpy(&ovf, &c->s.cnt->overflow, sizeof(int), cudaMemcpyDeviceToHost);
+    // the counters as the last fwd (and bwd: overflow bit 2, its evaluations) left them
+    cudaMemcpy(c->h_cnt, c->s.cnt, sizeof(Counters), cudaMemcpyDeviceToHost);
+    if (c->cache_alloc) cudaMemcpy(c->h_cst, c->cb.st, sizeof(CacheState), cudaMemcpyDeviceToHost);
+    const int ovf = c->h_cnt->overflow;
     const Counters &h = *c->h_cnt;
     memset(out, 0, sizeof *out);
     out->n_active = h.A;
