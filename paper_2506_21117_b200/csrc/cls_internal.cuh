@@ -149,6 +149,7 @@ struct CacheBufs {      // the cache's device buffers (passed by value)
     int2 *tl_drng;      // [max items] per-item ranges of the step's tile lists
     unsigned *icnt;     // [V*T] direct lists: the step's pairs per work item
     unsigned *ioff;     // [V*T] ... their exclusive offsets (end offsets after k_tl_dscatter)
+    unsigned long long *dl_st;   // look-back status of the direct lists' two scans (zeroed per step)
     int *ibig;          // [V*T][2] (offset, count) of the items of more than 64 pairs (k_tl_dsort_big)
 };
 

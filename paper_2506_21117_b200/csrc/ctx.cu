@@ -199,7 +199,7 @@ cls_status cls_destroy(cls_ctx *c)
         if (p) cudaFree(p);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     void *cp[] = {c->cb.st, c->cb.ccnt, c->cb.dyn_of, c->cb.s0, c->cb.flag, c->cb.excl, c->cb.scan_status, c->cb.dmask,
-                  c->cb.dmdiff, c->cb.urec, c->cb.cfvd, c->cb.cfgid, c->cb.cseg_lb, c->cb.dpos, c->cb.db, c->cb.dq, c->cb.dmi, c->cb.mitems, c->cb.dlist, c->cb.dM, c->cb.dcand, c->cb.dcinfo, c->cb.tl_foff, c->cb.tl_drng, c->cb.icnt, c->cb.ioff, c->cb.ibig, c->cb.smp_k, c->cb.smp_g, c->d_dsat,
+                  c->cb.dmdiff, c->cb.urec, c->cb.cfvd, c->cb.cfgid, c->cb.cseg_lb, c->cb.dpos, c->cb.db, c->cb.dq, c->cb.dmi, c->cb.mitems, c->cb.dlist, c->cb.dM, c->cb.dcand, c->cb.dcinfo, c->cb.tl_foff, c->cb.tl_drng, c->cb.icnt, c->cb.ioff, c->cb.dl_st, c->cb.ibig, c->cb.smp_k, c->cb.smp_g, c->d_dsat,
                   c->d_drowmask, c->d_dbbox, c->d_cukey, c->d_cukey_alt};
     for (void *p : cp)
         if (p) cudaFree(p);
@@ -304,7 +304,8 @@ static cls_status cache_allocate(cls_ctx *c)
               dalloc(&c->d_cukey, P) && dalloc(&c->d_cukey_alt, P) && dalloc(&cb.dq, P) && dalloc(&cb.dmi, P) && dalloc(&cb.dlist, N) &&
               dalloc(&cb.dM, N * 12) && dalloc(&cb.dcand, (size_t)Dcap) && dalloc(&cb.dcinfo, (size_t)Dcap) &&
               dalloc(&cb.mitems, P / 4096 + NSEG + 1) && dalloc(&cb.tl_foff, VT + 1) && dalloc(&cb.tl_drng, VT) &&
-              dalloc(&cb.icnt, VT) && dalloc(&cb.ioff, VT) && dalloc(&cb.ibig, 2 * VT) &&
+              dalloc(&cb.icnt, VT) && dalloc(&cb.ioff, VT) &&
+              dalloc(&cb.dl_st, (size_t)scan_status_words((int)Dcap) + scan_status_words((int)VT)) && dalloc(&cb.ibig, 2 * VT) &&
               dalloc(&cb.smp_k, (size_t)R / 1024 + 2) && dalloc(&cb.smp_g, (size_t)R / 1024 + 2) &&
               cudaMallocHost((void **)&c->h_cst, sizeof(CacheState)) == cudaSuccess;
     if (!ok) {
@@ -477,10 +478,27 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
         }
         c->cache_refresh = -1;
     }
-    cls_memset(s.cnt, 0, sizeof(Counters), st);
+    const bool direct = cached && g_tiles && !g_tl_sort;   // the step's own tile lists built directly (k_tiles.cu)
+    if (cached) {   // the step's accumulators in one kernel (separate memset kernels would each cost a link)
+        ZeroSet z{};
+        z.add(s.cnt, sizeof(Counters));
+        z.add(s.st_member, sizeof(unsigned long long) * (size_t)member_status_words(d.n));
+        z.add(&c->cb.st->n_dyn_extra, sizeof(int));
+        z.add(&c->cb.st->n_dcand, sizeof(int));
+        z.add(s.mdiff, sizeof(int) * (size_t)d.V * (d.TY + 1) * (d.TX + 1));
+        z.add(s.st_tiles, sizeof(unsigned long long) * (size_t)items_status_words(d.V * d.T));
+        if (direct) {
+            z.add(c->cb.icnt, sizeof(unsigned) * (size_t)d.V * d.T);
+            z.add(c->cb.dl_st, sizeof(unsigned long long) * ((size_t)scan_status_words((int)c->cb.Dcap) +
+                                                                  scan_status_words(d.V * d.T)));
+        }
+        launch_zero_set(z, st);
+    } else {
+        cls_memset(s.cnt, 0, sizeof(Counters), st);
+    }
     run(c, P_MEMBER, st, [&] {
         if (cached) {   // full membership only until the cache is valid; then only S0's rows can be active
-            launch_member(p, d, regs, s, st, &c->cb.st->list_ok);
+            launch_member(p, d, regs, s, st, &c->cb.st->list_ok, true);
             launch_member_list(p, c->cb.s0, &c->cb.st->A0, &c->cb.st->list_ok, regs, s, st);
         } else {
             launch_member(p, d, regs, s, st);
@@ -494,9 +512,9 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     if (!c->captured) cudaEventRecord(c->ev_member, c->aux);
     cudaEventRecord(c->ev_copied[0], c->aux);
     run(c, P_MASK, st, [&] {
-        if (cached) launch_dyn_mask(p, d, cs, c->cb, s, st);   // one projection of the step's rows (k_cache.cu)
+        if (cached) launch_dyn_mask(p, d, cs, c->cb, s, st, true);   // one projection of the step's rows (k_cache.cu)
         else launch_active_mask(p, d, cs, s, st);
-        launch_bin_items(d, s, st);
+        launch_bin_items(d, s, st, cached);
     });
     // host-resident (pinned, mapped) targets: gather only the active tiles' pixels on the side
     // stream, overlapped with projection and binning; the fwd waits for it
@@ -588,7 +606,6 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
         cls_memset(s.vis, 0, (size_t)d.V * (size_t)s.max_active, st);
         // direct tile lists (default with the tile lists): the step's records are not sorted at all; their pairs
         // are counted per tile and each tile's few entries are ordered on their own (k_cache.cu, k_tiles.cu)
-        const bool direct = g_tiles && !g_tl_sort;
         // the staged candidates vs the mask
         run(c, P_PROJECT_EXACT, st, [&] { launch_dyn_emit(d, cb, sd, st, false); });
         const unsigned long long *tl_d = nullptr;

@@ -345,11 +345,13 @@ static int bits_for(long long x)   // bits to represent 0..x
 }
 
 // 0. items: the active (view, tile)s in (view, tile) order (right after the tile mask)
-void launch_bin_items(const StepDims &d, Scratch &s, cudaStream_t st)
+int items_status_words(int VT) { return (VT + TSCAN_TILE - 1) / TSCAN_TILE; }
+
+void launch_bin_items(const StepDims &d, Scratch &s, cudaStream_t st, bool zeroed)
 {
     const int VT = d.V * d.T;
     const int blocks = (VT + TSCAN_TILE - 1) / TSCAN_TILE;
-    cls_memset(s.st_tiles, 0, sizeof(unsigned long long) * blocks, st);
+    if (!zeroed) cls_memset(s.st_tiles, 0, sizeof(unsigned long long) * blocks, st);
     cls_launch(k_tiles_scan, blocks, TSCAN_THREADS, 0, st, VT, s);
     g_launches++;
 }

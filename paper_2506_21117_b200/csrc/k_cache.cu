@@ -805,11 +805,13 @@ __global__ void __launch_bounds__(256) k_dyn_emit(CacheBufs cb, Scratch s, int T
 }
 
 void launch_dyn_mask(const Params &g, const StepDims &d, const CamSet &cams, const CacheBufs &cb, const Scratch &s,
-                     cudaStream_t st)
+                     cudaStream_t st, bool zeroed)
 {
-    cls_memset(&cb.st->n_dyn_extra, 0, sizeof(int), st);
-    cls_memset(&cb.st->n_dcand, 0, sizeof(int), st);
-    cls_memset(s.mdiff, 0, sizeof(int) * (size_t)d.V * (d.TY + 1) * (d.TX + 1), st);
+    if (!zeroed) {
+        cls_memset(&cb.st->n_dyn_extra, 0, sizeof(int), st);
+        cls_memset(&cb.st->n_dcand, 0, sizeof(int), st);
+        cls_memset(s.mdiff, 0, sizeof(int) * (size_t)d.V * (d.TY + 1) * (d.TX + 1), st);
+    }
     cls_launch(k_dyn_list, 148 * 2, 256, 0, st, cb, s, d.n, g.mean_op, g.quat, g.log_scale);
     const int grid = 148 * 3;
     switch (d.D) {

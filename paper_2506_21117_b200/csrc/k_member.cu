@@ -83,11 +83,13 @@ k_member(const float4 *__restrict__ mean_op, int n, const __grid_constant__ RegS
     }
 }
 
+int member_status_words(int n) { return (n + MEMBER_TILE - 1) / MEMBER_TILE; }
+
 void launch_member(const Params &g, const StepDims &d, const RegSet &regs, const Scratch &s, cudaStream_t st,
-                   const int *skip)
+                   const int *skip, bool zeroed)
 {
     const int blocks = (d.n + MEMBER_TILE - 1) / MEMBER_TILE;
-    cls_memset(s.st_member, 0, sizeof(unsigned long long) * blocks, st);
+    if (!zeroed) cls_memset(s.st_member, 0, sizeof(unsigned long long) * blocks, st);
     cls_launch(k_member, blocks, MEMBER_THREADS, 0, st, g.mean_op, d.n, regs, s, skip);
     g_launches++;
 }

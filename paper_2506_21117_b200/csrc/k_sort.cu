@@ -413,12 +413,36 @@ void cls_memset(void *p, int byte, size_t bytes, cudaStream_t st)
     g_launches++;
 }
 
+int scan_status_words(int max_n) { return (max_n + SC_TILE - 1) / SC_TILE + 1; }
+
+__global__ void __launch_bounds__(256) k_zero_set(ZeroSet z)
+{
+    CLS_PDL_WAIT();
+    const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x, nt = (size_t)gridDim.x * blockDim.x;
+    for (int k = 0; k < z.n; k++) {   // every range is 4-byte aligned and a multiple of 4 bytes
+        unsigned *q = reinterpret_cast<unsigned *>(z.p[k]);
+        const size_t nw = z.bytes[k] / 4;
+        for (size_t i = tid; i < nw; i += nt) q[i] = 0u;
+    }
+}
+
+void launch_zero_set(const ZeroSet &z, cudaStream_t st)
+{
+    unsigned long long tot = 0;
+    for (int k = 0; k < z.n; k++) tot += z.bytes[k];
+    const unsigned blocks = (unsigned)std::min<unsigned long long>(std::max<unsigned long long>(tot / 4 / 256, 1), 148 * 4);
+    cls_launch(k_zero_set, blocks, 256, 0, st, z);
+    g_launches++;
+}
+
 void scan_excl_u32(const unsigned *in, unsigned *out, const int *n_ptr, int max_n, unsigned long long *status,
-                   int *ticket, unsigned long long *total, const int *skip, cudaStream_t st)
+                   int *ticket, unsigned long long *total, const int *skip, cudaStream_t st, bool zeroed)
 {
     const int tiles = (max_n + SC_TILE - 1) / SC_TILE;
-    cls_memset(status, 0, sizeof(unsigned long long) * (size_t)(tiles + 1), st);
-    cls_memset(ticket, 0, sizeof(int), st);
+    if (!zeroed) {
+        cls_memset(status, 0, sizeof(unsigned long long) * (size_t)(tiles + 1), st);
+        cls_memset(ticket, 0, sizeof(int), st);
+    }
     cls_launch(k_scan_excl, 148 * 4, SC_THREADS, 0, st, in, out, n_ptr, max_n, status, ticket, total, skip);
     g_launches++;
 }

@@ -23,7 +23,8 @@ struct Params {
 
 // (1) membership + stable compaction -> idx, ord, A        (k_member.cu)
 void launch_member(const Params &g, const StepDims &d, const RegSet &regs, const Scratch &s, cudaStream_t st,
-                   const int *skip = nullptr);
+                   const int *skip = nullptr, bool zeroed = false);
+int member_status_words(int n);   // look-back status words of k_member for n rows
 void launch_member_list(const Params &g, const int *list, const int *n_list, const int *valid, const RegSet &regs,
                         const Scratch &s, cudaStream_t st);
 // (1b) active tile mask per view + summed-area tables       (k_member.cu)
@@ -33,7 +34,8 @@ void launch_project_cand(const Params &g, const StepDims &d, const CamSet &cams,
                          const int *rows = nullptr, const int *n_rows = nullptr, const int *exclude = nullptr);
 void launch_project_exact(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st);
 // (3) binning: record depth sort, exact pair counts, ordered emission, pair sort by tile (k_bin.cu)
-void launch_bin_items(const StepDims &d, Scratch &s, cudaStream_t st);
+void launch_bin_items(const StepDims &d, Scratch &s, cudaStream_t st, bool zeroed = false);
+int items_status_words(int VT);   // look-back status words of k_tiles_scan
 void launch_gather_targets_u8(const StepDims &d, const CamSet &cams, const Scratch &s, const unsigned char *targets,
                               cudaStream_t st);
 void launch_gather_targets(const StepDims &d, const CamSet &cams, const Scratch &s, const float *host_targets,
@@ -46,8 +48,18 @@ void launch_bin_pairsort(const StepDims &d, const CamSet &cams, Scratch &s, cuda
 int radix_sort_u64(unsigned long long *keys, unsigned long long *keys_alt, unsigned *vals, unsigned *vals_alt,
                    const int *n_ptr, int max_n, int begin_bit, int end_bit, int digit_bits, unsigned *counts,
                    unsigned *totals, const int *skip, cudaStream_t st);
+// zeroed: `status` and `ticket` are already zero (a ZeroSet at the start of the step)
 void scan_excl_u32(const unsigned *in, unsigned *out, const int *n_ptr, int max_n, unsigned long long *status,
-                   int *ticket, unsigned long long *total, const int *skip, cudaStream_t st);
+                   int *ticket, unsigned long long *total, const int *skip, cudaStream_t st, bool zeroed = false);
+int scan_status_words(int max_n);   // status words scan_excl_u32 needs for max_n values
+// several buffers zeroed by one PDL kernel (the step's scratch that its kernels accumulate into)
+struct ZeroSet {
+    void *p[12];
+    unsigned long long bytes[12];
+    int n;
+    void add(void *q, unsigned long long b) { p[n] = q; bytes[n] = b; n++; }
+};
+void launch_zero_set(const ZeroSet &z, cudaStream_t st);
 #define RS_GRID (148 * 4)
 
 unsigned long long *launch_unit_sort(const StepDims &d, Scratch &s, cudaStream_t st);
@@ -55,7 +67,7 @@ void launch_sat_only(const StepDims &d, const CamSet &cams, const Scratch &s, co
                      bool sat = true);
 // static cache of the frozen rows' records and units (k_cache.cu)
 void launch_dyn_mask(const Params &g, const StepDims &d, const CamSet &cams, const CacheBufs &cb, const Scratch &s,
-                     cudaStream_t st);
+                     cudaStream_t st, bool zeroed = false);
 void launch_dyn_emit(const StepDims &d, const CacheBufs &cb, const Scratch &sd, cudaStream_t st, bool rank);
 void launch_dyn_units(const StepDims &d, const CamSet &cams, const CacheBufs &cb, const Scratch &sd, int mode,
                       long long cap, unsigned long long *keys, unsigned *vals, cudaStream_t st);
