@@ -487,6 +487,7 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
         z.add(&c->cb.st->n_dcand, sizeof(int));
         z.add(s.mdiff, sizeof(int) * (size_t)d.V * (d.TY + 1) * (d.TX + 1));
         z.add(s.st_tiles, sizeof(unsigned long long) * (size_t)items_status_words(d.V * d.T));
+        z.add(s.vis, ((size_t)d.V * (size_t)s.max_active + 3) & ~(size_t)3);
         if (direct) {
             z.add(c->cb.icnt, sizeof(unsigned) * (size_t)d.V * d.T);
             z.add(c->cb.dl_st, sizeof(unsigned long long) * ((size_t)scan_status_words((int)c->cb.Dcap) +
@@ -602,8 +603,7 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
         launch_cache_finalize(d, cb, s, st);
         Scratch sd = s;   // the step's own records: S0 x views, ids after the frozen ones
         sd.rec = cb.urec + cb.Fcap;
-        sd.max_records = cb.Dcap;
-        cls_memset(s.vis, 0, (size_t)d.V * (size_t)s.max_active, st);
+        sd.max_records = cb.Dcap;   // (s.vis: zeroed with the step's accumulators; the build projects no active row)
         // direct tile lists (default with the tile lists): the step's records are not sorted at all; their pairs
         // are counted per tile and each tile's few entries are ordered on their own (k_cache.cu, k_tiles.cu)
         // the staged candidates vs the mask
