@@ -591,6 +591,7 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
                                               cudaStreamCaptureModeRelaxed) != cudaSuccess)
                 return fail(c, CLS_ERR_CUDA, "body capture: %s", cudaGetErrorString(cudaGetLastError()));
             launch_cache_build(p, d, cs, cb, s, sb, &fsorted, c->body_stream, g_tiles ? &c->tl_fsorted : nullptr);
+            launch_cache_finalize(d, cb, s, c->body_stream);   // (a warm step's part: in k_cache_check's decision)
             cudaGraph_t out_body = nullptr;
             if (cudaStreamEndCapture(c->body_stream, &out_body) != cudaSuccess)
                 return fail(c, CLS_ERR_CUDA, "body capture end: %s", cudaGetErrorString(cudaGetLastError()));
@@ -600,7 +601,7 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
                 launch_cache_build(p, d, cs, cb, s, sb, &fsorted, st, g_tiles ? &c->tl_fsorted : nullptr);
             });
         }
-        launch_cache_finalize(d, cb, s, st);
+        if (!use_cond) launch_cache_finalize(d, cb, s, st);
         Scratch sd = s;   // the step's own records: S0 x views, ids after the frozen ones
         sd.rec = cb.urec + cb.Fcap;
         sd.max_records = cb.Dcap;   // (s.vis: zeroed with the step's accumulators; the build projects no active row)

@@ -24,7 +24,8 @@ namespace cls {
 
 // ---- checks and decision ----
 
-__device__ __forceinline__ void cache_decide(const CacheBufs &cb, int n, cudaGraphConditionalHandle cond, int use_cond)
+__device__ __forceinline__ void cache_decide(const CacheBufs &cb, int n, cudaGraphConditionalHandle cond, int use_cond,
+                                             Counters *step_cnt)
 {
     CacheState &c = *cb.st;
     const bool req = c.refresh_req != 0;
@@ -56,6 +57,11 @@ __device__ __forceinline__ void cache_decide(const CacheBufs &cb, int n, cudaGra
         cb.ccnt->overflow = CACHE_SKIP;   // warm step, or a refresh (only the S0 compaction runs)
         if (mode == 3) c.refreshes++;
     }
+    if (use_cond && mode == 0) {   // captured warm step: the body (and the k_cache_finalize at its end) is
+        c.need = 0;                // skipped, so its warm-step part is done here
+        c.list_ok = c.valid;
+        if (c.ovf) atomicOr(&step_cnt->overflow, 8);
+    }
 }
 
 // the checks over the mask and the active rows; the last block to finish decides (k_cache_decide's work
@@ -82,7 +88,7 @@ __global__ void __launch_bounds__(256) k_cache_check(CacheBufs cb, Scratch s, in
     if (s_last && threadIdx.x == 0) {
         __threadfence();
         cb.st->check_done = 0;
-        cache_decide(cb, n, cond, use_cond);
+        cache_decide(cb, n, cond, use_cond, s.cnt);
     }
 }
 
