@@ -490,8 +490,7 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
         z.add(s.vis, ((size_t)d.V * (size_t)s.max_active + 3) & ~(size_t)3);
         if (direct) {
             z.add(c->cb.icnt, sizeof(unsigned) * (size_t)d.V * d.T);
-            z.add(c->cb.dl_st, sizeof(unsigned long long) * ((size_t)scan_status_words((int)c->cb.Dcap) +
-                                                                  scan_status_words(d.V * d.T)));
+            z.add(c->cb.dl_st, sizeof(unsigned long long) * (size_t)scan_status_words(d.V * d.T));
         }
         launch_zero_set(z, st);
     } else {

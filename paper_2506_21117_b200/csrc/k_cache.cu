@@ -283,9 +283,9 @@ __global__ void __launch_bounds__(256) k_dyn_pos(CacheBufs cb, Scratch sd)
 }
 
 // The step's own tile lists without sorting its records ("direct" lists).  The records of the
-// step stay in creation order; their (record, tile row) units are enumerated through an exclusive scan of
-// the records' row counts (as k_units does for the sorted records: a warp takes 32 records, then their
-// units, lane = unit).  Per unit the footprint's active tiles in that row, then per (record, active tile):
+// step stay in creation order; a warp takes 32 records and then their (record, tile row) units, lane = unit,
+// numbered by a scan of the 32 records' row counts over the lanes (as k_units does with the sorted
+// records' global offsets).  Per unit the footprint's active tiles in that row, then per (record, active tile):
 //   MODE 1: count the tile's pairs (icnt[view tile]); per record also its rank position among the frozen
 //           records (as k_dyn_pos)
 //   MODE 2: one entry at the tile's next free slot (ioff, exclusive offsets of icnt): keys = depth << 32 | Gaussian
@@ -326,10 +326,18 @@ __global__ void __launch_bounds__(DU_THREADS) k_dyn_units(const __grid_constant_
     unsigned char *own = sown[wid];
     for (int i0 = (blockIdx.x * DU_WARPS + wid) * 32; i0 < n; i0 += gridDim.x * DU_THREADS) {
         const int i = i0 + lane;
-        unsigned o = 0xffffffffu, c = 0u;   // invalid lanes: an offset beyond every unit
+        // the warp's 32 records' units numbered locally (exclusive scan of their row counts over the lanes):
+        // no device-wide scan, nothing is stored per unit
+        unsigned c = i < n ? s.rrows[i] : 0u, o = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const unsigned t = __shfl_up_sync(0xffffffffu, o, d);
+            if (lane >= d) o += t;
+        }
+        const unsigned utot = __shfl_sync(0xffffffffu, o, 31);
+        o -= c;
+        if (MODE == 1 && lane == 0 && utot) atomicAdd(&s.cnt->n_units, (unsigned long long)utot);
         if (i < n) {
-            o = s.roff[i];
-            c = s.rrows[i];
             const unsigned long long key = s.rkey[i] >> RK_IDX_BITS;   // (view, depth)
             const int view = (int)(key >> RK_DEPTH_BITS);
             const FootRec f = foot_make(s.rec[i], view, (unsigned)i);
@@ -342,9 +350,7 @@ __global__ void __launch_bounds__(DU_THREADS) k_dyn_units(const __grid_constant_
         }
         I[2][lane] = o;
         __syncwarp();
-        const int last = min(31, n - 1 - i0);
-        const unsigned ubeg = __shfl_sync(0xffffffffu, o, 0);
-        const unsigned uend = __shfl_sync(0xffffffffu, o + c, last);
+        const unsigned ubeg = 0u, uend = utot;
         int carry = 0;
         for (unsigned ub = ubeg; ub < uend; ub += 32) {
             const bool st = c > 0u && o >= ub && o - ub < 32u;

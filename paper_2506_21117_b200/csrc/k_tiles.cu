@@ -303,20 +303,18 @@ __global__ void __launch_bounds__(DS_BIG_THREADS) k_tl_dsort_big(CacheBufs cb, S
     }
 }
 
-// the step's tile lists, direct: units of the unsorted records (row counts scanned) -> per-tile counts ->
-// tile offsets -> entries -> per-tile order.  keys, out: [cap] u64; vals, alt_v: [cap] u32.  Returns out.
+// the step's tile lists, direct: units of the unsorted records -> per-tile counts -> tile offsets -> entries ->
+// per-tile order.  keys, out: [cap] u64; vals, alt_v: [cap] u32.  Returns out.
 const unsigned long long *launch_dyn_tile_lists(const StepDims &d, const CamSet &cams, const CacheBufs &cb,
                                                 const Scratch &sd, unsigned long long *keys, unsigned *vals,
                                                 unsigned long long *out, unsigned *alt_v, long long cap, cudaStream_t st)
 {
     const int VT = d.V * d.T;
-    // cb.dl_st (two scans' look-back status), cb.icnt and the scan tickets (Counters) were zeroed at the start of
-    // the step (ZeroSet, ctx.cu)
-    scan_excl_u32(sd.rrows, sd.roff, &sd.cnt->n_records, (int)sd.max_records, cb.dl_st, &sd.cnt->scan_ticket,
-                  &sd.cnt->n_units, &sd.cnt->overflow, st, true);
+    // cb.dl_st (the tile scan's look-back status), cb.icnt and the scan ticket (Counters) were zeroed at the start
+    // of the step (ZeroSet, ctx.cu)
     launch_dyn_units(d, cams, cb, sd, 1, cap, keys, vals, st);
-    scan_excl_u32(cb.icnt, cb.ioff, nullptr, VT, cb.dl_st + scan_status_words((int)sd.max_records), &sd.cnt->scan_ticket2,
-                  &sd.cnt->n_pairs, &sd.cnt->overflow, st, true);
+    scan_excl_u32(cb.icnt, cb.ioff, nullptr, VT, cb.dl_st, &sd.cnt->scan_ticket2, &sd.cnt->n_pairs, &sd.cnt->overflow,
+                  st, true);
     launch_dyn_units(d, cams, cb, sd, 2, cap, keys, vals, st);
     cls_launch(k_tl_dsort, 148 * 8, 32 * DS_WARPS, 0, st, cb, sd, (const unsigned long long *)keys,
                (const unsigned *)vals, out, (unsigned)cb.Fcap);
