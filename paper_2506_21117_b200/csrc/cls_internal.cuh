@@ -223,6 +223,7 @@ struct Scratch {
     // a step's entry of position p precedes the frozen record f iff p <= f.  List positions (px_last,
     // first_active) are then list indices.
     int tl_on;
+    int g2d_zero;           // k_fwd zeroes grad2d's V x A rows (the backward then launches no zeroing kernel)
     unsigned *ucnt;                     // k_units also writes each unit's active-tile count here (or null)
     const unsigned long long *tl_f;     // frozen pairs sorted by tile: (tile << 32 | frozen record id)
     const int *tl_foff;                 // [V*T + 1] each tile's range of tl_f

@@ -28,7 +28,8 @@ struct cls_ctx {
     cudaEvent_t ev_fork[2] = {}, ev_copied[2] = {};
     cudaEvent_t ev_items = nullptr, ev_gather = nullptr;
     bool fwd_valid = false, has_targets = false, bwd_valid = false;
-    bool captured = false;   // the last fwd was recorded into a CUDA graph: its events are not usable
+    bool captured = false;
+    bool bwd_since_fwd = false;   // a bwd ran since the last fwd (grad2d holds its sums)   // the last fwd was recorded into a CUDA graph: its events are not usable
     // the scene of the last fwd (SURVEY §8(b) generation check of cls_render_bwd)
     const void *g_ptr[4] = {nullptr, nullptr, nullptr, nullptr};
     int64_t g_n = 0, g_gen = 0;
@@ -657,6 +658,7 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
         }
         c->s_rec = sd;
     }
+    sr.g2d_zero = getenv("CLS_G2D_ZERO_KERNEL") ? 0 : 1;   // the bwd's zeroing folded into k_fwd
     run(c, P_FWD, st, [&] { launch_fwd(d, cs, sr, targets, (flags & CLS_FLAG_TARGETS_U8) != 0, staged, images, loss_scale, bgc, st); });
     if (images) run(c, P_FILL, st, [&] { launch_fill_bg(d, s, images, bgc, st); });
     if (staged) {   // the loss terms need the gathered targets; the compositing above did not
@@ -673,6 +675,7 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     cls_status e = check_cuda(c, "cls_render_fwd");
     if (e != CLS_OK) return e;
     c->s_fwd = sr;
+    c->bwd_since_fwd = false;
     if (!cached) c->s_rec = sr;
     c->fwd_cached = cached;
     c->dims = d;
@@ -735,7 +738,9 @@ cls_status cls_render_bwd(cls_ctx *c, const cls_gaussians *g, const float *dL_di
     Params p{reinterpret_cast<const float4 *>(g->mean_op), reinterpret_cast<const float4 *>(g->quat),
              reinterpret_cast<const float4 *>(g->log_scale), reinterpret_cast<const float4 *>(g->sh)};
     Scratch s = c->s_fwd;
-    run(c, P_ZERO, st, [&] { launch_zero_grad2d(c->dims, s, (long long)c->lim.max_active, st); });
+    // k_fwd zeroed the 2D-gradient sums for the first bwd after it; a repeated bwd zeroes them again
+    if (!s.g2d_zero || c->bwd_since_fwd) run(c, P_ZERO, st, [&] { launch_zero_grad2d(c->dims, s, (long long)c->lim.max_active, st); });
+    c->bwd_since_fwd = true;
     run(c, P_BWD_RASTER, st, [&] { launch_bwd_raster(c->dims, s, dL_dimages, c->bg, st); });
     run(c, P_BWD_PROJECT, st, [&] { launch_bwd_project(p, c->dims, c->cams, s, grad_active, st); });
     cls_status e = check_cuda(c, "cls_render_bwd");

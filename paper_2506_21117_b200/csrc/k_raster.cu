@@ -535,6 +535,18 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
     __shared__ unsigned s_rid[RT_SLOTS];
     __shared__ unsigned s_bm[(RT_SCAN * RT_THREADS) / 32];   // virtual merge: the window's own units of the step
     __shared__ float s_u8[TARGET ? 256 : 1];   // k -> k / 255 (fp32, IEEE division) for 8-bit targets
+    if (s.g2d_zero) {   // the backward's 2D-gradient sums zeroed here, hidden under the compositing (k_zero_grad2d)
+        const long long A = s.cnt->A;
+        if (A > s.max_active) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&s.cnt->overflow, 4);
+        } else {
+            const long long total = (long long)cams.n * A * (G2D_STRIDE / 2);
+            double2 *g = reinterpret_cast<double2 *>(s.grad2d);
+            for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+                 e += (long long)gridDim.x * blockDim.x)
+                g[e] = make_double2(0.0, 0.0);
+        }
+    }
     if (s.cnt->overflow) return;
     if (TARGET && targets8)
         for (int k = threadIdx.x; k < 256; k += blockDim.x) s_u8[k] = __fdiv_rn((float)k, 255.0f);
