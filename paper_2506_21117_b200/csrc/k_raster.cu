@@ -906,6 +906,10 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         const int v = e / T, t = e - v * T;
         const int tx = t % TX, ty = t / TX;
         const int first = s.first_active[item];   // segment position of the first active entry (fwd)
+        if (first == 0x7fffffff) {   // the forward composited no active entry here (about half the items):
+            __syncthreads();         // no gradient, no per-pixel state to load (all threads have read s_item)
+            continue;
+        }
         const int x = tx * CLS_TILE + lx;
         // per-pixel state as fp32x2 pairs over the pixel pairs (p0, p1), (p2, p3) -- rows ly + 4p
         f2_t Tp[2], Tfp[2], S0[2], S1[2], S2[2], G0[2], G1[2], G2[2];
