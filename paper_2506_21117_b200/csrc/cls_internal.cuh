@@ -194,6 +194,7 @@ struct Scratch {
     int *items;             // [V*T] (v*T + t) of active tiles, in (v, t) order
     int *item_of_tile;      // [V*T] item index or -1
     int *first_active;      // [items] segment position of the first active entry the fwd staged (INT_MAX if none)
+    int2 *item_ml;          // [items] the largest last-composited position of the item's pixels, per warp of k_fwd
     long long max_pairs;
     unsigned *rs_counts, *rs_totals;    // radix sort scratch
     // per-pixel forward state, per item [items][256]

@@ -536,10 +536,8 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
     __shared__ unsigned s_bm[(RT_SCAN * RT_THREADS) / 32];   // virtual merge: the window's own units of the step
     __shared__ float s_u8[TARGET ? 256 : 1];   // k -> k / 255 (fp32, IEEE division) for 8-bit targets
     if (s.g2d_zero) {   // the backward's 2D-gradient sums zeroed here, hidden under the compositing (k_zero_grad2d)
-        const long long A = s.cnt->A;
-        if (A > s.max_active) {
-            if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&s.cnt->overflow, 4);
-        } else {
+        const long long A = s.cnt->A;   // (A > max_active: k_bwd reports the overflow and skips)
+        if (A <= s.max_active) {
             const long long total = (long long)cams.n * A * (G2D_STRIDE / 2);
             double2 *g = reinterpret_cast<double2 *>(s.grad2d);
             for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
@@ -624,6 +622,12 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         if (tid == 0) {
             s.first_active[item] = s_first;
             atomicMax(&s.cnt->max_list, lbase);
+        }
+        {   // the item's largest last-composited position (per warp): k_bwd skips items with none >= first
+            int ml = max(max(s_lastp[tid], s_lastp[tid + RT_THREADS]),
+                         max(s_lastp[tid + 2 * RT_THREADS], s_lastp[tid + 3 * RT_THREADS]));
+            ml = __reduce_max_sync(0xffffffffu, ml);
+            if ((tid & 31) == 0) reinterpret_cast<int *>(s.item_ml)[2 * item + (tid >> 5)] = ml;
         }
         float l1 = 0.f;
         float Tr[RT_PX];
@@ -884,9 +888,13 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
     __shared__ int s_item, s_maxlast, s_split, s_pos[RT_SLOTS], s_wc[2 * RT_SCAN];
     __shared__ unsigned s_rid[RT_SLOTS];
     __shared__ unsigned s_bm[(RT_SCAN * RT_THREADS) / 32];   // virtual merge window map
+    const int A = s.cnt->A;
+    if (A > s.max_active) {   // more active rows than the gradient buffers hold: reported, nothing written
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&s.cnt->overflow, 4);
+        return;
+    }
     if (s.cnt->overflow) return;
     const int n_items = s.cnt->n_items;
-    const int A = s.cnt->A;
     const int tid = threadIdx.x, lane = tid & 31;
     const int lx = tid & 15, ly = tid >> 4;
     const float flx = (float)lx;
@@ -906,8 +914,9 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         const int v = e / T, t = e - v * T;
         const int tx = t % TX, ty = t / TX;
         const int first = s.first_active[item];   // segment position of the first active entry (fwd)
-        if (first == 0x7fffffff) {   // the forward composited no active entry here (about half the items):
-            __syncthreads();         // no gradient, no per-pixel state to load (all threads have read s_item)
+        const int2 iml = s.item_ml[item];
+        if (max(iml.x, iml.y) < first) {   // no pixel composited an active entry (over half the items on c4):
+            __syncthreads();               // no gradient, no per-pixel state to load (all threads read s_item)
             continue;
         }
         const int x = tx * CLS_TILE + lx;
