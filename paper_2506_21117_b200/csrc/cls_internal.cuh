@@ -71,6 +71,7 @@ struct Counters {
     unsigned long long bwd_evals;   // (pixel, list entry) evaluations of the backward walk
     unsigned long long fwd_exec;    // (pixel, entry) evaluations the forward executed (entries walked x the warp's pixels)
     int n_big_items;        // direct tile lists: items queued for k_tl_dsort_big
+    int n_bwd_items;        // work items with gradient work (k_fwd -> k_bwd)
     int big_work;           // k_tl_dsort_big's item ticket
 };
 
@@ -195,6 +196,7 @@ struct Scratch {
     int *item_of_tile;      // [V*T] item index or -1
     int *first_active;      // [items] segment position of the first active entry the fwd staged (INT_MAX if none)
     int2 *item_ml;          // [items] the largest last-composited position of the item's pixels, per warp of k_fwd
+    int *bwd_items;         // [items] the items whose pixels composited an active entry (k_fwd appends, k_bwd walks)
     long long max_pairs;
     unsigned *rs_counts, *rs_totals;    // radix sort scratch
     // per-pixel forward state, per item [items][256]

@@ -177,7 +177,7 @@ cls_status cls_destroy(cls_ctx *c)
                     c->s.srid, c->s.long_runs, c->s.rec_gid, c->s.rrows, c->s.cand, c->s.rkey,
                     c->s.rkey_alt, c->s.rcnt, c->s.ukey, c->s.ukey_alt,
                     c->s.roff, c->s.st_scan, c->s.seg_off, c->s.seg_end, c->s.st_tiles, c->s.items, c->s.item_of_tile,
-                    c->s.first_active, c->s.item_ml, c->s.vis, c->s.rs_counts, c->s.rs_totals, c->s.px_T, c->s.px_last, c->s.px_dl, c->s.tgt,
+                    c->s.first_active, c->s.item_ml, c->s.bwd_items, c->s.vis, c->s.rs_counts, c->s.rs_totals, c->s.px_T, c->s.px_last, c->s.px_dl, c->s.tgt,
                     c->s.item_loss, c->s.grad2d, c->s.cnt};
     for (void *p : ptrs)
         if (p) cudaFree(p);
@@ -250,7 +250,7 @@ cls_status cls_create(cls_ctx **out, int device, const cls_limits *lim)
               dalloc(&s.ukey_alt, std::max(P, R)) && dalloc(&s.roff, R) &&
               dalloc(&s.st_scan, std::max(R, P) / 2048 + 2) && dalloc(&s.seg_off, V * c->maxTY) &&
               dalloc(&s.seg_end, V * c->maxTY) && dalloc(&s.st_tiles, VT / 2048 + 2) &&
-              dalloc(&s.items, VT) && dalloc(&s.item_of_tile, VT) && dalloc(&s.first_active, VT) && dalloc(&s.item_ml, VT) &&
+              dalloc(&s.items, VT) && dalloc(&s.item_of_tile, VT) && dalloc(&s.first_active, VT) && dalloc(&s.item_ml, VT) && dalloc(&s.bwd_items, VT) &&
               dalloc(&s.rs_counts, (size_t)512 * RS_GRID) &&
               dalloc(&s.rs_totals, 512) && dalloc(&s.px_T, VT * 256) && dalloc(&s.px_last, VT * 256) &&
               dalloc(&s.px_dl, VT * 768) && dalloc(&s.tgt, VT * 768) && dalloc(&s.item_loss, VT) &&

@@ -223,6 +223,7 @@ k_bwd_project(const float4 *__restrict__ mean_op, const float4 *__restrict__ qua
               const __grid_constant__ CamSet cams, Scratch s, float4 *__restrict__ out)
 {
     CLS_PDL_WAIT();
+    if (blockIdx.x == 0 && threadIdx.x == 0) s.cnt->bwd_work = 0;   // k_bwd is done: a repeated bwd starts afresh
     if (s.cnt->overflow) return;   // capacity overflow (records, pairs, A > max_active): no rows are valid
     const int A = s.cnt->A;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < A; k += gridDim.x * blockDim.x)

@@ -535,6 +535,7 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
     __shared__ unsigned s_rid[RT_SLOTS];
     __shared__ unsigned s_bm[(RT_SCAN * RT_THREADS) / 32];   // virtual merge: the window's own units of the step
     __shared__ float s_u8[TARGET ? 256 : 1];   // k -> k / 255 (fp32, IEEE division) for 8-bit targets
+    __shared__ int s_wml[RT_THREADS / 32];
     if (s.g2d_zero) {   // the backward's 2D-gradient sums zeroed here, hidden under the compositing (k_zero_grad2d)
         const long long A = s.cnt->A;   // (A > max_active: k_bwd reports the overflow and skips)
         if (A <= s.max_active) {
@@ -623,11 +624,17 @@ k_fwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
             s.first_active[item] = s_first;
             atomicMax(&s.cnt->max_list, lbase);
         }
-        {   // the item's largest last-composited position (per warp): k_bwd skips items with none >= first
+        {   // the item's largest last-composited position (per warp); the items where it reaches an active entry
+            // go on k_bwd's work list (the others have no gradient work)
             int ml = max(max(s_lastp[tid], s_lastp[tid + RT_THREADS]),
                          max(s_lastp[tid + 2 * RT_THREADS], s_lastp[tid + 3 * RT_THREADS]));
             ml = __reduce_max_sync(0xffffffffu, ml);
-            if ((tid & 31) == 0) reinterpret_cast<int *>(s.item_ml)[2 * item + (tid >> 5)] = ml;
+            if ((tid & 31) == 0) {
+                reinterpret_cast<int *>(s.item_ml)[2 * item + (tid >> 5)] = ml;
+                s_wml[tid >> 5] = ml;
+            }
+            __syncthreads();
+            if (tid == 0 && max(s_wml[0], s_wml[1]) >= s_first) s.bwd_items[atomicAdd(&s.cnt->n_bwd_items, 1)] = item;
         }
         float l1 = 0.f;
         float Tr[RT_PX];
@@ -894,7 +901,7 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
         return;
     }
     if (s.cnt->overflow) return;
-    const int n_items = s.cnt->n_items;
+    const int n_items = s.cnt->n_items, n_work = s.cnt->n_bwd_items;
     const int tid = threadIdx.x, lane = tid & 31;
     const int lx = tid & 15, ly = tid >> 4;
     const float flx = (float)lx;
@@ -904,7 +911,8 @@ k_bwd(const __grid_constant__ CamSet cams, Scratch s, const float *__restrict__ 
     unsigned long long evals = 0;
     while (true) {
         if (tid == 0) {
-            s_item = atomicAdd(&s.cnt->bwd_work, 1);
+            const int b = atomicAdd(&s.cnt->bwd_work, 1);   // over the forward's work list
+            s_item = b < n_work ? s.bwd_items[b] : n_items;
             s_maxlast = -1;
         }
         __syncthreads();

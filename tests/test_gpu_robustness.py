@@ -110,3 +110,22 @@ def test_pageable_host_targets_rejected(torch_cuda):
     assert st == 1, st
     assert b"pageable" in lib.cls_last_error(opt.ctx)
     opt.close()
+
+
+@pytest.mark.parametrize("cached", [False, True])
+def test_repeated_backward_after_one_forward(torch_cuda, cached):
+    """Two cls_render_bwd calls after one fwd give the same gradient rows: the forward zeroes the 2D
+    gradient sums for the first backward only (k_fwd), the second zeroes them itself, and the
+    backward's work ticket is reset after each backward."""
+    torch = torch_cuda
+    from paper_2506_21117_b200 import GaussianParams, LocalOptimizer, default_limits
+    sc = synth.make_scene("c2", n=20000, width=296, height=232, n_views=2)
+    p = GaussianParams.from_scene(sc)
+    opt = LocalOptimizer(p, sc.regions, limits=default_limits(sc.n, 2, sc.width, sc.height), static_cache=cached)
+    tg = torch.from_numpy(np.ascontiguousarray(sc.targets)).cuda()
+    opt.forward(sc.cameras, tg)
+    g1 = opt.backward().clone()
+    g2 = opt.backward().clone()
+    assert g1.abs().sum() > 0
+    torch.testing.assert_close(g2, g1, rtol=1e-6, atol=1e-12)
+    opt.close()
