@@ -486,7 +486,7 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
         z.add(s.st_member, sizeof(unsigned long long) * (size_t)member_status_words(d.n));
         z.add(&c->cb.st->n_dyn_extra, sizeof(int));
         z.add(&c->cb.st->n_dcand, sizeof(int));
-        z.add(s.mdiff, sizeof(int) * (size_t)d.V * (d.TY + 1) * (d.TX + 1));
+        z.add(s.rowmask, sizeof(unsigned) * (size_t)d.V * d.TY * ((d.TX + 31) / 32));   // k_dyn_project ORs rects in
         z.add(s.st_tiles, sizeof(unsigned long long) * (size_t)items_status_words(d.V * d.T));
         z.add(s.vis, ((size_t)d.V * (size_t)s.max_active + 3) & ~(size_t)3);
         if (direct) {
@@ -515,7 +515,7 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     run(c, P_MASK, st, [&] {
         if (cached) launch_dyn_mask(p, d, cs, c->cb, s, st, true);   // one projection of the step's rows (k_cache.cu)
         else launch_active_mask(p, d, cs, s, st);
-        launch_bin_items(d, s, st, cached);
+        launch_bin_items(d, s, st, cached, cached);
     });
     // host-resident (pinned, mapped) targets: gather only the active tiles' pixels on the side
     // stream, overlapped with projection and binning; the fwd waits for it

@@ -23,7 +23,10 @@ namespace cls {
 #define TSCAN_ITEMS 8
 #define TSCAN_TILE (TSCAN_THREADS * TSCAN_ITEMS)
 
-__global__ void __launch_bounds__(TSCAN_THREADS) k_tiles_scan(int total, Scratch s)
+// ROWS (the static cache's warm step): the mask is read from the row bitmasks k_dyn_project set, and its bytes
+// and per-view counts are written here (no summed-area table is built for the step)
+template <bool ROWS>
+__global__ void __launch_bounds__(TSCAN_THREADS) k_tiles_scan(int total, Scratch s, int TX, int TY)
 {
     CLS_PDL_WAIT();
     __shared__ int s_tile;
@@ -36,12 +39,34 @@ __global__ void __launch_bounds__(TSCAN_THREADS) k_tiles_scan(int total, Scratch
     const int base = tile * TSCAN_TILE + tid * TSCAN_ITEMS;
     unsigned vals = 0u, sum = 0u;
 #pragma unroll
+    const int W32 = (TX + 31) >> 5, T = TX * TY;
+    const int v0 = ROWS ? min(base, total - 1) / T : 0;
+    int n0 = 0;   // ROWS: active tiles of view v0 among this thread's (the rare others are added one by one)
     for (int k = 0; k < TSCAN_ITEMS; k++) {
         const int e = base + k;
-        if (e < total && s.mask[e]) {
+        bool m = false;
+        if (e < total) {
+            if (ROWS) {
+                const int v = e / T, t = e - v * T, ty = t / TX, tx = t - ty * TX;
+                m = (s.rowmask[((size_t)v * TY + ty) * W32 + (tx >> 5)] >> (tx & 31)) & 1u;
+                s.mask[e] = m ? 1 : 0;
+                if (m) {
+                    if (v == v0) n0++;
+                    else atomicAdd(&s.cnt->active_tiles[v], 1);
+                }
+            } else {
+                m = s.mask[e] != 0;
+            }
+        }
+        if (m) {
             vals |= 1u << k;
             sum++;
         }
+    }
+    if (ROWS) {   // per view over the warp: one atomic per (warp, view)
+        const unsigned grp = __match_any_sync(0xffffffffu, v0);
+        const int tot = __reduce_add_sync(grp, n0);
+        if (tot && lane == __ffs(grp) - 1) atomicAdd(&s.cnt->active_tiles[v0], tot);
     }
     unsigned inc = sum;
     for (int o = 1; o < 32; o <<= 1) {
@@ -347,12 +372,17 @@ static int bits_for(long long x)   // bits to represent 0..x
 // 0. items: the active (view, tile)s in (view, tile) order (right after the tile mask)
 int items_status_words(int VT) { return (VT + TSCAN_TILE - 1) / TSCAN_TILE; }
 
-void launch_bin_items(const StepDims &d, Scratch &s, cudaStream_t st, bool zeroed)
+void launch_bin_items(const StepDims &d, Scratch &s, cudaStream_t st, bool zeroed, bool from_rows)
 {
     const int VT = d.V * d.T;
     const int blocks = (VT + TSCAN_TILE - 1) / TSCAN_TILE;
     if (!zeroed) cls_memset(s.st_tiles, 0, sizeof(unsigned long long) * blocks, st);
-    cls_launch(k_tiles_scan, blocks, TSCAN_THREADS, 0, st, VT, s);
+    if (from_rows) {
+        cls_launch(k_tiles_scan<true>, blocks, TSCAN_THREADS, 0, st, VT, s, d.TX, d.TY);
+        g_launches++;
+        return;
+    }
+    cls_launch(k_tiles_scan<false>, blocks, TSCAN_THREADS, 0, st, VT, s, d.TX, d.TY);
     g_launches++;
 }
 

@@ -685,7 +685,7 @@ __global__ void __launch_bounds__(256, 3) k_dyn_project(CacheBufs cb, Scratch s,
     for (int k = threadIdx.x; k < cams.n; k += blockDim.x) s_lims[k] = view_lims(cams.c[k], cams.W, cams.H);
     __syncthreads();
     const int rows = s.cnt->A + cb.st->n_dyn_extra;
-    const int V = cams.n, TX = cams.TX, TY = cams.TY, P = TX + 1;
+    const int V = cams.n, TX = cams.TX, TY = cams.TY;
     const int lane = threadIdx.x & 31;
     const long long total = (long long)rows * V;
     for (long long b0 = blockIdx.x * (long long)blockDim.x; b0 < total; b0 += (long long)gridDim.x * blockDim.x) {
@@ -706,12 +706,13 @@ __global__ void __launch_bounds__(256, 3) k_dyn_project(CacheBufs cb, Scratch s,
             qcut = Mr[10];
             mo = __ldg(mean_op + i);
             if (project_view(mo, M, s_cams[v], s_lims[v], TX, TY, p)) {
-                if (view_ordinal(s, i, s_cams[v].set) >= 0) {   // active here: its rect joins the mask (R9)
-                    int *Dd = s.mdiff + (size_t)v * (TY + 1) * P;
-                    atomicAdd(Dd + p.y0 * P + p.x0, 1);
-                    atomicAdd(Dd + p.y0 * P + p.x1, -1);
-                    atomicAdd(Dd + p.y1 * P + p.x0, -1);
-                    atomicAdd(Dd + p.y1 * P + p.x1, 1);
+                if (view_ordinal(s, i, s_cams[v].set) >= 0 && p.x1 > p.x0) {   // active here: its rect joins
+                    const int W32 = (TX + 31) >> 5;                         // the mask (R9), as row bits
+                    unsigned *rmv = s.rowmask + (size_t)v * TY * W32;
+                    for (int y = p.y0; y < p.y1; y++)
+                        for (int w = p.x0 >> 5; w <= (p.x1 - 1) >> 5; w++)
+                            atomicOr(rmv + y * W32 + w, (0xffffffffu >> (31 - min(p.x1 - 1 - 32 * w, 31))) &
+                                                            (0xffffffffu << max(p.x0 - 32 * w, 0)));
                 }
                 if (qcut >= 0.0) {   // the alpha-footprint rect, as in k_project_exact
                     const double hx = sqrt(qcut * p.A) + 1e-3, hy = sqrt(qcut * p.C) + 1e-3;
@@ -822,7 +823,7 @@ void launch_dyn_mask(const Params &g, const StepDims &d, const CamSet &cams, con
     if (!zeroed) {
         cls_memset(&cb.st->n_dyn_extra, 0, sizeof(int), st);
         cls_memset(&cb.st->n_dcand, 0, sizeof(int), st);
-        cls_memset(s.mdiff, 0, sizeof(int) * (size_t)d.V * (d.TY + 1) * (d.TX + 1), st);
+        cls_memset(s.rowmask, 0, sizeof(unsigned) * (size_t)d.V * d.TY * ((d.TX + 31) / 32), st);
     }
     cls_launch(k_dyn_list, 148 * 2, 256, 0, st, cb, s, d.n, g.mean_op, g.quat, g.log_scale);
     const int grid = 148 * 3;
@@ -833,7 +834,7 @@ void launch_dyn_mask(const Params &g, const StepDims &d, const CamSet &cams, con
     default: cls_launch(k_dyn_project<3>, grid, 256, 0, st, cb, s, g.mean_op, g.sh, d.n, cams); break;
     }
     g_launches += 2;
-    launch_sat_only(d, cams, s, nullptr, st, false);   // k_dyn_emit tests the records against the row bitmasks
+    // the mask is the row bitmasks k_dyn_project set; k_tiles_scan expands them (launch_bin_items, from_rows)
 }
 
 void launch_dyn_emit(const StepDims &d, const CacheBufs &cb, const Scratch &sd, cudaStream_t st, bool rank)
