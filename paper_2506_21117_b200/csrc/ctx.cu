@@ -512,10 +512,28 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
     cudaMemcpyAsync(c->h_A, &s.cnt->A, sizeof(int), cudaMemcpyDeviceToHost, c->aux);
     if (!c->captured) cudaEventRecord(c->ev_member, c->aux);
     cudaEventRecord(c->ev_copied[0], c->aux);
+    // captured into a CUDA graph: the cache build becomes the body of a conditional node set by the cache
+    // check's decision (fused into k_tiles_scan<true>); warm replays skip the body whole
+    cudaGraph_t cap_graph = nullptr;
+    cudaGraphConditionalHandle cond = 0;
+    bool use_cond = false;
+    if (cached && c->captured && !getenv("CLS_NO_COND_GRAPH")) {
+        cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+        if (cudaStreamGetCaptureInfo(st, &cst, nullptr, &cap_graph, nullptr, nullptr) == cudaSuccess &&
+            cst == cudaStreamCaptureStatusActive &&
+            cudaGraphConditionalHandleCreate(&cond, cap_graph, 0, cudaGraphCondAssignDefault) == cudaSuccess)
+            use_cond = true;
+        else
+            cudaGetLastError();
+    }
     run(c, P_MASK, st, [&] {
-        if (cached) launch_dyn_mask(p, d, cs, c->cb, s, st, true);   // one projection of the step's rows (k_cache.cu)
-        else launch_active_mask(p, d, cs, s, st);
-        launch_bin_items(d, s, st, cached, cached);
+        if (cached) {   // one projection of the step's rows (k_cache.cu); the items with the cache check
+            launch_dyn_mask(p, d, cs, c->cb, s, st, true);
+            launch_bin_items(d, s, st, true, &c->cb, cond, use_cond ? 1 : 0);
+        } else {
+            launch_active_mask(p, d, cs, s, st);
+            launch_bin_items(d, s, st);
+        }
     });
     // host-resident (pinned, mapped) targets: gather only the active tiles' pixels on the side
     // stream, overlapped with projection and binning; the fwd waits for it
@@ -558,21 +576,8 @@ cls_status cls_render_fwd(cls_ctx *c, const cls_gaussians *g, const cls_camera *
         sb.max_records = cb.Fcap;
         sb.max_units = c->cache_P;
         unsigned long long *fsorted = nullptr;
-        // captured into a CUDA graph: the build becomes the body of a conditional node set by
-        // k_cache_decide (warm replays skip it whole); eager: every build kernel returns at once
-        cudaGraph_t cap_graph = nullptr;
-        cudaGraphConditionalHandle cond = 0;
-        bool use_cond = false;
-        if (c->captured && !getenv("CLS_NO_COND_GRAPH")) {
-            cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
-            if (cudaStreamGetCaptureInfo(st, &cst, nullptr, &cap_graph, nullptr, nullptr) == cudaSuccess &&
-                cst == cudaStreamCaptureStatusActive &&
-                cudaGraphConditionalHandleCreate(&cond, cap_graph, 0, cudaGraphCondAssignDefault) == cudaSuccess)
-                use_cond = true;
-            else
-                cudaGetLastError();
-        }
-        run(c, P_CACHE_CHECK, st, [&] { launch_cache_check(cb, d, s, st, cond, use_cond ? 1 : 0); });
+        // (the cache check ran with the items, k_tiles_scan<true>; eager: every build kernel returns at once
+        // unless the decision asked for a build)
         if (use_cond) {
             cudaStreamCaptureStatus cst;
             const cudaGraphNode_t *deps = nullptr;

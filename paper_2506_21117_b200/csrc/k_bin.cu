@@ -25,8 +25,11 @@ namespace cls {
 
 // ROWS (the static cache's warm step): the mask is read from the row bitmasks k_dyn_project set, and its bytes
 // and per-view counts are written here (no summed-area table is built for the step)
+// With ROWS the static cache's check is fused in (k_cache_check's work: an active tile outside the dilated mask,
+// an active row outside S0; the last CTA to finish decides the step's cache mode)
 template <bool ROWS>
-__global__ void __launch_bounds__(TSCAN_THREADS) k_tiles_scan(int total, Scratch s, int TX, int TY)
+__global__ void __launch_bounds__(TSCAN_THREADS) k_tiles_scan(int total, Scratch s, int TX, int TY, CacheBufs cb, int n,
+                                                              cudaGraphConditionalHandle cond, int use_cond)
 {
     CLS_PDL_WAIT();
     __shared__ int s_tile;
@@ -67,6 +70,17 @@ __global__ void __launch_bounds__(TSCAN_THREADS) k_tiles_scan(int total, Scratch
         const unsigned grp = __match_any_sync(0xffffffffu, v0);
         const int tot = __reduce_add_sync(grp, n0);
         if (tot && lane == __ffs(grp) - 1) atomicAdd(&s.cnt->active_tiles[v0], tot);
+        // the cache check
+        int need = 0;
+        for (int k = 0; k < TSCAN_ITEMS; k++)
+            if ((vals >> k) & 1u)
+                if (!cb.dmask[base + k]) need |= 1;
+        const int A = s.cnt->A;
+        if (cb.st->valid)
+            for (int e = tile * TSCAN_THREADS + tid; e < A; e += (int)gridDim.x * TSCAN_THREADS)
+                if (cb.dyn_of[s.idx[e]] < 0) need |= 2;
+        need = __reduce_or_sync(0xffffffffu, need);
+        if (lane == 0 && need) atomicOr(&cb.st->need, need);
     }
     unsigned inc = sum;
     for (int o = 1; o < 32; o <<= 1) {
@@ -102,6 +116,18 @@ __global__ void __launch_bounds__(TSCAN_THREADS) k_tiles_scan(int total, Scratch
             run++;
         } else {
             s.item_of_tile[e] = -1;
+        }
+    }
+    if (ROWS) {   // the last CTA decides
+        __shared__ int s_last;
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) s_last = atomicAdd(&cb.st->check_done, 1) == (int)gridDim.x - 1;
+        __syncthreads();
+        if (s_last && tid == 0) {
+            __threadfence();
+            cb.st->check_done = 0;
+            cache_decide(cb, n, cond, use_cond, s.cnt);
         }
     }
 }
@@ -372,17 +398,20 @@ static int bits_for(long long x)   // bits to represent 0..x
 // 0. items: the active (view, tile)s in (view, tile) order (right after the tile mask)
 int items_status_words(int VT) { return (VT + TSCAN_TILE - 1) / TSCAN_TILE; }
 
-void launch_bin_items(const StepDims &d, Scratch &s, cudaStream_t st, bool zeroed, bool from_rows)
+void launch_bin_items(const StepDims &d, Scratch &s, cudaStream_t st, bool zeroed, const CacheBufs *cb,
+                      cudaGraphConditionalHandle cond, int use_cond)
 {
+    const bool from_rows = cb != nullptr;
     const int VT = d.V * d.T;
     const int blocks = (VT + TSCAN_TILE - 1) / TSCAN_TILE;
     if (!zeroed) cls_memset(s.st_tiles, 0, sizeof(unsigned long long) * blocks, st);
     if (from_rows) {
-        cls_launch(k_tiles_scan<true>, blocks, TSCAN_THREADS, 0, st, VT, s, d.TX, d.TY);
+        cls_launch(k_tiles_scan<true>, blocks, TSCAN_THREADS, 0, st, VT, s, d.TX, d.TY, *cb, d.n, cond, use_cond);
         g_launches++;
         return;
     }
-    cls_launch(k_tiles_scan<false>, blocks, TSCAN_THREADS, 0, st, VT, s, d.TX, d.TY);
+    cls_launch(k_tiles_scan<false>, blocks, TSCAN_THREADS, 0, st, VT, s, d.TX, d.TY, CacheBufs{}, 0,
+               (cudaGraphConditionalHandle)0, 0);
     g_launches++;
 }
 

@@ -24,45 +24,7 @@ namespace cls {
 
 // ---- checks and decision ----
 
-__device__ __forceinline__ void cache_decide(const CacheBufs &cb, int n, cudaGraphConditionalHandle cond, int use_cond,
-                                             Counters *step_cnt)
-{
-    CacheState &c = *cb.st;
-    const bool req = c.refresh_req != 0;
-    // a suffix operation changed rows >= n_static only: the frozen part stands if all its rows lie below
-    // (and the mask is still inside the dilated one); S0's old row indices are stale either way
-    const bool refresh = req && c.valid && !(c.need & 1) && c.fmaxgid < c.refresh_nstatic;
-    const int mode = refresh ? 3 : ((!c.valid || req) ? 2 : ((c.need & 2) ? 2 : ((c.need & 1) ? 1 : 0)));
-    c.s0_union = mode == 2 && c.valid && !req;
-    c.refresh_step = req;
-    c.refresh_req = 0;
-    // in a CUDA graph the build is the body of a conditional node: skipped whole on warm steps
-    if (use_cond) cudaGraphSetConditional(cond, mode != 0 ? 1u : 0u);
-    c.mode = mode;
-    c.skip_full = mode != 2 && mode != 3;
-    c.skip_build = mode == 0 || mode == 3;
-    c.n = n;
-    // the dilation adapts: a rebuild because the mask escaped means the active rects move faster than
-    // the margin, so the next build gets 2 more tiles (up to 12)
-    if (c.dil < cb.dilate) c.dil = cb.dilate;
-    if (mode == 1) c.dil = min(c.dil + 2, 12);
-    if (mode == 1 || mode == 2) {
-        int *w = reinterpret_cast<int *>(cb.ccnt);
-        for (int k = 0; k < (int)(sizeof(Counters) / sizeof(int)); k++) w[k] = 0;
-        c.builds++;
-        c.fmaxgid = -1;
-        if (mode == 1) c.mask_builds++;
-        else c.full_builds++;
-    } else {
-        cb.ccnt->overflow = CACHE_SKIP;   // warm step, or a refresh (only the S0 compaction runs)
-        if (mode == 3) c.refreshes++;
-    }
-    if (use_cond && mode == 0) {   // captured warm step: the body (and the k_cache_finalize at its end) is
-        c.need = 0;                // skipped, so its warm-step part is done here
-        c.list_ok = c.valid;
-        if (c.ovf) atomicOr(&step_cnt->overflow, 8);
-    }
-}
+// cache_decide: cls_internal.cuh (k_tiles_scan<true> decides too)
 
 // the checks over the mask and the active rows; the last block to finish decides (k_cache_decide's work
 // without a launch of its own: a fence, a ticket, the decision by the block that draws the last one)

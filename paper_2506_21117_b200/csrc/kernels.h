@@ -34,7 +34,9 @@ void launch_project_cand(const Params &g, const StepDims &d, const CamSet &cams,
                          const int *rows = nullptr, const int *n_rows = nullptr, const int *exclude = nullptr);
 void launch_project_exact(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s, cudaStream_t st);
 // (3) binning: record depth sort, exact pair counts, ordered emission, pair sort by tile (k_bin.cu)
-void launch_bin_items(const StepDims &d, Scratch &s, cudaStream_t st, bool zeroed = false, bool from_rows = false);
+// cb (the static cache's warm step): the mask from the row bitmasks and the cache check fused in
+void launch_bin_items(const StepDims &d, Scratch &s, cudaStream_t st, bool zeroed = false, const CacheBufs *cb = nullptr,
+                      cudaGraphConditionalHandle cond = 0, int use_cond = 0);
 int items_status_words(int VT);   // look-back status words of k_tiles_scan
 void launch_gather_targets_u8(const StepDims &d, const CamSet &cams, const Scratch &s, const unsigned char *targets,
                               cudaStream_t st);
