@@ -619,18 +619,28 @@ def run_loop(args):
     with ClockSampler(0) as clk:
         torch.cuda.synchronize()
         e0.record(stream)
+        trace = [] if os.environ.get("CLS_LOOP_TRACE") else None   # host phases (diagnostic, stderr)
         for k in range(args.steps):
+            t0 = time.perf_counter()
             if k > 0 and k % args.prune_every == 0:
                 removed += opt.prune_outside()     # O^t rows whose centre left the spheres
                 prunes += 1
                 gs = None                          # n changed: the captured step is stale
+            t1 = time.perf_counter()
             if gs is None:
                 gs = GraphStep(opt, cams, tg)
                 captures += 1
+            t2 = time.perf_counter()
             loss = gs.replay()
+            if trace is not None:
+                trace.append((k, round(1e3 * (t1 - t0), 2), round(1e3 * (t2 - t1), 2),
+                              round(1e3 * (time.perf_counter() - t2), 2)))
         e1.record(stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    if trace is not None:
+        print(json.dumps({"loop_ms": round(ms, 2), "host_ms": round(sum(sum(t[1:]) for t in trace), 2),
+                          "slow": sorted(trace, key=lambda t: -sum(t[1:]))[:10]}), file=sys.stderr)
     stats = opt.stats()
     # per-kernel breakdown: K eager steps right after (same workload)
     opt.profile(True)

@@ -8,6 +8,7 @@ parameters out in the ABI's chunk-major float4 SoA format and marshals host stru
 from __future__ import annotations
 
 import ctypes
+import time
 import math
 from dataclasses import dataclass
 from typing import Callable, Optional, Sequence
@@ -538,15 +539,25 @@ class GraphStep:
         self.step_dev = torch.tensor([p.step + 1], dtype=torch.int32, device=dev)
         self.stream = torch.cuda.Stream(device=dev)
         self.stream.wait_stream(torch.cuda.current_stream())
+        t0 = time.perf_counter()
         with torch.cuda.stream(self.stream):
             self._fwd_bwd()                      # warm-up (one-time kernel attribute set-up), no update
         self.stream.synchronize()
+        t1 = time.perf_counter()
         self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph, stream=self.stream):
-            self._fwd_bwd()
-            if self.allreduce is not None:
-                self.allreduce(self.packed.flat)
-            self._adam()
+        # capture_begin/end directly, not `with torch.cuda.graph(...)`: its __enter__ empties torch's device
+        # and pinned-host caches, and the cudaFree / cudaFreeHost of whatever an earlier step released
+        # (a re-capture after a prune) stalled the host 20-60 ms at random (tools/loop_host_probe.py)
+        with torch.cuda.stream(self.stream):
+            self.graph.capture_begin()
+            try:
+                self._fwd_bwd()
+                if self.allreduce is not None:
+                    self.allreduce(self.packed.flat)
+                self._adam()
+            finally:
+                self.graph.capture_end()
+        self.host_ms = {"warmup": 1e3 * (t1 - t0), "capture": 1e3 * (time.perf_counter() - t1)}   # host phases
 
     def _fwd_bwd(self):
         o, p = self.opt, self.opt.params

@@ -23,7 +23,7 @@ class A:
 sc, u8 = bench.bench_scene(A)
 params = GaussianParams.from_scene(sc, device="cuda:0")
 lim = bench.limits_for("c5", sc.n, len(sc.cameras), sc.width, sc.height, False)
-opt = LocalOptimizer(params, sc.regions, limits=lim, static_cache=True)
+opt = LocalOptimizer(params, sc.regions, limits=lim, static_cache=True, per_set="--per-set" in sys.argv)
 opt.spatial_order()
 opt.partition_static()
 tg = torch.from_numpy(np.ascontiguousarray(u8)).cuda()
@@ -45,6 +45,8 @@ for k in range(100):
         gs = None
     if gs is None:
         t0 = time.perf_counter(); gs = GraphStep(opt, sc.cameras, tg); ph["graphstep"].append(time.perf_counter() - t0)
+        ph.setdefault("warmup", []).append(gs.host_ms["warmup"] / 1e3)
+        ph.setdefault("capture", []).append(gs.host_ms["capture"] / 1e3)
         ph.setdefault("mode_after_warmup", []).append(int(opt.stats()["cache_mode"]))
     t0 = time.perf_counter(); gs.replay(); ph["replay"].append(time.perf_counter() - t0)
 torch.cuda.synchronize()
