@@ -36,13 +36,20 @@ __global__ void __launch_bounds__(256) k_adam(const __grid_constant__ AdamArgs a
     CLS_PDL_WAIT();
     if (s.cnt->overflow) return;   // capacity overflow: the gradient rows are not valid, nothing is updated
     const int A = s.cnt->A;
-    float bc1 = a.bc1, bc2 = a.bc2;
-    if (a.step_dev) {   // same double-precision bias correction as the host path
-        const int t = *a.step_dev;
-        bc1 = (float)(1.0 - pow((double)a.b1, (double)t));
-        bc2 = (float)(1.0 - pow((double)a.b2, (double)t));
-    }
     const long long total = (long long)A * a.ROW4;
+    if ((long long)blockIdx.x * blockDim.x >= total) return;   // (the grid is sized for n rows, not A)
+    float bc1 = a.bc1, bc2 = a.bc2;
+    if (a.step_dev) {   // same double-precision bias correction as the host path, once per block
+        __shared__ float s_bc[2];
+        if (threadIdx.x == 0) {
+            const int t = *a.step_dev;
+            s_bc[0] = (float)(1.0 - pow((double)a.b1, (double)t));
+            s_bc[1] = (float)(1.0 - pow((double)a.b2, (double)t));
+        }
+        __syncthreads();
+        bc1 = s_bc[0];
+        bc2 = s_bc[1];
+    }
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x) {
         const int k = (int)(e / a.ROW4), c = (int)(e - (long long)k * a.ROW4);
