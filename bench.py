@@ -173,6 +173,7 @@ def run_ours(args):
     # cold step: an eager step that builds the static cache (after a first step that also allocated it:
     # a new content generation invalidates the cache, so the timed step rebuilds it from scratch)
     step()
+    n_active0 = int(opt.stats()["n_active"])   # |O^t| of the initial scene (the workload's, as the reference arm's)
     params.touch()
     torch.cuda.synchronize()
     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -413,15 +414,9 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "impl": "ours",
-            "config": {"workload": args.config, "gaussians": sc.n, "views": V, "width": W, "height": H,
-                       "sh_degree": sc.sh_degree, "active": int(stats["n_active"]),
-                       "mode": "all-tiles (w/o kernel)" if args.all_tiles else "masked (local kernel)",
-                       "parallelism": f"views/dp{world}",
-                       "row_order": "generator order" if args.no_spatial_order else "Morton (cls_spatial_order at load)",
-                       "targets": ("u8 8-bit images (k / 255 in fp32, gathered per active tile)" if args.targets == "u8"
-                                   else "fp32"),
-                       "l2": "inputs larger than L2 (params+moments "
-                       f"{sc.n * (12 + 3 * 4 * 4) * 4 * 3 / 1e9:.2f} GB)"},
+            "config": workload_config(args, sc, world, n_active0),
+            "row_order": "generator order" if args.no_spatial_order else "Morton (cls_spatial_order at load)",
+            "targets_read": "active tiles' pixels only (gathered per active tile)",
             "mpix_per_s": {"rendered": round(sum(stats["n_active_tiles"]) * 256 * world * value / 1e6, 2),
                            "frame_equivalent": round(V * W * H * value / 1e6, 2)},
             "e2e": e2e, "gpu_launches": int(launches), "roofline": roof, "clocks": clocks,
@@ -553,6 +548,16 @@ def bench_scene(args):
     return dataclasses.replace(sc, targets=u8.astype(np.float32) / np.float32(255.0)), u8
 
 
+def workload_config(args, sc, world: int, n_active: int) -> dict:
+    """The workload both arms report (`config`): the same dict for `--impl ours` and `--impl reference`."""
+    return {"workload": args.config, "gaussians": sc.n, "views": len(sc.cameras), "width": sc.width,
+            "height": sc.height, "sh_degree": sc.sh_degree, "active": n_active,
+            "mode": "all-tiles (w/o kernel)" if getattr(args, "all_tiles", False) else "masked (local kernel)",
+            "parallelism": f"views/dp{world}",
+            "targets": "u8 8-bit images (k / 255 in fp32)" if args.targets == "u8" else "fp32",
+            "l2": f"inputs larger than L2 (params+moments {sc.n * (12 + 3 * 4 * 4) * 4 * 3 / 1e9:.2f} GB)"}
+
+
 def run_reference(args):
     """Reference arm = the CPU oracle as it stands, on this arm's config and metric."""
     rank = int(os.environ.get("RANK", "0"))
@@ -573,6 +578,7 @@ def run_reference(args):
         oracle.adam_rows(np.zeros_like(rows), np.zeros_like(rows), np.zeros_like(rows), rows, lr, step=1)
         if k >= args.warmup:
             times.append(time.perf_counter() - t0)
+    n_active = int(len(fb["idx"]))             # |O^t|: the whole scene's membership, as in the GPU arm
     step_s = statistics.mean(times) * V          # one sampled view per step, scaled to all V views
     value = 1.0 / step_s
     sample = f"1 of {V} views per step (fwd+bwd+Adam, fp64 oracle), EXTRAPOLATED x{V} to the whole step"
@@ -580,9 +586,7 @@ def run_reference(args):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 2),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": args.config, "gaussians": sc.n, "views": V, "width": sc.width,
-                       "height": sc.height, "sh_degree": sc.sh_degree,
-                       "targets": ("u8 8-bit images (k / 255 in fp32)" if args.targets == "u8" else "fp32")},
+            "config": workload_config(args, sc, world, n_active),
             "cpu_baseline": {"value": round(value, 6), "unit": "steps/s", "cores": oracle.num_threads(),
                              "kind": "oracle", "sample": sample, "extrapolated": V != 1, "scale": V},
             "e2e": {"value": round(value, 6), "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
