@@ -584,6 +584,7 @@ def run_reference(args):
     sample = f"1 of {V} views per step (fwd+bwd+Adam, fp64 oracle), EXTRAPOLATED x{V} to the whole step"
     return {"metric": "local-opt steps/s (fwd+bwd+masked Adam)", "value": round(value, 6), "unit": "steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 2),
+            "sample_ms_per_step": round(statistics.mean(times) * 1e3, 2),   # measured; ms_per_step = this x V
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
             "config": workload_config(args, sc, world, n_active),
