@@ -2,8 +2,8 @@
 //
 // PAPER.md Supp. L541 (modification 3): "we terminate threads performing the backward
 // pass of the preprocessing step for Gaussians that are not part of O^t".  On B200 no
-// thread exists for a frozen Gaussian: one thread per ACTIVE Gaussian (ordinal k) sums,
-// over the views of the call and in a fixed order (deterministic, no atomics), the
+// thread exists for a frozen Gaussian: BP_G threads per ACTIVE Gaussian (ordinal k), each over the
+// views v = j mod BP_G, then added in a fixed order (deterministic, no atomics), sum the
 // chain rule from its per-view 2D gradients (u, v, conic, opacity, rgb) to its raw
 // parameters, recomputing the view geometry in fp64:
 //   conic -> Sigma' (dSigma' = -Q Ghat Q), Sigma' -> Sigma and J (via T = J W),
@@ -14,6 +14,11 @@
 #include "kernels.h"
 
 namespace cls {
+
+// BP_G warps per block of 128 threads: lane = one of the block's 32 rows, warp j = its views v = j mod BP_G
+// (loads of one view's 2D-gradient sums stay coalesced over the rows); warp 0 adds the other warps'
+// partial sums in warp order (shared memory) and writes the row
+#define BP_G 4
 
 // gradient of the fp32 SH basis w.r.t. the unit direction components (R15)
 __device__ __forceinline__ void sh_basis_grad(int D, float x, float y, float z, float dY[16][3])
@@ -49,13 +54,17 @@ template <int D>
 __device__ __forceinline__ void bwd_project_row(const float4 *__restrict__ mean_op, const float4 *__restrict__ quat,
                                                 const float4 *__restrict__ log_scale, const float4 *__restrict__ sh,
                                                 int n, const CamSet &cams, const Scratch &s, float4 *__restrict__ out,
-                                                int A, int k)
+                                                int A, int k, bool active, int j, double (*s_d)[13][32],
+                                                float (*s_f)[48][32])
 {
     constexpr int K = (D + 1) * (D + 1);
     constexpr int K4 = (3 * K + 3) / 4;
     constexpr int ROW4 = 3 + K4;
-    const int i = s.idx[k];
-    const float4 mo = mean_op[i], q4 = quat[i], ls = log_scale[i];
+    const int lane = threadIdx.x & 31;
+    const int i = active ? s.idx[k] : 0;
+    const float4 mo = active ? mean_op[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 q4 = active ? quat[i] : make_float4(1.f, 0.f, 0.f, 0.f);
+    const float4 ls = active ? log_scale[i] : make_float4(0.f, 0.f, 0.f, 0.f);
     // parameter-only quantities
     const double qw0 = q4.x, qx0 = q4.y, qy0 = q4.z, qz0 = q4.w;
     const double qn = sqrt(qw0 * qw0 + qx0 * qx0 + qy0 * qy0 + qz0 * qz0);
@@ -73,7 +82,7 @@ __device__ __forceinline__ void bwd_project_row(const float4 *__restrict__ mean_
 #pragma unroll
     for (int e = 0; e < 3 * K; e++) gsh[e] = 0.f;
 
-    for (int v = 0; v < cams.n; v++) {
+    for (int v = j; active && v < cams.n; v += BP_G) {   // this warp's views v = j mod BP_G
         // the raster's per-view sums (fp64 accumulation of its warp partials: order independent)
         const double2 *g2p = reinterpret_cast<const double2 *>(s.grad2d + ((size_t)v * A + k) * G2D_STRIDE);
         const double2 g01 = g2p[0], g23 = g2p[1], g45 = g2p[2], g67 = g2p[3];
@@ -187,6 +196,26 @@ __device__ __forceinline__ void bwd_project_row(const float4 *__restrict__ mean_
             gmu[2] += (double)((dd[2] - dir[2] * dot) * inv_len);
         }
     }
+    // the BP_G warps' partial sums of the row, added by warp 0 in warp order (fixed: deterministic)
+    if (j > 0) {
+        for (int a = 0; a < 3; a++) s_d[j - 1][a][lane] = gmu[a];
+        for (int a = 0; a < 9; a++) s_d[j - 1][3 + a][lane] = gM[a];
+        s_d[j - 1][12][lane] = gop;
+#pragma unroll
+        for (int e = 0; e < 3 * K; e++) s_f[j - 1][e][lane] = gsh[e];
+    }
+    __syncthreads();
+    if (j == 0) {
+        for (int w = 0; w < BP_G - 1; w++) {
+            for (int a = 0; a < 3; a++) gmu[a] += s_d[w][a][lane];
+            for (int a = 0; a < 9; a++) gM[a] += s_d[w][3 + a][lane];
+            gop += s_d[w][12][lane];
+#pragma unroll
+            for (int e = 0; e < 3 * K; e++) gsh[e] += s_f[w][e][lane];
+        }
+    }
+    __syncthreads();
+    if (j != 0 || !active) return;
     // M -> (s, q^) -> (l, q)
     double gs[3], gR[9];
     for (int b = 0; b < 3; b++) gs[b] = gM[b] * Rq[b] + gM[3 + b] * Rq[3 + b] + gM[6 + b] * Rq[6 + b];
@@ -226,15 +255,18 @@ k_bwd_project(const float4 *__restrict__ mean_op, const float4 *__restrict__ qua
     if (blockIdx.x == 0 && threadIdx.x == 0) s.cnt->bwd_work = 0;   // k_bwd is done: a repeated bwd starts afresh
     if (s.cnt->overflow) return;   // capacity overflow (records, pairs, A > max_active): no rows are valid
     const int A = s.cnt->A;
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < A; k += gridDim.x * blockDim.x)
-        bwd_project_row<D>(mean_op, quat, log_scale, sh, n, cams, s, out, A, k);
+    __shared__ double s_d[BP_G - 1][13][32];
+    __shared__ float s_f[BP_G - 1][48][32];
+    const int lane = threadIdx.x & 31, j = threadIdx.x >> 5;   // lane: the row of the tile, j: the view group
+    for (int kb = blockIdx.x * 32; kb < A; kb += gridDim.x * 32)   // uniform over the block (barriers inside)
+        bwd_project_row<D>(mean_op, quat, log_scale, sh, n, cams, s, out, A, kb + lane, kb + lane < A, j, s_d, s_f);
 }
 
 
 void launch_bwd_project(const Params &g, const StepDims &d, const CamSet &cams, const Scratch &s,
                         float *grad_active, cudaStream_t st)
 {
-    const int blocks = std::max(1, std::min((d.n + 127) / 128, 148 * 4));   // grid-stride over the A rows
+    const int blocks = std::max(1, std::min((d.n + 31) / 32, 148 * 4));   // 32 rows per block, grid-stride over A
     float4 *out = reinterpret_cast<float4 *>(grad_active);
     switch (d.D) {
     case 0: cls_launch(k_bwd_project<0>, blocks, 128, 0, st, g.mean_op, g.quat, g.log_scale, g.sh, d.n, cams, s, out); break;
